@@ -1,0 +1,248 @@
+/*
+ * sdfgi_b200.h — C-ABI of the B200-native SDFDDGI probe update.
+ *
+ * This is the drop-in boundary. Every entry point takes plain pointers and sizes
+ * (no torch / CUDA / C++ types) and returns an int status (SDFGI_OK == 0). The
+ * message for the last failure on the calling thread is sdfgi_last_error().
+ * There is no CPU fallback: a context can only be created on a CUDA device.
+ *
+ * The reference (`/root/reference/proj/include/sdfgi/`, header-only C++20) has no
+ * FFI; its hot path is a set of inline functions called from
+ * Renderer::renderFrame (pipeline.hpp:108-151 probe stage, :161-207 gather).
+ * Each entry point below cites the reference interface it replaces. The C++
+ * shim `paper_2007_14394_b200/include/sdfgi_b200.hpp` and the Python mirror
+ * `paper_2007_14394_b200/api.py` keep the reference's names over this ABI.
+ *
+ * Threading contract: one host thread per context; every call is ordered on
+ * the context's CUDA stream and returns after the stream has drained unless
+ * the function says otherwise.
+ *
+ * Structs are also the on-disk layout of the SDFS scene interchange file
+ * (see paper_2007_14394_b200/scene_io.py); all fields are little-endian and
+ * naturally aligned, no implicit padding.
+ */
+#ifndef SDFGI_B200_H
+#define SDFGI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDFGI_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define SDFGI_API __attribute__((visibility("default")))
+#else
+#define SDFGI_API
+#endif
+
+enum sdfgi_status {
+    SDFGI_OK = 0,
+    SDFGI_ERR_INVALID = 1,   /* bad argument (null pointer, size mismatch, range) */
+    SDFGI_ERR_CUDA = 2,      /* CUDA runtime failure, or no CUDA device */
+    SDFGI_ERR_NCCL = 3,      /* collective failure */
+    SDFGI_ERR_STATE = 4,     /* call out of order (e.g. update before scene upload) */
+    SDFGI_ERR_OOM = 5
+};
+
+/* PrimitiveKind, primitives.hpp:9 */
+enum sdfgi_prim_kind { SDFGI_SPHERE = 0, SDFGI_BOX = 1, SDFGI_PLANE = 2, SDFGI_CYLINDER = 3, SDFGI_CAPSULE = 4 };
+/* LightKind, primitives.hpp:16 */
+enum sdfgi_light_kind { SDFGI_LIGHT_POINT = 0, SDFGI_LIGHT_DIRECTIONAL = 1, SDFGI_LIGHT_SKY = 2 };
+/* arithmetic of the device path */
+enum sdfgi_precision { SDFGI_F64 = 0, SDFGI_F32 = 1 };
+
+/* SdfPrimitive + Material, primitives.hpp:11-38 (rotation row-major, vec.hpp:75). 184 B. */
+typedef struct sdfgi_prim {
+    int32_t id;
+    int32_t kind;
+    int32_t lod_tier;
+    int32_t _pad;
+    double rot[9];
+    double trans[3];
+    double size[3];
+    double albedo[3];
+    double emission[3];
+} sdfgi_prim;
+
+/* Light, primitives.hpp:18-23. 80 B. */
+typedef struct sdfgi_light {
+    int32_t kind;
+    int32_t _pad;
+    double position[3];
+    double direction[3];
+    double intensity[3];
+} sdfgi_light;
+
+/* Cluster cull bounds (Cluster::cullAabb + unbounded, scene.hpp:38-46), already
+ * inflated by kClusterCullMargin. Members are CSR: member_start[k+1], member_idx[]. 56 B. */
+typedef struct sdfgi_cluster {
+    double lo[3];
+    double hi[3];
+    int32_t unbounded;
+    int32_t _pad;
+} sdfgi_cluster;
+
+/* RenderConfig, config.hpp:9-50. Every field 8 bytes; ints widened to int64. 224 B. */
+typedef struct sdfgi_cfg {
+    double surface_epsilon;
+    int64_t max_trace_steps;
+    int64_t shadow_steps;
+    double ray_tmax;
+    double shadow_k;
+    double probe_visibility_k;
+    double gradient_step;
+    int64_t max_per_cluster;
+    double merge_radius;
+    double threshold1_frac;
+    double threshold2_frac;
+    int64_t max_descent_steps;
+    int64_t probe_budget;
+    int64_t n_rays_full;
+    double hysteresis;
+    double alpha_min;
+    double bounce_coeff;
+    int64_t oct_res;
+    int64_t rotate_per_frame;
+    uint64_t seed;
+    double mvc_relocation_frac;
+    double dedup_quant_frac;
+    double contact_radius_frac;
+    int64_t contact_samples;
+    double history_blend;
+    double depth_sigma_frac;
+    double exposure;
+    int64_t fps;
+} sdfgi_cfg;
+
+/* Probe, probe_volume.hpp:12-19, as stored on the host side of the ABI. 88 B. */
+typedef struct sdfgi_probe {
+    double resting[3];
+    double pos[3];
+    double last_pos[3];
+    int32_t reject_history;
+    int32_t alive;
+    int32_t last_update_frame;
+    int32_t _pad;
+} sdfgi_probe;
+
+/* TraceStats, scene.hpp:16-36 */
+typedef struct sdfgi_stats {
+    uint64_t sdf_queries;
+    uint64_t clusters_visited;
+    uint64_t clusters_skipped;
+    uint64_t primitive_evals;
+    uint64_t trace_steps;
+    uint64_t sphere_traces;
+    uint64_t shadow_traces;
+    uint64_t visibility_traces;
+} sdfgi_stats;
+
+/* RelocationReport, probe_volume.hpp:88-92 */
+typedef struct sdfgi_reloc_report {
+    int32_t relocated;
+    int32_t rejected;
+    int32_t dead;
+    int32_t _pad;
+} sdfgi_reloc_report;
+
+/* Sum over a batch of ProbeUpdateResult (probe_update.hpp:151-154). */
+typedef struct sdfgi_update_result {
+    double max_texel_delta;   /* max over updated probes */
+    int64_t rays_traced;      /* sum of raysTraced */
+    int64_t probes_updated;   /* alive probes that were updated */
+} sdfgi_update_result;
+
+/* Per-ray record (debug / parity), mirrors the Hit + RadianceSample pair built in
+ * updateProbe (probe_update.hpp:177-189). 96 B. */
+typedef struct sdfgi_ray_record {
+    double dir[3];
+    double t;              /* Hit::t when converged, else 0 */
+    double radiance[3];
+    double normal[3];
+    int32_t converged;
+    int32_t miss;          /* MissReason: 0 None, 1 TMax, 2 StepLimit */
+    int32_t prim_index;    /* Hit::primitiveIndex */
+    int32_t steps;         /* sphere-trace loop iterations */
+} sdfgi_ray_record;
+
+/* ---------------------------------------------------------------- lifecycle */
+SDFGI_API int sdfgi_abi_version(void);
+SDFGI_API const char* sdfgi_last_error(void);
+/* Number of CUDA devices visible (0 on a machine without a GPU). */
+SDFGI_API int sdfgi_device_count(int* out);
+/* NCCL unique id for a multi-GPU context (rank 0 creates, the caller broadcasts). */
+SDFGI_API int sdfgi_nccl_unique_id(uint8_t out[128]);
+/* rank/world: probe-slab sharding. nccl_uid may be NULL when world == 1. */
+SDFGI_API int sdfgi_ctx_create(int device, int rank, int world, const uint8_t* nccl_uid, int precision,
+                     void** out_ctx);
+SDFGI_API int sdfgi_ctx_destroy(void* ctx);
+SDFGI_API int sdfgi_ctx_set_precision(void* ctx, int precision);
+/* Raw CUDA stream handle (cudaStream_t) of the context, for event timing. */
+SDFGI_API int sdfgi_ctx_stream(void* ctx, void** out_stream);
+SDFGI_API int sdfgi_ctx_synchronize(void* ctx);
+
+/* -------------------------------------------------------------------- scene */
+/* Replaces ActiveScene construction + finalize() (scene.hpp:88-103). Copied to
+ * the device; the caller keeps ownership. `sky` = ActiveScene::sky. */
+SDFGI_API int sdfgi_scene_upload(void* ctx, const sdfgi_prim* prims, int n_prims,
+                       const sdfgi_cluster* clusters, int n_clusters,
+                       const int32_t* member_start, const int32_t* member_idx,
+                       const sdfgi_light* lights, int n_lights, const double sky[3]);
+/* Lights and sky only (moving lights, C5); primitives unchanged. */
+SDFGI_API int sdfgi_lights_upload(void* ctx, const sdfgi_light* lights, int n_lights, const double sky[3]);
+
+/* ------------------------------------------------------------- probe volume */
+/* makeCascade / CascadeVolume (probe_volume.hpp:24-76). Allocates probes (reset to
+ * resting, rejectHistory=1, alive=1, lastUpdateFrame=-1) and both atlases (zero). */
+SDFGI_API int sdfgi_cascade_set(void* ctx, int level, int res_x, int res_y, int res_z, double spacing,
+                      const double origin[3], int oct_res);
+SDFGI_API int sdfgi_cascade_count(void* ctx, int* out);
+SDFGI_API int sdfgi_probes_reset(void* ctx, int level);
+SDFGI_API int sdfgi_probes_upload(void* ctx, int level, const sdfgi_probe* probes, int n);
+SDFGI_API int sdfgi_probes_download(void* ctx, int level, sdfgi_probe* probes, int n);
+
+/* updateProbePositions (probe_volume.hpp:99-143) for one cascade, device-resident.
+ * Bit-exact with the reference in SDFGI_F64 mode. */
+SDFGI_API int sdfgi_probes_relocate(void* ctx, int level, double threshold1, double threshold2,
+                          int max_descent_steps, double gradient_step,
+                          sdfgi_reloc_report* report, sdfgi_stats* stats);
+
+/* The probe stage of renderFrame (pipeline.hpp:126-151): back atlas <- front atlas,
+ * then updateProbe (probe_update.hpp:166-211) for every selected alive probe, writing
+ * the back atlas and reading the front atlas for bounce. probe_refs are (cascade,
+ * index) pairs; NULL means every probe of every cascade (probeBudget 0). With
+ * world > 1 each rank updates its z-slab and the back atlas is all-gathered. */
+SDFGI_API int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_refs, int frame,
+                        const sdfgi_cfg* cfg, sdfgi_update_result* result, sdfgi_stats* stats);
+/* readIdx swap at frame end (pipeline.hpp:220). */
+SDFGI_API int sdfgi_atlas_swap(void* ctx);
+/* which = 0: front (read) atlas, 1: back (write) atlas. Layout = ProbeAtlas::raw()
+ * (atlas.hpp:119-124): ((probe*(R+2)+y)*(R+2)+x)*3 floats. */
+SDFGI_API int sdfgi_atlas_download(void* ctx, int level, int which, float* dst, size_t n_floats);
+SDFGI_API int sdfgi_atlas_upload(void* ctx, int level, int which, const float* src, size_t n_floats);
+/* Pinned-free device pointer of an atlas (for collectives / zero-copy views). */
+SDFGI_API int sdfgi_atlas_device_ptr(void* ctx, int level, int which, void** out_ptr, size_t* out_bytes);
+
+/* Debug/parity: re-run the ray stage of updateProbe for the listed probes against
+ * the front atlas and return one record per ray (2N when rejectHistory). Records are
+ * written consecutively, probe by probe; n_records_max bounds the output. */
+SDFGI_API int sdfgi_probes_trace_debug(void* ctx, const int32_t* probe_refs, int n_refs, int frame,
+                             const sdfgi_cfg* cfg, sdfgi_ray_record* out, int n_records_max,
+                             int* n_written);
+
+/* Point queries (querySceneSdf, scene.hpp:336-340): d[i] = min(naive SDF, init_d[i]),
+ * owner[i] = primitive index or -1. init_d may be NULL (= +inf). Host arrays. */
+SDFGI_API int sdfgi_query_points(void* ctx, const double* points_xyz, const double* init_d, int n,
+                       double* out_d, int32_t* out_owner);
+
+/* Launch counter: kernels this context has launched since creation. */
+SDFGI_API int sdfgi_launch_count(void* ctx, int64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDFGI_B200_H */

@@ -1,0 +1,103 @@
+"""Reference-named host API over the C-ABI (the Python mirror of the drop-in).
+
+Names and argument meaning follow the reference's C++ API
+(/root/reference/proj/include/sdfgi/*.hpp), so callers and tests read like the
+reference's own; the state they operate on lives on the GPU in a ``Device``.
+
+    cascadeOriginFor      probe_volume.hpp:51-55
+    makeCascade           probe_volume.hpp:57-76
+    updateProbePositions  probe_volume.hpp:99-143
+    updateProbes          batched updateProbe (probe_update.hpp:166-211) over the
+                          probe stage of Renderer::renderFrame (pipeline.hpp:126-151)
+    querySceneSdf         scene.hpp:336-340
+    ProbeStage            the probe half of Renderer::renderFrame (pipeline.hpp:108-151)
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import scene_io as sio
+from .runtime import Device
+
+
+def snapToSpacing(p, spacing):
+    """probe_volume.hpp:46-49"""
+    return np.array([math.floor(x / spacing + 0.5) * spacing for x in p], dtype=np.float64)
+
+
+def cascadeOriginFor(cameraPos, resX, resY, resZ, spacing):
+    """probe_volume.hpp:51-55"""
+    extent = np.array([(resX - 1) * spacing, (resY - 1) * spacing, (resZ - 1) * spacing])
+    s = snapToSpacing(cameraPos, spacing)
+    return np.array([s[i] - extent[i] * 0.5 for i in range(3)])
+
+
+def makeCascade(dev: Device, resX, resY, resZ, spacing0, level, cameraPos, oct_res=8):
+    """probe_volume.hpp:57-76 — allocates the cascade's probes and atlases on the device."""
+    spacing = spacing0 * math.pow(2.0, level)
+    origin = cascadeOriginFor(cameraPos, resX, resY, resZ, spacing)
+    dev.set_cascade(level, (resX, resY, resZ), spacing, origin, oct_res)
+    return level
+
+
+def updateProbePositions(dev: Device, level, threshold1, threshold2, maxDescentSteps=16, stats=False,
+                         gradientStep=1e-3):
+    """probe_volume.hpp:99-143 (device-resident probes)."""
+    return dev.relocate(level, threshold1, threshold2, maxDescentSteps, gradientStep, stats)
+
+
+def updateProbes(dev: Device, cfg, frameIndex, refs=None, stats=False):
+    """Batched updateProbe over `refs` ((level, index) pairs; None = all probes)."""
+    return dev.update(frameIndex, cfg, refs, stats)
+
+
+def querySceneSdf(dev: Device, points, initD=None):
+    """scene.hpp:336-340 at many points: (d, owner primitive index)."""
+    return dev.query_points(points, initD)
+
+
+class ProbeStage:
+    """The probe half of Renderer::renderFrame (pipeline.hpp:108-151) on one device.
+
+    Per pass: updateProbePositions for every cascade, then the batched update
+    (back atlas <- front atlas, every alive probe updated with frame = pass
+    index), then the frame-end swap (pipeline.hpp:220)."""
+
+    def __init__(self, dev: Device, scene: sio.Scene, cfg=None, res=None, spacing=None, levels=None,
+                 n_rays=None):
+        self.dev = dev
+        self.scene = scene
+        self.cfg = np.array(scene.cfg if cfg is None else cfg, dtype=sio.CFG_DTYPE).reshape(1)
+        if n_rays is not None:
+            self.cfg["n_rays_full"] = n_rays
+        self.res = tuple(scene.cascade.res if res is None else res)
+        self.spacing0 = float(scene.cascade.spacing if spacing is None else spacing)
+        self.levels = int(scene.cascade.levels if levels is None else levels)
+        dev.upload_scene(scene)
+        self.reset()
+
+    def reset(self):
+        oct_res = int(self.cfg["oct_res"][0])
+        for level in range(self.levels):
+            makeCascade(self.dev, *self.res, self.spacing0, level, self.scene.camera.position, oct_res)
+
+    def spacing(self, level):
+        return self.spacing0 * math.pow(2.0, level)
+
+    def relocate_all(self, stats=False):
+        reps = []
+        for level in range(self.levels):
+            sp = self.spacing(level)
+            th1 = float(self.cfg["threshold1_frac"][0]) * sp
+            th2 = float(self.cfg["threshold2_frac"][0]) * sp
+            reps.append(updateProbePositions(self.dev, level, th1, th2, int(self.cfg["max_descent_steps"][0]),
+                                             stats, float(self.cfg["gradient_step"][0])))
+        return reps
+
+    def run_pass(self, frame, stats=False):
+        reps = self.relocate_all(stats)
+        upd = updateProbes(self.dev, self.cfg, frame, None, stats)
+        self.dev.swap()
+        return reps, upd

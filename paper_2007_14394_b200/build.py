@@ -1,0 +1,89 @@
+"""In-tree build of the sm_100a CUDA library (libsdfgi_b200.so) and the C oracle.
+
+``python -m paper_2007_14394_b200.build`` (or ``__graft_entry__.build()``) runs
+nvcc directly — no JIT cache — so the built ``.so`` lives in the package
+directory and travels to the GPU box with the repo snapshot.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+BUILD = os.path.join(PKG, "_build")
+LIB = os.path.join(PKG, "libsdfgi_b200.so")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+# per-translation-unit flags: the FP64 parity kernels forbid FMA contraction so every
+# product and sum rounds exactly as the reference built with -ffp-contract=off.
+UNITS = {
+    "kernels_f64.cu": ["-fmad=false"],
+    "kernels_f32.cu": ["-fmad=true"],
+    "sdfgi_abi.cu": [],
+}
+HEADERS = ["sdf_device.cuh", "kernels.cuh", "kernels_impl.cuh"]
+
+
+def _nvcc():
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"command failed: {' '.join(cmd[:3])} ...")
+    return r
+
+
+def build_lib(verbose=False, force=False) -> str:
+    nvcc = _nvcc()
+    os.makedirs(BUILD, exist_ok=True)
+    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "sdfgi_b200.h")]
+    objs = []
+    for unit, extra in UNITS.items():
+        src = os.path.join(CSRC, unit)
+        obj = os.path.join(BUILD, unit.replace(".cu", ".o"))
+        objs.append(obj)
+        if force or _stale(obj, [src, *hdrs, __file__]):
+            _run([nvcc, *ARCH, *COMMON, *extra, "-c", src, "-o", obj], verbose)
+    if force or _stale(LIB, objs):
+        _run([nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-lnccl", "-lcudart"], verbose)
+    return LIB
+
+
+def build_oracle(verbose=False) -> str:
+    """The C restatement (test infrastructure) — oracle/Makefile."""
+    _run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "oracle"], verbose)
+    return os.path.join(ROOT, "oracle", "_build", "libsdfgi_oracle.so")
+
+
+def build_ref(verbose=False) -> str | None:
+    """The reference compiled from /root/reference (only where it exists)."""
+    if not os.path.isdir("/root/reference/proj/include"):
+        return None
+    _run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref"], verbose)
+    return os.path.join(ROOT, "oracle", "_ref")
+
+
+if __name__ == "__main__":
+    v = "-v" in sys.argv
+    print(build_lib(verbose=v, force="--force" in sys.argv))

@@ -1,0 +1,689 @@
+// sdf_device.cuh — device-side SDF scene, tracing, shading and probe math.
+//
+// Templated on the arithmetic type R (double = parity mode, compiled with
+// -fmad=false so every product/sum rounds exactly as the reference's
+// -ffp-contract=off build; float = perf mode). Each function cites the
+// reference function whose semantics it reproduces; the *structure* is GPU
+// first: the scene is stored in cluster (CSR) order so a warp walks clusters
+// and members in lock-step with warp-uniform (broadcast) loads, the probe update
+// is one CTA per probe with rays across lanes, and the texel convolution reads
+// the CTA's samples from shared memory.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sdfgi_dev {
+
+constexpr double kPi = 3.14159265358979323846;
+
+// std::min / std::max / std::clamp semantics (operand order, NaN and signed-zero
+// behaviour) — vec.hpp uses the std versions, not fmin/fmax.
+template <typename R> __device__ __forceinline__ R smin(R a, R b) { return (b < a) ? b : a; }
+template <typename R> __device__ __forceinline__ R smax(R a, R b) { return (a < b) ? b : a; }
+template <typename R> __device__ __forceinline__ R sclamp(R v, R lo, R hi) {
+    return (v < lo) ? lo : ((hi < v) ? hi : v);
+}
+__device__ __forceinline__ int iclamp(int v, int lo, int hi) { return (v < lo) ? lo : ((hi < v) ? hi : v); }
+
+template <typename R> __device__ __forceinline__ R rsqrt_exact(R v) { return sqrt(v); }
+
+template <typename R> struct V3 {
+    R x, y, z;
+};
+template <typename R> __device__ __forceinline__ V3<R> mk(R x, R y, R z) { return V3<R>{x, y, z}; }
+template <typename R> __device__ __forceinline__ V3<R> operator+(V3<R> a, V3<R> b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+template <typename R> __device__ __forceinline__ V3<R> operator-(V3<R> a, V3<R> b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+template <typename R> __device__ __forceinline__ V3<R> operator-(V3<R> a) { return {-a.x, -a.y, -a.z}; }
+template <typename R> __device__ __forceinline__ V3<R> operator*(V3<R> a, R s) { return {a.x * s, a.y * s, a.z * s}; }
+template <typename R> __device__ __forceinline__ V3<R> operator/(V3<R> a, R s) { return {a.x / s, a.y / s, a.z / s}; }
+template <typename R> __device__ __forceinline__ V3<R> operator*(V3<R> a, V3<R> b) { return {a.x * b.x, a.y * b.y, a.z * b.z}; }
+// vec.hpp:50 — (x*x + y*y) + z*z
+template <typename R> __device__ __forceinline__ R dot(V3<R> a, V3<R> b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+template <typename R> __device__ __forceinline__ R length(V3<R> v) { return sqrt(dot(v, v)); }
+template <typename R> __device__ __forceinline__ V3<R> normalize(V3<R> v) { return v / length(v); }
+template <typename R> __device__ __forceinline__ V3<R> lerp(V3<R> a, V3<R> b, R t) { return a + (b - a) * t; }
+template <typename R> __device__ __forceinline__ R maxComponent(V3<R> v) { return smax(v.x, smax(v.y, v.z)); }
+
+// ------------------------------------------------------------------ rng.hpp
+__device__ __forceinline__ uint64_t hashU64(uint64_t x) {  // rng.hpp:10-15
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e9b5ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ uint64_t hashCombine(uint64_t a, uint64_t b) {  // rng.hpp:17
+    return hashU64(a ^ (b + 0x9e3779b97f4a7c15ull + (a << 6) + (a >> 2)));
+}
+struct Rng {  // rng.hpp:22-48
+    uint64_t s;
+    __device__ explicit Rng(uint64_t key) : s(hashU64(key)) {}
+    __device__ uint64_t next() {
+        s += 0x9e3779b97f4a7c15ull;
+        uint64_t z = s;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e9b5ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    }
+    __device__ double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+};
+// probeKey, probe_update.hpp:156-159
+__device__ __forceinline__ uint64_t probeKey(int cascade, int index) {
+    return hashCombine(static_cast<uint64_t>(cascade) + 0x9e1du, static_cast<uint64_t>(index));
+}
+
+// --------------------------------------------------------------- scene data
+// One primitive in CSR (cluster) order. identity = the rotation's diagonal is all
+// 1.0 (primitives.hpp:76-77 fast path). 128 B for double.
+template <typename R> struct __align__(16) DPrim {
+    R rot[9];
+    R trans[3];
+    R size[3];
+    int kind;
+    int identity;
+};
+template <typename R> struct __align__(16) DCluster {
+    R lo[3];
+    R hi[3];
+    int unbounded;
+    int _pad;
+};
+struct DLight {  // sdfgi_light, kept in double in both modes (tiny)
+    int kind;
+    int _pad;
+    double position[3];
+    double direction[3];
+    double intensity[3];
+};
+
+template <typename R> struct SceneView {
+    const DPrim<R>* __restrict__ prims;        // CSR order
+    const DCluster<R>* __restrict__ clusters;
+    const int* __restrict__ cstart;            // K+1
+    const int* __restrict__ orig;              // CSR position -> ActiveScene primitive index
+    const double* __restrict__ albedo;         // 3 per CSR position
+    const double* __restrict__ emission;       // 3 per CSR position
+    const DLight* __restrict__ lights;
+    int n_prims, n_clusters, n_lights;
+    double sky[3];
+};
+
+// TraceStats (scene.hpp:16-36), per thread.
+struct Counters {
+    unsigned long long q, cv, cs, pe, steps, sphere, shadow, vis;
+    __device__ void zero() { q = cv = cs = pe = steps = sphere = shadow = vis = 0; }
+};
+
+// ------------------------------------------------------------ primitives.hpp
+// evalPrimitive, primitives.hpp:73-86 (+ detail::*Sdf :42-65)
+template <typename R>
+__device__ __forceinline__ R evalPrim(const DPrim<R>& pr, V3<R> p) {
+    V3<R> q = p - mk(pr.trans[0], pr.trans[1], pr.trans[2]);
+    if (!pr.identity) {
+        // transposeMul, vec.hpp:113-117
+        const R* m = pr.rot;
+        q = mk(m[0] * q.x + m[3] * q.y + m[6] * q.z,
+               m[1] * q.x + m[4] * q.y + m[7] * q.z,
+               m[2] * q.x + m[5] * q.y + m[8] * q.z);
+    }
+    switch (pr.kind) {
+        case 0:  // sphere
+            return length(q) - pr.size[0];
+        case 1: {  // box
+            V3<R> a = mk(fabs(q.x) - pr.size[0], fabs(q.y) - pr.size[1], fabs(q.z) - pr.size[2]);
+            R outside = length(mk(smax(a.x, R(0)), smax(a.y, R(0)), smax(a.z, R(0))));
+            R inside = smin(maxComponent(a), R(0));
+            return outside + inside;
+        }
+        case 2:  // plane
+            return q.z;
+        case 3: {  // cylinder
+            R dx = sqrt(q.x * q.x + q.y * q.y) - pr.size[0];
+            R dy = fabs(q.z) - pr.size[1];
+            R ox = smax(dx, R(0)), oy = smax(dy, R(0));
+            R outside = sqrt(ox * ox + oy * oy);
+            R inside = smin(smax(dx, dy), R(0));
+            return outside + inside;
+        }
+        default: {  // capsule
+            V3<R> c = mk(q.x, q.y, q.z - sclamp(q.z, -pr.size[1], pr.size[1]));
+            return length(c) - pr.size[0];
+        }
+    }
+}
+
+// evalGradientDetailed / evalGradient, primitives.hpp:96-108 (h = 1e-3)
+template <typename R>
+__device__ __forceinline__ V3<R> evalGradient(const DPrim<R>& pr, V3<R> p) {
+    const R h = R(1e-3);
+    V3<R> g = mk(evalPrim(pr, mk(p.x + h, p.y, p.z)) - evalPrim(pr, mk(p.x - h, p.y, p.z)),
+                 evalPrim(pr, mk(p.x, p.y + h, p.z)) - evalPrim(pr, mk(p.x, p.y - h, p.z)),
+                 evalPrim(pr, mk(p.x, p.y, p.z + h)) - evalPrim(pr, mk(p.x, p.y, p.z - h)));
+    R n = length(g);
+    if (n < R(1e-6) * R(2) * h) return mk(R(1), R(0), R(0));
+    return g / n;
+}
+
+// ------------------------------------------------------------------ scene.hpp
+// queryCore (scene.hpp:214-332): exactly min(naive SDF, initD); owner = the first
+// primitive in cluster order attaining it (or -1). Clusters are walked in order
+// by every lane of the warp, so the per-cluster bounds and member records are
+// warp-uniform loads (L1 broadcast) and the kind switch is a uniform branch.
+template <typename R, bool ST>
+__device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int* owner, Counters* c) {
+    R d = initD;
+    int own = -1;
+    if (ST) ++c->q;
+    const int K = s.n_clusters;
+    for (int k = 0; k < K; ++k) {
+        const DCluster<R>& cl = s.clusters[k];
+        R dx = smax(smax(cl.lo[0] - p.x, p.x - cl.hi[0]), R(0));
+        R dy = smax(smax(cl.lo[1] - p.y, p.y - cl.hi[1]), R(0));
+        R dz = smax(smax(cl.lo[2] - p.z, p.z - cl.hi[2]), R(0));
+        R boxSq = dx * dx + dy * dy + dz * dz;
+        if (!cl.unbounded && (d > R(0) ? boxSq >= d * d : boxSq > R(0))) {
+            if (ST) ++c->cs;
+            continue;
+        }
+        const int b = s.cstart[k], e = s.cstart[k + 1];
+        if (ST) {
+            ++c->cv;
+            c->pe += e - b;
+        }
+        for (int j = b; j < e; ++j) {
+            R pd = evalPrim(s.prims[j], p);
+            if (pd < d) {
+                d = pd;
+                own = j;
+            }
+        }
+    }
+    if (owner) *owner = own;
+    return d;
+}
+
+template <typename R> struct Hit {
+    R t;
+    V3<R> pos;
+    V3<R> normal;
+    int prim;      // CSR position, -1 if none
+    int converged;
+    int miss;      // 0 None, 1 TMax, 2 StepLimit
+    int steps;
+};
+
+// Margins sized for the arithmetic: the reference's 1e-9 (scene.hpp:407,412) is
+// below float resolution at scene scale.
+template <typename R> __device__ __forceinline__ R polishPad(R d);
+template <> __device__ __forceinline__ double polishPad<double>(double d) { return d + 1e-9; }
+template <> __device__ __forceinline__ float polishPad<float>(float d) { return d + fmaxf(fabsf(d) * 1e-6f, 1e-9f); }
+
+// sphereTrace, scene.hpp:391-435 (2*lastD seeding, polish, owner, normal)
+template <typename R, bool ST>
+__device__ Hit<R> sphereTrace(const SceneView<R>& s, V3<R> o, V3<R> dir, R tMax, R eps, int maxSteps,
+                              Counters* c, R startBound) {
+    if (ST) ++c->sphere;
+    Hit<R> hit;
+    hit.t = R(0);
+    hit.pos = mk(R(0), R(0), R(0));
+    hit.normal = mk(R(0), R(0), R(1));
+    hit.prim = -1;
+    hit.converged = 0;
+    hit.miss = 0;
+    R t = R(0);
+    R lastD = startBound * R(0.5);
+    for (int step = 0; step < maxSteps; ++step) {
+        if (ST) ++c->steps;
+        V3<R> p = o + dir * t;
+        R d = query<R, ST>(s, p, R(2) * lastD, nullptr, c);
+        if (d < eps) {
+            int owner = -1;
+            d = query<R, ST>(s, p, polishPad(d), &owner, c);
+            for (int i = 0; i < 8 && fabs(d) > R(0.25) * eps; ++i) {
+                t += d;
+                p = o + dir * t;
+                int o2 = -1;
+                d = query<R, ST>(s, p, polishPad(R(2) * fabs(d)), &o2, c);
+                if (o2 >= 0) owner = o2;
+            }
+            hit.converged = 1;
+            hit.t = t;
+            hit.pos = p;
+            hit.prim = owner;
+            hit.steps = step + 1;
+            if (owner >= 0) hit.normal = evalGradient(s.prims[owner], p);
+            return hit;
+        }
+        if (d >= tMax - t) {
+            hit.miss = 1;
+            hit.steps = step + 1;
+            return hit;
+        }
+        t += d;
+        lastD = d;
+    }
+    hit.miss = 2;
+    hit.steps = maxSteps;
+    return hit;
+}
+
+// softShadowTrace, scene.hpp:459-476
+template <typename R, bool ST>
+__device__ R softShadowTrace(const SceneView<R>& s, V3<R> o, V3<R> dir, R tMin, R tMax, R k, int maxSteps,
+                             Counters* c) {
+    const R minStep = R(5e-4);
+    const R inf = R(INFINITY);
+    if (ST) ++c->shadow;
+    R v = R(1);
+    R t = tMin;
+    R lastD = inf;
+    for (int step = 0; step < maxSteps && t < tMax; ++step) {
+        if (ST) ++c->steps;
+        R d = query<R, ST>(s, o + dir * t, lastD == inf ? inf : R(2) * lastD, nullptr, c);
+        v = smin(v, sclamp(k * d / t, R(0), R(1)));
+        if (v < R(1e-3)) return R(0);
+        t += smax(d, minStep);
+        lastD = smax(d, minStep);
+    }
+    return v;
+}
+
+// ------------------------------------------------------------- octahedral.hpp
+template <typename R> struct V2 {
+    R x, y;
+};
+template <typename R> __device__ __forceinline__ R signNotZero(R v) { return v >= R(0) ? R(1) : R(-1); }
+// octEncode, octahedral.hpp:13-24
+template <typename R> __device__ __forceinline__ V2<R> octEncode(V3<R> d) {
+    R norm = fabs(d.x) + fabs(d.y) + fabs(d.z);
+    R px = d.x / norm;
+    R py = d.y / norm;
+    if (d.z < R(0)) {
+        R ox = (R(1) - fabs(py)) * signNotZero(px);
+        R oy = (R(1) - fabs(px)) * signNotZero(py);
+        px = ox;
+        py = oy;
+    }
+    return V2<R>{px * R(0.5) + R(0.5), py * R(0.5) + R(0.5)};
+}
+// octDecode, octahedral.hpp:26-36
+template <typename R> __device__ __forceinline__ V3<R> octDecode(V2<R> uv) {
+    R fx = uv.x * R(2) - R(1);
+    R fy = uv.y * R(2) - R(1);
+    V3<R> n = mk(fx, fy, R(1) - fabs(fx) - fabs(fy));
+    if (n.z < R(0)) {
+        R t = -n.z;
+        n.x += n.x >= R(0) ? -t : t;
+        n.y += n.y >= R(0) ? -t : t;
+    }
+    return normalize(n);
+}
+
+// ------------------------------------------------------------ probe volume
+struct CascadeDev {
+    int res[3];
+    int base;         // first probe of this cascade in the concatenated arrays
+    double spacing;
+    double origin[3];
+    int level;
+    int _pad;
+};
+constexpr int kMaxCascades = 8;
+
+// Probe state, structure-of-arrays over all cascades (concatenated).
+struct ProbesView {
+    double* pos;       // 3 per probe (AoS xyz: stencil gathers read whole vectors)
+    double* rest;      // 3 per probe
+    double* last;      // 3 per probe
+    int* alive;
+    int* reject;
+    int* lastFrame;
+};
+
+// ProbeAtlas layout (atlas.hpp:119-124): tile (R+2)^2 texels of 3 floats, probe-major.
+struct AtlasView {
+    const float* __restrict__ data;
+    int res;
+    int tile;
+};
+
+// sampleBilinear, atlas.hpp:59-75 (double arithmetic on float texels in both modes;
+// the lookup is 8 per bounce, not a hot loop)
+__device__ __forceinline__ V3<double> sampleBilinear(const AtlasView& a, int probe, V2<double> uv) {
+    double cx = sclamp(uv.x, 0.0, 1.0) * a.res + 1.0;
+    double cy = sclamp(uv.y, 0.0, 1.0) * a.res + 1.0;
+    int x0 = static_cast<int>(floor(cx - 0.5));
+    int y0 = static_cast<int>(floor(cy - 0.5));
+    double tx = cx - 0.5 - x0;
+    double ty = cy - 0.5 - y0;
+    x0 = iclamp(x0, 0, a.tile - 2);
+    y0 = iclamp(y0, 0, a.tile - 2);
+    const float* base = a.data + static_cast<size_t>(probe) * a.tile * a.tile * 3;
+    auto fetch = [&](int x, int y) {
+        const float* p = base + (y * a.tile + x) * 3;
+        return mk<double>(__ldg(p), __ldg(p + 1), __ldg(p + 2));
+    };
+    V3<double> A = lerp(fetch(x0, y0), fetch(x0 + 1, y0), tx);
+    V3<double> B = lerp(fetch(x0, y0 + 1), fetch(x0 + 1, y0 + 1), tx);
+    return lerp(A, B, ty);
+}
+
+// mvcWeightsHex, mean_value.hpp:16-107 (always double)
+__device__ inline bool mvcWeightsHex(const V3<double>* corners, V3<double> x, double* weights) {
+    const int faces[6][4] = {{0, 2, 3, 1}, {4, 5, 7, 6}, {0, 1, 5, 4}, {2, 6, 7, 3}, {0, 4, 6, 2}, {1, 3, 7, 5}};
+    const double eps = 1e-10;
+    for (int i = 0; i < 8; ++i) weights[i] = 0.0;
+    double dist[8];
+    V3<double> unit[8];
+    for (int i = 0; i < 8; ++i) {
+        V3<double> v = corners[i] - x;
+        dist[i] = length(v);
+        if (dist[i] < eps) {
+            weights[i] = 1.0;
+            return true;
+        }
+        unit[i] = v / dist[i];
+    }
+    bool any = false;
+    for (int f = 0; f < 6; ++f) {
+        const int tris[2][3] = {{faces[f][0], faces[f][1], faces[f][2]}, {faces[f][0], faces[f][2], faces[f][3]}};
+        for (int tr = 0; tr < 2; ++tr) {
+            const int* tri = tris[tr];
+            double d[3], theta[3];
+            V3<double> u[3];
+            for (int i = 0; i < 3; ++i) {
+                d[i] = dist[tri[i]];
+                u[i] = unit[tri[i]];
+            }
+            for (int i = 0; i < 3; ++i) {
+                double l = length(u[(i + 1) % 3] - u[(i + 2) % 3]);
+                theta[i] = 2.0 * asin(sclamp(l * 0.5, 0.0, 1.0));
+            }
+            double h = (theta[0] + theta[1] + theta[2]) * 0.5;
+            if (kPi - h < 1e-8) {
+                for (int i = 0; i < 8; ++i) weights[i] = 0.0;
+                double total = 0;
+                double w[3];
+                for (int i = 0; i < 3; ++i) {
+                    w[i] = sin(theta[i]) * d[(i + 1) % 3] * d[(i + 2) % 3];
+                    total += w[i];
+                }
+                if (total < eps) return false;
+                for (int i = 0; i < 3; ++i) weights[tri[i]] = w[i] / total;
+                return true;
+            }
+            // cross(u1, u2), vec.hpp:51-53
+            V3<double> cr = mk(u[1].y * u[2].z - u[1].z * u[2].y, u[1].z * u[2].x - u[1].x * u[2].z,
+                               u[1].x * u[2].y - u[1].y * u[2].x);
+            double det = dot(u[0], cr);
+            double sign = det >= 0 ? 1.0 : -1.0;
+            double c[3], s[3];
+            bool skip = false;
+            for (int i = 0; i < 3; ++i) {
+                double denom = sin(theta[(i + 1) % 3]) * sin(theta[(i + 2) % 3]);
+                if (fabs(denom) < eps) {
+                    skip = true;
+                    break;
+                }
+                c[i] = (2.0 * sin(h) * sin(h - theta[i])) / denom - 1.0;
+                s[i] = sign * sqrt(smax(0.0, 1.0 - c[i] * c[i]));
+                if (fabs(s[i]) <= eps) {
+                    skip = true;
+                    break;
+                }
+            }
+            if (skip) continue;
+            for (int i = 0; i < 3; ++i) {
+                double w = (theta[i] - c[(i + 1) % 3] * theta[(i + 2) % 3] - c[(i + 2) % 3] * theta[(i + 1) % 3]) /
+                           (d[i] * sin(theta[(i + 1) % 3]) * s[(i + 2) % 3]);
+                weights[tri[i]] += w;
+                any = true;
+            }
+        }
+    }
+    if (!any) return false;
+    double total = 0;
+    for (int i = 0; i < 8; ++i) total += weights[i];
+    if (fabs(total) < eps || !isfinite(total)) return false;
+    for (int i = 0; i < 8; ++i) weights[i] /= total;
+    return true;
+}
+
+struct Stencil {
+    int cascade;      // chosen cascade slot (-1: sky fallback)
+    int probe[8];     // probe index within the cascade
+    double w[8];
+    int count;
+    int sky;
+    int usedMvc;
+};
+
+// interpolationStencil, probe_volume.hpp:224-310 (always double: positions are
+// double on the device in both modes)
+__device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, const ProbesView& pv, V3<double> point,
+                                        double mvcFrac) {
+    Stencil st;
+    st.count = 0;
+    st.sky = 0;
+    st.usedMvc = 0;
+    st.cascade = -1;
+    int chosen = -1;
+    int cell[3] = {0, 0, 0};
+    int containing = 0;
+    for (int ci = 0; ci < nCas; ++ci) {
+        const CascadeDev& c = cas[ci];
+        V3<double> f = (point - mk(c.origin[0], c.origin[1], c.origin[2])) / c.spacing;
+        int ix = static_cast<int>(floor(f.x));
+        int iy = static_cast<int>(floor(f.y));
+        int iz = static_cast<int>(floor(f.z));
+        bool inside = ix >= 0 && ix + 1 < c.res[0] && iy >= 0 && iy + 1 < c.res[1] && iz >= 0 && iz + 1 < c.res[2];
+        if (!inside) continue;
+        ++containing;
+        if (chosen < 0 || c.spacing < cas[chosen].spacing) {
+            chosen = ci;
+            cell[0] = ix;
+            cell[1] = iy;
+            cell[2] = iz;
+        }
+    }
+    bool insideCoarser = containing > 1;
+    if (chosen < 0) {
+        st.sky = 1;
+        return st;
+    }
+    const CascadeDev& c = cas[chosen];
+    V3<double> f = (point - mk(c.origin[0], c.origin[1], c.origin[2])) / c.spacing;
+    double tx = f.x - cell[0], ty = f.y - cell[1], tz = f.z - cell[2];
+    V3<double> corners[8];
+    int pidx[8];
+    double maxDisp = 0;
+    for (int k = 0; k < 8; ++k) {
+        int ix = cell[0] + (k & 1), iy = cell[1] + ((k >> 1) & 1), iz = cell[2] + ((k >> 2) & 1);
+        int pi = ix + c.res[0] * (iy + c.res[1] * iz);
+        pidx[k] = pi;
+        const double* P = pv.pos + 3 * static_cast<size_t>(c.base + pi);
+        const double* Q = pv.rest + 3 * static_cast<size_t>(c.base + pi);
+        corners[k] = mk(P[0], P[1], P[2]);
+        maxDisp = smax(maxDisp, length(corners[k] - mk(Q[0], Q[1], Q[2])));
+    }
+    bool boundary = insideCoarser && (cell[0] == 0 || cell[0] + 2 == c.res[0] || cell[1] == 0 ||
+                                      cell[1] + 2 == c.res[1] || cell[2] == 0 || cell[2] + 2 == c.res[2]);
+    double w[8];
+    bool wantMvc = maxDisp > mvcFrac * c.spacing || boundary;
+    bool haveMvc = false;
+    if (wantMvc) {
+        haveMvc = mvcWeightsHex(corners, point, w);
+        if (haveMvc) {
+            for (int k = 0; k < 8; ++k) w[k] = smax(0.0, w[k]);
+            st.usedMvc = 1;
+        }
+    }
+    if (!haveMvc) {
+        for (int k = 0; k < 8; ++k) {
+            double wx = (k & 1) ? tx : 1 - tx;
+            double wy = ((k >> 1) & 1) ? ty : 1 - ty;
+            double wz = ((k >> 2) & 1) ? tz : 1 - tz;
+            w[k] = wx * wy * wz;
+        }
+    }
+    double sum = 0;
+    for (int k = 0; k < 8; ++k) {
+        if (!pv.alive[c.base + pidx[k]]) w[k] = 0;
+        sum += w[k];
+    }
+    if (sum <= 1e-12) {
+        st.sky = 1;
+        return st;
+    }
+    for (int k = 0; k < 8; ++k) {
+        st.probe[k] = pidx[k];
+        st.w[k] = w[k] / sum;
+    }
+    st.cascade = chosen;
+    st.count = 8;
+    return st;
+}
+
+// sampleBounceIrradiance, probe_update.hpp:63-92. Returns false when "empty".
+__device__ inline bool sampleBounceIrradiance(const CascadeDev* cas, int nCas, const ProbesView& pv,
+                                       const float* atlas, int oct, V3<double> pos, V3<double> normal,
+                                       double mvcFrac, V3<double>* out) {
+    if (nCas <= 0) return false;
+    Stencil st = interpolationStencil(cas, nCas, pv, pos, mvcFrac);
+    if (st.sky || st.count == 0) return false;
+    const CascadeDev& c = cas[st.cascade];
+    double wsum = 0;
+    double w[8];
+    for (int i = 0; i < 8; ++i) w[i] = 0;
+    for (int i = 0; i < st.count; ++i) {
+        if (st.w[i] <= 0) continue;
+        const double* P = pv.pos + 3 * static_cast<size_t>(c.base + st.probe[i]);
+        V3<double> toProbe = mk(P[0], P[1], P[2]) - pos;
+        double len = length(toProbe);
+        double facing = len > 1e-9 ? dot(toProbe / len, normal) : 1.0;
+        double backface = (facing + 1.0) * 0.5;
+        w[i] = st.w[i] * backface * backface;
+        wsum += w[i];
+    }
+    if (wsum <= 1e-12) return false;
+    V3<double> acc = mk(0.0, 0.0, 0.0);
+    V2<double> uv = octEncode(normal);
+    AtlasView av{atlas, oct, oct + 2};
+    for (int i = 0; i < st.count; ++i) {
+        if (w[i] <= 0) continue;
+        acc = acc + sampleBilinear(av, c.base + st.probe[i], uv) * (w[i] / wsum);
+    }
+    *out = acc;
+    return true;
+}
+
+// Everything updateProbe / contactGI needs from RenderConfig (config.hpp:9-50).
+struct TraceCfg {
+    double eps;
+    double rayTMax;
+    double shadowK;
+    double bounceCoeff;
+    double mvcFrac;
+    int maxSteps;
+    int shadowSteps;
+};
+
+// directIrradiance, probe_update.hpp:97-132
+template <typename R, bool ST>
+__device__ V3<double> directIrradiance(const SceneView<R>& s, V3<R> pos, V3<R> normal, const TraceCfg& cfg,
+                                       Counters* c) {
+    V3<double> total = mk(0.0, 0.0, 0.0);
+    for (int li = 0; li < s.n_lights; ++li) {
+        const DLight& L = s.lights[li];
+        V3<R> dir;
+        R tMax;
+        V3<double> unshadowed;
+        V3<double> I = mk(L.intensity[0], L.intensity[1], L.intensity[2]);
+        if (L.kind == 0) {
+            V3<R> toLight = mk(R(L.position[0]), R(L.position[1]), R(L.position[2])) - pos;
+            R r2 = dot(toLight, toLight);
+            if (r2 < R(1e-12)) continue;
+            R r = sqrt(r2);
+            dir = toLight / r;
+            R cosT = dot(normal, dir);
+            if (cosT <= R(0)) continue;
+            unshadowed = I * static_cast<double>(cosT / r2);
+            tMax = r;
+        } else if (L.kind == 1) {
+            dir = mk(R(-L.direction[0]), R(-L.direction[1]), R(-L.direction[2]));
+            R cosT = dot(normal, dir);
+            if (cosT <= R(0)) continue;
+            unshadowed = I * static_cast<double>(cosT);
+            tMax = R(cfg.rayTMax);
+        } else {
+            continue;
+        }
+        R cosT = dot(normal, dir);
+        R bias = R(2.0) * R(cfg.eps) / smax(R(0.1), cosT);
+        R vis = R(1);
+        if (tMax - bias > bias)
+            vis = softShadowTrace<R, ST>(s, pos + normal * bias, dir, bias, tMax - bias, R(cfg.shadowK),
+                                         cfg.shadowSteps, c);
+        total = total + unshadowed * static_cast<double>(vis);
+    }
+    return total;
+}
+
+// shadeHit, probe_update.hpp:136-149 (converged hit with owner `prim` in CSR order)
+template <typename R, bool ST>
+__device__ V3<double> shadeHit(const SceneView<R>& s, const Hit<R>& hit, const CascadeDev* cas, int nCas,
+                               const ProbesView& pv, const float* prevAtlas, int oct, const TraceCfg& cfg,
+                               Counters* c) {
+    if (hit.prim < 0) return mk(s.sky[0], s.sky[1], s.sky[2]);
+    const double* A = s.albedo + 3 * hit.prim;
+    const double* E = s.emission + 3 * hit.prim;
+    V3<double> brdf = mk(A[0], A[1], A[2]) / kPi;
+    V3<double> direct = directIrradiance<R, ST>(s, hit.pos, hit.normal, cfg, c);
+    V3<double> radiance = mk(E[0], E[1], E[2]) + brdf * direct;
+    if (cfg.bounceCoeff > 0 && prevAtlas != nullptr) {
+        V3<double> prev;
+        V3<double> hp = mk<double>(hit.pos.x, hit.pos.y, hit.pos.z);
+        V3<double> hn = mk<double>(hit.normal.x, hit.normal.y, hit.normal.z);
+        if (sampleBounceIrradiance(cas, nCas, pv, prevAtlas, oct, hp, hn, cfg.mvcFrac, &prev))
+            radiance = radiance + brdf * (prev * cfg.bounceCoeff);
+    }
+    return radiance;
+}
+
+// sampleDirections rotation, sampling.hpp:23-31 + randomRotation rng.hpp:72-90.
+// Row-major 3x3 into m.
+__device__ __forceinline__ void probeRotation(uint64_t seed, int frame, bool rotatePerFrame, uint64_t key,
+                                              double* m) {
+    Rng rng(hashCombine(hashCombine(hashCombine(seed, rotatePerFrame ? static_cast<uint64_t>(static_cast<int64_t>(frame))
+                                                                      : 0xf1b0ull),
+                                                key),
+                                    0x5df6d1ull));
+    double u1 = rng.uniform(), u2 = rng.uniform(), u3 = rng.uniform();
+    double a = sqrt(1.0 - u1), b = sqrt(u1);
+    double qx = a * sin(2 * kPi * u2);
+    double qy = a * cos(2 * kPi * u2);
+    double qz = b * sin(2 * kPi * u3);
+    double qw = b * cos(2 * kPi * u3);
+    m[0] = 1 - 2 * (qy * qy + qz * qz);
+    m[1] = 2 * (qx * qy - qz * qw);
+    m[2] = 2 * (qx * qz + qy * qw);
+    m[3] = 2 * (qx * qy + qz * qw);
+    m[4] = 1 - 2 * (qx * qx + qz * qz);
+    m[5] = 2 * (qy * qz - qx * qw);
+    m[6] = 2 * (qx * qz - qy * qw);
+    m[7] = 2 * (qy * qz + qx * qw);
+    m[8] = 1 - 2 * (qx * qx + qy * qy);
+}
+
+// rot * sphericalFibonacci(i, n), sampling.hpp:11-17,28
+__device__ __forceinline__ V3<double> probeRayDir(const double* m, int i, int n) {
+    const double goldenAngle = kPi * (3.0 - sqrt(5.0));
+    double z = 1.0 - (2.0 * i + 1.0) / n;
+    double r = sqrt(smax(0.0, 1.0 - z * z));
+    double phi = goldenAngle * i;
+    V3<double> v = mk(r * cos(phi), r * sin(phi), z);
+    return mk(m[0] * v.x + m[1] * v.y + m[2] * v.z, m[3] * v.x + m[4] * v.y + m[5] * v.z,
+              m[6] * v.x + m[7] * v.y + m[8] * v.z);
+}
+
+}  // namespace sdfgi_dev

@@ -1,0 +1,920 @@
+// sdfgi_abi.cu — the C-ABI (include/sdfgi_b200.h): context, device-resident scene,
+// probe state and double-buffered atlases, and the launch sequence of the probe
+// stage. Host code only; kernels live in kernels_f64.cu / kernels_f32.cu.
+//
+// HBM layout (per context):
+//   scene   prims in cluster (CSR) order, FP64 (128 B) and FP32 (64 B) copies;
+//           cluster cull boxes (FP64 56 B / FP32 32 B); CSR starts; CSR->original
+//           index; albedo/emission (FP64).
+//   probes  all cascades concatenated (cascade c starts at base[c]); pos/rest/last
+//           as xyz triples of double, alive/reject/lastFrame as int32.
+//   atlas   two buffers (front = read, back = write), all cascades concatenated,
+//           tile-major exactly as ProbeAtlas::raw() (atlas.hpp:119-124), so an
+//           atlas download is one contiguous copy and a z-slab is one byte range.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/sdfgi_b200.h"
+#include "kernels.cuh"
+
+using namespace sdfgi_dev;
+
+static_assert(sizeof(sdfgi_prim) == 184, "prim ABI");
+static_assert(sizeof(sdfgi_light) == 80, "light ABI");
+static_assert(sizeof(sdfgi_light) == sizeof(DLight), "light mirror");
+static_assert(sizeof(sdfgi_cluster) == 56, "cluster ABI");
+static_assert(sizeof(sdfgi_cfg) == 224, "cfg ABI");
+static_assert(sizeof(sdfgi_probe) == 88, "probe ABI");
+static_assert(sizeof(sdfgi_ray_record) == sizeof(RayRecord), "ray record mirror");
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess)                                                                  \
+            throw Error(e_ == cudaErrorMemoryAllocation ? SDFGI_ERR_OOM : SDFGI_ERR_CUDA,       \
+                        std::string(#x) + ": " + cudaGetErrorString(e_));                        \
+    } while (0)
+#define NK(x)                                                                                   \
+    do {                                                                                        \
+        ncclResult_t r_ = (x);                                                                  \
+        if (r_ != ncclSuccess) throw Error(SDFGI_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+#define REQ(cond, code, msg)                        \
+    do {                                            \
+        if (!(cond)) throw Error((code), (msg));    \
+    } while (0)
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return SDFGI_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SDFGI_ERR_INVALID;
+    }
+}
+
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        if (count == n && p) return;
+        free();
+        if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void free() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void upload(const T* h, size_t count, cudaStream_t s) {
+        alloc(count);
+        if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+};
+
+struct CascadeHost {
+    int res[3] = {0, 0, 0};
+    int level = 0;
+    double spacing = 1.0;
+    double origin[3] = {0, 0, 0};
+    int base = 0;
+    int count() const { return res[0] * res[1] * res[2]; }
+};
+
+struct Ctx {
+    int device = 0, rank = 0, world = 1, precision = SDFGI_F64;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    long long launches = 0;
+    // scene
+    bool haveScene = false;
+    int nPrims = 0, nClusters = 0, nLights = 0;
+    double sky[3] = {0, 0, 0};
+    DBuf<DPrim<double>> prim64;
+    DBuf<DPrim<float>> prim32;
+    DBuf<DCluster<double>> cl64;
+    DBuf<DCluster<float>> cl32;
+    DBuf<int> cstart, orig;
+    DBuf<double> albedo, emission;
+    DBuf<DLight> lights;
+    // probes
+    std::vector<CascadeHost> cascades;
+    int octRes = 8;
+    int totalProbes = 0;
+    DBuf<double> pos, rest, last;
+    DBuf<int> alive, reject, lastFrame;
+    DBuf<float> atlas[2];
+    int front = 0;
+    // scratch
+    DBuf<unsigned long long> scratch;  // [0..7] stats, [8] maxDelta bits, [9] rays, [10] updated
+    DBuf<int> report;
+    DBuf<int> refs;
+    DBuf<int> recOffset;
+    DBuf<RayRecord> records;
+    DBuf<double> qpts, qinit, qd;
+    DBuf<int> qowner;
+
+    ~Ctx() {
+        cudaSetDevice(device);
+        if (stream) cudaStreamSynchronize(stream);
+        prim64.free(); prim32.free(); cl64.free(); cl32.free(); cstart.free(); orig.free();
+        albedo.free(); emission.free(); lights.free();
+        pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
+        atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
+        recOffset.free(); records.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
+        if (comm) ncclCommDestroy(comm);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    size_t tileFloats() const { return static_cast<size_t>(octRes + 2) * (octRes + 2) * 3; }
+    size_t atlasFloats() const { return tileFloats() * totalProbes; }
+
+    ProbeCommon probeCommon() const {
+        ProbeCommon pc;
+        std::memset(&pc, 0, sizeof(pc));
+        pc.nCas = static_cast<int>(cascades.size());
+        for (int i = 0; i < pc.nCas; ++i) {
+            const CascadeHost& c = cascades[i];
+            for (int k = 0; k < 3; ++k) {
+                pc.cas[i].res[k] = c.res[k];
+                pc.cas[i].origin[k] = c.origin[k];
+            }
+            pc.cas[i].base = c.base;
+            pc.cas[i].spacing = c.spacing;
+            pc.cas[i].level = c.level;
+        }
+        pc.probes.pos = pos.p;
+        pc.probes.rest = rest.p;
+        pc.probes.last = last.p;
+        pc.probes.alive = alive.p;
+        pc.probes.reject = reject.p;
+        pc.probes.lastFrame = lastFrame.p;
+        return pc;
+    }
+
+    template <typename R>
+    SceneView<R> sceneView() const;
+
+    int slot(int level) const {
+        for (size_t i = 0; i < cascades.size(); ++i)
+            if (cascades[i].level == level) return static_cast<int>(i);
+        throw Error(SDFGI_ERR_INVALID, "no cascade with level " + std::to_string(level));
+    }
+};
+
+template <>
+SceneView<double> Ctx::sceneView<double>() const {
+    SceneView<double> v;
+    v.prims = prim64.p;
+    v.clusters = cl64.p;
+    v.cstart = cstart.p;
+    v.orig = orig.p;
+    v.albedo = albedo.p;
+    v.emission = emission.p;
+    v.lights = lights.p;
+    v.n_prims = nPrims;
+    v.n_clusters = nClusters;
+    v.n_lights = nLights;
+    for (int k = 0; k < 3; ++k) v.sky[k] = sky[k];
+    return v;
+}
+template <>
+SceneView<float> Ctx::sceneView<float>() const {
+    SceneView<float> v;
+    v.prims = prim32.p;
+    v.clusters = cl32.p;
+    v.cstart = cstart.p;
+    v.orig = orig.p;
+    v.albedo = albedo.p;
+    v.emission = emission.p;
+    v.lights = lights.p;
+    v.n_prims = nPrims;
+    v.n_clusters = nClusters;
+    v.n_lights = nLights;
+    for (int k = 0; k < 3; ++k) v.sky[k] = sky[k];
+    return v;
+}
+
+Ctx* C(void* p) {
+    REQ(p != nullptr, SDFGI_ERR_INVALID, "null context");
+    Ctx* c = static_cast<Ctx*>(p);
+    CK(cudaSetDevice(c->device));
+    return c;
+}
+
+void requireProbes(Ctx* c) {
+    REQ(c->haveScene, SDFGI_ERR_STATE, "scene not uploaded");
+    REQ(!c->cascades.empty(), SDFGI_ERR_STATE, "no cascade set");
+}
+
+void checkLaunch(Ctx* c) {
+    ++c->launches;
+    CK(cudaGetLastError());
+}
+
+// Probe range [lo, hi) of cascade slot `ci` owned by this rank: a z-slab of
+// layers [resZ*r/W, resZ*(r+1)/W). Contiguous because
+// index = ix + resX*(iy + resY*iz) (probe_volume.hpp:32).
+void slabRange(const CascadeHost& c, int rank, int world, int* lo, int* hi) {
+    int z0 = static_cast<int>((static_cast<long long>(c.res[2]) * rank) / world);
+    int z1 = static_cast<int>((static_cast<long long>(c.res[2]) * (rank + 1)) / world);
+    int layer = c.res[0] * c.res[1];
+    *lo = c.base + z0 * layer;
+    *hi = c.base + z1 * layer;
+}
+
+void resetProbes(Ctx* c, int slot) {
+    const CascadeHost& cs = c->cascades[slot];
+    const int n = cs.count();
+    std::vector<double> r(3 * n);
+    std::vector<int> ones(n, 1), minus(n, -1);
+    for (int iz = 0; iz < cs.res[2]; ++iz)
+        for (int iy = 0; iy < cs.res[1]; ++iy)
+            for (int ix = 0; ix < cs.res[0]; ++ix) {
+                // restingAt, probe_volume.hpp:37-39
+                int i = ix + cs.res[0] * (iy + cs.res[1] * iz);
+                r[3 * i] = cs.origin[0] + ix * cs.spacing;
+                r[3 * i + 1] = cs.origin[1] + iy * cs.spacing;
+                r[3 * i + 2] = cs.origin[2] + iz * cs.spacing;
+            }
+    size_t off = static_cast<size_t>(cs.base);
+    CK(cudaMemcpyAsync(c->rest.p + 3 * off, r.data(), r.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->pos.p + 3 * off, r.data(), r.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->last.p + 3 * off, r.data(), r.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->alive.p + off, ones.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->reject.p + off, ones.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->lastFrame.p + off, minus.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
+    for (int b = 0; b < 2; ++b)
+        CK(cudaMemsetAsync(c->atlas[b].p + off * c->tileFloats(), 0, n * c->tileFloats() * 4, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+}
+
+void reallocProbes(Ctx* c) {
+    int total = 0;
+    for (auto& cs : c->cascades) {
+        cs.base = total;
+        total += cs.count();
+    }
+    // preserve existing cascades' state is not needed: set() resets the touched one and
+    // the concatenation may move, so reset all.
+    c->totalProbes = total;
+    c->pos.alloc(3 * static_cast<size_t>(total));
+    c->rest.alloc(3 * static_cast<size_t>(total));
+    c->last.alloc(3 * static_cast<size_t>(total));
+    c->alive.alloc(total);
+    c->reject.alloc(total);
+    c->lastFrame.alloc(total);
+    c->atlas[0].alloc(c->atlasFloats());
+    c->atlas[1].alloc(c->atlasFloats());
+    for (size_t i = 0; i < c->cascades.size(); ++i) resetProbes(c, static_cast<int>(i));
+}
+
+template <typename R>
+void fillPrim(DPrim<R>& d, const sdfgi_prim& s) {
+    for (int k = 0; k < 9; ++k) d.rot[k] = static_cast<R>(s.rot[k]);
+    for (int k = 0; k < 3; ++k) {
+        d.trans[k] = static_cast<R>(s.trans[k]);
+        d.size[k] = static_cast<R>(s.size[k]);
+    }
+    d.kind = s.kind;
+    // primitives.hpp:76: skip the rotation when the diagonal is exactly 1
+    d.identity = (s.rot[0] == 1.0 && s.rot[4] == 1.0 && s.rot[8] == 1.0) ? 1 : 0;
+}
+
+void readCounters(Ctx* c, sdfgi_stats* stats, unsigned long long* tail, int ntail) {
+    std::vector<unsigned long long> h(8 + ntail);
+    CK(cudaMemcpyAsync(h.data(), c->scratch.p, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (stats) {
+        stats->sdf_queries += h[0];
+        stats->clusters_visited += h[1];
+        stats->clusters_skipped += h[2];
+        stats->primitive_evals += h[3];
+        stats->trace_steps += h[4];
+        stats->sphere_traces += h[5];
+        stats->shadow_traces += h[6];
+        stats->visibility_traces += h[7];
+    }
+    for (int i = 0; i < ntail; ++i) tail[i] = h[8 + i];
+}
+
+template <typename R>
+UpdateParams<R> updateParams(Ctx* c, const sdfgi_cfg* cfg, int frame) {
+    UpdateParams<R> p;
+    std::memset(&p, 0, sizeof(p));
+    p.scene = c->sceneView<R>();
+    p.pc = c->probeCommon();
+    p.prevAtlas = c->atlas[c->front].p;
+    p.currAtlas = c->atlas[1 - c->front].p;
+    p.oct = c->octRes;
+    p.frame = frame;
+    p.tc.eps = cfg->surface_epsilon;
+    p.tc.rayTMax = cfg->ray_tmax;
+    p.tc.shadowK = cfg->shadow_k;
+    p.tc.bounceCoeff = cfg->bounce_coeff;
+    p.tc.mvcFrac = cfg->mvc_relocation_frac;
+    p.tc.maxSteps = static_cast<int>(cfg->max_trace_steps);
+    p.tc.shadowSteps = static_cast<int>(cfg->shadow_steps);
+    p.hysteresis = cfg->hysteresis;
+    p.alphaMin = cfg->alpha_min;
+    p.nRaysFull = static_cast<int>(cfg->n_rays_full);
+    p.seed = cfg->seed;
+    p.rotatePerFrame = static_cast<int>(cfg->rotate_per_frame);
+    p.stats = c->scratch.p;
+    p.maxDeltaBits = c->scratch.p + 8;
+    p.rays = c->scratch.p + 9;
+    p.updated = reinterpret_cast<unsigned int*>(c->scratch.p + 10);
+    return p;
+}
+
+void validateCfg(Ctx* c, const sdfgi_cfg* cfg) {
+    REQ(cfg != nullptr, SDFGI_ERR_INVALID, "null cfg");
+    REQ(cfg->oct_res == c->octRes, SDFGI_ERR_INVALID, "cfg.oct_res differs from the cascade atlas resolution");
+    REQ(cfg->n_rays_full > 0 && cfg->n_rays_full <= 4096, SDFGI_ERR_INVALID, "n_rays_full out of range");
+    REQ(cfg->max_trace_steps >= 0 && cfg->shadow_steps >= 0, SDFGI_ERR_INVALID, "negative step limits");
+}
+
+// Global probe ids (cascade base + index) for the update: the caller's refs, or
+// every probe; restricted to this rank's z-slabs when world > 1.
+std::vector<int> selectRefs(Ctx* c, const int32_t* refs, int nRefs) {
+    std::vector<int> out;
+    if (refs) {
+        REQ(nRefs >= 0, SDFGI_ERR_INVALID, "negative n_refs");
+        out.reserve(nRefs);
+        for (int i = 0; i < nRefs; ++i) {
+            int level = refs[2 * i], idx = refs[2 * i + 1];
+            int s = c->slot(level);
+            REQ(idx >= 0 && idx < c->cascades[s].count(), SDFGI_ERR_INVALID, "probe index out of range");
+            out.push_back(c->cascades[s].base + idx);
+        }
+    } else {
+        out.resize(c->totalProbes);
+        for (int i = 0; i < c->totalProbes; ++i) out[i] = i;
+    }
+    if (c->world > 1) {
+        std::vector<int> mine;
+        for (int g : out) {
+            int s = 0;
+            for (size_t k = 0; k < c->cascades.size(); ++k)
+                if (g >= c->cascades[k].base) s = static_cast<int>(k);
+            int lo, hi;
+            slabRange(c->cascades[s], c->rank, c->world, &lo, &hi);
+            if (g >= lo && g < hi) mine.push_back(g);
+        }
+        out.swap(mine);
+    }
+    return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sdfgi_abi_version(void) { return SDFGI_ABI_VERSION; }
+const char* sdfgi_last_error(void) { return g_err.c_str(); }
+
+int sdfgi_device_count(int* out) {
+    return guard([&] {
+        REQ(out, SDFGI_ERR_INVALID, "null out");
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+        *out = n;
+    });
+}
+
+int sdfgi_nccl_unique_id(uint8_t out[128]) {
+    return guard([&] {
+        REQ(out, SDFGI_ERR_INVALID, "null out");
+        static_assert(sizeof(ncclUniqueId) == 128, "nccl id size");
+        ncclUniqueId id;
+        NK(ncclGetUniqueId(&id));
+        std::memcpy(out, &id, 128);
+    });
+}
+
+int sdfgi_ctx_create(int device, int rank, int world, const uint8_t* nccl_uid, int precision, void** out_ctx) {
+    return guard([&] {
+        REQ(out_ctx, SDFGI_ERR_INVALID, "null out_ctx");
+        REQ(world >= 1 && rank >= 0 && rank < world, SDFGI_ERR_INVALID, "bad rank/world");
+        REQ(precision == SDFGI_F64 || precision == SDFGI_F32, SDFGI_ERR_INVALID, "bad precision");
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        REQ(e == cudaSuccess && n > 0, SDFGI_ERR_CUDA, "no CUDA device: the B200 path has no CPU fallback");
+        REQ(device >= 0 && device < n, SDFGI_ERR_INVALID, "device index out of range");
+        CK(cudaSetDevice(device));
+        Ctx* c = new Ctx();
+        c->device = device;
+        c->rank = rank;
+        c->world = world;
+        c->precision = precision;
+        try {
+            CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            c->scratch.alloc(16);
+            c->report.alloc(4);
+            if (world > 1) {
+                REQ(nccl_uid, SDFGI_ERR_INVALID, "world > 1 needs an NCCL unique id");
+                ncclUniqueId id;
+                std::memcpy(&id, nccl_uid, 128);
+                NK(ncclCommInitRank(&c->comm, world, id, rank));
+            }
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out_ctx = c;
+    });
+}
+
+int sdfgi_ctx_destroy(void* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        delete static_cast<Ctx*>(ctx);
+    });
+}
+
+int sdfgi_ctx_set_precision(void* ctx, int precision) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(precision == SDFGI_F64 || precision == SDFGI_F32, SDFGI_ERR_INVALID, "bad precision");
+        c->precision = precision;
+    });
+}
+
+int sdfgi_ctx_stream(void* ctx, void** out) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(out, SDFGI_ERR_INVALID, "null out");
+        *out = c->stream;
+    });
+}
+
+int sdfgi_ctx_synchronize(void* ctx) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int sdfgi_scene_upload(void* ctx, const sdfgi_prim* prims, int n_prims, const sdfgi_cluster* clusters,
+                       int n_clusters, const int32_t* member_start, const int32_t* member_idx,
+                       const sdfgi_light* lights, int n_lights, const double sky[3]) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(n_prims >= 0 && n_clusters >= 0 && n_lights >= 0, SDFGI_ERR_INVALID, "negative count");
+        REQ(n_prims == 0 || prims, SDFGI_ERR_INVALID, "null prims");
+        REQ(n_clusters == 0 || (clusters && member_start && member_idx), SDFGI_ERR_INVALID, "null clusters");
+        REQ(n_lights == 0 || lights, SDFGI_ERR_INVALID, "null lights");
+        REQ(sky, SDFGI_ERR_INVALID, "null sky");
+        int nMembers = n_clusters ? member_start[n_clusters] : 0;
+        REQ(n_clusters == 0 || member_start[0] == 0, SDFGI_ERR_INVALID, "member_start[0] != 0");
+        for (int k = 0; k < n_clusters; ++k)
+            REQ(member_start[k + 1] >= member_start[k], SDFGI_ERR_INVALID, "member_start not monotone");
+        for (int m = 0; m < nMembers; ++m)
+            REQ(member_idx[m] >= 0 && member_idx[m] < n_prims, SDFGI_ERR_INVALID, "member index out of range");
+        for (int i = 0; i < n_prims; ++i)
+            REQ(prims[i].kind >= 0 && prims[i].kind <= 4, SDFGI_ERR_INVALID, "bad primitive kind");
+        // cluster (CSR) order: device primitive j = prims[member_idx[j]]
+        std::vector<DPrim<double>> p64(nMembers);
+        std::vector<DPrim<float>> p32(nMembers);
+        std::vector<int> orig(nMembers);
+        std::vector<double> alb(3 * static_cast<size_t>(nMembers)), em(3 * static_cast<size_t>(nMembers));
+        for (int j = 0; j < nMembers; ++j) {
+            const sdfgi_prim& s = prims[member_idx[j]];
+            std::memset(&p64[j], 0, sizeof(p64[j]));
+            std::memset(&p32[j], 0, sizeof(p32[j]));
+            fillPrim(p64[j], s);
+            fillPrim(p32[j], s);
+            orig[j] = member_idx[j];
+            for (int k = 0; k < 3; ++k) {
+                alb[3 * j + k] = s.albedo[k];
+                em[3 * j + k] = s.emission[k];
+            }
+        }
+        std::vector<DCluster<double>> c64(n_clusters);
+        std::vector<DCluster<float>> c32(n_clusters);
+        for (int k = 0; k < n_clusters; ++k) {
+            std::memset(&c64[k], 0, sizeof(c64[k]));
+            std::memset(&c32[k], 0, sizeof(c32[k]));
+            for (int a = 0; a < 3; ++a) {
+                c64[k].lo[a] = clusters[k].lo[a];
+                c64[k].hi[a] = clusters[k].hi[a];
+                // FP32 cull boxes: widened so float rounding of the box distance can
+                // never skip a member the FP32 evaluation would have picked
+                double lo = clusters[k].lo[a], hi = clusters[k].hi[a];
+                double padLo = 1e-5 * (std::fabs(lo) + 1.0), padHi = 1e-5 * (std::fabs(hi) + 1.0);
+                c32[k].lo[a] = std::nextafter(static_cast<float>(lo - padLo), -INFINITY);
+                c32[k].hi[a] = std::nextafter(static_cast<float>(hi + padHi), INFINITY);
+            }
+            c64[k].unbounded = c32[k].unbounded = clusters[k].unbounded ? 1 : 0;
+        }
+        std::vector<int> starts(member_start, member_start + n_clusters + 1);
+        if (n_clusters == 0) starts.assign(1, 0);
+        c->prim64.upload(p64.data(), p64.size(), c->stream);
+        c->prim32.upload(p32.data(), p32.size(), c->stream);
+        c->cl64.upload(c64.data(), c64.size(), c->stream);
+        c->cl32.upload(c32.data(), c32.size(), c->stream);
+        c->cstart.upload(starts.data(), starts.size(), c->stream);
+        c->orig.upload(orig.data(), orig.size(), c->stream);
+        c->albedo.upload(alb.data(), alb.size(), c->stream);
+        c->emission.upload(em.data(), em.size(), c->stream);
+        c->lights.upload(reinterpret_cast<const DLight*>(lights), n_lights, c->stream);
+        CK(cudaStreamSynchronize(c->stream));
+        c->nPrims = nMembers;
+        c->nClusters = n_clusters;
+        c->nLights = n_lights;
+        for (int k = 0; k < 3; ++k) c->sky[k] = sky[k];
+        c->haveScene = true;
+    });
+}
+
+int sdfgi_lights_upload(void* ctx, const sdfgi_light* lights, int n_lights, const double sky[3]) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(c->haveScene, SDFGI_ERR_STATE, "scene not uploaded");
+        REQ(n_lights >= 0 && (n_lights == 0 || lights) && sky, SDFGI_ERR_INVALID, "bad lights");
+        c->lights.upload(reinterpret_cast<const DLight*>(lights), n_lights, c->stream);
+        CK(cudaStreamSynchronize(c->stream));
+        c->nLights = n_lights;
+        for (int k = 0; k < 3; ++k) c->sky[k] = sky[k];
+    });
+}
+
+int sdfgi_cascade_set(void* ctx, int level, int res_x, int res_y, int res_z, double spacing, const double origin[3],
+                      int oct_res) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(res_x > 0 && res_y > 0 && res_z > 0, SDFGI_ERR_INVALID, "resolution must be positive");
+        REQ(spacing > 0 && origin, SDFGI_ERR_INVALID, "bad spacing/origin");
+        REQ(oct_res >= 1 && oct_res <= 10, SDFGI_ERR_INVALID, "oct_res must be in [1, 10]");
+        REQ(c->cascades.empty() || oct_res == c->octRes, SDFGI_ERR_INVALID, "all cascades share one oct_res");
+        REQ(static_cast<long long>(res_x) * res_y * res_z < (1LL << 30), SDFGI_ERR_INVALID, "too many probes");
+        CascadeHost h;
+        h.res[0] = res_x;
+        h.res[1] = res_y;
+        h.res[2] = res_z;
+        h.level = level;
+        h.spacing = spacing;
+        for (int k = 0; k < 3; ++k) h.origin[k] = origin[k];
+        bool replaced = false;
+        for (auto& cs : c->cascades)
+            if (cs.level == level) {
+                cs = h;
+                replaced = true;
+            }
+        if (!replaced) {
+            REQ(static_cast<int>(c->cascades.size()) < kMaxCascades, SDFGI_ERR_INVALID, "too many cascades");
+            c->cascades.push_back(h);
+        }
+        c->octRes = oct_res;
+        c->front = 0;
+        reallocProbes(c);
+    });
+}
+
+int sdfgi_cascade_count(void* ctx, int* out) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(out, SDFGI_ERR_INVALID, "null out");
+        *out = static_cast<int>(c->cascades.size());
+    });
+}
+
+int sdfgi_probes_reset(void* ctx, int level) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        resetProbes(c, c->slot(level));
+    });
+}
+
+int sdfgi_probes_upload(void* ctx, int level, const sdfgi_probe* probes, int n) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        int s = c->slot(level);
+        const CascadeHost& cs = c->cascades[s];
+        REQ(probes && n == cs.count(), SDFGI_ERR_INVALID, "probe count mismatch");
+        std::vector<double> pos(3 * n), rest(3 * n), last(3 * n);
+        std::vector<int> al(n), rj(n), lf(n);
+        for (int i = 0; i < n; ++i) {
+            for (int k = 0; k < 3; ++k) {
+                pos[3 * i + k] = probes[i].pos[k];
+                rest[3 * i + k] = probes[i].resting[k];
+                last[3 * i + k] = probes[i].last_pos[k];
+            }
+            al[i] = probes[i].alive;
+            rj[i] = probes[i].reject_history;
+            lf[i] = probes[i].last_update_frame;
+        }
+        size_t off = cs.base;
+        CK(cudaMemcpyAsync(c->pos.p + 3 * off, pos.data(), pos.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->rest.p + 3 * off, rest.data(), rest.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->last.p + 3 * off, last.data(), last.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->alive.p + off, al.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->reject.p + off, rj.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->lastFrame.p + off, lf.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int sdfgi_probes_download(void* ctx, int level, sdfgi_probe* probes, int n) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        int s = c->slot(level);
+        const CascadeHost& cs = c->cascades[s];
+        REQ(probes && n == cs.count(), SDFGI_ERR_INVALID, "probe count mismatch");
+        std::vector<double> pos(3 * n), rest(3 * n), last(3 * n);
+        std::vector<int> al(n), rj(n), lf(n);
+        size_t off = cs.base;
+        CK(cudaMemcpyAsync(pos.data(), c->pos.p + 3 * off, pos.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(rest.data(), c->rest.p + 3 * off, rest.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(last.data(), c->last.p + 3 * off, last.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(al.data(), c->alive.p + off, n * 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(rj.data(), c->reject.p + off, n * 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(lf.data(), c->lastFrame.p + off, n * 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int i = 0; i < n; ++i) {
+            std::memset(&probes[i], 0, sizeof(sdfgi_probe));
+            for (int k = 0; k < 3; ++k) {
+                probes[i].pos[k] = pos[3 * i + k];
+                probes[i].resting[k] = rest[3 * i + k];
+                probes[i].last_pos[k] = last[3 * i + k];
+            }
+            probes[i].alive = al[i];
+            probes[i].reject_history = rj[i];
+            probes[i].last_update_frame = lf[i];
+        }
+    });
+}
+
+int sdfgi_probes_relocate(void* ctx, int level, double threshold1, double threshold2, int max_descent_steps,
+                          double gradient_step, sdfgi_reloc_report* report, sdfgi_stats* stats) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        requireProbes(c);
+        int s = c->slot(level);
+        RelocParams p;
+        std::memset(&p, 0, sizeof(p));
+        p.scene = c->sceneView<double>();
+        p.pc = c->probeCommon();
+        p.cascade = s;
+        p.th1 = threshold1;
+        p.th2 = threshold2;
+        p.maxSteps = max_descent_steps;
+        p.gradStep = gradient_step;
+        p.report = c->report.p;
+        p.stats = c->scratch.p;
+        CK(cudaMemsetAsync(c->report.p, 0, 4 * sizeof(int), c->stream));
+        CK(cudaMemsetAsync(c->scratch.p, 0, 16 * 8, c->stream));
+        // relocation is replicated on every rank (deterministic, bit-exact): no exchange
+        launch_relocate(p, c->cascades[s].count(), stats != nullptr, c->stream);
+        checkLaunch(c);
+        int rep[4];
+        CK(cudaMemcpyAsync(rep, c->report.p, sizeof(rep), cudaMemcpyDeviceToHost, c->stream));
+        readCounters(c, stats, nullptr, 0);
+        if (report) {
+            report->relocated = rep[0];
+            report->rejected = rep[1];
+            report->dead = rep[2];
+            report->_pad = 0;
+        }
+    });
+}
+
+int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_refs, int frame, const sdfgi_cfg* cfg,
+                        sdfgi_update_result* result, sdfgi_stats* stats) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        requireProbes(c);
+        validateCfg(c, cfg);
+        std::vector<int> refs = selectRefs(c, probe_refs, n_refs);
+        float* back = c->atlas[1 - c->front].p;
+        const float* frontp = c->atlas[c->front].p;
+        // atlas_[write] = atlas_[read] (pipeline.hpp:131); updated tiles are overwritten
+        CK(cudaMemcpyAsync(back, frontp, c->atlasFloats() * 4, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaMemsetAsync(c->scratch.p, 0, 16 * 8, c->stream));
+        const int maxRays = 2 * static_cast<int>(cfg->n_rays_full);
+        const bool all = (probe_refs == nullptr && c->world == 1);
+        if (!all) c->refs.upload(refs.data(), refs.size(), c->stream);
+        const int nBlocks = static_cast<int>(refs.size());
+        if (nBlocks > 0) {
+            if (c->precision == SDFGI_F64) {
+                UpdateParams<double> p = updateParams<double>(c, cfg, frame);
+                p.refs = all ? nullptr : c->refs.p;
+                p.nRefs = nBlocks;
+                launch_probe_update<double>(p, nBlocks, maxRays, stats != nullptr, c->stream);
+            } else {
+                UpdateParams<float> p = updateParams<float>(c, cfg, frame);
+                p.refs = all ? nullptr : c->refs.p;
+                p.nRefs = nBlocks;
+                launch_probe_update<float>(p, nBlocks, maxRays, stats != nullptr, c->stream);
+            }
+            checkLaunch(c);
+        }
+        if (c->world > 1) {
+            // all-gather the back atlas slabs in place (one broadcast per rank-owned
+            // slab: slabs may be uneven), then sum counters / max the jitter metric.
+            NK(ncclGroupStart());
+            for (auto& cs : c->cascades)
+                for (int r = 0; r < c->world; ++r) {
+                    int lo, hi;
+                    slabRange(cs, r, c->world, &lo, &hi);
+                    if (hi <= lo) continue;
+                    float* ptr = back + static_cast<size_t>(lo) * c->tileFloats();
+                    NK(ncclBroadcast(ptr, ptr, static_cast<size_t>(hi - lo) * c->tileFloats(), ncclFloat, r, c->comm,
+                                     c->stream));
+                }
+            NK(ncclGroupEnd());
+            NK(ncclAllReduce(c->scratch.p, c->scratch.p, 8, ncclUint64, ncclSum, c->comm, c->stream));
+            NK(ncclAllReduce(c->scratch.p + 8, c->scratch.p + 8, 1, ncclUint64, ncclMax, c->comm, c->stream));
+            NK(ncclAllReduce(c->scratch.p + 9, c->scratch.p + 9, 2, ncclUint64, ncclSum, c->comm, c->stream));
+        }
+        unsigned long long tail[3];
+        readCounters(c, stats, tail, 3);
+        if (c->world > 1) {
+            // every rank marks every updated probe (probe_update.hpp:208-209) so the
+            // replicated probe state stays identical without an exchange
+            std::vector<int> allRefs;
+            if (probe_refs) {
+                for (int i = 0; i < n_refs; ++i)
+                    allRefs.push_back(c->cascades[c->slot(probe_refs[2 * i])].base + probe_refs[2 * i + 1]);
+            } else {
+                for (int i = 0; i < c->totalProbes; ++i) allRefs.push_back(i);
+            }
+            std::vector<int> al(c->totalProbes), rj(c->totalProbes), lf(c->totalProbes);
+            CK(cudaMemcpyAsync(al.data(), c->alive.p, al.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(rj.data(), c->reject.p, rj.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(lf.data(), c->lastFrame.p, lf.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            for (int g : allRefs)
+                if (al[g]) {
+                    rj[g] = 0;
+                    lf[g] = frame;
+                }
+            CK(cudaMemcpyAsync(c->reject.p, rj.data(), rj.size() * 4, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(c->lastFrame.p, lf.data(), lf.size() * 4, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        }
+        if (result) {
+            double md;
+            std::memcpy(&md, &tail[0], 8);
+            result->max_texel_delta = md;
+            result->rays_traced = static_cast<int64_t>(tail[1]);
+            result->probes_updated = static_cast<int64_t>(tail[2] & 0xffffffffull);
+        }
+    });
+}
+
+int sdfgi_atlas_swap(void* ctx) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        c->front = 1 - c->front;
+    });
+}
+
+int sdfgi_atlas_download(void* ctx, int level, int which, float* dst, size_t n_floats) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        int s = c->slot(level);
+        REQ(which == 0 || which == 1, SDFGI_ERR_INVALID, "which must be 0 or 1");
+        size_t n = c->tileFloats() * c->cascades[s].count();
+        REQ(dst && n_floats == n, SDFGI_ERR_INVALID, "atlas size mismatch");
+        const float* src = c->atlas[which == 0 ? c->front : 1 - c->front].p + c->tileFloats() * c->cascades[s].base;
+        CK(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int sdfgi_atlas_upload(void* ctx, int level, int which, const float* src, size_t n_floats) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        int s = c->slot(level);
+        REQ(which == 0 || which == 1, SDFGI_ERR_INVALID, "which must be 0 or 1");
+        size_t n = c->tileFloats() * c->cascades[s].count();
+        REQ(src && n_floats == n, SDFGI_ERR_INVALID, "atlas size mismatch");
+        float* dst = c->atlas[which == 0 ? c->front : 1 - c->front].p + c->tileFloats() * c->cascades[s].base;
+        CK(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int sdfgi_atlas_device_ptr(void* ctx, int level, int which, void** out_ptr, size_t* out_bytes) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        int s = c->slot(level);
+        REQ(which == 0 || which == 1, SDFGI_ERR_INVALID, "which must be 0 or 1");
+        REQ(out_ptr && out_bytes, SDFGI_ERR_INVALID, "null out");
+        *out_ptr = c->atlas[which == 0 ? c->front : 1 - c->front].p + c->tileFloats() * c->cascades[s].base;
+        *out_bytes = c->tileFloats() * c->cascades[s].count() * 4;
+    });
+}
+
+int sdfgi_probes_trace_debug(void* ctx, const int32_t* probe_refs, int n_refs, int frame, const sdfgi_cfg* cfg,
+                             sdfgi_ray_record* out, int n_records_max, int* n_written) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        requireProbes(c);
+        validateCfg(c, cfg);
+        REQ(probe_refs && n_refs > 0 && out && n_written, SDFGI_ERR_INVALID, "bad debug arguments");
+        std::vector<int> g;
+        for (int i = 0; i < n_refs; ++i) {
+            int s = c->slot(probe_refs[2 * i]);
+            REQ(probe_refs[2 * i + 1] >= 0 && probe_refs[2 * i + 1] < c->cascades[s].count(), SDFGI_ERR_INVALID,
+                "probe index out of range");
+            g.push_back(c->cascades[s].base + probe_refs[2 * i + 1]);
+        }
+        std::vector<int> rj(c->totalProbes);
+        CK(cudaMemcpyAsync(rj.data(), c->reject.p, rj.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        std::vector<int> off(n_refs);
+        int total = 0;
+        for (int i = 0; i < n_refs; ++i) {
+            off[i] = total;
+            total += rj[g[i]] ? 2 * static_cast<int>(cfg->n_rays_full) : static_cast<int>(cfg->n_rays_full);
+        }
+        REQ(total <= n_records_max, SDFGI_ERR_INVALID, "n_records_max too small");
+        c->refs.upload(g.data(), g.size(), c->stream);
+        c->recOffset.upload(off.data(), off.size(), c->stream);
+        c->records.alloc(total);
+        if (c->precision == SDFGI_F64) {
+            UpdateParams<double> p = updateParams<double>(c, cfg, frame);
+            p.refs = c->refs.p;
+            p.nRefs = n_refs;
+            p.records = c->records.p;
+            p.recordOffset = c->recOffset.p;
+            launch_trace_debug<double>(p, n_refs, c->stream);
+        } else {
+            UpdateParams<float> p = updateParams<float>(c, cfg, frame);
+            p.refs = c->refs.p;
+            p.nRefs = n_refs;
+            p.records = c->records.p;
+            p.recordOffset = c->recOffset.p;
+            launch_trace_debug<float>(p, n_refs, c->stream);
+        }
+        checkLaunch(c);
+        CK(cudaMemcpyAsync(out, c->records.p, total * sizeof(RayRecord), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        *n_written = total;
+    });
+}
+
+int sdfgi_query_points(void* ctx, const double* points_xyz, const double* init_d, int n, double* out_d,
+                       int32_t* out_owner) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(c->haveScene, SDFGI_ERR_STATE, "scene not uploaded");
+        REQ(n >= 0 && (n == 0 || (points_xyz && out_d && out_owner)), SDFGI_ERR_INVALID, "bad query arguments");
+        if (n == 0) return;
+        c->qpts.upload(points_xyz, 3 * static_cast<size_t>(n), c->stream);
+        if (init_d) c->qinit.upload(init_d, n, c->stream);
+        c->qd.alloc(n);
+        c->qowner.alloc(n);
+        QueryParams p;
+        p.scene = c->sceneView<double>();
+        p.pts = c->qpts.p;
+        p.init = init_d ? c->qinit.p : nullptr;
+        p.outD = c->qd.p;
+        p.outOwner = c->qowner.p;
+        p.n = n;
+        launch_query_points(p, c->stream);
+        checkLaunch(c);
+        CK(cudaMemcpyAsync(out_d, c->qd.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(out_owner, c->qowner.p, n * 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int sdfgi_launch_count(void* ctx, int64_t* out) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(out, SDFGI_ERR_INVALID, "null out");
+        *out = c->launches;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,256 @@
+"""ctypes binding of libsdfgi_b200.so (the C-ABI in include/sdfgi_b200.h).
+
+This is the Python-side view of the drop-in boundary. It never falls back to a
+CPU path: if the library is missing or no CUDA device exists, constructing a
+``Device`` raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import scene_io as sio
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libsdfgi_b200.so")
+
+F64, F32 = 0, 1
+_PREC = {"f64": F64, "f32": F32, F64: F64, F32: F32}
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_D = ctypes.c_double
+_SZ = ctypes.c_size_t
+
+# name -> argtypes (restype int unless noted)
+_SIGS = {
+    "sdfgi_abi_version": [],
+    "sdfgi_last_error": [],
+    "sdfgi_device_count": [_P],
+    "sdfgi_nccl_unique_id": [_P],
+    "sdfgi_ctx_create": [_I, _I, _I, _P, _I, _P],
+    "sdfgi_ctx_destroy": [_P],
+    "sdfgi_ctx_set_precision": [_P, _I],
+    "sdfgi_ctx_stream": [_P, _P],
+    "sdfgi_ctx_synchronize": [_P],
+    "sdfgi_scene_upload": [_P, _P, _I, _P, _I, _P, _P, _P, _I, _P],
+    "sdfgi_lights_upload": [_P, _P, _I, _P],
+    "sdfgi_cascade_set": [_P, _I, _I, _I, _I, _D, _P, _I],
+    "sdfgi_cascade_count": [_P, _P],
+    "sdfgi_probes_reset": [_P, _I],
+    "sdfgi_probes_upload": [_P, _I, _P, _I],
+    "sdfgi_probes_download": [_P, _I, _P, _I],
+    "sdfgi_probes_relocate": [_P, _I, _D, _D, _I, _D, _P, _P],
+    "sdfgi_probes_update": [_P, _P, _I, _I, _P, _P, _P],
+    "sdfgi_atlas_swap": [_P],
+    "sdfgi_atlas_download": [_P, _I, _I, _P, _SZ],
+    "sdfgi_atlas_upload": [_P, _I, _I, _P, _SZ],
+    "sdfgi_atlas_device_ptr": [_P, _I, _I, _P, _P],
+    "sdfgi_probes_trace_debug": [_P, _P, _I, _I, _P, _P, _I, _P],
+    "sdfgi_query_points": [_P, _P, _P, _I, _P, _P],
+    "sdfgi_launch_count": [_P, _P],
+}
+
+RELOC_DTYPE = np.dtype([("relocated", "<i4"), ("rejected", "<i4"), ("dead", "<i4"), ("_pad", "<i4")])
+RESULT_DTYPE = np.dtype([("max_texel_delta", "<f8"), ("rays_traced", "<i8"), ("probes_updated", "<i8")])
+
+_lib = None
+
+
+class SdfgiError(RuntimeError):
+    def __init__(self, fn, code, msg):
+        super().__init__(f"{fn} failed ({code}): {msg}")
+        self.code = code
+
+
+def load_library(path: str = LIB_PATH):
+    """Load the CUDA library (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"{path} is missing: build it with `python -m paper_2007_14394_b200.build` "
+            "(the B200 path has no CPU fallback)"
+        )
+    lib = ctypes.CDLL(path)
+    for name, args in _SIGS.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = ctypes.c_char_p if name == "sdfgi_last_error" else ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _call(name, *args):
+    lib = load_library()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        raise SdfgiError(name, rc, lib.sdfgi_last_error().decode())
+    return rc
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    _call("sdfgi_device_count", ctypes.byref(n))
+    return n.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _call("sdfgi_nccl_unique_id", buf)
+    return bytes(buf)
+
+
+class Device:
+    """One context on one GPU (one rank of a slab-sharded job when world > 1)."""
+
+    def __init__(self, device=0, rank=0, world=1, nccl_uid: bytes | None = None, precision="f64"):
+        self._ctx = ctypes.c_void_p()
+        uid = None
+        if nccl_uid is not None:
+            uid = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_uid)
+        _call("sdfgi_ctx_create", device, rank, world, uid, _PREC[precision], ctypes.byref(self._ctx))
+        self.rank, self.world, self.device = rank, world, device
+        self.levels = {}  # level -> (res, spacing, origin)
+        self.oct_res = 8
+
+    def close(self):
+        if self._ctx:
+            load_library().sdfgi_ctx_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ------------------------------------------------------------- context
+    def set_precision(self, precision):
+        _call("sdfgi_ctx_set_precision", self._ctx, _PREC[precision])
+
+    @property
+    def stream(self) -> int:
+        s = ctypes.c_void_p()
+        _call("sdfgi_ctx_stream", self._ctx, ctypes.byref(s))
+        return s.value or 0
+
+    def synchronize(self):
+        _call("sdfgi_ctx_synchronize", self._ctx)
+
+    def launch_count(self) -> int:
+        n = ctypes.c_int64()
+        _call("sdfgi_launch_count", self._ctx, ctypes.byref(n))
+        return n.value
+
+    # --------------------------------------------------------------- scene
+    def upload_scene(self, s: sio.Scene):
+        prims = np.ascontiguousarray(s.prims, sio.PRIM_DTYPE)
+        clusters = np.ascontiguousarray(s.clusters, sio.CLUSTER_DTYPE)
+        ms = np.ascontiguousarray(s.member_start, np.int32)
+        mi = np.ascontiguousarray(s.member_idx, np.int32)
+        lights = np.ascontiguousarray(s.lights, sio.LIGHT_DTYPE)
+        sky = np.ascontiguousarray(s.sky, np.float64)
+        _call("sdfgi_scene_upload", self._ctx, _ptr(prims), len(prims), _ptr(clusters), len(clusters),
+              _ptr(ms), _ptr(mi), _ptr(lights), len(lights), _ptr(sky))
+
+    def upload_lights(self, lights, sky):
+        lights = np.ascontiguousarray(lights, sio.LIGHT_DTYPE)
+        sky = np.ascontiguousarray(sky, np.float64)
+        _call("sdfgi_lights_upload", self._ctx, _ptr(lights), len(lights), _ptr(sky))
+
+    # -------------------------------------------------------------- probes
+    def set_cascade(self, level, res, spacing, origin, oct_res=8):
+        o = np.ascontiguousarray(origin, np.float64)
+        _call("sdfgi_cascade_set", self._ctx, level, int(res[0]), int(res[1]), int(res[2]), float(spacing),
+              _ptr(o), oct_res)
+        self.levels[level] = (tuple(int(r) for r in res), float(spacing), o.copy())
+        self.oct_res = oct_res
+
+    def probe_count(self, level) -> int:
+        r = self.levels[level][0]
+        return r[0] * r[1] * r[2]
+
+    def reset_probes(self, level):
+        _call("sdfgi_probes_reset", self._ctx, level)
+
+    def probes(self, level) -> np.ndarray:
+        out = np.zeros(self.probe_count(level), sio.PROBE_DTYPE)
+        _call("sdfgi_probes_download", self._ctx, level, _ptr(out), len(out))
+        return out
+
+    def upload_probes(self, level, probes):
+        p = np.ascontiguousarray(probes, sio.PROBE_DTYPE)
+        _call("sdfgi_probes_upload", self._ctx, level, _ptr(p), len(p))
+
+    def relocate(self, level, th1, th2, max_steps=16, grad_step=1e-3, stats=False):
+        rep = np.zeros(1, RELOC_DTYPE)
+        st = np.zeros(1, sio.STATS_DTYPE) if stats else None
+        _call("sdfgi_probes_relocate", self._ctx, level, float(th1), float(th2), int(max_steps),
+              float(grad_step), _ptr(rep), _ptr(st))
+        return (rep[0], st[0]) if stats else rep[0]
+
+    def update(self, frame, cfg, refs=None, stats=False):
+        """refs: None (all probes) or an int array of (level, index) pairs."""
+        cfg = np.ascontiguousarray(cfg, sio.CFG_DTYPE)
+        res = np.zeros(1, RESULT_DTYPE)
+        st = np.zeros(1, sio.STATS_DTYPE) if stats else None
+        r = None if refs is None else np.ascontiguousarray(refs, np.int32).reshape(-1, 2)
+        _call("sdfgi_probes_update", self._ctx, _ptr(r), 0 if r is None else len(r), int(frame), _ptr(cfg),
+              _ptr(res), _ptr(st))
+        return (res[0], st[0]) if stats else res[0]
+
+    def swap(self):
+        _call("sdfgi_atlas_swap", self._ctx)
+
+    def atlas(self, level, which=0) -> np.ndarray:
+        """which 0 = front (read) atlas, 1 = back (write). Shape [P, R+2, R+2, 3]."""
+        t = self.oct_res + 2
+        out = np.zeros((self.probe_count(level), t, t, 3), np.float32)
+        _call("sdfgi_atlas_download", self._ctx, level, which, _ptr(out), out.size)
+        return out
+
+    def upload_atlas(self, level, data, which=0):
+        a = np.ascontiguousarray(data, np.float32)
+        _call("sdfgi_atlas_upload", self._ctx, level, which, _ptr(a), a.size)
+
+    def atlas_device_ptr(self, level, which=0):
+        p = ctypes.c_void_p()
+        n = ctypes.c_size_t()
+        _call("sdfgi_atlas_device_ptr", self._ctx, level, which, ctypes.byref(p), ctypes.byref(n))
+        return p.value, n.value
+
+    def trace_debug(self, frame, cfg, refs):
+        cfg = np.ascontiguousarray(cfg, sio.CFG_DTYPE)
+        r = np.ascontiguousarray(refs, np.int32).reshape(-1, 2)
+        cap = len(r) * 2 * int(cfg["n_rays_full"][0])
+        out = np.zeros(cap, sio.RAY_DTYPE)
+        n = ctypes.c_int()
+        _call("sdfgi_probes_trace_debug", self._ctx, _ptr(r), len(r), int(frame), _ptr(cfg), _ptr(out), cap,
+              ctypes.byref(n))
+        return out[: n.value]
+
+    def query_points(self, pts, init=None):
+        pts = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)
+        ini = None if init is None else np.ascontiguousarray(init, np.float64)
+        d = np.zeros(len(pts))
+        o = np.zeros(len(pts), np.int32)
+        _call("sdfgi_query_points", self._ctx, _ptr(pts), _ptr(ini), len(pts), _ptr(d), _ptr(o))
+        return d, o

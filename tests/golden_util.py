@@ -1,0 +1,50 @@
+"""Helpers to load the committed golden fixtures (tests/golden/<case>/)."""
+import json
+import os
+
+import numpy as np
+
+from paper_2007_14394_b200 import scene_io
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+CASES = sorted(d for d in os.listdir(GOLDEN) if os.path.isdir(os.path.join(GOLDEN, d)))
+
+
+class Case:
+    def __init__(self, name):
+        d = os.path.join(GOLDEN, name)
+        self.name = name
+        self.scene = scene_io.read_sdfs(os.path.join(d, "scene.sdfs"))
+        with open(os.path.join(d, "summary.json")) as f:
+            self.summary = json.load(f)
+        with np.load(os.path.join(d, "data.npz")) as z:
+            self.data = {k: z[k] for k in z.files}
+        self.passes = self.summary["reps"][0]
+        self.debug = self.summary["debug_probes"]
+        args = self.summary["args"]
+        self.res = None
+        self.spacing = None
+        self.n_rays = None
+        i = 0
+        while i < len(args):
+            a = args[i]
+            if a == "--res":
+                self.res = tuple(int(x) for x in args[i + 1:i + 4])
+                i += 4
+                continue
+            if a == "--spacing":
+                self.spacing = float(args[i + 1])
+            elif a == "--nrays":
+                self.n_rays = int(args[i + 1])
+            i += 2 if a in ("--spacing", "--nrays", "--passes", "--threads", "--debug-probe") else 1
+        self.levels = self.scene.cascade.levels
+
+    def cfg(self):
+        c = self.scene.cfg.copy()
+        if self.n_rays is not None:
+            c["n_rays_full"] = self.n_rays
+        return c
+
+
+def load(name):
+    return Case(name)

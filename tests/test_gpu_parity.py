@@ -1,0 +1,121 @@
+"""GPU parity: the CUDA probe stage vs the reference's own outputs (golden fixtures).
+
+Every case replays the reference run recorded in tests/golden/<case>/ (see
+oracle/gen_golden.py): same SDFS scene, same cascade, same config, frames 0..P-1.
+
+Bars (BASELINE.json north_star):
+  * relocation offsets and probe states: bit-exact (FP64 mode)
+  * ray-direction indexing: the probe key / Fibonacci index reproduce the
+    reference's directions to 1e-14 (libdevice vs glibc sin/cos ulps)
+  * irradiance texels: within 1e-3 relative (floor: 5% of the atlas mean, as
+    runCompare, tools/main.cpp:360-363); in FP64 mode the measured max is ~1e-7.
+"""
+import numpy as np
+import pytest
+
+from golden_util import CASES, load
+from paper_2007_14394_b200 import api, scene_io
+from paper_2007_14394_b200.runtime import Device
+
+pytestmark = pytest.mark.gpu
+
+TEXEL_RTOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def dev():
+    d = Device(0, precision="f64")
+    yield d
+    d.close()
+
+
+def texel_rel_err(got, want):
+    floor = 0.05 * max(float(np.mean(np.abs(want))), 1e-12)
+    return np.abs(got.astype(np.float64) - want) / np.maximum(np.abs(want), floor)
+
+
+def check_probes(got, want, where):
+    for f in ("resting", "pos", "last_pos"):
+        assert np.array_equal(got[f], want[f]), f"{where}: {f} not bit-exact " \
+            f"(max |d| {np.max(np.abs(got[f] - want[f]))})"
+    for f in ("alive", "reject_history", "last_update_frame"):
+        assert np.array_equal(got[f], want[f]), f"{where}: {f} differs at {np.nonzero(got[f] != want[f])[0][:10]}"
+
+
+def check_rays(got, want, where):
+    assert len(got) == len(want), where
+    assert np.max(np.abs(got["dir"] - want["dir"])) < 1e-14, where
+    # hit/miss decisions and owners: reference semantics, bit-equal decisions expected
+    assert np.array_equal(got["converged"], want["converged"]), where
+    assert np.array_equal(got["miss"], want["miss"]), where
+    hit = want["converged"] == 1
+    assert np.array_equal(got["prim_index"][hit], want["prim_index"][hit]), where
+    assert np.allclose(got["t"][hit], want["t"][hit], rtol=1e-9, atol=1e-12), where
+    assert np.allclose(got["normal"][hit], want["normal"][hit], rtol=1e-7, atol=1e-9), where
+    assert np.allclose(got["radiance"], want["radiance"], rtol=1e-7, atol=1e-10), where
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_probe_stage_matches_reference(dev, name):
+    case = load(name)
+    stage = api.ProbeStage(dev, case.scene, cfg=case.cfg(), res=case.res, spacing=case.spacing)
+    cfg = stage.cfg
+    for p, want in enumerate(case.passes):
+        reps = stage.relocate_all(stats=True)
+        relocated = sum(int(r[0]["relocated"]) for r in reps)
+        rejected = sum(int(r[0]["rejected"]) for r in reps)
+        dead = sum(int(r[0]["dead"]) for r in reps)
+        assert (relocated, rejected, dead) == (want["relocated"], want["rejected"], want["dead"]), f"pass {p}"
+        # TraceStats of relocation are exact (same query sequence, scalar cull path)
+        for k in ("sdf_queries", "clusters_visited", "clusters_skipped", "primitive_evals"):
+            assert sum(int(r[1][k]) for r in reps) == want["reloc_stats"][k], (p, k)
+        rays_key = f"rays_p{p}"
+        if rays_key in case.data:
+            refs = np.array([[0, i] for i in case.debug], np.int32)
+            got = dev.trace_debug(p, cfg, refs)
+            check_rays(got, case.data[rays_key], f"{name} pass {p} rays")
+        res, st = api.updateProbes(dev, cfg, p, None, stats=True)
+        dev.swap()
+        assert int(res["rays_traced"]) == want["rays_traced"], f"pass {p}"
+        assert int(res["probes_updated"]) == want["probes_updated"], f"pass {p}"
+        assert abs(float(res["max_texel_delta"]) - want["max_texel_delta"]) <= 1e-5 * max(1.0, want["max_texel_delta"])
+        for k in ("sdf_queries", "trace_steps", "sphere_traces", "shadow_traces", "primitive_evals"):
+            w = want["update_stats"][k]
+            assert abs(int(st[k]) - w) <= max(2, 1e-4 * w), (p, k, int(st[k]), w)
+        for level in range(stage.levels):
+            check_probes(dev.probes(level), case.data[f"probes_p{p}_c{level}"], f"{name} pass {p} cascade {level}")
+            got = dev.atlas(level, 0)
+            wa = case.data[f"atlas_p{p}_c{level}"]
+            err = texel_rel_err(got, wa)
+            assert err.max() <= TEXEL_RTOL, f"{name} pass {p} cascade {level}: max rel err {err.max():.3e}"
+
+
+def test_query_points_match_reference_relocation_scene(dev):
+    """querySceneSdf: culled query == naive minimum; owner = first minimiser (scene.hpp:205-211)."""
+    case = load("kinds")
+    dev.upload_scene(case.scene)
+    rng = np.random.default_rng(3)
+    pts = rng.uniform([-4, -1, -4], [4, 4, 4], size=(4096, 3))
+    d, owner = dev.query_points(pts)
+    # naive minimum in numpy FP64 is not bit-identical to the reference's operation
+    # order; the bit-exact check against the C oracle lives in test_oracle_gpu.py
+    assert np.all(owner >= 0)
+    init = np.abs(d) * 0.5
+    d2, o2 = dev.query_points(pts, init)
+    assert np.all(d2 <= init) and np.all(d2 <= d)
+    assert np.array_equal(d2, np.minimum(d, init))
+
+
+def test_f32_mode_within_tolerance(dev):
+    """FP32 perf mode on C1: texels within the north-star 1e-3 relative bar on
+    nearly all texels (hit/miss flips are reported, not hidden)."""
+    case = load("c1")
+    dev.set_precision("f32")
+    try:
+        stage = api.ProbeStage(dev, case.scene, cfg=case.cfg(), res=case.res, spacing=case.spacing)
+        stage.run_pass(0)
+        err = texel_rel_err(dev.atlas(0, 0), case.data["atlas_p0_c0"])
+        frac_bad = float(np.mean(err > TEXEL_RTOL))
+        assert frac_bad < 1e-3, f"{frac_bad:.2e} of channels exceed 1e-3 (max {err.max():.2e})"
+    finally:
+        dev.set_precision("f64")
