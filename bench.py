@@ -1,0 +1,419 @@
+#!/usr/bin/env python3
+"""Benchmark: SDFDDGI per-frame probe update on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): the ~2k-primitive synthetic
+Sponza-scale scene (paper_2007_14394_b200/data/c2.sdfs, clusters built by the
+reference's buildClusters), a 32x16x32 probe volume at spacing 0.45, 256 rays per
+probe, 3 bounces. One step = a fresh probe volume taken through 3 passes
+(frames 0, 1, 2), each pass = relocation (d) + the batched probe update (a,b,c)
+reading the previous pass's atlas + the atlas swap. Pass 0 traces 2N rays per
+probe (fresh probes reject history, probe_update.hpp:173).
+
+  value        Grays/s = probe rays (sum of raysTraced) / device time of the step,
+               inputs resident in HBM, CUDA events on the context's stream, L2
+               flushed (256 MB write) before every timed step, max over ranks.
+  e2e          same metric through the public API with host buffers: scene upload,
+               fresh-probe upload from pinned host memory, 3 passes, atlas download
+               into pinned host memory, all inside the timed region (wall clock).
+  roofline     dominant kernel k_probe_update: algorithmic FP instructions
+               (workmodel.py x the kernel's own counters) / its event-timed
+               duration, against the FMA-pipe rate measured live on this GPU.
+  cpu_baseline the reference itself (oracle/_ref, compiled from /root/reference)
+               on the host's cores over a bounded sample of the same workload.
+
+--impl reference runs only the CPU reference arm (rank 0), on the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import re
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_2007_14394_b200 import scene_io, workmodel  # noqa: E402
+
+C2_PATH = os.path.join(ROOT, "paper_2007_14394_b200", "data", "c2.sdfs")
+PASSES = 3
+METRIC = "probe-update Grays/s & ms/frame (32x16x32 probes, 256 rays)"
+UNIT = "Grays/s"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+# ------------------------------------------------------------------ CPU reference
+def ref_binary():
+    """The reference compiled from /root/reference by oracle/Makefile (travels in-tree)."""
+    try:
+        flags = open("/proc/cpuinfo").read()
+    except OSError:
+        flags = ""
+    names = (["ref_perf_v4"] if "avx512f" in flags else []) + ["ref_perf_v3"]
+    for n in names:
+        p = os.path.join(ROOT, "oracle", "_ref", n)
+        if os.path.exists(p):
+            return p
+    return None
+
+
+def cpu_reference_sample(stride, threads, reps=1):
+    """Run the reference probe stage (pipeline.hpp:108-151) for PASSES passes on every
+    `stride`-th probe. Returns per-rep (rays, seconds) with relocation time scaled to the
+    sampled fraction (relocation always runs on the whole volume)."""
+    exe = ref_binary()
+    if exe is None:
+        return None, "oracle/_ref not built"
+    cmd = [exe, "passes", C2_PATH, os.devnull, "--passes", str(PASSES), "--threads", str(threads),
+           "--stride", str(stride), "--reps", str(reps), "--no-dump"]
+    r = subprocess.run(cmd, capture_output=True, text=True, check=True)
+    out = json.loads(r.stdout)
+    res = []
+    for rep in out["reps"]:
+        rays = sum(p["rays_traced"] for p in rep)
+        secs = sum(p["update_ms"] + p["reloc_ms"] / stride for p in rep) / 1e3
+        res.append((rays, secs))
+    return res, os.path.basename(exe)
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2007_14394_b200 import api
+    from paper_2007_14394_b200.runtime import Device, nccl_unique_id
+
+    torch.cuda.set_device(local_rank)
+    uid = None
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    scene = scene_io.read_sdfs(C2_PATH)
+    dev = Device(local_rank, rank, world, uid, precision=args.precision)
+    stage = api.ProbeStage(dev, scene)
+    cfg = stage.cfg
+    ext = torch.cuda.ExternalStream(dev.stream)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def fresh_volume():
+        for level in range(stage.levels):
+            dev.reset_probes(level)
+
+    def one_step(stats=False):
+        rays, upd_ms, ops, work_all = 0, 0.0, 0, []
+        for p in range(PASSES):
+            reps = stage.relocate_all(stats=stats)
+            r = api.updateProbes(dev, cfg, p, None, stats=stats)
+            if stats:
+                res, st = r
+                work = dev.last_work()
+                ops += workmodel.update_ops(st, work, int(res["rays_traced"]))
+                work_all.append((dict(zip(st.dtype.names, map(int, st))), [int(w) for w in work]))
+            else:
+                res = r
+            upd_ms += dev.last_kernel_ms()[0]
+            rays += int(res["rays_traced"])
+            dev.swap()
+        return rays, upd_ms, ops, work_all
+
+    # algorithmic work of one step (untimed stats run: counters cost registers/atomics)
+    fresh_volume()
+    rays_stats, _, ops_step, work_all = one_step(stats=True)
+    for _ in range(args.warmup):
+        fresh_volume()
+        one_step()
+    torch.cuda.synchronize()
+    launches0 = dev.launch_count()
+    times, kern = [], []
+    rays_step = None
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            fresh_volume()
+            flush.fill_(1.0)  # L2 flush (256 MB > 126 MB L2) outside the timed window
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(ext)
+            rays, upd_ms, _, _ = one_step()
+            e1.record(ext)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+            kern.append(upd_ms)
+            rays_step = rays
+        barrier()
+        torch.cuda.synchronize()
+    launches = dev.launch_count() - launches0
+    total_ms = sum(times)
+    if dist is not None:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    value = rays_step * args.steps / (total_ms * 1e-3) / 1e9
+
+    # e2e through the public API with host buffers (pinned), copies inside the timed region
+    e2e_val, h2d, d2h = e2e_run(args, dev, stage, scene, barrier, dist, torch)
+
+    # roofline of the dominant kernel (k_probe_update): algorithmic ops / kernel time
+    f64_rate, f32_rate = dev.measure_fp_peak()
+    peak_rate = f64_rate if args.precision == "f64" else f32_rate
+    kern_ms = statistics.median(kern)
+    achieved = ops_step / (kern_ms * 1e-3)  # ops/s over the step's update launches
+    roofline = {
+        "bound": "fp64" if args.precision == "f64" else "fp32",
+        "kernel": "k_probe_update",
+        "achieved": achieved / 1e12,
+        "peak": peak_rate / 1e12,
+        "unit": "Tinstr/s",
+        "frac": achieved / peak_rate,
+        "traffic": None,
+        "peak_source": "measured live: sdfgi_measure_fp_peak FMA-instruction rate (MEASURED_PEAKS.json has no FP pipe entry)",
+        "work_per_step_instr": ops_step,
+        "update_kernel_ms_per_step": kern_ms,
+        "kernel_share_of_step": kern_ms / ms_step,
+    }
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": args.precision,
+        "data": "synthetic (deterministic C2 scene, SURVEY §8d; no network)",
+        "config": {
+            "workload": "C2: ~2k-primitive synthetic Sponza-scale SDF scene, 32x16x32 probes, 256 rays, 3 bounces, relocation each pass",
+            "primitives": int(len(scene.prims)),
+            "clusters": int(len(scene.clusters)),
+            "probes": 32 * 16 * 32,
+            "rays_per_probe": 256,
+            "bounces": PASSES,
+            "rays_per_step": rays_step,
+            "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+            "l2": "flushed (256 MB write) before every timed step",
+            "precision_mode": args.precision,
+        },
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "roofline": roofline,
+        "clocks": clk.summary(),
+        "algorithmic_counters_step": work_all,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(rays_step)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dev.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def e2e_run(args, dev, stage, scene, barrier, dist, torch):
+    from paper_2007_14394_b200 import api
+
+    # pinned host buffers for the inputs (fresh probes) and the result (atlas)
+    n = 32 * 16 * 32
+    t = dev.oct_res + 2
+    probes_pin = torch.empty(n * scene_io.PROBE_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True)
+    probes_host = probes_pin.numpy().view(scene_io.PROBE_DTYPE)
+    stage.reset()
+    probes_host[:] = dev.probes(0)  # the fresh volume (makeCascade state)
+    atlas_pin = torch.empty(n * t * t * 3, dtype=torch.float32, pin_memory=True)
+    atlas_host = atlas_pin.numpy().reshape(n, t, t, 3)
+    scene_bytes = (scene.prims.nbytes + scene.clusters.nbytes + scene.member_start.nbytes +
+                   scene.member_idx.nbytes + scene.lights.nbytes + 24)
+    h2d = int(scene_bytes + probes_host.nbytes)
+    d2h = int(atlas_host.nbytes)
+    steps = max(1, min(args.steps, 5))
+    total, rays = 0.0, 0
+    for i in range(steps + 1):
+        barrier()
+        t0 = time.perf_counter()
+        dev.upload_scene(scene)
+        dev.reset_probes(0)  # fresh volume: zero atlases (makeCascade)
+        dev.upload_probes(0, probes_host)
+        r = 0
+        for p in range(PASSES):
+            stage.relocate_all()
+            res = api.updateProbes(dev, stage.cfg, p)
+            r += int(res["rays_traced"])
+            dev.swap()
+        atlas_host[:] = dev.atlas(0, 0)
+        dt = time.perf_counter() - t0
+        if i > 0:  # first iteration is a warm-up
+            total += dt
+            rays = r
+    if dist is not None:
+        tt = torch.tensor([total], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total = float(tt.item())
+    return rays * steps / total / 1e9, h2d, d2h
+
+
+def cpu_baseline(rays_full_step):
+    threads = cpu_threads()
+    stride = int(os.environ.get("SDFGI_CPU_STRIDE", "8"))
+    res, kind = cpu_reference_sample(stride, threads)
+    if res is None:
+        return {"value": None, "unit": UNIT, "cores": threads, "kind": "reference", "sample": kind}
+    rays, secs = res[0]
+    return {
+        "value": rays / secs / 1e9,
+        "unit": UNIT,
+        "cores": threads,
+        "kind": "reference",
+        "binary": kind,
+        "sample": f"C2 scene, 3 passes, every {stride}th probe ({rays} rays, {secs:.2f} s; relocation time "
+                  f"scaled by 1/{stride}); full step = {rays_full_step} rays",
+    }
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    threads = cpu_threads()
+    stride = int(os.environ.get("SDFGI_CPU_STRIDE", "8"))
+    res, kind = cpu_reference_sample(stride, threads, reps=args.warmup + args.steps)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": kind}))
+        return
+    timed = res[args.warmup:]
+    rays = sum(r for r, _ in timed)
+    secs = sum(s for _, s in timed)
+    value = rays / secs / 1e9
+    sample = (f"C2 scene, 3 passes, every {stride}th probe per step ({timed[0][0]} rays/step), "
+              f"{threads} threads, relocation time scaled by 1/{stride}")
+    print(json.dumps({
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": secs / len(timed) * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (deterministic C2 scene)",
+        "config": {"workload": "C2 sample (reference CPU path, pipeline.hpp:108-151)", "stride": stride,
+                   "binary": kind},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -201,6 +201,8 @@ SDFGI_API int sdfgi_lights_upload(void* ctx, const sdfgi_light* lights, int n_li
 SDFGI_API int sdfgi_cascade_set(void* ctx, int level, int res_x, int res_y, int res_z, double spacing,
                       const double origin[3], int oct_res);
 SDFGI_API int sdfgi_cascade_count(void* ctx, int* out);
+/* Drop every cascade (probes and atlases); the next cascade_set starts a new volume. */
+SDFGI_API int sdfgi_cascades_clear(void* ctx);
 SDFGI_API int sdfgi_probes_reset(void* ctx, int level);
 SDFGI_API int sdfgi_probes_upload(void* ctx, int level, const sdfgi_probe* probes, int n);
 SDFGI_API int sdfgi_probes_download(void* ctx, int level, sdfgi_probe* probes, int n);
@@ -238,6 +240,20 @@ SDFGI_API int sdfgi_probes_trace_debug(void* ctx, const int32_t* probe_refs, int
  * owner[i] = primitive index or -1. init_d may be NULL (= +inf). Host arrays. */
 SDFGI_API int sdfgi_query_points(void* ctx, const double* points_xyz, const double* init_d, int n,
                        double* out_d, int32_t* out_owner);
+
+/* Device time (CUDA events on the context stream, bracketing only the kernel) of the
+ * most recent k_probe_update launch and of the most recent relocation launch, in ms. */
+SDFGI_API int sdfgi_last_kernel_ms(void* ctx, double* update_ms, double* relocate_ms);
+
+/* Primitive evaluations of the most recent stats-enabled relocate/update call, by
+ * PrimitiveKind (sphere, box, plane, cylinder, capsule) and [5] how many of them
+ * were rotated: with sdfgi_stats these define the algorithmic work. */
+SDFGI_API int sdfgi_last_work(void* ctx, uint64_t out[6]);
+
+/* FP pipe throughput microbenchmark on the context's device: FP64 and FP32 fused
+ * multiply-add instructions per second (the roofline denominators for the tracing
+ * kernels, which MEASURED_PEAKS.json does not carry). */
+SDFGI_API int sdfgi_measure_fp_peak(void* ctx, double* f64_fma_per_s, double* f32_fma_per_s);
 
 /* Launch counter: kernels this context has launched since creation. */
 SDFGI_API int sdfgi_launch_count(void* ctx, int64_t* out);

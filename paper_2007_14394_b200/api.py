@@ -80,6 +80,7 @@ class ProbeStage:
 
     def reset(self):
         oct_res = int(self.cfg["oct_res"][0])
+        self.dev.clear_cascades()
         for level in range(self.levels):
             makeCascade(self.dev, *self.res, self.spacing0, level, self.scene.camera.position, oct_res)
 

@@ -26,6 +26,7 @@ UNITS = {
     "kernels_f64.cu": ["-fmad=false"],
     "kernels_f32.cu": ["-fmad=true"],
     "sdfgi_abi.cu": [],
+    "fp_peak.cu": [],
 }
 HEADERS = ["sdf_device.cuh", "kernels.cuh", "kernels_impl.cuh"]
 

@@ -14,9 +14,10 @@ __device__ __forceinline__ int cascadeOf(const ProbeCommon& pc, int gp) {
 
 __device__ __forceinline__ void flushCounters(const Counters& c, unsigned long long* out) {
     // warp reduce then one atomic per warp per counter
-    unsigned long long v[8] = {c.q, c.cv, c.cs, c.pe, c.steps, c.sphere, c.shadow, c.vis};
+    unsigned long long v[14] = {c.q,     c.cv,    c.cs,    c.pe,    c.steps, c.sphere, c.shadow,
+                                c.vis,   c.ek[0], c.ek[1], c.ek[2], c.ek[3], c.ek[4],  c.ek[5]};
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 14; ++i) {
         unsigned long long x = v[i];
         for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
         if ((threadIdx.x & 31) == 0 && x) atomicAdd(out + i, x);

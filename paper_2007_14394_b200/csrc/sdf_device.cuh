@@ -109,9 +109,15 @@ template <typename R> struct SceneView {
 };
 
 // TraceStats (scene.hpp:16-36), per thread.
+// ek[0..4]: primitive evaluations by PrimitiveKind, ek[5]: of those, rotated ones
+// (the algorithmic-work accounting of SURVEY §8d weights evaluations by kind).
 struct Counters {
     unsigned long long q, cv, cs, pe, steps, sphere, shadow, vis;
-    __device__ void zero() { q = cv = cs = pe = steps = sphere = shadow = vis = 0; }
+    unsigned long long ek[6];
+    __device__ void zero() {
+        q = cv = cs = pe = steps = sphere = shadow = vis = 0;
+        for (int i = 0; i < 6; ++i) ek[i] = 0;
+    }
 };
 
 // ------------------------------------------------------------ primitives.hpp
@@ -191,6 +197,10 @@ __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int*
             c->pe += e - b;
         }
         for (int j = b; j < e; ++j) {
+            if (ST) {
+                ++c->ek[s.prims[j].kind];
+                c->ek[5] += s.prims[j].identity ? 0 : 1;
+            }
             R pd = evalPrim(s.prims[j], p);
             if (pd < d) {
                 d = pd;

@@ -26,6 +26,10 @@
 
 using namespace sdfgi_dev;
 
+namespace sdfgi_dev {
+double measure_fma_rate(bool f64, cudaStream_t st);
+}
+
 static_assert(sizeof(sdfgi_prim) == 184, "prim ABI");
 static_assert(sizeof(sdfgi_light) == 80, "light ABI");
 static_assert(sizeof(sdfgi_light) == sizeof(DLight), "light mirror");
@@ -107,6 +111,8 @@ struct CascadeHost {
 struct Ctx {
     int device = 0, rank = 0, world = 1, precision = SDFGI_F64;
     cudaStream_t stream = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // update start/end, relocate start/end
+    bool evUpdate = false, evReloc = false;
     ncclComm_t comm = nullptr;
     long long launches = 0;
     // scene
@@ -129,7 +135,10 @@ struct Ctx {
     DBuf<float> atlas[2];
     int front = 0;
     // scratch
-    DBuf<unsigned long long> scratch;  // [0..7] stats, [8] maxDelta bits, [9] rays, [10] updated
+    // [0..7] TraceStats, [8..13] evaluations by kind + rotated, [16] maxDelta bits,
+    // [17] rays, [18] probes updated
+    DBuf<unsigned long long> scratch;
+    unsigned long long lastWork[6] = {0, 0, 0, 0, 0, 0};
     DBuf<int> report;
     DBuf<int> refs;
     DBuf<int> recOffset;
@@ -145,6 +154,8 @@ struct Ctx {
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
         recOffset.free(); records.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
         if (comm) ncclCommDestroy(comm);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -305,10 +316,11 @@ void fillPrim(DPrim<R>& d, const sdfgi_prim& s) {
 }
 
 void readCounters(Ctx* c, sdfgi_stats* stats, unsigned long long* tail, int ntail) {
-    std::vector<unsigned long long> h(8 + ntail);
+    std::vector<unsigned long long> h(32);
     CK(cudaMemcpyAsync(h.data(), c->scratch.p, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (stats) {
+        for (int i = 0; i < 6; ++i) c->lastWork[i] = h[8 + i];
         stats->sdf_queries += h[0];
         stats->clusters_visited += h[1];
         stats->clusters_skipped += h[2];
@@ -318,7 +330,7 @@ void readCounters(Ctx* c, sdfgi_stats* stats, unsigned long long* tail, int ntai
         stats->shadow_traces += h[6];
         stats->visibility_traces += h[7];
     }
-    for (int i = 0; i < ntail; ++i) tail[i] = h[8 + i];
+    for (int i = 0; i < ntail; ++i) tail[i] = h[16 + i];
 }
 
 template <typename R>
@@ -344,9 +356,9 @@ UpdateParams<R> updateParams(Ctx* c, const sdfgi_cfg* cfg, int frame) {
     p.seed = cfg->seed;
     p.rotatePerFrame = static_cast<int>(cfg->rotate_per_frame);
     p.stats = c->scratch.p;
-    p.maxDeltaBits = c->scratch.p + 8;
-    p.rays = c->scratch.p + 9;
-    p.updated = reinterpret_cast<unsigned int*>(c->scratch.p + 10);
+    p.maxDeltaBits = c->scratch.p + 16;
+    p.rays = c->scratch.p + 17;
+    p.updated = reinterpret_cast<unsigned int*>(c->scratch.p + 18);
     return p;
 }
 
@@ -436,7 +448,8 @@ int sdfgi_ctx_create(int device, int rank, int world, const uint8_t* nccl_uid, i
         c->precision = precision;
         try {
             CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-            c->scratch.alloc(16);
+            for (auto& e : c->ev) CK(cudaEventCreate(&e));
+            c->scratch.alloc(32);
             c->report.alloc(4);
             if (world > 1) {
                 REQ(nccl_uid, SDFGI_ERR_INVALID, "world > 1 needs an NCCL unique id");
@@ -606,6 +619,15 @@ int sdfgi_cascade_count(void* ctx, int* out) {
     });
 }
 
+int sdfgi_cascades_clear(void* ctx) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        c->cascades.clear();
+        c->front = 0;
+        reallocProbes(c);
+    });
+}
+
 int sdfgi_probes_reset(void* ctx, int level) {
     return guard([&] {
         Ctx* c = C(ctx);
@@ -690,10 +712,13 @@ int sdfgi_probes_relocate(void* ctx, int level, double threshold1, double thresh
         p.report = c->report.p;
         p.stats = c->scratch.p;
         CK(cudaMemsetAsync(c->report.p, 0, 4 * sizeof(int), c->stream));
-        CK(cudaMemsetAsync(c->scratch.p, 0, 16 * 8, c->stream));
+        CK(cudaMemsetAsync(c->scratch.p, 0, 32 * 8, c->stream));
         // relocation is replicated on every rank (deterministic, bit-exact): no exchange
+        CK(cudaEventRecord(c->ev[2], c->stream));
         launch_relocate(p, c->cascades[s].count(), stats != nullptr, c->stream);
         checkLaunch(c);
+        CK(cudaEventRecord(c->ev[3], c->stream));
+        c->evReloc = true;
         int rep[4];
         CK(cudaMemcpyAsync(rep, c->report.p, sizeof(rep), cudaMemcpyDeviceToHost, c->stream));
         readCounters(c, stats, nullptr, 0);
@@ -717,12 +742,13 @@ int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_refs, int fr
         const float* frontp = c->atlas[c->front].p;
         // atlas_[write] = atlas_[read] (pipeline.hpp:131); updated tiles are overwritten
         CK(cudaMemcpyAsync(back, frontp, c->atlasFloats() * 4, cudaMemcpyDeviceToDevice, c->stream));
-        CK(cudaMemsetAsync(c->scratch.p, 0, 16 * 8, c->stream));
+        CK(cudaMemsetAsync(c->scratch.p, 0, 32 * 8, c->stream));
         const int maxRays = 2 * static_cast<int>(cfg->n_rays_full);
         const bool all = (probe_refs == nullptr && c->world == 1);
         if (!all) c->refs.upload(refs.data(), refs.size(), c->stream);
         const int nBlocks = static_cast<int>(refs.size());
         if (nBlocks > 0) {
+            CK(cudaEventRecord(c->ev[0], c->stream));
             if (c->precision == SDFGI_F64) {
                 UpdateParams<double> p = updateParams<double>(c, cfg, frame);
                 p.refs = all ? nullptr : c->refs.p;
@@ -735,6 +761,8 @@ int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_refs, int fr
                 launch_probe_update<float>(p, nBlocks, maxRays, stats != nullptr, c->stream);
             }
             checkLaunch(c);
+            CK(cudaEventRecord(c->ev[1], c->stream));
+            c->evUpdate = true;
         }
         if (c->world > 1) {
             // all-gather the back atlas slabs in place (one broadcast per rank-owned
@@ -750,9 +778,9 @@ int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_refs, int fr
                                      c->stream));
                 }
             NK(ncclGroupEnd());
-            NK(ncclAllReduce(c->scratch.p, c->scratch.p, 8, ncclUint64, ncclSum, c->comm, c->stream));
-            NK(ncclAllReduce(c->scratch.p + 8, c->scratch.p + 8, 1, ncclUint64, ncclMax, c->comm, c->stream));
-            NK(ncclAllReduce(c->scratch.p + 9, c->scratch.p + 9, 2, ncclUint64, ncclSum, c->comm, c->stream));
+            NK(ncclAllReduce(c->scratch.p, c->scratch.p, 14, ncclUint64, ncclSum, c->comm, c->stream));
+            NK(ncclAllReduce(c->scratch.p + 16, c->scratch.p + 16, 1, ncclUint64, ncclMax, c->comm, c->stream));
+            NK(ncclAllReduce(c->scratch.p + 17, c->scratch.p + 17, 2, ncclUint64, ncclSum, c->comm, c->stream));
         }
         unsigned long long tail[3];
         readCounters(c, stats, tail, 3);
@@ -906,6 +934,35 @@ int sdfgi_query_points(void* ctx, const double* points_xyz, const double* init_d
         CK(cudaMemcpyAsync(out_d, c->qd.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaMemcpyAsync(out_owner, c->qowner.p, n * 4, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int sdfgi_last_kernel_ms(void* ctx, double* update_ms, double* relocate_ms) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        CK(cudaStreamSynchronize(c->stream));
+        float a = 0.f, b = 0.f;
+        if (c->evUpdate) CK(cudaEventElapsedTime(&a, c->ev[0], c->ev[1]));
+        if (c->evReloc) CK(cudaEventElapsedTime(&b, c->ev[2], c->ev[3]));
+        if (update_ms) *update_ms = a;
+        if (relocate_ms) *relocate_ms = b;
+    });
+}
+
+int sdfgi_last_work(void* ctx, uint64_t out[6]) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(out, SDFGI_ERR_INVALID, "null out");
+        for (int i = 0; i < 6; ++i) out[i] = c->lastWork[i];
+    });
+}
+
+int sdfgi_measure_fp_peak(void* ctx, double* f64_fma_per_s, double* f32_fma_per_s) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        if (f64_fma_per_s) *f64_fma_per_s = measure_fma_rate(true, c->stream);
+        if (f32_fma_per_s) *f32_fma_per_s = measure_fma_rate(false, c->stream);
+        CK(cudaGetLastError());
     });
 }
 

@@ -39,6 +39,7 @@ _SIGS = {
     "sdfgi_lights_upload": [_P, _P, _I, _P],
     "sdfgi_cascade_set": [_P, _I, _I, _I, _I, _D, _P, _I],
     "sdfgi_cascade_count": [_P, _P],
+    "sdfgi_cascades_clear": [_P],
     "sdfgi_probes_reset": [_P, _I],
     "sdfgi_probes_upload": [_P, _I, _P, _I],
     "sdfgi_probes_download": [_P, _I, _P, _I],
@@ -50,6 +51,9 @@ _SIGS = {
     "sdfgi_atlas_device_ptr": [_P, _I, _I, _P, _P],
     "sdfgi_probes_trace_debug": [_P, _P, _I, _I, _P, _P, _I, _P],
     "sdfgi_query_points": [_P, _P, _P, _I, _P, _P],
+    "sdfgi_last_kernel_ms": [_P, _P, _P],
+    "sdfgi_last_work": [_P, _P],
+    "sdfgi_measure_fp_peak": [_P, _P, _P],
     "sdfgi_launch_count": [_P, _P],
 }
 
@@ -155,6 +159,25 @@ class Device:
     def synchronize(self):
         _call("sdfgi_ctx_synchronize", self._ctx)
 
+    def last_kernel_ms(self):
+        """(update kernel ms, relocation kernel ms) of the most recent launches."""
+        a, b = ctypes.c_double(), ctypes.c_double()
+        _call("sdfgi_last_kernel_ms", self._ctx, ctypes.byref(a), ctypes.byref(b))
+        return a.value, b.value
+
+    def last_work(self):
+        """Evaluations by kind (sphere, box, plane, cylinder, capsule, rotated) of the last
+        stats-enabled call."""
+        out = np.zeros(6, np.uint64)
+        _call("sdfgi_last_work", self._ctx, _ptr(out))
+        return out
+
+    def measure_fp_peak(self):
+        """(FP64 FMA/s, FP32 FMA/s) measured on this device."""
+        a, b = ctypes.c_double(), ctypes.c_double()
+        _call("sdfgi_measure_fp_peak", self._ctx, ctypes.byref(a), ctypes.byref(b))
+        return a.value, b.value
+
     def launch_count(self) -> int:
         n = ctypes.c_int64()
         _call("sdfgi_launch_count", self._ctx, ctypes.byref(n))
@@ -183,6 +206,10 @@ class Device:
               _ptr(o), oct_res)
         self.levels[level] = (tuple(int(r) for r in res), float(spacing), o.copy())
         self.oct_res = oct_res
+
+    def clear_cascades(self):
+        _call("sdfgi_cascades_clear", self._ctx)
+        self.levels = {}
 
     def probe_count(self, level) -> int:
         r = self.levels[level][0]
