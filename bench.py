@@ -283,6 +283,7 @@ def run_ours(args, rank, world, local_rank):
             "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
             "l2": "flushed (256 MB write) before every timed step",
             "precision_mode": args.precision,
+            "cluster_walk": dev.accel_info(),
         },
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,

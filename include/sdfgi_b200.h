@@ -255,6 +255,13 @@ SDFGI_API int sdfgi_last_work(void* ctx, uint64_t out[6]);
  * kernels, which MEASURED_PEAKS.json does not carry). */
 SDFGI_API int sdfgi_measure_fp_peak(void* ctx, double* f64_fma_per_s, double* f32_fma_per_s);
 
+/* Cluster-walk strategy of every SDF query: 0 = the reference's flat walk in cluster
+ * order (TraceStats identical to the reference), 1 = candidate-cluster grid (default;
+ * identical query values and owners, far fewer cluster tests). */
+SDFGI_API int sdfgi_set_accel(void* ctx, int mode);
+/* {mode, grid built, dim x, dim y, dim z, candidate list entries} */
+SDFGI_API int sdfgi_accel_info(void* ctx, int64_t out[6]);
+
 /* Launch counter: kernels this context has launched since creation. */
 SDFGI_API int sdfgi_launch_count(void* ctx, int64_t* out);
 

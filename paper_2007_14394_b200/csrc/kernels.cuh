@@ -74,12 +74,28 @@ struct QueryParams {
     int n;
 };
 
+// Candidate-grid build (see GridDev in sdf_device.cuh), FP64.
+struct GridBuildParams {
+    SceneView<double> scene;  // useGrid = 0: exact flat walk
+    double lo[3];
+    double h;
+    int dim[3];
+    double pad;     // cell boxes are padded by this much on every side
+    double margin;  // absolute slack on the bound
+    double* U;
+    int* counts;
+    const int* start;
+    int* list;
+};
+
 template <typename R>
 void launch_probe_update(const UpdateParams<R>& p, int nBlocks, int maxRays, bool stats, cudaStream_t st);
 template <typename R>
 void launch_trace_debug(const UpdateParams<R>& p, int nBlocks, cudaStream_t st);
 void launch_relocate(const RelocParams& p, int nProbes, bool stats, cudaStream_t st);
 void launch_query_points(const QueryParams& p, cudaStream_t st);
+void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st);
+void launch_grid_list(const GridBuildParams& p, int ncells, bool fill, cudaStream_t st);
 
 constexpr int kUpdateThreads = 128;
 

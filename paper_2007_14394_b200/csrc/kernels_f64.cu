@@ -16,6 +16,53 @@ __global__ void __launch_bounds__(128) k_query_points(QueryParams P) {
     P.outOwner[i] = owner >= 0 ? P.scene.orig[owner] : -1;
 }
 
+__global__ void __launch_bounds__(128) k_grid_bound(GridBuildParams P, int ncells) {
+    const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+    if (cell >= ncells) return;
+    const int ix = cell % P.dim[0], iy = (cell / P.dim[0]) % P.dim[1], iz = cell / (P.dim[0] * P.dim[1]);
+    V3<double> c = mk(P.lo[0] + (ix + 0.5) * P.h, P.lo[1] + (iy + 0.5) * P.h, P.lo[2] + (iz + 0.5) * P.h);
+    Counters cnt;
+    double f = query<double, false>(P.scene, c, INFINITY, nullptr, &cnt);
+    double half = 0.5 * sqrt(3.0) * (P.h + 2.0 * P.pad);
+    P.U[cell] = f + half * (1.0 + 1e-12) + P.margin;
+}
+
+__global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells, int fill) {
+    const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+    if (cell >= ncells) return;
+    const int ix = cell % P.dim[0], iy = (cell / P.dim[0]) % P.dim[1], iz = cell / (P.dim[0] * P.dim[1]);
+    const double lo[3] = {P.lo[0] + ix * P.h - P.pad, P.lo[1] + iy * P.h - P.pad, P.lo[2] + iz * P.h - P.pad};
+    const double hi[3] = {lo[0] + P.h + 2 * P.pad, lo[1] + P.h + 2 * P.pad, lo[2] + P.h + 2 * P.pad};
+    const double r = fmax(P.U[cell], 0.0) + P.margin;
+    const double r2 = isinf(r) ? INFINITY : r * r;
+    int n = 0;
+    int out = fill ? P.start[cell] : 0;
+    for (int k = 0; k < P.scene.n_clusters; ++k) {
+        const DCluster<double>& cl = P.scene.clusters[k];
+        bool cand = cl.unbounded != 0;
+        if (!cand) {
+            double g2 = 0;
+            for (int a = 0; a < 3; ++a) {
+                double g = fmax(fmax(cl.lo[a] - hi[a], lo[a] - cl.hi[a]), 0.0);
+                g2 += g * g;
+            }
+            cand = g2 <= r2;
+        }
+        if (cand) {
+            if (fill) P.list[out + n] = k;
+            ++n;
+        }
+    }
+    if (!fill) P.counts[cell] = n;
+}
+
+void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st) {
+    k_grid_bound<<<(ncells + 127) / 128, 128, 0, st>>>(p, ncells);
+}
+void launch_grid_list(const GridBuildParams& p, int ncells, bool fill, cudaStream_t st) {
+    k_grid_list<<<(ncells + 127) / 128, 128, 0, st>>>(p, ncells, fill ? 1 : 0);
+}
+
 void launch_relocate(const RelocParams& p, int nProbes, bool stats, cudaStream_t st) {
     const int blocks = (nProbes + 127) / 128;
     if (stats)

@@ -96,6 +96,23 @@ struct DLight {  // sdfgi_light, kept in double in both modes (tiny)
     double intensity[3];
 };
 
+// Candidate-cluster grid (exact acceleration of the cluster walk). For every cell
+// of a uniform grid over the bounded clusters, U = SDF(cell centre) + half the
+// (padded) cell diagonal bounds the scene SDF anywhere in the cell (1-Lipschitz),
+// so only clusters whose cull box lies within max(U, 0) of the cell can hold the
+// minimum — or tie with it — at any point of the cell. Lists keep ascending
+// cluster order, so the first-minimiser owner rule of queryCore is unchanged and
+// query values/owners are identical to the reference's flat walk. Points outside
+// the grid take the flat walk.
+struct GridDev {
+    double lo[3];
+    double invH;
+    int dim[3];
+    int _pad;
+    const int* __restrict__ start;  // ncells + 1
+    const int* __restrict__ list;
+};
+
 template <typename R> struct SceneView {
     const DPrim<R>* __restrict__ prims;        // CSR order
     const DCluster<R>* __restrict__ clusters;
@@ -106,6 +123,8 @@ template <typename R> struct SceneView {
     const DLight* __restrict__ lights;
     int n_prims, n_clusters, n_lights;
     double sky[3];
+    GridDev grid;
+    int useGrid;
 };
 
 // TraceStats (scene.hpp:16-36), per thread.
@@ -175,38 +194,64 @@ __device__ __forceinline__ V3<R> evalGradient(const DPrim<R>& pr, V3<R> p) {
 // primitive in cluster order attaining it (or -1). Clusters are walked in order
 // by every lane of the warp, so the per-cluster bounds and member records are
 // warp-uniform loads (L1 broadcast) and the kind switch is a uniform branch.
+// One cluster of queryCore's walk: skip test against the running minimum, then
+// the member evaluations (scene.hpp:228-248,294-304).
+template <typename R, bool ST>
+__device__ __forceinline__ void visitCluster(const SceneView<R>& s, int k, V3<R> p, R& d, int& own, Counters* c) {
+    const DCluster<R>& cl = s.clusters[k];
+    R dx = smax(smax(cl.lo[0] - p.x, p.x - cl.hi[0]), R(0));
+    R dy = smax(smax(cl.lo[1] - p.y, p.y - cl.hi[1]), R(0));
+    R dz = smax(smax(cl.lo[2] - p.z, p.z - cl.hi[2]), R(0));
+    R boxSq = dx * dx + dy * dy + dz * dz;
+    if (!cl.unbounded && (d > R(0) ? boxSq >= d * d : boxSq > R(0))) {
+        if (ST) ++c->cs;
+        return;
+    }
+    const int b = s.cstart[k], e = s.cstart[k + 1];
+    if (ST) {
+        ++c->cv;
+        c->pe += e - b;
+    }
+    for (int j = b; j < e; ++j) {
+        if (ST) {
+            ++c->ek[s.prims[j].kind];
+            c->ek[5] += s.prims[j].identity ? 0 : 1;
+        }
+        R pd = evalPrim(s.prims[j], p);
+        if (pd < d) {
+            d = pd;
+            own = j;
+        }
+    }
+}
+
+// queryCore (scene.hpp:214-332): exactly min(naive SDF, initD); owner = the first
+// primitive in cluster order attaining it (or -1). Inside the candidate grid a lane
+// walks its cell's ascending candidate list; elsewhere every cluster in order.
 template <typename R, bool ST>
 __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int* owner, Counters* c) {
     R d = initD;
     int own = -1;
     if (ST) ++c->q;
-    const int K = s.n_clusters;
-    for (int k = 0; k < K; ++k) {
-        const DCluster<R>& cl = s.clusters[k];
-        R dx = smax(smax(cl.lo[0] - p.x, p.x - cl.hi[0]), R(0));
-        R dy = smax(smax(cl.lo[1] - p.y, p.y - cl.hi[1]), R(0));
-        R dz = smax(smax(cl.lo[2] - p.z, p.z - cl.hi[2]), R(0));
-        R boxSq = dx * dx + dy * dy + dz * dz;
-        if (!cl.unbounded && (d > R(0) ? boxSq >= d * d : boxSq > R(0))) {
-            if (ST) ++c->cs;
-            continue;
+    bool done = false;
+    if (s.useGrid) {
+        const GridDev& g = s.grid;
+        R fx = (p.x - R(g.lo[0])) * R(g.invH);
+        R fy = (p.y - R(g.lo[1])) * R(g.invH);
+        R fz = (p.z - R(g.lo[2])) * R(g.invH);
+        if (fx >= R(0) && fy >= R(0) && fz >= R(0) && fx < R(g.dim[0]) && fy < R(g.dim[1]) && fz < R(g.dim[2])) {
+            int ix = min(static_cast<int>(fx), g.dim[0] - 1);
+            int iy = min(static_cast<int>(fy), g.dim[1] - 1);
+            int iz = min(static_cast<int>(fz), g.dim[2] - 1);
+            int cell = ix + g.dim[0] * (iy + g.dim[1] * iz);
+            const int b = g.start[cell], e = g.start[cell + 1];
+            for (int i = b; i < e; ++i) visitCluster<R, ST>(s, g.list[i], p, d, own, c);
+            done = true;
         }
-        const int b = s.cstart[k], e = s.cstart[k + 1];
-        if (ST) {
-            ++c->cv;
-            c->pe += e - b;
-        }
-        for (int j = b; j < e; ++j) {
-            if (ST) {
-                ++c->ek[s.prims[j].kind];
-                c->ek[5] += s.prims[j].identity ? 0 : 1;
-            }
-            R pd = evalPrim(s.prims[j], p);
-            if (pd < d) {
-                d = pd;
-                own = j;
-            }
-        }
+    }
+    if (!done) {
+        const int K = s.n_clusters;
+        for (int k = 0; k < K; ++k) visitCluster<R, ST>(s, k, p, d, own, c);
     }
     if (owner) *owner = own;
     return d;

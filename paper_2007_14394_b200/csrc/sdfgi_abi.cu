@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -126,6 +127,13 @@ struct Ctx {
     DBuf<int> cstart, orig;
     DBuf<double> albedo, emission;
     DBuf<DLight> lights;
+    // candidate-cluster grid (GridDev, sdf_device.cuh)
+    int accel = 1;
+    bool haveGrid = false;
+    GridDev grid{};
+    long long gridEntries = 0;
+    DBuf<int> gridStart, gridList, gridCounts;
+    DBuf<double> gridU;
     // probes
     std::vector<CascadeHost> cascades;
     int octRes = 8;
@@ -151,6 +159,7 @@ struct Ctx {
         if (stream) cudaStreamSynchronize(stream);
         prim64.free(); prim32.free(); cl64.free(); cl32.free(); cstart.free(); orig.free();
         albedo.free(); emission.free(); lights.free();
+        gridStart.free(); gridList.free(); gridCounts.free(); gridU.free();
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
         recOffset.free(); records.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
@@ -210,6 +219,8 @@ SceneView<double> Ctx::sceneView<double>() const {
     v.n_clusters = nClusters;
     v.n_lights = nLights;
     for (int k = 0; k < 3; ++k) v.sky[k] = sky[k];
+    v.grid = grid;
+    v.useGrid = (accel && haveGrid) ? 1 : 0;
     return v;
 }
 template <>
@@ -226,6 +237,8 @@ SceneView<float> Ctx::sceneView<float>() const {
     v.n_clusters = nClusters;
     v.n_lights = nLights;
     for (int k = 0; k < 3; ++k) v.sky[k] = sky[k];
+    v.grid = grid;
+    v.useGrid = (accel && haveGrid) ? 1 : 0;
     return v;
 }
 
@@ -313,6 +326,94 @@ void fillPrim(DPrim<R>& d, const sdfgi_prim& s) {
     d.kind = s.kind;
     // primitives.hpp:76: skip the rotation when the diagonal is exactly 1
     d.identity = (s.rot[0] == 1.0 && s.rot[4] == 1.0 && s.rot[8] == 1.0) ? 1 : 0;
+}
+
+// Build the candidate-cluster grid over the bounded clusters (exact; see GridDev).
+void buildGrid(Ctx* c, const sdfgi_cluster* clusters, int n) {
+    c->haveGrid = false;
+    c->gridEntries = 0;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    int bounded = 0;
+    for (int k = 0; k < n; ++k) {
+        if (clusters[k].unbounded) continue;
+        ++bounded;
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], clusters[k].lo[a]);
+            hi[a] = std::max(hi[a], clusters[k].hi[a]);
+        }
+    }
+    if (bounded == 0 || n < 2) return;
+    double ext[3], scale = 0;
+    for (int a = 0; a < 3; ++a) {
+        double e = hi[a] - lo[a];
+        double m = 0.02 * e + 1e-3;
+        lo[a] -= m;
+        hi[a] += m;
+        ext[a] = hi[a] - lo[a];
+        scale = std::max(scale, std::max(std::fabs(lo[a]), std::fabs(hi[a])));
+    }
+    const char* env = std::getenv("SDFGI_GRID_CELLS");
+    double target = env ? std::atof(env) : 262144.0;
+    if (target < 1) return;
+    double h = std::cbrt(ext[0] * ext[1] * ext[2] / target);
+    int dim[3];
+    for (int a = 0; a < 3; ++a) {
+        h = std::max(h, ext[a] / 1024.0);
+    }
+    long long ncells = 1;
+    for (int a = 0; a < 3; ++a) {
+        dim[a] = std::max(1, static_cast<int>(std::ceil(ext[a] / h)));
+        ncells *= dim[a];
+    }
+    REQ(ncells < (1LL << 26), SDFGI_ERR_INVALID, "candidate grid too large");
+    GridBuildParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.scene = c->sceneView<double>();
+    p.scene.useGrid = 0;  // the bound kernel uses the exact flat walk
+    for (int a = 0; a < 3; ++a) {
+        p.lo[a] = lo[a];
+        p.dim[a] = dim[a];
+    }
+    p.h = h;
+    // pad the cells for FP32 point->cell rounding; slack covers every rounding on the way
+    p.pad = 1e-4 * h + 4e-6 * scale;
+    p.margin = 1e-5 * (scale + 1.0);
+    c->gridU.alloc(ncells);
+    c->gridCounts.alloc(ncells);
+    c->gridStart.alloc(ncells + 1);
+    p.U = c->gridU.p;
+    p.counts = c->gridCounts.p;
+    launch_grid_bound(p, static_cast<int>(ncells), c->stream);
+    checkLaunch(c);
+    launch_grid_list(p, static_cast<int>(ncells), false, c->stream);
+    checkLaunch(c);
+    std::vector<int> counts(ncells);
+    CK(cudaMemcpyAsync(counts.data(), c->gridCounts.p, ncells * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<int> start(ncells + 1);
+    long long total = 0;
+    for (long long i = 0; i < ncells; ++i) {
+        start[i] = static_cast<int>(total);
+        total += counts[i];
+        REQ(total < (1LL << 30), SDFGI_ERR_INVALID, "candidate lists too large");
+    }
+    start[ncells] = static_cast<int>(total);
+    c->gridStart.upload(start.data(), start.size(), c->stream);
+    c->gridList.alloc(std::max<long long>(total, 1));
+    p.start = c->gridStart.p;
+    p.list = c->gridList.p;
+    launch_grid_list(p, static_cast<int>(ncells), true, c->stream);
+    checkLaunch(c);
+    CK(cudaStreamSynchronize(c->stream));
+    for (int a = 0; a < 3; ++a) {
+        c->grid.lo[a] = lo[a];
+        c->grid.dim[a] = dim[a];
+    }
+    c->grid.invH = 1.0 / h;
+    c->grid.start = c->gridStart.p;
+    c->grid.list = c->gridList.p;
+    c->gridEntries = total;
+    c->haveGrid = true;
 }
 
 void readCounters(Ctx* c, sdfgi_stats* stats, unsigned long long* tail, int ntail) {
@@ -564,6 +665,7 @@ int sdfgi_scene_upload(void* ctx, const sdfgi_prim* prims, int n_prims, const sd
         c->nLights = n_lights;
         for (int k = 0; k < 3; ++k) c->sky[k] = sky[k];
         c->haveScene = true;
+        buildGrid(c, clusters, n_clusters);
     });
 }
 
@@ -963,6 +1065,27 @@ int sdfgi_measure_fp_peak(void* ctx, double* f64_fma_per_s, double* f32_fma_per_
         if (f64_fma_per_s) *f64_fma_per_s = measure_fma_rate(true, c->stream);
         if (f32_fma_per_s) *f32_fma_per_s = measure_fma_rate(false, c->stream);
         CK(cudaGetLastError());
+    });
+}
+
+int sdfgi_set_accel(void* ctx, int mode) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(mode == 0 || mode == 1, SDFGI_ERR_INVALID, "accel mode must be 0 or 1");
+        c->accel = mode;
+    });
+}
+
+int sdfgi_accel_info(void* ctx, int64_t out[6]) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(out, SDFGI_ERR_INVALID, "null out");
+        out[0] = c->accel;
+        out[1] = c->haveGrid ? 1 : 0;
+        out[2] = c->grid.dim[0];
+        out[3] = c->grid.dim[1];
+        out[4] = c->grid.dim[2];
+        out[5] = c->gridEntries;
     });
 }
 

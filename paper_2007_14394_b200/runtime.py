@@ -54,6 +54,8 @@ _SIGS = {
     "sdfgi_last_kernel_ms": [_P, _P, _P],
     "sdfgi_last_work": [_P, _P],
     "sdfgi_measure_fp_peak": [_P, _P, _P],
+    "sdfgi_set_accel": [_P, _I],
+    "sdfgi_accel_info": [_P, _P],
     "sdfgi_launch_count": [_P, _P],
 }
 
@@ -177,6 +179,16 @@ class Device:
         a, b = ctypes.c_double(), ctypes.c_double()
         _call("sdfgi_measure_fp_peak", self._ctx, ctypes.byref(a), ctypes.byref(b))
         return a.value, b.value
+
+    def set_accel(self, mode: int):
+        """0: reference flat cluster walk (exact TraceStats); 1: candidate grid (default)."""
+        _call("sdfgi_set_accel", self._ctx, int(mode))
+
+    def accel_info(self):
+        out = np.zeros(6, np.int64)
+        _call("sdfgi_accel_info", self._ctx, _ptr(out))
+        return {"mode": int(out[0]), "grid": bool(out[1]), "dim": tuple(int(x) for x in out[2:5]),
+                "entries": int(out[5])}
 
     def launch_count(self) -> int:
         n = ctypes.c_int64()
