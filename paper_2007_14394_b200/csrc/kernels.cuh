@@ -1,15 +1,25 @@
 // kernels.cuh — the probe-stage kernels and their launch parameter blocks.
 //
-//   k_relocate       (d) updateProbePositions, probe_volume.hpp:99-143. One thread
-//                    per probe, always FP64 (bit-exact relocation in every mode).
-//   k_probe_update   (a)(b)(c) updateProbe, probe_update.hpp:166-211. One CTA per
-//                    probe: rays strided over the CTA's lanes (sphere trace ->
-//                    shadeHit), radiance samples in shared memory, one texel per
-//                    lane for the cosine convolution + hysteresis blend, octahedral
-//                    border fill in shared memory, the finished 1200-byte tile
-//                    stored with coalesced 16-byte stores.
-//   k_trace_debug    per-ray records of the same ray stage (parity tests).
-//   k_query_points   querySceneSdf at arbitrary points (parity tests).
+// Probe update (a)(b)(c) = updateProbe (probe_update.hpp:166-211) for a batch of
+// probes, as a wavefront of four kernels so that the expensive part — SDF
+// queries — runs with full SIMT lanes:
+//   k_ray_setup      K0: per selected probe its ray count (2N on history reject,
+//                    N, 0 when dead) and the per-probe rotation of sampleDirections
+//                    (sampling.hpp:23-31); block prefix sums give every ray an id.
+//   k_trace_primary  K1: persistent, self-refilling lanes. Every loop iteration is
+//                    one SDF query for every active lane, stepping a per-lane state
+//                    machine (march / polish) that reproduces sphereTrace
+//                    (scene.hpp:391-435) exactly; idle lanes fetch the next ray id
+//                    with one warp-aggregated atomic. Converged hits are compacted.
+//   k_trace_shadow   K2: same scheme over (hit x light) items: the penumbra march of
+//                    softShadowTrace (scene.hpp:459-476) set up as directIrradiance
+//                    (probe_update.hpp:97-132) does.
+//   k_shade_convolve K3: one CTA per probe: shadeHit (emission + shadowed direct +
+//                    bounce from the previous atlas through the 8-probe stencil),
+//                    radiance samples in shared memory, the cosine convolution of
+//                    every texel in the reference's summation order, hysteresis
+//                    blend, octahedral border fill, coalesced 16-byte tile stores.
+// Relocation (d): k_relocate, one thread per probe, FP64 in every mode.
 #pragma once
 
 #include "sdf_device.cuh"
@@ -30,30 +40,7 @@ struct RelocParams {
     int maxSteps;
     double gradStep;
     int* report;          // relocated, rejected, dead
-    unsigned long long* stats;  // 8 counters or null
-};
-
-template <typename R> struct UpdateParams {
-    SceneView<R> scene;
-    ProbeCommon pc;
-    const float* prevAtlas;   // front (read) atlas, all cascades concatenated
-    float* currAtlas;         // back (write) atlas
-    int oct;
-    const int* refs;          // global probe ids (cascade base + index); null = all
-    int nRefs;
-    int frame;
-    TraceCfg tc;
-    double hysteresis, alphaMin;
-    int nRaysFull;
-    uint64_t seed;
-    int rotatePerFrame;
-    unsigned long long* stats;       // 8 counters or null
-    unsigned long long* maxDeltaBits;
-    unsigned long long* rays;
-    unsigned int* updated;
-    // debug
-    struct RayRecord* records;
-    const int* recordOffset;
+    unsigned long long* stats;  // counters or null
 };
 
 // Mirror of sdfgi_ray_record (include/sdfgi_b200.h).
@@ -63,6 +50,48 @@ struct RayRecord {
     double radiance[3];
     double normal[3];
     int converged, miss, prim_index, steps;
+};
+
+// One primary-ray result (K1 -> K2, K3).
+template <typename R> struct __align__(16) HitRec {
+    R p[3];
+    R n[3];
+    R t;
+    int owner;   // CSR position or -1
+    int status;  // bit0 converged, bits1-2 MissReason, bits 8.. steps
+};
+
+template <typename R> struct WaveParams {
+    SceneView<R> scene;
+    ProbeCommon pc;
+    TraceCfg tc;
+    const float* prevAtlas;   // front (read) atlas, all cascades concatenated
+    float* currAtlas;         // back (write) atlas
+    int oct;
+    int frame;
+    double hysteresis, alphaMin;
+    int nRaysFull;
+    uint64_t seed;
+    int rotatePerFrame;
+    // batch
+    const int* cand;          // global probe ids of the batch (null: 0..nCand-1)
+    int nCand;
+    int* rayCount;            // per candidate (K0)
+    long long* rayStart;      // nCand + 1 exclusive prefix (K0 scan)
+    double* rot;              // 9 per candidate
+    const double* fib;        // sphericalFibonacci table: n=N (N xyz) then n=2N (2N xyz)
+    HitRec<R>* hits;          // per ray
+    int* hitList;             // compacted ray ids of converged hits with an owner
+    R* vis;                   // per (ray, light)
+    unsigned long long* ctr;  // [0] K1 ray cursor, [1] hit count, [2] K2 item cursor
+    // results
+    unsigned long long* stats;       // counters or null
+    unsigned long long* maxDeltaBits;
+    unsigned long long* rays;
+    unsigned int* updated;
+    // debug: per-ray records instead of atlas/state writes
+    RayRecord* records;
+    int debug;
 };
 
 struct QueryParams {
@@ -88,15 +117,19 @@ struct GridBuildParams {
     int* list;
 };
 
+// Launch the whole wavefront for one batch (K0..K3) on `st`. `persistBlocks` sizes
+// the persistent K1/K2 grids; `ev` (optional, 2 events) brackets K1..K3.
 template <typename R>
-void launch_probe_update(const UpdateParams<R>& p, int nBlocks, int maxRays, bool stats, cudaStream_t st);
-template <typename R>
-void launch_trace_debug(const UpdateParams<R>& p, int nBlocks, cudaStream_t st);
+void launch_wavefront(const WaveParams<R>& p, int persistBlocks, bool stats, cudaStream_t st,
+                      cudaEvent_t evStart, cudaEvent_t evEnd, long long* launches);
+void launch_fib_table(double* out, int n, cudaStream_t st);
 void launch_relocate(const RelocParams& p, int nProbes, bool stats, cudaStream_t st);
 void launch_query_points(const QueryParams& p, cudaStream_t st);
 void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st);
 void launch_grid_list(const GridBuildParams& p, int ncells, bool fill, cudaStream_t st);
 
-constexpr int kUpdateThreads = 128;
+constexpr int kWaveThreads = 128;   // K1/K2 persistent CTAs
+constexpr int kShadeThreads = 128;  // K3 CTA per probe
+constexpr int kScanThreads = 1024;  // K0 prefix sum
 
 }  // namespace sdfgi_dev

@@ -5,7 +5,7 @@
 
 namespace sdfgi_dev {
 
-template void launch_probe_update<float>(const UpdateParams<float>&, int, int, bool, cudaStream_t);
-template void launch_trace_debug<float>(const UpdateParams<float>&, int, cudaStream_t);
+template void launch_wavefront<float>(const WaveParams<float>&, int, bool, cudaStream_t, cudaEvent_t, cudaEvent_t,
+                                      long long*);
 
 }  // namespace sdfgi_dev

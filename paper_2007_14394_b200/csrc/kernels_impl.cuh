@@ -5,6 +5,8 @@
 
 namespace sdfgi_dev {
 
+constexpr unsigned kFull = 0xffffffffu;
+
 __device__ __forceinline__ int cascadeOf(const ProbeCommon& pc, int gp) {
     int ci = 0;
     for (int k = 1; k < pc.nCas; ++k)
@@ -13,15 +15,36 @@ __device__ __forceinline__ int cascadeOf(const ProbeCommon& pc, int gp) {
 }
 
 __device__ __forceinline__ void flushCounters(const Counters& c, unsigned long long* out) {
-    // warp reduce then one atomic per warp per counter
+    // warp reduce then one atomic per warp per counter (all 32 lanes must call)
     unsigned long long v[14] = {c.q,     c.cv,    c.cs,    c.pe,    c.steps, c.sphere, c.shadow,
                                 c.vis,   c.ek[0], c.ek[1], c.ek[2], c.ek[3], c.ek[4],  c.ek[5]};
 #pragma unroll
     for (int i = 0; i < 14; ++i) {
         unsigned long long x = v[i];
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
         if ((threadIdx.x & 31) == 0 && x) atomicAdd(out + i, x);
     }
+}
+
+// Warp-aggregated work fetch for persistent, self-refilling lanes: every idle,
+// not-yet-exhausted lane of the warp gets the next item id with one atomic.
+// Must be called by all 32 lanes. Returns true for lanes that got an item.
+__device__ __forceinline__ bool fetchItem(unsigned long long* cursor, unsigned long long total, bool active,
+                                          bool& exhausted, unsigned long long& item) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned need = __ballot_sync(kFull, !active && !exhausted);
+    if (need == 0) return false;
+    const int leader = __ffs(need) - 1;
+    unsigned long long base = 0;
+    if (static_cast<int>(lane) == leader) base = atomicAdd(cursor, static_cast<unsigned long long>(__popc(need)));
+    base = __shfl_sync(kFull, base, leader);
+    if (active || exhausted) return false;
+    item = base + __popc(need & ((1u << lane) - 1u));
+    if (item >= total) {
+        exhausted = true;
+        return false;
+    }
+    return true;
 }
 
 // ------------------------------------------------------------ (d) relocation
@@ -84,11 +107,10 @@ __global__ void __launch_bounds__(128) k_relocate(RelocParams P) {
             }
         }
     }
-    // block-aggregated report
     for (int o = 16; o > 0; o >>= 1) {
-        relocated += __shfl_xor_sync(0xffffffffu, relocated, o);
-        rejected += __shfl_xor_sync(0xffffffffu, rejected, o);
-        dead += __shfl_xor_sync(0xffffffffu, dead, o);
+        relocated += __shfl_xor_sync(kFull, relocated, o);
+        rejected += __shfl_xor_sync(kFull, rejected, o);
+        dead += __shfl_xor_sync(kFull, dead, o);
     }
     if ((threadIdx.x & 31) == 0) {
         if (relocated) atomicAdd(P.report + 0, relocated);
@@ -98,76 +120,436 @@ __global__ void __launch_bounds__(128) k_relocate(RelocParams P) {
     if (ST) flushCounters(cnt, P.stats);
 }
 
-// ---------------------------------------------------------- (a)(b)(c) update
+// ---------------------------------------------------------------- K0 setup
+// Ray count (probe_update.hpp:173; dead probes are skipped, pipeline.hpp:141) and the
+// sampleDirections rotation of every probe of the batch.
+template <typename R>
+__global__ void __launch_bounds__(128) k_ray_setup(WaveParams<R> P) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= P.nCand) return;
+    const int g = P.cand ? P.cand[s] : s;
+    const ProbesView& pv = P.pc.probes;
+    int n = 0;
+    if (pv.alive[g] || P.debug) {  // debug traces dead probes too (per-ray parity)
+        n = pv.reject[g] ? 2 * P.nRaysFull : P.nRaysFull;
+        const int ci = cascadeOf(P.pc, g);
+        probeRotation(P.seed, P.frame, P.rotatePerFrame != 0, probeKey(P.pc.cas[ci].level, g - P.pc.cas[ci].base),
+                      P.rot + 9 * static_cast<size_t>(s));
+    }
+    P.rayCount[s] = n;
+}
+
+// Exclusive prefix sum of the ray counts in one CTA (chunked per thread).
+template <typename R>
+__global__ void __launch_bounds__(kScanThreads) k_ray_scan(WaveParams<R> P) {
+    __shared__ long long warpSums[kScanThreads / 32];
+    const int n = P.nCand;
+    const int chunk = (n + kScanThreads - 1) / kScanThreads;
+    const int b = threadIdx.x * chunk, e = min(n, b + chunk);
+    long long local = 0;
+    for (int i = b; i < e; ++i) local += P.rayCount[i];
+    // block exclusive scan of `local`
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    long long x = local;
+    for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warpSums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        long long w = warpSums[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            long long y = __shfl_up_sync(kFull, w, o);
+            if (lane >= o) w += y;
+        }
+        warpSums[lane] = w;
+    }
+    __syncthreads();
+    long long run = x - local + (warp ? warpSums[warp - 1] : 0);
+    for (int i = b; i < e; ++i) {
+        P.rayStart[i] = run;
+        run += P.rayCount[i];
+    }
+    if (threadIdx.x == kScanThreads - 1) P.rayStart[n] = warpSums[31];
+}
+
+// sphericalFibonacci(i, n), sampling.hpp:11-17 — one table per ray count.
+static __global__ void k_fib_table(double* out, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double goldenAngle = kPi * (3.0 - sqrt(5.0));
+    double z = 1.0 - (2.0 * i + 1.0) / n;
+    double r = sqrt(smax(0.0, 1.0 - z * z));
+    double phi = goldenAngle * i;
+    out[3 * i] = r * cos(phi);
+    out[3 * i + 1] = r * sin(phi);
+    out[3 * i + 2] = z;
+}
+
+__device__ __forceinline__ int findCandidate(const long long* start, int n, long long rid) {
+    int lo = 0, hi = n;  // start[lo] <= rid < start[hi]
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (start[mid] <= rid)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// rot * sphericalFibonacci(i, n) (sampling.hpp:28, vec.hpp:106-110)
+template <typename R>
+__device__ __forceinline__ V3<double> rayDirection(const WaveParams<R>& P, int s, int i, int n) {
+    const double* m = P.rot + 9 * static_cast<size_t>(s);
+    const double* v = P.fib + (n == P.nRaysFull ? 0 : 3 * P.nRaysFull) + 3 * i;
+    return mk(m[0] * v[0] + m[1] * v[1] + m[2] * v[2], m[3] * v[0] + m[4] * v[1] + m[5] * v[2],
+              m[6] * v[0] + m[7] * v[1] + m[8] * v[2]);
+}
+
+// --------------------------------------------------------- K1 primary rays
+// sphereTrace (scene.hpp:391-435) as a per-lane state machine: state 0 marches
+// (query at 2*lastD), state 1 is the owner-resolving query at the converged point
+// (d + 1e-9), state 2 the polish loop (t += d, 2|d| + 1e-9, at most 8). Every
+// iteration is exactly one query for every active lane.
 template <typename R, bool ST>
-__device__ __forceinline__ V3<double> traceAndShade(const UpdateParams<R>& P, V3<double> origin, V3<double> dir,
-                                                    Counters* cnt, Hit<R>* hitOut) {
-    const TraceCfg& tc = P.tc;
-    V3<R> o = mk(R(origin.x), R(origin.y), R(origin.z));
-    V3<R> d = mk(R(dir.x), R(dir.y), R(dir.z));
-    Hit<R> hit = sphereTrace<R, ST>(P.scene, o, d, R(tc.rayTMax), R(tc.eps), tc.maxSteps, cnt, R(INFINITY));
-    if (hitOut) *hitOut = hit;
-    if (hit.converged)
-        return shadeHit<R, ST>(P.scene, hit, P.pc.cas, P.pc.nCas, P.pc.probes, P.prevAtlas, P.oct, tc, cnt);
-    return mk(P.scene.sky[0], P.scene.sky[1], P.scene.sky[2]);
+__global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P) {
+    const long long total = P.rayStart[P.nCand];
+    const R eps = R(P.tc.eps), tMax = R(P.tc.rayTMax);
+    const int maxSteps = P.tc.maxSteps;
+    Counters cnt;
+    cnt.zero();
+    bool active = false, exhausted = false;
+    unsigned long long rid = 0;
+    V3<R> o = mk(R(0), R(0), R(0)), dir = o;
+    R t = 0, lastD = 0, d = 0;
+    int step = 0, state = 0, pol = 0, owner = -1;
+    while (true) {
+        __syncwarp();
+        unsigned long long item;
+        if (fetchItem(P.ctr + 0, static_cast<unsigned long long>(total), active, exhausted, item)) {
+            rid = item;
+            const int s = findCandidate(P.rayStart, P.nCand, static_cast<long long>(rid));
+            const int i = static_cast<int>(static_cast<long long>(rid) - P.rayStart[s]);
+            const int n = static_cast<int>(P.rayStart[s + 1] - P.rayStart[s]);
+            const int g = P.cand ? P.cand[s] : s;
+            const double* pp = P.pc.probes.pos + 3 * static_cast<size_t>(g);
+            V3<double> dd = rayDirection(P, s, i, n);
+            o = mk(R(pp[0]), R(pp[1]), R(pp[2]));
+            dir = mk(R(dd.x), R(dd.y), R(dd.z));
+            t = R(0);
+            lastD = R(INFINITY) * R(0.5);
+            step = 0;
+            state = 0;
+            owner = -1;
+            active = true;
+            if (ST) ++cnt.sphere;
+            if (maxSteps <= 0) {  // loop never runs: StepLimit
+                HitRec<R> h;
+                h.p[0] = h.p[1] = h.p[2] = R(0);
+                h.n[0] = h.n[1] = R(0);
+                h.n[2] = R(1);
+                h.t = R(0);
+                h.owner = -1;
+                h.status = 2 << 1;
+                P.hits[rid] = h;
+                active = false;
+            }
+        }
+        if (!__any_sync(kFull, active)) {
+            if (__all_sync(kFull, exhausted)) break;
+            continue;
+        }
+        if (active) {
+            if (state == 2) t += d;
+            V3<R> p = o + dir * t;
+            R initD;
+            if (state == 0) {
+                if (ST) ++cnt.steps;
+                initD = R(2) * lastD;
+            } else if (state == 1) {
+                initD = polishPad(d);
+            } else {
+                initD = polishPad(R(2) * fabs(d));
+            }
+            int o2 = -1;
+            R nd = query<R, ST>(P.scene, p, initD, &o2, &cnt);
+            int done = 0;  // 1 converged, 2 TMax, 3 StepLimit
+            if (state == 0) {
+                if (nd < eps) {
+                    d = nd;
+                    state = 1;
+                } else if (nd >= tMax - t) {
+                    done = 2;
+                } else {
+                    t += nd;
+                    lastD = nd;
+                    if (++step >= maxSteps) done = 3;
+                }
+            } else {
+                d = nd;
+                if (state == 1) {
+                    owner = o2;
+                    pol = 0;
+                    state = 2;
+                } else {
+                    if (o2 >= 0) owner = o2;
+                    ++pol;
+                }
+                if (!(pol < 8 && fabs(d) > R(0.25) * eps)) done = 1;
+            }
+            if (done) {
+                HitRec<R> h;
+                h.owner = -1;
+                h.n[0] = h.n[1] = R(0);
+                h.n[2] = R(1);
+                if (done == 1) {
+                    h.p[0] = p.x;
+                    h.p[1] = p.y;
+                    h.p[2] = p.z;
+                    h.t = t;
+                    h.owner = owner;
+                    if (owner >= 0) {
+                        V3<R> nn = evalGradient(P.scene.prims[owner], p);
+                        h.n[0] = nn.x;
+                        h.n[1] = nn.y;
+                        h.n[2] = nn.z;
+                    }
+                    h.status = 1 | ((step + 1) << 8);
+                } else {
+                    h.p[0] = h.p[1] = h.p[2] = R(0);
+                    h.t = R(0);
+                    h.status = ((done == 2 ? 1 : 2) << 1) | ((done == 2 ? step + 1 : maxSteps) << 8);
+                }
+                P.hits[rid] = h;
+                active = false;
+            }
+            // compaction of converged hits with an owner (the only ones shadeHit lights)
+            const bool lit = done == 1 && owner >= 0;
+            const unsigned m = __ballot_sync(__activemask(), lit);
+            if (lit) {
+                const int leader = __ffs(m) - 1;
+                const unsigned lane = threadIdx.x & 31;
+                unsigned long long base = 0;
+                if (static_cast<int>(lane) == leader) base = atomicAdd(P.ctr + 1, static_cast<unsigned long long>(__popc(m)));
+                base = __shfl_sync(m, base, leader);
+                P.hitList[base + __popc(m & ((1u << lane) - 1u))] = static_cast<int>(rid);
+            }
+        }
+    }
+    if (ST) flushCounters(cnt, P.stats);
+}
+
+// ----------------------------------------------------------- K2 shadow rays
+// One (converged hit, light) item per lane: directIrradiance's setup
+// (probe_update.hpp:100-128) and the softShadowTrace march (scene.hpp:459-476),
+// one query per iteration. vis = 1 when the segment is too short to trace.
+template <typename R, bool ST>
+__global__ void __launch_bounds__(kWaveThreads) k_trace_shadow(WaveParams<R> P) {
+    const int L = P.scene.n_lights;
+    const unsigned long long total = P.ctr[1] * static_cast<unsigned long long>(L);
+    const R minStep = R(5e-4), inf = R(INFINITY), k = R(P.tc.shadowK);
+    const int maxSteps = P.tc.shadowSteps;
+    Counters cnt;
+    cnt.zero();
+    bool active = false, exhausted = false;
+    unsigned long long slot = 0;
+    V3<R> o = mk(R(0), R(0), R(0)), dir = o;
+    R t = 0, tEnd = 0, v = 0, lastD = 0;
+    int step = 0;
+    while (true) {
+        __syncwarp();
+        unsigned long long item;
+        if (fetchItem(P.ctr + 2, total, active, exhausted, item)) {
+            const int rid = P.hitList[item / L];
+            const int li = static_cast<int>(item % L);
+            slot = static_cast<unsigned long long>(rid) * L + li;
+            const HitRec<R>& h = P.hits[rid];
+            const V3<R> pos = mk(h.p[0], h.p[1], h.p[2]);
+            const V3<R> nrm = mk(h.n[0], h.n[1], h.n[2]);
+            const DLight& Lt = P.scene.lights[li];
+            bool skip = false;
+            R tMax = R(0);
+            if (Lt.kind == 0) {
+                V3<R> toLight = mk(R(Lt.position[0]), R(Lt.position[1]), R(Lt.position[2])) - pos;
+                R r2 = dot(toLight, toLight);
+                if (r2 < R(1e-12)) {
+                    skip = true;
+                } else {
+                    R r = sqrt(r2);
+                    dir = toLight / r;
+                    if (dot(nrm, dir) <= R(0)) skip = true;
+                    tMax = r;
+                }
+            } else if (Lt.kind == 1) {
+                dir = mk(R(-Lt.direction[0]), R(-Lt.direction[1]), R(-Lt.direction[2]));
+                if (dot(nrm, dir) <= R(0)) skip = true;
+                tMax = R(P.tc.rayTMax);
+            } else {
+                skip = true;
+            }
+            if (skip) {
+                P.vis[slot] = R(-1);
+            } else {
+                const R cosT = dot(nrm, dir);
+                const R bias = R(2.0) * R(P.tc.eps) / smax(R(0.1), cosT);
+                if (tMax - bias > bias) {
+                    if (ST) ++cnt.shadow;
+                    o = pos + nrm * bias;
+                    t = bias;
+                    tEnd = tMax - bias;
+                    v = R(1);
+                    lastD = inf;
+                    step = 0;
+                    active = true;
+                } else {
+                    P.vis[slot] = R(1);
+                }
+            }
+        }
+        if (!__any_sync(kFull, active)) {
+            if (__all_sync(kFull, exhausted)) break;
+            continue;
+        }
+        if (active) {
+            bool done = false;
+            if (!(step < maxSteps && t < tEnd)) {
+                done = true;
+            } else {
+                if (ST) ++cnt.steps;
+                R d = query<R, ST>(P.scene, o + dir * t, lastD == inf ? inf : R(2) * lastD, nullptr, &cnt);
+                v = smin(v, sclamp(k * d / t, R(0), R(1)));
+                if (v < R(1e-3)) {
+                    v = R(0);
+                    done = true;
+                } else {
+                    t += smax(d, minStep);
+                    lastD = smax(d, minStep);
+                    ++step;
+                }
+            }
+            if (done) {
+                P.vis[slot] = v;
+                active = false;
+            }
+        }
+    }
+    if (ST) flushCounters(cnt, P.stats);
+}
+
+// ------------------------------------------------- K3 shade + convolve + blend
+// shadeHit (probe_update.hpp:136-149) with directIrradiance's sum in light order
+// (visibility from K2), then convolveIrradiance + hysteresis blend + fillBorder
+// (probe_update.hpp:192-209, atlas.hpp:44-56) for one probe per CTA.
+template <typename R>
+__device__ __forceinline__ V3<double> shadeRay(const WaveParams<R>& P, const HitRec<R>& h, unsigned long long rid) {
+    const SceneView<R>& s = P.scene;
+    if (!(h.status & 1) || h.owner < 0) return mk(s.sky[0], s.sky[1], s.sky[2]);
+    const V3<R> pos = mk(h.p[0], h.p[1], h.p[2]);
+    const V3<R> nrm = mk(h.n[0], h.n[1], h.n[2]);
+    V3<double> total = mk(0.0, 0.0, 0.0);
+    for (int li = 0; li < s.n_lights; ++li) {
+        const DLight& L = s.lights[li];
+        V3<double> I = mk(L.intensity[0], L.intensity[1], L.intensity[2]);
+        V3<double> unshadowed;
+        if (L.kind == 0) {
+            V3<R> toLight = mk(R(L.position[0]), R(L.position[1]), R(L.position[2])) - pos;
+            R r2 = dot(toLight, toLight);
+            if (r2 < R(1e-12)) continue;
+            R r = sqrt(r2);
+            V3<R> dir = toLight / r;
+            R cosT = dot(nrm, dir);
+            if (cosT <= R(0)) continue;
+            unshadowed = I * static_cast<double>(cosT / r2);
+        } else if (L.kind == 1) {
+            V3<R> dir = mk(R(-L.direction[0]), R(-L.direction[1]), R(-L.direction[2]));
+            R cosT = dot(nrm, dir);
+            if (cosT <= R(0)) continue;
+            unshadowed = I * static_cast<double>(cosT);
+        } else {
+            continue;
+        }
+        const R vis = P.vis[rid * s.n_lights + li];
+        total = total + unshadowed * static_cast<double>(vis);
+    }
+    const double* A = s.albedo + 3 * h.owner;
+    const double* E = s.emission + 3 * h.owner;
+    V3<double> brdf = mk(A[0], A[1], A[2]) / kPi;
+    V3<double> radiance = mk(E[0], E[1], E[2]) + brdf * total;
+    if (P.tc.bounceCoeff > 0 && P.prevAtlas != nullptr) {
+        V3<double> prev;
+        V3<double> hp = mk<double>(h.p[0], h.p[1], h.p[2]);
+        V3<double> hn = mk<double>(h.n[0], h.n[1], h.n[2]);
+        if (sampleBounceIrradiance(P.pc.cas, P.pc.nCas, P.pc.probes, P.prevAtlas, P.oct, hp, hn, P.tc.mvcFrac, &prev))
+            radiance = radiance + brdf * (prev * P.tc.bounceCoeff);
+    }
+    return radiance;
 }
 
 template <typename R, bool ST>
-__global__ void __launch_bounds__(kUpdateThreads) k_probe_update(UpdateParams<R> P) {
+__global__ void __launch_bounds__(kShadeThreads) k_shade_convolve(WaveParams<R> P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ double rot[9];
     __shared__ __align__(16) float tile[12 * 12 * 3 + 4];
-    __shared__ unsigned long long redDelta[kUpdateThreads / 32];
+    __shared__ unsigned long long redDelta[kShadeThreads / 32];
 
-    const int gp = P.refs ? P.refs[blockIdx.x] : static_cast<int>(blockIdx.x);
+    const int s = blockIdx.x;
+    const int n = P.rayCount[s];
+    if (n == 0) return;  // dead probe: its back tile is the copied front tile
+    const int g = P.cand ? P.cand[s] : s;
     const ProbesView& pv = P.pc.probes;
-    if (!pv.alive[gp]) return;  // pipeline.hpp:141; its back tile is the copied front tile
-    const int ci = cascadeOf(P.pc, gp);
-    const int level = P.pc.cas[ci].level;
-    const int local = gp - P.pc.cas[ci].base;
-    const int reject = pv.reject[gp];
-    const int n = reject ? 2 * P.nRaysFull : P.nRaysFull;
-    const V3<double> origin = mk(pv.pos[3 * gp], pv.pos[3 * gp + 1], pv.pos[3 * gp + 2]);
+    const int reject = n != P.nRaysFull;  // 2N rays <=> rejectHistory at setup
+    const long long start = P.rayStart[s];
+    R* sdir = reinterpret_cast<R*>(smem_raw);  // 3n
+    R* srad = sdir + 3 * n;                    // 3n
 
-    R* sdir = reinterpret_cast<R*>(smem_raw);        // 3n
-    R* srad = sdir + 3 * n;                           // 3n
-
-    if (threadIdx.x == 0)
-        probeRotation(P.seed, P.frame, P.rotatePerFrame != 0, probeKey(level, local), rot);
-    __syncthreads();
-
-    Counters cnt;
-    cnt.zero();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        V3<double> dir = probeRayDir(rot, i, n);
-        V3<double> L = traceAndShade<R, ST>(P, origin, dir, &cnt, nullptr);
+        const unsigned long long rid = static_cast<unsigned long long>(start + i);
+        const HitRec<R> h = P.hits[rid];
+        V3<double> dir = rayDirection(P, s, i, n);
+        V3<double> L = shadeRay(P, h, rid);
         sdir[3 * i] = R(dir.x);
         sdir[3 * i + 1] = R(dir.y);
         sdir[3 * i + 2] = R(dir.z);
         srad[3 * i] = R(L.x);
         srad[3 * i + 1] = R(L.y);
         srad[3 * i + 2] = R(L.z);
+        if (P.debug) {
+            RayRecord r;
+            r.dir[0] = dir.x;
+            r.dir[1] = dir.y;
+            r.dir[2] = dir.z;
+            const bool conv = h.status & 1;
+            r.t = conv ? double(h.t) : 0.0;
+            r.radiance[0] = L.x;
+            r.radiance[1] = L.y;
+            r.radiance[2] = L.z;
+            r.normal[0] = h.n[0];
+            r.normal[1] = h.n[1];
+            r.normal[2] = h.n[2];
+            r.converged = conv ? 1 : 0;
+            r.miss = (h.status >> 1) & 3;
+            r.prim_index = h.owner >= 0 ? P.scene.orig[h.owner] : -1;
+            r.steps = h.status >> 8;
+            P.records[rid] = r;
+        }
     }
+    if (P.debug) return;
     __syncthreads();
 
-    // convolveIrradiance + hysteresis blend (probe_update.hpp:25-34,192-206)
     const int res = P.oct;
     const int T = res + 2;
-    const double alpha = reject ? 1.0
-                                : sclamp((1.0 - P.hysteresis) * n / P.nRaysFull, P.alphaMin, 1.0);
+    const double alpha = reject ? 1.0 : sclamp((1.0 - P.hysteresis) * n / P.nRaysFull, P.alphaMin, 1.0);
     const double scale = 4.0 * kPi / static_cast<double>(n);
-    const float* oldTile = P.prevAtlas + static_cast<size_t>(gp) * T * T * 3;
+    const float* oldTile = P.prevAtlas + static_cast<size_t>(g) * T * T * 3;
     double maxDelta = 0.0;
     for (int tx = threadIdx.x; tx < res * res; tx += blockDim.x) {
         const int y = tx / res, x = tx % res;
-        V3<R> D;
-        {
-            V3<double> dd = octDecode(V2<double>{(x + 0.5) / res, (y + 0.5) / res});
-            D = mk(R(dd.x), R(dd.y), R(dd.z));
-        }
+        V3<double> dd = octDecode(V2<double>{(x + 0.5) / res, (y + 0.5) / res});
+        const R Dx = R(dd.x), Dy = R(dd.y), Dz = R(dd.z);
         R ax = 0, ay = 0, az = 0;
         for (int i = 0; i < n; ++i) {
-            R w = D.x * sdir[3 * i] + D.y * sdir[3 * i + 1] + D.z * sdir[3 * i + 2];
+            R w = Dx * sdir[3 * i] + Dy * sdir[3 * i + 1] + Dz * sdir[3 * i + 2];
             if (w > R(0)) {
                 ax = ax + srad[3 * i] * w;
                 ay = ay + srad[3 * i + 1] * w;
@@ -180,14 +562,13 @@ __global__ void __launch_bounds__(kUpdateThreads) k_probe_update(UpdateParams<R>
         V3<double> bl = lerp(old, fresh, alpha);
         V3<double> df = bl - old;
         maxDelta = smax(maxDelta, maxComponent(mk(fabs(df.x), fabs(df.y), fabs(df.z))));
-        float* t = tile + ((y + 1) * T + (x + 1)) * 3;
-        t[0] = static_cast<float>(bl.x);
-        t[1] = static_cast<float>(bl.y);
-        t[2] = static_cast<float>(bl.z);
+        float* tp = tile + ((y + 1) * T + (x + 1)) * 3;
+        tp[0] = static_cast<float>(bl.x);
+        tp[1] = static_cast<float>(bl.y);
+        tp[2] = static_cast<float>(bl.z);
     }
     __syncthreads();
-    // fillBorder, atlas.hpp:44-56: edges copy the adjacent interior row/column
-    // reversed, corners the diagonally opposite interior corner.
+    // fillBorder, atlas.hpp:44-56
     for (int k = threadIdx.x; k < 4 * res + 4; k += blockDim.x) {
         int dx, dy, sx, sy;
         if (k < 4 * res) {
@@ -203,15 +584,14 @@ __global__ void __launch_bounds__(kUpdateThreads) k_probe_update(UpdateParams<R>
             else if (e == 2) { dx = 0; dy = res + 1; sx = res; sy = 1; }
             else { dx = res + 1; dy = res + 1; sx = 1; sy = 1; }
         }
-        const float* s = tile + (sy * T + sx) * 3;
-        float* d = tile + (dy * T + dx) * 3;
-        d[0] = s[0];
-        d[1] = s[1];
-        d[2] = s[2];
+        const float* sp = tile + (sy * T + sx) * 3;
+        float* dp = tile + (dy * T + dx) * 3;
+        dp[0] = sp[0];
+        dp[1] = sp[1];
+        dp[2] = sp[2];
     }
     __syncthreads();
-    // coalesced tile store: T*T*3 floats, 16-byte aligned when T*T*3 % 4 == 0
-    float* dst = P.currAtlas + static_cast<size_t>(gp) * T * T * 3;
+    float* dst = P.currAtlas + static_cast<size_t>(g) * T * T * 3;
     const int nf = T * T * 3;
     if ((nf & 3) == 0) {
         const float4* s4 = reinterpret_cast<const float4*>(tile);
@@ -220,80 +600,61 @@ __global__ void __launch_bounds__(kUpdateThreads) k_probe_update(UpdateParams<R>
     } else {
         for (int k = threadIdx.x; k < nf; k += blockDim.x) dst[k] = tile[k];
     }
-    // jitter metric and counters
     unsigned long long bits = __double_as_longlong(maxDelta);
     for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long other = __shfl_xor_sync(0xffffffffu, bits, o);
+        unsigned long long other = __shfl_xor_sync(kFull, bits, o);
         bits = other > bits ? other : bits;
     }
     if ((threadIdx.x & 31) == 0) redDelta[threadIdx.x >> 5] = bits;
-    if (ST) flushCounters(cnt, P.stats);
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long m = 0;
-        for (int w = 0; w < static_cast<int>(blockDim.x) / 32; ++w) m = redDelta[w] > m ? redDelta[w] : m;
+        for (int w = 0; w < kShadeThreads / 32; ++w) m = redDelta[w] > m ? redDelta[w] : m;
         atomicMax(P.maxDeltaBits, m);
         atomicAdd(P.rays, static_cast<unsigned long long>(n));
         atomicAdd(P.updated, 1u);
-        pv.reject[gp] = 0;  // probe_update.hpp:208-209
-        pv.lastFrame[gp] = P.frame;
+        pv.reject[g] = 0;  // probe_update.hpp:208-209
+        pv.lastFrame[g] = P.frame;
     }
 }
 
-// Per-ray records of the update's ray stage for the listed probes (no state change).
-template <typename R>
-__global__ void __launch_bounds__(kUpdateThreads) k_trace_debug(UpdateParams<R> P) {
-    __shared__ double rot[9];
-    const int gp = P.refs[blockIdx.x];
-    const ProbesView& pv = P.pc.probes;
-    const int ci = cascadeOf(P.pc, gp);
-    const int level = P.pc.cas[ci].level;
-    const int local = gp - P.pc.cas[ci].base;
-    const int n = pv.reject[gp] ? 2 * P.nRaysFull : P.nRaysFull;
-    const V3<double> origin = mk(pv.pos[3 * gp], pv.pos[3 * gp + 1], pv.pos[3 * gp + 2]);
-    if (threadIdx.x == 0) probeRotation(P.seed, P.frame, P.rotatePerFrame != 0, probeKey(level, local), rot);
-    __syncthreads();
-    RayRecord* out = P.records + P.recordOffset[blockIdx.x];
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        V3<double> dir = probeRayDir(rot, i, n);
-        Hit<R> hit;
-        V3<double> L = traceAndShade<R, false>(P, origin, dir, nullptr, &hit);
-        RayRecord r;
-        r.dir[0] = dir.x;
-        r.dir[1] = dir.y;
-        r.dir[2] = dir.z;
-        r.t = hit.converged ? double(hit.t) : 0.0;
-        r.radiance[0] = L.x;
-        r.radiance[1] = L.y;
-        r.radiance[2] = L.z;
-        r.normal[0] = hit.normal.x;
-        r.normal[1] = hit.normal.y;
-        r.normal[2] = hit.normal.z;
-        r.converged = hit.converged;
-        r.miss = hit.miss;
-        r.prim_index = hit.prim >= 0 ? P.scene.orig[hit.prim] : -1;
-        r.steps = hit.steps;
-        out[i] = r;
-    }
+template <typename K>
+static int persistentBlocks(K kernel, int threads, int cap) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, 0);
+    int b = sms * (per > 0 ? per : 1);
+    return cap > 0 ? min(b, cap) : b;
+}
+
+template <typename R, bool ST>
+static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1,
+                      long long* launches) {
+    if (p.nCand <= 0) return;
+    k_ray_setup<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
+    k_ray_scan<R><<<1, kScanThreads, 0, st>>>(p);
+    cudaMemsetAsync(p.ctr, 0, 4 * sizeof(unsigned long long), st);
+    if (e0) cudaEventRecord(e0, st);
+    static int b1 = persistentBlocks(k_trace_primary<R, ST>, kWaveThreads, 0);
+    static int b2 = persistentBlocks(k_trace_shadow<R, ST>, kWaveThreads, 0);
+    k_trace_primary<R, ST><<<cap > 0 ? min(cap, b1) : b1, kWaveThreads, 0, st>>>(p);
+    k_trace_shadow<R, ST><<<cap > 0 ? min(cap, b2) : b2, kWaveThreads, 0, st>>>(p);
+    const size_t smem = static_cast<size_t>(2 * p.nRaysFull) * 6 * sizeof(R);
+    auto k3 = k_shade_convolve<R, ST>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k3<<<p.nCand, kShadeThreads, smem, st>>>(p);
+    if (e1) cudaEventRecord(e1, st);
+    if (launches) *launches += 5;
 }
 
 template <typename R>
-void launch_probe_update(const UpdateParams<R>& p, int nBlocks, int maxRays, bool stats, cudaStream_t st) {
-    size_t smem = static_cast<size_t>(maxRays) * 6 * sizeof(R);
-    if (stats) {
-        auto k = k_probe_update<R, true>;
-        if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k<<<nBlocks, kUpdateThreads, smem, st>>>(p);
-    } else {
-        auto k = k_probe_update<R, false>;
-        if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k<<<nBlocks, kUpdateThreads, smem, st>>>(p);
-    }
-}
-
-template <typename R>
-void launch_trace_debug(const UpdateParams<R>& p, int nBlocks, cudaStream_t st) {
-    k_trace_debug<R><<<nBlocks, kUpdateThreads, 0, st>>>(p);
+void launch_wavefront(const WaveParams<R>& p, int cap, bool stats, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1,
+                      long long* launches) {
+    if (stats)
+        wavefront<R, true>(p, cap, st, e0, e1, launches);
+    else
+        wavefront<R, false>(p, cap, st, e0, e1, launches);
 }
 
 }  // namespace sdfgi_dev

@@ -149,8 +149,15 @@ struct Ctx {
     unsigned long long lastWork[6] = {0, 0, 0, 0, 0, 0};
     DBuf<int> report;
     DBuf<int> refs;
-    DBuf<int> recOffset;
     DBuf<RayRecord> records;
+    // wavefront scratch (kernels.cuh)
+    DBuf<int> wRayCount, wHitList;
+    DBuf<long long> wRayStart;
+    DBuf<double> wRot, fib;
+    int fibN = -1;
+    DBuf<unsigned char> wHits, wVis;
+    DBuf<unsigned long long> wCtr;
+    int persistCap = 0;  // 0 = occupancy-sized persistent grids
     DBuf<double> qpts, qinit, qd;
     DBuf<int> qowner;
 
@@ -162,7 +169,9 @@ struct Ctx {
         gridStart.free(); gridList.free(); gridCounts.free(); gridU.free();
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
-        recOffset.free(); records.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
+        records.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
+        wRayCount.free(); wHitList.free(); wRayStart.free(); wRot.free(); fib.free(); wHits.free();
+        wVis.free(); wCtr.free();
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (comm) ncclCommDestroy(comm);
@@ -434,12 +443,46 @@ void readCounters(Ctx* c, sdfgi_stats* stats, unsigned long long* tail, int ntai
     for (int i = 0; i < ntail; ++i) tail[i] = h[16 + i];
 }
 
+// Wavefront scratch (kernels.cuh): grow-only so repeated passes never reallocate.
+template <typename T>
+void reserve(DBuf<T>& b, size_t count) {
+    if (b.n < count) b.alloc(count);
+}
+
 template <typename R>
-UpdateParams<R> updateParams(Ctx* c, const sdfgi_cfg* cfg, int frame) {
-    UpdateParams<R> p;
+WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand) {
+    const int N = static_cast<int>(cfg->n_rays_full);
+    const size_t maxRays = static_cast<size_t>(nCand) * 2 * N;
+    const int L = std::max(c->nLights, 1);
+    reserve(c->wRayCount, std::max(nCand, 1));
+    reserve(c->wRayStart, static_cast<size_t>(nCand) + 1);
+    reserve(c->wRot, 9 * static_cast<size_t>(std::max(nCand, 1)));
+    reserve(c->wHits, std::max<size_t>(maxRays, 1) * sizeof(HitRec<R>));
+    reserve(c->wHitList, std::max<size_t>(maxRays, 1));
+    reserve(c->wVis, std::max<size_t>(maxRays, 1) * L * sizeof(R));
+    reserve(c->wCtr, 4);
+    if (c->fibN != N) {
+        reserve(c->fib, 9 * static_cast<size_t>(N));
+        launch_fib_table(c->fib.p, N, c->stream);
+        launch_fib_table(c->fib.p + 3 * N, 2 * N, c->stream);
+        checkLaunch(c);
+        ++c->launches;
+        c->fibN = N;
+    }
+    WaveParams<R> p;
     std::memset(&p, 0, sizeof(p));
     p.scene = c->sceneView<R>();
     p.pc = c->probeCommon();
+    p.cand = cand;
+    p.nCand = nCand;
+    p.rayCount = c->wRayCount.p;
+    p.rayStart = c->wRayStart.p;
+    p.rot = c->wRot.p;
+    p.fib = c->fib.p;
+    p.hits = reinterpret_cast<HitRec<R>*>(c->wHits.p);
+    p.hitList = c->wHitList.p;
+    p.vis = reinterpret_cast<R*>(c->wVis.p);
+    p.ctr = c->wCtr.p;
     p.prevAtlas = c->atlas[c->front].p;
     p.currAtlas = c->atlas[1 - c->front].p;
     p.oct = c->octRes;
@@ -466,7 +509,8 @@ UpdateParams<R> updateParams(Ctx* c, const sdfgi_cfg* cfg, int frame) {
 void validateCfg(Ctx* c, const sdfgi_cfg* cfg) {
     REQ(cfg != nullptr, SDFGI_ERR_INVALID, "null cfg");
     REQ(cfg->oct_res == c->octRes, SDFGI_ERR_INVALID, "cfg.oct_res differs from the cascade atlas resolution");
-    REQ(cfg->n_rays_full > 0 && cfg->n_rays_full <= 4096, SDFGI_ERR_INVALID, "n_rays_full out of range");
+    // K3 keeps 2N direction+radiance samples in shared memory (<= 227 KB in FP64)
+    REQ(cfg->n_rays_full > 0 && cfg->n_rays_full <= 2048, SDFGI_ERR_INVALID, "n_rays_full out of range [1, 2048]");
     REQ(cfg->max_trace_steps >= 0 && cfg->shadow_steps >= 0, SDFGI_ERR_INVALID, "negative step limits");
 }
 
@@ -845,25 +889,21 @@ int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_refs, int fr
         // atlas_[write] = atlas_[read] (pipeline.hpp:131); updated tiles are overwritten
         CK(cudaMemcpyAsync(back, frontp, c->atlasFloats() * 4, cudaMemcpyDeviceToDevice, c->stream));
         CK(cudaMemsetAsync(c->scratch.p, 0, 32 * 8, c->stream));
-        const int maxRays = 2 * static_cast<int>(cfg->n_rays_full);
         const bool all = (probe_refs == nullptr && c->world == 1);
         if (!all) c->refs.upload(refs.data(), refs.size(), c->stream);
-        const int nBlocks = static_cast<int>(refs.size());
-        if (nBlocks > 0) {
-            CK(cudaEventRecord(c->ev[0], c->stream));
+        const int nCand = static_cast<int>(refs.size());
+        if (nCand > 0) {
+            const int* cand = all ? nullptr : c->refs.p;
             if (c->precision == SDFGI_F64) {
-                UpdateParams<double> p = updateParams<double>(c, cfg, frame);
-                p.refs = all ? nullptr : c->refs.p;
-                p.nRefs = nBlocks;
-                launch_probe_update<double>(p, nBlocks, maxRays, stats != nullptr, c->stream);
+                WaveParams<double> p = waveParams<double>(c, cfg, frame, cand, nCand);
+                launch_wavefront<double>(p, c->persistCap, stats != nullptr, c->stream, c->ev[0], c->ev[1],
+                                         &c->launches);
             } else {
-                UpdateParams<float> p = updateParams<float>(c, cfg, frame);
-                p.refs = all ? nullptr : c->refs.p;
-                p.nRefs = nBlocks;
-                launch_probe_update<float>(p, nBlocks, maxRays, stats != nullptr, c->stream);
+                WaveParams<float> p = waveParams<float>(c, cfg, frame, cand, nCand);
+                launch_wavefront<float>(p, c->persistCap, stats != nullptr, c->stream, c->ev[0], c->ev[1],
+                                        &c->launches);
             }
-            checkLaunch(c);
-            CK(cudaEventRecord(c->ev[1], c->stream));
+            CK(cudaGetLastError());
             c->evUpdate = true;
         }
         if (c->world > 1) {
@@ -978,35 +1018,26 @@ int sdfgi_probes_trace_debug(void* ctx, const int32_t* probe_refs, int n_refs, i
                 "probe index out of range");
             g.push_back(c->cascades[s].base + probe_refs[2 * i + 1]);
         }
-        std::vector<int> rj(c->totalProbes);
-        CK(cudaMemcpyAsync(rj.data(), c->reject.p, rj.size() * 4, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        std::vector<int> off(n_refs);
-        int total = 0;
-        for (int i = 0; i < n_refs; ++i) {
-            off[i] = total;
-            total += rj[g[i]] ? 2 * static_cast<int>(cfg->n_rays_full) : static_cast<int>(cfg->n_rays_full);
-        }
-        REQ(total <= n_records_max, SDFGI_ERR_INVALID, "n_records_max too small");
+        const size_t cap = static_cast<size_t>(n_refs) * 2 * static_cast<size_t>(cfg->n_rays_full);
         c->refs.upload(g.data(), g.size(), c->stream);
-        c->recOffset.upload(off.data(), off.size(), c->stream);
-        c->records.alloc(total);
+        reserve(c->records, cap);
+        // the same K0..K3 wavefront in debug mode: per-ray records, no atlas/state writes
         if (c->precision == SDFGI_F64) {
-            UpdateParams<double> p = updateParams<double>(c, cfg, frame);
-            p.refs = c->refs.p;
-            p.nRefs = n_refs;
+            WaveParams<double> p = waveParams<double>(c, cfg, frame, c->refs.p, n_refs);
             p.records = c->records.p;
-            p.recordOffset = c->recOffset.p;
-            launch_trace_debug<double>(p, n_refs, c->stream);
+            p.debug = 1;
+            launch_wavefront<double>(p, c->persistCap, false, c->stream, nullptr, nullptr, &c->launches);
         } else {
-            UpdateParams<float> p = updateParams<float>(c, cfg, frame);
-            p.refs = c->refs.p;
-            p.nRefs = n_refs;
+            WaveParams<float> p = waveParams<float>(c, cfg, frame, c->refs.p, n_refs);
             p.records = c->records.p;
-            p.recordOffset = c->recOffset.p;
-            launch_trace_debug<float>(p, n_refs, c->stream);
+            p.debug = 1;
+            launch_wavefront<float>(p, c->persistCap, false, c->stream, nullptr, nullptr, &c->launches);
         }
-        checkLaunch(c);
+        CK(cudaGetLastError());
+        long long total = 0;
+        CK(cudaMemcpyAsync(&total, c->wRayStart.p + n_refs, sizeof(total), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        REQ(total <= n_records_max, SDFGI_ERR_INVALID, "n_records_max too small");
         CK(cudaMemcpyAsync(out, c->records.p, total * sizeof(RayRecord), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         *n_written = total;
