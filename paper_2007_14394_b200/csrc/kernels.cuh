@@ -80,6 +80,7 @@ template <typename R> struct WaveParams {
     long long* rayStart;      // nCand + 1 exclusive prefix (K0 scan)
     double* rot;              // 9 per candidate
     const double* fib;        // sphericalFibonacci table: n=N (N xyz) then n=2N (2N xyz)
+    const int* perm;          // coherent trace order of the sample indices: n=N then n=2N
     HitRec<R>* hits;          // per ray
     int* hitList;             // compacted ray ids of converged hits with an owner
     R* vis;                   // per (ray, light)

@@ -229,10 +229,13 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P)
         __syncwarp();
         unsigned long long item;
         if (fetchItem(P.ctr + 0, static_cast<unsigned long long>(total), active, exhausted, item)) {
-            rid = item;
-            const int s = findCandidate(P.rayStart, P.nCand, static_cast<long long>(rid));
-            const int i = static_cast<int>(static_cast<long long>(rid) - P.rayStart[s]);
+            const int s = findCandidate(P.rayStart, P.nCand, static_cast<long long>(item));
+            const int j = static_cast<int>(static_cast<long long>(item) - P.rayStart[s]);
             const int n = static_cast<int>(P.rayStart[s + 1] - P.rayStart[s]);
+            // slot j traces sample i = perm[j]: consecutive lanes get neighbouring
+            // directions (coherent warps); results are stored by sample index
+            const int i = P.perm[(n == P.nRaysFull ? 0 : P.nRaysFull) + j];
+            rid = static_cast<unsigned long long>(P.rayStart[s] + i);
             const int g = P.cand ? P.cand[s] : s;
             const double* pp = P.pc.probes.pos + 3 * static_cast<size_t>(g);
             V3<double> dd = rayDirection(P, s, i, n);
@@ -261,10 +264,11 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P)
             if (__all_sync(kFull, exhausted)) break;
             continue;
         }
+        V3<R> p = o;
+        R initD = R(0);
         if (active) {
             if (state == 2) t += d;
-            V3<R> p = o + dir * t;
-            R initD;
+            p = o + dir * t;
             if (state == 0) {
                 if (ST) ++cnt.steps;
                 initD = R(2) * lastD;
@@ -273,8 +277,10 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P)
             } else {
                 initD = polishPad(R(2) * fabs(d));
             }
-            int o2 = -1;
-            R nd = query<R, ST>(P.scene, p, initD, &o2, &cnt);
+        }
+        int o2 = -1;
+        const R nd = queryWarp<R, ST>(P.scene, active, p, initD, &o2, &cnt);
+        if (active) {
             int done = 0;  // 1 converged, 2 TMax, 3 StepLimit
             if (state == 0) {
                 if (nd < eps) {
@@ -348,7 +354,8 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P)
 template <typename R, bool ST>
 __global__ void __launch_bounds__(kWaveThreads) k_trace_shadow(WaveParams<R> P) {
     const int L = P.scene.n_lights;
-    const unsigned long long total = P.ctr[1] * static_cast<unsigned long long>(L);
+    const unsigned long long nHits = P.ctr[1];
+    const unsigned long long total = nHits * static_cast<unsigned long long>(L);
     const R minStep = R(5e-4), inf = R(INFINITY), k = R(P.tc.shadowK);
     const int maxSteps = P.tc.shadowSteps;
     Counters cnt;
@@ -362,8 +369,9 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_shadow(WaveParams<R> P) 
         __syncwarp();
         unsigned long long item;
         if (fetchItem(P.ctr + 2, total, active, exhausted, item)) {
-            const int rid = P.hitList[item / L];
-            const int li = static_cast<int>(item % L);
+            // light-major: consecutive lanes take consecutive hits toward the same light
+            const int rid = P.hitList[item % nHits];
+            const int li = static_cast<int>(item / nHits);
             slot = static_cast<unsigned long long>(rid) * L + li;
             const HitRec<R>& h = P.hits[rid];
             const V3<R> pos = mk(h.p[0], h.p[1], h.p[2]);
@@ -412,13 +420,18 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_shadow(WaveParams<R> P) 
             if (__all_sync(kFull, exhausted)) break;
             continue;
         }
+        const bool want = active && step < maxSteps && t < tEnd;
+        V3<R> p = o;
+        if (want) {
+            if (ST) ++cnt.steps;
+            p = o + dir * t;
+        }
+        const R d = queryWarp<R, ST>(P.scene, want, p, lastD == inf ? inf : R(2) * lastD, nullptr, &cnt);
         if (active) {
             bool done = false;
-            if (!(step < maxSteps && t < tEnd)) {
+            if (!want) {
                 done = true;
             } else {
-                if (ST) ++cnt.steps;
-                R d = query<R, ST>(P.scene, o + dir * t, lastD == inf ? inf : R(2) * lastD, nullptr, &cnt);
                 v = smin(v, sclamp(k * d / t, R(0), R(1)));
                 if (v < R(1e-3)) {
                     v = R(0);

@@ -257,6 +257,54 @@ __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int*
     return d;
 }
 
+// Warp-cooperative form of query() for persistent-lane kernels: called by all 32
+// lanes (`active` false for lanes without a query this iteration). Each lane has
+// its ascending cluster list (grid cell, or 0..K-1 off the grid); the warp walks
+// the ascending UNION of the lists with one __reduce_min_sync per step, and every
+// lane whose list holds that cluster visits it. Each lane therefore sees exactly
+// its own clusters in its own order — values, owners and TraceStats are those of
+// query() — but lanes sharing a cluster run it together: uniform bounds/member
+// loads and a uniform kind switch instead of 32 divergent list walks.
+template <typename R, bool ST>
+__device__ __forceinline__ R queryWarp(const SceneView<R>& s, bool active, V3<R> p, R initD, int* owner,
+                                       Counters* c) {
+    R d = initD;
+    int own = -1;
+    int cur = 0, end = 0;
+    const int* lst = nullptr;
+    if (active) {
+        if (ST) ++c->q;
+        end = s.n_clusters;
+        if (s.useGrid) {
+            const GridDev& g = s.grid;
+            R fx = (p.x - R(g.lo[0])) * R(g.invH);
+            R fy = (p.y - R(g.lo[1])) * R(g.invH);
+            R fz = (p.z - R(g.lo[2])) * R(g.invH);
+            if (fx >= R(0) && fy >= R(0) && fz >= R(0) && fx < R(g.dim[0]) && fy < R(g.dim[1]) &&
+                fz < R(g.dim[2])) {
+                int ix = min(static_cast<int>(fx), g.dim[0] - 1);
+                int iy = min(static_cast<int>(fy), g.dim[1] - 1);
+                int iz = min(static_cast<int>(fz), g.dim[2] - 1);
+                int cell = ix + g.dim[0] * (iy + g.dim[1] * iz);
+                lst = g.list;
+                cur = g.start[cell];
+                end = g.start[cell + 1];
+            }
+        }
+    }
+    while (true) {
+        const unsigned head = cur < end ? static_cast<unsigned>(lst ? lst[cur] : cur) : 0xffffffffu;
+        const unsigned m = __reduce_min_sync(0xffffffffu, head);
+        if (m == 0xffffffffu) break;
+        if (head == m) {
+            visitCluster<R, ST>(s, static_cast<int>(m), p, d, own, c);
+            ++cur;
+        }
+    }
+    if (owner) *owner = own;
+    return d;
+}
+
 template <typename R> struct Hit {
     R t;
     V3<R> pos;

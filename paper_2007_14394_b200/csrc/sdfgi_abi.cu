@@ -154,6 +154,7 @@ struct Ctx {
     DBuf<int> wRayCount, wHitList;
     DBuf<long long> wRayStart;
     DBuf<double> wRot, fib;
+    DBuf<int> perm;
     int fibN = -1;
     DBuf<unsigned char> wHits, wVis;
     DBuf<unsigned long long> wCtr;
@@ -171,7 +172,7 @@ struct Ctx {
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
         records.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
         wRayCount.free(); wHitList.free(); wRayStart.free(); wRot.free(); fib.free(); wHits.free();
-        wVis.free(); wCtr.free();
+        wVis.free(); wCtr.free(); perm.free();
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (comm) ncclCommDestroy(comm);
@@ -443,6 +444,42 @@ void readCounters(Ctx* c, sdfgi_stats* stats, unsigned long long* tail, int ntai
     for (int i = 0; i < ntail; ++i) tail[i] = h[16 + i];
 }
 
+// Trace order of the n Fibonacci samples: sorted along a Morton curve over their
+// octahedral coordinates, so the 32 lanes of a warp march neighbouring directions
+// (the per-probe random rotation is rigid and keeps neighbours neighbours). Only
+// the scheduling order changes; samples are stored and summed by index.
+std::vector<int> coherentOrder(int n) {
+    const double golden = M_PI * (3.0 - std::sqrt(5.0));
+    std::vector<std::pair<uint32_t, int>> keys(n);
+    auto spread = [](uint32_t x) {
+        x &= 0xffff;
+        x = (x | (x << 8)) & 0x00ff00ff;
+        x = (x | (x << 4)) & 0x0f0f0f0f;
+        x = (x | (x << 2)) & 0x33333333;
+        x = (x | (x << 1)) & 0x55555555;
+        return x;
+    };
+    for (int i = 0; i < n; ++i) {
+        double z = 1.0 - (2.0 * i + 1.0) / n, r = std::sqrt(std::max(0.0, 1.0 - z * z)), phi = golden * i;
+        double x = r * std::cos(phi), y = r * std::sin(phi);
+        double nrm = std::fabs(x) + std::fabs(y) + std::fabs(z);
+        double px = x / nrm, py = y / nrm;
+        if (z < 0) {
+            double ox = (1.0 - std::fabs(py)) * (px >= 0 ? 1.0 : -1.0);
+            double oy = (1.0 - std::fabs(px)) * (py >= 0 ? 1.0 : -1.0);
+            px = ox;
+            py = oy;
+        }
+        uint32_t u = static_cast<uint32_t>(std::min(65535.0, (px * 0.5 + 0.5) * 65535.0));
+        uint32_t v = static_cast<uint32_t>(std::min(65535.0, (py * 0.5 + 0.5) * 65535.0));
+        keys[i] = {spread(u) | (spread(v) << 1), i};
+    }
+    std::sort(keys.begin(), keys.end());
+    std::vector<int> perm(n);
+    for (int j = 0; j < n; ++j) perm[j] = keys[j].second;
+    return perm;
+}
+
 // Wavefront scratch (kernels.cuh): grow-only so repeated passes never reallocate.
 template <typename T>
 void reserve(DBuf<T>& b, size_t count) {
@@ -467,6 +504,10 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
         launch_fib_table(c->fib.p + 3 * N, 2 * N, c->stream);
         checkLaunch(c);
         ++c->launches;
+        std::vector<int> perm = coherentOrder(N);
+        std::vector<int> perm2 = coherentOrder(2 * N);
+        perm.insert(perm.end(), perm2.begin(), perm2.end());
+        c->perm.upload(perm.data(), perm.size(), c->stream);
         c->fibN = N;
     }
     WaveParams<R> p;
@@ -479,6 +520,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.rayStart = c->wRayStart.p;
     p.rot = c->wRot.p;
     p.fib = c->fib.p;
+    p.perm = c->perm.p;
     p.hits = reinterpret_cast<HitRec<R>*>(c->wHits.p);
     p.hitList = c->wHitList.p;
     p.vis = reinterpret_cast<R*>(c->wVis.p);
