@@ -279,7 +279,8 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P)
             }
         }
         int o2 = -1;
-        const R nd = queryWarp<R, ST>(P.scene, active, p, initD, &o2, &cnt);
+        R nd = R(0);
+        if (active) nd = query<R, ST>(P.scene, p, initD, &o2, &cnt);
         if (active) {
             int done = 0;  // 1 converged, 2 TMax, 3 StepLimit
             if (state == 0) {
@@ -426,7 +427,8 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_shadow(WaveParams<R> P) 
             if (ST) ++cnt.steps;
             p = o + dir * t;
         }
-        const R d = queryWarp<R, ST>(P.scene, want, p, lastD == inf ? inf : R(2) * lastD, nullptr, &cnt);
+        R d = R(0);
+        if (want) d = query<R, ST>(P.scene, p, lastD == inf ? inf : R(2) * lastD, nullptr, &cnt);
         if (active) {
             bool done = false;
             if (!want) {

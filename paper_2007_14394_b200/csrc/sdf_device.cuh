@@ -82,6 +82,20 @@ template <typename R> struct __align__(16) DPrim {
     int kind;
     int identity;
 };
+// FP32 perf-mode record: every bounded kind in one branch-free form (see
+// evalPrim<float>): e = extents of a box (mode 0) or of a radial shape (mode 1:
+// cylinder r/h, capsule 0/h, sphere 0/0), rr = rounding radius (capsule, sphere);
+// mode 2 = plane. 80 B.
+template <> struct __align__(16) DPrim<float> {
+    float rot[9];
+    float trans[3];
+    float e[3];
+    float rr;
+    int mode;
+    int kind;
+    int identity;
+    int _pad;
+};
 template <typename R> struct __align__(16) DCluster {
     R lo[3];
     R hi[3];
@@ -177,6 +191,32 @@ __device__ __forceinline__ R evalPrim(const DPrim<R>& pr, V3<R> p) {
     }
 }
 
+// FP32 perf mode: the five kinds as one branch-free formula so lanes evaluating
+// different kinds do not serialise. With q = R^T (p - t):
+//   u = (radial ? |q.xy| : |q.x|) - e0,  v = radial ? -inf : |q.y| - e1,  w = |q.z| - e2
+//   d = |max((u, v, w), 0)| + min(max(u, v, w), 0) - rr      (plane: q.z)
+// box (e = half extents), cylinder (radial, e = r, -, h), capsule (radial,
+// e = 0, -, h, rr = r) and sphere (radial, e = 0, rr = r) are exactly the
+// reference's formulas (primitives.hpp:42-65) in exact arithmetic.
+template <>
+__device__ __forceinline__ float evalPrim<float>(const DPrim<float>& pr, V3<float> p) {
+    const float px = p.x - pr.trans[0], py = p.y - pr.trans[1], pz = p.z - pr.trans[2];
+    const float* m = pr.rot;
+    const float qx = fmaf(m[0], px, fmaf(m[3], py, m[6] * pz));
+    const float qy = fmaf(m[1], px, fmaf(m[4], py, m[7] * pz));
+    const float qz = fmaf(m[2], px, fmaf(m[5], py, m[8] * pz));
+    const bool radial = pr.mode == 1;
+    const float rho = sqrtf(fmaf(qx, qx, qy * qy));
+    const float u = (radial ? rho : fabsf(qx)) - pr.e[0];
+    const float v = radial ? -1e30f : fabsf(qy) - pr.e[1];
+    const float w = fabsf(qz) - pr.e[2];
+    const float ou = fmaxf(u, 0.f), ov = fmaxf(v, 0.f), ow = fmaxf(w, 0.f);
+    const float outside = sqrtf(fmaf(ou, ou, fmaf(ov, ov, ow * ow)));
+    const float inside = fminf(fmaxf(u, fmaxf(v, w)), 0.f);
+    const float d = outside + inside - pr.rr;
+    return pr.mode == 2 ? qz : d;
+}
+
 // evalGradientDetailed / evalGradient, primitives.hpp:96-108 (h = 1e-3)
 template <typename R>
 __device__ __forceinline__ V3<R> evalGradient(const DPrim<R>& pr, V3<R> p) {
@@ -190,50 +230,31 @@ __device__ __forceinline__ V3<R> evalGradient(const DPrim<R>& pr, V3<R> p) {
 }
 
 // ------------------------------------------------------------------ scene.hpp
-// queryCore (scene.hpp:214-332): exactly min(naive SDF, initD); owner = the first
-// primitive in cluster order attaining it (or -1). Clusters are walked in order
-// by every lane of the warp, so the per-cluster bounds and member records are
-// warp-uniform loads (L1 broadcast) and the kind switch is a uniform branch.
-// One cluster of queryCore's walk: skip test against the running minimum, then
-// the member evaluations (scene.hpp:228-248,294-304).
-template <typename R, bool ST>
-__device__ __forceinline__ void visitCluster(const SceneView<R>& s, int k, V3<R> p, R& d, int& own, Counters* c) {
-    const DCluster<R>& cl = s.clusters[k];
+// Skip test of queryCore (scene.hpp:231, 299): a cluster is skipped when its box is
+// at least the running minimum away (d > 0) or does not contain p (d <= 0).
+template <typename R>
+__device__ __forceinline__ bool clusterSkipped(const DCluster<R>& cl, V3<R> p, R d) {
     R dx = smax(smax(cl.lo[0] - p.x, p.x - cl.hi[0]), R(0));
     R dy = smax(smax(cl.lo[1] - p.y, p.y - cl.hi[1]), R(0));
     R dz = smax(smax(cl.lo[2] - p.z, p.z - cl.hi[2]), R(0));
     R boxSq = dx * dx + dy * dy + dz * dz;
-    if (!cl.unbounded && (d > R(0) ? boxSq >= d * d : boxSq > R(0))) {
-        if (ST) ++c->cs;
-        return;
-    }
-    const int b = s.cstart[k], e = s.cstart[k + 1];
-    if (ST) {
-        ++c->cv;
-        c->pe += e - b;
-    }
-    for (int j = b; j < e; ++j) {
-        if (ST) {
-            ++c->ek[s.prims[j].kind];
-            c->ek[5] += s.prims[j].identity ? 0 : 1;
-        }
-        R pd = evalPrim(s.prims[j], p);
-        if (pd < d) {
-            d = pd;
-            own = j;
-        }
-    }
+    return !cl.unbounded && (d > R(0) ? boxSq >= d * d : boxSq > R(0));
 }
 
 // queryCore (scene.hpp:214-332): exactly min(naive SDF, initD); owner = the first
 // primitive in cluster order attaining it (or -1). Inside the candidate grid a lane
-// walks its cell's ascending candidate list; elsewhere every cluster in order.
+// walks its cell's ascending candidate list, elsewhere every cluster in order.
+// The cluster -> member walk is flattened into ONE loop with one primitive
+// evaluation per iteration (the next visited cluster's skip tests run when a
+// member range is exhausted), so lanes whose lists and clusters differ in length
+// stay converged on the evaluation instead of splitting over nested loops.
 template <typename R, bool ST>
 __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int* owner, Counters* c) {
     R d = initD;
     int own = -1;
     if (ST) ++c->q;
-    bool done = false;
+    int cur = 0, end = s.n_clusters;
+    const int* lst = nullptr;
     if (s.useGrid) {
         const GridDev& g = s.grid;
         R fx = (p.x - R(g.lo[0])) * R(g.invH);
@@ -244,62 +265,38 @@ __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int*
             int iy = min(static_cast<int>(fy), g.dim[1] - 1);
             int iz = min(static_cast<int>(fz), g.dim[2] - 1);
             int cell = ix + g.dim[0] * (iy + g.dim[1] * iz);
-            const int b = g.start[cell], e = g.start[cell + 1];
-            for (int i = b; i < e; ++i) visitCluster<R, ST>(s, g.list[i], p, d, own, c);
-            done = true;
+            lst = g.list;
+            cur = g.start[cell];
+            end = g.start[cell + 1];
         }
     }
-    if (!done) {
-        const int K = s.n_clusters;
-        for (int k = 0; k < K; ++k) visitCluster<R, ST>(s, k, p, d, own, c);
-    }
-    if (owner) *owner = own;
-    return d;
-}
-
-// Warp-cooperative form of query() for persistent-lane kernels: called by all 32
-// lanes (`active` false for lanes without a query this iteration). Each lane has
-// its ascending cluster list (grid cell, or 0..K-1 off the grid); the warp walks
-// the ascending UNION of the lists with one __reduce_min_sync per step, and every
-// lane whose list holds that cluster visits it. Each lane therefore sees exactly
-// its own clusters in its own order — values, owners and TraceStats are those of
-// query() — but lanes sharing a cluster run it together: uniform bounds/member
-// loads and a uniform kind switch instead of 32 divergent list walks.
-template <typename R, bool ST>
-__device__ __forceinline__ R queryWarp(const SceneView<R>& s, bool active, V3<R> p, R initD, int* owner,
-                                       Counters* c) {
-    R d = initD;
-    int own = -1;
-    int cur = 0, end = 0;
-    const int* lst = nullptr;
-    if (active) {
-        if (ST) ++c->q;
-        end = s.n_clusters;
-        if (s.useGrid) {
-            const GridDev& g = s.grid;
-            R fx = (p.x - R(g.lo[0])) * R(g.invH);
-            R fy = (p.y - R(g.lo[1])) * R(g.invH);
-            R fz = (p.z - R(g.lo[2])) * R(g.invH);
-            if (fx >= R(0) && fy >= R(0) && fz >= R(0) && fx < R(g.dim[0]) && fy < R(g.dim[1]) &&
-                fz < R(g.dim[2])) {
-                int ix = min(static_cast<int>(fx), g.dim[0] - 1);
-                int iy = min(static_cast<int>(fy), g.dim[1] - 1);
-                int iz = min(static_cast<int>(fz), g.dim[2] - 1);
-                int cell = ix + g.dim[0] * (iy + g.dim[1] * iz);
-                lst = g.list;
-                cur = g.start[cell];
-                end = g.start[cell + 1];
+    int j = 0, je = 0;  // member range of the cluster being visited
+    while (true) {
+        while (j >= je && cur < end) {
+            const int k = lst ? lst[cur] : cur;
+            ++cur;
+            if (clusterSkipped(s.clusters[k], p, d)) {
+                if (ST) ++c->cs;
+                continue;
+            }
+            j = s.cstart[k];
+            je = s.cstart[k + 1];
+            if (ST) {
+                ++c->cv;
+                c->pe += je - j;
             }
         }
-    }
-    while (true) {
-        const unsigned head = cur < end ? static_cast<unsigned>(lst ? lst[cur] : cur) : 0xffffffffu;
-        const unsigned m = __reduce_min_sync(0xffffffffu, head);
-        if (m == 0xffffffffu) break;
-        if (head == m) {
-            visitCluster<R, ST>(s, static_cast<int>(m), p, d, own, c);
-            ++cur;
+        if (j >= je) break;
+        if (ST) {
+            ++c->ek[s.prims[j].kind];
+            c->ek[5] += s.prims[j].identity ? 0 : 1;
         }
+        const R pd = evalPrim(s.prims[j], p);
+        if (pd < d) {
+            d = pd;
+            own = j;
+        }
+        ++j;
     }
     if (owner) *owner = own;
     return d;

@@ -338,6 +338,37 @@ void fillPrim(DPrim<R>& d, const sdfgi_prim& s) {
     d.identity = (s.rot[0] == 1.0 && s.rot[4] == 1.0 && s.rot[8] == 1.0) ? 1 : 0;
 }
 
+// FP32 unified record (DPrim<float>, evalPrim<float>): the per-kind `size`
+// meanings of primitives.hpp:25-30 mapped onto (mode, e, rr).
+void fillPrim(DPrim<float>& d, const sdfgi_prim& s) {
+    for (int k = 0; k < 9; ++k) d.rot[k] = static_cast<float>(s.rot[k]);
+    for (int k = 0; k < 3; ++k) {
+        d.trans[k] = static_cast<float>(s.trans[k]);
+        d.e[k] = 0.f;
+    }
+    d.rr = 0.f;
+    switch (s.kind) {
+        case SDFGI_SPHERE: d.mode = 1; d.rr = static_cast<float>(s.size[0]); break;
+        case SDFGI_BOX:
+            d.mode = 0;
+            for (int k = 0; k < 3; ++k) d.e[k] = static_cast<float>(s.size[k]);
+            break;
+        case SDFGI_PLANE: d.mode = 2; break;
+        case SDFGI_CYLINDER:
+            d.mode = 1;
+            d.e[0] = static_cast<float>(s.size[0]);
+            d.e[2] = static_cast<float>(s.size[1]);
+            break;
+        default:  // capsule
+            d.mode = 1;
+            d.e[2] = static_cast<float>(s.size[1]);
+            d.rr = static_cast<float>(s.size[0]);
+            break;
+    }
+    d.kind = s.kind;
+    d.identity = (s.rot[0] == 1.0 && s.rot[4] == 1.0 && s.rot[8] == 1.0) ? 1 : 0;
+}
+
 // Build the candidate-cluster grid over the bounded clusters (exact; see GridDev).
 void buildGrid(Ctx* c, const sdfgi_cluster* clusters, int n) {
     c->haveGrid = false;
