@@ -53,7 +53,33 @@ __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells
             ++n;
         }
     }
-    if (!fill) P.counts[cell] = n;
+    if (!fill) {
+        P.counts[cell] = n;
+        return;
+    }
+    // nearest first (box distance to the cell centre): the running minimum drops
+    // early and later candidates are skipped; order does not affect results
+    // (queries break ties towards the lowest CSR position)
+    const double cx = 0.5 * (lo[0] + hi[0]), cy = 0.5 * (lo[1] + hi[1]), cz = 0.5 * (lo[2] + hi[2]);
+    auto key = [&](int k) {
+        const DCluster<double>& cl = P.scene.clusters[k];
+        if (cl.unbounded) return -1.0;
+        double gx = fmax(fmax(cl.lo[0] - cx, cx - cl.hi[0]), 0.0);
+        double gy = fmax(fmax(cl.lo[1] - cy, cy - cl.hi[1]), 0.0);
+        double gz = fmax(fmax(cl.lo[2] - cz, cz - cl.hi[2]), 0.0);
+        return gx * gx + gy * gy + gz * gz;
+    };
+    int* L = P.list + out;
+    for (int a = 1; a < n; ++a) {
+        const int v = L[a];
+        const double kv = key(v);
+        int b = a - 1;
+        while (b >= 0 && key(L[b]) > kv) {
+            L[b + 1] = L[b];
+            --b;
+        }
+        L[b + 1] = v;
+    }
 }
 
 void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st) {

@@ -114,17 +114,25 @@ struct DLight {  // sdfgi_light, kept in double in both modes (tiny)
 // of a uniform grid over the bounded clusters, U = SDF(cell centre) + half the
 // (padded) cell diagonal bounds the scene SDF anywhere in the cell (1-Lipschitz),
 // so only clusters whose cull box lies within max(U, 0) of the cell can hold the
-// minimum — or tie with it — at any point of the cell. Lists keep ascending
-// cluster order, so the first-minimiser owner rule of queryCore is unchanged and
-// query values/owners are identical to the reference's flat walk. Points outside
-// the grid take the flat walk.
+// minimum — or tie with it — at any point of the cell (lists are sorted nearest
+// first). Points outside the grid walk superclusters: Morton-ordered groups of 8
+// bounded clusters under one box (a group is skipped only if every member would
+// be), then the unbounded clusters. Visiting order no longer follows cluster
+// order, so queryAccel breaks distance ties explicitly towards the lowest CSR
+// position — the primitive the reference's in-order walk keeps (scene.hpp:243) —
+// and values and owners stay identical to the reference's.
 struct GridDev {
     double lo[3];
     double invH;
     int dim[3];
-    int _pad;
+    int nSuper;
     const int* __restrict__ start;  // ncells + 1
     const int* __restrict__ list;
+    const int* __restrict__ superStart;     // nSuper + 1 into superList
+    const int* __restrict__ superList;      // cluster ids; unbounded clusters last (always visited)
+    const double* __restrict__ superBox;    // 6 per supercluster (lo xyz, hi xyz)
+    int nUnbounded;
+    int _pad2;
 };
 
 template <typename R> struct SceneView {
@@ -248,55 +256,110 @@ __device__ __forceinline__ bool clusterSkipped(const DCluster<R>& cl, V3<R> p, R
 // evaluation per iteration (the next visited cluster's skip tests run when a
 // member range is exhausted), so lanes whose lists and clusters differ in length
 // stay converged on the evaluation instead of splitting over nested loops.
-template <typename R, bool ST>
-__device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int* owner, Counters* c) {
-    R d = initD;
-    int own = -1;
-    if (ST) ++c->q;
-    int cur = 0, end = s.n_clusters;
-    const int* lst = nullptr;
-    if (s.useGrid) {
-        const GridDev& g = s.grid;
-        R fx = (p.x - R(g.lo[0])) * R(g.invH);
-        R fy = (p.y - R(g.lo[1])) * R(g.invH);
-        R fz = (p.z - R(g.lo[2])) * R(g.invH);
-        if (fx >= R(0) && fy >= R(0) && fz >= R(0) && fx < R(g.dim[0]) && fy < R(g.dim[1]) && fz < R(g.dim[2])) {
-            int ix = min(static_cast<int>(fx), g.dim[0] - 1);
-            int iy = min(static_cast<int>(fy), g.dim[1] - 1);
-            int iz = min(static_cast<int>(fz), g.dim[2] - 1);
-            int cell = ix + g.dim[0] * (iy + g.dim[1] * iz);
-            lst = g.list;
-            cur = g.start[cell];
-            end = g.start[cell + 1];
-        }
+// Members of one visited cluster: in order with the reference's strict `<`
+// (TIE = false), or with the explicit lowest-CSR-position tie-break (TIE = true)
+// when clusters are visited out of order.
+template <typename R, bool ST, bool TIE>
+__device__ __forceinline__ void visitMembers(const SceneView<R>& s, int k, V3<R> p, R& d, int& own, Counters* c) {
+    const int b = s.cstart[k], e = s.cstart[k + 1];
+    if (ST) {
+        ++c->cv;
+        c->pe += e - b;
     }
-    int j = 0, je = 0;  // member range of the cluster being visited
-    while (true) {
-        while (j >= je && cur < end) {
-            const int k = lst ? lst[cur] : cur;
-            ++cur;
-            if (clusterSkipped(s.clusters[k], p, d)) {
-                if (ST) ++c->cs;
-                continue;
-            }
-            j = s.cstart[k];
-            je = s.cstart[k + 1];
-            if (ST) {
-                ++c->cv;
-                c->pe += je - j;
-            }
-        }
-        if (j >= je) break;
+    for (int j = b; j < e; ++j) {
         if (ST) {
             ++c->ek[s.prims[j].kind];
             c->ek[5] += s.prims[j].identity ? 0 : 1;
         }
         const R pd = evalPrim(s.prims[j], p);
-        if (pd < d) {
+        if (pd < d || (TIE && pd == d && own >= 0 && j < own)) {
             d = pd;
             own = j;
         }
-        ++j;
+    }
+}
+
+template <typename R>
+__device__ __forceinline__ bool boxSkipped(const double* b, V3<R> p, R d) {
+    R dx = smax(smax(R(b[0]) - p.x, p.x - R(b[3])), R(0));
+    R dy = smax(smax(R(b[1]) - p.y, p.y - R(b[4])), R(0));
+    R dz = smax(smax(R(b[2]) - p.z, p.z - R(b[5])), R(0));
+    R boxSq = dx * dx + dy * dy + dz * dz;
+    return d > R(0) ? boxSq >= d * d : boxSq > R(0);
+}
+
+template <typename R, bool ST>
+__device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int* owner, Counters* c) {
+    R d = initD;
+    int own = -1;
+    if (ST) ++c->q;
+    if (!s.useGrid) {
+        // the reference's walk: every cluster in order, strict `<`
+        for (int k = 0; k < s.n_clusters; ++k) {
+            if (clusterSkipped(s.clusters[k], p, d)) {
+                if (ST) ++c->cs;
+                continue;
+            }
+            visitMembers<R, ST, false>(s, k, p, d, own, c);
+        }
+        if (owner) *owner = own;
+        return d;
+    }
+    const GridDev& g = s.grid;
+    R fx = (p.x - R(g.lo[0])) * R(g.invH);
+    R fy = (p.y - R(g.lo[1])) * R(g.invH);
+    R fz = (p.z - R(g.lo[2])) * R(g.invH);
+    if (fx >= R(0) && fy >= R(0) && fz >= R(0) && fx < R(g.dim[0]) && fy < R(g.dim[1]) && fz < R(g.dim[2])) {
+        int ix = min(static_cast<int>(fx), g.dim[0] - 1);
+        int iy = min(static_cast<int>(fy), g.dim[1] - 1);
+        int iz = min(static_cast<int>(fz), g.dim[2] - 1);
+        int cell = ix + g.dim[0] * (iy + g.dim[1] * iz);
+        int cur = g.start[cell];
+        const int end = g.start[cell + 1];
+        // cluster -> member walk flattened into one loop, one evaluation per
+        // iteration: lanes whose lists/clusters differ in length stay converged
+        int j = 0, je = 0;
+        while (true) {
+            while (j >= je && cur < end) {
+                const int k = g.list[cur++];
+                if (clusterSkipped(s.clusters[k], p, d)) {
+                    if (ST) ++c->cs;
+                    continue;
+                }
+                j = s.cstart[k];
+                je = s.cstart[k + 1];
+                if (ST) {
+                    ++c->cv;
+                    c->pe += je - j;
+                }
+            }
+            if (j >= je) break;
+            if (ST) {
+                ++c->ek[s.prims[j].kind];
+                c->ek[5] += s.prims[j].identity ? 0 : 1;
+            }
+            const R pd = evalPrim(s.prims[j], p);
+            if (pd < d || (pd == d && own >= 0 && j < own)) {
+                d = pd;
+                own = j;
+            }
+            ++j;
+        }
+    } else {
+        // off the grid: superclusters, then the unbounded clusters
+        for (int sc = 0; sc < g.nSuper; ++sc) {
+            if (boxSkipped(g.superBox + 6 * sc, p, d)) continue;
+            for (int i = g.superStart[sc]; i < g.superStart[sc + 1]; ++i) {
+                const int k = g.superList[i];
+                if (clusterSkipped(s.clusters[k], p, d)) {
+                    if (ST) ++c->cs;
+                    continue;
+                }
+                visitMembers<R, ST, true>(s, k, p, d, own, c);
+            }
+        }
+        const int u0 = g.superStart[g.nSuper];
+        for (int i = u0; i < u0 + g.nUnbounded; ++i) visitMembers<R, ST, true>(s, g.superList[i], p, d, own, c);
     }
     if (owner) *owner = own;
     return d;

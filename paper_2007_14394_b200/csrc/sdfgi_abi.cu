@@ -133,7 +133,8 @@ struct Ctx {
     GridDev grid{};
     long long gridEntries = 0;
     DBuf<int> gridStart, gridList, gridCounts;
-    DBuf<double> gridU;
+    DBuf<double> gridU, superBox;
+    DBuf<int> superStart, superList;
     // probes
     std::vector<CascadeHost> cascades;
     int octRes = 8;
@@ -168,6 +169,7 @@ struct Ctx {
         prim64.free(); prim32.free(); cl64.free(); cl32.free(); cstart.free(); orig.free();
         albedo.free(); emission.free(); lights.free();
         gridStart.free(); gridList.free(); gridCounts.free(); gridU.free();
+        superBox.free(); superStart.free(); superList.free();
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
         records.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
@@ -454,6 +456,65 @@ void buildGrid(Ctx* c, const sdfgi_cluster* clusters, int n) {
     c->grid.start = c->gridStart.p;
     c->grid.list = c->gridList.p;
     c->gridEntries = total;
+
+    // superclusters for points off the grid: bounded clusters in Morton order of
+    // their box centres, 8 per group; boxes padded like the FP32 cluster boxes so
+    // the group skip is conservative in both precisions.
+    auto spread10 = [](uint32_t x) {
+        x &= 0x3ff;
+        x = (x | (x << 16)) & 0x030000ff;
+        x = (x | (x << 8)) & 0x0300f00f;
+        x = (x | (x << 4)) & 0x030c30c3;
+        x = (x | (x << 2)) & 0x09249249;
+        return x;
+    };
+    std::vector<std::pair<uint32_t, int>> order;
+    std::vector<int> unb;
+    for (int k = 0; k < n; ++k) {
+        if (clusters[k].unbounded) {
+            unb.push_back(k);
+            continue;
+        }
+        uint32_t code = 0;
+        for (int a = 0; a < 3; ++a) {
+            double cc = 0.5 * (clusters[k].lo[a] + clusters[k].hi[a]);
+            double u = std::min(1.0, std::max(0.0, (cc - lo[a]) / ext[a]));
+            code |= spread10(static_cast<uint32_t>(u * 1023.0)) << a;
+        }
+        order.push_back({code, k});
+    }
+    std::sort(order.begin(), order.end());
+    const int per = 8;
+    const int nSuper = static_cast<int>((order.size() + per - 1) / per);
+    std::vector<int> sStart(nSuper + 1), sList;
+    std::vector<double> sBox(6 * static_cast<size_t>(std::max(nSuper, 1)));
+    for (int sc = 0; sc < nSuper; ++sc) {
+        sStart[sc] = static_cast<int>(sList.size());
+        double blo[3] = {INFINITY, INFINITY, INFINITY}, bhi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (size_t i = sc * per; i < std::min(order.size(), static_cast<size_t>(sc + 1) * per); ++i) {
+            const int k = order[i].second;
+            sList.push_back(k);
+            for (int a = 0; a < 3; ++a) {
+                blo[a] = std::min(blo[a], clusters[k].lo[a]);
+                bhi[a] = std::max(bhi[a], clusters[k].hi[a]);
+            }
+        }
+        for (int a = 0; a < 3; ++a) {
+            sBox[6 * sc + a] = blo[a] - 2e-5 * (std::fabs(blo[a]) + 1.0);
+            sBox[6 * sc + 3 + a] = bhi[a] + 2e-5 * (std::fabs(bhi[a]) + 1.0);
+        }
+    }
+    sStart[nSuper] = static_cast<int>(sList.size());
+    sList.insert(sList.end(), unb.begin(), unb.end());
+    c->superStart.upload(sStart.data(), sStart.size(), c->stream);
+    c->superList.upload(sList.data(), std::max<size_t>(sList.size(), 1), c->stream);
+    c->superBox.upload(sBox.data(), sBox.size(), c->stream);
+    CK(cudaStreamSynchronize(c->stream));
+    c->grid.nSuper = nSuper;
+    c->grid.superStart = c->superStart.p;
+    c->grid.superList = c->superList.p;
+    c->grid.superBox = c->superBox.p;
+    c->grid.nUnbounded = static_cast<int>(unb.size());
     c->haveGrid = true;
 }
 
