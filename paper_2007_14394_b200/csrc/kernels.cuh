@@ -112,6 +112,7 @@ struct GridBuildParams {
     int dim[3];
     double pad;     // cell boxes are padded by this much on every side
     double margin;  // absolute slack on the bound
+    const double* primBox;  // conservative AABB per CSR primitive (lo xyz, hi xyz; -inf/+inf unbounded)
     double* U;
     int* counts;
     const int* start;

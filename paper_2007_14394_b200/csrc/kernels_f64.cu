@@ -35,38 +35,42 @@ __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells
     const double hi[3] = {lo[0] + P.h + 2 * P.pad, lo[1] + P.h + 2 * P.pad, lo[2] + P.h + 2 * P.pad};
     const double r = fmax(P.U[cell], 0.0) + P.margin;
     const double r2 = isinf(r) ? INFINITY : r * r;
+    auto gap2 = [&](const double* blo, const double* bhi) {
+        double g2 = 0;
+        for (int a = 0; a < 3; ++a) {
+            double g = fmax(fmax(blo[a] - hi[a], lo[a] - bhi[a]), 0.0);
+            g2 += g * g;
+        }
+        return g2;
+    };
+    // candidate PRIMITIVES: every member of an unbounded cluster, and members of
+    // nearby clusters whose own conservative box is within r of the cell
     int n = 0;
     int out = fill ? P.start[cell] : 0;
     for (int k = 0; k < P.scene.n_clusters; ++k) {
         const DCluster<double>& cl = P.scene.clusters[k];
-        bool cand = cl.unbounded != 0;
-        if (!cand) {
-            double g2 = 0;
-            for (int a = 0; a < 3; ++a) {
-                double g = fmax(fmax(cl.lo[a] - hi[a], lo[a] - cl.hi[a]), 0.0);
-                g2 += g * g;
+        if (!cl.unbounded && gap2(cl.lo, cl.hi) > r2) continue;
+        for (int j = P.scene.cstart[k]; j < P.scene.cstart[k + 1]; ++j) {
+            const double* b = P.primBox + 6 * static_cast<size_t>(j);
+            if (cl.unbounded || isinf(b[0]) || gap2(b, b + 3) <= r2) {
+                if (fill) P.list[out + n] = j;
+                ++n;
             }
-            cand = g2 <= r2;
-        }
-        if (cand) {
-            if (fill) P.list[out + n] = k;
-            ++n;
         }
     }
     if (!fill) {
         P.counts[cell] = n;
         return;
     }
-    // nearest first (box distance to the cell centre): the running minimum drops
-    // early and later candidates are skipped; order does not affect results
-    // (queries break ties towards the lowest CSR position)
+    // nearest first (box distance to the cell centre): order does not affect
+    // results (queries break ties towards the lowest CSR position)
     const double cx = 0.5 * (lo[0] + hi[0]), cy = 0.5 * (lo[1] + hi[1]), cz = 0.5 * (lo[2] + hi[2]);
-    auto key = [&](int k) {
-        const DCluster<double>& cl = P.scene.clusters[k];
-        if (cl.unbounded) return -1.0;
-        double gx = fmax(fmax(cl.lo[0] - cx, cx - cl.hi[0]), 0.0);
-        double gy = fmax(fmax(cl.lo[1] - cy, cy - cl.hi[1]), 0.0);
-        double gz = fmax(fmax(cl.lo[2] - cz, cz - cl.hi[2]), 0.0);
+    auto key = [&](int j) {
+        const double* b = P.primBox + 6 * static_cast<size_t>(j);
+        if (isinf(b[0])) return -1.0;
+        double gx = fmax(fmax(b[0] - cx, cx - b[3]), 0.0);
+        double gy = fmax(fmax(b[1] - cy, cy - b[4]), 0.0);
+        double gz = fmax(fmax(b[2] - cz, cz - b[5]), 0.0);
         return gx * gx + gy * gy + gz * gz;
     };
     int* L = P.list + out;

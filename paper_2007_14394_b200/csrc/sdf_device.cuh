@@ -110,12 +110,13 @@ struct DLight {  // sdfgi_light, kept in double in both modes (tiny)
     double intensity[3];
 };
 
-// Candidate-cluster grid (exact acceleration of the cluster walk). For every cell
-// of a uniform grid over the bounded clusters, U = SDF(cell centre) + half the
-// (padded) cell diagonal bounds the scene SDF anywhere in the cell (1-Lipschitz),
-// so only clusters whose cull box lies within max(U, 0) of the cell can hold the
-// minimum — or tie with it — at any point of the cell (lists are sorted nearest
-// first). Points outside the grid walk superclusters: Morton-ordered groups of 8
+// Candidate grid (exact acceleration of the cluster walk). For every cell of a
+// uniform grid over the bounded clusters, U = SDF(cell centre) + half the (padded)
+// cell diagonal bounds the scene SDF anywhere in the cell (1-Lipschitz), so only
+// primitives whose conservative AABB lies within max(U, 0) of the cell can hold
+// the minimum — or tie with it — at any point of the cell; the cell's list holds
+// exactly those (CSR positions, nearest first) and the query evaluates them
+// without cluster tests. Points outside the grid walk superclusters: Morton-ordered groups of 8
 // bounded clusters under one box (a group is skipped only if every member would
 // be), then the unbounded clusters. Visiting order no longer follows cluster
 // order, so queryAccel breaks distance ties explicitly towards the lowest CSR
@@ -314,26 +315,11 @@ __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int*
         int iy = min(static_cast<int>(fy), g.dim[1] - 1);
         int iz = min(static_cast<int>(fz), g.dim[2] - 1);
         int cell = ix + g.dim[0] * (iy + g.dim[1] * iz);
-        int cur = g.start[cell];
-        const int end = g.start[cell + 1];
-        // cluster -> member walk flattened into one loop, one evaluation per
-        // iteration: lanes whose lists/clusters differ in length stay converged
-        int j = 0, je = 0;
-        while (true) {
-            while (j >= je && cur < end) {
-                const int k = g.list[cur++];
-                if (clusterSkipped(s.clusters[k], p, d)) {
-                    if (ST) ++c->cs;
-                    continue;
-                }
-                j = s.cstart[k];
-                je = s.cstart[k + 1];
-                if (ST) {
-                    ++c->cv;
-                    c->pe += je - j;
-                }
-            }
-            if (j >= je) break;
+        // the cell's candidate primitives, one evaluation per iteration
+        const int b = g.start[cell], e = g.start[cell + 1];
+        if (ST) c->pe += e - b;
+        for (int i = b; i < e; ++i) {
+            const int j = g.list[i];
             if (ST) {
                 ++c->ek[s.prims[j].kind];
                 c->ek[5] += s.prims[j].identity ? 0 : 1;
@@ -343,7 +329,6 @@ __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int*
                 d = pd;
                 own = j;
             }
-            ++j;
         }
     } else {
         // off the grid: superclusters, then the unbounded clusters

@@ -133,7 +133,7 @@ struct Ctx {
     GridDev grid{};
     long long gridEntries = 0;
     DBuf<int> gridStart, gridList, gridCounts;
-    DBuf<double> gridU, superBox;
+    DBuf<double> gridU, superBox, primBox;
     DBuf<int> superStart, superList;
     // probes
     std::vector<CascadeHost> cascades;
@@ -169,7 +169,7 @@ struct Ctx {
         prim64.free(); prim32.free(); cl64.free(); cl32.free(); cstart.free(); orig.free();
         albedo.free(); emission.free(); lights.free();
         gridStart.free(); gridList.free(); gridCounts.free(); gridU.free();
-        superBox.free(); superStart.free(); superList.free();
+        superBox.free(); superStart.free(); superList.free(); primBox.free();
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
         records.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
@@ -372,7 +372,44 @@ void fillPrim(DPrim<float>& d, const sdfgi_prim& s) {
 }
 
 // Build the candidate-cluster grid over the bounded clusters (exact; see GridDev).
-void buildGrid(Ctx* c, const sdfgi_cluster* clusters, int n) {
+// Conservative world AABB of a primitive's surface (primitiveAabb, primitives.hpp:112-151),
+// widened by a small relative margin; planes are unbounded (+-inf).
+void primAabb(const sdfgi_prim& s, double* out) {
+    double lo[3], hi[3];
+    auto fromHalf = [&](double hx, double hy, double hz) {
+        for (int i = 0; i < 3; ++i) {
+            double e = std::fabs(s.rot[3 * i]) * hx + std::fabs(s.rot[3 * i + 1]) * hy + std::fabs(s.rot[3 * i + 2]) * hz;
+            lo[i] = s.trans[i] - e;
+            hi[i] = s.trans[i] + e;
+        }
+    };
+    switch (s.kind) {
+        case SDFGI_SPHERE:
+            for (int i = 0; i < 3; ++i) {
+                lo[i] = s.trans[i] - s.size[0];
+                hi[i] = s.trans[i] + s.size[0];
+            }
+            break;
+        case SDFGI_BOX: fromHalf(s.size[0], s.size[1], s.size[2]); break;
+        case SDFGI_CYLINDER: fromHalf(s.size[0], s.size[0], s.size[1]); break;
+        case SDFGI_CAPSULE:
+            for (int i = 0; i < 3; ++i) {
+                double a = s.rot[3 * i + 2] * s.size[1];  // R * (0, 0, h)
+                lo[i] = s.trans[i] - std::fabs(a) - s.size[0];
+                hi[i] = s.trans[i] + std::fabs(a) + s.size[0];
+            }
+            break;
+        default:
+            for (int i = 0; i < 6; ++i) out[i] = i < 3 ? -INFINITY : INFINITY;
+            return;
+    }
+    for (int i = 0; i < 3; ++i) {
+        out[i] = lo[i] - (1e-7 * (std::fabs(lo[i]) + 1.0));
+        out[3 + i] = hi[i] + (1e-7 * (std::fabs(hi[i]) + 1.0));
+    }
+}
+
+void buildGrid(Ctx* c, const sdfgi_prim* prims, const int32_t* member_idx, const sdfgi_cluster* clusters, int n) {
     c->haveGrid = false;
     c->gridEntries = 0;
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
@@ -424,6 +461,12 @@ void buildGrid(Ctx* c, const sdfgi_cluster* clusters, int n) {
     c->gridU.alloc(ncells);
     c->gridCounts.alloc(ncells);
     c->gridStart.alloc(ncells + 1);
+    {
+        std::vector<double> boxes(6 * static_cast<size_t>(c->nPrims));
+        for (int j = 0; j < c->nPrims; ++j) primAabb(prims[member_idx[j]], &boxes[6 * static_cast<size_t>(j)]);
+        c->primBox.upload(boxes.data(), boxes.size(), c->stream);
+    }
+    p.primBox = c->primBox.p;
     p.U = c->gridU.p;
     p.counts = c->gridCounts.p;
     launch_grid_bound(p, static_cast<int>(ncells), c->stream);
@@ -843,7 +886,7 @@ int sdfgi_scene_upload(void* ctx, const sdfgi_prim* prims, int n_prims, const sd
         c->nLights = n_lights;
         for (int k = 0; k < 3; ++k) c->sky[k] = sky[k];
         c->haveScene = true;
-        buildGrid(c, clusters, n_clusters);
+        buildGrid(c, prims, member_idx, clusters, n_clusters);
     });
 }
 
