@@ -1,0 +1,897 @@
+/*
+ * sdfgi_oracle.c — TEST INFRASTRUCTURE (see sdfgi_oracle.h). Plain C99 restatement
+ * of the reference's probe path, one scalar function per reference function, in
+ * the reference's operation order (compile with -ffp-contract=off).
+ */
+#include "sdfgi_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORA_PI 3.14159265358979323846
+#define ORA_INF INFINITY
+#define MAXCAS 8
+
+/* ------------------------------------------------------------------ vec.hpp */
+typedef struct { double x, y, z; } v3;
+typedef struct { double x, y; } v2;
+
+static inline v3 V(double x, double y, double z) { v3 r = {x, y, z}; return r; }
+static inline v3 add(v3 a, v3 b) { return V(a.x + b.x, a.y + b.y, a.z + b.z); }
+static inline v3 sub(v3 a, v3 b) { return V(a.x - b.x, a.y - b.y, a.z - b.z); }
+static inline v3 muls(v3 a, double s) { return V(a.x * s, a.y * s, a.z * s); }
+static inline v3 divs(v3 a, double s) { return V(a.x / s, a.y / s, a.z / s); }
+static inline v3 mulv(v3 a, v3 b) { return V(a.x * b.x, a.y * b.y, a.z * b.z); }
+static inline double dot(v3 a, v3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }  /* vec.hpp:50 */
+static inline double len(v3 v) { return sqrt(dot(v, v)); }
+static inline v3 norm(v3 v) { return divs(v, len(v)); }                            /* vec.hpp:56 */
+static inline v3 lerp3(v3 a, v3 b, double t) { return add(a, muls(sub(b, a), t)); } /* vec.hpp:64 */
+/* std::min / std::max / std::clamp */
+static inline double smin(double a, double b) { return (b < a) ? b : a; }
+static inline double smax(double a, double b) { return (a < b) ? b : a; }
+static inline double sclamp(double v, double lo, double hi) { return (v < lo) ? lo : ((hi < v) ? hi : v); }
+static inline int iclamp(int v, int lo, int hi) { return (v < lo) ? lo : ((hi < v) ? hi : v); }
+static inline double maxc(v3 v) { return smax(v.x, smax(v.y, v.z)); }
+
+/* ------------------------------------------------------------------ rng.hpp */
+static inline uint64_t hashU64(uint64_t x) { /* rng.hpp:10-15 */
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e9b5ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+static inline uint64_t hashCombine(uint64_t a, uint64_t b) { /* rng.hpp:17 */
+    return hashU64(a ^ (b + 0x9e3779b97f4a7c15ull + (a << 6) + (a >> 2)));
+}
+typedef struct { uint64_t s; } rng_t;
+static inline rng_t rng_key(uint64_t key) { rng_t r; r.s = hashU64(key); return r; } /* rng.hpp:28 */
+static inline uint64_t rng_next(rng_t* r) {                                          /* rng.hpp:31-38 */
+    r->s += 0x9e3779b97f4a7c15ull;
+    uint64_t z = r->s;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e9b5ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+static inline double rng_uniform(rng_t* r) { return (double)(rng_next(r) >> 11) * 0x1.0p-53; } /* rng.hpp:41 */
+
+/* ---------------------------------------------------------------- scene state */
+typedef struct {
+    int res[3], level, base, oct;
+    double spacing, origin[3];
+} cascade_t;
+
+typedef struct {
+    v3 rest, pos, last;
+    int reject, alive, last_frame;
+} probe_t;
+
+struct ora_stage {
+    int np, nk, nl, nm;
+    sdfgi_prim* prims;
+    sdfgi_cluster* clusters;
+    int32_t* mstart;
+    int32_t* midx;
+    sdfgi_light* lights;
+    v3 sky;
+    int ncas, nprobes, oct;
+    cascade_t cas[MAXCAS];
+    probe_t* probes;
+    float* atlas[2];
+    int front;
+};
+
+typedef struct { uint64_t q, cv, cs, pe, steps, sphere, shadow, vis; } stats_t;
+
+/* ------------------------------------------------------------ primitives.hpp */
+static double evalPrimitive(const sdfgi_prim* pr, v3 p) { /* primitives.hpp:73-86 */
+    const double* m = pr->rot;
+    v3 q = sub(p, V(pr->trans[0], pr->trans[1], pr->trans[2]));
+    if (!(m[0] == 1.0 && m[4] == 1.0 && m[8] == 1.0))
+        q = V(m[0] * q.x + m[3] * q.y + m[6] * q.z, m[1] * q.x + m[4] * q.y + m[7] * q.z,
+              m[2] * q.x + m[5] * q.y + m[8] * q.z); /* transposeMul, vec.hpp:113-117 */
+    switch (pr->kind) {
+        case SDFGI_SPHERE: return len(q) - pr->size[0];                        /* :42 */
+        case SDFGI_BOX: {                                                      /* :44-49 */
+            v3 a = V(fabs(q.x) - pr->size[0], fabs(q.y) - pr->size[1], fabs(q.z) - pr->size[2]);
+            double outside = len(V(smax(a.x, 0.0), smax(a.y, 0.0), smax(a.z, 0.0)));
+            double inside = smin(maxc(a), 0.0);
+            return outside + inside;
+        }
+        case SDFGI_PLANE: return q.z;                                          /* :51 */
+        case SDFGI_CYLINDER: {                                                 /* :53-60 */
+            double dx = sqrt(q.x * q.x + q.y * q.y) - pr->size[0];
+            double dy = fabs(q.z) - pr->size[1];
+            double outside = sqrt(smax(dx, 0.0) * smax(dx, 0.0) + smax(dy, 0.0) * smax(dy, 0.0));
+            double inside = smin(smax(dx, dy), 0.0);
+            return outside + inside;
+        }
+        default: {                                                              /* :62-65 */
+            v3 c = V(q.x, q.y, q.z - sclamp(q.z, -pr->size[1], pr->size[1]));
+            return len(c) - pr->size[0];
+        }
+    }
+}
+
+static v3 evalGradient(const sdfgi_prim* pr, v3 p) { /* primitives.hpp:96-108, h = 1e-3 */
+    const double h = 1e-3;
+    v3 g = V(evalPrimitive(pr, V(p.x + h, p.y, p.z)) - evalPrimitive(pr, V(p.x - h, p.y, p.z)),
+             evalPrimitive(pr, V(p.x, p.y + h, p.z)) - evalPrimitive(pr, V(p.x, p.y - h, p.z)),
+             evalPrimitive(pr, V(p.x, p.y, p.z + h)) - evalPrimitive(pr, V(p.x, p.y, p.z - h)));
+    double n = len(g);
+    if (n < 1e-6 * 2 * h) return V(1, 0, 0);
+    return divs(g, n);
+}
+
+/* ------------------------------------------------------------------ scene.hpp */
+/* queryCore scalar path (scene.hpp:214-332, the #else branch :293-305) */
+static double query(const ora_stage* s, v3 p, double initD, stats_t* st, int* owner) {
+    double d = initD;
+    int own = -1;
+    if (st) ++st->q;
+    for (int c = 0; c < s->nk; ++c) {
+        const sdfgi_cluster* cl = &s->clusters[c];
+        double dx = smax(smax(cl->lo[0] - p.x, p.x - cl->hi[0]), 0.0);
+        double dy = smax(smax(cl->lo[1] - p.y, p.y - cl->hi[1]), 0.0);
+        double dz = smax(smax(cl->lo[2] - p.z, p.z - cl->hi[2]), 0.0);
+        double boxSq = dx * dx + dy * dy + dz * dz;
+        if (!cl->unbounded && (d > 0 ? boxSq >= d * d : boxSq > 0)) {
+            if (st) ++st->cs;
+            continue;
+        }
+        int end = s->mstart[c + 1];
+        if (st) {
+            ++st->cv;
+            st->pe += (uint64_t)(end - s->mstart[c]);
+        }
+        for (int m = s->mstart[c]; m < end; ++m) {
+            int idx = s->midx[m];
+            double pd = evalPrimitive(&s->prims[idx], p);
+            if (pd < d) {
+                d = pd;
+                own = idx;
+            }
+        }
+    }
+    if (owner) *owner = own;
+    return d;
+}
+
+typedef struct {
+    int converged, miss, prim, steps;
+    double t;
+    v3 pos, normal;
+} hit_t;
+
+/* sphereTrace, scene.hpp:391-435 */
+static hit_t sphereTrace(const ora_stage* s, v3 o, v3 dir, double tMax, double eps, int maxSteps, stats_t* st,
+                         double startBound) {
+    if (st) ++st->sphere;
+    hit_t h;
+    memset(&h, 0, sizeof(h));
+    h.normal = V(0, 0, 1);
+    h.prim = -1;
+    double t = 0, lastD = startBound * 0.5;
+    for (int step = 0; step < maxSteps; ++step) {
+        if (st) ++st->steps;
+        v3 p = add(o, muls(dir, t));
+        double d = query(s, p, 2 * lastD, st, NULL);
+        if (d < eps) {
+            int owner = -1;
+            d = query(s, p, d + 1e-9, st, &owner);
+            for (int i = 0; i < 8 && fabs(d) > 0.25 * eps; ++i) {
+                t += d;
+                p = add(o, muls(dir, t));
+                int o2 = -1;
+                d = query(s, p, 2 * fabs(d) + 1e-9, st, &o2);
+                if (o2 >= 0) owner = o2;
+            }
+            h.converged = 1;
+            h.t = t;
+            h.pos = p;
+            h.prim = owner;
+            h.steps = step + 1;
+            if (owner >= 0) h.normal = evalGradient(&s->prims[owner], p);
+            return h;
+        }
+        if (d >= tMax - t) {
+            h.miss = 1;
+            h.steps = step + 1;
+            return h;
+        }
+        t += d;
+        lastD = d;
+    }
+    h.miss = 2;
+    h.steps = maxSteps;
+    return h;
+}
+
+/* softShadowTrace, scene.hpp:459-476 */
+static double softShadowTrace(const ora_stage* s, v3 o, v3 dir, double tMin, double tMax, double k, stats_t* st,
+                              int maxSteps) {
+    const double minStep = 5e-4;
+    if (st) ++st->shadow;
+    double v = 1.0, t = tMin, lastD = ORA_INF;
+    for (int step = 0; step < maxSteps && t < tMax; ++step) {
+        if (st) ++st->steps;
+        double d = query(s, add(o, muls(dir, t)), lastD == ORA_INF ? ORA_INF : 2 * lastD, st, NULL);
+        v = smin(v, sclamp(k * d / t, 0.0, 1.0));
+        if (v < 1e-3) return 0.0;
+        t += smax(d, minStep);
+        lastD = smax(d, minStep);
+    }
+    return v;
+}
+
+/* ------------------------------------------------------------- octahedral.hpp */
+static inline double signNotZero(double v) { return v >= 0.0 ? 1.0 : -1.0; }
+static v2 octEncode(v3 d) { /* octahedral.hpp:13-24 */
+    double n = fabs(d.x) + fabs(d.y) + fabs(d.z);
+    double px = d.x / n, py = d.y / n;
+    if (d.z < 0) {
+        double ox = (1.0 - fabs(py)) * signNotZero(px);
+        double oy = (1.0 - fabs(px)) * signNotZero(py);
+        px = ox;
+        py = oy;
+    }
+    v2 r = {px * 0.5 + 0.5, py * 0.5 + 0.5};
+    return r;
+}
+static v3 octDecode(v2 uv) { /* octahedral.hpp:26-36 */
+    double fx = uv.x * 2.0 - 1.0, fy = uv.y * 2.0 - 1.0;
+    v3 n = V(fx, fy, 1.0 - fabs(fx) - fabs(fy));
+    if (n.z < 0) {
+        double t = -n.z;
+        n.x += n.x >= 0 ? -t : t;
+        n.y += n.y >= 0 ? -t : t;
+    }
+    return norm(n);
+}
+
+/* ------------------------------------------------------------------ atlas.hpp */
+static inline size_t tileFloats(int oct) { return (size_t)(oct + 2) * (oct + 2) * 3; }
+static inline float* at(float* a, int oct, int probe, int x, int y) {
+    int T = oct + 2;
+    return a + (((size_t)probe * T + y) * T + x) * 3; /* atlas.hpp:119-124 */
+}
+static v3 sampleBilinear(const float* a, int oct, int probe, v2 uv) { /* atlas.hpp:59-75 */
+    int T = oct + 2;
+    double cx = sclamp(uv.x, 0.0, 1.0) * oct + 1.0;
+    double cy = sclamp(uv.y, 0.0, 1.0) * oct + 1.0;
+    int x0 = (int)floor(cx - 0.5), y0 = (int)floor(cy - 0.5);
+    double tx = cx - 0.5 - x0, ty = cy - 0.5 - y0;
+    x0 = iclamp(x0, 0, T - 2);
+    y0 = iclamp(y0, 0, T - 2);
+    const float* p00 = at((float*)a, oct, probe, x0, y0);
+    const float* p10 = at((float*)a, oct, probe, x0 + 1, y0);
+    const float* p01 = at((float*)a, oct, probe, x0, y0 + 1);
+    const float* p11 = at((float*)a, oct, probe, x0 + 1, y0 + 1);
+    v3 A = lerp3(V(p00[0], p00[1], p00[2]), V(p10[0], p10[1], p10[2]), tx);
+    v3 B = lerp3(V(p01[0], p01[1], p01[2]), V(p11[0], p11[1], p11[2]), tx);
+    return lerp3(A, B, ty);
+}
+static void copyTexel(float* a, int oct, int probe, int dx, int dy, int sx, int sy) {
+    memcpy(at(a, oct, probe, dx, dy), at(a, oct, probe, sx, sy), 3 * sizeof(float));
+}
+static void fillBorder(float* a, int oct, int probe) { /* atlas.hpp:44-56 */
+    int r = oct;
+    for (int i = 1; i <= r; ++i) {
+        copyTexel(a, oct, probe, i, 0, r + 1 - i, 1);
+        copyTexel(a, oct, probe, i, r + 1, r + 1 - i, r);
+        copyTexel(a, oct, probe, 0, i, 1, r + 1 - i);
+        copyTexel(a, oct, probe, r + 1, i, r, r + 1 - i);
+    }
+    copyTexel(a, oct, probe, 0, 0, r, r);
+    copyTexel(a, oct, probe, r + 1, 0, 1, r);
+    copyTexel(a, oct, probe, 0, r + 1, r, 1);
+    copyTexel(a, oct, probe, r + 1, r + 1, 1, 1);
+}
+
+/* ------------------------------------------------------------- mean_value.hpp */
+static int mvcWeightsHex(const v3* corners, v3 x, double* w) { /* mean_value.hpp:16-107 */
+    static const int faces[6][4] = {{0, 2, 3, 1}, {4, 5, 7, 6}, {0, 1, 5, 4}, {2, 6, 7, 3}, {0, 4, 6, 2}, {1, 3, 7, 5}};
+    const double eps = 1e-10;
+    double dist[8];
+    v3 unit[8];
+    for (int i = 0; i < 8; ++i) w[i] = 0.0;
+    for (int i = 0; i < 8; ++i) {
+        v3 v = sub(corners[i], x);
+        dist[i] = len(v);
+        if (dist[i] < eps) {
+            w[i] = 1.0;
+            return 1;
+        }
+        unit[i] = divs(v, dist[i]);
+    }
+    int any = 0;
+    for (int f = 0; f < 6; ++f) {
+        int tris[2][3] = {{faces[f][0], faces[f][1], faces[f][2]}, {faces[f][0], faces[f][2], faces[f][3]}};
+        for (int tr = 0; tr < 2; ++tr) {
+            const int* tri = tris[tr];
+            double d[3], theta[3], c[3], sn[3];
+            v3 u[3];
+            for (int i = 0; i < 3; ++i) {
+                d[i] = dist[tri[i]];
+                u[i] = unit[tri[i]];
+            }
+            for (int i = 0; i < 3; ++i) {
+                double l = len(sub(u[(i + 1) % 3], u[(i + 2) % 3]));
+                theta[i] = 2.0 * asin(sclamp(l * 0.5, 0.0, 1.0));
+            }
+            double h = (theta[0] + theta[1] + theta[2]) * 0.5;
+            if (ORA_PI - h < 1e-8) {
+                double total = 0, ww[3];
+                for (int i = 0; i < 8; ++i) w[i] = 0.0;
+                for (int i = 0; i < 3; ++i) {
+                    ww[i] = sin(theta[i]) * d[(i + 1) % 3] * d[(i + 2) % 3];
+                    total += ww[i];
+                }
+                if (total < eps) return 0;
+                for (int i = 0; i < 3; ++i) w[tri[i]] = ww[i] / total;
+                return 1;
+            }
+            v3 cr = V(u[1].y * u[2].z - u[1].z * u[2].y, u[1].z * u[2].x - u[1].x * u[2].z,
+                      u[1].x * u[2].y - u[1].y * u[2].x); /* cross, vec.hpp:51-53 */
+            double det = dot(u[0], cr);
+            double sign = det >= 0 ? 1.0 : -1.0;
+            int skip = 0;
+            for (int i = 0; i < 3; ++i) {
+                double denom = sin(theta[(i + 1) % 3]) * sin(theta[(i + 2) % 3]);
+                if (fabs(denom) < eps) {
+                    skip = 1;
+                    break;
+                }
+                c[i] = (2.0 * sin(h) * sin(h - theta[i])) / denom - 1.0;
+                sn[i] = sign * sqrt(smax(0.0, 1.0 - c[i] * c[i]));
+                if (fabs(sn[i]) <= eps) {
+                    skip = 1;
+                    break;
+                }
+            }
+            if (skip) continue;
+            for (int i = 0; i < 3; ++i) {
+                double wi = (theta[i] - c[(i + 1) % 3] * theta[(i + 2) % 3] - c[(i + 2) % 3] * theta[(i + 1) % 3]) /
+                            (d[i] * sin(theta[(i + 1) % 3]) * sn[(i + 2) % 3]);
+                w[tri[i]] += wi;
+                any = 1;
+            }
+        }
+    }
+    if (!any) return 0;
+    double total = 0;
+    for (int i = 0; i < 8; ++i) total += w[i];
+    if (fabs(total) < eps || !isfinite(total)) return 0;
+    for (int i = 0; i < 8; ++i) w[i] /= total;
+    return 1;
+}
+
+/* ------------------------------------------------------------ probe_volume.hpp */
+typedef struct {
+    int cascade; /* slot */
+    int probe[8];
+    double w[8];
+    int count, sky;
+} stencil_t;
+
+/* interpolationStencil, probe_volume.hpp:224-310 */
+static stencil_t interpolationStencil(const ora_stage* s, v3 point, double frac) {
+    stencil_t st;
+    memset(&st, 0, sizeof(st));
+    int chosen = -1, cell[3] = {0, 0, 0}, containing = 0;
+    for (int ci = 0; ci < s->ncas; ++ci) {
+        const cascade_t* c = &s->cas[ci];
+        v3 f = divs(sub(point, V(c->origin[0], c->origin[1], c->origin[2])), c->spacing);
+        int ix = (int)floor(f.x), iy = (int)floor(f.y), iz = (int)floor(f.z);
+        int inside = ix >= 0 && ix + 1 < c->res[0] && iy >= 0 && iy + 1 < c->res[1] && iz >= 0 && iz + 1 < c->res[2];
+        if (!inside) continue;
+        ++containing;
+        if (chosen < 0 || c->spacing < s->cas[chosen].spacing) {
+            chosen = ci;
+            cell[0] = ix;
+            cell[1] = iy;
+            cell[2] = iz;
+        }
+    }
+    int insideCoarser = containing > 1;
+    if (chosen < 0) {
+        st.sky = 1;
+        return st;
+    }
+    const cascade_t* c = &s->cas[chosen];
+    v3 f = divs(sub(point, V(c->origin[0], c->origin[1], c->origin[2])), c->spacing);
+    double tx = f.x - cell[0], ty = f.y - cell[1], tz = f.z - cell[2];
+    v3 corners[8];
+    int pidx[8];
+    double maxDisp = 0, w[8];
+    for (int k = 0; k < 8; ++k) {
+        int ix = cell[0] + (k & 1), iy = cell[1] + ((k >> 1) & 1), iz = cell[2] + ((k >> 2) & 1);
+        int pi = ix + c->res[0] * (iy + c->res[1] * iz);
+        pidx[k] = pi;
+        const probe_t* pr = &s->probes[c->base + pi];
+        corners[k] = pr->pos;
+        maxDisp = smax(maxDisp, len(sub(pr->pos, pr->rest)));
+    }
+    int boundary = insideCoarser && (cell[0] == 0 || cell[0] + 2 == c->res[0] || cell[1] == 0 ||
+                                     cell[1] + 2 == c->res[1] || cell[2] == 0 || cell[2] + 2 == c->res[2]);
+    int wantMvc = maxDisp > frac * c->spacing || boundary, haveMvc = 0;
+    if (wantMvc) {
+        haveMvc = mvcWeightsHex(corners, point, w);
+        if (haveMvc)
+            for (int k = 0; k < 8; ++k) w[k] = smax(0.0, w[k]);
+    }
+    if (!haveMvc)
+        for (int k = 0; k < 8; ++k) {
+            double wx = (k & 1) ? tx : 1 - tx;
+            double wy = ((k >> 1) & 1) ? ty : 1 - ty;
+            double wz = ((k >> 2) & 1) ? tz : 1 - tz;
+            w[k] = wx * wy * wz;
+        }
+    double sum = 0;
+    for (int k = 0; k < 8; ++k) {
+        if (!s->probes[c->base + pidx[k]].alive) w[k] = 0;
+        sum += w[k];
+    }
+    if (sum <= 1e-12) {
+        st.sky = 1;
+        return st;
+    }
+    for (int k = 0; k < 8; ++k) {
+        st.probe[k] = pidx[k];
+        st.w[k] = w[k] / sum;
+    }
+    st.cascade = chosen;
+    st.count = 8;
+    return st;
+}
+
+/* ------------------------------------------------------------ probe_update.hpp */
+/* sampleBounceIrradiance, probe_update.hpp:63-92; prev = front atlas */
+static int sampleBounce(const ora_stage* s, v3 pos, v3 normal, double frac, v3* out) {
+    if (s->ncas <= 0) return 0;
+    stencil_t st = interpolationStencil(s, pos, frac);
+    if (st.sky || st.count == 0) return 0;
+    const cascade_t* c = &s->cas[st.cascade];
+    double wsum = 0, w[8] = {0};
+    for (int i = 0; i < st.count; ++i) {
+        if (st.w[i] <= 0) continue;
+        v3 toProbe = sub(s->probes[c->base + st.probe[i]].pos, pos);
+        double l = len(toProbe);
+        double facing = l > 1e-9 ? dot(divs(toProbe, l), normal) : 1.0;
+        double backface = (facing + 1.0) * 0.5;
+        w[i] = st.w[i] * backface * backface;
+        wsum += w[i];
+    }
+    if (wsum <= 1e-12) return 0;
+    v3 acc = V(0, 0, 0);
+    v2 uv = octEncode(normal);
+    for (int i = 0; i < st.count; ++i) {
+        if (w[i] <= 0) continue;
+        acc = add(acc, muls(sampleBilinear(s->atlas[s->front], s->oct, c->base + st.probe[i], uv), w[i] / wsum));
+    }
+    *out = acc;
+    return 1;
+}
+
+/* directIrradiance, probe_update.hpp:97-132 */
+static v3 directIrradiance(const ora_stage* s, v3 pos, v3 normal, const sdfgi_cfg* cfg, stats_t* st) {
+    v3 total = V(0, 0, 0);
+    for (int li = 0; li < s->nl; ++li) {
+        const sdfgi_light* L = &s->lights[li];
+        v3 dir, unshadowed, I = V(L->intensity[0], L->intensity[1], L->intensity[2]);
+        double tMax;
+        if (L->kind == SDFGI_LIGHT_POINT) {
+            v3 toLight = sub(V(L->position[0], L->position[1], L->position[2]), pos);
+            double r2 = dot(toLight, toLight);
+            if (r2 < 1e-12) continue;
+            double r = sqrt(r2);
+            dir = divs(toLight, r);
+            double cosT = dot(normal, dir);
+            if (cosT <= 0) continue;
+            unshadowed = muls(I, cosT / r2);
+            tMax = r;
+        } else if (L->kind == SDFGI_LIGHT_DIRECTIONAL) {
+            dir = V(-L->direction[0], -L->direction[1], -L->direction[2]);
+            double cosT = dot(normal, dir);
+            if (cosT <= 0) continue;
+            unshadowed = muls(I, cosT);
+            tMax = cfg->ray_tmax;
+        } else {
+            continue;
+        }
+        double cosT = dot(normal, dir);
+        double bias = 2.0 * cfg->surface_epsilon / smax(0.1, cosT);
+        double vis = 1.0;
+        if (tMax - bias > bias)
+            vis = softShadowTrace(s, add(pos, muls(normal, bias)), dir, bias, tMax - bias, cfg->shadow_k, st,
+                                  (int)cfg->shadow_steps);
+        total = add(total, muls(unshadowed, vis));
+    }
+    return total;
+}
+
+/* shadeHit, probe_update.hpp:136-149 */
+static v3 shadeHit(const ora_stage* s, const hit_t* h, const sdfgi_cfg* cfg, stats_t* st) {
+    if (h->prim < 0) return s->sky;
+    const sdfgi_prim* pr = &s->prims[h->prim];
+    v3 brdf = divs(V(pr->albedo[0], pr->albedo[1], pr->albedo[2]), ORA_PI);
+    v3 radiance = add(V(pr->emission[0], pr->emission[1], pr->emission[2]),
+                      mulv(brdf, directIrradiance(s, h->pos, h->normal, cfg, st)));
+    if (cfg->bounce_coeff > 0) {
+        v3 prev;
+        if (sampleBounce(s, h->pos, h->normal, cfg->mvc_relocation_frac, &prev))
+            radiance = add(radiance, mulv(brdf, muls(prev, cfg->bounce_coeff)));
+    }
+    return radiance;
+}
+
+/* sampleDirections, sampling.hpp:23-31 (randomRotation rng.hpp:72-90) */
+static void sampleDirections(int n, int frame, uint64_t key, uint64_t seed, int rotatePerFrame, v3* dirs) {
+    rng_t r = rng_key(hashCombine(hashCombine(hashCombine(seed, rotatePerFrame ? (uint64_t)(int64_t)frame : 0xf1b0u),
+                                              key),
+                                  0x5df6d1u));
+    double u1 = rng_uniform(&r), u2 = rng_uniform(&r), u3 = rng_uniform(&r);
+    double a = sqrt(1.0 - u1), b = sqrt(u1);
+    double qx = a * sin(2 * ORA_PI * u2), qy = a * cos(2 * ORA_PI * u2);
+    double qz = b * sin(2 * ORA_PI * u3), qw = b * cos(2 * ORA_PI * u3);
+    double m[9] = {1 - 2 * (qy * qy + qz * qz), 2 * (qx * qy - qz * qw), 2 * (qx * qz + qy * qw),
+                   2 * (qx * qy + qz * qw),     1 - 2 * (qx * qx + qz * qz), 2 * (qy * qz - qx * qw),
+                   2 * (qx * qz - qy * qw),     2 * (qy * qz + qx * qw), 1 - 2 * (qx * qx + qy * qy)};
+    const double golden = ORA_PI * (3.0 - sqrt(5.0));
+    for (int i = 0; i < n; ++i) { /* sphericalFibonacci, sampling.hpp:11-17 */
+        double z = 1.0 - (2.0 * i + 1.0) / n;
+        double rr = sqrt(smax(0.0, 1.0 - z * z));
+        double phi = golden * i;
+        v3 v = V(rr * cos(phi), rr * sin(phi), z);
+        dirs[i] = V(m[0] * v.x + m[1] * v.y + m[2] * v.z, m[3] * v.x + m[4] * v.y + m[5] * v.z,
+                    m[6] * v.x + m[7] * v.y + m[8] * v.z);
+    }
+}
+
+static inline uint64_t probeKey(int cascade, int index) { /* probe_update.hpp:156-159 */
+    return hashCombine((uint64_t)cascade + 0x9e1du, (uint64_t)index);
+}
+
+/* updateProbe, probe_update.hpp:166-211, writing the back atlas `curr` */
+static void updateProbe(ora_stage* s, int slot, int pi, float* curr, const sdfgi_cfg* cfg, int frame,
+                        stats_t* st, double* maxDelta, int* raysOut) {
+    const cascade_t* c = &s->cas[slot];
+    probe_t* probe = &s->probes[c->base + pi];
+    int N = (int)cfg->n_rays_full;
+    int rays = probe->reject ? N * 2 : N;
+    v3* dirs = (v3*)malloc(sizeof(v3) * rays);
+    v3* rad = (v3*)malloc(sizeof(v3) * rays);
+    sampleDirections(rays, frame, probeKey(c->level, pi), cfg->seed, (int)cfg->rotate_per_frame, dirs);
+    for (int i = 0; i < rays; ++i) {
+        hit_t h = sphereTrace(s, probe->pos, dirs[i], cfg->ray_tmax, cfg->surface_epsilon, (int)cfg->max_trace_steps,
+                              st, ORA_INF);
+        rad[i] = h.converged ? shadeHit(s, &h, cfg, st) : s->sky;
+    }
+    *raysOut = rays;
+    double alpha = probe->reject ? 1.0 : sclamp((1.0 - cfg->hysteresis) * rays / cfg->n_rays_full, cfg->alpha_min, 1.0);
+    int r = s->oct;
+    double md = 0;
+    for (int y = 0; y < r; ++y)
+        for (int x = 0; x < r; ++x) {
+            v3 D = octDecode((v2){(x + 0.5) / r, (y + 0.5) / r}); /* octTexelDir */
+            v3 acc = V(0, 0, 0);                                  /* convolveIrradiance :25-34 */
+            for (int i = 0; i < rays; ++i) {
+                double w = dot(D, dirs[i]);
+                if (w > 0) acc = add(acc, muls(rad[i], w));
+            }
+            v3 fresh = muls(acc, 4.0 * ORA_PI / (double)rays);
+            float* t = at(curr, s->oct, c->base + pi, x + 1, y + 1);
+            v3 old = V(t[0], t[1], t[2]);
+            v3 bl = lerp3(old, fresh, alpha);
+            v3 df = sub(bl, old);
+            md = smax(md, maxc(V(fabs(df.x), fabs(df.y), fabs(df.z))));
+            t[0] = (float)bl.x;
+            t[1] = (float)bl.y;
+            t[2] = (float)bl.z;
+        }
+    fillBorder(curr, s->oct, c->base + pi);
+    probe->reject = 0;
+    probe->last_frame = frame;
+    *maxDelta = md;
+    free(dirs);
+    free(rad);
+}
+
+/* ================================================================== C API */
+ora_stage* ora_create(const sdfgi_prim* prims, int n_prims, const sdfgi_cluster* clusters, int n_clusters,
+                      const int32_t* member_start, const int32_t* member_idx, const sdfgi_light* lights,
+                      int n_lights, const double sky[3]) {
+    ora_stage* s = (ora_stage*)calloc(1, sizeof(ora_stage));
+    s->np = n_prims;
+    s->nk = n_clusters;
+    s->nl = n_lights;
+    s->nm = n_clusters ? member_start[n_clusters] : 0;
+    s->prims = (sdfgi_prim*)malloc(sizeof(sdfgi_prim) * (n_prims + 1));
+    memcpy(s->prims, prims, sizeof(sdfgi_prim) * n_prims);
+    s->clusters = (sdfgi_cluster*)malloc(sizeof(sdfgi_cluster) * (n_clusters + 1));
+    memcpy(s->clusters, clusters, sizeof(sdfgi_cluster) * n_clusters);
+    s->mstart = (int32_t*)malloc(4 * (n_clusters + 1));
+    memcpy(s->mstart, member_start, 4 * (n_clusters + 1));
+    s->midx = (int32_t*)malloc(4 * (s->nm + 1));
+    memcpy(s->midx, member_idx, 4 * s->nm);
+    s->lights = (sdfgi_light*)malloc(sizeof(sdfgi_light) * (n_lights + 1));
+    memcpy(s->lights, lights, sizeof(sdfgi_light) * n_lights);
+    s->sky = V(sky[0], sky[1], sky[2]);
+    s->oct = 8;
+    return s;
+}
+
+void ora_destroy(ora_stage* s) {
+    if (!s) return;
+    free(s->prims);
+    free(s->clusters);
+    free(s->mstart);
+    free(s->midx);
+    free(s->lights);
+    free(s->probes);
+    free(s->atlas[0]);
+    free(s->atlas[1]);
+    free(s);
+}
+
+int ora_add_cascade(ora_stage* s, int level, int rx, int ry, int rz, double spacing, const double origin[3],
+                    int oct_res) {
+    if (s->ncas >= MAXCAS || (s->ncas && oct_res != s->oct)) return 1;
+    cascade_t* c = &s->cas[s->ncas];
+    c->res[0] = rx;
+    c->res[1] = ry;
+    c->res[2] = rz;
+    c->level = level;
+    c->spacing = spacing;
+    c->oct = oct_res;
+    for (int k = 0; k < 3; ++k) c->origin[k] = origin[k];
+    c->base = s->nprobes;
+    int n = rx * ry * rz;
+    s->oct = oct_res;
+    s->probes = (probe_t*)realloc(s->probes, sizeof(probe_t) * (s->nprobes + n));
+    for (int iz = 0; iz < rz; ++iz)
+        for (int iy = 0; iy < ry; ++iy)
+            for (int ix = 0; ix < rx; ++ix) { /* makeCascade, probe_volume.hpp:66-74 */
+                probe_t* p = &s->probes[c->base + ix + rx * (iy + ry * iz)];
+                p->rest = add(V(origin[0], origin[1], origin[2]), V(ix * spacing, iy * spacing, iz * spacing));
+                p->pos = p->rest;
+                p->last = p->rest;
+                p->reject = 1;
+                p->alive = 1;
+                p->last_frame = -1;
+            }
+    s->nprobes += n;
+    size_t nf = tileFloats(oct_res) * (size_t)s->nprobes;
+    for (int b = 0; b < 2; ++b) {
+        s->atlas[b] = (float*)realloc(s->atlas[b], nf * sizeof(float));
+        memset(s->atlas[b] + tileFloats(oct_res) * c->base, 0, tileFloats(oct_res) * n * sizeof(float));
+    }
+    s->ncas++;
+    return 0;
+}
+
+static void addStats(uint64_t* out, const stats_t* st) {
+    if (!out) return;
+    out[0] += st->q;
+    out[1] += st->cv;
+    out[2] += st->cs;
+    out[3] += st->pe;
+    out[4] += st->steps;
+    out[5] += st->sphere;
+    out[6] += st->shadow;
+    out[7] += st->vis;
+}
+
+int ora_relocate(ora_stage* s, int slot, double th1, double th2, int max_steps, double grad_step, int report[3],
+                 uint64_t stats[8]) { /* updateProbePositions, probe_volume.hpp:99-143 */
+    if (slot < 0 || slot >= s->ncas) return 1;
+    const cascade_t* c = &s->cas[slot];
+    int n = c->res[0] * c->res[1] * c->res[2];
+    int rel = 0, rej = 0, dead = 0;
+    stats_t st;
+    memset(&st, 0, sizeof(st));
+    double budgetTotal = 0.5 * c->spacing;
+    for (int i = 0; i < n; ++i) {
+        probe_t* p = &s->probes[c->base + i];
+        v3 prev = p->pos, pos = p->rest;
+        double d = query(s, pos, ORA_INF, &st, NULL);
+        int alive = 1;
+        if (d < th1) {
+            double budget = budgetTotal, h = grad_step;
+            for (int step = 0; step < max_steps && d < th1 && budget > 0; ++step) {
+                /* sceneGradient, scene.hpp:360-371 */
+                v3 g = V(query(s, V(pos.x + h, pos.y, pos.z), ORA_INF, &st, NULL) -
+                             query(s, V(pos.x - h, pos.y, pos.z), ORA_INF, &st, NULL),
+                         query(s, V(pos.x, pos.y + h, pos.z), ORA_INF, &st, NULL) -
+                             query(s, V(pos.x, pos.y - h, pos.z), ORA_INF, &st, NULL),
+                         query(s, V(pos.x, pos.y, pos.z + h), ORA_INF, &st, NULL) -
+                             query(s, V(pos.x, pos.y, pos.z - h), ORA_INF, &st, NULL));
+                double gn = len(g);
+                v3 dir = gn < 1e-6 * 2 * h ? V(1, 0, 0) : divs(g, gn);
+                double want = smin((th1 - d) * 1.25, budget);
+                pos = add(pos, muls(dir, want));
+                budget -= want;
+                d = query(s, pos, ORA_INF, &st, NULL);
+            }
+            alive = d >= th1;
+            if (alive && len(sub(pos, p->rest)) > 1e-12) ++rel;
+        }
+        if (!alive) {
+            ++dead;
+            p->alive = 0;
+            p->last = prev;
+            p->pos = pos;
+            continue;
+        }
+        p->alive = 1;
+        p->last = prev;
+        p->pos = pos;
+        int hadHistory = p->last_frame >= 0 && !p->reject;
+        if (len(sub(pos, prev)) > th2) {
+            p->reject = 1;
+            if (hadHistory) ++rej;
+        }
+    }
+    if (report) {
+        report[0] = rel;
+        report[1] = rej;
+        report[2] = dead;
+    }
+    addStats(stats, &st);
+    return 0;
+}
+
+typedef struct {
+    ora_stage* s;
+    const sdfgi_cfg* cfg;
+    int frame, slot, stride, worker, workers;
+    double md;
+    int64_t rays, updated;
+    stats_t st;
+} work_t;
+
+/* parallelFor's strided split (parallel.hpp:19-36): worker w owns items w, w+W, ... */
+static void* updateWorker(void* arg) {
+    work_t* w = (work_t*)arg;
+    const cascade_t* c = &w->s->cas[w->slot];
+    int n = c->res[0] * c->res[1] * c->res[2];
+    float* back = w->s->atlas[1 - w->s->front];
+    for (int item = w->worker; item * w->stride < n; item += w->workers) {
+        int i = item * w->stride;
+        if (!w->s->probes[c->base + i].alive) continue; /* pipeline.hpp:141 */
+        double d;
+        int r;
+        updateProbe(w->s, w->slot, i, back, w->cfg, w->frame, &w->st, &d, &r);
+        w->md = smax(w->md, d);
+        w->rays += r;
+        w->updated += 1;
+    }
+    return NULL;
+}
+
+int ora_update(ora_stage* s, const sdfgi_cfg* cfg, int frame, int stride, int threads, double* max_delta,
+               int64_t* rays, int64_t* updated, uint64_t stats[8]) {
+    if (cfg->oct_res != s->oct) return 1;
+    int front = s->front, back = 1 - front;
+    size_t nf = tileFloats(s->oct) * (size_t)s->nprobes;
+    memcpy(s->atlas[back], s->atlas[front], nf * sizeof(float)); /* pipeline.hpp:131 */
+    if (stride < 1) stride = 1;
+    if (threads < 1) threads = 1;
+    double md = 0;
+    int64_t nr = 0, nu = 0;
+    stats_t tot;
+    memset(&tot, 0, sizeof(tot));
+    work_t* ws = (work_t*)calloc((size_t)threads, sizeof(work_t));
+    pthread_t* th = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+    for (int slot = 0; slot < s->ncas; ++slot) {
+        for (int w = 0; w < threads; ++w) {
+            memset(&ws[w], 0, sizeof(work_t));
+            ws[w].s = s;
+            ws[w].cfg = cfg;
+            ws[w].frame = frame;
+            ws[w].slot = slot;
+            ws[w].stride = stride;
+            ws[w].worker = w;
+            ws[w].workers = threads;
+            if (threads > 1)
+                pthread_create(&th[w], NULL, updateWorker, &ws[w]);
+            else
+                updateWorker(&ws[w]);
+        }
+        for (int w = 0; w < threads; ++w) {
+            if (threads > 1) pthread_join(th[w], NULL);
+            md = smax(md, ws[w].md);
+            nr += ws[w].rays;
+            nu += ws[w].updated;
+            tot.q += ws[w].st.q;
+            tot.cv += ws[w].st.cv;
+            tot.cs += ws[w].st.cs;
+            tot.pe += ws[w].st.pe;
+            tot.steps += ws[w].st.steps;
+            tot.sphere += ws[w].st.sphere;
+            tot.shadow += ws[w].st.shadow;
+            tot.vis += ws[w].st.vis;
+        }
+    }
+    free(ws);
+    free(th);
+    s->front = back; /* frame-end swap, pipeline.hpp:220 */
+    if (max_delta) *max_delta = md;
+    if (rays) *rays = nr;
+    if (updated) *updated = nu;
+    addStats(stats, &tot);
+    return 0;
+}
+
+int ora_probes(const ora_stage* s, int slot, sdfgi_probe* out, int n) {
+    if (slot < 0 || slot >= s->ncas) return 1;
+    const cascade_t* c = &s->cas[slot];
+    if (n != c->res[0] * c->res[1] * c->res[2]) return 1;
+    for (int i = 0; i < n; ++i) {
+        const probe_t* p = &s->probes[c->base + i];
+        memset(&out[i], 0, sizeof(sdfgi_probe));
+        double* dst[3] = {out[i].resting, out[i].pos, out[i].last_pos};
+        const v3* src[3] = {&p->rest, &p->pos, &p->last};
+        for (int k = 0; k < 3; ++k) {
+            dst[k][0] = src[k]->x;
+            dst[k][1] = src[k]->y;
+            dst[k][2] = src[k]->z;
+        }
+        out[i].reject_history = p->reject;
+        out[i].alive = p->alive;
+        out[i].last_update_frame = p->last_frame;
+    }
+    return 0;
+}
+
+int ora_atlas(const ora_stage* s, int slot, float* out, int64_t n_floats) {
+    if (slot < 0 || slot >= s->ncas) return 1;
+    const cascade_t* c = &s->cas[slot];
+    int64_t n = (int64_t)tileFloats(s->oct) * c->res[0] * c->res[1] * c->res[2];
+    if (n != n_floats) return 1;
+    memcpy(out, s->atlas[s->front] + tileFloats(s->oct) * c->base, (size_t)n * sizeof(float));
+    return 0;
+}
+
+int ora_trace_rays(const ora_stage* s, const sdfgi_cfg* cfg, int frame, int slot, int probe, sdfgi_ray_record* out,
+                   int cap) {
+    if (slot < 0 || slot >= s->ncas) return -1;
+    const cascade_t* c = &s->cas[slot];
+    const probe_t* p = &s->probes[c->base + probe];
+    int N = (int)cfg->n_rays_full, n = p->reject ? 2 * N : N;
+    if (n > cap) return -1;
+    v3* dirs = (v3*)malloc(sizeof(v3) * n);
+    sampleDirections(n, frame, probeKey(c->level, probe), cfg->seed, (int)cfg->rotate_per_frame, dirs);
+    for (int i = 0; i < n; ++i) {
+        hit_t h = sphereTrace(s, p->pos, dirs[i], cfg->ray_tmax, cfg->surface_epsilon, (int)cfg->max_trace_steps,
+                              NULL, ORA_INF);
+        v3 L = h.converged ? shadeHit(s, &h, cfg, NULL) : s->sky;
+        sdfgi_ray_record* r = &out[i];
+        memset(r, 0, sizeof(*r));
+        r->dir[0] = dirs[i].x;
+        r->dir[1] = dirs[i].y;
+        r->dir[2] = dirs[i].z;
+        r->t = h.converged ? h.t : 0.0;
+        r->radiance[0] = L.x;
+        r->radiance[1] = L.y;
+        r->radiance[2] = L.z;
+        r->normal[0] = h.normal.x;
+        r->normal[1] = h.normal.y;
+        r->normal[2] = h.normal.z;
+        r->converged = h.converged;
+        r->miss = h.miss;
+        r->prim_index = h.prim;
+        r->steps = h.steps;
+    }
+    free(dirs);
+    return n;
+}
+
+void ora_query(const ora_stage* s, const double* pts, const double* init, int n, double* d, int32_t* owner) {
+    for (int i = 0; i < n; ++i) {
+        int o = -1;
+        d[i] = query(s, V(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]), init ? init[i] : ORA_INF, NULL, &o);
+        owner[i] = o;
+    }
+}

@@ -1,0 +1,59 @@
+/*
+ * sdfgi_oracle.h — TEST INFRASTRUCTURE: a plain-C restatement of the reference's
+ * probe path, used only as the checker (tests/, __graft_entry__.smoke(), and the
+ * bench's CPU-baseline leg). Never linked into or called by the product.
+ *
+ * Every function restates the reference function cited beside it
+ * (/root/reference/proj/include/sdfgi/*.hpp). Built with -ffp-contract=off, the
+ * same flag pinning as oracle/_ref/ref_parity, it is bit-exact with the reference
+ * (checked against tests/golden/ by tests/test_oracle.py).
+ *
+ * Parity is pinned: the golden fixtures were produced by the reference itself.
+ */
+#ifndef SDFGI_ORACLE_H
+#define SDFGI_ORACLE_H
+
+#include <stdint.h>
+
+#include "../include/sdfgi_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ora_stage ora_stage;
+
+/* ActiveScene (scene.hpp:88-103) from the ABI arrays; the arrays are copied. */
+ora_stage* ora_create(const sdfgi_prim* prims, int n_prims, const sdfgi_cluster* clusters, int n_clusters,
+                      const int32_t* member_start, const int32_t* member_idx, const sdfgi_light* lights,
+                      int n_lights, const double sky[3]);
+void ora_destroy(ora_stage* s);
+
+/* makeCascade-equivalent volume (probe_volume.hpp:57-76): fresh probes, zero atlases. */
+int ora_add_cascade(ora_stage* s, int level, int rx, int ry, int rz, double spacing, const double origin[3],
+                    int oct_res);
+
+/* updateProbePositions (probe_volume.hpp:99-143) for cascade slot `slot`. */
+int ora_relocate(ora_stage* s, int slot, double th1, double th2, int max_steps, double grad_step, int report[3],
+                 uint64_t stats[8]);
+
+/* The probe stage of renderFrame (pipeline.hpp:126-151): back <- front, updateProbe
+ * (probe_update.hpp:166-211) for every alive probe whose index % stride == 0, using
+ * `threads` OpenMP threads (results are thread-count independent), then swap. */
+int ora_update(ora_stage* s, const sdfgi_cfg* cfg, int frame, int stride, int threads, double* max_delta,
+               int64_t* rays, int64_t* updated, uint64_t stats[8]);
+
+int ora_probes(const ora_stage* s, int slot, sdfgi_probe* out, int n);
+int ora_atlas(const ora_stage* s, int slot, float* out, int64_t n_floats); /* front atlas */
+
+/* Per-ray records of updateProbe's ray stage (probe_update.hpp:173-189) for one probe. */
+int ora_trace_rays(const ora_stage* s, const sdfgi_cfg* cfg, int frame, int slot, int probe, sdfgi_ray_record* out,
+                   int cap);
+
+/* querySceneSdf (scene.hpp:336-340) at n points; init may be NULL (+inf). */
+void ora_query(const ora_stage* s, const double* pts, const double* init, int n, double* d, int32_t* owner);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
