@@ -81,7 +81,7 @@ def build_ref(verbose=False) -> str | None:
     """The reference compiled from /root/reference (only where it exists)."""
     if not os.path.isdir("/root/reference/proj/include"):
         return None
-    _run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref"], verbose)
+    _run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref", "dropin"], verbose)
     return os.path.join(ROOT, "oracle", "_ref")
 
 
