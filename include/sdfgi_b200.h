@@ -262,6 +262,11 @@ SDFGI_API int sdfgi_set_accel(void* ctx, int mode);
 /* {mode, grid built, dim x, dim y, dim z, candidate list entries} */
 SDFGI_API int sdfgi_accel_info(void* ctx, int64_t out[6]);
 
+/* Probe-index range [lo, hi) of a cascade that rank `rank` of `world` updates: the
+ * z-slab of layers [res_z*rank/world, res_z*(rank+1)/world). Pure
+ * function (no context, no device). */
+SDFGI_API int sdfgi_slab_range(int res_x, int res_y, int res_z, int rank, int world, int* lo, int* hi);
+
 /* Launch counter: kernels this context has launched since creation. */
 SDFGI_API int sdfgi_launch_count(void* ctx, int64_t* out);
 

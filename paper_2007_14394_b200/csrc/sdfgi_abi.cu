@@ -1297,6 +1297,19 @@ int sdfgi_accel_info(void* ctx, int64_t out[6]) {
     });
 }
 
+int sdfgi_slab_range(int res_x, int res_y, int res_z, int rank, int world, int* lo, int* hi) {
+    return guard([&] {
+        REQ(res_x > 0 && res_y > 0 && res_z > 0 && world >= 1 && rank >= 0 && rank < world && lo && hi,
+            SDFGI_ERR_INVALID, "bad slab arguments");
+        CascadeHost c;
+        c.res[0] = res_x;
+        c.res[1] = res_y;
+        c.res[2] = res_z;
+        c.base = 0;
+        slabRange(c, rank, world, lo, hi);
+    });
+}
+
 int sdfgi_launch_count(void* ctx, int64_t* out) {
     return guard([&] {
         Ctx* c = C(ctx);

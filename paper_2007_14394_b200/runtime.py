@@ -56,6 +56,7 @@ _SIGS = {
     "sdfgi_measure_fp_peak": [_P, _P, _P],
     "sdfgi_set_accel": [_P, _I],
     "sdfgi_accel_info": [_P, _P],
+    "sdfgi_slab_range": [_I, _I, _I, _I, _I, _P, _P],
     "sdfgi_launch_count": [_P, _P],
 }
 
