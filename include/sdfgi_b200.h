@@ -169,6 +169,28 @@ typedef struct sdfgi_ray_record {
     int32_t steps;         /* sphere-trace loop iterations */
 } sdfgi_ray_record;
 
+/* GBufferPixel (shading.hpp:13-22): depth along the view ray (+inf = sky), normal,
+ * albedo, emission, world position, motion (pixel offset to last frame), owner. 128 B. */
+typedef struct sdfgi_gbuffer_pixel {
+    double depth;
+    double normal[3];
+    double albedo[3];
+    double emission[3];
+    double world_pos[3];
+    double motion[2];
+    int32_t prim_index;
+    int32_t _pad;
+} sdfgi_gbuffer_pixel;
+
+/* Camera (camera.hpp:9-49): orthonormal frame + vertical fov in degrees. 104 B. */
+typedef struct sdfgi_camera {
+    double position[3];
+    double forward[3];
+    double right[3];
+    double up[3];
+    double fov_y_deg;
+} sdfgi_camera;
+
 /* ---------------------------------------------------------------- lifecycle */
 SDFGI_API int sdfgi_abi_version(void);
 SDFGI_API const char* sdfgi_last_error(void);

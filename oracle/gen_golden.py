@@ -159,12 +159,54 @@ def build_case(name, spec):
     print(name, {k: v.shape for k, v in data.items()})
 
 
+# C3 gather fixtures: probe passes, then renderGBuffer + the gather stages for two
+# frames (frame 0 without history, frame 1 with) at a small resolution.
+GATHER_CASES = {
+    "gather_c1": dict(src="c1", passes=2, extra=["--res", 8, 8, 8, "--spacing", 1.0, "--nrays", 64], size=(96, 64)),
+    "gather_sponza": dict(src="sponza", passes=2, extra=["--nrays", 32], size=(128, 72)),
+    "gather_openfield": dict(src="openfield", passes=1, extra=["--nrays", 16], size=(96, 54)),
+}
+
+
+def build_gather_case(name, spec):
+    d = os.path.join(OUT, name)
+    os.makedirs(d, exist_ok=True)
+    sdfs = os.path.join(OUT, spec["src"], "scene.sdfs")
+    with tempfile.TemporaryDirectory() as tmp:
+        args = ["gather", sdfs, tmp, "--passes", spec["passes"], "--threads", 2, *spec["extra"],
+                "--size", *spec["size"], "--gather-frames", 2]
+        summary = json.loads(run(*args))
+        data = {}
+        for fn in sorted(os.listdir(tmp)):
+            base, ext = os.path.splitext(fn)
+            path = os.path.join(tmp, fn)
+            if ext == ".sdfa":
+                data[base] = scene_io.read_sdfa(path)[2]
+            elif base == "gbuffer":
+                data[base] = np.fromfile(path, scene_io.GBUFFER_DTYPE)
+            elif base.startswith("gprobes"):
+                data[base] = np.fromfile(path, scene_io.PROBE_DTYPE)
+            elif base.startswith(("half_src", "sel", "sparse_valid", "sparse_anchor")):
+                data[base] = np.fromfile(path, "<i4")
+            else:
+                data[base] = np.fromfile(path, "<f8")
+    summary.update(case=name, src=spec["src"], args=[str(a) for a in args[3:]], size=list(spec["size"]),
+                   generator="oracle/gen_golden.py via oracle/_ref/ref_parity gather (-ffp-contract=off)")
+    with open(os.path.join(d, "summary.json"), "w") as f:
+        json.dump(summary, f, indent=1)
+    np.savez_compressed(os.path.join(d, "data.npz"), **data)
+    print(name, {k: v.shape for k, v in data.items()})
+
+
 def main():
     if not os.path.exists(REF):
         sys.exit("build oracle/_ref first: make -C oracle ref")
-    names = sys.argv[1:] or list(CASES)
+    names = sys.argv[1:] or list(CASES) + list(GATHER_CASES)
     for n in names:
-        build_case(n, CASES[n])
+        if n in GATHER_CASES:
+            build_gather_case(n, GATHER_CASES[n])
+        else:
+            build_case(n, CASES[n])
 
 
 if __name__ == "__main__":

@@ -37,6 +37,8 @@ def load():
         "ora_atlas": ([_P, _I, _P, ctypes.c_int64], _I),
         "ora_trace_rays": ([_P, _P, _I, _I, _I, _P, _I], _I),
         "ora_query": ([_P, _P, _P, _I, _P, _P], None),
+        "ora_render_gbuffer": ([_P, _P, _I, _I, _P, _P, _P], _I),
+        "ora_gather_frame": ([_P, _P, _I, _I, _I, _P, _P, _P, _I] + [_P] * 10, _I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -134,6 +136,38 @@ class Stage:
         n = load().ora_trace_rays(self.h, _p(self.cfg), frame, level, probe, _p(out), cap)
         assert n >= 0
         return out[:n]
+
+    def camera(self):
+        c = self.scene.camera
+        cam = np.zeros(1, self.sio.CAMERA_DTYPE)
+        cam["position"], cam["forward"], cam["right"], cam["up"] = c.position, c.forward, c.right, c.up
+        cam["fov_y_deg"] = c.fov_y
+        return cam
+
+    def render_gbuffer(self, w, h):
+        out = np.zeros(w * h, self.sio.GBUFFER_DTYPE)
+        stats = np.zeros(8, np.uint64)
+        load().ora_render_gbuffer(self.h, _p(self.camera()), w, h, _p(self.cfg), _p(out), _p(stats))
+        return out, stats
+
+    def gather_frame(self, gb, w, h, frame, hist=None):
+        """One gather frame (pipeline.hpp:161-207); hist = (resolved[w*h*3], depth[w*h]) or None."""
+        hw, hh = (w + 1) // 2, (h + 1) // 2
+        sw, sh = (hw + 1) // 2, (hh + 1) // 2
+        out = dict(half_depth=np.zeros(hw * hh), half_src=np.zeros(hw * hh, np.int32),
+                   sel=np.zeros(sw * sh, np.int32), sparse_irr=np.zeros(sw * sh * 3),
+                   sparse_valid=np.zeros(sw * sh, np.int32), sparse_anchor=np.zeros(sw * sh, np.int32),
+                   resolved=np.zeros(w * h * 3), indirect=np.zeros(w * h * 3),
+                   vis_stats=np.zeros(8, np.uint64), contact_stats=np.zeros(8, np.uint64))
+        gb = np.ascontiguousarray(gb, self.sio.GBUFFER_DTYPE)
+        hi = None if hist is None else np.ascontiguousarray(hist[0], np.float64)
+        hd = None if hist is None else np.ascontiguousarray(hist[1], np.float64)
+        n = load().ora_gather_frame(self.h, _p(gb), w, h, frame, _p(self.cfg), _p(hi), _p(hd),
+                                    0 if hist is None else 1, *[_p(out[k]) for k in (
+                                        "half_depth", "half_src", "sel", "sparse_irr", "sparse_valid",
+                                        "sparse_anchor", "resolved", "indirect", "vis_stats", "contact_stats")])
+        out["tasks"] = n
+        return out
 
     def query(self, pts, init=None):
         pts = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)

@@ -566,6 +566,121 @@ int cmdPasses(int argc, char** argv) {
     return 0;
 }
 
+void dumpImage(const std::string& path, const ImageRgb& img) {
+    std::vector<double> v;
+    v.reserve(img.pixels.size() * 3);
+    for (const Vec3& p : img.pixels) {
+        v.push_back(p.x);
+        v.push_back(p.y);
+        v.push_back(p.z);
+    }
+    writeVec(path, v);
+}
+
+// C3: probe passes, then renderGBuffer + the gather stages of renderFrame
+// (pipeline.hpp:155-207) for --gather-frames frames against the final atlas.
+int cmdGather(int argc, char** argv) {
+    using Clock = std::chrono::steady_clock;
+    if (argc < 4) throw std::runtime_error("usage: gather <in.sdfs> <outdir> [opts]");
+    Loaded L = readSdfs(argv[2]);
+    std::string dir = argv[3];
+    Opts o = parseOpts(argc, argv, 4);
+    if (o.width <= 0) throw std::runtime_error("--size W H required");
+    ProbeStage st;
+    initStage(st, L, o);
+    for (int p = 0; p < o.passes; ++p) runPass(st, p, o, nullptr);
+    const int W = o.width, H = o.height, T = std::max(1, o.threads);
+    TraceStats gst;
+    auto t0 = Clock::now();
+    GBuffer gb = renderGBuffer(st.scene, st.camera, st.camera, W, H, st.cfg, &gst, T);
+    double gbMs = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+    if (o.dump) {
+        std::vector<sdfgi_gbuffer_pixel> px(gb.pixels.size());
+        for (size_t i = 0; i < px.size(); ++i) {
+            const GBufferPixel& g = gb.pixels[i];
+            sdfgi_gbuffer_pixel& q = px[i];
+            std::memset(&q, 0, sizeof(q));
+            q.depth = g.depth;
+            v3out(q.normal, g.normal);
+            v3out(q.albedo, g.albedo);
+            v3out(q.emission, g.emission);
+            v3out(q.world_pos, g.worldPos);
+            q.motion[0] = g.motion.x;
+            q.motion[1] = g.motion.y;
+            q.prim_index = g.primitiveIndex;
+        }
+        writeVec(dir + "/gbuffer.bin", px);
+        for (size_t ci = 0; ci < st.cascades.size(); ++ci) {
+            std::string c = "_c" + std::to_string(ci);
+            writeVec(dir + "/gprobes" + c + ".bin", probeDump(st.cascades[ci]));
+            st.atlas[st.readIdx][ci].dump(dir + "/gatlas" + c + ".sdfa");
+        }
+    }
+    IrradianceField field{&st.cascades, &st.atlas[st.readIdx]};
+    HistoryBuffers history;
+    std::ostringstream js;
+    js << "{\"gbuffer_ms\": " << gbMs << ", \"gbuffer_stats\": " << statsJson(gst) << ", \"frames\": [";
+    for (int f = 0; f < o.gatherFrames; ++f) {
+        TraceStats vs, cs;
+        auto a = Clock::now();
+        HalfResDepth half = downsampleDepthCheckerboard(gb);
+        SelectedPixels sel = selectVisibilityPixels(half, f);
+        VisibilityWork work = buildVisibilityTasks(st.cascades, gb, half, sel, st.cfg);
+        std::vector<double> vis = runVisibilityTasks(st.scene, st.cascades, work, st.cfg, &vs, T);
+        SparseGi sparse;  // pipeline.hpp:173-185
+        sparse.width = sel.width;
+        sparse.height = sel.height;
+        sparse.irradiance.resize(work.pixels.size());
+        sparse.anchorPixel.resize(work.pixels.size());
+        sparse.valid.assign(work.pixels.size(), 0);
+        for (size_t i = 0; i < work.pixels.size(); ++i) {
+            int anchor = half.srcPixel[sel.halfResIndex[i]];
+            sparse.anchorPixel[i] = anchor;
+            PixelGiResult r = shadePixelGI(work.pixels[i], vis, gb.pixels[anchor].normal, field);
+            sparse.irradiance[i] = r.irradiance;
+            sparse.valid[i] = r.valid ? 1 : 0;
+        }
+        auto b = Clock::now();
+        ImageRgb resolved = upsampleAndResolve(sparse, gb, history, st.cascades, field, st.cfg, T);
+        auto c = Clock::now();
+        double radius = st.cfg.contactRadiusFrac * st.cascades[0].spacing;
+        ImageRgb indirect = contactGI(st.scene, gb, resolved, field, radius, st.cfg.contactSamples, st.cfg, &cs, T);
+        auto d = Clock::now();
+        if (o.dump) {
+            std::string sfx = "_f" + std::to_string(f);
+            writeVec(dir + "/half_depth" + sfx + ".bin", half.depth);
+            writeVec(dir + "/half_src" + sfx + ".bin", half.srcPixel);
+            writeVec(dir + "/sel" + sfx + ".bin", sel.halfResIndex);
+            std::vector<double> irr;
+            std::vector<int32_t> valid(sparse.valid.begin(), sparse.valid.end());
+            for (const Vec3& v : sparse.irradiance) {
+                irr.push_back(v.x);
+                irr.push_back(v.y);
+                irr.push_back(v.z);
+            }
+            writeVec(dir + "/sparse_irr" + sfx + ".bin", irr);
+            writeVec(dir + "/sparse_valid" + sfx + ".bin", valid);
+            writeVec(dir + "/sparse_anchor" + sfx + ".bin", sparse.anchorPixel);
+            writeVec(dir + "/vis" + sfx + ".bin", vis);
+            dumpImage(dir + "/resolved" + sfx + ".bin", resolved);
+            dumpImage(dir + "/indirect" + sfx + ".bin", indirect);
+        }
+        if (f) js << ", ";
+        js << "{\"frame\": " << f << ", \"tasks\": " << work.tasks.size()
+           << ", \"visibility_ms\": " << std::chrono::duration<double, std::milli>(b - a).count()
+           << ", \"resolve_ms\": " << std::chrono::duration<double, std::milli>(c - b).count()
+           << ", \"contact_ms\": " << std::chrono::duration<double, std::milli>(d - c).count()
+           << ", \"vis_stats\": " << statsJson(vs) << ", \"contact_stats\": " << statsJson(cs) << "}";
+        history.irradiance = std::move(resolved);  // pipeline.hpp:214-218
+        history.depth.resize(gb.pixels.size());
+        for (size_t i = 0; i < gb.pixels.size(); ++i) history.depth[i] = gb.pixels[i].depth;
+        history.valid = true;
+    }
+    js << "]}";
+    std::cout << js.str() << std::endl;
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -578,6 +693,7 @@ int main(int argc, char** argv) {
         if (cmd == "scene") return cmdScene(argc, argv);
         if (cmd == "passes") return cmdPasses(argc, argv);
         if (cmd == "recluster") return cmdRecluster(argc, argv);
+        if (cmd == "gather") return cmdGather(argc, argv);
         std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
         return 2;
     } catch (const std::exception& e) {

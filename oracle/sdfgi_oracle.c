@@ -895,3 +895,363 @@ void ora_query(const ora_stage* s, const double* pts, const double* init, int n,
         owner[i] = o;
     }
 }
+
+/* ================================================================= gather (e) */
+static v3 P3(const double* a) { return V(a[0], a[1], a[2]); }
+
+/* Camera::rayDir / project, camera.hpp:29-48 */
+static v3 camRayDir(const sdfgi_camera* c, double px, double py, int w, int h) {
+    double tanHalf = tan(c->fov_y_deg * ORA_PI / 360.0);
+    double aspect = (double)w / h;
+    double ndcX = (2.0 * (px + 0.5) / w - 1.0) * tanHalf * aspect;
+    double ndcY = (1.0 - 2.0 * (py + 0.5) / h) * tanHalf;
+    return norm(add(add(P3(c->forward), muls(P3(c->right), ndcX)), muls(P3(c->up), ndcY)));
+}
+static int camProject(const sdfgi_camera* c, v3 world, int w, int h, double* ox, double* oy) {
+    v3 rel = sub(world, P3(c->position));
+    double z = dot(rel, P3(c->forward));
+    if (z <= 1e-9) return 0;
+    double tanHalf = tan(c->fov_y_deg * ORA_PI / 360.0);
+    double aspect = (double)w / h;
+    double ndcX = dot(rel, P3(c->right)) / (z * tanHalf * aspect);
+    double ndcY = dot(rel, P3(c->up)) / (z * tanHalf);
+    *ox = (ndcX + 1.0) * 0.5 * w - 0.5;
+    *oy = (1.0 - ndcY) * 0.5 * h - 0.5;
+    return 1;
+}
+
+int ora_render_gbuffer(const ora_stage* s, const sdfgi_camera* cam, int w, int h, const sdfgi_cfg* cfg,
+                       sdfgi_gbuffer_pixel* out, uint64_t stats[8]) { /* shading.hpp:39-72 */
+    stats_t st;
+    memset(&st, 0, sizeof(st));
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            sdfgi_gbuffer_pixel* px = &out[(size_t)y * w + x];
+            memset(px, 0, sizeof(*px));
+            px->depth = ORA_INF;
+            px->normal[2] = 1.0;
+            px->prim_index = -1;
+            v3 dir = camRayDir(cam, x, (double)y, w, h);
+            hit_t hit = sphereTrace(s, P3(cam->position), dir, cfg->ray_tmax, cfg->surface_epsilon,
+                                    (int)cfg->max_trace_steps, &st, ORA_INF);
+            if (!hit.converged) continue;
+            px->depth = hit.t;
+            px->normal[0] = hit.normal.x;
+            px->normal[1] = hit.normal.y;
+            px->normal[2] = hit.normal.z;
+            px->world_pos[0] = hit.pos.x;
+            px->world_pos[1] = hit.pos.y;
+            px->world_pos[2] = hit.pos.z;
+            px->prim_index = hit.prim;
+            if (hit.prim >= 0) {
+                memcpy(px->albedo, s->prims[hit.prim].albedo, sizeof(px->albedo));
+                memcpy(px->emission, s->prims[hit.prim].emission, sizeof(px->emission));
+            }
+            double ppx, ppy;
+            if (camProject(cam, hit.pos, w, h, &ppx, &ppy)) {
+                px->motion[0] = ppx - x;
+                px->motion[1] = ppy - y;
+            }
+        }
+    addStats(stats, &st);
+    return 0;
+}
+
+static int isSky(const sdfgi_gbuffer_pixel* p) { return !(p->depth < ORA_INF); } /* shading.hpp:22 */
+
+/* orthonormalBasis vec.hpp:188-194; cosineHemisphereDir rng.hpp:58-69 */
+static v3 cosineHemisphereDir(rng_t* r, v3 n) {
+    double u1 = rng_uniform(r), u2 = rng_uniform(r);
+    double rr = sqrt(u1), phi = 2.0 * ORA_PI * u2;
+    double lx = rr * cos(phi), ly = rr * sin(phi), lz = sqrt(smax(0.0, 1.0 - u1));
+    double sign = copysign(1.0, n.z);
+    double a = -1.0 / (sign + n.z);
+    double c = n.x * n.y * a;
+    v3 t = V(1.0 + sign * n.x * n.x * a, sign * c, -sign * n.x);
+    v3 b = V(c, sign + n.y * n.y * a, -n.y);
+    return norm(add(add(muls(t, lx), muls(b, ly)), muls(n, lz)));
+}
+
+typedef struct {
+    int key[5];
+} tkey_t;
+
+int ora_gather_frame(const ora_stage* s, const sdfgi_gbuffer_pixel* gb, int w, int h, int frame, const sdfgi_cfg* cfg,
+                     const double* hist_irr, const double* hist_depth, int hist_valid, double* half_depth,
+                     int32_t* half_src, int32_t* sel, double* sparse_irr, int32_t* sparse_valid,
+                     int32_t* sparse_anchor, double* resolved, double* indirect, uint64_t vis_stats[8],
+                     uint64_t contact_stats[8]) {
+    const int hw = (w + 1) / 2, hh = (h + 1) / 2;
+    const int sw = (hw + 1) / 2, sh = (hh + 1) / 2;
+    double* hd = (double*)malloc(sizeof(double) * hw * hh);
+    int* hs = (int*)malloc(sizeof(int) * hw * hh);
+    /* downsampleDepthCheckerboard, shading.hpp:85-112 */
+    for (int y = 0; y < hh; ++y)
+        for (int x = 0; x < hw; ++x) {
+            int takeMax = ((x + y) & 1) == 0;
+            double best = takeMax ? -ORA_INF : ORA_INF;
+            int bestSrc = 0;
+            for (int dy = 0; dy < 2; ++dy)
+                for (int dx = 0; dx < 2; ++dx) {
+                    int sx = 2 * x + dx < w - 1 ? 2 * x + dx : w - 1;
+                    int sy = 2 * y + dy < h - 1 ? 2 * y + dy : h - 1;
+                    double d = gb[(size_t)sy * w + sx].depth;
+                    if (takeMax ? d > best : d < best) {
+                        best = d;
+                        bestSrc = sy * w + sx;
+                    }
+                }
+            hd[y * hw + x] = best;
+            hs[y * hw + x] = bestSrc;
+        }
+    /* selectVisibilityPixels, shading.hpp:125-161 */
+    static const int offs[4][2] = {{0, 0}, {1, 0}, {0, 1}, {1, 1}};
+    int* sl = (int*)malloc(sizeof(int) * sw * sh);
+    int rot = frame & 3;
+    for (int y = 0; y < sh; ++y)
+        for (int x = 0; x < sw; ++x) {
+            int hx0 = 2 * x, hy0 = 2 * y;
+            double lo = ORA_INF, hi = -ORA_INF;
+            int loIdx = -1, hiIdx = -1;
+            for (int k = 0; k < 4; ++k) {
+                int hx = hx0 + offs[k][0] < hw - 1 ? hx0 + offs[k][0] : hw - 1;
+                int hy = hy0 + offs[k][1] < hh - 1 ? hy0 + offs[k][1] : hh - 1;
+                double d = hd[hy * hw + hx];
+                if (!isfinite(d)) continue;
+                if (d < lo) { lo = d; loIdx = hy * hw + hx; }
+                if (d > hi) { hi = d; hiIdx = hy * hw + hx; }
+            }
+            int hx = hx0 + offs[rot][0] < hw - 1 ? hx0 + offs[rot][0] : hw - 1;
+            int hy = hy0 + offs[rot][1] < hh - 1 ? hy0 + offs[rot][1] : hh - 1;
+            int pick = hy * hw + hx;
+            if (loIdx >= 0) {
+                int rotSky = !isfinite(hd[pick]);
+                int spread = (hi - lo) > 0.1 * hi;
+                if (spread)
+                    pick = (frame & 1) == 0 ? loIdx : hiIdx;
+                else if (rotSky)
+                    pick = loIdx;
+            }
+            sl[y * sw + x] = pick;
+        }
+    /* buildVisibilityTasks (shading.hpp:185-259) + runVisibilityTasks (:281-300) +
+       shadePixelGI (:319-338): per 4x4 half-res tile, dedup in insertion order */
+    int ncell = sw * sh;
+    double* sirr = (double*)calloc((size_t)ncell * 3, sizeof(double));
+    int* svalid = (int*)calloc((size_t)ncell, sizeof(int));
+    int* sanchor = (int*)calloc((size_t)ncell, sizeof(int));
+    stats_t vst;
+    memset(&vst, 0, sizeof(vst));
+    int ntasks = 0;
+    int tilesX = (sw + 1) / 2, tilesY = (sh + 1) / 2;
+    const float* front = s->atlas[s->front];
+    for (int ty = 0; ty < tilesY; ++ty)
+        for (int tx = 0; tx < tilesX; ++tx) {
+            tkey_t keys[32];
+            double tvis[32];
+            int nk = 0;
+            stencil_t stc[4];
+            int cellOf[4], valid[4], tIdx[4][8];
+            for (int q = 0; q < 4; ++q) {
+                valid[q] = 0;
+                cellOf[q] = -1;
+                int cx = 2 * tx + (q & 1), cy = 2 * ty + (q >> 1);
+                if (cx >= sw || cy >= sh) continue;
+                int cell = cy * sw + cx;
+                cellOf[q] = cell;
+                int src = hs[sl[cell]];
+                const sdfgi_gbuffer_pixel* px = &gb[src];
+                if (isSky(px)) continue;
+                stc[q] = interpolationStencil(s, P3(px->world_pos), cfg->mvc_relocation_frac);
+                if (stc[q].sky || stc[q].count == 0) continue;
+                valid[q] = 1;
+                for (int e = 0; e < stc[q].count; ++e) {
+                    if (stc[q].w[e] <= 0) {
+                        tIdx[q][e] = -1;
+                        continue;
+                    }
+                    double quant = cfg->dedup_quant_frac * s->cas[stc[q].cascade].spacing;
+                    tkey_t k = {{stc[q].cascade, stc[q].probe[e], (int32_t)floor(px->world_pos[0] / quant),
+                                 (int32_t)floor(px->world_pos[1] / quant), (int32_t)floor(px->world_pos[2] / quant)}};
+                    int found = -1;
+                    for (int i = 0; i < nk; ++i)
+                        if (memcmp(&keys[i], &k, sizeof(k)) == 0) {
+                            found = i;
+                            break;
+                        }
+                    if (found < 0) {
+                        /* probeVisibility, shading.hpp:264-279 */
+                        const cascade_t* c = &s->cas[stc[q].cascade];
+                        v3 sp = P3(px->world_pos), nn = P3(px->normal);
+                        v3 toProbe = sub(s->probes[c->base + stc[q].probe[e]].pos, sp);
+                        double dist = len(toProbe), vis = 1.0;
+                        if (dist >= 1e-9) {
+                            v3 dir = divs(toProbe, dist);
+                            double cosT = dot(nn, dir);
+                            double bias = 2.0 * cfg->surface_epsilon / smax(0.1, cosT);
+                            double tMax = dist - cfg->threshold1_frac * c->spacing;
+                            if (tMax > bias) {
+                                ++vst.vis;
+                                vis = softShadowTrace(s, add(sp, muls(nn, bias)), dir, bias, tMax,
+                                                      cfg->probe_visibility_k, &vst, (int)cfg->shadow_steps);
+                            }
+                        }
+                        found = nk;
+                        keys[nk] = k;
+                        tvis[nk] = vis;
+                        ++nk;
+                        ++ntasks;
+                    }
+                    tIdx[q][e] = found;
+                }
+            }
+            for (int q = 0; q < 4; ++q) {
+                int cell = cellOf[q];
+                if (cell < 0) continue;
+                sanchor[cell] = hs[sl[cell]];
+                if (!valid[q]) continue;
+                const sdfgi_gbuffer_pixel* px = &gb[sanchor[cell]];
+                const cascade_t* c = &s->cas[stc[q].cascade];
+                double wsum = 0;
+                v2 uv = octEncode(P3(px->normal));
+                v3 acc = V(0, 0, 0);
+                for (int e = 0; e < stc[q].count; ++e) {
+                    if (stc[q].w[e] <= 0 || tIdx[q][e] < 0) continue;
+                    double ww = stc[q].w[e] * tvis[tIdx[q][e]];
+                    if (ww <= 0) continue;
+                    acc = add(acc, muls(sampleBilinear(front, s->oct, c->base + stc[q].probe[e], uv), ww));
+                    wsum += ww;
+                }
+                if (wsum <= 1e-9) continue;
+                v3 irr = divs(acc, wsum);
+                sirr[3 * cell] = irr.x;
+                sirr[3 * cell + 1] = irr.y;
+                sirr[3 * cell + 2] = irr.z;
+                svalid[cell] = 1;
+            }
+        }
+    /* upsampleAndResolve, shading.hpp:350-426 */
+    double* res = (double*)calloc((size_t)w * h * 3, sizeof(double));
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            const sdfgi_gbuffer_pixel* px = &gb[(size_t)y * w + x];
+            if (isSky(px)) continue;
+            int qx = x / 4, qy = y / 4;
+            v3 acc = V(0, 0, 0), cmin = V(ORA_INF, ORA_INF, ORA_INF), cmax = V(-ORA_INF, -ORA_INF, -ORA_INF);
+            double wsum = 0;
+            int anyN = 0;
+            double sigma = smax(1e-6, cfg->depth_sigma_frac * px->depth);
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    int nx = qx + dx, ny = qy + dy;
+                    if (nx < 0 || ny < 0 || nx >= sw || ny >= sh) continue;
+                    int cell = ny * sw + nx;
+                    if (!svalid[cell]) continue;
+                    const sdfgi_gbuffer_pixel* an = &gb[sanchor[cell]];
+                    double ww = exp(-fabs(an->depth - px->depth) / sigma) *
+                                pow(smax(0.0, dot(P3(an->normal), P3(px->normal))), 4.0);
+                    if (ww <= 1e-6) continue;
+                    v3 si = P3(&sirr[3 * cell]);
+                    acc = add(acc, muls(si, ww));
+                    wsum += ww;
+                    cmin = V(smin(cmin.x, si.x), smin(cmin.y, si.y), smin(cmin.z, si.z));
+                    cmax = V(smax(cmax.x, si.x), smax(cmax.y, si.y), smax(cmax.z, si.z));
+                    anyN = 1;
+                }
+            v3 cur = V(0, 0, 0), hist = V(0, 0, 0), o = V(0, 0, 0);
+            int haveCur = wsum > 1e-9, haveHist = 0;
+            if (haveCur) cur = divs(acc, wsum);
+            if (hist_valid) {
+                int hx = (int)lround(x + px->motion[0]), hy = (int)lround(y + px->motion[1]);
+                if (hx >= 0 && hy >= 0 && hx < w && hy < h) {
+                    double hdp = hist_depth[(size_t)hy * w + hx];
+                    if (isfinite(hdp) && fabs(hdp - px->depth) <= 0.1 * smax(hdp, px->depth)) {
+                        hist = P3(&hist_irr[3 * ((size_t)hy * w + hx)]);
+                        if (anyN)
+                            hist = V(smin(smax(hist.x, cmin.x), cmax.x), smin(smax(hist.y, cmin.y), cmax.y),
+                                     smin(smax(hist.z, cmin.z), cmax.z));
+                        haveHist = 1;
+                    }
+                }
+            }
+            if (haveCur && haveHist)
+                o = add(muls(cur, cfg->history_blend), muls(hist, 1.0 - cfg->history_blend));
+            else if (haveCur)
+                o = cur;
+            else if (haveHist)
+                o = hist;
+            else {
+                stencil_t st = interpolationStencil(s, P3(px->world_pos), cfg->mvc_relocation_frac);
+                if (!st.sky) { /* sampleIrradianceRaw, probe_update.hpp:47-57 */
+                    v2 uv = octEncode(P3(px->normal));
+                    const cascade_t* c = &s->cas[st.cascade];
+                    for (int e = 0; e < st.count; ++e) {
+                        if (st.w[e] <= 0) continue;
+                        o = add(o, muls(sampleBilinear(front, s->oct, c->base + st.probe[e], uv), st.w[e]));
+                    }
+                }
+            }
+            double* r = &res[3 * ((size_t)y * w + x)];
+            r[0] = o.x;
+            r[1] = o.y;
+            r[2] = o.z;
+        }
+    /* contactGI, shading.hpp:431-477 */
+    stats_t cst;
+    memset(&cst, 0, sizeof(cst));
+    double radius = cfg->contact_radius_frac * s->cas[0].spacing;
+    int nS = (int)cfg->contact_samples;
+    if (indirect)
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x) {
+                const sdfgi_gbuffer_pixel* px = &gb[(size_t)y * w + x];
+                double* out = &indirect[3 * ((size_t)y * w + x)];
+                out[0] = out[1] = out[2] = 0;
+                if (isSky(px)) continue;
+                v3 brdf = divs(P3(px->albedo), ORA_PI);
+                v3 probeGi = mulv(brdf, P3(&res[3 * ((size_t)y * w + x)]));
+                if (nS <= 0 || radius <= 0) {
+                    out[0] = probeGi.x;
+                    out[1] = probeGi.y;
+                    out[2] = probeGi.z;
+                    continue;
+                }
+                rng_t r = rng_key(hashCombine(hashCombine(cfg->seed, 0xc0417ffull), (uint64_t)y * w + x));
+                int unocc = 0;
+                v3 occ = V(0, 0, 0), nn = P3(px->normal), wp = P3(px->world_pos);
+                for (int k = 0; k < nS; ++k) {
+                    v3 dir = cosineHemisphereDir(&r, nn);
+                    double cosT = smax(0.1, dot(dir, nn));
+                    double bias = 2.0 * cfg->surface_epsilon / cosT;
+                    hit_t hit = sphereTrace(s, add(wp, muls(nn, bias)), dir, radius, cfg->surface_epsilon,
+                                            (int)cfg->max_trace_steps, &cst, bias + cfg->surface_epsilon);
+                    if (!hit.converged)
+                        ++unocc;
+                    else
+                        occ = add(occ, shadeHit(s, &hit, cfg, &cst));
+                }
+                double ao = (double)unocc / nS;
+                v3 contact = mulv(muls(divs(P3(px->albedo), ORA_PI), ORA_PI / nS), occ);
+                v3 o = add(muls(probeGi, ao), contact);
+                out[0] = o.x;
+                out[1] = o.y;
+                out[2] = o.z;
+            }
+    if (half_depth) memcpy(half_depth, hd, sizeof(double) * hw * hh);
+    if (half_src) memcpy(half_src, hs, sizeof(int) * hw * hh);
+    if (sel) memcpy(sel, sl, sizeof(int) * ncell);
+    if (sparse_irr) memcpy(sparse_irr, sirr, sizeof(double) * 3 * ncell);
+    if (sparse_valid) memcpy(sparse_valid, svalid, sizeof(int) * ncell);
+    if (sparse_anchor) memcpy(sparse_anchor, sanchor, sizeof(int) * ncell);
+    if (resolved) memcpy(resolved, res, sizeof(double) * 3 * w * h);
+    addStats(vis_stats, &vst);
+    addStats(contact_stats, &cst);
+    free(hd);
+    free(hs);
+    free(sl);
+    free(sirr);
+    free(svalid);
+    free(sanchor);
+    free(res);
+    return ntasks;
+}

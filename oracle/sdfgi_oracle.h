@@ -53,6 +53,23 @@ int ora_trace_rays(const ora_stage* s, const sdfgi_cfg* cfg, int frame, int slot
 /* querySceneSdf (scene.hpp:336-340) at n points; init may be NULL (+inf). */
 void ora_query(const ora_stage* s, const double* pts, const double* init, int n, double* d, int32_t* owner);
 
+/* renderGBuffer (shading.hpp:39-72) with prevCamera == camera. out: w*h pixels. */
+int ora_render_gbuffer(const ora_stage* s, const sdfgi_camera* cam, int w, int h, const sdfgi_cfg* cfg,
+                       sdfgi_gbuffer_pixel* out, uint64_t stats[8]);
+
+/* One gather frame of renderFrame (pipeline.hpp:161-207) against the front atlas:
+ * downsampleDepthCheckerboard, selectVisibilityPixels, buildVisibilityTasks,
+ * runVisibilityTasks, shadePixelGI, upsampleAndResolve (with the given history;
+ * hist_valid = 0 for none), contactGI (radius = contactRadiusFrac * cascade-0
+ * spacing). Outputs (any may be NULL): half depth/src ((w+1)/2 x (h+1)/2), selection
+ * (quarter grid), sparse irradiance (3 per cell) / valid / anchor, resolved and
+ * indirect (3 doubles per pixel). Returns the number of visibility tasks. */
+int ora_gather_frame(const ora_stage* s, const sdfgi_gbuffer_pixel* gb, int w, int h, int frame, const sdfgi_cfg* cfg,
+                     const double* hist_irr, const double* hist_depth, int hist_valid, double* half_depth,
+                     int32_t* half_src, int32_t* sel, double* sparse_irr, int32_t* sparse_valid,
+                     int32_t* sparse_anchor, double* resolved, double* indirect, uint64_t vis_stats[8],
+                     uint64_t contact_stats[8]);
+
 #ifdef __cplusplus
 }
 #endif

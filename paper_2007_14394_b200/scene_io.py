@@ -110,6 +110,23 @@ RAY_DTYPE = np.dtype(
         ("steps", "<i4"),
     ]
 )
+GBUFFER_DTYPE = np.dtype(
+    [
+        ("depth", "<f8"),
+        ("normal", "<f8", (3,)),
+        ("albedo", "<f8", (3,)),
+        ("emission", "<f8", (3,)),
+        ("world_pos", "<f8", (3,)),
+        ("motion", "<f8", (2,)),
+        ("prim_index", "<i4"),
+        ("_pad", "<i4"),
+    ]
+)
+CAMERA_DTYPE = np.dtype(
+    [("position", "<f8", (3,)), ("forward", "<f8", (3,)), ("right", "<f8", (3,)), ("up", "<f8", (3,)),
+     ("fov_y_deg", "<f8")]
+)
+assert GBUFFER_DTYPE.itemsize == 128 and CAMERA_DTYPE.itemsize == 104
 assert PRIM_DTYPE.itemsize == 184 and LIGHT_DTYPE.itemsize == 80
 assert CLUSTER_DTYPE.itemsize == 56 and CFG_DTYPE.itemsize == 224
 assert PROBE_DTYPE.itemsize == 88 and RAY_DTYPE.itemsize == 96

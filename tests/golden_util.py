@@ -48,3 +48,28 @@ class Case:
 
 def load(name):
     return Case(name)
+
+
+GATHER_CASES = sorted(d for d in CASES if d.startswith("gather_"))
+CASES = [d for d in CASES if not d.startswith("gather_")]
+
+
+class GatherCase:
+    """A C3 fixture: probe passes of the source case, G-buffer, two gather frames."""
+
+    def __init__(self, name):
+        d = os.path.join(GOLDEN, name)
+        with open(os.path.join(d, "summary.json")) as f:
+            self.summary = json.load(f)
+        with np.load(os.path.join(d, "data.npz")) as z:
+            self.data = {k: z[k] for k in z.files}
+        self.src = Case(self.summary["src"])
+        self.scene = self.src.scene
+        self.w, self.h = self.summary["size"]
+        args = self.summary["args"]
+        self.passes = int(args[args.index("--passes") + 1])
+        self.frames = self.summary["frames"]
+
+
+def load_gather(name):
+    return GatherCase(name)
