@@ -289,6 +289,27 @@ SDFGI_API int sdfgi_accel_info(void* ctx, int64_t out[6]);
  * function (no context, no device). */
 SDFGI_API int sdfgi_slab_range(int res_x, int res_y, int res_z, int rank, int world, int* lo, int* hi);
 
+/* ------------------------------------------------------------ gather (e) */
+/* Input G-buffer (renderGBuffer, shading.hpp:39-72): upload the caller's, or render
+ * it on the device from the camera (prev_cam NULL = same camera, motion 0). */
+SDFGI_API int sdfgi_gbuffer_upload(void* ctx, int w, int h, const sdfgi_gbuffer_pixel* px);
+SDFGI_API int sdfgi_gbuffer_render(void* ctx, const sdfgi_camera* cam, const sdfgi_camera* prev_cam, int w, int h,
+                                   const sdfgi_cfg* cfg);
+SDFGI_API int sdfgi_gbuffer_download(void* ctx, sdfgi_gbuffer_pixel* out, size_t n_pixels);
+/* One gather frame of renderFrame (pipeline.hpp:161-207) against the FRONT atlas
+ * (prevField): downsampleDepthCheckerboard, selectVisibilityPixels,
+ * buildVisibilityTasks + runVisibilityTasks + shadePixelGI, upsampleAndResolve with
+ * the context's history, contactGI; then rolls the history (pipeline.hpp:213-218). */
+SDFGI_API int sdfgi_gather(void* ctx, int frame, const sdfgi_cfg* cfg, int64_t* n_tasks, sdfgi_stats* vis_stats,
+                           sdfgi_stats* contact_stats);
+SDFGI_API int sdfgi_gather_reset_history(void* ctx);
+/* which: 0 resolved E, 1 indirect (contactGI output), 2 half-res depth, 3 half-res
+ * source pixel, 4 selection, 5 sparse irradiance, 6 sparse valid, 7 sparse anchor.
+ * Doubles for 0,1,2,5 (3 per pixel/cell for 0,1,5), int32 otherwise. */
+SDFGI_API int sdfgi_gather_download(void* ctx, int which, void* dst, size_t bytes);
+/* Device ms of the last gather: {downsample+select, tiles, resolve, contact}. */
+SDFGI_API int sdfgi_last_gather_ms(void* ctx, double out[4]);
+
 /* Launch counter: kernels this context has launched since creation. */
 SDFGI_API int sdfgi_launch_count(void* ctx, int64_t* out);
 

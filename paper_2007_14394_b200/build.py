@@ -28,7 +28,7 @@ UNITS = {
     "sdfgi_abi.cu": [],
     "fp_peak.cu": [],
 }
-HEADERS = ["sdf_device.cuh", "kernels.cuh", "kernels_impl.cuh"]
+HEADERS = ["sdf_device.cuh", "kernels.cuh", "kernels_impl.cuh", "gather_impl.cuh"]
 
 
 def _nvcc():

@@ -95,6 +95,54 @@ template <typename R> struct WaveParams {
     int debug;
 };
 
+// Mirror of sdfgi_gbuffer_pixel (GBufferPixel, shading.hpp:13-22).
+struct GPix {
+    double depth;
+    double normal[3];
+    double albedo[3];
+    double emission[3];
+    double world_pos[3];
+    double motion[2];
+    int prim;
+    int _pad;
+};
+
+// Mirror of sdfgi_camera (Camera, camera.hpp:9-49).
+struct CameraDev {
+    double pos[3], fwd[3], right[3], up[3];
+    double fov;
+};
+
+// Gather (e) launch parameters: shading.hpp:85-477 over one G-buffer.
+template <typename R> struct GatherParams {
+    SceneView<R> scene;
+    ProbeCommon pc;
+    TraceCfg tc;
+    const float* atlas;  // front (previous) atlas, prevField of pipeline.hpp:127
+    int oct;
+    int w, h, hw, hh, sw, sh;
+    int frame;
+    CameraDev cam, prevCam;
+    GPix* gb;
+    double* halfDepth;
+    int* halfSrc;
+    int* sel;
+    double* sparseIrr;
+    int* sparseValid;
+    int* sparseAnchor;
+    double* resolved;
+    double* indirect;
+    const double* histIrr;
+    const double* histDepth;
+    int histValid;
+    double dedupFrac, th1Frac, visK, depthSigmaFrac, historyBlend, contactRadius;
+    int contactSamples;
+    uint64_t seed;
+    unsigned long long* visStats;
+    unsigned long long* contactStats;
+    unsigned long long* taskCount;
+};
+
 struct QueryParams {
     SceneView<double> scene;
     const double* pts;
@@ -125,6 +173,10 @@ template <typename R>
 void launch_wavefront(const WaveParams<R>& p, int persistBlocks, bool stats, cudaStream_t st,
                       cudaEvent_t evStart, cudaEvent_t evEnd, long long* launches);
 void launch_fib_table(double* out, int n, cudaStream_t st);
+// stage 0 G-buffer, 1 downsample+select, 2 tiles (tasks+visibility+shadePixelGI),
+// 3 resolve, 4 contact
+template <typename R>
+void launch_gather(const GatherParams<R>& p, int stage, bool stats, cudaStream_t st);
 void launch_relocate(const RelocParams& p, int nProbes, bool stats, cudaStream_t st);
 void launch_query_points(const QueryParams& p, cudaStream_t st);
 void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st);

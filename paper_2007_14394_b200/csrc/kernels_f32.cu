@@ -2,10 +2,13 @@
 // positions, stencils, MVC, atlas lookups and relocation stay FP64; the sphere
 // traces, soft shadows and the texel convolution run in FP32.
 #include "kernels_impl.cuh"
+#include "gather_impl.cuh"
 
 namespace sdfgi_dev {
 
 template void launch_wavefront<float>(const WaveParams<float>&, int, bool, cudaStream_t, cudaEvent_t, cudaEvent_t,
                                       long long*);
+
+template void launch_gather<float>(const GatherParams<float>&, int, bool, cudaStream_t);
 
 }  // namespace sdfgi_dev

@@ -2,6 +2,7 @@
 // every product and sum rounds separately, matching the reference built with
 // -ffp-contract=off (SURVEY §7 hard part 1); sqrt and division are IEEE.
 #include "kernels_impl.cuh"
+#include "gather_impl.cuh"
 
 namespace sdfgi_dev {
 
@@ -109,5 +110,7 @@ void launch_fib_table(double* out, int n, cudaStream_t st) { k_fib_table<<<(n + 
 
 template void launch_wavefront<double>(const WaveParams<double>&, int, bool, cudaStream_t, cudaEvent_t, cudaEvent_t,
                                        long long*);
+
+template void launch_gather<double>(const GatherParams<double>&, int, bool, cudaStream_t);
 
 }  // namespace sdfgi_dev

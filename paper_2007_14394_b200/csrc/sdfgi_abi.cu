@@ -160,6 +160,14 @@ struct Ctx {
     DBuf<unsigned char> wHits, wVis;
     DBuf<unsigned long long> wCtr;
     int persistCap = 0;  // 0 = occupancy-sized persistent grids
+    // gather (e): G-buffer, stage buffers, history (pipeline.hpp:213-218)
+    int gw = 0, gh = 0;
+    DBuf<GPix> gbuf;
+    DBuf<double> halfDepth, sparseIrr, resolved, indirect, histIrr, histDepth;
+    DBuf<int> halfSrc, sel, sparseValid, sparseAnchor;
+    int histValid = 0;
+    cudaEvent_t gev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    bool gevValid = false;
     DBuf<double> qpts, qinit, qd;
     DBuf<int> qowner;
 
@@ -175,6 +183,10 @@ struct Ctx {
         records.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
         wRayCount.free(); wHitList.free(); wRayStart.free(); wRot.free(); fib.free(); wHits.free();
         wVis.free(); wCtr.free(); perm.free();
+        gbuf.free(); halfDepth.free(); sparseIrr.free(); resolved.free(); indirect.free(); histIrr.free();
+        histDepth.free(); halfSrc.free(); sel.free(); sparseValid.free(); sparseAnchor.free();
+        for (auto& e : gev)
+            if (e) cudaEventDestroy(e);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (comm) ncclCommDestroy(comm);
@@ -1294,6 +1306,253 @@ int sdfgi_accel_info(void* ctx, int64_t out[6]) {
         out[3] = c->grid.dim[1];
         out[4] = c->grid.dim[2];
         out[5] = c->gridEntries;
+    });
+}
+
+}  // extern "C"
+
+namespace {
+
+CameraDev toCam(const sdfgi_camera& c) {
+    CameraDev d;
+    for (int k = 0; k < 3; ++k) {
+        d.pos[k] = c.position[k];
+        d.fwd[k] = c.forward[k];
+        d.right[k] = c.right[k];
+        d.up[k] = c.up[k];
+    }
+    d.fov = c.fov_y_deg;
+    return d;
+}
+
+void ensureGather(Ctx* c, int w, int h) {
+    REQ(w > 0 && h > 0 && static_cast<long long>(w) * h < (1LL << 28), SDFGI_ERR_INVALID, "bad G-buffer size");
+    if (w != c->gw || h != c->gh) c->histValid = 0;
+    c->gw = w;
+    c->gh = h;
+    const size_t np = static_cast<size_t>(w) * h;
+    const int hw = (w + 1) / 2, hh = (h + 1) / 2, sw = (hw + 1) / 2, sh = (hh + 1) / 2;
+    c->gbuf.alloc(np);
+    c->halfDepth.alloc(static_cast<size_t>(hw) * hh);
+    c->halfSrc.alloc(static_cast<size_t>(hw) * hh);
+    c->sel.alloc(static_cast<size_t>(sw) * sh);
+    c->sparseIrr.alloc(3 * static_cast<size_t>(sw) * sh);
+    c->sparseValid.alloc(static_cast<size_t>(sw) * sh);
+    c->sparseAnchor.alloc(static_cast<size_t>(sw) * sh);
+    c->resolved.alloc(3 * np);
+    c->indirect.alloc(3 * np);
+    c->histIrr.alloc(3 * np);
+    c->histDepth.alloc(np);
+    for (auto& e : c->gev)
+        if (!e) CK(cudaEventCreate(&e));
+}
+
+template <typename R>
+GatherParams<R> gatherParams(Ctx* c, const sdfgi_cfg* cfg, int frame) {
+    GatherParams<R> p;
+    std::memset(&p, 0, sizeof(p));
+    p.scene = c->sceneView<R>();
+    p.pc = c->probeCommon();
+    p.tc.eps = cfg->surface_epsilon;
+    p.tc.rayTMax = cfg->ray_tmax;
+    p.tc.shadowK = cfg->shadow_k;
+    p.tc.bounceCoeff = cfg->bounce_coeff;
+    p.tc.mvcFrac = cfg->mvc_relocation_frac;
+    p.tc.maxSteps = static_cast<int>(cfg->max_trace_steps);
+    p.tc.shadowSteps = static_cast<int>(cfg->shadow_steps);
+    p.atlas = c->cascades.empty() ? nullptr : c->atlas[c->front].p;
+    p.oct = c->octRes;
+    p.w = c->gw;
+    p.h = c->gh;
+    p.hw = (p.w + 1) / 2;
+    p.hh = (p.h + 1) / 2;
+    p.sw = (p.hw + 1) / 2;
+    p.sh = (p.hh + 1) / 2;
+    p.frame = frame;
+    p.gb = c->gbuf.p;
+    p.halfDepth = c->halfDepth.p;
+    p.halfSrc = c->halfSrc.p;
+    p.sel = c->sel.p;
+    p.sparseIrr = c->sparseIrr.p;
+    p.sparseValid = c->sparseValid.p;
+    p.sparseAnchor = c->sparseAnchor.p;
+    p.resolved = c->resolved.p;
+    p.indirect = c->indirect.p;
+    p.histIrr = c->histIrr.p;
+    p.histDepth = c->histDepth.p;
+    p.histValid = c->histValid;
+    p.dedupFrac = cfg->dedup_quant_frac;
+    p.th1Frac = cfg->threshold1_frac;
+    p.visK = cfg->probe_visibility_k;
+    p.depthSigmaFrac = cfg->depth_sigma_frac;
+    p.historyBlend = cfg->history_blend;
+    // contactRadiusFrac * cascade-0 spacing (pipeline.hpp:200)
+    double sp0 = 1.0;
+    if (!c->cascades.empty()) sp0 = c->cascades[0].spacing / std::pow(2.0, c->cascades[0].level);
+    p.contactRadius = cfg->contact_radius_frac * sp0;
+    p.contactSamples = static_cast<int>(cfg->contact_samples);
+    p.seed = cfg->seed;
+    // visibility and contact counters share scratch[0..13]: sdfgi_gather reads the
+    // visibility ones and clears them before the contact pass
+    p.visStats = c->scratch.p;
+    p.contactStats = c->scratch.p;
+    p.taskCount = c->scratch.p + 19;
+    return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sdfgi_gbuffer_upload(void* ctx, int w, int h, const sdfgi_gbuffer_pixel* px) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(px, SDFGI_ERR_INVALID, "null pixels");
+        ensureGather(c, w, h);
+        static_assert(sizeof(GPix) == sizeof(sdfgi_gbuffer_pixel), "gbuffer mirror");
+        CK(cudaMemcpyAsync(c->gbuf.p, px, sizeof(GPix) * static_cast<size_t>(w) * h, cudaMemcpyHostToDevice,
+                           c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int sdfgi_gbuffer_render(void* ctx, const sdfgi_camera* cam, const sdfgi_camera* prev_cam, int w, int h,
+                         const sdfgi_cfg* cfg) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(c->haveScene, SDFGI_ERR_STATE, "scene not uploaded");
+        REQ(cam && cfg, SDFGI_ERR_INVALID, "null camera/cfg");
+        ensureGather(c, w, h);
+        if (c->precision == SDFGI_F64) {
+            GatherParams<double> p = gatherParams<double>(c, cfg, 0);
+            p.cam = toCam(*cam);
+            p.prevCam = toCam(prev_cam ? *prev_cam : *cam);
+            launch_gather<double>(p, 0, false, c->stream);
+        } else {
+            GatherParams<float> p = gatherParams<float>(c, cfg, 0);
+            p.cam = toCam(*cam);
+            p.prevCam = toCam(prev_cam ? *prev_cam : *cam);
+            launch_gather<float>(p, 0, false, c->stream);
+        }
+        checkLaunch(c);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int sdfgi_gbuffer_download(void* ctx, sdfgi_gbuffer_pixel* out, size_t n_pixels) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(out && n_pixels == static_cast<size_t>(c->gw) * c->gh && n_pixels > 0, SDFGI_ERR_INVALID,
+            "G-buffer size mismatch");
+        CK(cudaMemcpyAsync(out, c->gbuf.p, sizeof(GPix) * n_pixels, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int sdfgi_gather(void* ctx, int frame, const sdfgi_cfg* cfg, int64_t* n_tasks, sdfgi_stats* vis_stats,
+                 sdfgi_stats* contact_stats) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        requireProbes(c);
+        REQ(cfg, SDFGI_ERR_INVALID, "null cfg");
+        REQ(c->gw > 0 && c->gbuf.p, SDFGI_ERR_STATE, "no G-buffer (upload or render one first)");
+        REQ(cfg->oct_res == c->octRes, SDFGI_ERR_INVALID, "cfg.oct_res differs from the atlas resolution");
+        const bool st = vis_stats != nullptr || contact_stats != nullptr;
+        CK(cudaMemsetAsync(c->scratch.p, 0, 32 * 8, c->stream));
+        CK(cudaEventRecord(c->gev[0], c->stream));
+        auto run = [&](auto p) {
+            launch_gather(p, 1, st, c->stream);  // downsample + select
+            CK(cudaEventRecord(c->gev[1], c->stream));
+            launch_gather(p, 2, st, c->stream);  // tiles: tasks + visibility + shadePixelGI
+            CK(cudaEventRecord(c->gev[2], c->stream));
+            launch_gather(p, 3, st, c->stream);  // upsample + temporal resolve
+            CK(cudaEventRecord(c->gev[3], c->stream));
+            return p;
+        };
+        unsigned long long visH[32];
+        if (c->precision == SDFGI_F64) {
+            auto p = run(gatherParams<double>(c, cfg, frame));
+            CK(cudaMemcpyAsync(visH, c->scratch.p, sizeof(visH), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            CK(cudaMemsetAsync(c->scratch.p, 0, 19 * 8, c->stream));
+            launch_gather(p, 4, st, c->stream);
+        } else {
+            auto p = run(gatherParams<float>(c, cfg, frame));
+            CK(cudaMemcpyAsync(visH, c->scratch.p, sizeof(visH), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            CK(cudaMemsetAsync(c->scratch.p, 0, 19 * 8, c->stream));
+            launch_gather(p, 4, st, c->stream);
+        }
+        c->launches += 5;
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(c->gev[4], c->stream));
+        c->gevValid = true;
+        unsigned long long conH[32];
+        CK(cudaMemcpyAsync(conH, c->scratch.p, sizeof(conH), cudaMemcpyDeviceToHost, c->stream));
+        // roll history (pipeline.hpp:213-218): resolved E and this frame's depth
+        const size_t np = static_cast<size_t>(c->gw) * c->gh;
+        CK(cudaMemcpyAsync(c->histIrr.p, c->resolved.p, 3 * np * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaMemcpy2DAsync(c->histDepth.p, sizeof(double), c->gbuf.p, sizeof(GPix), sizeof(double), np,
+                             cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        c->histValid = 1;
+        auto fill = [](sdfgi_stats* s, const unsigned long long* h) {
+            if (!s) return;
+            s->sdf_queries += h[0];
+            s->clusters_visited += h[1];
+            s->clusters_skipped += h[2];
+            s->primitive_evals += h[3];
+            s->trace_steps += h[4];
+            s->sphere_traces += h[5];
+            s->shadow_traces += h[6];
+            s->visibility_traces += h[7];
+        };
+        fill(vis_stats, visH);
+        fill(contact_stats, conH);
+        if (n_tasks) *n_tasks = static_cast<int64_t>(visH[19]);
+    });
+}
+
+int sdfgi_gather_reset_history(void* ctx) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        c->histValid = 0;
+    });
+}
+
+int sdfgi_gather_download(void* ctx, int which, void* dst, size_t bytes) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(dst, SDFGI_ERR_INVALID, "null dst");
+        const void* src = nullptr;
+        size_t n = 0;
+        switch (which) {
+            case 0: src = c->resolved.p; n = c->resolved.n * 8; break;
+            case 1: src = c->indirect.p; n = c->indirect.n * 8; break;
+            case 2: src = c->halfDepth.p; n = c->halfDepth.n * 8; break;
+            case 3: src = c->halfSrc.p; n = c->halfSrc.n * 4; break;
+            case 4: src = c->sel.p; n = c->sel.n * 4; break;
+            case 5: src = c->sparseIrr.p; n = c->sparseIrr.n * 8; break;
+            case 6: src = c->sparseValid.p; n = c->sparseValid.n * 4; break;
+            case 7: src = c->sparseAnchor.p; n = c->sparseAnchor.n * 4; break;
+            default: throw Error(SDFGI_ERR_INVALID, "unknown gather buffer");
+        }
+        REQ(src && bytes == n, SDFGI_ERR_INVALID, "gather buffer size mismatch");
+        CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int sdfgi_last_gather_ms(void* ctx, double out[4]) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(out && c->gevValid, SDFGI_ERR_STATE, "no gather timed yet");
+        CK(cudaStreamSynchronize(c->stream));
+        for (int i = 0; i < 4; ++i) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, c->gev[i], c->gev[i + 1]));
+            out[i] = ms;
+        }
     });
 }
 

@@ -57,6 +57,13 @@ _SIGS = {
     "sdfgi_set_accel": [_P, _I],
     "sdfgi_accel_info": [_P, _P],
     "sdfgi_slab_range": [_I, _I, _I, _I, _I, _P, _P],
+    "sdfgi_gbuffer_upload": [_P, _I, _I, _P],
+    "sdfgi_gbuffer_render": [_P, _P, _P, _I, _I, _P],
+    "sdfgi_gbuffer_download": [_P, _P, _SZ],
+    "sdfgi_gather": [_P, _I, _P, _P, _P, _P],
+    "sdfgi_gather_reset_history": [_P],
+    "sdfgi_gather_download": [_P, _I, _P, _SZ],
+    "sdfgi_last_gather_ms": [_P, _P],
     "sdfgi_launch_count": [_P, _P],
 }
 
@@ -105,6 +112,14 @@ def _call(name, *args):
     if rc != 0:
         raise SdfgiError(name, rc, lib.sdfgi_last_error().decode())
     return rc
+
+
+def camera_struct(cam) -> np.ndarray:
+    """scene_io.Camera -> sdfgi_camera (1-element array)."""
+    c = np.zeros(1, sio.CAMERA_DTYPE)
+    c["position"], c["forward"], c["right"], c["up"] = cam.position, cam.forward, cam.right, cam.up
+    c["fov_y_deg"] = cam.fov_y
+    return c
 
 
 def device_count() -> int:
@@ -190,6 +205,56 @@ class Device:
         _call("sdfgi_accel_info", self._ctx, _ptr(out))
         return {"mode": int(out[0]), "grid": bool(out[1]), "dim": tuple(int(x) for x in out[2:5]),
                 "entries": int(out[5])}
+
+    # ---------------------------------------------------------- gather (e)
+    def upload_gbuffer(self, w, h, pixels):
+        px = np.ascontiguousarray(pixels, sio.GBUFFER_DTYPE)
+        assert len(px) == w * h
+        _call("sdfgi_gbuffer_upload", self._ctx, int(w), int(h), _ptr(px))
+        self.gsize = (int(w), int(h))
+
+    def render_gbuffer(self, camera, w, h, cfg, prev_camera=None):
+        cam = camera_struct(camera)
+        prev = None if prev_camera is None else camera_struct(prev_camera)
+        cfg = np.ascontiguousarray(cfg, sio.CFG_DTYPE)
+        _call("sdfgi_gbuffer_render", self._ctx, _ptr(cam), _ptr(prev), int(w), int(h), _ptr(cfg))
+        self.gsize = (int(w), int(h))
+
+    def gbuffer(self):
+        w, h = self.gsize
+        out = np.zeros(w * h, sio.GBUFFER_DTYPE)
+        _call("sdfgi_gbuffer_download", self._ctx, _ptr(out), out.size)
+        return out
+
+    def gather(self, frame, cfg, stats=False):
+        """One gather frame; returns the number of visibility tasks (and stats)."""
+        cfg = np.ascontiguousarray(cfg, sio.CFG_DTYPE)
+        n = ctypes.c_int64()
+        vs = np.zeros(1, sio.STATS_DTYPE) if stats else None
+        cs = np.zeros(1, sio.STATS_DTYPE) if stats else None
+        _call("sdfgi_gather", self._ctx, int(frame), _ptr(cfg), ctypes.byref(n), _ptr(vs), _ptr(cs))
+        return (n.value, vs[0], cs[0]) if stats else n.value
+
+    def reset_history(self):
+        _call("sdfgi_gather_reset_history", self._ctx)
+
+    def gather_buffer(self, name):
+        w, h = self.gsize
+        hw, hh = (w + 1) // 2, (h + 1) // 2
+        sw, sh = (hw + 1) // 2, (hh + 1) // 2
+        spec = {"resolved": (0, w * h * 3, np.float64), "indirect": (1, w * h * 3, np.float64),
+                "half_depth": (2, hw * hh, np.float64), "half_src": (3, hw * hh, np.int32),
+                "sel": (4, sw * sh, np.int32), "sparse_irr": (5, sw * sh * 3, np.float64),
+                "sparse_valid": (6, sw * sh, np.int32), "sparse_anchor": (7, sw * sh, np.int32)}
+        which, n, dt = spec[name]
+        out = np.zeros(n, dt)
+        _call("sdfgi_gather_download", self._ctx, which, _ptr(out), out.nbytes)
+        return out
+
+    def last_gather_ms(self):
+        out = np.zeros(4)
+        _call("sdfgi_last_gather_ms", self._ctx, _ptr(out))
+        return out
 
     def launch_count(self) -> int:
         n = ctypes.c_int64()
