@@ -191,10 +191,14 @@ __global__ void __launch_bounds__(128) k_tiles(GatherParams<R> P) {
         key[4] = static_cast<int>(floor(wp.z / quant));
     }
     // dedup: the first lane (insertion order) holding the same key owns the task
+    // (every lane executes every shuffle: no short-circuit around __shfl_sync)
     int owner = lane;
     for (int j = 0; j < 32; ++j) {
-        bool same = __shfl_sync(kFull, has, j);
-        for (int k = 0; k < 5; ++k) same = same && (__shfl_sync(kFull, key[k], j) == key[k]);
+        int same = __shfl_sync(kFull, has ? 1 : 0, j);
+        for (int k = 0; k < 5; ++k) {
+            const int kj = __shfl_sync(kFull, key[k], j);
+            same &= kj == key[k] ? 1 : 0;
+        }
         if (has && same && j < owner) owner = j;
     }
     Counters cnt;

@@ -81,15 +81,17 @@ def test_gather_1080p_properties(dev):
     stage = api.ProbeStage(dev, scene)
     for p in range(3):
         stage.run_pass(p)
+    # G-buffer parity with the oracle at a size the CPU finishes quickly
+    sw, sh = 160, 90
+    dev.render_gbuffer(scene.camera, sw, sh, stage.cfg)
+    small = dev.gbuffer()
+    ogb, _ = oracle_py.Stage(scene).render_gbuffer(sw, sh)
+    assert np.array_equal(np.isfinite(small["depth"]), np.isfinite(ogb["depth"]))
+    geo = np.isfinite(ogb["depth"])
+    assert np.mean(small["prim_index"][geo] == ogb["prim_index"][geo]) > 0.999
     w, h = 1920, 1080
     dev.render_gbuffer(scene.camera, w, h, stage.cfg)
     gb = dev.gbuffer()
-    ora = oracle_py.Stage(scene)
-    rows = [0, 137, 540, 1079]
-    ogb, _ = ora.render_gbuffer(w, h)  # full oracle G-buffer is a few seconds of CPU
-    for r in rows:
-        a, b = gb[r * w:(r + 1) * w], ogb[r * w:(r + 1) * w]
-        assert np.array_equal(np.isfinite(a["depth"]), np.isfinite(b["depth"]))
     dev.reset_history()
     for f in range(2):
         dev.gather(f, stage.cfg)
