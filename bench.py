@@ -240,6 +240,7 @@ def run_ours(args, rank, world, local_rank):
 
     # e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e_val, h2d, d2h = e2e_run(args, dev, stage, scene, barrier, dist, torch)
+    gather = gather_bench(args, dev, stage, scene, torch, ext, flush) if not args.no_gather else None
 
     # roofline of the dominant kernel (k_probe_update): algorithmic ops / kernel time
     f64_rate, f32_rate = dev.measure_fp_peak()
@@ -290,6 +291,8 @@ def run_ours(args, rank, world, local_rank):
         "roofline": roofline,
         "clocks": clk.summary(),
         "algorithmic_counters_step": work_all,
+        "gather_c3": gather,
+        "frame_ms_update_plus_gather": (ms_step + gather["ms_per_frame"]) if gather else None,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(rays_step)
@@ -340,6 +343,69 @@ def e2e_run(args, dev, stage, scene, barrier, dist, torch):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total = float(tt.item())
     return rays * steps / total / 1e9, h2d, d2h
+
+
+def gather_bench(args, dev, stage, scene, torch, ext, flush):
+    """C3: 1920x1080 gather on the C2 volume after its 3 bounces. The
+    G-buffer is the gather's input (rendered once on the device, not timed, as the
+    reference's t_gbuffer is separate, pipeline.hpp:155-159); each timed frame runs
+    the whole gather (downsample, selection, tile visibility + shadePixelGI, resolve
+    with history, Contact GI) against the front atlas, L2 flushed before it."""
+    w, h = 1920, 1080
+    cfg = stage.cfg
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(ext)
+    dev.render_gbuffer(scene.camera, w, h, cfg)
+    e1.record(ext)
+    e1.synchronize()
+    gbuffer_ms = e0.elapsed_time(e1)
+    dev.reset_history()
+    tasks, vs, cs = dev.gather(0, cfg, stats=True)
+    for f in range(1, args.warmup + 1):
+        dev.gather(f, cfg)
+    times, stages = [], []
+    for k in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        e0.record(ext)
+        dev.gather(args.warmup + 1 + k, cfg)
+        e1.record(ext)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        stages.append(dev.last_gather_ms())
+    st = np.median(np.array(stages), axis=0)
+    res = {
+        "config": "C3: 1920x1080, frame with history, C2 scene and volume after 3 bounces",
+        "ms_per_frame": float(np.median(times)),
+        "stage_ms": {"downsample_select": st[0], "tiles_visibility_shadePixelGI": st[1], "resolve": st[2],
+                     "contact_gi": st[3]},
+        "gbuffer_ms_input": gbuffer_ms,
+        "visibility_tasks": int(tasks),
+        "visibility_traces_per_pixel": int(vs["visibility_traces"]) / (w * h),
+        "contact_rays_per_pixel": int(cs["sphere_traces"]) / (w * h),
+        "contact_sdf_queries_per_pixel": int(cs["sdf_queries"]) / (w * h),
+    }
+    if not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_gather_baseline()
+    return res
+
+
+def cpu_gather_baseline():
+    """The reference gather (pipeline.hpp:161-207) on all host threads at 480x270
+    (1/16 of the 1080p pixels; 3 probe passes of 32 rays seed the atlas), frame 1."""
+    exe = ref_binary()
+    if exe is None:
+        return None
+    threads = cpu_threads()
+    cmd = [exe, "gather", C2_PATH, os.devnull, "--passes", "1", "--nrays", "32", "--threads", str(threads),
+           "--size", "480", "270", "--gather-frames", "2", "--no-dump"]
+    r = subprocess.run(cmd, capture_output=True, text=True, check=True)
+    out = json.loads(r.stdout)
+    f = out["frames"][1]
+    ms = f["visibility_ms"] + f["resolve_ms"] + f["contact_ms"]
+    return {"ms_per_frame_sample": ms, "ms_per_frame_1080p_scaled": ms * 16, "cores": threads,
+            "kind": "reference", "sample": "480x270 (1/16 of 1080p pixels), frame with history; scaled x16"}
 
 
 def cpu_baseline(rays_full_step):
@@ -405,6 +471,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gather", action="store_true", help="skip the C3 1080p gather measurement")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))
