@@ -331,20 +331,37 @@ __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int*
             }
         }
     } else {
-        // off the grid: superclusters, then the unbounded clusters
-        for (int sc = 0; sc < g.nSuper; ++sc) {
-            if (boxSkipped(g.superBox + 6 * sc, p, d)) continue;
-            for (int i = g.superStart[sc]; i < g.superStart[sc + 1]; ++i) {
-                const int k = g.superList[i];
-                if (clusterSkipped(s.clusters[k], p, d)) {
-                    if (ST) ++c->cs;
-                    continue;
-                }
-                visitMembers<R, ST, true>(s, k, p, d, own, c);
-            }
-        }
+        // off the grid: the unbounded clusters, then the supercluster nearest to p
+        // (seeds the running minimum), then every other supercluster against it
         const int u0 = g.superStart[g.nSuper];
         for (int i = u0; i < u0 + g.nUnbounded; ++i) visitMembers<R, ST, true>(s, g.superList[i], p, d, own, c);
+        int nearest = -1;
+        R best = R(INFINITY);
+        for (int sc = 0; sc < g.nSuper; ++sc) {
+            const double* b = g.superBox + 6 * sc;
+            R dx = smax(smax(R(b[0]) - p.x, p.x - R(b[3])), R(0));
+            R dy = smax(smax(R(b[1]) - p.y, p.y - R(b[4])), R(0));
+            R dz = smax(smax(R(b[2]) - p.z, p.z - R(b[5])), R(0));
+            R bs = dx * dx + dy * dy + dz * dz;
+            if (bs < best) {
+                best = bs;
+                nearest = sc;
+            }
+        }
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int sc = (pass ? 0 : nearest); sc < (pass ? g.nSuper : nearest + 1); ++sc) {
+                if (sc < 0 || (pass && sc == nearest)) continue;
+                if (boxSkipped(g.superBox + 6 * sc, p, d)) continue;
+                for (int i = g.superStart[sc]; i < g.superStart[sc + 1]; ++i) {
+                    const int k = g.superList[i];
+                    if (clusterSkipped(s.clusters[k], p, d)) {
+                        if (ST) ++c->cs;
+                        continue;
+                    }
+                    visitMembers<R, ST, true>(s, k, p, d, own, c);
+                }
+            }
+        }
     }
     if (owner) *owner = own;
     return d;

@@ -436,9 +436,13 @@ void buildGrid(Ctx* c, const sdfgi_prim* prims, const int32_t* member_idx, const
     }
     if (bounded == 0 || n < 2) return;
     double ext[3], scale = 0;
+    // the grid extends past the geometry so rays leaving the scene stay on the
+    // (cheap) candidate lists for their first steps; SDFGI_GRID_MARGIN overrides
+    const char* menv = std::getenv("SDFGI_GRID_MARGIN");
+    const double marginFrac = menv ? std::atof(menv) : 0.02;
     for (int a = 0; a < 3; ++a) {
         double e = hi[a] - lo[a];
-        double m = 0.02 * e + 1e-3;
+        double m = marginFrac * e + 1e-3;
         lo[a] -= m;
         hi[a] += m;
         ext[a] = hi[a] - lo[a];
