@@ -289,22 +289,37 @@ __device__ __forceinline__ bool boxSkipped(const double* b, V3<R> p, R d) {
     return d > R(0) ? boxSq >= d * d : boxSq > R(0);
 }
 
+// An SDF query in flight: the point, the running minimum/owner, and (inside the
+// candidate grid) the cursor over the cell's candidate list. queryBegin either
+// sets the cursor or — off the grid, or with the grid disabled — completes the
+// whole query at once; queryStep evaluates one candidate. Splitting the query
+// lets the persistent kernels interleave one evaluation per loop iteration with
+// per-lane ray state, so a lane whose query ends early moves on instead of
+// waiting for the slowest lane of its warp.
+template <typename R> struct QueryState {
+    V3<R> p;
+    R d;
+    int own;
+    int cur, end;
+};
+
 template <typename R, bool ST>
-__device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int* owner, Counters* c) {
-    R d = initD;
-    int own = -1;
+__device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R initD, QueryState<R>& q, Counters* c) {
+    q.p = p;
+    q.d = initD;
+    q.own = -1;
+    q.cur = q.end = 0;
     if (ST) ++c->q;
     if (!s.useGrid) {
         // the reference's walk: every cluster in order, strict `<`
         for (int k = 0; k < s.n_clusters; ++k) {
-            if (clusterSkipped(s.clusters[k], p, d)) {
+            if (clusterSkipped(s.clusters[k], p, q.d)) {
                 if (ST) ++c->cs;
                 continue;
             }
-            visitMembers<R, ST, false>(s, k, p, d, own, c);
+            visitMembers<R, ST, false>(s, k, p, q.d, q.own, c);
         }
-        if (owner) *owner = own;
-        return d;
+        return;
     }
     const GridDev& g = s.grid;
     R fx = (p.x - R(g.lo[0])) * R(g.invH);
@@ -315,56 +330,66 @@ __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int*
         int iy = min(static_cast<int>(fy), g.dim[1] - 1);
         int iz = min(static_cast<int>(fz), g.dim[2] - 1);
         int cell = ix + g.dim[0] * (iy + g.dim[1] * iz);
-        // the cell's candidate primitives, one evaluation per iteration
-        const int b = g.start[cell], e = g.start[cell + 1];
-        if (ST) c->pe += e - b;
-        for (int i = b; i < e; ++i) {
-            const int j = g.list[i];
-            if (ST) {
-                ++c->ek[s.prims[j].kind];
-                c->ek[5] += s.prims[j].identity ? 0 : 1;
-            }
-            const R pd = evalPrim(s.prims[j], p);
-            if (pd < d || (pd == d && own >= 0 && j < own)) {
-                d = pd;
-                own = j;
-            }
+        q.cur = g.start[cell];
+        q.end = g.start[cell + 1];
+        if (ST) c->pe += q.end - q.cur;
+        return;
+    }
+    // off the grid: the unbounded clusters, then the supercluster nearest to p
+    // (seeds the running minimum), then every other supercluster against it
+    const int u0 = g.superStart[g.nSuper];
+    for (int i = u0; i < u0 + g.nUnbounded; ++i) visitMembers<R, ST, true>(s, g.superList[i], p, q.d, q.own, c);
+    int nearest = -1;
+    R best = R(INFINITY);
+    for (int sc = 0; sc < g.nSuper; ++sc) {
+        const double* b = g.superBox + 6 * sc;
+        R dx = smax(smax(R(b[0]) - p.x, p.x - R(b[3])), R(0));
+        R dy = smax(smax(R(b[1]) - p.y, p.y - R(b[4])), R(0));
+        R dz = smax(smax(R(b[2]) - p.z, p.z - R(b[5])), R(0));
+        R bs = dx * dx + dy * dy + dz * dz;
+        if (bs < best) {
+            best = bs;
+            nearest = sc;
         }
-    } else {
-        // off the grid: the unbounded clusters, then the supercluster nearest to p
-        // (seeds the running minimum), then every other supercluster against it
-        const int u0 = g.superStart[g.nSuper];
-        for (int i = u0; i < u0 + g.nUnbounded; ++i) visitMembers<R, ST, true>(s, g.superList[i], p, d, own, c);
-        int nearest = -1;
-        R best = R(INFINITY);
-        for (int sc = 0; sc < g.nSuper; ++sc) {
-            const double* b = g.superBox + 6 * sc;
-            R dx = smax(smax(R(b[0]) - p.x, p.x - R(b[3])), R(0));
-            R dy = smax(smax(R(b[1]) - p.y, p.y - R(b[4])), R(0));
-            R dz = smax(smax(R(b[2]) - p.z, p.z - R(b[5])), R(0));
-            R bs = dx * dx + dy * dy + dz * dz;
-            if (bs < best) {
-                best = bs;
-                nearest = sc;
-            }
-        }
-        for (int pass = 0; pass < 2; ++pass) {
-            for (int sc = (pass ? 0 : nearest); sc < (pass ? g.nSuper : nearest + 1); ++sc) {
-                if (sc < 0 || (pass && sc == nearest)) continue;
-                if (boxSkipped(g.superBox + 6 * sc, p, d)) continue;
-                for (int i = g.superStart[sc]; i < g.superStart[sc + 1]; ++i) {
-                    const int k = g.superList[i];
-                    if (clusterSkipped(s.clusters[k], p, d)) {
-                        if (ST) ++c->cs;
-                        continue;
-                    }
-                    visitMembers<R, ST, true>(s, k, p, d, own, c);
+    }
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int sc = (pass ? 0 : nearest); sc < (pass ? g.nSuper : nearest + 1); ++sc) {
+            if (sc < 0 || (pass && sc == nearest)) continue;
+            if (boxSkipped(g.superBox + 6 * sc, p, q.d)) continue;
+            for (int i = g.superStart[sc]; i < g.superStart[sc + 1]; ++i) {
+                const int k = g.superList[i];
+                if (clusterSkipped(s.clusters[k], p, q.d)) {
+                    if (ST) ++c->cs;
+                    continue;
                 }
+                visitMembers<R, ST, true>(s, k, p, q.d, q.own, c);
             }
         }
     }
-    if (owner) *owner = own;
-    return d;
+}
+
+// One candidate of the cell list (lowest-CSR-position tie-break: order-free).
+template <typename R, bool ST>
+__device__ __forceinline__ void queryStep(const SceneView<R>& s, QueryState<R>& q, Counters* c) {
+    const int j = s.grid.list[q.cur++];
+    if (ST) {
+        ++c->ek[s.prims[j].kind];
+        c->ek[5] += s.prims[j].identity ? 0 : 1;
+    }
+    const R pd = evalPrim(s.prims[j], q.p);
+    if (pd < q.d || (pd == q.d && q.own >= 0 && j < q.own)) {
+        q.d = pd;
+        q.own = j;
+    }
+}
+
+template <typename R, bool ST>
+__device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int* owner, Counters* c) {
+    QueryState<R> q;
+    queryBegin<R, ST>(s, p, initD, q, c);
+    while (q.cur < q.end) queryStep<R, ST>(s, q, c);
+    if (owner) *owner = q.own;
+    return q.d;
 }
 
 template <typename R> struct Hit {
