@@ -209,51 +209,44 @@ __device__ __forceinline__ V3<double> rayDirection(const WaveParams<R>& P, int s
 }
 
 // --------------------------------------------------------- K1 primary rays
-// sphereTrace (scene.hpp:391-435) as a per-lane state machine over the split
-// query: every loop iteration performs ONE candidate evaluation for each lane
-// whose query is open; a lane whose query has completed advances its own ray —
-// state 0 marches (next query at 2*lastD), state 1 is the owner-resolving query
-// at the converged point (d + 1e-9), state 2 the polish loop (t += d, 2|d| +
-// 1e-9, at most 8) — and opens its next query, or finishes the ray and takes the
-// next one, without waiting for the rest of the warp. Rays are assigned grid-
-// stride over the coherent (Morton-sorted direction) order, so the loop has no
-// warp-level synchronisation at all.
-template <typename R, bool ST>
-__device__ __forceinline__ bool primaryInit(const WaveParams<R>& P, long long item, unsigned long long& rid, V3<R>& o,
-                                            V3<R>& dir) {
-    const long long total = P.rayStart[P.nCand];
-    if (item >= total) return false;
-    const int s = findCandidate(P.rayStart, P.nCand, item);
-    const int j = static_cast<int>(item - P.rayStart[s]);
-    const int n = static_cast<int>(P.rayStart[s + 1] - P.rayStart[s]);
-    const int i = P.perm[(n == P.nRaysFull ? 0 : P.nRaysFull) + j];
-    rid = static_cast<unsigned long long>(P.rayStart[s] + i);
-    const int g = P.cand ? P.cand[s] : s;
-    const double* pp = P.pc.probes.pos + 3 * static_cast<size_t>(g);
-    const V3<double> dd = rayDirection(P, s, i, n);
-    o = mk(R(pp[0]), R(pp[1]), R(pp[2]));
-    dir = mk(R(dd.x), R(dd.y), R(dd.z));
-    return true;
-}
-
+// sphereTrace (scene.hpp:391-435) as a per-lane state machine: state 0 marches
+// (query at 2*lastD), state 1 is the owner-resolving query at the converged point
+// (d + 1e-9), state 2 the polish loop (t += d, 2|d| + 1e-9, at most 8). Every
+// iteration is exactly one query for every active lane.
 template <typename R, bool ST>
 __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P) {
+    const long long total = P.rayStart[P.nCand];
     const R eps = R(P.tc.eps), tMax = R(P.tc.rayTMax);
     const int maxSteps = P.tc.maxSteps;
-    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-    long long item = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     Counters cnt;
     cnt.zero();
+    bool active = false, exhausted = false;
     unsigned long long rid = 0;
-    V3<R> o, dir;
+    V3<R> o = mk(R(0), R(0), R(0)), dir = o;
     R t = 0, lastD = 0, d = 0;
     int step = 0, state = 0, pol = 0, owner = -1;
-    QueryState<R> q;
-    bool alive = false;
-    // open the first ray's first query (rays with maxSteps <= 0 never query)
-    auto startRay = [&]() {
-        while (primaryInit<R, ST>(P, item, rid, o, dir)) {
-            item += stride;
+    while (true) {
+        __syncwarp();
+        unsigned long long item;
+        if (fetchItem(P.ctr + 0, static_cast<unsigned long long>(total), active, exhausted, item)) {
+            const int s = findCandidate(P.rayStart, P.nCand, static_cast<long long>(item));
+            const int j = static_cast<int>(static_cast<long long>(item) - P.rayStart[s]);
+            const int n = static_cast<int>(P.rayStart[s + 1] - P.rayStart[s]);
+            // slot j traces sample i = perm[j]: consecutive lanes get neighbouring
+            // directions (coherent warps); results are stored by sample index
+            const int i = P.perm[(n == P.nRaysFull ? 0 : P.nRaysFull) + j];
+            rid = static_cast<unsigned long long>(P.rayStart[s] + i);
+            const int g = P.cand ? P.cand[s] : s;
+            const double* pp = P.pc.probes.pos + 3 * static_cast<size_t>(g);
+            V3<double> dd = rayDirection(P, s, i, n);
+            o = mk(R(pp[0]), R(pp[1]), R(pp[2]));
+            dir = mk(R(dd.x), R(dd.y), R(dd.z));
+            t = R(0);
+            lastD = R(INFINITY) * R(0.5);
+            step = 0;
+            state = 0;
+            owner = -1;
+            active = true;
             if (ST) ++cnt.sphere;
             if (maxSteps <= 0) {  // loop never runs: StepLimit
                 HitRec<R> h;
@@ -264,205 +257,200 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P)
                 h.owner = -1;
                 h.status = 2 << 1;
                 P.hits[rid] = h;
-                continue;
+                active = false;
             }
-            t = R(0);
-            lastD = R(INFINITY) * R(0.5);
-            step = 0;
-            state = 0;
-            owner = -1;
-            if (ST) ++cnt.steps;
-            queryBegin<R, ST>(P.scene, o, R(2) * lastD, q, &cnt);
-            return true;
         }
-        return false;
-    };
-    alive = startRay();
-    while (alive) {
-        if (q.cur < q.end) {
-            queryStep<R, ST>(P.scene, q, &cnt);
+        if (!__any_sync(kFull, active)) {
+            if (__all_sync(kFull, exhausted)) break;
             continue;
         }
-        // the open query is complete: advance this lane's ray
-        const R nd = q.d;
-        const int o2 = q.own;
-        const V3<R> p = q.p;
-        int done = 0;  // 1 converged, 2 TMax, 3 StepLimit
-        if (state == 0) {
-            if (nd < eps) {
-                d = nd;
-                state = 1;
-            } else if (nd >= tMax - t) {
-                done = 2;
-            } else {
-                t += nd;
-                lastD = nd;
-                if (++step >= maxSteps) done = 3;
-            }
-        } else {
-            d = nd;
-            if (state == 1) {
-                owner = o2;
-                pol = 0;
-                state = 2;
-            } else {
-                if (o2 >= 0) owner = o2;
-                ++pol;
-            }
-            if (!(pol < 8 && fabs(d) > R(0.25) * eps)) done = 1;
-        }
-        if (!done) {
-            R initD;
+        V3<R> p = o;
+        R initD = R(0);
+        if (active) {
+            if (state == 2) t += d;
+            p = o + dir * t;
             if (state == 0) {
                 if (ST) ++cnt.steps;
                 initD = R(2) * lastD;
             } else if (state == 1) {
                 initD = polishPad(d);
             } else {
-                t += d;
                 initD = polishPad(R(2) * fabs(d));
             }
-            queryBegin<R, ST>(P.scene, state == 1 ? p : o + dir * t, initD, q, &cnt);
-            continue;
         }
-        HitRec<R> h;
-        h.owner = -1;
-        h.n[0] = h.n[1] = R(0);
-        h.n[2] = R(1);
-        if (done == 1) {
-            h.p[0] = p.x;
-            h.p[1] = p.y;
-            h.p[2] = p.z;
-            h.t = t;
-            h.owner = owner;
-            if (owner >= 0) {
-                V3<R> nn = evalGradient(P.scene.prims[owner], p);
-                h.n[0] = nn.x;
-                h.n[1] = nn.y;
-                h.n[2] = nn.z;
+        int o2 = -1;
+        R nd = R(0);
+        if (active) nd = query<R, ST>(P.scene, p, initD, &o2, &cnt);
+        if (active) {
+            int done = 0;  // 1 converged, 2 TMax, 3 StepLimit
+            if (state == 0) {
+                if (nd < eps) {
+                    d = nd;
+                    state = 1;
+                } else if (nd >= tMax - t) {
+                    done = 2;
+                } else {
+                    t += nd;
+                    lastD = nd;
+                    if (++step >= maxSteps) done = 3;
+                }
+            } else {
+                d = nd;
+                if (state == 1) {
+                    owner = o2;
+                    pol = 0;
+                    state = 2;
+                } else {
+                    if (o2 >= 0) owner = o2;
+                    ++pol;
+                }
+                if (!(pol < 8 && fabs(d) > R(0.25) * eps)) done = 1;
             }
-            h.status = 1 | ((step + 1) << 8);
-        } else {
-            h.p[0] = h.p[1] = h.p[2] = R(0);
-            h.t = R(0);
-            h.status = ((done == 2 ? 1 : 2) << 1) | ((done == 2 ? step + 1 : maxSteps) << 8);
+            if (done) {
+                HitRec<R> h;
+                h.owner = -1;
+                h.n[0] = h.n[1] = R(0);
+                h.n[2] = R(1);
+                if (done == 1) {
+                    h.p[0] = p.x;
+                    h.p[1] = p.y;
+                    h.p[2] = p.z;
+                    h.t = t;
+                    h.owner = owner;
+                    if (owner >= 0) {
+                        V3<R> nn = evalGradient(P.scene.prims[owner], p);
+                        h.n[0] = nn.x;
+                        h.n[1] = nn.y;
+                        h.n[2] = nn.z;
+                    }
+                    h.status = 1 | ((step + 1) << 8);
+                } else {
+                    h.p[0] = h.p[1] = h.p[2] = R(0);
+                    h.t = R(0);
+                    h.status = ((done == 2 ? 1 : 2) << 1) | ((done == 2 ? step + 1 : maxSteps) << 8);
+                }
+                P.hits[rid] = h;
+                active = false;
+            }
+            // compaction of converged hits with an owner (the only ones shadeHit lights)
+            const bool lit = done == 1 && owner >= 0;
+            const unsigned m = __ballot_sync(__activemask(), lit);
+            if (lit) {
+                const int leader = __ffs(m) - 1;
+                const unsigned lane = threadIdx.x & 31;
+                unsigned long long base = 0;
+                if (static_cast<int>(lane) == leader) base = atomicAdd(P.ctr + 1, static_cast<unsigned long long>(__popc(m)));
+                base = __shfl_sync(m, base, leader);
+                P.hitList[base + __popc(m & ((1u << lane) - 1u))] = static_cast<int>(rid);
+            }
         }
-        P.hits[rid] = h;
-        alive = startRay();
     }
-    if (ST) {
-        __syncwarp();
-        flushCounters(cnt, P.stats);
-    }
+    if (ST) flushCounters(cnt, P.stats);
 }
 
 // ----------------------------------------------------------- K2 shadow rays
-// One (ray, light) item per lane at a time, light-major over the same coherent ray
-// order: directIrradiance's setup (probe_update.hpp:100-128) for converged hits
-// with an owner, then the softShadowTrace march (scene.hpp:459-476) over the split
-// query, one candidate evaluation per loop iteration. vis = 1 when the segment is
-// too short to trace; other items are skipped (K3 re-derives which lights apply).
+// One (converged hit, light) item per lane: directIrradiance's setup
+// (probe_update.hpp:100-128) and the softShadowTrace march (scene.hpp:459-476),
+// one query per iteration. vis = 1 when the segment is too short to trace.
 template <typename R, bool ST>
 __global__ void __launch_bounds__(kWaveThreads) k_trace_shadow(WaveParams<R> P) {
     const int L = P.scene.n_lights;
-    const long long nRays = P.rayStart[P.nCand];
-    const long long total = nRays * L;
+    const unsigned long long nHits = P.ctr[1];
+    const unsigned long long total = nHits * static_cast<unsigned long long>(L);
     const R minStep = R(5e-4), inf = R(INFINITY), k = R(P.tc.shadowK);
     const int maxSteps = P.tc.shadowSteps;
-    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-    long long item = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     Counters cnt;
     cnt.zero();
+    bool active = false, exhausted = false;
     unsigned long long slot = 0;
-    V3<R> o, dir;
+    V3<R> o = mk(R(0), R(0), R(0)), dir = o;
     R t = 0, tEnd = 0, v = 0, lastD = 0;
     int step = 0;
-    QueryState<R> q;
-    // next item that needs a march; trivially-resolved items are written on the way
-    auto startItem = [&]() {
-        while (item < total) {
-            const int li = static_cast<int>(item / nRays);
-            const long long ri = item % nRays;
-            item += stride;
-            const int s = findCandidate(P.rayStart, P.nCand, ri);
-            const int j = static_cast<int>(ri - P.rayStart[s]);
-            const int n = static_cast<int>(P.rayStart[s + 1] - P.rayStart[s]);
-            const long long rid = P.rayStart[s] + P.perm[(n == P.nRaysFull ? 0 : P.nRaysFull) + j];
-            const HitRec<R> h = P.hits[rid];
-            if (!(h.status & 1) || h.owner < 0) continue;  // miss / no owner: sky, no light
+    while (true) {
+        __syncwarp();
+        unsigned long long item;
+        if (fetchItem(P.ctr + 2, total, active, exhausted, item)) {
+            // light-major: consecutive lanes take consecutive hits toward the same light
+            const int rid = P.hitList[item % nHits];
+            const int li = static_cast<int>(item / nHits);
             slot = static_cast<unsigned long long>(rid) * L + li;
+            const HitRec<R>& h = P.hits[rid];
             const V3<R> pos = mk(h.p[0], h.p[1], h.p[2]);
             const V3<R> nrm = mk(h.n[0], h.n[1], h.n[2]);
             const DLight& Lt = P.scene.lights[li];
+            bool skip = false;
             R tMax = R(0);
             if (Lt.kind == 0) {
                 V3<R> toLight = mk(R(Lt.position[0]), R(Lt.position[1]), R(Lt.position[2])) - pos;
                 R r2 = dot(toLight, toLight);
-                if (r2 < R(1e-12)) continue;
-                R r = sqrt(r2);
-                dir = toLight / r;
-                if (dot(nrm, dir) <= R(0)) continue;
-                tMax = r;
+                if (r2 < R(1e-12)) {
+                    skip = true;
+                } else {
+                    R r = sqrt(r2);
+                    dir = toLight / r;
+                    if (dot(nrm, dir) <= R(0)) skip = true;
+                    tMax = r;
+                }
             } else if (Lt.kind == 1) {
                 dir = mk(R(-Lt.direction[0]), R(-Lt.direction[1]), R(-Lt.direction[2]));
-                if (dot(nrm, dir) <= R(0)) continue;
+                if (dot(nrm, dir) <= R(0)) skip = true;
                 tMax = R(P.tc.rayTMax);
             } else {
-                continue;
+                skip = true;
             }
-            const R cosT = dot(nrm, dir);
-            const R bias = R(2.0) * R(P.tc.eps) / smax(R(0.1), cosT);
-            if (!(tMax - bias > bias)) {
-                P.vis[slot] = R(1);
-                continue;
+            if (skip) {
+                P.vis[slot] = R(-1);
+            } else {
+                const R cosT = dot(nrm, dir);
+                const R bias = R(2.0) * R(P.tc.eps) / smax(R(0.1), cosT);
+                if (tMax - bias > bias) {
+                    if (ST) ++cnt.shadow;
+                    o = pos + nrm * bias;
+                    t = bias;
+                    tEnd = tMax - bias;
+                    v = R(1);
+                    lastD = inf;
+                    step = 0;
+                    active = true;
+                } else {
+                    P.vis[slot] = R(1);
+                }
             }
-            if (ST) ++cnt.shadow;
-            o = pos + nrm * bias;
-            t = bias;
-            tEnd = tMax - bias;
-            v = R(1);
-            lastD = inf;
-            step = 0;
-            if (!(step < maxSteps && t < tEnd)) {
+        }
+        if (!__any_sync(kFull, active)) {
+            if (__all_sync(kFull, exhausted)) break;
+            continue;
+        }
+        const bool want = active && step < maxSteps && t < tEnd;
+        V3<R> p = o;
+        if (want) {
+            if (ST) ++cnt.steps;
+            p = o + dir * t;
+        }
+        R d = R(0);
+        if (want) d = query<R, ST>(P.scene, p, lastD == inf ? inf : R(2) * lastD, nullptr, &cnt);
+        if (active) {
+            bool done = false;
+            if (!want) {
+                done = true;
+            } else {
+                v = smin(v, sclamp(k * d / t, R(0), R(1)));
+                if (v < R(1e-3)) {
+                    v = R(0);
+                    done = true;
+                } else {
+                    t += smax(d, minStep);
+                    lastD = smax(d, minStep);
+                    ++step;
+                }
+            }
+            if (done) {
                 P.vis[slot] = v;
-                continue;
+                active = false;
             }
-            if (ST) ++cnt.steps;
-            queryBegin<R, ST>(P.scene, o + dir * t, inf, q, &cnt);
-            return true;
         }
-        return false;
-    };
-    bool alive = startItem();
-    while (alive) {
-        if (q.cur < q.end) {
-            queryStep<R, ST>(P.scene, q, &cnt);
-            continue;
-        }
-        const R d = q.d;
-        bool done = false;
-        v = smin(v, sclamp(k * d / t, R(0), R(1)));
-        if (v < R(1e-3)) {
-            v = R(0);
-            done = true;
-        } else {
-            t += smax(d, minStep);
-            lastD = smax(d, minStep);
-            ++step;
-            if (!(step < maxSteps && t < tEnd)) done = true;
-        }
-        if (!done) {
-            if (ST) ++cnt.steps;
-            queryBegin<R, ST>(P.scene, o + dir * t, R(2) * lastD, q, &cnt);
-            continue;
-        }
-        P.vis[slot] = v;
-        alive = startItem();
     }
-    if (ST) {
-        __syncwarp();
-        flushCounters(cnt, P.stats);
-    }
+    if (ST) flushCounters(cnt, P.stats);
 }
 
 // ------------------------------------------------- K3 shade + convolve + blend
