@@ -439,7 +439,7 @@ void buildGrid(Ctx* c, const sdfgi_prim* prims, const int32_t* member_idx, const
     // the grid extends past the geometry so rays leaving the scene stay on the
     // (cheap) candidate lists for their first steps; SDFGI_GRID_MARGIN overrides
     const char* menv = std::getenv("SDFGI_GRID_MARGIN");
-    const double marginFrac = menv ? std::atof(menv) : 0.02;
+    const double marginFrac = menv ? std::atof(menv) : 0.3;  // measured on C2: 0.02 -> 0.3 = -23% K1+K2
     for (int a = 0; a < 3; ++a) {
         double e = hi[a] - lo[a];
         double m = marginFrac * e + 1e-3;
@@ -449,7 +449,9 @@ void buildGrid(Ctx* c, const sdfgi_prim* prims, const int32_t* member_idx, const
         scale = std::max(scale, std::max(std::fabs(lo[a]), std::fabs(hi[a])));
     }
     const char* env = std::getenv("SDFGI_GRID_CELLS");
-    double target = env ? std::atof(env) : 262144.0;
+    // finer cells -> smaller U -> shorter, more uniform candidate lists (C2: 8M cells,
+    // ~4 candidates per query); memory ~ 4 B/cell + 4 B/entry
+    double target = env ? std::atof(env) : 8388608.0;
     if (target < 1) return;
     double h = std::cbrt(ext[0] * ext[1] * ext[2] / target);
     int dim[3];
