@@ -84,6 +84,7 @@ template <typename R> struct WaveParams {
     HitRec<R>* hits;          // per ray
     int* hitList;             // compacted ray ids of converged hits with an owner
     R* vis;                   // per (ray, light)
+    R* rad;                   // per ray: shaded radiance (3)
     unsigned long long* ctr;  // [0] K1 ray cursor, [1] hit count, [2] K2 item cursor
     // results
     unsigned long long* stats;       // counters or null
@@ -183,7 +184,8 @@ void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st);
 void launch_grid_list(const GridBuildParams& p, int ncells, bool fill, cudaStream_t st);
 
 constexpr int kWaveThreads = 128;   // K1/K2 persistent CTAs
-constexpr int kShadeThreads = 128;  // K3 CTA per probe
+constexpr int kShadeThreads = 128;  // per-ray shading
+constexpr int kConvThreads = 192;   // K3b CTA per probe: one thread per (texel, channel) at R = 8
 constexpr int kScanThreads = 1024;  // K0 prefix sum
 
 }  // namespace sdfgi_dev

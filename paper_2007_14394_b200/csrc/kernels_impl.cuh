@@ -502,34 +502,25 @@ __device__ __forceinline__ V3<double> shadeRay(const WaveParams<R>& P, const Hit
     return radiance;
 }
 
+// K3a: shadeHit per ray (thread per ray, grid-stride): emission + directIrradiance
+// summed in light order with the K2 visibilities + the bounce lookup; radiance to
+// P.rad (3 per ray). Kept apart from the convolution so the stencil/MVC register
+// footprint does not cap the convolution's occupancy.
 template <typename R, bool ST>
-__global__ void __launch_bounds__(kShadeThreads) k_shade_convolve(WaveParams<R> P) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ __align__(16) float tile[12 * 12 * 3 + 4];
-    __shared__ unsigned long long redDelta[kShadeThreads / 32];
-
-    const int s = blockIdx.x;
-    const int n = P.rayCount[s];
-    if (n == 0) return;  // dead probe: its back tile is the copied front tile
-    const int g = P.cand ? P.cand[s] : s;
-    const ProbesView& pv = P.pc.probes;
-    const int reject = n != P.nRaysFull;  // 2N rays <=> rejectHistory at setup
-    const long long start = P.rayStart[s];
-    R* sdir = reinterpret_cast<R*>(smem_raw);  // 3n
-    R* srad = sdir + 3 * n;                    // 3n
-
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const unsigned long long rid = static_cast<unsigned long long>(start + i);
+__global__ void __launch_bounds__(128) k_shade_rays(WaveParams<R> P) {
+    const long long total = P.rayStart[P.nCand];
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long rid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; rid < total; rid += stride) {
         const HitRec<R> h = P.hits[rid];
-        V3<double> dir = rayDirection(P, s, i, n);
-        V3<double> L = shadeRay(P, h, rid);
-        sdir[3 * i] = R(dir.x);
-        sdir[3 * i + 1] = R(dir.y);
-        sdir[3 * i + 2] = R(dir.z);
-        srad[3 * i] = R(L.x);
-        srad[3 * i + 1] = R(L.y);
-        srad[3 * i + 2] = R(L.z);
+        const V3<double> L = shadeRay(P, h, static_cast<unsigned long long>(rid));
+        P.rad[3 * rid] = R(L.x);
+        P.rad[3 * rid + 1] = R(L.y);
+        P.rad[3 * rid + 2] = R(L.z);
         if (P.debug) {
+            const int s = findCandidate(P.rayStart, P.nCand, rid);
+            const int i = static_cast<int>(rid - P.rayStart[s]);
+            const int n = static_cast<int>(P.rayStart[s + 1] - P.rayStart[s]);
+            const V3<double> dir = rayDirection(P, s, i, n);
             RayRecord r;
             r.dir[0] = dir.x;
             r.dir[1] = dir.y;
@@ -549,7 +540,34 @@ __global__ void __launch_bounds__(kShadeThreads) k_shade_convolve(WaveParams<R> 
             P.records[rid] = r;
         }
     }
-    if (P.debug) return;
+}
+
+// K3b: one CTA per probe, one thread per (texel, channel): convolveIrradiance
+// (probe_update.hpp:25-34) — every channel summed over the rays in the
+// reference's order, so FP64 texels are bit-identical — hysteresis blend
+// (:192-206), fillBorder (atlas.hpp:44-56) in shared memory, 16-byte tile stores.
+template <typename R, bool ST>
+__global__ void __launch_bounds__(kConvThreads) k_convolve(WaveParams<R> P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ __align__(16) float tile[12 * 12 * 3 + 4];
+    __shared__ unsigned long long redDelta[kConvThreads / 32];
+
+    const int s = blockIdx.x;
+    const int n = P.rayCount[s];
+    if (n == 0) return;  // dead probe: its back tile is the copied front tile
+    const int g = P.cand ? P.cand[s] : s;
+    const ProbesView& pv = P.pc.probes;
+    const int reject = n != P.nRaysFull;  // 2N rays <=> rejectHistory at setup
+    const long long start = P.rayStart[s];
+    R* sdir = reinterpret_cast<R*>(smem_raw);  // 3n
+    R* srad = sdir + 3 * n;                    // 3n
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const V3<double> dir = rayDirection(P, s, i, n);
+        sdir[3 * i] = R(dir.x);
+        sdir[3 * i + 1] = R(dir.y);
+        sdir[3 * i + 2] = R(dir.z);
+    }
+    for (int k = threadIdx.x; k < 3 * n; k += blockDim.x) srad[k] = P.rad[3 * start + k];
     __syncthreads();
 
     const int res = P.oct;
@@ -558,32 +576,23 @@ __global__ void __launch_bounds__(kShadeThreads) k_shade_convolve(WaveParams<R> 
     const double scale = 4.0 * kPi / static_cast<double>(n);
     const float* oldTile = P.prevAtlas + static_cast<size_t>(g) * T * T * 3;
     double maxDelta = 0.0;
-    for (int tx = threadIdx.x; tx < res * res; tx += blockDim.x) {
+    for (int item = threadIdx.x; item < 3 * res * res; item += blockDim.x) {
+        const int tx = item / 3, ch = item % 3;
         const int y = tx / res, x = tx % res;
-        V3<double> dd = octDecode(V2<double>{(x + 0.5) / res, (y + 0.5) / res});
+        const V3<double> dd = octDecode(V2<double>{(x + 0.5) / res, (y + 0.5) / res});
         const R Dx = R(dd.x), Dy = R(dd.y), Dz = R(dd.z);
-        R ax = 0, ay = 0, az = 0;
+        R a = 0;
         for (int i = 0; i < n; ++i) {
-            R w = Dx * sdir[3 * i] + Dy * sdir[3 * i + 1] + Dz * sdir[3 * i + 2];
-            if (w > R(0)) {
-                ax = ax + srad[3 * i] * w;
-                ay = ay + srad[3 * i + 1] * w;
-                az = az + srad[3 * i + 2] * w;
-            }
+            const R w = Dx * sdir[3 * i] + Dy * sdir[3 * i + 1] + Dz * sdir[3 * i + 2];
+            if (w > R(0)) a = a + srad[3 * i + ch] * w;
         }
-        V3<double> fresh = mk(double(ax), double(ay), double(az)) * scale;
-        const float* o = oldTile + ((y + 1) * T + (x + 1)) * 3;
-        V3<double> old = mk<double>(o[0], o[1], o[2]);
-        V3<double> bl = lerp(old, fresh, alpha);
-        V3<double> df = bl - old;
-        maxDelta = smax(maxDelta, maxComponent(mk(fabs(df.x), fabs(df.y), fabs(df.z))));
-        float* tp = tile + ((y + 1) * T + (x + 1)) * 3;
-        tp[0] = static_cast<float>(bl.x);
-        tp[1] = static_cast<float>(bl.y);
-        tp[2] = static_cast<float>(bl.z);
+        const double fresh = double(a) * scale;
+        const double old = oldTile[((y + 1) * T + (x + 1)) * 3 + ch];
+        const double bl = old + (fresh - old) * alpha;
+        maxDelta = smax(maxDelta, fabs(bl - old));
+        tile[((y + 1) * T + (x + 1)) * 3 + ch] = static_cast<float>(bl);
     }
     __syncthreads();
-    // fillBorder, atlas.hpp:44-56
     for (int k = threadIdx.x; k < 4 * res + 4; k += blockDim.x) {
         int dx, dy, sx, sy;
         if (k < 4 * res) {
@@ -624,7 +633,7 @@ __global__ void __launch_bounds__(kShadeThreads) k_shade_convolve(WaveParams<R> 
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long m = 0;
-        for (int w = 0; w < kShadeThreads / 32; ++w) m = redDelta[w] > m ? redDelta[w] : m;
+        for (int w = 0; w < kConvThreads / 32; ++w) m = redDelta[w] > m ? redDelta[w] : m;
         atomicMax(P.maxDeltaBits, m);
         atomicAdd(P.rays, static_cast<unsigned long long>(n));
         atomicAdd(P.updated, 1u);
@@ -653,14 +662,18 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
     if (e0) cudaEventRecord(e0, st);
     static int b1 = persistentBlocks(k_trace_primary<R, ST>, kWaveThreads, 0);
     static int b2 = persistentBlocks(k_trace_shadow<R, ST>, kWaveThreads, 0);
+    static int b3 = persistentBlocks(k_shade_rays<R, ST>, 128, 0);
     k_trace_primary<R, ST><<<cap > 0 ? min(cap, b1) : b1, kWaveThreads, 0, st>>>(p);
     k_trace_shadow<R, ST><<<cap > 0 ? min(cap, b2) : b2, kWaveThreads, 0, st>>>(p);
-    const size_t smem = static_cast<size_t>(2 * p.nRaysFull) * 6 * sizeof(R);
-    auto k3 = k_shade_convolve<R, ST>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k3<<<p.nCand, kShadeThreads, smem, st>>>(p);
+    k_shade_rays<R, ST><<<b3, 128, 0, st>>>(p);
+    if (!p.debug) {
+        const size_t smem = static_cast<size_t>(2 * p.nRaysFull) * 6 * sizeof(R);
+        auto k3 = k_convolve<R, ST>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        k3<<<p.nCand, kConvThreads, smem, st>>>(p);
+    }
     if (e1) cudaEventRecord(e1, st);
-    if (launches) *launches += 5;
+    if (launches) *launches += p.debug ? 5 : 6;
 }
 
 template <typename R>

@@ -157,7 +157,7 @@ struct Ctx {
     DBuf<double> wRot, fib;
     DBuf<int> perm;
     int fibN = -1;
-    DBuf<unsigned char> wHits, wVis;
+    DBuf<unsigned char> wHits, wVis, wRad;
     DBuf<unsigned long long> wCtr;
     int persistCap = 0;  // 0 = occupancy-sized persistent grids
     // gather (e): G-buffer, stage buffers, history (pipeline.hpp:213-218)
@@ -182,7 +182,7 @@ struct Ctx {
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
         records.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
         wRayCount.free(); wHitList.free(); wRayStart.free(); wRot.free(); fib.free(); wHits.free();
-        wVis.free(); wCtr.free(); perm.free();
+        wVis.free(); wCtr.free(); perm.free(); wRad.free();
         gbuf.free(); halfDepth.free(); sparseIrr.free(); resolved.free(); indirect.free(); histIrr.free();
         histDepth.free(); halfSrc.free(); sel.free(); sparseValid.free(); sparseAnchor.free();
         for (auto& e : gev)
@@ -650,6 +650,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     reserve(c->wHits, std::max<size_t>(maxRays, 1) * sizeof(HitRec<R>));
     reserve(c->wHitList, std::max<size_t>(maxRays, 1));
     reserve(c->wVis, std::max<size_t>(maxRays, 1) * L * sizeof(R));
+    reserve(c->wRad, std::max<size_t>(maxRays, 1) * 3 * sizeof(R));
     reserve(c->wCtr, 4);
     if (c->fibN != N) {
         reserve(c->fib, 9 * static_cast<size_t>(N));
@@ -677,6 +678,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.hits = reinterpret_cast<HitRec<R>*>(c->wHits.p);
     p.hitList = c->wHitList.p;
     p.vis = reinterpret_cast<R*>(c->wVis.p);
+    p.rad = reinterpret_cast<R*>(c->wRad.p);
     p.ctr = c->wCtr.p;
     p.prevAtlas = c->atlas[c->front].p;
     p.currAtlas = c->atlas[1 - c->front].p;
