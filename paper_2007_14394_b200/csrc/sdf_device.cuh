@@ -558,15 +558,27 @@ __device__ __forceinline__ V3<double> sampleBilinear(const AtlasView& a, int pro
     return lerp(A, B, ty);
 }
 
-// mvcWeightsHex, mean_value.hpp:16-107 (always double)
-__device__ inline bool mvcWeightsHex(const V3<double>* corners, V3<double> x, double* weights) {
+// mvcWeightsHex, mean_value.hpp:16-107, evaluated in precision M (double in the
+// parity mode — identical arithmetic to the reference, the sine of each angle is
+// computed once and reused, which changes no value; float in the FP32 perf mode).
+__device__ __forceinline__ double msin(double v) { return sin(v); }
+__device__ __forceinline__ float msin(float v) { return sinf(v); }
+__device__ __forceinline__ double masin(double v) { return asin(v); }
+__device__ __forceinline__ float masin(float v) { return asinf(v); }
+
+template <typename M>
+__device__ inline bool mvcWeightsHex(const V3<double>* corners, V3<double> xd, double* weights) {
     const int faces[6][4] = {{0, 2, 3, 1}, {4, 5, 7, 6}, {0, 1, 5, 4}, {2, 6, 7, 3}, {0, 4, 6, 2}, {1, 3, 7, 5}};
-    const double eps = 1e-10;
+    const M eps = M(1e-10);
+    const M pi = M(kPi);
+    M wts[8];
+    for (int i = 0; i < 8; ++i) wts[i] = M(0);
     for (int i = 0; i < 8; ++i) weights[i] = 0.0;
-    double dist[8];
-    V3<double> unit[8];
+    M dist[8];
+    V3<M> unit[8];
+    const V3<M> x = mk(M(xd.x), M(xd.y), M(xd.z));
     for (int i = 0; i < 8; ++i) {
-        V3<double> v = corners[i] - x;
+        V3<M> v = mk(M(corners[i].x), M(corners[i].y), M(corners[i].z)) - x;
         dist[i] = length(v);
         if (dist[i] < eps) {
             weights[i] = 1.0;
@@ -579,63 +591,65 @@ __device__ inline bool mvcWeightsHex(const V3<double>* corners, V3<double> x, do
         const int tris[2][3] = {{faces[f][0], faces[f][1], faces[f][2]}, {faces[f][0], faces[f][2], faces[f][3]}};
         for (int tr = 0; tr < 2; ++tr) {
             const int* tri = tris[tr];
-            double d[3], theta[3];
-            V3<double> u[3];
+            M d[3], theta[3], st[3];
+            V3<M> u[3];
             for (int i = 0; i < 3; ++i) {
                 d[i] = dist[tri[i]];
                 u[i] = unit[tri[i]];
             }
             for (int i = 0; i < 3; ++i) {
-                double l = length(u[(i + 1) % 3] - u[(i + 2) % 3]);
-                theta[i] = 2.0 * asin(sclamp(l * 0.5, 0.0, 1.0));
+                M l = length(u[(i + 1) % 3] - u[(i + 2) % 3]);
+                theta[i] = M(2.0) * masin(sclamp(l * M(0.5), M(0), M(1)));
+                st[i] = msin(theta[i]);
             }
-            double h = (theta[0] + theta[1] + theta[2]) * 0.5;
-            if (kPi - h < 1e-8) {
-                for (int i = 0; i < 8; ++i) weights[i] = 0.0;
-                double total = 0;
-                double w[3];
+            M h = (theta[0] + theta[1] + theta[2]) * M(0.5);
+            if (pi - h < M(1e-8)) {
+                M total = 0;
+                M w[3];
                 for (int i = 0; i < 3; ++i) {
-                    w[i] = sin(theta[i]) * d[(i + 1) % 3] * d[(i + 2) % 3];
+                    w[i] = st[i] * d[(i + 1) % 3] * d[(i + 2) % 3];
                     total += w[i];
                 }
                 if (total < eps) return false;
-                for (int i = 0; i < 3; ++i) weights[tri[i]] = w[i] / total;
+                for (int i = 0; i < 8; ++i) weights[i] = 0.0;
+                for (int i = 0; i < 3; ++i) weights[tri[i]] = double(w[i] / total);
                 return true;
             }
             // cross(u1, u2), vec.hpp:51-53
-            V3<double> cr = mk(u[1].y * u[2].z - u[1].z * u[2].y, u[1].z * u[2].x - u[1].x * u[2].z,
-                               u[1].x * u[2].y - u[1].y * u[2].x);
-            double det = dot(u[0], cr);
-            double sign = det >= 0 ? 1.0 : -1.0;
-            double c[3], s[3];
+            V3<M> cr = mk(u[1].y * u[2].z - u[1].z * u[2].y, u[1].z * u[2].x - u[1].x * u[2].z,
+                          u[1].x * u[2].y - u[1].y * u[2].x);
+            M det = dot(u[0], cr);
+            M sign = det >= M(0) ? M(1) : M(-1);
+            M c[3], sv[3];
             bool skip = false;
+            const M sh = msin(h);
             for (int i = 0; i < 3; ++i) {
-                double denom = sin(theta[(i + 1) % 3]) * sin(theta[(i + 2) % 3]);
+                M denom = st[(i + 1) % 3] * st[(i + 2) % 3];
                 if (fabs(denom) < eps) {
                     skip = true;
                     break;
                 }
-                c[i] = (2.0 * sin(h) * sin(h - theta[i])) / denom - 1.0;
-                s[i] = sign * sqrt(smax(0.0, 1.0 - c[i] * c[i]));
-                if (fabs(s[i]) <= eps) {
+                c[i] = (M(2.0) * sh * msin(h - theta[i])) / denom - M(1.0);
+                sv[i] = sign * sqrt(smax(M(0), M(1.0) - c[i] * c[i]));
+                if (fabs(sv[i]) <= eps) {
                     skip = true;
                     break;
                 }
             }
             if (skip) continue;
             for (int i = 0; i < 3; ++i) {
-                double w = (theta[i] - c[(i + 1) % 3] * theta[(i + 2) % 3] - c[(i + 2) % 3] * theta[(i + 1) % 3]) /
-                           (d[i] * sin(theta[(i + 1) % 3]) * s[(i + 2) % 3]);
-                weights[tri[i]] += w;
+                M w = (theta[i] - c[(i + 1) % 3] * theta[(i + 2) % 3] - c[(i + 2) % 3] * theta[(i + 1) % 3]) /
+                      (d[i] * st[(i + 1) % 3] * sv[(i + 2) % 3]);
+                wts[tri[i]] += w;
                 any = true;
             }
         }
     }
     if (!any) return false;
-    double total = 0;
-    for (int i = 0; i < 8; ++i) total += weights[i];
+    M total = 0;
+    for (int i = 0; i < 8; ++i) total += wts[i];
     if (fabs(total) < eps || !isfinite(total)) return false;
-    for (int i = 0; i < 8; ++i) weights[i] /= total;
+    for (int i = 0; i < 8; ++i) weights[i] = double(wts[i] / total);
     return true;
 }
 
@@ -648,8 +662,9 @@ struct Stencil {
     int usedMvc;
 };
 
-// interpolationStencil, probe_volume.hpp:224-310 (always double: positions are
-// double on the device in both modes)
+// interpolationStencil, probe_volume.hpp:224-310 (cell and trilinear weights in
+// double in both modes; MVC in precision M)
+template <typename M = double>
 __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, const ProbesView& pv, V3<double> point,
                                         double mvcFrac) {
     Stencil st;
@@ -702,7 +717,7 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
     bool wantMvc = maxDisp > mvcFrac * c.spacing || boundary;
     bool haveMvc = false;
     if (wantMvc) {
-        haveMvc = mvcWeightsHex(corners, point, w);
+        haveMvc = mvcWeightsHex<M>(corners, point, w);
         if (haveMvc) {
             for (int k = 0; k < 8; ++k) w[k] = smax(0.0, w[k]);
             st.usedMvc = 1;
@@ -735,11 +750,12 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
 }
 
 // sampleBounceIrradiance, probe_update.hpp:63-92. Returns false when "empty".
+template <typename M = double>
 __device__ inline bool sampleBounceIrradiance(const CascadeDev* cas, int nCas, const ProbesView& pv,
                                        const float* atlas, int oct, V3<double> pos, V3<double> normal,
                                        double mvcFrac, V3<double>* out) {
     if (nCas <= 0) return false;
-    Stencil st = interpolationStencil(cas, nCas, pv, pos, mvcFrac);
+    Stencil st = interpolationStencil<M>(cas, nCas, pv, pos, mvcFrac);
     if (st.sky || st.count == 0) return false;
     const CascadeDev& c = cas[st.cascade];
     double wsum = 0;
@@ -834,7 +850,7 @@ __device__ V3<double> shadeHit(const SceneView<R>& s, const Hit<R>& hit, const C
         V3<double> prev;
         V3<double> hp = mk<double>(hit.pos.x, hit.pos.y, hit.pos.z);
         V3<double> hn = mk<double>(hit.normal.x, hit.normal.y, hit.normal.z);
-        if (sampleBounceIrradiance(cas, nCas, pv, prevAtlas, oct, hp, hn, cfg.mvcFrac, &prev))
+        if (sampleBounceIrradiance<R>(cas, nCas, pv, prevAtlas, oct, hp, hn, cfg.mvcFrac, &prev))
             radiance = radiance + brdf * (prev * cfg.bounceCoeff);
     }
     return radiance;
