@@ -43,19 +43,6 @@ __device__ __forceinline__ bool camProject(const CameraDev& c, V3<double> world,
     return true;
 }
 
-// cosineHemisphereDir (rng.hpp:58-69) with orthonormalBasis (vec.hpp:188-194)
-__device__ __forceinline__ V3<double> cosineHemisphereDir(Rng& rng, V3<double> n) {
-    double u1 = rng.uniform(), u2 = rng.uniform();
-    double r = sqrt(u1), phi = 2.0 * kPi * u2;
-    double lx = r * cos(phi), ly = r * sin(phi), lz = sqrt(smax(0.0, 1.0 - u1));
-    double sign = copysign(1.0, n.z);
-    double a = -1.0 / (sign + n.z);
-    double c = n.x * n.y * a;
-    V3<double> t = mk(1.0 + sign * n.x * n.x * a, sign * c, -sign * n.x);
-    V3<double> b = mk(c, sign + n.y * n.y * a, -n.y);
-    return normalize(t * lx + b * ly + n * lz);
-}
-
 __device__ __forceinline__ bool isSky(const GPix& p) { return !(p.depth < INFINITY); }
 
 // ------------------------------------------------------------------ G-buffer

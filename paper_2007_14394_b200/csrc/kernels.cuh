@@ -94,6 +94,13 @@ template <typename R> struct WaveParams {
     // debug: per-ray records instead of atlas/state writes
     RayRecord* records;
     int debug;
+    // contact batch (Contact GI rays, shading.hpp:431-477); nRaysDirect < 0 = probe batch
+    long long nRaysDirect;
+    const struct GPix* gb;
+    int gw, gh, contactSamples;
+    double contactRadius;
+    const double* resolved;
+    double* indirect;
 };
 
 // Mirror of sdfgi_gbuffer_pixel (GBufferPixel, shading.hpp:13-22).
@@ -170,6 +177,8 @@ struct GridBuildParams {
 
 // Launch the whole wavefront for one batch (K0..K3) on `st`. `persistBlocks` sizes
 // the persistent K1/K2 grids; `ev` (optional, 2 events) brackets K1..K3.
+template <typename R>
+void launch_contact(const WaveParams<R>& p, bool stats, cudaStream_t st, long long* launches);
 template <typename R>
 void launch_wavefront(const WaveParams<R>& p, int persistBlocks, bool stats, cudaStream_t st,
                       cudaEvent_t evStart, cudaEvent_t evEnd, long long* launches);

@@ -213,42 +213,93 @@ __device__ __forceinline__ V3<double> rayDirection(const WaveParams<R>& P, int s
 // (query at 2*lastD), state 1 is the owner-resolving query at the converged point
 // (d + 1e-9), state 2 the polish loop (t += d, 2|d| + 1e-9, at most 8). Every
 // iteration is exactly one query for every active lane.
-template <typename R, bool ST>
+// Total rays of a batch: the probe batch's prefix sum, or the direct count of a
+// contact batch.
+template <typename R>
+__device__ __forceinline__ long long rayTotal(const WaveParams<R>& P) {
+    return P.nRaysDirect >= 0 ? P.nRaysDirect : P.rayStart[P.nCand];
+}
+
+// Contact ray `item` = (pixel, sample), contactGI (shading.hpp:694-703): the
+// pixel's Rng(seed, 0xc0417ff, y*W + x) stream advanced 2*sample draws (random
+// access into the splitmix64 sequence), cosineHemisphereDir, the normal-offset
+// origin, tMax = radius and startBound = bias + eps. False for sky pixels.
+template <typename R>
+__device__ __forceinline__ bool contactRay(const WaveParams<R>& P, long long item, V3<R>& o, V3<R>& dir, R& tMax,
+                                           R& startBound) {
+    const long long pix = item / P.contactSamples;
+    const int smp = static_cast<int>(item - pix * P.contactSamples);
+    const GPix& px = P.gb[pix];
+    if (!(px.depth < INFINITY)) return false;
+    const int x = static_cast<int>(pix % P.gw), y = static_cast<int>(pix / P.gw);
+    Rng rng(hashCombine(hashCombine(P.seed, 0xc0417ffull), static_cast<uint64_t>(y) * P.gw + x));
+    rng.s += 2ull * smp * 0x9e3779b97f4a7c15ull;
+    const V3<double> nn = mk(px.normal[0], px.normal[1], px.normal[2]);
+    const V3<double> dd = cosineHemisphereDir(rng, nn);
+    const double cosT = smax(0.1, dot(dd, nn));
+    const double bias = 2.0 * P.tc.eps / cosT;
+    const V3<double> oo = mk(px.world_pos[0], px.world_pos[1], px.world_pos[2]) + nn * bias;
+    o = mk(R(oo.x), R(oo.y), R(oo.z));
+    dir = mk(R(dd.x), R(dd.y), R(dd.z));
+    tMax = R(P.contactRadius);
+    startBound = R(bias + P.tc.eps);
+    return true;
+}
+
+template <typename R, bool ST, int MODE>
 __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P) {
-    const long long total = P.rayStart[P.nCand];
-    const R eps = R(P.tc.eps), tMax = R(P.tc.rayTMax);
+    const long long total = rayTotal(P);
+    const R eps = R(P.tc.eps);
     const int maxSteps = P.tc.maxSteps;
     Counters cnt;
     cnt.zero();
     bool active = false, exhausted = false;
     unsigned long long rid = 0;
     V3<R> o = mk(R(0), R(0), R(0)), dir = o;
-    R t = 0, lastD = 0, d = 0;
+    R t = 0, lastD = 0, d = 0, tMax = 0;
     int step = 0, state = 0, pol = 0, owner = -1;
     while (true) {
         __syncwarp();
         unsigned long long item;
         if (fetchItem(P.ctr + 0, static_cast<unsigned long long>(total), active, exhausted, item)) {
-            const int s = findCandidate(P.rayStart, P.nCand, static_cast<long long>(item));
-            const int j = static_cast<int>(static_cast<long long>(item) - P.rayStart[s]);
-            const int n = static_cast<int>(P.rayStart[s + 1] - P.rayStart[s]);
-            // slot j traces sample i = perm[j]: consecutive lanes get neighbouring
-            // directions (coherent warps); results are stored by sample index
-            const int i = P.perm[(n == P.nRaysFull ? 0 : P.nRaysFull) + j];
-            rid = static_cast<unsigned long long>(P.rayStart[s] + i);
-            const int g = P.cand ? P.cand[s] : s;
-            const double* pp = P.pc.probes.pos + 3 * static_cast<size_t>(g);
-            V3<double> dd = rayDirection(P, s, i, n);
-            o = mk(R(pp[0]), R(pp[1]), R(pp[2]));
-            dir = mk(R(dd.x), R(dd.y), R(dd.z));
+            R startBound = R(INFINITY);
+            bool ok = true;
+            if (MODE == 0) {
+                const int s = findCandidate(P.rayStart, P.nCand, static_cast<long long>(item));
+                const int j = static_cast<int>(static_cast<long long>(item) - P.rayStart[s]);
+                const int n = static_cast<int>(P.rayStart[s + 1] - P.rayStart[s]);
+                // slot j traces sample i = perm[j]: consecutive lanes get neighbouring
+                // directions (coherent warps); results are stored by sample index
+                const int i = P.perm[(n == P.nRaysFull ? 0 : P.nRaysFull) + j];
+                rid = static_cast<unsigned long long>(P.rayStart[s] + i);
+                const int g = P.cand ? P.cand[s] : s;
+                const double* pp = P.pc.probes.pos + 3 * static_cast<size_t>(g);
+                V3<double> dd = rayDirection(P, s, i, n);
+                o = mk(R(pp[0]), R(pp[1]), R(pp[2]));
+                dir = mk(R(dd.x), R(dd.y), R(dd.z));
+                tMax = R(P.tc.rayTMax);
+            } else {
+                rid = item;
+                ok = contactRay(P, static_cast<long long>(item), o, dir, tMax, startBound);
+            }
             t = R(0);
-            lastD = R(INFINITY) * R(0.5);
+            lastD = startBound * R(0.5);
             step = 0;
             state = 0;
             owner = -1;
-            active = true;
-            if (ST) ++cnt.sphere;
-            if (maxSteps <= 0) {  // loop never runs: StepLimit
+            active = ok;
+            if (!ok) {  // sky pixel of a contact batch: no ray (the combine skips it)
+                HitRec<R> h;
+                h.p[0] = h.p[1] = h.p[2] = R(0);
+                h.n[0] = h.n[1] = R(0);
+                h.n[2] = R(1);
+                h.t = R(0);
+                h.owner = -1;
+                h.status = 0;
+                P.hits[rid] = h;
+            }
+            if (ST && ok) ++cnt.sphere;
+            if (ok && maxSteps <= 0) {  // loop never runs: StepLimit
                 HitRec<R> h;
                 h.p[0] = h.p[1] = h.p[2] = R(0);
                 h.n[0] = h.n[1] = R(0);
@@ -508,7 +559,7 @@ __device__ __forceinline__ V3<double> shadeRay(const WaveParams<R>& P, const Hit
 // footprint does not cap the convolution's occupancy.
 template <typename R, bool ST>
 __global__ void __launch_bounds__(128) k_shade_rays(WaveParams<R> P) {
-    const long long total = P.rayStart[P.nCand];
+    const long long total = rayTotal(P);
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
     for (long long rid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; rid < total; rid += stride) {
         const HitRec<R> h = P.hits[rid];
@@ -660,10 +711,10 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
     k_ray_scan<R><<<1, kScanThreads, 0, st>>>(p);
     cudaMemsetAsync(p.ctr, 0, 4 * sizeof(unsigned long long), st);
     if (e0) cudaEventRecord(e0, st);
-    static int b1 = persistentBlocks(k_trace_primary<R, ST>, kWaveThreads, 0);
+    static int b1 = persistentBlocks(k_trace_primary<R, ST, 0>, kWaveThreads, 0);
     static int b2 = persistentBlocks(k_trace_shadow<R, ST>, kWaveThreads, 0);
     static int b3 = persistentBlocks(k_shade_rays<R, ST>, 128, 0);
-    k_trace_primary<R, ST><<<cap > 0 ? min(cap, b1) : b1, kWaveThreads, 0, st>>>(p);
+    k_trace_primary<R, ST, 0><<<cap > 0 ? min(cap, b1) : b1, kWaveThreads, 0, st>>>(p);
     k_trace_shadow<R, ST><<<cap > 0 ? min(cap, b2) : b2, kWaveThreads, 0, st>>>(p);
     k_shade_rays<R, ST><<<b3, 128, 0, st>>>(p);
     if (!p.debug) {
@@ -674,6 +725,72 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
     }
     if (e1) cudaEventRecord(e1, st);
     if (launches) *launches += p.debug ? 5 : 6;
+}
+
+// contactGI's per-pixel sum (shading.hpp:686-713): AO from the missed samples,
+// occluder radiance (K3a) summed in sample order, probe GI from the resolve.
+template <typename R>
+__global__ void __launch_bounds__(128) k_contact_combine(WaveParams<R> P) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<long long>(P.gw) * P.gh) return;
+    const GPix& px = P.gb[i];
+    double* out = P.indirect + 3 * i;
+    if (!(px.depth < INFINITY)) {
+        out[0] = out[1] = out[2] = 0;
+        return;
+    }
+    const V3<double> alb = mk(px.albedo[0], px.albedo[1], px.albedo[2]);
+    const V3<double> brdf = alb / kPi;
+    const double* re = P.resolved + 3 * i;
+    const V3<double> probeGi = brdf * mk(re[0], re[1], re[2]);
+    const int nS = P.contactSamples;
+    if (nS <= 0 || P.contactRadius <= 0) {
+        out[0] = probeGi.x;
+        out[1] = probeGi.y;
+        out[2] = probeGi.z;
+        return;
+    }
+    int unocc = 0;
+    V3<double> occ = mk(0.0, 0.0, 0.0);
+    for (int s = 0; s < nS; ++s) {
+        const long long rid = i * nS + s;
+        if (!(P.hits[rid].status & 1)) {
+            ++unocc;
+        } else {
+            occ = occ + mk(double(P.rad[3 * rid]), double(P.rad[3 * rid + 1]), double(P.rad[3 * rid + 2]));
+        }
+    }
+    const double ao = static_cast<double>(unocc) / nS;
+    const V3<double> contact = (alb / kPi) * (kPi / nS) * occ;
+    const V3<double> o = probeGi * ao + contact;
+    out[0] = o.x;
+    out[1] = o.y;
+    out[2] = o.z;
+}
+
+// Contact GI as a wavefront over (pixel, sample) rays: K1 in contact mode, the
+// shared K2 (shadow rays of the compacted hits) and K3a (shadeHit with bounce),
+// then the per-pixel combine. Replaces the per-pixel k_contact loop.
+template <typename R, bool ST>
+static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long* launches) {
+    cudaMemsetAsync(p.ctr, 0, 4 * sizeof(unsigned long long), st);
+    static int b1 = persistentBlocks(k_trace_primary<R, ST, 1>, kWaveThreads, 0);
+    static int b2 = persistentBlocks(k_trace_shadow<R, ST>, kWaveThreads, 0);
+    static int b3 = persistentBlocks(k_shade_rays<R, ST>, 128, 0);
+    k_trace_primary<R, ST, 1><<<b1, kWaveThreads, 0, st>>>(p);
+    k_trace_shadow<R, ST><<<b2, kWaveThreads, 0, st>>>(p);
+    k_shade_rays<R, ST><<<b3, 128, 0, st>>>(p);
+    const long long np = static_cast<long long>(p.gw) * p.gh;
+    k_contact_combine<R><<<static_cast<int>((np + 127) / 128), 128, 0, st>>>(p);
+    if (launches) *launches += 4;
+}
+
+template <typename R>
+void launch_contact(const WaveParams<R>& p, bool stats, cudaStream_t st, long long* launches) {
+    if (stats)
+        contactWavefront<R, true>(p, st, launches);
+    else
+        contactWavefront<R, false>(p, st, launches);
 }
 
 template <typename R>

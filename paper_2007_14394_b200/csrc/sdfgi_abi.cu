@@ -1355,6 +1355,51 @@ void ensureGather(Ctx* c, int w, int h) {
         if (!e) CK(cudaEventCreate(&e));
 }
 
+// Wavefront parameters for the Contact GI batch: every (pixel, sample) ray of the
+// current G-buffer; reuses the probe wavefront's scratch buffers.
+template <typename R>
+WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
+    const long long nr = static_cast<long long>(c->gw) * c->gh * std::max<long long>(cfg->contact_samples, 0);
+    const size_t cap = static_cast<size_t>(std::max<long long>(nr, 1));
+    const int L = std::max(c->nLights, 1);
+    reserve(c->wHits, cap * sizeof(HitRec<R>));
+    reserve(c->wHitList, cap);
+    reserve(c->wVis, cap * L * sizeof(R));
+    reserve(c->wRad, cap * 3 * sizeof(R));
+    reserve(c->wCtr, 4);
+    WaveParams<R> p;
+    std::memset(&p, 0, sizeof(p));
+    p.scene = c->sceneView<R>();
+    p.pc = c->probeCommon();
+    p.tc.eps = cfg->surface_epsilon;
+    p.tc.rayTMax = cfg->ray_tmax;
+    p.tc.shadowK = cfg->shadow_k;
+    p.tc.bounceCoeff = cfg->bounce_coeff;
+    p.tc.mvcFrac = cfg->mvc_relocation_frac;
+    p.tc.maxSteps = static_cast<int>(cfg->max_trace_steps);
+    p.tc.shadowSteps = static_cast<int>(cfg->shadow_steps);
+    p.prevAtlas = c->atlas[c->front].p;
+    p.oct = c->octRes;
+    p.seed = cfg->seed;
+    p.hits = reinterpret_cast<HitRec<R>*>(c->wHits.p);
+    p.hitList = c->wHitList.p;
+    p.vis = reinterpret_cast<R*>(c->wVis.p);
+    p.rad = reinterpret_cast<R*>(c->wRad.p);
+    p.ctr = c->wCtr.p;
+    p.stats = c->scratch.p;
+    p.nRaysDirect = nr;
+    p.gb = c->gbuf.p;
+    p.gw = c->gw;
+    p.gh = c->gh;
+    p.contactSamples = static_cast<int>(cfg->contact_samples);
+    double sp0 = 1.0;
+    if (!c->cascades.empty()) sp0 = c->cascades[0].spacing / std::pow(2.0, c->cascades[0].level);
+    p.contactRadius = cfg->contact_radius_frac * sp0;  // pipeline.hpp:200
+    p.resolved = c->resolved.p;
+    p.indirect = c->indirect.p;
+    return p;
+}
+
 template <typename R>
 GatherParams<R> gatherParams(Ctx* c, const sdfgi_cfg* cfg, int frame) {
     GatherParams<R> p;
@@ -1478,20 +1523,29 @@ int sdfgi_gather(void* ctx, int frame, const sdfgi_cfg* cfg, int64_t* n_tasks, s
             return p;
         };
         unsigned long long visH[32];
+        // Contact GI (shading.hpp:431-477) as a wavefront over (pixel, sample) rays
+        const char* cenv = std::getenv("SDFGI_CONTACT_PER_PIXEL");  // 1: the per-pixel loop kernel
+        const bool perPixel = cenv && std::atoi(cenv) == 1;
         if (c->precision == SDFGI_F64) {
             auto p = run(gatherParams<double>(c, cfg, frame));
             CK(cudaMemcpyAsync(visH, c->scratch.p, sizeof(visH), cudaMemcpyDeviceToHost, c->stream));
             CK(cudaStreamSynchronize(c->stream));
             CK(cudaMemsetAsync(c->scratch.p, 0, 19 * 8, c->stream));
-            launch_gather(p, 4, st, c->stream);
+            if (perPixel)
+                launch_gather(p, 4, st, c->stream);
+            else
+                launch_contact<double>(contactParams<double>(c, cfg), st, c->stream, &c->launches);
         } else {
             auto p = run(gatherParams<float>(c, cfg, frame));
             CK(cudaMemcpyAsync(visH, c->scratch.p, sizeof(visH), cudaMemcpyDeviceToHost, c->stream));
             CK(cudaStreamSynchronize(c->stream));
             CK(cudaMemsetAsync(c->scratch.p, 0, 19 * 8, c->stream));
-            launch_gather(p, 4, st, c->stream);
+            if (perPixel)
+                launch_gather(p, 4, st, c->stream);
+            else
+                launch_contact<float>(contactParams<float>(c, cfg), st, c->stream, &c->launches);
         }
-        c->launches += 5;
+        c->launches += 4;
         CK(cudaGetLastError());
         CK(cudaEventRecord(c->gev[4], c->stream));
         c->gevValid = true;
