@@ -675,6 +675,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.rot = c->wRot.p;
     p.fib = c->fib.p;
     p.perm = c->perm.p;
+    p.nRaysDirect = -1;  // probe batch: ray count from the K0 prefix sum
     p.hits = reinterpret_cast<HitRec<R>*>(c->wHits.p);
     p.hitList = c->wHitList.p;
     p.vis = reinterpret_cast<R*>(c->wVis.p);
