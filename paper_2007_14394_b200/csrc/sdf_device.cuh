@@ -82,19 +82,15 @@ template <typename R> struct __align__(16) DPrim {
     int kind;
     int identity;
 };
-// FP32 perf-mode record: every bounded kind in one branch-free form (see
-// evalPrim<float>): e = extents of a box (mode 0) or of a radial shape (mode 1:
-// cylinder r/h, capsule 0/h, sphere 0/0), rr = rounding radius (capsule, sphere);
-// mode 2 = plane. 80 B.
+// FP32 perf-mode record: every kind in one branch-free form (see evalPrim<float>):
+// e = half extents of a box, or (e0, -1, e2) for a radial shape (cylinder r/h,
+// capsule 0/h, sphere 0/0: e1 < 0 marks radial), rr = rounding radius (capsule,
+// sphere); rr < 0 marks a plane. 64 B = four 16-byte loads.
 template <> struct __align__(16) DPrim<float> {
     float rot[9];
     float trans[3];
     float e[3];
     float rr;
-    int mode;
-    int kind;
-    int identity;
-    int _pad;
 };
 template <typename R> struct __align__(16) DCluster {
     R lo[3];
@@ -125,6 +121,8 @@ struct DLight {  // sdfgi_light, kept in double in both modes (tiny)
 struct GridDev {
     double lo[3];
     double invH;
+    float flo[3];   // the same in float for the FP32 path
+    float finvH;
     int dim[3];
     int nSuper;
     const int* __restrict__ start;  // ncells + 1
@@ -143,6 +141,7 @@ template <typename R> struct SceneView {
     const int* __restrict__ orig;              // CSR position -> ActiveScene primitive index
     const double* __restrict__ albedo;         // 3 per CSR position
     const double* __restrict__ emission;       // 3 per CSR position
+    const int* __restrict__ kindId;            // kind | identity << 8 per CSR position (statistics)
     const DLight* __restrict__ lights;
     int n_prims, n_clusters, n_lights;
     double sky[3];
@@ -214,7 +213,7 @@ __device__ __forceinline__ float evalPrim<float>(const DPrim<float>& pr, V3<floa
     const float qx = fmaf(m[0], px, fmaf(m[3], py, m[6] * pz));
     const float qy = fmaf(m[1], px, fmaf(m[4], py, m[7] * pz));
     const float qz = fmaf(m[2], px, fmaf(m[5], py, m[8] * pz));
-    const bool radial = pr.mode == 1;
+    const bool radial = pr.e[1] < 0.f;
     const float rho = sqrtf(fmaf(qx, qx, qy * qy));
     const float u = (radial ? rho : fabsf(qx)) - pr.e[0];
     const float v = radial ? -1e30f : fabsf(qy) - pr.e[1];
@@ -223,7 +222,7 @@ __device__ __forceinline__ float evalPrim<float>(const DPrim<float>& pr, V3<floa
     const float outside = sqrtf(fmaf(ou, ou, fmaf(ov, ov, ow * ow)));
     const float inside = fminf(fmaxf(u, fmaxf(v, w)), 0.f);
     const float d = outside + inside - pr.rr;
-    return pr.mode == 2 ? qz : d;
+    return pr.rr < 0.f ? qz : d;
 }
 
 // evalGradientDetailed / evalGradient, primitives.hpp:96-108 (h = 1e-3)
@@ -269,8 +268,8 @@ __device__ __forceinline__ void visitMembers(const SceneView<R>& s, int k, V3<R>
     }
     for (int j = b; j < e; ++j) {
         if (ST) {
-            ++c->ek[s.prims[j].kind];
-            c->ek[5] += s.prims[j].identity ? 0 : 1;
+            ++c->ek[s.kindId[j] & 0xff];
+            c->ek[5] += (s.kindId[j] >> 8) ? 0 : 1;
         }
         const R pd = evalPrim(s.prims[j], p);
         if (pd < d || (TIE && pd == d && own >= 0 && j < own)) {
@@ -322,9 +321,12 @@ __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R ini
         return;
     }
     const GridDev& g = s.grid;
-    R fx = (p.x - R(g.lo[0])) * R(g.invH);
-    R fy = (p.y - R(g.lo[1])) * R(g.invH);
-    R fz = (p.z - R(g.lo[2])) * R(g.invH);
+    const bool f32 = sizeof(R) == 4;
+    const R lx = f32 ? R(g.flo[0]) : R(g.lo[0]), ly = f32 ? R(g.flo[1]) : R(g.lo[1]);
+    const R lz = f32 ? R(g.flo[2]) : R(g.lo[2]), ih = f32 ? R(g.finvH) : R(g.invH);
+    R fx = (p.x - lx) * ih;
+    R fy = (p.y - ly) * ih;
+    R fz = (p.z - lz) * ih;
     if (fx >= R(0) && fy >= R(0) && fz >= R(0) && fx < R(g.dim[0]) && fy < R(g.dim[1]) && fz < R(g.dim[2])) {
         int ix = min(static_cast<int>(fx), g.dim[0] - 1);
         int iy = min(static_cast<int>(fy), g.dim[1] - 1);
@@ -373,8 +375,8 @@ template <typename R, bool ST>
 __device__ __forceinline__ void queryStep(const SceneView<R>& s, QueryState<R>& q, Counters* c) {
     const int j = s.grid.list[q.cur++];
     if (ST) {
-        ++c->ek[s.prims[j].kind];
-        c->ek[5] += s.prims[j].identity ? 0 : 1;
+        ++c->ek[s.kindId[j] & 0xff];
+        c->ek[5] += (s.kindId[j] >> 8) ? 0 : 1;
     }
     const R pd = evalPrim(s.prims[j], q.p);
     if (pd < q.d || (pd == q.d && q.own >= 0 && j < q.own)) {

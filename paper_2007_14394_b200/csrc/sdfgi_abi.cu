@@ -126,6 +126,7 @@ struct Ctx {
     DBuf<DCluster<float>> cl32;
     DBuf<int> cstart, orig;
     DBuf<double> albedo, emission;
+    DBuf<int> kindId;
     DBuf<DLight> lights;
     // candidate-cluster grid (GridDev, sdf_device.cuh)
     int accel = 1;
@@ -175,7 +176,7 @@ struct Ctx {
         cudaSetDevice(device);
         if (stream) cudaStreamSynchronize(stream);
         prim64.free(); prim32.free(); cl64.free(); cl32.free(); cstart.free(); orig.free();
-        albedo.free(); emission.free(); lights.free();
+        albedo.free(); emission.free(); lights.free(); kindId.free();
         gridStart.free(); gridList.free(); gridCounts.free(); gridU.free();
         superBox.free(); superStart.free(); superList.free(); primBox.free();
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
@@ -238,6 +239,7 @@ SceneView<double> Ctx::sceneView<double>() const {
     v.orig = orig.p;
     v.albedo = albedo.p;
     v.emission = emission.p;
+    v.kindId = kindId.p;
     v.lights = lights.p;
     v.n_prims = nPrims;
     v.n_clusters = nClusters;
@@ -256,6 +258,7 @@ SceneView<float> Ctx::sceneView<float>() const {
     v.orig = orig.p;
     v.albedo = albedo.p;
     v.emission = emission.p;
+    v.kindId = kindId.p;
     v.lights = lights.p;
     v.n_prims = nPrims;
     v.n_clusters = nClusters;
@@ -353,7 +356,8 @@ void fillPrim(DPrim<R>& d, const sdfgi_prim& s) {
 }
 
 // FP32 unified record (DPrim<float>, evalPrim<float>): the per-kind `size`
-// meanings of primitives.hpp:25-30 mapped onto (mode, e, rr).
+// meanings of primitives.hpp:25-30 mapped onto (e, rr); e1 < 0 marks radial
+// shapes, rr < 0 a plane.
 void fillPrim(DPrim<float>& d, const sdfgi_prim& s) {
     for (int k = 0; k < 9; ++k) d.rot[k] = static_cast<float>(s.rot[k]);
     for (int k = 0; k < 3; ++k) {
@@ -362,25 +366,22 @@ void fillPrim(DPrim<float>& d, const sdfgi_prim& s) {
     }
     d.rr = 0.f;
     switch (s.kind) {
-        case SDFGI_SPHERE: d.mode = 1; d.rr = static_cast<float>(s.size[0]); break;
+        case SDFGI_SPHERE: d.e[1] = -1.f; d.rr = static_cast<float>(s.size[0]); break;
         case SDFGI_BOX:
-            d.mode = 0;
             for (int k = 0; k < 3; ++k) d.e[k] = static_cast<float>(s.size[k]);
             break;
-        case SDFGI_PLANE: d.mode = 2; break;
+        case SDFGI_PLANE: d.rr = -1.f; break;
         case SDFGI_CYLINDER:
-            d.mode = 1;
             d.e[0] = static_cast<float>(s.size[0]);
+            d.e[1] = -1.f;
             d.e[2] = static_cast<float>(s.size[1]);
             break;
         default:  // capsule
-            d.mode = 1;
+            d.e[1] = -1.f;
             d.e[2] = static_cast<float>(s.size[1]);
             d.rr = static_cast<float>(s.size[0]);
             break;
     }
-    d.kind = s.kind;
-    d.identity = (s.rot[0] == 1.0 && s.rot[4] == 1.0 && s.rot[8] == 1.0) ? 1 : 0;
 }
 
 // Build the candidate-cluster grid over the bounded clusters (exact; see GridDev).
@@ -514,6 +515,8 @@ void buildGrid(Ctx* c, const sdfgi_prim* prims, const int32_t* member_idx, const
         c->grid.dim[a] = dim[a];
     }
     c->grid.invH = 1.0 / h;
+    for (int a = 0; a < 3; ++a) c->grid.flo[a] = static_cast<float>(lo[a]);
+    c->grid.finvH = static_cast<float>(1.0 / h);
     c->grid.start = c->gridStart.p;
     c->grid.list = c->gridList.p;
     c->gridEntries = total;
@@ -859,7 +862,7 @@ int sdfgi_scene_upload(void* ctx, const sdfgi_prim* prims, int n_prims, const sd
         // cluster (CSR) order: device primitive j = prims[member_idx[j]]
         std::vector<DPrim<double>> p64(nMembers);
         std::vector<DPrim<float>> p32(nMembers);
-        std::vector<int> orig(nMembers);
+        std::vector<int> orig(nMembers), kid(std::max(nMembers, 1));
         std::vector<double> alb(3 * static_cast<size_t>(nMembers)), em(3 * static_cast<size_t>(nMembers));
         for (int j = 0; j < nMembers; ++j) {
             const sdfgi_prim& s = prims[member_idx[j]];
@@ -868,6 +871,7 @@ int sdfgi_scene_upload(void* ctx, const sdfgi_prim* prims, int n_prims, const sd
             fillPrim(p64[j], s);
             fillPrim(p32[j], s);
             orig[j] = member_idx[j];
+            kid[j] = s.kind | (p64[j].identity << 8);
             for (int k = 0; k < 3; ++k) {
                 alb[3 * j + k] = s.albedo[k];
                 em[3 * j + k] = s.emission[k];
@@ -900,6 +904,7 @@ int sdfgi_scene_upload(void* ctx, const sdfgi_prim* prims, int n_prims, const sd
         c->orig.upload(orig.data(), orig.size(), c->stream);
         c->albedo.upload(alb.data(), alb.size(), c->stream);
         c->emission.upload(em.data(), em.size(), c->stream);
+        c->kindId.upload(kid.data(), kid.size(), c->stream);
         c->lights.upload(reinterpret_cast<const DLight*>(lights), n_lights, c->stream);
         CK(cudaStreamSynchronize(c->stream));
         c->nPrims = nMembers;
