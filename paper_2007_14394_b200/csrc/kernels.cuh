@@ -173,6 +173,7 @@ struct GridBuildParams {
     int* counts;
     const int* start;
     int* list;
+    float* lkey;  // per entry: lower bound of the candidate's SDF over the cell
 };
 
 // Launch the whole wavefront for one batch (K0..K3) on `st`. `persistBlocks` sizes

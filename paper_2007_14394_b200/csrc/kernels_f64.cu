@@ -85,6 +85,20 @@ __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells
         }
         L[b + 1] = v;
     }
+    // lower bound of each candidate's SDF over the cell: its surface box is at
+    // least sqrt(key) - (half diagonal) from any point of the cell, and the SDF
+    // outside the box is at least the distance to it. Rounded down into float with
+    // the build margin, so `bound > d` proves the candidate cannot reach (or tie) d.
+    const double half = 0.5 * sqrt(3.0) * (P.h + 2.0 * P.pad);
+    for (int a = 0; a < n; ++a) {
+        const double kv = key(L[a]);
+        float lb = -INFINITY;
+        if (kv >= 0) {
+            const double b = sqrt(kv) - half - P.margin;
+            lb = b > 0 ? __double2float_rd(b) : -INFINITY;  // no bound inside the reach of the cell
+        }
+        P.lkey[out + a] = lb;
+    }
 }
 
 void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st) {

@@ -127,6 +127,10 @@ struct GridDev {
     int nSuper;
     const int* __restrict__ start;  // ncells + 1
     const int* __restrict__ list;
+    // per list entry: a lower bound on that primitive's SDF anywhere in the cell
+    // (box distance to the cell centre - padded half diagonal, rounded down);
+    // entries are sorted by it, so a query stops at the first bound > its minimum
+    const float* __restrict__ lkey;
     const int* __restrict__ superStart;     // nSuper + 1 into superList
     const int* __restrict__ superList;      // cluster ids; unbounded clusters last (always visited)
     const double* __restrict__ superBox;    // 6 per supercluster (lo xyz, hi xyz)
@@ -373,6 +377,10 @@ __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R ini
 // One candidate of the cell list (lowest-CSR-position tie-break: order-free).
 template <typename R, bool ST>
 __device__ __forceinline__ void queryStep(const SceneView<R>& s, QueryState<R>& q, Counters* c) {
+    if (R(s.grid.lkey[q.cur]) > q.d) {  // this and every later candidate is farther
+        q.cur = q.end;
+        return;
+    }
     const int j = s.grid.list[q.cur++];
     if (ST) {
         ++c->ek[s.kindId[j] & 0xff];

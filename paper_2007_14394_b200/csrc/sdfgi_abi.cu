@@ -134,6 +134,7 @@ struct Ctx {
     GridDev grid{};
     long long gridEntries = 0;
     DBuf<int> gridStart, gridList, gridCounts;
+    DBuf<float> gridKey;
     DBuf<double> gridU, superBox, primBox;
     DBuf<int> superStart, superList;
     // probes
@@ -177,7 +178,7 @@ struct Ctx {
         if (stream) cudaStreamSynchronize(stream);
         prim64.free(); prim32.free(); cl64.free(); cl32.free(); cstart.free(); orig.free();
         albedo.free(); emission.free(); lights.free(); kindId.free();
-        gridStart.free(); gridList.free(); gridCounts.free(); gridU.free();
+        gridStart.free(); gridList.free(); gridCounts.free(); gridU.free(); gridKey.free();
         superBox.free(); superStart.free(); superList.free(); primBox.free();
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
@@ -505,6 +506,8 @@ void buildGrid(Ctx* c, const sdfgi_prim* prims, const int32_t* member_idx, const
     start[ncells] = static_cast<int>(total);
     c->gridStart.upload(start.data(), start.size(), c->stream);
     c->gridList.alloc(std::max<long long>(total, 1));
+    c->gridKey.alloc(std::max<long long>(total, 1));
+    p.lkey = c->gridKey.p;
     p.start = c->gridStart.p;
     p.list = c->gridList.p;
     launch_grid_list(p, static_cast<int>(ncells), true, c->stream);
@@ -519,6 +522,7 @@ void buildGrid(Ctx* c, const sdfgi_prim* prims, const int32_t* member_idx, const
     c->grid.finvH = static_cast<float>(1.0 / h);
     c->grid.start = c->gridStart.p;
     c->grid.list = c->gridList.p;
+    c->grid.lkey = c->gridKey.p;
     c->gridEntries = total;
 
     // superclusters for points off the grid: bounded clusters in Morton order of
