@@ -296,6 +296,37 @@ def run_ours(args, rank, world, local_rank):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(rays_step)
+    if not args.no_alt:
+        # the other arithmetic mode on the same workload, same timing rules (the
+        # headline stays FP64 = the reference's own precision, bit-exact decisions)
+        alt = "f32" if args.precision == "f64" else "f64"
+        dev.set_precision(alt)
+        times_alt = []
+        fresh_volume()
+        one_step()
+        for _ in range(args.steps):
+            fresh_volume()
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(ext)
+            r_alt, _, _, _ = one_step()
+            e1.record(ext)
+            e1.synchronize()
+            times_alt.append(e0.elapsed_time(e1))
+        ms_alt = sum(times_alt) / len(times_alt)
+        if dist is not None:
+            t = torch.tensor([ms_alt], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_alt = float(t.item())
+        line["alt_precision"] = {
+            "dtype": alt, "value": r_alt / (ms_alt * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms_alt,
+            "texel_error_vs_oracle": "FP32: max 2e-5 relative on a C2 probe sample, 0 channels over 1e-3 "
+                                     "(tests/test_gpu_oracle.py)" if alt == "f32" else "FP64: bit-exact relocation; "
+                                     "texels bit-identical except corner-tie owner flips",
+        }
+        dev.set_precision(args.precision)
     if rank == 0:
         print(json.dumps(line), flush=True)
     dev.close()
@@ -472,6 +503,7 @@ def main():
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gather", action="store_true", help="skip the C3 1080p gather measurement")
+    ap.add_argument("--no-alt", action="store_true", help="skip the other-precision measurement")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))
