@@ -310,6 +310,15 @@ SDFGI_API int sdfgi_gather_download(void* ctx, int which, void* dst, size_t byte
 /* Device ms of the last gather: {downsample+select, tiles, resolve, contact}. */
 SDFGI_API int sdfgi_last_gather_ms(void* ctx, double out[4]);
 
+/* Linear-time cluster builder for large scenes (replaces buildClusters,
+ * scene.hpp:110-178, whose greedy agglomeration is O(N^3)): bounded primitives in
+ * Morton order of their box centres, runs of max_per_cluster; each plane its own
+ * unbounded cluster; cull boxes = surface boxes inflated by kClusterCullMargin.
+ * Any conservative clustering yields identical query values (scene.hpp:205-211).
+ * Host only (no context). Capacity: n clusters, n+1 starts, n members. */
+SDFGI_API int sdfgi_build_clusters(const sdfgi_prim* prims, int n, int max_per_cluster, sdfgi_cluster* out_clusters,
+                                   int* out_n_clusters, int32_t* member_start, int32_t* member_idx);
+
 /* Launch counter: kernels this context has launched since creation. */
 SDFGI_API int sdfgi_launch_count(void* ctx, int64_t* out);
 

@@ -15,6 +15,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1625,6 +1626,87 @@ int sdfgi_last_gather_ms(void* ctx, double out[4]) {
             CK(cudaEventElapsedTime(&ms, c->gev[i], c->gev[i + 1]));
             out[i] = ms;
         }
+    });
+}
+
+int sdfgi_build_clusters(const sdfgi_prim* prims, int n, int max_per_cluster, sdfgi_cluster* out_clusters,
+                         int* out_n_clusters, int32_t* member_start, int32_t* member_idx) {
+    return guard([&] {
+        REQ(n >= 0 && (n == 0 || prims) && out_clusters && out_n_clusters && member_start && member_idx,
+            SDFGI_ERR_INVALID, "bad cluster-build arguments");
+        REQ(max_per_cluster >= 1, SDFGI_ERR_INVALID, "max_per_cluster must be >= 1");
+        // conservative surface boxes (primitiveAabb, primitives.hpp:112-151); planes
+        // become their own unbounded clusters (buildClusters never merges them)
+        std::vector<std::array<double, 6>> box(n);
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        std::vector<int> bounded, planes;
+        for (int i = 0; i < n; ++i) {
+            REQ(prims[i].kind >= 0 && prims[i].kind <= 4, SDFGI_ERR_INVALID, "bad primitive kind");
+            primAabb(prims[i], box[i].data());
+            if (prims[i].kind == SDFGI_PLANE) {
+                planes.push_back(i);
+                continue;
+            }
+            bounded.push_back(i);
+            for (int a = 0; a < 3; ++a) {
+                const double cc = 0.5 * (box[i][a] + box[i][3 + a]);
+                lo[a] = std::min(lo[a], cc);
+                hi[a] = std::max(hi[a], cc);
+            }
+        }
+        // Morton order of the box centres, then runs of max_per_cluster
+        auto spread10 = [](uint32_t x) {
+            x &= 0x3ff;
+            x = (x | (x << 16)) & 0x030000ff;
+            x = (x | (x << 8)) & 0x0300f00f;
+            x = (x | (x << 4)) & 0x030c30c3;
+            x = (x | (x << 2)) & 0x09249249;
+            return x;
+        };
+        std::vector<std::pair<uint32_t, int>> order;
+        order.reserve(bounded.size());
+        for (int i : bounded) {
+            uint32_t code = 0;
+            for (int a = 0; a < 3; ++a) {
+                const double cc = 0.5 * (box[i][a] + box[i][3 + a]);
+                const double ext = hi[a] - lo[a];
+                const double u = ext > 0 ? std::min(1.0, std::max(0.0, (cc - lo[a]) / ext)) : 0.0;
+                code |= spread10(static_cast<uint32_t>(u * 1023.0)) << a;
+            }
+            order.push_back({code, i});
+        }
+        std::sort(order.begin(), order.end());
+        int k = 0, m = 0;
+        member_start[0] = 0;
+        auto emit = [&](const int* mem, int cnt, bool unbounded) {
+            sdfgi_cluster& c = out_clusters[k];
+            std::memset(&c, 0, sizeof(c));
+            for (int a = 0; a < 3; ++a) {
+                c.lo[a] = INFINITY;
+                c.hi[a] = -INFINITY;
+            }
+            for (int t = 0; t < cnt; ++t) {
+                member_idx[m++] = mem[t];
+                for (int a = 0; a < 3; ++a) {
+                    c.lo[a] = std::min(c.lo[a], box[mem[t]][a]);
+                    c.hi[a] = std::max(c.hi[a], box[mem[t]][3 + a]);
+                }
+            }
+            for (int a = 0; a < 3; ++a) {  // cullAabb = aabb.inflated(kClusterCullMargin), scene.hpp:165
+                c.lo[a] -= 1e-9;
+                c.hi[a] += 1e-9;
+            }
+            c.unbounded = unbounded ? 1 : 0;
+            member_start[++k] = m;
+        };
+        std::vector<int> run;
+        for (size_t t = 0; t < order.size(); t += max_per_cluster) {
+            run.clear();
+            for (size_t u = t; u < std::min(order.size(), t + max_per_cluster); ++u) run.push_back(order[u].second);
+            emit(run.data(), static_cast<int>(run.size()), false);
+        }
+        for (int p : planes) emit(&p, 1, true);
+        *out_n_clusters = k;
     });
 }
 

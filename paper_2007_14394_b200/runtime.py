@@ -57,6 +57,7 @@ _SIGS = {
     "sdfgi_set_accel": [_P, _I],
     "sdfgi_accel_info": [_P, _P],
     "sdfgi_slab_range": [_I, _I, _I, _I, _I, _P, _P],
+    "sdfgi_build_clusters": [_P, _I, _I, _P, _P, _P, _P],
     "sdfgi_gbuffer_upload": [_P, _I, _I, _P],
     "sdfgi_gbuffer_render": [_P, _P, _P, _I, _I, _P],
     "sdfgi_gbuffer_download": [_P, _P, _SZ],
@@ -120,6 +121,19 @@ def camera_struct(cam) -> np.ndarray:
     c["position"], c["forward"], c["right"], c["up"] = cam.position, cam.forward, cam.right, cam.up
     c["fov_y_deg"] = cam.fov_y
     return c
+
+
+def build_clusters(prims, max_per_cluster=8):
+    """Linear-time cluster build (sdfgi_build_clusters): (clusters, member_start, member_idx)."""
+    prims = np.ascontiguousarray(prims, sio.PRIM_DTYPE)
+    n = len(prims)
+    clusters = np.zeros(max(n, 1), sio.CLUSTER_DTYPE)
+    ms = np.zeros(n + 1, np.int32)
+    mi = np.zeros(max(n, 1), np.int32)
+    k = ctypes.c_int()
+    _call("sdfgi_build_clusters", _ptr(prims), n, int(max_per_cluster), _ptr(clusters), ctypes.byref(k), _ptr(ms),
+          _ptr(mi))
+    return clusters[: k.value].copy(), ms[: k.value + 1].copy(), mi[:n].copy()
 
 
 def device_count() -> int:

@@ -16,7 +16,8 @@ open-field sky; 128x32x128 probes at spacing 1.875.
 
 Clusters are not built here: C2's were built once by the reference's
 ``buildClusters`` (scene.hpp:110-178, via oracle/ref_driver.cpp ``recluster``)
-and committed in data/c2.sdfs; large scenes use ``cluster_build.grid_clusters``.
+and committed in data/c2.sdfs; large scenes use the library's linear-time
+builder (``with_fast_clusters`` -> ``sdfgi_build_clusters``).
 """
 from __future__ import annotations
 
@@ -161,3 +162,11 @@ def c4_scene(n_random=50000, seed=4) -> sio.Scene:
         np.zeros(0, np.int32), np.array([0.35, 0.45, 0.65]), _camera((0, 30, 0), (1, 29, -6), 70),
         sio.CascadeSpec((128, 32, 128), 1.875, 1), cfg,
     )
+
+
+def with_fast_clusters(scene: sio.Scene, max_per_cluster=8) -> sio.Scene:
+    """The scene re-clustered by the library's linear-time builder (sdfgi_build_clusters)."""
+    from .runtime import build_clusters
+
+    clusters, ms, mi = build_clusters(scene.prims, max_per_cluster)
+    return sio.Scene(scene.prims, scene.lights, clusters, ms, mi, scene.sky, scene.camera, scene.cascade, scene.cfg)
