@@ -174,6 +174,7 @@ struct GridBuildParams {
     const int* start;
     int* list;
     float* lkey;  // per entry: lower bound of the candidate's SDF over the cell
+    int maxList;  // longer lists keep the nearest maxList + a sentinel (list = -1)
 };
 
 // Launch the whole wavefront for one batch (K0..K3) on `st`. `persistBlocks` sizes

@@ -46,21 +46,21 @@ __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells
     };
     // candidate PRIMITIVES: every member of an unbounded cluster, and members of
     // nearby clusters whose own conservative box is within r of the cell
-    int n = 0;
-    int out = fill ? P.start[cell] : 0;
-    for (int k = 0; k < P.scene.n_clusters; ++k) {
-        const DCluster<double>& cl = P.scene.clusters[k];
-        if (!cl.unbounded && gap2(cl.lo, cl.hi) > r2) continue;
-        for (int j = P.scene.cstart[k]; j < P.scene.cstart[k + 1]; ++j) {
-            const double* b = P.primBox + 6 * static_cast<size_t>(j);
-            if (cl.unbounded || isinf(b[0]) || gap2(b, b + 3) <= r2) {
-                if (fill) P.list[out + n] = j;
-                ++n;
+    auto forEach = [&](auto&& f) {
+        for (int k = 0; k < P.scene.n_clusters; ++k) {
+            const DCluster<double>& cl = P.scene.clusters[k];
+            if (!cl.unbounded && gap2(cl.lo, cl.hi) > r2) continue;
+            for (int j = P.scene.cstart[k]; j < P.scene.cstart[k + 1]; ++j) {
+                const double* b = P.primBox + 6 * static_cast<size_t>(j);
+                if (cl.unbounded || isinf(b[0]) || gap2(b, b + 3) <= r2) f(j);
             }
         }
-    }
+    };
+    const int K = P.maxList;
     if (!fill) {
-        P.counts[cell] = n;
+        int n = 0;
+        forEach([&](int) { ++n; });
+        P.counts[cell] = n > K ? K + 1 : n;
         return;
     }
     // nearest first (box distance to the cell centre): order does not affect
@@ -74,30 +74,51 @@ __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells
         double gz = fmax(fmax(b[2] - cz, cz - b[5]), 0.0);
         return gx * gx + gy * gy + gz * gz;
     };
+    const int out = P.start[cell];
+    const int slots = P.start[cell + 1] - out;
+    const bool truncated = slots == K + 1;
     int* L = P.list + out;
-    for (int a = 1; a < n; ++a) {
-        const int v = L[a];
+    // insertion into the sorted prefix, keeping at most K; the smallest key pushed
+    // out (or never admitted) bounds every omitted candidate
+    int m = 0;
+    double tail = INFINITY;
+    forEach([&](int v) {
         const double kv = key(v);
-        int b = a - 1;
+        if (m == K) {
+            const double kl = key(L[K - 1]);
+            if (!(kv < kl)) {
+                tail = fmin(tail, kv);
+                return;
+            }
+            tail = fmin(tail, kl);
+            --m;
+        }
+        int b = m - 1;
         while (b >= 0 && key(L[b]) > kv) {
             L[b + 1] = L[b];
             --b;
         }
         L[b + 1] = v;
-    }
+        ++m;
+    });
     // lower bound of each candidate's SDF over the cell: its surface box is at
     // least sqrt(key) - (half diagonal) from any point of the cell, and the SDF
     // outside the box is at least the distance to it. Rounded down into float with
     // the build margin, so `bound > d` proves the candidate cannot reach (or tie) d.
     const double half = 0.5 * sqrt(3.0) * (P.h + 2.0 * P.pad);
-    for (int a = 0; a < n; ++a) {
-        const double kv = key(L[a]);
+    auto bound = [&](double kv) {
         float lb = -INFINITY;
         if (kv >= 0) {
             const double b = sqrt(kv) - half - P.margin;
             lb = b > 0 ? __double2float_rd(b) : -INFINITY;  // no bound inside the reach of the cell
         }
-        P.lkey[out + a] = lb;
+        return lb;
+    };
+    for (int a = 0; a < m; ++a) P.lkey[out + a] = bound(key(L[a]));
+    if (truncated) {
+        // sentinel: a query still open here walks the cluster hierarchy
+        L[m] = -1;
+        P.lkey[out + m] = bound(tail);
     }
 }
 

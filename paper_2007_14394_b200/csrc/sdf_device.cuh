@@ -135,7 +135,9 @@ struct GridDev {
     const int* __restrict__ superList;      // cluster ids; unbounded clusters last (always visited)
     const double* __restrict__ superBox;    // 6 per supercluster (lo xyz, hi xyz)
     int nUnbounded;
-    int _pad2;
+    int nGroup;                             // groups of up to 16 consecutive superclusters
+    const int* __restrict__ groupStart;     // nGroup + 1 into the superclusters
+    const double* __restrict__ groupBox;    // 6 per group
 };
 
 template <typename R> struct SceneView {
@@ -304,7 +306,51 @@ template <typename R> struct QueryState {
     R d;
     int own;
     int cur, end;
+    bool walk;  // the query completes through hierarchyWalk
 };
+
+// Off the grid (and behind a truncated cell list): the unbounded clusters, then the
+// group of superclusters nearest to p (seeds the running minimum), then every other
+// group against it; inside a group, superclusters and clusters are skipped by their
+// boxes. Every skip is conservative, so the value and (with the CSR tie-break) the
+// owner are exact whatever the running minimum was on entry.
+template <typename R, bool ST>
+__device__ __forceinline__ void hierarchyWalk(const SceneView<R>& s, QueryState<R>& q, Counters* c) {
+    const GridDev& g = s.grid;
+    const V3<R> p = q.p;
+    const int u0 = g.superStart[g.nSuper];
+    for (int i = u0; i < u0 + g.nUnbounded; ++i) visitMembers<R, ST, true>(s, g.superList[i], p, q.d, q.own, c);
+    int nearest = -1;
+    R best = R(INFINITY);
+    for (int gr = 0; gr < g.nGroup; ++gr) {
+        const double* b = g.groupBox + 6 * gr;
+        R dx = smax(smax(R(b[0]) - p.x, p.x - R(b[3])), R(0));
+        R dy = smax(smax(R(b[1]) - p.y, p.y - R(b[4])), R(0));
+        R dz = smax(smax(R(b[2]) - p.z, p.z - R(b[5])), R(0));
+        R bs = dx * dx + dy * dy + dz * dz;
+        if (bs < best) {
+            best = bs;
+            nearest = gr;
+        }
+    }
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int gr = (pass ? 0 : nearest); gr < (pass ? g.nGroup : nearest + 1); ++gr) {
+            if (gr < 0 || (pass && gr == nearest)) continue;
+            if (pass && boxSkipped(g.groupBox + 6 * gr, p, q.d)) continue;
+            for (int sc = g.groupStart[gr]; sc < g.groupStart[gr + 1]; ++sc) {
+                if (boxSkipped(g.superBox + 6 * sc, p, q.d)) continue;
+                for (int i = g.superStart[sc]; i < g.superStart[sc + 1]; ++i) {
+                    const int k = g.superList[i];
+                    if (clusterSkipped(s.clusters[k], p, q.d)) {
+                        if (ST) ++c->cs;
+                        continue;
+                    }
+                    visitMembers<R, ST, true>(s, k, p, q.d, q.own, c);
+                }
+            }
+        }
+    }
+}
 
 template <typename R, bool ST>
 __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R initD, QueryState<R>& q, Counters* c) {
@@ -312,6 +358,7 @@ __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R ini
     q.d = initD;
     q.own = -1;
     q.cur = q.end = 0;
+    q.walk = false;
     if (ST) ++c->q;
     if (!s.useGrid) {
         // the reference's walk: every cluster in order, strict `<`
@@ -341,40 +388,12 @@ __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R ini
         if (ST) c->pe += q.end - q.cur;
         return;
     }
-    // off the grid: the unbounded clusters, then the supercluster nearest to p
-    // (seeds the running minimum), then every other supercluster against it
-    const int u0 = g.superStart[g.nSuper];
-    for (int i = u0; i < u0 + g.nUnbounded; ++i) visitMembers<R, ST, true>(s, g.superList[i], p, q.d, q.own, c);
-    int nearest = -1;
-    R best = R(INFINITY);
-    for (int sc = 0; sc < g.nSuper; ++sc) {
-        const double* b = g.superBox + 6 * sc;
-        R dx = smax(smax(R(b[0]) - p.x, p.x - R(b[3])), R(0));
-        R dy = smax(smax(R(b[1]) - p.y, p.y - R(b[4])), R(0));
-        R dz = smax(smax(R(b[2]) - p.z, p.z - R(b[5])), R(0));
-        R bs = dx * dx + dy * dy + dz * dz;
-        if (bs < best) {
-            best = bs;
-            nearest = sc;
-        }
-    }
-    for (int pass = 0; pass < 2; ++pass) {
-        for (int sc = (pass ? 0 : nearest); sc < (pass ? g.nSuper : nearest + 1); ++sc) {
-            if (sc < 0 || (pass && sc == nearest)) continue;
-            if (boxSkipped(g.superBox + 6 * sc, p, q.d)) continue;
-            for (int i = g.superStart[sc]; i < g.superStart[sc + 1]; ++i) {
-                const int k = g.superList[i];
-                if (clusterSkipped(s.clusters[k], p, q.d)) {
-                    if (ST) ++c->cs;
-                    continue;
-                }
-                visitMembers<R, ST, true>(s, k, p, q.d, q.own, c);
-            }
-        }
-    }
+    q.walk = true;
 }
 
-// One candidate of the cell list (lowest-CSR-position tie-break: order-free).
+// One candidate of the cell list (lowest-CSR-position tie-break: order-free). A
+// truncated list ends in a sentinel (-1) whose bound covers every omitted candidate;
+// a query still open there completes through the cluster hierarchy.
 template <typename R, bool ST>
 __device__ __forceinline__ void queryStep(const SceneView<R>& s, QueryState<R>& q, Counters* c) {
     if (R(s.grid.lkey[q.cur]) > q.d) {  // this and every later candidate is farther
@@ -382,6 +401,11 @@ __device__ __forceinline__ void queryStep(const SceneView<R>& s, QueryState<R>& 
         return;
     }
     const int j = s.grid.list[q.cur++];
+    if (j < 0) {
+        q.walk = true;
+        q.cur = q.end;
+        return;
+    }
     if (ST) {
         ++c->ek[s.kindId[j] & 0xff];
         c->ek[5] += (s.kindId[j] >> 8) ? 0 : 1;
@@ -398,6 +422,7 @@ __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int*
     QueryState<R> q;
     queryBegin<R, ST>(s, p, initD, q, c);
     while (q.cur < q.end) queryStep<R, ST>(s, q, c);
+    if (q.walk) hierarchyWalk<R, ST>(s, q, c);
     if (owner) *owner = q.own;
     return q.d;
 }

@@ -136,8 +136,15 @@ struct Ctx {
     long long gridEntries = 0;
     DBuf<int> gridStart, gridList, gridCounts;
     DBuf<float> gridKey;
-    DBuf<double> gridU, superBox, primBox;
-    DBuf<int> superStart, superList;
+    DBuf<double> gridU, superBox, primBox, groupBox;
+    DBuf<int> superStart, superList, groupStart;
+    double gridBox[6] = {0, 0, 0, 0, 0, 0};  // region the cells cover
+    bool hintValid = false;
+    double hint[6] = {0, 0, 0, 0, 0, 0};     // probe volumes the grid must cover
+    // host copy of the uploaded scene (the grid is rebuilt when the hint grows)
+    std::vector<sdfgi_prim> hPrims;
+    std::vector<int32_t> hMember;
+    std::vector<sdfgi_cluster> hClusters;
     // probes
     std::vector<CascadeHost> cascades;
     int octRes = 8;
@@ -181,6 +188,7 @@ struct Ctx {
         albedo.free(); emission.free(); lights.free(); kindId.free();
         gridStart.free(); gridList.free(); gridCounts.free(); gridU.free(); gridKey.free();
         superBox.free(); superStart.free(); superList.free(); primBox.free();
+        groupBox.free(); groupStart.free();
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
         records.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
@@ -424,7 +432,11 @@ void primAabb(const sdfgi_prim& s, double* out) {
     }
 }
 
-void buildGrid(Ctx* c, const sdfgi_prim* prims, const int32_t* member_idx, const sdfgi_cluster* clusters, int n) {
+void buildGrid(Ctx* c) {
+    const sdfgi_prim* prims = c->hPrims.data();
+    const int32_t* member_idx = c->hMember.data();
+    const sdfgi_cluster* clusters = c->hClusters.data();
+    const int n = static_cast<int>(c->hClusters.size());
     c->haveGrid = false;
     c->gridEntries = 0;
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
@@ -440,7 +452,9 @@ void buildGrid(Ctx* c, const sdfgi_prim* prims, const int32_t* member_idx, const
     if (bounded == 0 || n < 2) return;
     double ext[3], scale = 0;
     // the grid extends past the geometry so rays leaving the scene stay on the
-    // (cheap) candidate lists for their first steps; SDFGI_GRID_MARGIN overrides
+    // (cheap) candidate lists for their first steps; SDFGI_GRID_MARGIN overrides.
+    // It also covers the probe volumes (the hint box grown by sdfgi_cascade_set):
+    // probes above an open scene would otherwise query off the grid every step.
     const char* menv = std::getenv("SDFGI_GRID_MARGIN");
     const double marginFrac = menv ? std::atof(menv) : 0.3;  // measured on C2: 0.02 -> 0.3 = -23% K1+K2
     for (int a = 0; a < 3; ++a) {
@@ -448,6 +462,10 @@ void buildGrid(Ctx* c, const sdfgi_prim* prims, const int32_t* member_idx, const
         double m = marginFrac * e + 1e-3;
         lo[a] -= m;
         hi[a] += m;
+        if (c->hintValid) {
+            lo[a] = std::min(lo[a], c->hint[a]);
+            hi[a] = std::max(hi[a], c->hint[3 + a]);
+        }
         ext[a] = hi[a] - lo[a];
         scale = std::max(scale, std::max(std::fabs(lo[a]), std::fabs(hi[a])));
     }
@@ -479,6 +497,11 @@ void buildGrid(Ctx* c, const sdfgi_prim* prims, const int32_t* member_idx, const
     // pad the cells for FP32 point->cell rounding; slack covers every rounding on the way
     p.pad = 1e-4 * h + 4e-6 * scale;
     p.margin = 1e-5 * (scale + 1.0);
+    // cells far from the geometry would list every primitive within their (large)
+    // bound; lists keep the maxList nearest plus a sentinel carrying the omitted
+    // candidates' lower bound (a query that cannot stop there walks the hierarchy)
+    const char* lenv = std::getenv("SDFGI_GRID_MAXLIST");
+    p.maxList = lenv ? std::max(8, std::atoi(lenv)) : 96;
     c->gridU.alloc(ncells);
     c->gridCounts.alloc(ncells);
     c->gridStart.alloc(ncells + 1);
@@ -517,6 +540,8 @@ void buildGrid(Ctx* c, const sdfgi_prim* prims, const int32_t* member_idx, const
     for (int a = 0; a < 3; ++a) {
         c->grid.lo[a] = lo[a];
         c->grid.dim[a] = dim[a];
+        c->gridBox[a] = lo[a];
+        c->gridBox[3 + a] = lo[a] + dim[a] * h;
     }
     c->grid.invH = 1.0 / h;
     for (int a = 0; a < 3; ++a) c->grid.flo[a] = static_cast<float>(lo[a]);
@@ -575,14 +600,39 @@ void buildGrid(Ctx* c, const sdfgi_prim* prims, const int32_t* member_idx, const
     }
     sStart[nSuper] = static_cast<int>(sList.size());
     sList.insert(sList.end(), unb.begin(), unb.end());
+    // second level: 16 Morton-consecutive superclusters per group, so an off-grid
+    // query scans nSuper/16 group boxes instead of every supercluster box
+    const int gper = 16;
+    const int nGroup = (nSuper + gper - 1) / gper;
+    std::vector<int> gStart(nGroup + 1);
+    std::vector<double> gBox(6 * static_cast<size_t>(std::max(nGroup, 1)));
+    for (int gr = 0; gr < nGroup; ++gr) {
+        gStart[gr] = gr * gper;
+        for (int a = 0; a < 3; ++a) {
+            gBox[6 * gr + a] = INFINITY;
+            gBox[6 * gr + 3 + a] = -INFINITY;
+        }
+        for (int sc = gr * gper; sc < std::min(nSuper, (gr + 1) * gper); ++sc) {
+            for (int a = 0; a < 3; ++a) {
+                gBox[6 * gr + a] = std::min(gBox[6 * gr + a], sBox[6 * sc + a]);
+                gBox[6 * gr + 3 + a] = std::max(gBox[6 * gr + 3 + a], sBox[6 * sc + 3 + a]);
+            }
+        }
+    }
+    gStart[nGroup] = nSuper;
     c->superStart.upload(sStart.data(), sStart.size(), c->stream);
     c->superList.upload(sList.data(), std::max<size_t>(sList.size(), 1), c->stream);
     c->superBox.upload(sBox.data(), sBox.size(), c->stream);
+    c->groupStart.upload(gStart.data(), gStart.size(), c->stream);
+    c->groupBox.upload(gBox.data(), gBox.size(), c->stream);
     CK(cudaStreamSynchronize(c->stream));
     c->grid.nSuper = nSuper;
     c->grid.superStart = c->superStart.p;
     c->grid.superList = c->superList.p;
     c->grid.superBox = c->superBox.p;
+    c->grid.nGroup = nGroup;
+    c->grid.groupStart = c->groupStart.p;
+    c->grid.groupBox = c->groupBox.p;
     c->grid.nUnbounded = static_cast<int>(unb.size());
     c->haveGrid = true;
 }
@@ -917,7 +967,10 @@ int sdfgi_scene_upload(void* ctx, const sdfgi_prim* prims, int n_prims, const sd
         c->nLights = n_lights;
         for (int k = 0; k < 3; ++k) c->sky[k] = sky[k];
         c->haveScene = true;
-        buildGrid(c, prims, member_idx, clusters, n_clusters);
+        c->hPrims.assign(prims, prims + n_prims);
+        c->hMember.assign(member_idx, member_idx + nMembers);
+        c->hClusters.assign(clusters, clusters + n_clusters);
+        buildGrid(c);
     });
 }
 
@@ -962,6 +1015,27 @@ int sdfgi_cascade_set(void* ctx, int level, int res_x, int res_y, int res_z, dou
         c->octRes = oct_res;
         c->front = 0;
         reallocProbes(c);
+        // grow the grid over this volume (one probe spacing of slack, plus a quarter
+        // of the volume so a scrolling cascade does not rebuild every frame)
+        double box[6];
+        bool covered = c->haveGrid;
+        for (int a = 0; a < 3; ++a) {
+            const int r = a == 0 ? res_x : (a == 1 ? res_y : res_z);
+            box[a] = origin[a] - spacing;
+            box[3 + a] = origin[a] + r * spacing;
+            covered = covered && box[a] >= c->gridBox[a] && box[3 + a] <= c->gridBox[3 + a];
+        }
+        const char* henv = std::getenv("SDFGI_GRID_HINT");
+        if (!covered && !(henv && std::atoi(henv) == 0)) {
+            for (int a = 0; a < 3; ++a) {
+                const double slack = 0.25 * (box[3 + a] - box[a]);
+                const double blo = box[a] - slack, bhi = box[3 + a] + slack;
+                c->hint[a] = c->hintValid ? std::min(c->hint[a], blo) : blo;
+                c->hint[3 + a] = c->hintValid ? std::max(c->hint[3 + a], bhi) : bhi;
+            }
+            c->hintValid = true;
+            if (c->haveScene) buildGrid(c);
+        }
     });
 }
 

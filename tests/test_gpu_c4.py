@@ -36,6 +36,16 @@ def test_c4_queries_bit_exact(c4):
         d_o, o_o = ora.query(pts)
         assert np.array_equal(d_g, d_o)
         assert np.array_equal(o_g, o_o)
+        # the C4 probe volume reaches y = 60, above the geometry grid: setting the
+        # cascade grows the grid over it (far cells end in truncated lists)
+        dim0 = info["dim"]
+        cs = c4.cascade
+        api.makeCascade(dev, *cs.res, cs.spacing, 0, c4.camera.position)
+        info = dev.accel_info()
+        assert info["dim"] != dim0 and info["grid"]
+        d_g, o_g = dev.query_points(pts)
+        assert np.array_equal(d_g, d_o)
+        assert np.array_equal(o_g, o_o)
 
 
 def test_c4_relocation_and_pass_subvolume(c4):
