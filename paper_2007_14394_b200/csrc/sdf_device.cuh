@@ -112,32 +112,39 @@ struct DLight {  // sdfgi_light, kept in double in both modes (tiny)
 // primitives whose conservative AABB lies within max(U, 0) of the cell can hold
 // the minimum — or tie with it — at any point of the cell; the cell's list holds
 // exactly those (CSR positions, nearest first) and the query evaluates them
-// without cluster tests. Points outside the grid walk superclusters: Morton-ordered groups of 8
-// bounded clusters under one box (a group is skipped only if every member would
-// be), then the unbounded clusters. Visiting order no longer follows cluster
-// order, so queryAccel breaks distance ties explicitly towards the lowest CSR
-// position — the primitive the reference's in-order walk keeps (scene.hpp:243) —
-// and values and owners stay identical to the reference's.
+// without cluster tests. Points outside the grid (and queries still open at a
+// truncated list's sentinel) walk a bounding-volume hierarchy over the bounded
+// clusters nearest child first, then visit the unbounded clusters. Visiting order
+// no longer follows cluster order, so the walks break distance ties explicitly
+// towards the lowest CSR position — the primitive the reference's in-order walk
+// keeps (scene.hpp:243) — and values and owners stay identical to the reference's.
+//
+// BVH node: the two children's boxes (padded outward, float) and their codes:
+// code >= 0 an inner node, code < 0 the cluster -code - 1.
+struct BNode {
+    float lo[2][3];
+    float hi[2][3];
+    int child[2];
+};
+constexpr int kBvhStack = 24;  // median splits: depth <= ceil(log2(clusters)) (16M clusters)
+
 struct GridDev {
     double lo[3];
     double invH;
     float flo[3];   // the same in float for the FP32 path
     float finvH;
     int dim[3];
-    int nSuper;
+    int bvhRoot;    // code of the root (see BNode); meaningless when nBounded == 0
     const int* __restrict__ start;  // ncells + 1
     const int* __restrict__ list;
     // per list entry: a lower bound on that primitive's SDF anywhere in the cell
     // (box distance to the cell centre - padded half diagonal, rounded down);
     // entries are sorted by it, so a query stops at the first bound > its minimum
     const float* __restrict__ lkey;
-    const int* __restrict__ superStart;     // nSuper + 1 into superList
-    const int* __restrict__ superList;      // cluster ids; unbounded clusters last (always visited)
-    const double* __restrict__ superBox;    // 6 per supercluster (lo xyz, hi xyz)
+    const BNode* __restrict__ bvh;
+    const int* __restrict__ unbounded;  // cluster ids of the unbounded clusters
     int nUnbounded;
-    int nGroup;                             // groups of up to 16 consecutive superclusters
-    const int* __restrict__ groupStart;     // nGroup + 1 into the superclusters
-    const double* __restrict__ groupBox;    // 6 per group
+    int nBounded;
 };
 
 template <typename R> struct SceneView {
@@ -285,15 +292,6 @@ __device__ __forceinline__ void visitMembers(const SceneView<R>& s, int k, V3<R>
     }
 }
 
-template <typename R>
-__device__ __forceinline__ bool boxSkipped(const double* b, V3<R> p, R d) {
-    R dx = smax(smax(R(b[0]) - p.x, p.x - R(b[3])), R(0));
-    R dy = smax(smax(R(b[1]) - p.y, p.y - R(b[4])), R(0));
-    R dz = smax(smax(R(b[2]) - p.z, p.z - R(b[5])), R(0));
-    R boxSq = dx * dx + dy * dy + dz * dz;
-    return d > R(0) ? boxSq >= d * d : boxSq > R(0);
-}
-
 // An SDF query in flight: the point, the running minimum/owner, and (inside the
 // candidate grid) the cursor over the cell's candidate list. queryBegin either
 // sets the cursor or — off the grid, or with the grid disabled — completes the
@@ -310,45 +308,64 @@ template <typename R> struct QueryState {
 };
 
 // Off the grid (and behind a truncated cell list): the unbounded clusters, then the
-// group of superclusters nearest to p (seeds the running minimum), then every other
-// group against it; inside a group, superclusters and clusters are skipped by their
-// boxes. Every skip is conservative, so the value and (with the CSR tie-break) the
-// owner are exact whatever the running minimum was on entry.
+// BVH nearest child first with a short stack. A subtree is dropped only when its
+// padded box is strictly farther than the running minimum (ties are visited), so
+// the value and (with the CSR tie-break) the owner are exact whatever the running
+// minimum was on entry.
+template <typename R>
+__device__ __forceinline__ R boxDistSq(const float* lo, const float* hi, V3<R> p) {
+    R dx = smax(smax(R(lo[0]) - p.x, p.x - R(hi[0])), R(0));
+    R dy = smax(smax(R(lo[1]) - p.y, p.y - R(hi[1])), R(0));
+    R dz = smax(smax(R(lo[2]) - p.z, p.z - R(hi[2])), R(0));
+    return dx * dx + dy * dy + dz * dz;
+}
+template <typename R>
+__device__ __forceinline__ bool boxReaches(R boxSq, R d) {
+    return d > R(0) ? boxSq <= d * d : boxSq <= R(0);
+}
+
 template <typename R, bool ST>
 __device__ __forceinline__ void hierarchyWalk(const SceneView<R>& s, QueryState<R>& q, Counters* c) {
     const GridDev& g = s.grid;
     const V3<R> p = q.p;
-    const int u0 = g.superStart[g.nSuper];
-    for (int i = u0; i < u0 + g.nUnbounded; ++i) visitMembers<R, ST, true>(s, g.superList[i], p, q.d, q.own, c);
-    int nearest = -1;
-    R best = R(INFINITY);
-    for (int gr = 0; gr < g.nGroup; ++gr) {
-        const double* b = g.groupBox + 6 * gr;
-        R dx = smax(smax(R(b[0]) - p.x, p.x - R(b[3])), R(0));
-        R dy = smax(smax(R(b[1]) - p.y, p.y - R(b[4])), R(0));
-        R dz = smax(smax(R(b[2]) - p.z, p.z - R(b[5])), R(0));
-        R bs = dx * dx + dy * dy + dz * dz;
-        if (bs < best) {
-            best = bs;
-            nearest = gr;
+    for (int i = 0; i < g.nUnbounded; ++i) visitMembers<R, ST, true>(s, g.unbounded[i], p, q.d, q.own, c);
+    if (g.nBounded == 0) return;
+    int stackN[kBvhStack];
+    R stackB[kBvhStack];
+    int sp = 0;
+    int next = g.bvhRoot;
+    while (true) {
+        if (next >= 0) {
+            const BNode& n = g.bvh[next];
+            const R b0 = boxDistSq(n.lo[0], n.hi[0], p), b1 = boxDistSq(n.lo[1], n.hi[1], p);
+            const bool k0 = boxReaches(b0, q.d), k1 = boxReaches(b1, q.d);
+            if (k0 && k1) {
+                const int nr = b1 < b0 ? 1 : 0;
+                stackN[sp] = n.child[1 - nr];
+                stackB[sp] = nr ? b0 : b1;
+                ++sp;
+                next = n.child[nr];
+                continue;
+            }
+            if (k0 || k1) {
+                next = n.child[k0 ? 0 : 1];
+                continue;
+            }
+            if (ST) c->cs += 2;
+        } else {
+            visitMembers<R, ST, true>(s, -next - 1, p, q.d, q.own, c);
         }
-    }
-    for (int pass = 0; pass < 2; ++pass) {
-        for (int gr = (pass ? 0 : nearest); gr < (pass ? g.nGroup : nearest + 1); ++gr) {
-            if (gr < 0 || (pass && gr == nearest)) continue;
-            if (pass && boxSkipped(g.groupBox + 6 * gr, p, q.d)) continue;
-            for (int sc = g.groupStart[gr]; sc < g.groupStart[gr + 1]; ++sc) {
-                if (boxSkipped(g.superBox + 6 * sc, p, q.d)) continue;
-                for (int i = g.superStart[sc]; i < g.superStart[sc + 1]; ++i) {
-                    const int k = g.superList[i];
-                    if (clusterSkipped(s.clusters[k], p, q.d)) {
-                        if (ST) ++c->cs;
-                        continue;
-                    }
-                    visitMembers<R, ST, true>(s, k, p, q.d, q.own, c);
-                }
+        // pop the nearest pending subtree still within reach
+        bool more = false;
+        while (sp > 0) {
+            --sp;
+            if (boxReaches(stackB[sp], q.d)) {
+                next = stackN[sp];
+                more = true;
+                break;
             }
         }
+        if (!more) break;
     }
 }
 

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -136,8 +137,9 @@ struct Ctx {
     long long gridEntries = 0;
     DBuf<int> gridStart, gridList, gridCounts;
     DBuf<float> gridKey;
-    DBuf<double> gridU, superBox, primBox, groupBox;
-    DBuf<int> superStart, superList, groupStart;
+    DBuf<double> gridU, primBox;
+    DBuf<BNode> bvh;
+    DBuf<int> unbList;
     double gridBox[6] = {0, 0, 0, 0, 0, 0};  // region the cells cover
     bool hintValid = false;
     double hint[6] = {0, 0, 0, 0, 0, 0};     // probe volumes the grid must cover
@@ -187,8 +189,7 @@ struct Ctx {
         prim64.free(); prim32.free(); cl64.free(); cl32.free(); cstart.free(); orig.free();
         albedo.free(); emission.free(); lights.free(); kindId.free();
         gridStart.free(); gridList.free(); gridCounts.free(); gridU.free(); gridKey.free();
-        superBox.free(); superStart.free(); superList.free(); primBox.free();
-        groupBox.free(); groupStart.free();
+        bvh.free(); unbList.free(); primBox.free();
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
         records.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
@@ -551,88 +552,79 @@ void buildGrid(Ctx* c) {
     c->grid.lkey = c->gridKey.p;
     c->gridEntries = total;
 
-    // superclusters for points off the grid: bounded clusters in Morton order of
-    // their box centres, 8 per group; boxes padded like the FP32 cluster boxes so
-    // the group skip is conservative in both precisions.
-    auto spread10 = [](uint32_t x) {
-        x &= 0x3ff;
-        x = (x | (x << 16)) & 0x030000ff;
-        x = (x | (x << 8)) & 0x0300f00f;
-        x = (x | (x << 4)) & 0x030c30c3;
-        x = (x | (x << 2)) & 0x09249249;
-        return x;
+    // BVH over the bounded clusters for points off the grid: median split of the
+    // box centres along the widest axis (depth <= ceil(log2 n) < kBvhStack), one
+    // cluster per leaf. Child boxes are padded like the FP32 cluster boxes and
+    // rounded outward to float, so the subtree tests are conservative in both
+    // precisions.
+    std::vector<int> unb, ids;
+    for (int k = 0; k < n; ++k) (clusters[k].unbounded ? unb : ids).push_back(k);
+    std::vector<BNode> nodes;
+    nodes.reserve(ids.size());
+    struct Box {
+        double lo[3], hi[3];
     };
-    std::vector<std::pair<uint32_t, int>> order;
-    std::vector<int> unb;
-    for (int k = 0; k < n; ++k) {
-        if (clusters[k].unbounded) {
-            unb.push_back(k);
-            continue;
-        }
-        uint32_t code = 0;
+    auto boxOf = [&](int b, int e) {
+        Box r;
         for (int a = 0; a < 3; ++a) {
-            double cc = 0.5 * (clusters[k].lo[a] + clusters[k].hi[a]);
-            double u = std::min(1.0, std::max(0.0, (cc - lo[a]) / ext[a]));
-            code |= spread10(static_cast<uint32_t>(u * 1023.0)) << a;
+            r.lo[a] = INFINITY;
+            r.hi[a] = -INFINITY;
         }
-        order.push_back({code, k});
-    }
-    std::sort(order.begin(), order.end());
-    const int per = 8;
-    const int nSuper = static_cast<int>((order.size() + per - 1) / per);
-    std::vector<int> sStart(nSuper + 1), sList;
-    std::vector<double> sBox(6 * static_cast<size_t>(std::max(nSuper, 1)));
-    for (int sc = 0; sc < nSuper; ++sc) {
-        sStart[sc] = static_cast<int>(sList.size());
-        double blo[3] = {INFINITY, INFINITY, INFINITY}, bhi[3] = {-INFINITY, -INFINITY, -INFINITY};
-        for (size_t i = sc * per; i < std::min(order.size(), static_cast<size_t>(sc + 1) * per); ++i) {
-            const int k = order[i].second;
-            sList.push_back(k);
+        for (int i = b; i < e; ++i)
             for (int a = 0; a < 3; ++a) {
-                blo[a] = std::min(blo[a], clusters[k].lo[a]);
-                bhi[a] = std::max(bhi[a], clusters[k].hi[a]);
+                r.lo[a] = std::min(r.lo[a], clusters[ids[i]].lo[a]);
+                r.hi[a] = std::max(r.hi[a], clusters[ids[i]].hi[a]);
             }
-        }
-        for (int a = 0; a < 3; ++a) {
-            sBox[6 * sc + a] = blo[a] - 2e-5 * (std::fabs(blo[a]) + 1.0);
-            sBox[6 * sc + 3 + a] = bhi[a] + 2e-5 * (std::fabs(bhi[a]) + 1.0);
-        }
-    }
-    sStart[nSuper] = static_cast<int>(sList.size());
-    sList.insert(sList.end(), unb.begin(), unb.end());
-    // second level: 16 Morton-consecutive superclusters per group, so an off-grid
-    // query scans nSuper/16 group boxes instead of every supercluster box
-    const int gper = 16;
-    const int nGroup = (nSuper + gper - 1) / gper;
-    std::vector<int> gStart(nGroup + 1);
-    std::vector<double> gBox(6 * static_cast<size_t>(std::max(nGroup, 1)));
-    for (int gr = 0; gr < nGroup; ++gr) {
-        gStart[gr] = gr * gper;
-        for (int a = 0; a < 3; ++a) {
-            gBox[6 * gr + a] = INFINITY;
-            gBox[6 * gr + 3 + a] = -INFINITY;
-        }
-        for (int sc = gr * gper; sc < std::min(nSuper, (gr + 1) * gper); ++sc) {
+        return r;
+    };
+    // returns the code of the subtree over ids[b, e)
+    std::function<int(int, int, int)> build = [&](int b, int e, int depth) -> int {
+        REQ(depth < kBvhStack, SDFGI_ERR_INVALID, "cluster BVH too deep");
+        if (e - b == 1) return -ids[b] - 1;
+        double clo[3] = {INFINITY, INFINITY, INFINITY}, chi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int i = b; i < e; ++i)
             for (int a = 0; a < 3; ++a) {
-                gBox[6 * gr + a] = std::min(gBox[6 * gr + a], sBox[6 * sc + a]);
-                gBox[6 * gr + 3 + a] = std::max(gBox[6 * gr + 3 + a], sBox[6 * sc + 3 + a]);
+                const double m = 0.5 * (clusters[ids[i]].lo[a] + clusters[ids[i]].hi[a]);
+                clo[a] = std::min(clo[a], m);
+                chi[a] = std::max(chi[a], m);
             }
+        int axis = 0;
+        for (int a = 1; a < 3; ++a)
+            if (chi[a] - clo[a] > chi[axis] - clo[axis]) axis = a;
+        const int mid = (b + e) / 2;
+        std::nth_element(ids.begin() + b, ids.begin() + mid, ids.begin() + e, [&](int x, int y) {
+            const double mx = clusters[x].lo[axis] + clusters[x].hi[axis];
+            const double my = clusters[y].lo[axis] + clusters[y].hi[axis];
+            return mx < my || (mx == my && x < y);
+        });
+        const int self = static_cast<int>(nodes.size());
+        nodes.emplace_back();
+        const int range[2][2] = {{b, mid}, {mid, e}};
+        for (int ch = 0; ch < 2; ++ch) {
+            const Box bx = boxOf(range[ch][0], range[ch][1]);
+            for (int a = 0; a < 3; ++a) {
+                const double lo = bx.lo[a] - 2e-5 * (std::fabs(bx.lo[a]) + 1.0);
+                const double hi = bx.hi[a] + 2e-5 * (std::fabs(bx.hi[a]) + 1.0);
+                nodes[self].lo[ch][a] = std::nextafter(static_cast<float>(lo), -INFINITY);
+                nodes[self].hi[ch][a] = std::nextafter(static_cast<float>(hi), INFINITY);
+            }
+            const int code = build(range[ch][0], range[ch][1], depth + 1);
+            nodes[self].child[ch] = code;
         }
-    }
-    gStart[nGroup] = nSuper;
-    c->superStart.upload(sStart.data(), sStart.size(), c->stream);
-    c->superList.upload(sList.data(), std::max<size_t>(sList.size(), 1), c->stream);
-    c->superBox.upload(sBox.data(), sBox.size(), c->stream);
-    c->groupStart.upload(gStart.data(), gStart.size(), c->stream);
-    c->groupBox.upload(gBox.data(), gBox.size(), c->stream);
+        return self;
+    };
+    int root = 0;
+    if (!ids.empty()) root = build(0, static_cast<int>(ids.size()), 0);
+    std::vector<int> unbPad(unb);
+    if (nodes.empty()) nodes.emplace_back();  // never read (nBounded < 2 uses the root code only)
+    if (unbPad.empty()) unbPad.push_back(0);
+    c->bvh.upload(nodes.data(), nodes.size(), c->stream);
+    c->unbList.upload(unbPad.data(), unbPad.size(), c->stream);
     CK(cudaStreamSynchronize(c->stream));
-    c->grid.nSuper = nSuper;
-    c->grid.superStart = c->superStart.p;
-    c->grid.superList = c->superList.p;
-    c->grid.superBox = c->superBox.p;
-    c->grid.nGroup = nGroup;
-    c->grid.groupStart = c->groupStart.p;
-    c->grid.groupBox = c->groupBox.p;
+    c->grid.bvh = c->bvh.p;
+    c->grid.bvhRoot = root;
+    c->grid.nBounded = static_cast<int>(ids.size());
+    c->grid.unbounded = c->unbList.p;
     c->grid.nUnbounded = static_cast<int>(unb.size());
     c->haveGrid = true;
 }
