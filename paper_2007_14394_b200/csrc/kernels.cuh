@@ -61,6 +61,22 @@ template <typename R> struct __align__(16) HitRec {
     int status;  // bit0 converged, bits1-2 MissReason, bits 8.. steps
 };
 
+// A march parked by K1 when its next point leaves the candidate grid; the far
+// phase of K1 resumes it (state exactly as before the parked query).
+template <typename R> struct __align__(16) ParkRay {
+    R o[3], dir[3];
+    R t, lastD, d, tMax;
+    int step, state, pol, owner;
+    unsigned long long rid;
+};
+// The same for a shadow march of K2.
+template <typename R> struct __align__(16) ParkShadow {
+    R o[3], dir[3];
+    R t, tEnd, v, lastD;
+    int step, pad;
+    unsigned long long slot;
+};
+
 template <typename R> struct WaveParams {
     SceneView<R> scene;
     ProbeCommon pc;
@@ -85,7 +101,14 @@ template <typename R> struct WaveParams {
     int* hitList;             // compacted ray ids of converged hits with an owner
     R* vis;                   // per (ray, light)
     R* rad;                   // per ray: shaded radiance (3)
-    unsigned long long* ctr;  // [0] K1 ray cursor, [1] hit count, [2] K2 item cursor
+    // [0] K1 ray cursor, [1] hit count, [2] K2 item cursor, [4] rays parked by K1,
+    // [5] K1 far-phase cursor, [6] shadow marches parked by K2, [7] K2 far cursor
+    unsigned long long* ctr;
+    // off-grid marches are parked here and resumed together by a far phase, so
+    // the hierarchy walks run side by side instead of stalling near-field warps
+    // (null: no parking). K1 and K2 reuse the buffer (K1's far phase ends first).
+    void* park;
+    unsigned long long parkBytes;
     // results
     unsigned long long* stats;       // counters or null
     unsigned long long* maxDeltaBits;

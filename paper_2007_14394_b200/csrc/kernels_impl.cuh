@@ -246,9 +246,25 @@ __device__ __forceinline__ bool contactRay(const WaveParams<R>& P, long long ite
     return true;
 }
 
-template <typename R, bool ST, int MODE>
+// Warp-aggregated slot in a parking buffer (all 32 lanes call; -1 = not parked).
+__device__ __forceinline__ long long parkSlot(unsigned long long* counter, bool park) {
+    const unsigned m = __ballot_sync(kFull, park);
+    if (m == 0) return -1;
+    const unsigned lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    unsigned long long base = 0;
+    if (static_cast<int>(lane) == leader) base = atomicAdd(counter, static_cast<unsigned long long>(__popc(m)));
+    base = __shfl_sync(kFull, base, leader);
+    return park ? static_cast<long long>(base + __popc(m & ((1u << lane) - 1u))) : -1;
+}
+
+// PHASE 0 traces new rays and parks every march whose next point is off the
+// candidate grid; PHASE 1 resumes the parked marches (no further parking).
+template <typename R, bool ST, int MODE, int PHASE>
 __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P) {
-    const long long total = rayTotal(P);
+    ParkRay<R>* const park = reinterpret_cast<ParkRay<R>*>(P.park);
+    const long long parkCap = static_cast<long long>(P.parkBytes / sizeof(ParkRay<R>));
+    const long long total = PHASE ? min(static_cast<long long>(P.ctr[4]), parkCap) : rayTotal(P);
     const R eps = R(P.tc.eps);
     const int maxSteps = P.tc.maxSteps;
     Counters cnt;
@@ -258,10 +274,28 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P)
     V3<R> o = mk(R(0), R(0), R(0)), dir = o;
     R t = 0, lastD = 0, d = 0, tMax = 0;
     int step = 0, state = 0, pol = 0, owner = -1;
+    bool fresh = false;  // resumed march: its pending t += d was applied before parking
     while (true) {
         __syncwarp();
         unsigned long long item;
-        if (fetchItem(P.ctr + 0, static_cast<unsigned long long>(total), active, exhausted, item)) {
+        if (PHASE == 1) {
+            if (fetchItem(P.ctr + 5, static_cast<unsigned long long>(total), active, exhausted, item)) {
+                const ParkRay<R>& r = park[item];
+                o = mk(r.o[0], r.o[1], r.o[2]);
+                dir = mk(r.dir[0], r.dir[1], r.dir[2]);
+                t = r.t;
+                lastD = r.lastD;
+                d = r.d;
+                tMax = r.tMax;
+                step = r.step;
+                state = r.state;
+                pol = r.pol;
+                owner = r.owner;
+                rid = r.rid;
+                active = true;
+                fresh = true;
+            }
+        } else if (fetchItem(P.ctr + 0, static_cast<unsigned long long>(total), active, exhausted, item)) {
             R startBound = R(INFINITY);
             bool ok = true;
             if (MODE == 0) {
@@ -317,16 +351,53 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P)
         }
         V3<R> p = o;
         R initD = R(0);
+        bool parkIt = false;
         if (active) {
-            if (state == 2) t += d;
+            if (state == 2 && !fresh) t += d;
+            fresh = false;
             p = o + dir * t;
-            if (state == 0) {
+            parkIt = PHASE == 0 && park && gridCell<R>(P.scene.grid, p) < 0;
+            if (parkIt) {
+            } else if (state == 0) {
                 if (ST) ++cnt.steps;
                 initD = R(2) * lastD;
             } else if (state == 1) {
                 initD = polishPad(d);
             } else {
                 initD = polishPad(R(2) * fabs(d));
+            }
+        }
+        if (PHASE == 0) {
+            const long long ps = parkSlot(P.ctr + 4, parkIt);
+            if (ps >= parkCap) {  // buffer full: this march queries here after all
+                parkIt = false;
+                if (state == 0) {
+                    if (ST) ++cnt.steps;
+                    initD = R(2) * lastD;
+                } else if (state == 1) {
+                    initD = polishPad(d);
+                } else {
+                    initD = polishPad(R(2) * fabs(d));
+                }
+            }
+            if (parkIt) {
+                ParkRay<R>& r = park[ps];
+                r.o[0] = o.x;
+                r.o[1] = o.y;
+                r.o[2] = o.z;
+                r.dir[0] = dir.x;
+                r.dir[1] = dir.y;
+                r.dir[2] = dir.z;
+                r.t = t;
+                r.lastD = lastD;
+                r.d = d;
+                r.tMax = tMax;
+                r.step = step;
+                r.state = state;
+                r.pol = pol;
+                r.owner = owner;
+                r.rid = rid;
+                active = false;
             }
         }
         int o2 = -1;
@@ -403,11 +474,14 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P)
 // One (converged hit, light) item per lane: directIrradiance's setup
 // (probe_update.hpp:100-128) and the softShadowTrace march (scene.hpp:459-476),
 // one query per iteration. vis = 1 when the segment is too short to trace.
-template <typename R, bool ST>
+// PHASE 0 / 1 as in K1: off-grid shadow marches are parked and resumed together.
+template <typename R, bool ST, int PHASE>
 __global__ void __launch_bounds__(kWaveThreads) k_trace_shadow(WaveParams<R> P) {
     const int L = P.scene.n_lights;
     const unsigned long long nHits = P.ctr[1];
-    const unsigned long long total = nHits * static_cast<unsigned long long>(L);
+    ParkShadow<R>* const park = reinterpret_cast<ParkShadow<R>*>(P.park);
+    const unsigned long long parkCap = P.parkBytes / sizeof(ParkShadow<R>);
+    const unsigned long long total = PHASE ? min(P.ctr[6], parkCap) : nHits * static_cast<unsigned long long>(L);
     const R minStep = R(5e-4), inf = R(INFINITY), k = R(P.tc.shadowK);
     const int maxSteps = P.tc.shadowSteps;
     Counters cnt;
@@ -420,7 +494,20 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_shadow(WaveParams<R> P) 
     while (true) {
         __syncwarp();
         unsigned long long item;
-        if (fetchItem(P.ctr + 2, total, active, exhausted, item)) {
+        if (PHASE == 1) {
+            if (fetchItem(P.ctr + 7, total, active, exhausted, item)) {
+                const ParkShadow<R>& r = park[item];
+                o = mk(r.o[0], r.o[1], r.o[2]);
+                dir = mk(r.dir[0], r.dir[1], r.dir[2]);
+                t = r.t;
+                tEnd = r.tEnd;
+                v = r.v;
+                lastD = r.lastD;
+                step = r.step;
+                slot = r.slot;
+                active = true;
+            }
+        } else if (fetchItem(P.ctr + 2, total, active, exhausted, item)) {
             // light-major: consecutive lanes take consecutive hits toward the same light
             const int rid = P.hitList[item % nHits];
             const int li = static_cast<int>(item / nHits);
@@ -472,12 +559,32 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_shadow(WaveParams<R> P) 
             if (__all_sync(kFull, exhausted)) break;
             continue;
         }
-        const bool want = active && step < maxSteps && t < tEnd;
+        bool want = active && step < maxSteps && t < tEnd;
         V3<R> p = o;
-        if (want) {
-            if (ST) ++cnt.steps;
-            p = o + dir * t;
+        if (want) p = o + dir * t;
+        if (PHASE == 0) {
+            bool parkIt = want && park && gridCell<R>(P.scene.grid, p) < 0;
+            const long long ps = parkSlot(P.ctr + 6, parkIt);
+            if (ps >= static_cast<long long>(parkCap)) parkIt = false;  // buffer full
+            if (parkIt) {
+                ParkShadow<R>& r = park[ps];
+                r.o[0] = o.x;
+                r.o[1] = o.y;
+                r.o[2] = o.z;
+                r.dir[0] = dir.x;
+                r.dir[1] = dir.y;
+                r.dir[2] = dir.z;
+                r.t = t;
+                r.tEnd = tEnd;
+                r.v = v;
+                r.lastD = lastD;
+                r.step = step;
+                r.slot = slot;
+                active = false;
+                want = false;
+            }
         }
+        if (ST && want) ++cnt.steps;
         R d = R(0);
         if (want) d = query<R, ST>(P.scene, p, lastD == inf ? inf : R(2) * lastD, nullptr, &cnt);
         if (active) {
@@ -709,13 +816,17 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
     if (p.nCand <= 0) return;
     k_ray_setup<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
     k_ray_scan<R><<<1, kScanThreads, 0, st>>>(p);
-    cudaMemsetAsync(p.ctr, 0, 4 * sizeof(unsigned long long), st);
+    cudaMemsetAsync(p.ctr, 0, 8 * sizeof(unsigned long long), st);
     if (e0) cudaEventRecord(e0, st);
-    static int b1 = persistentBlocks(k_trace_primary<R, ST, 0>, kWaveThreads, 0);
-    static int b2 = persistentBlocks(k_trace_shadow<R, ST>, kWaveThreads, 0);
+    static int b1 = persistentBlocks(k_trace_primary<R, ST, 0, 0>, kWaveThreads, 0);
+    static int b1f = persistentBlocks(k_trace_primary<R, ST, 0, 1>, kWaveThreads, 0);
+    static int b2 = persistentBlocks(k_trace_shadow<R, ST, 0>, kWaveThreads, 0);
+    static int b2f = persistentBlocks(k_trace_shadow<R, ST, 1>, kWaveThreads, 0);
     static int b3 = persistentBlocks(k_shade_rays<R, ST>, 128, 0);
-    k_trace_primary<R, ST, 0><<<cap > 0 ? min(cap, b1) : b1, kWaveThreads, 0, st>>>(p);
-    k_trace_shadow<R, ST><<<cap > 0 ? min(cap, b2) : b2, kWaveThreads, 0, st>>>(p);
+    k_trace_primary<R, ST, 0, 0><<<cap > 0 ? min(cap, b1) : b1, kWaveThreads, 0, st>>>(p);
+    k_trace_primary<R, ST, 0, 1><<<cap > 0 ? min(cap, b1f) : b1f, kWaveThreads, 0, st>>>(p);
+    k_trace_shadow<R, ST, 0><<<cap > 0 ? min(cap, b2) : b2, kWaveThreads, 0, st>>>(p);
+    k_trace_shadow<R, ST, 1><<<cap > 0 ? min(cap, b2f) : b2f, kWaveThreads, 0, st>>>(p);
     k_shade_rays<R, ST><<<b3, 128, 0, st>>>(p);
     if (!p.debug) {
         const size_t smem = static_cast<size_t>(2 * p.nRaysFull) * 6 * sizeof(R);
@@ -724,7 +835,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
         k3<<<p.nCand, kConvThreads, smem, st>>>(p);
     }
     if (e1) cudaEventRecord(e1, st);
-    if (launches) *launches += p.debug ? 5 : 6;
+    if (launches) *launches += p.debug ? 7 : 8;
 }
 
 // contactGI's per-pixel sum (shading.hpp:686-713): AO from the missed samples,
@@ -773,16 +884,20 @@ __global__ void __launch_bounds__(128) k_contact_combine(WaveParams<R> P) {
 // then the per-pixel combine. Replaces the per-pixel k_contact loop.
 template <typename R, bool ST>
 static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long* launches) {
-    cudaMemsetAsync(p.ctr, 0, 4 * sizeof(unsigned long long), st);
-    static int b1 = persistentBlocks(k_trace_primary<R, ST, 1>, kWaveThreads, 0);
-    static int b2 = persistentBlocks(k_trace_shadow<R, ST>, kWaveThreads, 0);
+    cudaMemsetAsync(p.ctr, 0, 8 * sizeof(unsigned long long), st);
+    static int b1 = persistentBlocks(k_trace_primary<R, ST, 1, 0>, kWaveThreads, 0);
+    static int b1f = persistentBlocks(k_trace_primary<R, ST, 1, 1>, kWaveThreads, 0);
+    static int b2 = persistentBlocks(k_trace_shadow<R, ST, 0>, kWaveThreads, 0);
+    static int b2f = persistentBlocks(k_trace_shadow<R, ST, 1>, kWaveThreads, 0);
     static int b3 = persistentBlocks(k_shade_rays<R, ST>, 128, 0);
-    k_trace_primary<R, ST, 1><<<b1, kWaveThreads, 0, st>>>(p);
-    k_trace_shadow<R, ST><<<b2, kWaveThreads, 0, st>>>(p);
+    k_trace_primary<R, ST, 1, 0><<<b1, kWaveThreads, 0, st>>>(p);
+    k_trace_primary<R, ST, 1, 1><<<b1f, kWaveThreads, 0, st>>>(p);
+    k_trace_shadow<R, ST, 0><<<b2, kWaveThreads, 0, st>>>(p);
+    k_trace_shadow<R, ST, 1><<<b2f, kWaveThreads, 0, st>>>(p);
     k_shade_rays<R, ST><<<b3, 128, 0, st>>>(p);
     const long long np = static_cast<long long>(p.gw) * p.gh;
     k_contact_combine<R><<<static_cast<int>((np + 127) / 128), 128, 0, st>>>(p);
-    if (launches) *launches += 4;
+    if (launches) *launches += 6;
 }
 
 template <typename R>

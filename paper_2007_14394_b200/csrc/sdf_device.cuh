@@ -369,6 +369,23 @@ __device__ __forceinline__ void hierarchyWalk(const SceneView<R>& s, QueryState<
     }
 }
 
+// The candidate-grid cell holding p, or -1 off the grid.
+template <typename R>
+__device__ __forceinline__ int gridCell(const GridDev& g, V3<R> p) {
+    const bool f32 = sizeof(R) == 4;
+    const R lx = f32 ? R(g.flo[0]) : R(g.lo[0]), ly = f32 ? R(g.flo[1]) : R(g.lo[1]);
+    const R lz = f32 ? R(g.flo[2]) : R(g.lo[2]), ih = f32 ? R(g.finvH) : R(g.invH);
+    R fx = (p.x - lx) * ih;
+    R fy = (p.y - ly) * ih;
+    R fz = (p.z - lz) * ih;
+    if (!(fx >= R(0) && fy >= R(0) && fz >= R(0) && fx < R(g.dim[0]) && fy < R(g.dim[1]) && fz < R(g.dim[2])))
+        return -1;
+    int ix = min(static_cast<int>(fx), g.dim[0] - 1);
+    int iy = min(static_cast<int>(fy), g.dim[1] - 1);
+    int iz = min(static_cast<int>(fz), g.dim[2] - 1);
+    return ix + g.dim[0] * (iy + g.dim[1] * iz);
+}
+
 template <typename R, bool ST>
 __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R initD, QueryState<R>& q, Counters* c) {
     q.p = p;
@@ -389,17 +406,8 @@ __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R ini
         return;
     }
     const GridDev& g = s.grid;
-    const bool f32 = sizeof(R) == 4;
-    const R lx = f32 ? R(g.flo[0]) : R(g.lo[0]), ly = f32 ? R(g.flo[1]) : R(g.lo[1]);
-    const R lz = f32 ? R(g.flo[2]) : R(g.lo[2]), ih = f32 ? R(g.finvH) : R(g.invH);
-    R fx = (p.x - lx) * ih;
-    R fy = (p.y - ly) * ih;
-    R fz = (p.z - lz) * ih;
-    if (fx >= R(0) && fy >= R(0) && fz >= R(0) && fx < R(g.dim[0]) && fy < R(g.dim[1]) && fz < R(g.dim[2])) {
-        int ix = min(static_cast<int>(fx), g.dim[0] - 1);
-        int iy = min(static_cast<int>(fy), g.dim[1] - 1);
-        int iz = min(static_cast<int>(fz), g.dim[2] - 1);
-        int cell = ix + g.dim[0] * (iy + g.dim[1] * iz);
+    const int cell = gridCell<R>(g, p);
+    if (cell >= 0) {
         q.cur = g.start[cell];
         q.end = g.start[cell + 1];
         if (ST) c->pe += q.end - q.cur;

@@ -169,7 +169,7 @@ struct Ctx {
     DBuf<double> wRot, fib;
     DBuf<int> perm;
     int fibN = -1;
-    DBuf<unsigned char> wHits, wVis, wRad;
+    DBuf<unsigned char> wHits, wVis, wRad, wPark;
     DBuf<unsigned long long> wCtr;
     int persistCap = 0;  // 0 = occupancy-sized persistent grids
     // gather (e): G-buffer, stage buffers, history (pipeline.hpp:213-218)
@@ -194,7 +194,7 @@ struct Ctx {
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
         records.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
         wRayCount.free(); wHitList.free(); wRayStart.free(); wRot.free(); fib.free(); wHits.free();
-        wVis.free(); wCtr.free(); perm.free(); wRad.free();
+        wVis.free(); wPark.free(); wCtr.free(); perm.free(); wRad.free();
         gbuf.free(); halfDepth.free(); sparseIrr.free(); resolved.free(); indirect.free(); histIrr.free();
         histDepth.free(); halfSrc.free(); sel.free(); sparseValid.free(); sparseAnchor.free();
         for (auto& e : gev)
@@ -689,6 +689,17 @@ void reserve(DBuf<T>& b, size_t count) {
     if (b.n < count) b.alloc(count);
 }
 
+// Parking buffer for off-grid marches (K1 / K2 far phases): room for every ray and
+// every (ray, light) march, capped by SDFGI_PARK_MB (default 8192); marches that
+// find it full are traced in place.
+template <typename R>
+void reservePark(Ctx* c, size_t rays, int lights) {
+    const size_t need = std::max(rays * sizeof(ParkRay<R>), rays * lights * sizeof(ParkShadow<R>));
+    const char* env = std::getenv("SDFGI_PARK_MB");
+    const size_t cap = static_cast<size_t>(env ? std::max(0.0, std::atof(env)) : 8192.0) << 20;
+    reserve(c->wPark, std::max<size_t>(std::min(need, cap), 64));
+}
+
 template <typename R>
 WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand) {
     const int N = static_cast<int>(cfg->n_rays_full);
@@ -701,7 +712,8 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     reserve(c->wHitList, std::max<size_t>(maxRays, 1));
     reserve(c->wVis, std::max<size_t>(maxRays, 1) * L * sizeof(R));
     reserve(c->wRad, std::max<size_t>(maxRays, 1) * 3 * sizeof(R));
-    reserve(c->wCtr, 4);
+    reserve(c->wCtr, 8);
+    reservePark<R>(c, maxRays, L);
     if (c->fibN != N) {
         reserve(c->fib, 9 * static_cast<size_t>(N));
         launch_fib_table(c->fib.p, N, c->stream);
@@ -731,6 +743,8 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.vis = reinterpret_cast<R*>(c->wVis.p);
     p.rad = reinterpret_cast<R*>(c->wRad.p);
     p.ctr = c->wCtr.p;
+    p.park = c->accel && c->haveGrid && c->wPark.n >= 4096 ? c->wPark.p : nullptr;  // SDFGI_PARK_MB=0: off
+    p.parkBytes = p.park ? c->wPark.n : 0;
     p.prevAtlas = c->atlas[c->front].p;
     p.currAtlas = c->atlas[1 - c->front].p;
     p.oct = c->octRes;
@@ -1443,7 +1457,8 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     reserve(c->wHitList, cap);
     reserve(c->wVis, cap * L * sizeof(R));
     reserve(c->wRad, cap * 3 * sizeof(R));
-    reserve(c->wCtr, 4);
+    reserve(c->wCtr, 8);
+    reservePark<R>(c, cap, L);
     WaveParams<R> p;
     std::memset(&p, 0, sizeof(p));
     p.scene = c->sceneView<R>();
@@ -1463,6 +1478,8 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     p.vis = reinterpret_cast<R*>(c->wVis.p);
     p.rad = reinterpret_cast<R*>(c->wRad.p);
     p.ctr = c->wCtr.p;
+    p.park = c->accel && c->haveGrid && c->wPark.n >= 4096 ? c->wPark.p : nullptr;  // SDFGI_PARK_MB=0: off
+    p.parkBytes = p.park ? c->wPark.n : 0;
     p.stats = c->scratch.p;
     p.nRaysDirect = nr;
     p.gb = c->gbuf.p;
