@@ -713,6 +713,106 @@ __device__ inline bool mvcWeightsHex(const V3<double>* corners, V3<double> xd, d
     return true;
 }
 
+// The FP32 perf mode's mvcWeightsHex: the same weights (mean_value.hpp:16-107) with
+// the sines taken algebraically from the half angles a_i = asin(l_i / 2) —
+// sin(theta_i) = 2 sin a_i cos a_i, sin(h) and sin(h - theta_i) by angle addition
+// over a_0 + a_1 + a_2 — and reciprocals instead of divisions: 3 asinf per
+// triangle instead of 3 asinf + 7 sinf. Same degenerate-case branches.
+__device__ inline bool mvcWeightsHexFast(const V3<double>* corners, V3<double> xd, double* weights) {
+    const int faces[6][4] = {{0, 2, 3, 1}, {4, 5, 7, 6}, {0, 1, 5, 4}, {2, 6, 7, 3}, {0, 4, 6, 2}, {1, 3, 7, 5}};
+    const float eps = 1e-10f;
+    const float pi = float(kPi);
+    float wts[8];
+    for (int i = 0; i < 8; ++i) wts[i] = 0.f;
+    for (int i = 0; i < 8; ++i) weights[i] = 0.0;
+    float dist[8];
+    V3<float> unit[8];
+    const V3<float> x = mk(float(xd.x), float(xd.y), float(xd.z));
+    for (int i = 0; i < 8; ++i) {
+        V3<float> v = mk(float(corners[i].x), float(corners[i].y), float(corners[i].z)) - x;
+        dist[i] = length(v);
+        if (dist[i] < eps) {
+            weights[i] = 1.0;
+            return true;
+        }
+        const float inv = 1.f / dist[i];
+        unit[i] = mk(v.x * inv, v.y * inv, v.z * inv);
+    }
+    bool any = false;
+#pragma unroll 1
+    for (int f = 0; f < 6; ++f) {
+#pragma unroll 1
+        for (int tr = 0; tr < 2; ++tr) {
+            const int t0 = faces[f][0], t1 = faces[f][tr ? 2 : 1], t2 = faces[f][tr ? 3 : 2];
+            const int tri[3] = {t0, t1, t2};
+            float d[3], sa[3], ca[3], theta[3], st[3];
+            V3<float> u[3];
+            for (int i = 0; i < 3; ++i) {
+                d[i] = dist[tri[i]];
+                u[i] = unit[tri[i]];
+            }
+            for (int i = 0; i < 3; ++i) {
+                const float l = length(u[(i + 1) % 3] - u[(i + 2) % 3]);
+                sa[i] = sclamp(l * 0.5f, 0.f, 1.f);
+                ca[i] = sqrtf(fmaxf(0.f, 1.f - sa[i] * sa[i]));
+                theta[i] = 2.f * asinf(sa[i]);
+                st[i] = 2.f * sa[i] * ca[i];
+            }
+            const float h = (theta[0] + theta[1] + theta[2]) * 0.5f;
+            if (pi - h < 1e-8f) {
+                float total = 0;
+                float w[3];
+                for (int i = 0; i < 3; ++i) {
+                    w[i] = st[i] * d[(i + 1) % 3] * d[(i + 2) % 3];
+                    total += w[i];
+                }
+                if (total < eps) return false;
+                for (int i = 0; i < 8; ++i) weights[i] = 0.0;
+                for (int i = 0; i < 3; ++i) weights[tri[i]] = double(w[i] / total);
+                return true;
+            }
+            V3<float> cr = mk(u[1].y * u[2].z - u[1].z * u[2].y, u[1].z * u[2].x - u[1].x * u[2].z,
+                              u[1].x * u[2].y - u[1].y * u[2].x);
+            const float sign = dot(u[0], cr) >= 0.f ? 1.f : -1.f;
+            // sin h, h = a0 + a1 + a2
+            const float sh = sa[0] * ca[1] * ca[2] + ca[0] * sa[1] * ca[2] + ca[0] * ca[1] * sa[2] - sa[0] * sa[1] * sa[2];
+            float c[3], sv[3];
+            bool skip = false;
+            for (int i = 0; i < 3; ++i) {
+                const int j = (i + 1) % 3, k = (i + 2) % 3;
+                const float denom = st[j] * st[k];
+                if (fabsf(denom) < eps) {
+                    skip = true;
+                    break;
+                }
+                // sin(h - theta_i) = sin(a_j + a_k - a_i)
+                const float sjk = sa[j] * ca[k] + ca[j] * sa[k], cjk = ca[j] * ca[k] - sa[j] * sa[k];
+                const float shi = sjk * ca[i] - cjk * sa[i];
+                c[i] = 2.f * sh * shi * (1.f / denom) - 1.f;
+                sv[i] = sign * sqrtf(fmaxf(0.f, 1.f - c[i] * c[i]));
+                if (fabsf(sv[i]) <= eps) {
+                    skip = true;
+                    break;
+                }
+            }
+            if (skip) continue;
+            for (int i = 0; i < 3; ++i) {
+                const int j = (i + 1) % 3, k = (i + 2) % 3;
+                const float w = (theta[i] - c[j] * theta[k] - c[k] * theta[j]) * (1.f / (d[i] * st[j] * sv[k]));
+                wts[tri[i]] += w;
+                any = true;
+            }
+        }
+    }
+    if (!any) return false;
+    float total = 0;
+    for (int i = 0; i < 8; ++i) total += wts[i];
+    if (fabsf(total) < eps || !isfinite(total)) return false;
+    const float inv = 1.f / total;
+    for (int i = 0; i < 8; ++i) weights[i] = double(wts[i] * inv);
+    return true;
+}
+
 struct Stencil {
     int cascade;      // chosen cascade slot (-1: sky fallback)
     int probe[8];     // probe index within the cascade
@@ -777,7 +877,10 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
     bool wantMvc = maxDisp > mvcFrac * c.spacing || boundary;
     bool haveMvc = false;
     if (wantMvc) {
-        haveMvc = mvcWeightsHex<M>(corners, point, w);
+        if constexpr (sizeof(M) == 4)
+            haveMvc = mvcWeightsHexFast(corners, point, w);
+        else
+            haveMvc = mvcWeightsHex<M>(corners, point, w);
         if (haveMvc) {
             for (int k = 0; k < 8; ++k) w[k] = smax(0.0, w[k]);
             st.usedMvc = 1;
@@ -825,8 +928,16 @@ __device__ inline bool sampleBounceIrradiance(const CascadeDev* cas, int nCas, c
         if (st.w[i] <= 0) continue;
         const double* P = pv.pos + 3 * static_cast<size_t>(c.base + st.probe[i]);
         V3<double> toProbe = mk(P[0], P[1], P[2]) - pos;
-        double len = length(toProbe);
-        double facing = len > 1e-9 ? dot(toProbe / len, normal) : 1.0;
+        double facing;
+        if constexpr (sizeof(M) == 4) {  // FP32 perf mode: one float reciprocal
+            const V3<float> tp = mk(float(toProbe.x), float(toProbe.y), float(toProbe.z));
+            const float len = length(tp);
+            facing = len > 1e-9f ? double(dot(tp, mk(float(normal.x), float(normal.y), float(normal.z))) * (1.f / len))
+                                 : 1.0;
+        } else {
+            double len = length(toProbe);
+            facing = len > 1e-9 ? dot(toProbe / len, normal) : 1.0;
+        }
         double backface = (facing + 1.0) * 0.5;
         w[i] = st.w[i] * backface * backface;
         wsum += w[i];
