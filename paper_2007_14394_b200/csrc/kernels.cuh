@@ -68,12 +68,13 @@ template <typename R> struct __align__(16) ParkRay {
     R t, lastD, d, tMax;
     int step, state, pol, owner;
     unsigned long long rid;
+    int seed, pad;  // last known nearest primitive (query seed of the far phase)
 };
 // The same for a shadow march of K2.
 template <typename R> struct __align__(16) ParkShadow {
     R o[3], dir[3];
     R t, tEnd, v, lastD;
-    int step, pad;
+    int step, seed;  // seed: last known nearest primitive
     unsigned long long slot;
 };
 

@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P)
     unsigned long long rid = 0;
     V3<R> o = mk(R(0), R(0), R(0)), dir = o;
     R t = 0, lastD = 0, d = 0, tMax = 0;
-    int step = 0, state = 0, pol = 0, owner = -1;
+    int step = 0, state = 0, pol = 0, owner = -1, seed = -1;
     bool fresh = false;  // resumed march: its pending t += d was applied before parking
     while (true) {
         __syncwarp();
@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P)
                 state = r.state;
                 pol = r.pol;
                 owner = r.owner;
+                seed = r.seed;
                 rid = r.rid;
                 active = true;
                 fresh = true;
@@ -321,6 +322,7 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P)
             step = 0;
             state = 0;
             owner = -1;
+            seed = -1;
             active = ok;
             if (!ok) {  // sky pixel of a contact batch: no ray (the combine skips it)
                 HitRec<R> h;
@@ -397,13 +399,15 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P)
                 r.pol = pol;
                 r.owner = owner;
                 r.rid = rid;
+                r.seed = seed;
                 active = false;
             }
         }
         int o2 = -1;
         R nd = R(0);
-        if (active) nd = query<R, ST>(P.scene, p, initD, &o2, &cnt);
+        if (active) nd = query<R, ST>(P.scene, p, initD, &o2, &cnt, PHASE ? seed : -1);
         if (active) {
+            if (o2 >= 0) seed = o2;
             int done = 0;  // 1 converged, 2 TMax, 3 StepLimit
             if (state == 0) {
                 if (nd < eps) {
@@ -490,7 +494,7 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_shadow(WaveParams<R> P) 
     unsigned long long slot = 0;
     V3<R> o = mk(R(0), R(0), R(0)), dir = o;
     R t = 0, tEnd = 0, v = 0, lastD = 0;
-    int step = 0;
+    int step = 0, seed = -1;
     while (true) {
         __syncwarp();
         unsigned long long item;
@@ -504,6 +508,7 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_shadow(WaveParams<R> P) 
                 v = r.v;
                 lastD = r.lastD;
                 step = r.step;
+                seed = r.seed;
                 slot = r.slot;
                 active = true;
             }
@@ -549,6 +554,7 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_shadow(WaveParams<R> P) 
                     v = R(1);
                     lastD = inf;
                     step = 0;
+                    seed = -1;
                     active = true;
                 } else {
                     P.vis[slot] = R(1);
@@ -579,6 +585,7 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_shadow(WaveParams<R> P) 
                 r.v = v;
                 r.lastD = lastD;
                 r.step = step;
+                r.seed = seed;
                 r.slot = slot;
                 active = false;
                 want = false;
@@ -586,7 +593,9 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_shadow(WaveParams<R> P) 
         }
         if (ST && want) ++cnt.steps;
         R d = R(0);
-        if (want) d = query<R, ST>(P.scene, p, lastD == inf ? inf : R(2) * lastD, nullptr, &cnt);
+        int o2 = -1;
+        if (want) d = query<R, ST>(P.scene, p, lastD == inf ? inf : R(2) * lastD, &o2, &cnt, PHASE ? seed : -1);
+        if (o2 >= 0) seed = o2;
         if (active) {
             bool done = false;
             if (!want) {

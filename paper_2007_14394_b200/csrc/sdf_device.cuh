@@ -443,9 +443,23 @@ __device__ __forceinline__ void queryStep(const SceneView<R>& s, QueryState<R>& 
 }
 
 template <typename R, bool ST>
-__device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int* owner, Counters* c) {
+__device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int* owner, Counters* c, int seed = -1) {
     QueryState<R> q;
     queryBegin<R, ST>(s, p, initD, q, c);
+    // seed (candidate-grid walks only, which break ties by CSR position in any
+    // visiting order): evaluate a likely owner first — e.g. the previous step's
+    // — so the hierarchy prunes against a tight minimum from its first node
+    if (seed >= 0 && s.useGrid) {
+        if (ST) {
+            ++c->ek[s.kindId[seed] & 0xff];
+            c->ek[5] += (s.kindId[seed] >> 8) ? 0 : 1;
+        }
+        const R pd = evalPrim(s.prims[seed], p);
+        if (pd < q.d || (pd == q.d && q.own >= 0 && seed < q.own)) {
+            q.d = pd;
+            q.own = seed;
+        }
+    }
     while (q.cur < q.end) queryStep<R, ST>(s, q, c);
     if (q.walk) hierarchyWalk<R, ST>(s, q, c);
     if (owner) *owner = q.own;

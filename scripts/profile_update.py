@@ -16,7 +16,9 @@ with Device(0, precision=prec) as dev:
     stage.relocate_all()
     n = 32 * 16 * 32
     refs = np.array([[0, i] for i in range(0, n, stride)], np.int32)
-    res = dev.update(0, stage.cfg, refs)
-    upd, _ = dev.last_kernel_ms()
+    reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+    for _ in range(reps):  # reps > 1: earlier calls warm up (lazy module loading), the last is reported
+        res = dev.update(0, stage.cfg, refs)
+        upd, _ = dev.last_kernel_ms()
     print(f"{prec} stride {stride}: {int(res['rays_traced'])} rays in {upd:.2f} ms "
           f"-> {int(res['rays_traced']) / upd / 1e6:.3f} Grays/s")
