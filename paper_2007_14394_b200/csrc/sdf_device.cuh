@@ -632,13 +632,17 @@ __device__ __forceinline__ V3<double> sampleBilinear(const AtlasView& a, int pro
     return lerp(A, B, ty);
 }
 
-// mvcWeightsHex, mean_value.hpp:16-107, evaluated in precision M (double in the
-// parity mode — identical arithmetic to the reference, the sine of each angle is
-// computed once and reused, which changes no value; float in the FP32 perf mode).
-__device__ __forceinline__ double msin(double v) { return sin(v); }
-__device__ __forceinline__ float msin(float v) { return sinf(v); }
-__device__ __forceinline__ double masin(double v) { return asin(v); }
-__device__ __forceinline__ float masin(float v) { return asinf(v); }
+// mvcWeightsHex, mean_value.hpp:16-107, in precision M (double in the parity
+// mode, float in the perf mode). The same weights with the sines taken
+// algebraically from the half angles a_i = asin(l_i / 2): sin(theta_i) =
+// 2 sin a_i cos a_i, and sin(h), sin(h - theta_i) by angle addition over
+// a_0 + a_1 + a_2 — 3 asin per triangle instead of 3 asin + 7 sin (the values
+// agree with the reference's to a few ulps of M). Same degenerate-case branches.
+template <typename M> __device__ __forceinline__ M mvcAsin(M v);
+template <> __device__ __forceinline__ double mvcAsin<double>(double v) { return asin(v); }
+template <> __device__ __forceinline__ float mvcAsin<float>(float v) { return asinf(v); }
+template <typename M> __device__ __forceinline__ M mvcDiv(M a, M b) { return a / b; }
+template <> __device__ __forceinline__ float mvcDiv<float>(float a, float b) { return __fdividef(a, b); }
 
 template <typename M>
 __device__ inline bool mvcWeightsHex(const V3<double>* corners, V3<double> xd, double* weights) {
@@ -658,25 +662,30 @@ __device__ inline bool mvcWeightsHex(const V3<double>* corners, V3<double> xd, d
             weights[i] = 1.0;
             return true;
         }
-        unit[i] = v / dist[i];
+        const M inv = mvcDiv(M(1), dist[i]);
+        unit[i] = mk(v.x * inv, v.y * inv, v.z * inv);
     }
     bool any = false;
+#pragma unroll 1
     for (int f = 0; f < 6; ++f) {
-        const int tris[2][3] = {{faces[f][0], faces[f][1], faces[f][2]}, {faces[f][0], faces[f][2], faces[f][3]}};
+#pragma unroll 1
         for (int tr = 0; tr < 2; ++tr) {
-            const int* tri = tris[tr];
-            M d[3], theta[3], st[3];
+            const int t0 = faces[f][0], t1 = faces[f][tr ? 2 : 1], t2 = faces[f][tr ? 3 : 2];
+            const int tri[3] = {t0, t1, t2};
+            M d[3], sa[3], ca[3], theta[3], st[3];
             V3<M> u[3];
             for (int i = 0; i < 3; ++i) {
                 d[i] = dist[tri[i]];
                 u[i] = unit[tri[i]];
             }
             for (int i = 0; i < 3; ++i) {
-                M l = length(u[(i + 1) % 3] - u[(i + 2) % 3]);
-                theta[i] = M(2.0) * masin(sclamp(l * M(0.5), M(0), M(1)));
-                st[i] = msin(theta[i]);
+                const M l = length(u[(i + 1) % 3] - u[(i + 2) % 3]);
+                sa[i] = sclamp(l * M(0.5), M(0), M(1));
+                ca[i] = sqrt(smax(M(0), M(1) - sa[i] * sa[i]));
+                theta[i] = M(2) * mvcAsin<M>(sa[i]);
+                st[i] = M(2) * sa[i] * ca[i];
             }
-            M h = (theta[0] + theta[1] + theta[2]) * M(0.5);
+            const M h = (theta[0] + theta[1] + theta[2]) * M(0.5);
             if (pi - h < M(1e-8)) {
                 M total = 0;
                 M w[3];
@@ -689,22 +698,25 @@ __device__ inline bool mvcWeightsHex(const V3<double>* corners, V3<double> xd, d
                 for (int i = 0; i < 3; ++i) weights[tri[i]] = double(w[i] / total);
                 return true;
             }
-            // cross(u1, u2), vec.hpp:51-53
             V3<M> cr = mk(u[1].y * u[2].z - u[1].z * u[2].y, u[1].z * u[2].x - u[1].x * u[2].z,
-                          u[1].x * u[2].y - u[1].y * u[2].x);
-            M det = dot(u[0], cr);
-            M sign = det >= M(0) ? M(1) : M(-1);
+                              u[1].x * u[2].y - u[1].y * u[2].x);
+            const M sign = dot(u[0], cr) >= M(0) ? M(1) : M(-1);
+            // sin h, h = a0 + a1 + a2
+            const M sh = sa[0] * ca[1] * ca[2] + ca[0] * sa[1] * ca[2] + ca[0] * ca[1] * sa[2] - sa[0] * sa[1] * sa[2];
             M c[3], sv[3];
             bool skip = false;
-            const M sh = msin(h);
             for (int i = 0; i < 3; ++i) {
-                M denom = st[(i + 1) % 3] * st[(i + 2) % 3];
+                const int j = (i + 1) % 3, k = (i + 2) % 3;
+                const M denom = st[j] * st[k];
                 if (fabs(denom) < eps) {
                     skip = true;
                     break;
                 }
-                c[i] = (M(2.0) * sh * msin(h - theta[i])) / denom - M(1.0);
-                sv[i] = sign * sqrt(smax(M(0), M(1.0) - c[i] * c[i]));
+                // sin(h - theta_i) = sin(a_j + a_k - a_i)
+                const M sjk = sa[j] * ca[k] + ca[j] * sa[k], cjk = ca[j] * ca[k] - sa[j] * sa[k];
+                const M shi = sjk * ca[i] - cjk * sa[i];
+                c[i] = mvcDiv(M(2) * sh * shi, denom) - M(1);
+                sv[i] = sign * sqrt(smax(M(0), M(1) - c[i] * c[i]));
                 if (fabs(sv[i]) <= eps) {
                     skip = true;
                     break;
@@ -712,8 +724,8 @@ __device__ inline bool mvcWeightsHex(const V3<double>* corners, V3<double> xd, d
             }
             if (skip) continue;
             for (int i = 0; i < 3; ++i) {
-                M w = (theta[i] - c[(i + 1) % 3] * theta[(i + 2) % 3] - c[(i + 2) % 3] * theta[(i + 1) % 3]) /
-                      (d[i] * st[(i + 1) % 3] * sv[(i + 2) % 3]);
+                const int j = (i + 1) % 3, k = (i + 2) % 3;
+                const M w = mvcDiv(theta[i] - c[j] * theta[k] - c[k] * theta[j], d[i] * st[j] * sv[k]);
                 wts[tri[i]] += w;
                 any = true;
             }
@@ -724,106 +736,6 @@ __device__ inline bool mvcWeightsHex(const V3<double>* corners, V3<double> xd, d
     for (int i = 0; i < 8; ++i) total += wts[i];
     if (fabs(total) < eps || !isfinite(total)) return false;
     for (int i = 0; i < 8; ++i) weights[i] = double(wts[i] / total);
-    return true;
-}
-
-// The FP32 perf mode's mvcWeightsHex: the same weights (mean_value.hpp:16-107) with
-// the sines taken algebraically from the half angles a_i = asin(l_i / 2) —
-// sin(theta_i) = 2 sin a_i cos a_i, sin(h) and sin(h - theta_i) by angle addition
-// over a_0 + a_1 + a_2 — and reciprocals instead of divisions: 3 asinf per
-// triangle instead of 3 asinf + 7 sinf. Same degenerate-case branches.
-__device__ inline bool mvcWeightsHexFast(const V3<double>* corners, V3<double> xd, double* weights) {
-    const int faces[6][4] = {{0, 2, 3, 1}, {4, 5, 7, 6}, {0, 1, 5, 4}, {2, 6, 7, 3}, {0, 4, 6, 2}, {1, 3, 7, 5}};
-    const float eps = 1e-10f;
-    const float pi = float(kPi);
-    float wts[8];
-    for (int i = 0; i < 8; ++i) wts[i] = 0.f;
-    for (int i = 0; i < 8; ++i) weights[i] = 0.0;
-    float dist[8];
-    V3<float> unit[8];
-    const V3<float> x = mk(float(xd.x), float(xd.y), float(xd.z));
-    for (int i = 0; i < 8; ++i) {
-        V3<float> v = mk(float(corners[i].x), float(corners[i].y), float(corners[i].z)) - x;
-        dist[i] = length(v);
-        if (dist[i] < eps) {
-            weights[i] = 1.0;
-            return true;
-        }
-        const float inv = 1.f / dist[i];
-        unit[i] = mk(v.x * inv, v.y * inv, v.z * inv);
-    }
-    bool any = false;
-#pragma unroll 1
-    for (int f = 0; f < 6; ++f) {
-#pragma unroll 1
-        for (int tr = 0; tr < 2; ++tr) {
-            const int t0 = faces[f][0], t1 = faces[f][tr ? 2 : 1], t2 = faces[f][tr ? 3 : 2];
-            const int tri[3] = {t0, t1, t2};
-            float d[3], sa[3], ca[3], theta[3], st[3];
-            V3<float> u[3];
-            for (int i = 0; i < 3; ++i) {
-                d[i] = dist[tri[i]];
-                u[i] = unit[tri[i]];
-            }
-            for (int i = 0; i < 3; ++i) {
-                const float l = length(u[(i + 1) % 3] - u[(i + 2) % 3]);
-                sa[i] = sclamp(l * 0.5f, 0.f, 1.f);
-                ca[i] = sqrtf(fmaxf(0.f, 1.f - sa[i] * sa[i]));
-                theta[i] = 2.f * asinf(sa[i]);
-                st[i] = 2.f * sa[i] * ca[i];
-            }
-            const float h = (theta[0] + theta[1] + theta[2]) * 0.5f;
-            if (pi - h < 1e-8f) {
-                float total = 0;
-                float w[3];
-                for (int i = 0; i < 3; ++i) {
-                    w[i] = st[i] * d[(i + 1) % 3] * d[(i + 2) % 3];
-                    total += w[i];
-                }
-                if (total < eps) return false;
-                for (int i = 0; i < 8; ++i) weights[i] = 0.0;
-                for (int i = 0; i < 3; ++i) weights[tri[i]] = double(w[i] / total);
-                return true;
-            }
-            V3<float> cr = mk(u[1].y * u[2].z - u[1].z * u[2].y, u[1].z * u[2].x - u[1].x * u[2].z,
-                              u[1].x * u[2].y - u[1].y * u[2].x);
-            const float sign = dot(u[0], cr) >= 0.f ? 1.f : -1.f;
-            // sin h, h = a0 + a1 + a2
-            const float sh = sa[0] * ca[1] * ca[2] + ca[0] * sa[1] * ca[2] + ca[0] * ca[1] * sa[2] - sa[0] * sa[1] * sa[2];
-            float c[3], sv[3];
-            bool skip = false;
-            for (int i = 0; i < 3; ++i) {
-                const int j = (i + 1) % 3, k = (i + 2) % 3;
-                const float denom = st[j] * st[k];
-                if (fabsf(denom) < eps) {
-                    skip = true;
-                    break;
-                }
-                // sin(h - theta_i) = sin(a_j + a_k - a_i)
-                const float sjk = sa[j] * ca[k] + ca[j] * sa[k], cjk = ca[j] * ca[k] - sa[j] * sa[k];
-                const float shi = sjk * ca[i] - cjk * sa[i];
-                c[i] = 2.f * sh * shi * (1.f / denom) - 1.f;
-                sv[i] = sign * sqrtf(fmaxf(0.f, 1.f - c[i] * c[i]));
-                if (fabsf(sv[i]) <= eps) {
-                    skip = true;
-                    break;
-                }
-            }
-            if (skip) continue;
-            for (int i = 0; i < 3; ++i) {
-                const int j = (i + 1) % 3, k = (i + 2) % 3;
-                const float w = (theta[i] - c[j] * theta[k] - c[k] * theta[j]) * (1.f / (d[i] * st[j] * sv[k]));
-                wts[tri[i]] += w;
-                any = true;
-            }
-        }
-    }
-    if (!any) return false;
-    float total = 0;
-    for (int i = 0; i < 8; ++i) total += wts[i];
-    if (fabsf(total) < eps || !isfinite(total)) return false;
-    const float inv = 1.f / total;
-    for (int i = 0; i < 8; ++i) weights[i] = double(wts[i] * inv);
     return true;
 }
 
@@ -891,10 +803,7 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
     bool wantMvc = maxDisp > mvcFrac * c.spacing || boundary;
     bool haveMvc = false;
     if (wantMvc) {
-        if constexpr (sizeof(M) == 4)
-            haveMvc = mvcWeightsHexFast(corners, point, w);
-        else
-            haveMvc = mvcWeightsHex<M>(corners, point, w);
+        haveMvc = mvcWeightsHex<M>(corners, point, w);
         if (haveMvc) {
             for (int k = 0; k < 8; ++k) w[k] = smax(0.0, w[k]);
             st.usedMvc = 1;
