@@ -219,6 +219,21 @@ void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st);
 void launch_grid_list(const GridBuildParams& p, int ncells, bool fill, cudaStream_t st);
 
 constexpr int kWaveThreads = 128;   // K1/K2 persistent CTAs
+// minimum resident K1/K2/K3a CTAs per SM (register cap = 64K / (128 * n)); the
+// tracing kernels are latency bound at low occupancy (measured, profiles/)
+#ifndef SDFGI_WAVE_MINB64
+#define SDFGI_WAVE_MINB64 8
+#endif
+#ifndef SDFGI_WAVE_MINB32
+#define SDFGI_WAVE_MINB32 10
+#endif
+#ifndef SDFGI_SHADE_MINB
+#define SDFGI_SHADE_MINB 4
+#endif
+template <typename R> struct WaveOcc {
+    static constexpr int trace = sizeof(R) == 8 ? SDFGI_WAVE_MINB64 : SDFGI_WAVE_MINB32;
+    static constexpr int shade = SDFGI_SHADE_MINB;
+};
 constexpr int kShadeThreads = 128;  // per-ray shading
 constexpr int kConvThreads = 192;   // K3b CTA per probe: one thread per (texel, channel) at R = 8
 constexpr int kScanThreads = 1024;  // K0 prefix sum

@@ -261,7 +261,7 @@ __device__ __forceinline__ long long parkSlot(unsigned long long* counter, bool 
 // PHASE 0 traces new rays and parks every march whose next point is off the
 // candidate grid; PHASE 1 resumes the parked marches (no further parking).
 template <typename R, bool ST, int MODE, int PHASE>
-__global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P) {
+__global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_primary(WaveParams<R> P) {
     ParkRay<R>* const park = reinterpret_cast<ParkRay<R>*>(P.park);
     const long long parkCap = static_cast<long long>(P.parkBytes / sizeof(ParkRay<R>));
     const long long total = PHASE ? min(static_cast<long long>(P.ctr[4]), parkCap) : rayTotal(P);
@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(kWaveThreads) k_trace_primary(WaveParams<R> P)
 // one query per iteration. vis = 1 when the segment is too short to trace.
 // PHASE 0 / 1 as in K1: off-grid shadow marches are parked and resumed together.
 template <typename R, bool ST, int PHASE>
-__global__ void __launch_bounds__(kWaveThreads) k_trace_shadow(WaveParams<R> P) {
+__global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_shadow(WaveParams<R> P) {
     const int L = P.scene.n_lights;
     const unsigned long long nHits = P.ctr[1];
     ParkShadow<R>* const park = reinterpret_cast<ParkShadow<R>*>(P.park);
@@ -674,7 +674,7 @@ __device__ __forceinline__ V3<double> shadeRay(const WaveParams<R>& P, const Hit
 // P.rad (3 per ray). Kept apart from the convolution so the stencil/MVC register
 // footprint does not cap the convolution's occupancy.
 template <typename R, bool ST>
-__global__ void __launch_bounds__(128) k_shade_rays(WaveParams<R> P) {
+__global__ void __launch_bounds__(128, WaveOcc<R>::shade) k_shade_rays(WaveParams<R> P) {
     const long long total = rayTotal(P);
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
     for (long long rid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; rid < total; rid += stride) {

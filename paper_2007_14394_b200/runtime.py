@@ -14,7 +14,8 @@ import numpy as np
 from . import scene_io as sio
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libsdfgi_b200.so")
+# SDFGI_LIB: load another build of the same library (kernel-variant experiments)
+LIB_PATH = os.environ.get("SDFGI_LIB") or os.path.join(_PKG, "libsdfgi_b200.so")
 
 F64, F32 = 0, 1
 _PREC = {"f64": F64, "f32": F32, F64: F64, F32: F32}

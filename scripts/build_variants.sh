@@ -1,0 +1,20 @@
+#!/bin/bash
+# Build libsdfgi_b200.so variants with different -D knobs into paper_2007_14394_b200/_variants/
+# usage: scripts/build_variants.sh NAME "-DFOO=1 -DBAR=2" [NAME2 "FLAGS2" ...]
+set -e
+cd "$(dirname "$0")/.."
+P=paper_2007_14394_b200
+OUT=$P/_variants
+mkdir -p $OUT
+COMMON="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr -I include"
+while [ $# -gt 1 ]; do
+  name=$1; flags=$2; shift 2
+  mkdir -p $OUT/$name
+  nvcc $COMMON $flags -fmad=false -c $P/csrc/kernels_f64.cu -o $OUT/$name/f64.o &
+  nvcc $COMMON $flags -fmad=true -c $P/csrc/kernels_f32.cu -o $OUT/$name/f32.o &
+  nvcc $COMMON $flags -c $P/csrc/sdfgi_abi.cu -o $OUT/$name/abi.o &
+  nvcc $COMMON $flags -c $P/csrc/fp_peak.cu -o $OUT/$name/fp.o &
+  wait
+  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/$name/libsdfgi_b200.so $OUT/$name/*.o -lnccl -lcudart
+  echo built $OUT/$name
+done
