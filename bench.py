@@ -48,6 +48,35 @@ METRIC = "probe-update Grays/s & ms/frame (32x16x32 probes, 256 rays)"
 UNIT = "Grays/s"
 
 
+STEP_KERNELS = ("k_relocate", "k_ray_setup", "k_ray_scan", "k_trace_primary", "k_trace_shadow", "k_shade_rays",
+                "k_convolve")
+
+
+def ncu_step_traffic(precision):
+    """DRAM bytes (read + write) of one C2 step's update kernels from the committed ncu
+    launch list of scripts/profile_step.py (profiles/r01_step_launches_<prec>_v*.csv,
+    the newest): kernels launched before the gather's first k_render_gbuffer."""
+    import csv
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r01_step_launches_{precision}_v*.csv")))
+    if not files:
+        return None, None
+    rows = [r for r in csv.reader(open(files[-1])) if len(r) > 10]
+    h = rows[0]
+    ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
+    total, seen_gather = 0.0, False
+    for r in sorted(rows[1:], key=lambda r: int(r[ii])):
+        name = r[ki]
+        if "k_render_gbuffer" in name:
+            seen_gather = True
+        if seen_gather or not any(k in name for k in STEP_KERNELS):
+            continue
+        if r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            total += float(r[vi].replace(",", ""))
+    return total, os.path.relpath(files[-1], ROOT)
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -247,6 +276,9 @@ def run_ours(args, rank, world, local_rank):
     peak_rate = f64_rate if args.precision == "f64" else f32_rate
     kern_ms = statistics.median(kern)
     achieved = ops_step / (kern_ms * 1e-3)  # ops/s over the step's update launches
+    traffic, traffic_src = ncu_step_traffic(args.precision)
+    # per probe per pass, read the previous tile interior (768 B) + write the tile (1,200 B)
+    hbm_alg = PASSES * 32 * 16 * 32 * (768 + 1200)
     roofline = {
         "bound": "fp64" if args.precision == "f64" else "fp32",
         "kernel": "k_probe_update",
@@ -254,7 +286,10 @@ def run_ours(args, rank, world, local_rank):
         "peak": peak_rate / 1e12,
         "unit": "Tinstr/s",
         "frac": achieved / peak_rate,
-        "traffic": None,
+        "traffic": traffic,
+        "traffic_unit": "DRAM bytes per step (ncu, serialised cold-cache launches)",
+        "traffic_source": traffic_src,
+        "algorithmic_hbm_bytes_per_step": hbm_alg,
         "peak_source": "measured live: sdfgi_measure_fp_peak FMA-instruction rate (MEASURED_PEAKS.json has no FP pipe entry)",
         "work_per_step_instr": ops_step,
         "update_kernel_ms_per_step": kern_ms,
