@@ -430,7 +430,8 @@ def gather_bench(args, dev, stage, scene, torch, ext, flush):
     tasks, vs, cs = dev.gather(0, cfg, stats=True)
     for f in range(1, args.warmup + 1):
         dev.gather(f, cfg)
-    times, stages = [], []
+    _, _, ps = dev.compose(cfg, stats=True)
+    times, stages, ctimes = [], [], []
     for k in range(args.steps):
         flush.fill_(1.0)
         torch.cuda.synchronize()
@@ -440,12 +441,20 @@ def gather_bench(args, dev, stage, scene, torch, ext, flush):
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
         stages.append(dev.last_gather_ms())
+        # composeFrame (f1, pipeline.hpp:209) on this frame's indirect image
+        e0.record(ext)
+        dev.compose(cfg)
+        e1.record(ext)
+        e1.synchronize()
+        ctimes.append(e0.elapsed_time(e1))
     st = np.median(np.array(stages), axis=0)
     res = {
         "config": "C3: 1920x1080, frame with history, C2 scene and volume after 3 bounces",
         "ms_per_frame": float(np.median(times)),
         "stage_ms": {"downsample_select": st[0], "tiles_visibility_shadePixelGI": st[1], "resolve": st[2],
                      "contact_gi": st[3]},
+        "compose_ms": float(np.median(ctimes)),
+        "compose_shadow_traces_per_pixel": int(ps["shadow_traces"]) / (w * h),
         "gbuffer_ms_input": gbuffer_ms,
         "visibility_tasks": int(tasks),
         "visibility_traces_per_pixel": int(vs["visibility_traces"]) / (w * h),
@@ -470,7 +479,9 @@ def cpu_gather_baseline():
     out = json.loads(r.stdout)
     f = out["frames"][1]
     ms = f["visibility_ms"] + f["resolve_ms"] + f["contact_ms"]
+    cms = f.get("compose_ms")
     return {"ms_per_frame_sample": ms, "ms_per_frame_1080p_scaled": ms * 16, "cores": threads,
+            "compose_ms_1080p_scaled": None if cms is None else cms * 16,
             "kind": "reference", "sample": "480x270 (1/16 of 1080p pixels), frame with history; scaled x16"}
 
 

@@ -304,11 +304,22 @@ SDFGI_API int sdfgi_gather(void* ctx, int frame, const sdfgi_cfg* cfg, int64_t* 
                            sdfgi_stats* contact_stats);
 SDFGI_API int sdfgi_gather_reset_history(void* ctx);
 /* which: 0 resolved E, 1 indirect (contactGI output), 2 half-res depth, 3 half-res
- * source pixel, 4 selection, 5 sparse irradiance, 6 sparse valid, 7 sparse anchor.
- * Doubles for 0,1,2,5 (3 per pixel/cell for 0,1,5), int32 otherwise. */
+ * source pixel, 4 selection, 5 sparse irradiance, 6 sparse valid, 7 sparse anchor,
+ * 8 composed image (sdfgi_compose). Doubles for 0,1,2,5,8 (3 per pixel/cell for
+ * 0,1,5,8), int32 otherwise. */
 SDFGI_API int sdfgi_gather_download(void* ctx, int which, void* dst, size_t bytes);
 /* Device ms of the last gather: {downsample+select, tiles, resolve, contact}. */
 SDFGI_API int sdfgi_last_gather_ms(void* ctx, double out[4]);
+/* Replace the indirect image (3 doubles per G-buffer pixel) — e.g. to compose an
+ * externally computed indirect term. */
+SDFGI_API int sdfgi_indirect_upload(void* ctx, const double* rgb, size_t n_doubles);
+/* composeFrame (shading.hpp:480-504; pipeline.hpp:209): per G-buffer pixel, sky
+ * radiance on sky pixels, else emission + albedo/pi * directIrradiance(worldPos,
+ * normal) + indirect, with the direct term's soft shadows traced on the device.
+ * Reads the context's G-buffer and indirect image (the last gather's, or the
+ * uploaded one); the result is gather buffer 8. stats (may be NULL) += TraceStats
+ * of the shadow traces; ms (may be NULL) = device time. */
+SDFGI_API int sdfgi_compose(void* ctx, const sdfgi_cfg* cfg, sdfgi_stats* stats, double* ms);
 
 /* Linear-time cluster builder for large scenes (replaces buildClusters,
  * scene.hpp:110-178, whose greedy agglomeration is O(N^3)): bounded primitives in

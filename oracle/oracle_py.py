@@ -39,6 +39,7 @@ def load():
         "ora_query": ([_P, _P, _P, _I, _P, _P], None),
         "ora_render_gbuffer": ([_P, _P, _I, _I, _P, _P, _P], _I),
         "ora_gather_frame": ([_P, _P, _I, _I, _I, _P, _P, _P, _I] + [_P] * 10, _I),
+        "ora_compose": ([_P, _P, _I, _I, _P, _P, _P, _P], _I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -168,6 +169,15 @@ class Stage:
                                         "sparse_anchor", "resolved", "indirect", "vis_stats", "contact_stats")])
         out["tasks"] = n
         return out
+
+    def compose(self, gb, w, h, indirect):
+        """composeFrame (shading.hpp:480-504): the final image, 3 doubles per pixel."""
+        gb = np.ascontiguousarray(gb, self.sio.GBUFFER_DTYPE)
+        ind = np.ascontiguousarray(indirect, np.float64)
+        out = np.zeros(w * h * 3)
+        stats = np.zeros(8, np.uint64)
+        load().ora_compose(self.h, _p(gb), w, h, _p(ind), _p(self.cfg), _p(out), _p(stats))
+        return out, stats
 
     def query(self, pts, init=None):
         pts = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)

@@ -646,6 +646,9 @@ int cmdGather(int argc, char** argv) {
         double radius = st.cfg.contactRadiusFrac * st.cascades[0].spacing;
         ImageRgb indirect = contactGI(st.scene, gb, resolved, field, radius, st.cfg.contactSamples, st.cfg, &cs, T);
         auto d = Clock::now();
+        TraceStats ps;
+        ImageRgb composed = composeFrame(st.scene, gb, indirect, st.cfg, &ps, T);  // pipeline.hpp:209
+        auto e = Clock::now();
         if (o.dump) {
             std::string sfx = "_f" + std::to_string(f);
             writeVec(dir + "/half_depth" + sfx + ".bin", half.depth);
@@ -664,13 +667,16 @@ int cmdGather(int argc, char** argv) {
             writeVec(dir + "/vis" + sfx + ".bin", vis);
             dumpImage(dir + "/resolved" + sfx + ".bin", resolved);
             dumpImage(dir + "/indirect" + sfx + ".bin", indirect);
+            dumpImage(dir + "/composed" + sfx + ".bin", composed);
         }
         if (f) js << ", ";
         js << "{\"frame\": " << f << ", \"tasks\": " << work.tasks.size()
            << ", \"visibility_ms\": " << std::chrono::duration<double, std::milli>(b - a).count()
            << ", \"resolve_ms\": " << std::chrono::duration<double, std::milli>(c - b).count()
            << ", \"contact_ms\": " << std::chrono::duration<double, std::milli>(d - c).count()
-           << ", \"vis_stats\": " << statsJson(vs) << ", \"contact_stats\": " << statsJson(cs) << "}";
+           << ", \"compose_ms\": " << std::chrono::duration<double, std::milli>(e - d).count()
+           << ", \"vis_stats\": " << statsJson(vs) << ", \"contact_stats\": " << statsJson(cs)
+           << ", \"compose_stats\": " << statsJson(ps) << "}";
         history.irradiance = std::move(resolved);  // pipeline.hpp:214-218
         history.depth.resize(gb.pixels.size());
         for (size_t i = 0; i < gb.pixels.size(); ++i) history.depth[i] = gb.pixels[i].depth;

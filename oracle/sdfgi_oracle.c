@@ -1255,3 +1255,32 @@ int ora_gather_frame(const ora_stage* s, const sdfgi_gbuffer_pixel* gb, int w, i
     free(res);
     return ntasks;
 }
+
+/* composeFrame, shading.hpp:480-504 (per pixel, row-major; statistics merged) */
+int ora_compose(const ora_stage* s, const sdfgi_gbuffer_pixel* gb, int w, int h, const double* indirect,
+                const sdfgi_cfg* cfg, double* out, uint64_t stats[8]) {
+    stats_t st;
+    memset(&st, 0, sizeof(st));
+    for (int64_t i = 0; i < (int64_t)w * h; ++i) {
+        const sdfgi_gbuffer_pixel* px = &gb[i];
+        v3 o;
+        if (!(px->depth < ORA_INF)) {
+            o = s->sky;
+        } else {
+            v3 pos = V(px->world_pos[0], px->world_pos[1], px->world_pos[2]);
+            v3 nrm = V(px->normal[0], px->normal[1], px->normal[2]);
+            v3 direct = directIrradiance(s, pos, nrm, cfg, &st);
+            v3 alb = V(px->albedo[0], px->albedo[1], px->albedo[2]);
+            v3 em = V(px->emission[0], px->emission[1], px->emission[2]);
+            o = add(add(em, mulv(divs(alb, ORA_PI), direct)), V(indirect[3 * i], indirect[3 * i + 1], indirect[3 * i + 2]));
+        }
+        out[3 * i] = o.x;
+        out[3 * i + 1] = o.y;
+        out[3 * i + 2] = o.z;
+    }
+    if (stats) {
+        const uint64_t v[8] = {st.q, st.cv, st.cs, st.pe, st.steps, st.sphere, st.shadow, st.vis};
+        for (int k = 0; k < 8; ++k) stats[k] += v[k];
+    }
+    return 0;
+}

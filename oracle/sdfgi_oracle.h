@@ -70,6 +70,12 @@ int ora_gather_frame(const ora_stage* s, const sdfgi_gbuffer_pixel* gb, int w, i
                      int32_t* sparse_anchor, double* resolved, double* indirect, uint64_t vis_stats[8],
                      uint64_t contact_stats[8]);
 
+/* composeFrame (shading.hpp:480-504): sky radiance on sky pixels, else
+ * emission + albedo/pi * directIrradiance(worldPos, normal) + indirect.
+ * indirect / out: 3 doubles per pixel. */
+int ora_compose(const ora_stage* s, const sdfgi_gbuffer_pixel* gb, int w, int h, const double* indirect,
+                const sdfgi_cfg* cfg, double* out, uint64_t stats[8]);
+
 #ifdef __cplusplus
 }
 #endif

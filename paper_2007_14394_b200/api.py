@@ -10,6 +10,7 @@ reference's own; the state they operate on lives on the GPU in a ``Device``.
     updateProbes          batched updateProbe (probe_update.hpp:166-211) over the
                           probe stage of Renderer::renderFrame (pipeline.hpp:126-151)
     querySceneSdf         scene.hpp:336-340
+    composeFrame          shading.hpp:480-504 (pipeline.hpp:209)
     ProbeStage            the probe half of Renderer::renderFrame (pipeline.hpp:108-151)
 """
 from __future__ import annotations
@@ -51,6 +52,16 @@ def updateProbePositions(dev: Device, level, threshold1, threshold2, maxDescentS
 def updateProbes(dev: Device, cfg, frameIndex, refs=None, stats=False):
     """Batched updateProbe over `refs` ((level, index) pairs; None = all probes)."""
     return dev.update(frameIndex, cfg, refs, stats)
+
+
+def composeFrame(dev: Device, cfg, indirect=None, stats=False):
+    """shading.hpp:480-504 on the device's G-buffer: emission + albedo/pi * direct
+    (soft-shadowed, traced on the GPU) + indirect (the last gather's contactGI
+    output, or `indirect` = w*h*3 doubles). Returns the image (and TraceStats)."""
+    if indirect is not None:
+        dev.upload_indirect(indirect)
+    r = dev.compose(cfg, stats=stats)
+    return (r[0], r[2]) if stats else r[0]
 
 
 def querySceneSdf(dev: Device, points, initD=None):

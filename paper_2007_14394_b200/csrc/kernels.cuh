@@ -123,8 +123,9 @@ template <typename R> struct WaveParams {
     const struct GPix* gb;
     int gw, gh, contactSamples;
     double contactRadius;
-    const double* resolved;
+    const double* resolved;   // contact batch: resolved irradiance; compose: the indirect image
     double* indirect;
+    double* composed;         // compose: the final image (3 per pixel)
 };
 
 // Mirror of sdfgi_gbuffer_pixel (GBufferPixel, shading.hpp:13-22).
@@ -205,6 +206,8 @@ struct GridBuildParams {
 // the persistent K1/K2 grids; `ev` (optional, 2 events) brackets K1..K3.
 template <typename R>
 void launch_contact(const WaveParams<R>& p, bool stats, cudaStream_t st, long long* launches);
+template <typename R>
+void launch_compose(const WaveParams<R>& p, bool stats, cudaStream_t st, long long* launches);
 template <typename R>
 void launch_wavefront(const WaveParams<R>& p, int persistBlocks, bool stats, cudaStream_t st,
                       cudaEvent_t evStart, cudaEvent_t evEnd, long long* launches);

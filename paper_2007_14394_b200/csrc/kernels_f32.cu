@@ -11,5 +11,6 @@ template void launch_wavefront<float>(const WaveParams<float>&, int, bool, cudaS
 
 template void launch_gather<float>(const GatherParams<float>&, int, bool, cudaStream_t);
 template void launch_contact<float>(const WaveParams<float>&, bool, cudaStream_t, long long*);
+template void launch_compose<float>(const WaveParams<float>&, bool, cudaStream_t, long long*);
 
 }  // namespace sdfgi_dev

@@ -148,5 +148,6 @@ template void launch_wavefront<double>(const WaveParams<double>&, int, bool, cud
 
 template void launch_gather<double>(const GatherParams<double>&, int, bool, cudaStream_t);
 template void launch_contact<double>(const WaveParams<double>&, bool, cudaStream_t, long long*);
+template void launch_compose<double>(const WaveParams<double>&, bool, cudaStream_t, long long*);
 
 }  // namespace sdfgi_dev

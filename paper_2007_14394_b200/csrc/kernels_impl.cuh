@@ -624,10 +624,11 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_shado
 // shadeHit (probe_update.hpp:136-149) with directIrradiance's sum in light order
 // (visibility from K2), then convolveIrradiance + hysteresis blend + fillBorder
 // (probe_update.hpp:192-209, atlas.hpp:44-56) for one probe per CTA.
+// directIrradiance (probe_update.hpp:97-132) summed in light order with the K2
+// visibilities of item rid (vis[rid * L + light]).
 template <typename R>
-__device__ __forceinline__ V3<double> shadeRay(const WaveParams<R>& P, const HitRec<R>& h, unsigned long long rid) {
+__device__ __forceinline__ V3<double> directLight(const WaveParams<R>& P, const HitRec<R>& h, unsigned long long rid) {
     const SceneView<R>& s = P.scene;
-    if (!(h.status & 1) || h.owner < 0) return mk(s.sky[0], s.sky[1], s.sky[2]);
     const V3<R> pos = mk(h.p[0], h.p[1], h.p[2]);
     const V3<R> nrm = mk(h.n[0], h.n[1], h.n[2]);
     V3<double> total = mk(0.0, 0.0, 0.0);
@@ -655,6 +656,14 @@ __device__ __forceinline__ V3<double> shadeRay(const WaveParams<R>& P, const Hit
         const R vis = P.vis[rid * s.n_lights + li];
         total = total + unshadowed * static_cast<double>(vis);
     }
+    return total;
+}
+
+template <typename R>
+__device__ __forceinline__ V3<double> shadeRay(const WaveParams<R>& P, const HitRec<R>& h, unsigned long long rid) {
+    const SceneView<R>& s = P.scene;
+    if (!(h.status & 1) || h.owner < 0) return mk(s.sky[0], s.sky[1], s.sky[2]);
+    const V3<double> total = directLight(P, h, rid);
     const double* A = s.albedo + 3 * h.owner;
     const double* E = s.emission + 3 * h.owner;
     V3<double> brdf = mk(A[0], A[1], A[2]) / kPi;
@@ -907,6 +916,77 @@ static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long*
     const long long np = static_cast<long long>(p.gw) * p.gh;
     k_contact_combine<R><<<static_cast<int>((np + 127) / 128), 128, 0, st>>>(p);
     if (launches) *launches += 6;
+}
+
+// composeFrame (shading.hpp:480-504) as a wavefront: every geometry pixel becomes a
+// "hit" at its G-buffer position/normal, K2 traces its shadow rays (parked far
+// phase included), and the combine sums emission + albedo/pi * direct + indirect.
+template <typename R>
+__global__ void __launch_bounds__(128) k_compose_setup(WaveParams<R> P) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long np = static_cast<long long>(P.gw) * P.gh;
+    bool geo = false;
+    if (i < np) {
+        const GPix& px = P.gb[i];
+        geo = px.depth < INFINITY;
+        if (geo) {
+            HitRec<R> h;
+            for (int k = 0; k < 3; ++k) {
+                h.p[k] = R(px.world_pos[k]);
+                h.n[k] = R(px.normal[k]);
+            }
+            h.t = R(0);
+            h.owner = px.prim;
+            h.status = 1;
+            P.hits[i] = h;
+        }
+    }
+    const long long slot = parkSlot(P.ctr + 1, geo);  // compacted pixel list for K2
+    if (geo) P.hitList[slot] = static_cast<int>(i);
+}
+
+template <typename R>
+__global__ void __launch_bounds__(128) k_compose(WaveParams<R> P) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<long long>(P.gw) * P.gh) return;
+    const GPix& px = P.gb[i];
+    double* out = P.composed + 3 * i;
+    if (!(px.depth < INFINITY)) {
+        out[0] = P.scene.sky[0];
+        out[1] = P.scene.sky[1];
+        out[2] = P.scene.sky[2];
+        return;
+    }
+    const V3<double> direct = directLight(P, P.hits[i], static_cast<unsigned long long>(i));
+    const V3<double> alb = mk(px.albedo[0], px.albedo[1], px.albedo[2]);
+    const V3<double> em = mk(px.emission[0], px.emission[1], px.emission[2]);
+    const double* ind = P.resolved + 3 * i;  // the indirect image (input)
+    const V3<double> o = (em + (alb / kPi) * direct) + mk(ind[0], ind[1], ind[2]);
+    out[0] = o.x;
+    out[1] = o.y;
+    out[2] = o.z;
+}
+
+template <typename R, bool ST>
+static void composeWavefront(const WaveParams<R>& p, cudaStream_t st, long long* launches) {
+    cudaMemsetAsync(p.ctr, 0, 8 * sizeof(unsigned long long), st);
+    const long long np = static_cast<long long>(p.gw) * p.gh;
+    const int blocks = static_cast<int>((np + 127) / 128);
+    static int b2 = persistentBlocks(k_trace_shadow<R, ST, 0>, kWaveThreads, 0);
+    static int b2f = persistentBlocks(k_trace_shadow<R, ST, 1>, kWaveThreads, 0);
+    k_compose_setup<R><<<blocks, 128, 0, st>>>(p);
+    k_trace_shadow<R, ST, 0><<<b2, kWaveThreads, 0, st>>>(p);
+    k_trace_shadow<R, ST, 1><<<b2f, kWaveThreads, 0, st>>>(p);
+    k_compose<R><<<blocks, 128, 0, st>>>(p);
+    if (launches) *launches += 4;
+}
+
+template <typename R>
+void launch_compose(const WaveParams<R>& p, bool stats, cudaStream_t st, long long* launches) {
+    if (stats)
+        composeWavefront<R, true>(p, st, launches);
+    else
+        composeWavefront<R, false>(p, st, launches);
 }
 
 template <typename R>

@@ -175,10 +175,11 @@ struct Ctx {
     // gather (e): G-buffer, stage buffers, history (pipeline.hpp:213-218)
     int gw = 0, gh = 0;
     DBuf<GPix> gbuf;
-    DBuf<double> halfDepth, sparseIrr, resolved, indirect, histIrr, histDepth;
+    DBuf<double> halfDepth, sparseIrr, resolved, indirect, histIrr, histDepth, composed;
     DBuf<int> halfSrc, sel, sparseValid, sparseAnchor;
     int histValid = 0;
     cudaEvent_t gev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t cev[2] = {nullptr, nullptr};  // compose
     bool gevValid = false;
     DBuf<double> qpts, qinit, qd;
     DBuf<int> qowner;
@@ -195,9 +196,11 @@ struct Ctx {
         records.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
         wRayCount.free(); wHitList.free(); wRayStart.free(); wRot.free(); fib.free(); wHits.free();
         wVis.free(); wPark.free(); wCtr.free(); perm.free(); wRad.free();
-        gbuf.free(); halfDepth.free(); sparseIrr.free(); resolved.free(); indirect.free(); histIrr.free();
+        gbuf.free(); halfDepth.free(); sparseIrr.free(); resolved.free(); indirect.free(); histIrr.free(); composed.free();
         histDepth.free(); halfSrc.free(); sel.free(); sparseValid.free(); sparseAnchor.free();
         for (auto& e : gev)
+            if (e) cudaEventDestroy(e);
+        for (auto& e : cev)
             if (e) cudaEventDestroy(e);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
@@ -1440,6 +1443,7 @@ void ensureGather(Ctx* c, int w, int h) {
     c->sparseAnchor.alloc(static_cast<size_t>(sw) * sh);
     c->resolved.alloc(3 * np);
     c->indirect.alloc(3 * np);
+    c->composed.alloc(3 * np);
     c->histIrr.alloc(3 * np);
     c->histDepth.alloc(np);
     for (auto& e : c->gev)
@@ -1491,6 +1495,41 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     p.contactRadius = cfg->contact_radius_frac * sp0;  // pipeline.hpp:200
     p.resolved = c->resolved.p;
     p.indirect = c->indirect.p;
+    return p;
+}
+
+// Wavefront parameters for composeFrame: one shadow-ray item per (geometry pixel,
+// light); hits/vis indexed by pixel.
+template <typename R>
+WaveParams<R> composeParams(Ctx* c, const sdfgi_cfg* cfg) {
+    const size_t np = static_cast<size_t>(c->gw) * c->gh;
+    const int L = std::max(c->nLights, 1);
+    reserve(c->wHits, np * sizeof(HitRec<R>));
+    reserve(c->wHitList, np);
+    reserve(c->wVis, np * L * sizeof(R));
+    reserve(c->wCtr, 8);
+    reservePark<R>(c, np, L);
+    WaveParams<R> p;
+    std::memset(&p, 0, sizeof(p));
+    p.scene = c->sceneView<R>();
+    p.pc = c->probeCommon();
+    p.tc.eps = cfg->surface_epsilon;
+    p.tc.rayTMax = cfg->ray_tmax;
+    p.tc.shadowK = cfg->shadow_k;
+    p.tc.shadowSteps = static_cast<int>(cfg->shadow_steps);
+    p.hits = reinterpret_cast<HitRec<R>*>(c->wHits.p);
+    p.hitList = c->wHitList.p;
+    p.vis = reinterpret_cast<R*>(c->wVis.p);
+    p.ctr = c->wCtr.p;
+    p.park = c->accel && c->haveGrid && c->wPark.n >= 4096 ? c->wPark.p : nullptr;
+    p.parkBytes = p.park ? c->wPark.n : 0;
+    p.stats = c->scratch.p;
+    p.nRaysDirect = static_cast<long long>(np);
+    p.gb = c->gbuf.p;
+    p.gw = c->gw;
+    p.gh = c->gh;
+    p.resolved = c->indirect.p;  // input: the indirect image
+    p.composed = c->composed.p;
     return p;
 }
 
@@ -1691,11 +1730,61 @@ int sdfgi_gather_download(void* ctx, int which, void* dst, size_t bytes) {
             case 5: src = c->sparseIrr.p; n = c->sparseIrr.n * 8; break;
             case 6: src = c->sparseValid.p; n = c->sparseValid.n * 4; break;
             case 7: src = c->sparseAnchor.p; n = c->sparseAnchor.n * 4; break;
+            case 8: src = c->composed.p; n = c->composed.n * 8; break;
             default: throw Error(SDFGI_ERR_INVALID, "unknown gather buffer");
         }
         REQ(src && bytes == n, SDFGI_ERR_INVALID, "gather buffer size mismatch");
         CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int sdfgi_indirect_upload(void* ctx, const double* rgb, size_t n_doubles) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(rgb, SDFGI_ERR_INVALID, "null image");
+        REQ(c->gw > 0 && n_doubles == 3 * static_cast<size_t>(c->gw) * c->gh, SDFGI_ERR_INVALID,
+            "indirect image size mismatch (3 doubles per G-buffer pixel)");
+        CK(cudaMemcpyAsync(c->indirect.p, rgb, n_doubles * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int sdfgi_compose(void* ctx, const sdfgi_cfg* cfg, sdfgi_stats* stats, double* ms) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(c->haveScene, SDFGI_ERR_STATE, "scene not uploaded");
+        REQ(cfg, SDFGI_ERR_INVALID, "null cfg");
+        REQ(c->gw > 0 && c->gbuf.p, SDFGI_ERR_STATE, "no G-buffer (upload or render one first)");
+        const bool st = stats != nullptr;
+        CK(cudaMemsetAsync(c->scratch.p, 0, 32 * 8, c->stream));
+        for (auto& e : c->cev)
+            if (!e) CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(c->cev[0], c->stream));
+        if (c->precision == SDFGI_F64)
+            launch_compose<double>(composeParams<double>(c, cfg), st, c->stream, &c->launches);
+        else
+            launch_compose<float>(composeParams<float>(c, cfg), st, c->stream, &c->launches);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(c->cev[1], c->stream));
+        unsigned long long h[32];
+        CK(cudaMemcpyAsync(h, c->scratch.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (ms) {
+            float e = 0;
+            CK(cudaEventElapsedTime(&e, c->cev[0], c->cev[1]));
+            *ms = e;
+        }
+        if (stats) {
+            stats->sdf_queries += h[0];
+            stats->clusters_visited += h[1];
+            stats->clusters_skipped += h[2];
+            stats->primitive_evals += h[3];
+            stats->trace_steps += h[4];
+            stats->sphere_traces += h[5];
+            stats->shadow_traces += h[6];
+            stats->visibility_traces += h[7];
+        }
     });
 }
 

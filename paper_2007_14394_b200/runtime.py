@@ -66,6 +66,8 @@ _SIGS = {
     "sdfgi_gather_reset_history": [_P],
     "sdfgi_gather_download": [_P, _I, _P, _SZ],
     "sdfgi_last_gather_ms": [_P, _P],
+    "sdfgi_indirect_upload": [_P, _P, _SZ],
+    "sdfgi_compose": [_P, _P, _P, _P],
     "sdfgi_launch_count": [_P, _P],
 }
 
@@ -253,6 +255,20 @@ class Device:
     def reset_history(self):
         _call("sdfgi_gather_reset_history", self._ctx)
 
+    def upload_indirect(self, rgb):
+        a = np.ascontiguousarray(rgb, np.float64).reshape(-1)
+        _call("sdfgi_indirect_upload", self._ctx, _ptr(a), a.size)
+
+    def compose(self, cfg, stats=False):
+        """composeFrame (shading.hpp:480-504) on the context's G-buffer and indirect
+        image; returns (image[w*h*3], device ms[, stats])."""
+        c = np.ascontiguousarray(cfg, sio.CFG_DTYPE)
+        st = np.zeros(1, sio.STATS_DTYPE) if stats else None
+        ms = np.zeros(1)
+        _call("sdfgi_compose", self._ctx, _ptr(c), _ptr(st), _ptr(ms))
+        img = self.gather_buffer("composed")
+        return (img, float(ms[0]), st[0]) if stats else (img, float(ms[0]))
+
     def gather_buffer(self, name):
         w, h = self.gsize
         hw, hh = (w + 1) // 2, (h + 1) // 2
@@ -260,7 +276,8 @@ class Device:
         spec = {"resolved": (0, w * h * 3, np.float64), "indirect": (1, w * h * 3, np.float64),
                 "half_depth": (2, hw * hh, np.float64), "half_src": (3, hw * hh, np.int32),
                 "sel": (4, sw * sh, np.int32), "sparse_irr": (5, sw * sh * 3, np.float64),
-                "sparse_valid": (6, sw * sh, np.int32), "sparse_anchor": (7, sw * sh, np.int32)}
+                "sparse_valid": (6, sw * sh, np.int32), "sparse_anchor": (7, sw * sh, np.int32),
+                "composed": (8, w * h * 3, np.float64)}
         which, n, dt = spec[name]
         out = np.zeros(n, dt)
         _call("sdfgi_gather_download", self._ctx, which, _ptr(out), out.nbytes)

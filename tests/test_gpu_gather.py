@@ -72,6 +72,31 @@ def test_gather_matches_reference(dev, name):
         assert np.mean(e > 1e-3) <= 1e-3 and e.max() <= 5e-2, (name, f, "indirect", e.max())
 
 
+@pytest.mark.parametrize("name", GATHER_CASES)
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_compose_matches_reference(name, precision):
+    """composeFrame (f1) on the reference's own G-buffer and indirect image: FP64
+    bit-identical to the reference with identical shadow-trace statistics; FP32
+    within the north-star 1e-3."""
+    g = load_gather(name)
+    src = g.src
+    with Device(0, precision=precision) as d:
+        stage = api.ProbeStage(d, g.scene, cfg=src.cfg(), res=src.res, spacing=src.spacing)
+        d.upload_gbuffer(g.w, g.h, g.data["gbuffer"])
+        for f, meta in enumerate(g.frames):
+            d.upload_indirect(g.data[f"indirect_f{f}"])
+            img, ms, st = d.compose(stage.cfg, stats=True)
+            want = g.data[f"composed_f{f}"]
+            if precision == "f64":
+                assert np.array_equal(img, want), (name, f, float(np.max(np.abs(img - want))))
+                ps = meta["compose_stats"]
+                assert int(st["shadow_traces"]) == ps["shadow_traces"]
+                assert int(st["sdf_queries"]) == ps["sdf_queries"]
+            else:
+                e = rel(img, want)
+                assert np.mean(e > 1e-3) <= 1e-3 and e.max() <= 5e-2, (name, f, e.max())
+
+
 def test_gather_1080p_properties(dev):
     """C3 at full size on the C2 scene: the G-buffer rendered on the device agrees with
     the oracle on a row sample; resolved irradiance is finite, >= 0, zero on sky."""

@@ -37,4 +37,11 @@ def test_oracle_gather_bit_exact(name):
         for k in ("half_depth", "half_src", "sel", "sparse_valid", "sparse_anchor", "sparse_irr", "resolved",
                   "indirect"):
             assert np.array_equal(out[k], g.data[f"{k}_f{f}"]), (name, f, k)
+        # composeFrame on the reference's own indirect image (pipeline.hpp:209)
+        img, cst = st.compose(want, g.w, g.h, g.data[f"indirect_f{f}"])
+        assert np.array_equal(img, g.data[f"composed_f{f}"]), (name, f, "composed")
+        ps = meta["compose_stats"]
+        assert [int(x) for x in cst] == [ps[k] for k in ("sdf_queries", "clusters_visited", "clusters_skipped",
+                                                          "primitive_evals", "trace_steps", "sphere_traces",
+                                                          "shadow_traces", "visibility_traces")]
         hist = (out["resolved"], want["depth"])
