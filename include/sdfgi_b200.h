@@ -229,6 +229,16 @@ SDFGI_API int sdfgi_probes_reset(void* ctx, int level);
 SDFGI_API int sdfgi_probes_upload(void* ctx, int level, const sdfgi_probe* probes, int n);
 SDFGI_API int sdfgi_probes_download(void* ctx, int level, sdfgi_probe* probes, int n);
 
+/* selectProbesForUpdate (probe_volume.hpp:154-198) over every cascade's device
+ * probes: priority = 1/(1 + dist/spacing) * (0.25 + 0.75 max(0, facing)) *
+ * staleness (x4 if rejectHistory); probes stale for >= ceil(total/budget) frames
+ * are forced first, oldest first; the first `budget` in the reference's
+ * stable-sort order. out_refs: 2 * min(budget, total) int32 (cascade level,
+ * index), ready for sdfgi_probes_update. budget <= 0 selects nothing (the caller
+ * passes the probe count for "all", pipeline.hpp:133). */
+SDFGI_API int sdfgi_select_probes(void* ctx, const double cam_pos[3], const double cam_fwd[3], int budget, int frame,
+                                  int32_t* out_refs, int* n_out);
+
 /* updateProbePositions (probe_volume.hpp:99-143) for one cascade, device-resident.
  * Bit-exact with the reference in SDFGI_F64 mode. */
 SDFGI_API int sdfgi_probes_relocate(void* ctx, int level, double threshold1, double threshold2,

@@ -123,6 +123,12 @@ CASES = {
     "openfield": dict(scene="open-field-cascade.scene", passes=2, extra=["--nrays", 16], debug=[40]),
     "furnace": dict(scene="furnace.scene", passes=1, extra=[], debug=[21]),
     "kinds": dict(scene=None, passes=2, extra=["--nrays", 24], debug=[3, 70, 200]),
+    # budgeted scheduling (selectProbesForUpdate, probe_volume.hpp:154-198): forced
+    # staleness kicks in after ceil(total / budget) frames
+    "sched_c1": dict(scene="cornell.scene", passes=8, extra=["--res", 8, 8, 8, "--spacing", 1.0, "--nrays", 32,
+                                                              "--budget", 96], debug=[]),
+    "sched_openfield": dict(scene="open-field-cascade.scene", passes=6, extra=["--nrays", 8, "--budget", 200],
+                            debug=[]),
 }
 
 
@@ -149,6 +155,8 @@ def build_case(name, spec):
                 data[base] = np.fromfile(path, scene_io.PROBE_DTYPE)
             elif base.startswith("rays"):
                 data[base] = np.fromfile(path, scene_io.RAY_DTYPE)
+            elif base.startswith("refs"):
+                data[base] = np.fromfile(path, "<i4").reshape(-1, 2)
     summary["case"] = name
     summary["args"] = [str(a) for a in args[3:]]
     summary["debug_probes"] = spec["debug"]

@@ -40,6 +40,8 @@ def load():
         "ora_render_gbuffer": ([_P, _P, _I, _I, _P, _P, _P], _I),
         "ora_gather_frame": ([_P, _P, _I, _I, _I, _P, _P, _P, _I] + [_P] * 10, _I),
         "ora_compose": ([_P, _P, _I, _I, _P, _P, _P, _P], _I),
+        "ora_select": ([_P, _P, _P, _I, _I, _P], _I),
+        "ora_update_refs": ([_P, _P, _I, _P, _I, _I, _P, _P, _P, _P], _I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -111,6 +113,24 @@ class Stage:
         stats = np.zeros(8, np.uint64)
         rc = load().ora_update(self.h, _p(self.cfg), frame, stride, threads, ctypes.byref(md), ctypes.byref(rays),
                                ctypes.byref(upd), _p(stats))
+        assert rc == 0
+        return md.value, rays.value, upd.value, stats
+
+    def select(self, budget, frame, cam_pos=None, cam_fwd=None):
+        """selectProbesForUpdate (probe_volume.hpp:154-198) -> (n, 2) int32 (slot, index)."""
+        cp = np.ascontiguousarray(self.scene.camera.position if cam_pos is None else cam_pos, np.float64)
+        cf = np.ascontiguousarray(self.scene.camera.forward if cam_fwd is None else cam_fwd, np.float64)
+        out = np.zeros((max(budget, 0), 2), np.int32)
+        n = load().ora_select(self.h, _p(cp), _p(cf), int(budget), int(frame), _p(out))
+        return out[:n]
+
+    def update_refs(self, frame, refs, threads=1):
+        refs = np.ascontiguousarray(refs, np.int32).reshape(-1, 2)
+        md = ctypes.c_double()
+        rays, upd = ctypes.c_int64(), ctypes.c_int64()
+        stats = np.zeros(8, np.uint64)
+        rc = load().ora_update_refs(self.h, _p(self.cfg), frame, _p(refs), len(refs), threads, ctypes.byref(md),
+                                    ctypes.byref(rays), ctypes.byref(upd), _p(stats))
         assert rc == 0
         return md.value, rays.value, upd.value, stats
 

@@ -317,6 +317,7 @@ struct Opts {
     std::vector<std::string> sets;  // "key value" config overrides
     int width = 0, height = 0;  // gather
     int gatherFrames = 2;
+    int budget = 0;  // probeBudget for selectProbesForUpdate (0 = every probe)
 };
 
 void applySet(RenderConfig& c, const std::string& kv) {
@@ -361,6 +362,7 @@ Opts parseOpts(int argc, char** argv, int first) {
             o.width = std::stoi(next());
             o.height = std::stoi(next());
         } else if (a == "--gather-frames") o.gatherFrames = std::stoi(next());
+        else if (a == "--budget") o.budget = std::stoi(next());
         else throw std::runtime_error("unknown option " + a);
     }
     return o;
@@ -408,6 +410,7 @@ struct PassResult {
     int updated = 0;
     double jitter = 0;
     double relocMs = 0, updateMs = 0;
+    std::vector<int32_t> refs;  // selected (cascade, index) pairs
 };
 
 // One probe pass of renderFrame (pipeline.hpp:108-151), frame = `frame`.
@@ -461,8 +464,13 @@ PassResult runPass(ProbeStage& st, int frame, const Opts& o, std::vector<sdfgi_r
     st.atlas[writeIdx] = st.atlas[st.readIdx];
     int total = 0;
     for (auto& c : st.cascades) total += c.probeCount();
-    auto refs = selectProbesForUpdate(st.cascades, st.camera.position, st.camera.forward, total,
-                                      frame);
+    // pipeline.hpp:133-135: budget = probeBudget > 0 ? probeBudget : every probe
+    auto refs = selectProbesForUpdate(st.cascades, st.camera.position, st.camera.forward,
+                                      o.budget > 0 ? o.budget : total, frame);
+    for (const ProbeRef& ref : refs) {
+        r.refs.push_back(ref.cascade);
+        r.refs.push_back(ref.index);
+    }
     if (o.stride > 1) {
         std::vector<ProbeRef> sub;
         for (auto& ref : refs)
@@ -549,6 +557,7 @@ int cmdPasses(int argc, char** argv) {
                     st.atlas[st.readIdx][ci].dump(dir + "/atlas" + sfx + c + ".sdfa");
                 }
                 if (!rays.empty()) writeVec(dir + "/rays" + sfx + ".bin", rays);
+                if (o.budget > 0) writeVec(dir + "/refs" + sfx + ".bin", r.refs);
             }
             if (p) js << ", ";
             js << "{\"pass\": " << p << ", \"relocated\": " << r.rep.relocated

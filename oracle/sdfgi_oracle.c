@@ -746,6 +746,8 @@ typedef struct {
     ora_stage* s;
     const sdfgi_cfg* cfg;
     int frame, slot, stride, worker, workers;
+    const int32_t* refs; /* (slot, index) pairs, or NULL: every stride-th probe of `slot` */
+    int nrefs;
     double md;
     int64_t rays, updated;
     stats_t st;
@@ -757,6 +759,19 @@ static void* updateWorker(void* arg) {
     const cascade_t* c = &w->s->cas[w->slot];
     int n = c->res[0] * c->res[1] * c->res[2];
     float* back = w->s->atlas[1 - w->s->front];
+    if (w->refs) {
+        for (int item = w->worker; item < w->nrefs; item += w->workers) {
+            int slot = w->refs[2 * item], i = w->refs[2 * item + 1];
+            if (!w->s->probes[w->s->cas[slot].base + i].alive) continue; /* pipeline.hpp:141 */
+            double d;
+            int r;
+            updateProbe(w->s, slot, i, back, w->cfg, w->frame, &w->st, &d, &r);
+            w->md = smax(w->md, d);
+            w->rays += r;
+            w->updated += 1;
+        }
+        return NULL;
+    }
     for (int item = w->worker; item * w->stride < n; item += w->workers) {
         int i = item * w->stride;
         if (!w->s->probes[c->base + i].alive) continue; /* pipeline.hpp:141 */
@@ -770,8 +785,27 @@ static void* updateWorker(void* arg) {
     return NULL;
 }
 
+static int updateCommon(ora_stage* s, const sdfgi_cfg* cfg, int frame, int stride, const int32_t* refs, int nrefs,
+                        int threads, double* max_delta, int64_t* rays, int64_t* updated, uint64_t stats[8]);
+
 int ora_update(ora_stage* s, const sdfgi_cfg* cfg, int frame, int stride, int threads, double* max_delta,
                int64_t* rays, int64_t* updated, uint64_t stats[8]) {
+    return updateCommon(s, cfg, frame, stride, NULL, 0, threads, max_delta, rays, updated, stats);
+}
+
+int ora_update_refs(ora_stage* s, const sdfgi_cfg* cfg, int frame, const int32_t* refs, int n_refs, int threads,
+                    double* max_delta, int64_t* rays, int64_t* updated, uint64_t stats[8]) {
+    for (int i = 0; i < n_refs; ++i) {
+        int slot = refs[2 * i], idx = refs[2 * i + 1];
+        if (slot < 0 || slot >= s->ncas) return 2;
+        const cascade_t* c = &s->cas[slot];
+        if (idx < 0 || idx >= c->res[0] * c->res[1] * c->res[2]) return 2;
+    }
+    return updateCommon(s, cfg, frame, 1, refs, n_refs, threads, max_delta, rays, updated, stats);
+}
+
+static int updateCommon(ora_stage* s, const sdfgi_cfg* cfg, int frame, int stride, const int32_t* refs, int nrefs,
+                        int threads, double* max_delta, int64_t* rays, int64_t* updated, uint64_t stats[8]) {
     if (cfg->oct_res != s->oct) return 1;
     int front = s->front, back = 1 - front;
     size_t nf = tileFloats(s->oct) * (size_t)s->nprobes;
@@ -784,13 +818,15 @@ int ora_update(ora_stage* s, const sdfgi_cfg* cfg, int frame, int stride, int th
     memset(&tot, 0, sizeof(tot));
     work_t* ws = (work_t*)calloc((size_t)threads, sizeof(work_t));
     pthread_t* th = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
-    for (int slot = 0; slot < s->ncas; ++slot) {
+    for (int slot = 0; slot < (refs ? 1 : s->ncas); ++slot) {
         for (int w = 0; w < threads; ++w) {
             memset(&ws[w], 0, sizeof(work_t));
             ws[w].s = s;
             ws[w].cfg = cfg;
             ws[w].frame = frame;
             ws[w].slot = slot;
+            ws[w].refs = refs;
+            ws[w].nrefs = nrefs;
             ws[w].stride = stride;
             ws[w].worker = w;
             ws[w].workers = threads;
@@ -1283,4 +1319,66 @@ int ora_compose(const ora_stage* s, const sdfgi_gbuffer_pixel* gb, int w, int h,
         for (int k = 0; k < 8; ++k) stats[k] += v[k];
     }
     return 0;
+}
+
+/* selectProbesForUpdate, probe_volume.hpp:154-198: priority favours near,
+ * camera-facing, stale and history-rejected probes; probes at least one fair
+ * period stale are forced (oldest first). std::stable_sort's order = this total
+ * order with the candidate position as the final key. */
+typedef struct {
+    int slot, index, staleness, forced;
+    double priority;
+    int64_t pos;
+} cand_t;
+
+static int candCmp(const void* pa, const void* pb) {
+    const cand_t* a = (const cand_t*)pa;
+    const cand_t* b = (const cand_t*)pb;
+    if (a->forced != b->forced) return a->forced ? -1 : 1;
+    if (a->forced) {
+        if (a->staleness != b->staleness) return a->staleness > b->staleness ? -1 : 1;
+    } else if (a->priority != b->priority) {
+        return a->priority > b->priority ? -1 : 1;
+    }
+    return a->pos < b->pos ? -1 : (a->pos > b->pos ? 1 : 0);
+}
+
+int ora_select(const ora_stage* s, const double cam_pos[3], const double cam_fwd[3], int budget, int frame,
+               int32_t* out_refs) {
+    int total = 0;
+    for (int ci = 0; ci < s->ncas; ++ci) total += s->cas[ci].res[0] * s->cas[ci].res[1] * s->cas[ci].res[2];
+    if (total == 0 || budget <= 0) return 0;
+    int period = (total + budget - 1) / budget;
+    int forceAge = period;
+    cand_t* c = (cand_t*)malloc(sizeof(cand_t) * (size_t)total);
+    v3 cp = V(cam_pos[0], cam_pos[1], cam_pos[2]), cf = V(cam_fwd[0], cam_fwd[1], cam_fwd[2]);
+    int64_t k = 0;
+    for (int ci = 0; ci < s->ncas; ++ci) {
+        const cascade_t* cs = &s->cas[ci];
+        int n = cs->res[0] * cs->res[1] * cs->res[2];
+        for (int i = 0; i < n; ++i) {
+            const probe_t* p = &s->probes[cs->base + i];
+            double dist = len(sub(p->pos, cp));
+            int staleness = frame - p->last_frame;
+            double angular = 0.25;
+            if (dist > 1e-9) angular += 0.75 * smax(0.0, dot(divs(sub(p->pos, cp), dist), cf));
+            double priority = (1.0 / (1.0 + dist / cs->spacing)) * angular * staleness;
+            if (p->reject) priority *= 4.0;
+            c[k].slot = ci;
+            c[k].index = i;
+            c[k].staleness = staleness;
+            c[k].forced = staleness >= forceAge;
+            c[k].priority = priority;
+            c[k].pos = k;
+            ++k;
+        }
+    }
+    qsort(c, (size_t)total, sizeof(cand_t), candCmp);
+    int n = budget < total ? budget : total;
+    for (int i = 0; i < n; ++i) {
+        out_refs[2 * i] = c[i].slot;
+        out_refs[2 * i + 1] = c[i].index;
+    }
+    free(c);
+    return n;
 }

@@ -43,6 +43,15 @@ int ora_relocate(ora_stage* s, int slot, double th1, double th2, int max_steps, 
 int ora_update(ora_stage* s, const sdfgi_cfg* cfg, int frame, int stride, int threads, double* max_delta,
                int64_t* rays, int64_t* updated, uint64_t stats[8]);
 
+/* ora_update over an explicit (slot, index) list (e.g. ora_select's). */
+int ora_update_refs(ora_stage* s, const sdfgi_cfg* cfg, int frame, const int32_t* refs, int n_refs, int threads,
+                    double* max_delta, int64_t* rays, int64_t* updated, uint64_t stats[8]);
+
+/* selectProbesForUpdate (probe_volume.hpp:154-198): up to `budget` (slot, index)
+ * pairs into out_refs, in the reference's order; returns the count. */
+int ora_select(const ora_stage* s, const double cam_pos[3], const double cam_fwd[3], int budget, int frame,
+               int32_t* out_refs);
+
 int ora_probes(const ora_stage* s, int slot, sdfgi_probe* out, int n);
 int ora_atlas(const ora_stage* s, int slot, float* out, int64_t n_floats); /* front atlas */
 

@@ -9,6 +9,8 @@ reference's own; the state they operate on lives on the GPU in a ``Device``.
     updateProbePositions  probe_volume.hpp:99-143
     updateProbes          batched updateProbe (probe_update.hpp:166-211) over the
                           probe stage of Renderer::renderFrame (pipeline.hpp:126-151)
+    selectProbesForUpdate probe_volume.hpp:154-198 (on the device)
+    recenterCascade       probe_volume.hpp:80-86
     querySceneSdf         scene.hpp:336-340
     composeFrame          shading.hpp:480-504 (pipeline.hpp:209)
     ProbeStage            the probe half of Renderer::renderFrame (pipeline.hpp:108-151)
@@ -41,6 +43,23 @@ def makeCascade(dev: Device, resX, resY, resZ, spacing0, level, cameraPos, oct_r
     origin = cascadeOriginFor(cameraPos, resX, resY, resZ, spacing)
     dev.set_cascade(level, (resX, resY, resZ), spacing, origin, oct_res)
     return level
+
+
+def recenterCascade(dev: Device, level, resX, resY, resZ, spacing0, origin, cameraPos, oct_res=8):
+    """probe_volume.hpp:80-86: True (and the cascade re-made: probes reset, atlases
+    cleared as pipeline.hpp:110-113 does) when the snapped origin moved."""
+    spacing = spacing0 * math.pow(2.0, level)
+    o = cascadeOriginFor(cameraPos, resX, resY, resZ, spacing)
+    if math.sqrt(float(np.dot(o - np.asarray(origin), o - np.asarray(origin)))) < 1e-12:
+        return False
+    dev.set_cascade(level, (resX, resY, resZ), spacing, o, oct_res)
+    return True
+
+
+def selectProbesForUpdate(dev: Device, cameraPos, cameraForward, budget, frameIndex):
+    """probe_volume.hpp:154-198 over the device's cascades: (n, 2) int32 (cascade
+    level, index) in the reference's order, n = min(budget, probes)."""
+    return dev.select(cameraPos, cameraForward, budget, frameIndex)
 
 
 def updateProbePositions(dev: Device, level, threshold1, threshold2, maxDescentSteps=16, stats=False,
@@ -108,8 +127,16 @@ class ProbeStage:
                                              stats, float(self.cfg["gradient_step"][0])))
         return reps
 
-    def run_pass(self, frame, stats=False):
+    def run_pass(self, frame, stats=False, camera=None):
+        """One pass; cfg.probe_budget > 0 schedules selectProbesForUpdate's refs
+        (pipeline.hpp:133-135) from `camera` (position, forward; default: the scene's)."""
         reps = self.relocate_all(stats)
-        upd = updateProbes(self.dev, self.cfg, frame, None, stats)
+        budget = int(self.cfg["probe_budget"][0])
+        refs = None
+        if budget > 0:
+            cam = self.scene.camera if camera is None else None
+            pos, fwd = (cam.position, cam.forward) if cam is not None else camera
+            refs = selectProbesForUpdate(self.dev, pos, fwd, budget, frame)
+        upd = updateProbes(self.dev, self.cfg, frame, refs, stats)
         self.dev.swap()
         return reps, upd

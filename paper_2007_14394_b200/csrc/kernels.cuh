@@ -176,6 +176,27 @@ template <typename R> struct GatherParams {
     unsigned long long* taskCount;
 };
 
+// selectProbesForUpdate on the device (select.cu).
+struct SelectParams {
+    ProbeCommon pc;
+    int total, frame, forceAge;
+    double camPos[3], camFwd[3];
+    char* forced;
+    char* other;
+    int* ids;
+    unsigned int* keyForced;
+    unsigned long long* keyOther;
+    int *idsF, *idsO, *idsF2, *idsO2;
+    unsigned int *kF, *kF2;
+    unsigned long long *kO, *kO2;
+    int* counts;   // [0] forced, [1] others
+    int* outRefs;  // 2 per selected probe: cascade level, index
+    void* temp;
+    size_t tempBytes;
+};
+size_t select_scratch_bytes(int total);
+int launch_select(const SelectParams& P, int budget, cudaStream_t st, long long* launches);
+
 struct QueryParams {
     SceneView<double> scene;
     const double* pts;

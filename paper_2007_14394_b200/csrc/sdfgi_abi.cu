@@ -181,6 +181,7 @@ struct Ctx {
     cudaEvent_t gev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t cev[2] = {nullptr, nullptr};  // compose
     bool gevValid = false;
+    DBuf<unsigned char> selScratch;  // sdfgi_select_probes
     DBuf<double> qpts, qinit, qd;
     DBuf<int> qowner;
 
@@ -193,7 +194,7 @@ struct Ctx {
         bvh.free(); unbList.free(); primBox.free();
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
-        records.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
+        records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
         wRayCount.free(); wHitList.free(); wRayStart.free(); wRot.free(); fib.free(); wHits.free();
         wVis.free(); wPark.free(); wCtr.free(); perm.free(); wRad.free();
         gbuf.free(); halfDepth.free(); sparseIrr.free(); resolved.free(); indirect.free(); histIrr.free(); composed.free();
@@ -1011,19 +1012,32 @@ int sdfgi_cascade_set(void* ctx, int level, int res_x, int res_y, int res_z, dou
         h.level = level;
         h.spacing = spacing;
         for (int k = 0; k < 3; ++k) h.origin[k] = origin[k];
-        bool replaced = false;
-        for (auto& cs : c->cascades)
+        bool replaced = false, sameShape = false;
+        int slot = -1;
+        for (size_t k = 0; k < c->cascades.size(); ++k) {
+            CascadeHost& cs = c->cascades[k];
             if (cs.level == level) {
+                sameShape = cs.count() == h.count();
+                h.base = cs.base;
                 cs = h;
                 replaced = true;
+                slot = static_cast<int>(k);
             }
+        }
         if (!replaced) {
             REQ(static_cast<int>(c->cascades.size()) < kMaxCascades, SDFGI_ERR_INVALID, "too many cascades");
             c->cascades.push_back(h);
         }
-        c->octRes = oct_res;
-        c->front = 0;
-        reallocProbes(c);
+        if (replaced && sameShape && oct_res == c->octRes) {
+            // recenterCascade (probe_volume.hpp:80-86): this cascade's probes are
+            // re-made and its atlas tiles cleared (pipeline.hpp:110-113); the other
+            // cascades and the front/back roles are untouched
+            resetProbes(c, slot);
+        } else {
+            c->octRes = oct_res;
+            c->front = 0;
+            reallocProbes(c);
+        }
         // grow the grid over this volume (one probe spacing of slack, plus a quarter
         // of the volume so a scrolling cascade does not rebuild every frame)
         double box[6];
@@ -1128,6 +1142,66 @@ int sdfgi_probes_download(void* ctx, int level, sdfgi_probe* probes, int n) {
             probes[i].reject_history = rj[i];
             probes[i].last_update_frame = lf[i];
         }
+    });
+}
+
+int sdfgi_select_probes(void* ctx, const double cam_pos[3], const double cam_fwd[3], int budget, int frame,
+                        int32_t* out_refs, int* n_out) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        requireProbes(c);
+        REQ(cam_pos && cam_fwd && n_out, SDFGI_ERR_INVALID, "null argument");
+        const int total = c->totalProbes;
+        *n_out = 0;
+        if (total == 0 || budget <= 0) return;  // probe_volume.hpp:171
+        REQ(out_refs, SDFGI_ERR_INVALID, "null out_refs");
+        SelectParams P;
+        std::memset(&P, 0, sizeof(P));
+        P.pc = c->probeCommon();
+        P.total = total;
+        P.frame = frame;
+        P.forceAge = static_cast<int>((static_cast<long long>(total) + budget - 1) / budget);  // one fair period
+        for (int k = 0; k < 3; ++k) {
+            P.camPos[k] = cam_pos[k];
+            P.camFwd[k] = cam_fwd[k];
+        }
+        const size_t n = static_cast<size_t>(total);
+        const size_t tempBytes = select_scratch_bytes(total);
+        size_t off = 0;
+        auto carve = [&](size_t bytes) {
+            size_t o = off;
+            off += (bytes + 255) & ~static_cast<size_t>(255);
+            return o;
+        };
+        const size_t oForced = carve(n), oOther = carve(n), oIds = carve(4 * n), oKeyF = carve(4 * n),
+                     oKeyO = carve(8 * n), oIdsF = carve(4 * n), oIdsO = carve(4 * n), oIdsF2 = carve(4 * n),
+                     oIdsO2 = carve(4 * n), oKF = carve(4 * n), oKF2 = carve(4 * n), oKO = carve(8 * n),
+                     oKO2 = carve(8 * n), oCounts = carve(8), oRefs = carve(8 * n), oTemp = carve(tempBytes);
+        reserve(c->selScratch, off);
+        unsigned char* b = c->selScratch.p;
+        P.forced = reinterpret_cast<char*>(b + oForced);
+        P.other = reinterpret_cast<char*>(b + oOther);
+        P.ids = reinterpret_cast<int*>(b + oIds);
+        P.keyForced = reinterpret_cast<unsigned int*>(b + oKeyF);
+        P.keyOther = reinterpret_cast<unsigned long long*>(b + oKeyO);
+        P.idsF = reinterpret_cast<int*>(b + oIdsF);
+        P.idsO = reinterpret_cast<int*>(b + oIdsO);
+        P.idsF2 = reinterpret_cast<int*>(b + oIdsF2);
+        P.idsO2 = reinterpret_cast<int*>(b + oIdsO2);
+        P.kF = reinterpret_cast<unsigned int*>(b + oKF);
+        P.kF2 = reinterpret_cast<unsigned int*>(b + oKF2);
+        P.kO = reinterpret_cast<unsigned long long*>(b + oKO);
+        P.kO2 = reinterpret_cast<unsigned long long*>(b + oKO2);
+        P.counts = reinterpret_cast<int*>(b + oCounts);
+        P.outRefs = reinterpret_cast<int*>(b + oRefs);
+        P.temp = b + oTemp;
+        P.tempBytes = tempBytes;
+        const int sel = launch_select(P, budget, c->stream, &c->launches);
+        checkLaunch(c);
+        if (sel > 0)
+            CK(cudaMemcpyAsync(out_refs, P.outRefs, 8 * static_cast<size_t>(sel), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        *n_out = sel;
     });
 }
 

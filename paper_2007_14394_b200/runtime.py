@@ -68,6 +68,7 @@ _SIGS = {
     "sdfgi_last_gather_ms": [_P, _P],
     "sdfgi_indirect_upload": [_P, _P, _SZ],
     "sdfgi_compose": [_P, _P, _P, _P],
+    "sdfgi_select_probes": [_P, _P, _P, _I, _I, _P, _P],
     "sdfgi_launch_count": [_P, _P],
 }
 
@@ -353,6 +354,16 @@ class Device:
         _call("sdfgi_probes_update", self._ctx, _ptr(r), 0 if r is None else len(r), int(frame), _ptr(cfg),
               _ptr(res), _ptr(st))
         return (res[0], st[0]) if stats else res[0]
+
+    def select(self, cam_pos, cam_fwd, budget, frame):
+        """selectProbesForUpdate on the device -> (n, 2) int32 (level, index)."""
+        cp = np.ascontiguousarray(cam_pos, np.float64)
+        cf = np.ascontiguousarray(cam_fwd, np.float64)
+        out = np.zeros((max(int(budget), 0), 2), np.int32)
+        n = ctypes.c_int()
+        _call("sdfgi_select_probes", self._ctx, _ptr(cp), _ptr(cf), int(budget), int(frame), _ptr(out),
+              ctypes.byref(n))
+        return out[:n.value]
 
     def swap(self):
         _call("sdfgi_atlas_swap", self._ctx)

@@ -14,6 +14,7 @@ while [ $# -gt 1 ]; do
   nvcc $COMMON $flags -fmad=true -c $P/csrc/kernels_f32.cu -o $OUT/$name/f32.o &
   nvcc $COMMON $flags -c $P/csrc/sdfgi_abi.cu -o $OUT/$name/abi.o &
   nvcc $COMMON $flags -c $P/csrc/fp_peak.cu -o $OUT/$name/fp.o &
+  nvcc $COMMON $flags -fmad=false -c $P/csrc/select.cu -o $OUT/$name/select.o &
   wait
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/$name/libsdfgi_b200.so $OUT/$name/*.o -lnccl -lcudart
   echo built $OUT/$name

@@ -25,6 +25,7 @@ class Case:
         self.res = None
         self.spacing = None
         self.n_rays = None
+        self.budget = 0
         i = 0
         while i < len(args):
             a = args[i]
@@ -36,7 +37,9 @@ class Case:
                 self.spacing = float(args[i + 1])
             elif a == "--nrays":
                 self.n_rays = int(args[i + 1])
-            i += 2 if a in ("--spacing", "--nrays", "--passes", "--threads", "--debug-probe") else 1
+            elif a == "--budget":
+                self.budget = int(args[i + 1])
+            i += 2 if a in ("--spacing", "--nrays", "--passes", "--threads", "--debug-probe", "--budget") else 1
         self.levels = self.scene.cascade.levels
 
     def cfg(self):
@@ -51,7 +54,8 @@ def load(name):
 
 
 GATHER_CASES = sorted(d for d in CASES if d.startswith("gather_"))
-CASES = [d for d in CASES if not d.startswith("gather_")]
+SCHED_CASES = sorted(d for d in CASES if d.startswith("sched_"))  # budgeted selectProbesForUpdate
+CASES = [d for d in CASES if not d.startswith(("gather_", "sched_"))]
 
 
 class GatherCase:

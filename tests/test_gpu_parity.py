@@ -13,7 +13,7 @@ Bars (BASELINE.json north_star):
 import numpy as np
 import pytest
 
-from golden_util import CASES, load
+from golden_util import CASES, SCHED_CASES, load
 from paper_2007_14394_b200 import api, scene_io
 from paper_2007_14394_b200.runtime import Device
 
@@ -135,3 +135,56 @@ def test_f32_mode_within_tolerance(dev):
         assert frac_bad < 1e-3, f"{frac_bad:.2e} of channels exceed 1e-3 (max {err.max():.2e})"
     finally:
         dev.set_precision("f64")
+
+
+@pytest.mark.parametrize("name", SCHED_CASES)
+def test_scheduler_matches_reference(dev, name):
+    """Budgeted passes (f3): the device's selectProbesForUpdate returns the
+    reference's refs in the reference's order; updating exactly those probes gives
+    the reference's probe states and texels."""
+    case = load(name)
+    stage = api.ProbeStage(dev, case.scene, cfg=case.cfg(), res=case.res, spacing=case.spacing)
+    cam = case.scene.camera
+    for p, want in enumerate(case.passes):
+        stage.relocate_all()
+        refs = api.selectProbesForUpdate(dev, cam.position, cam.forward, case.budget, p)
+        assert np.array_equal(refs, case.data[f"refs_p{p}"]), (name, p)
+        res = api.updateProbes(dev, stage.cfg, p, refs)
+        dev.swap()
+        assert int(res["rays_traced"]) == want["rays_traced"], (name, p)
+        assert int(res["probes_updated"]) == want["probes_updated"], (name, p)
+        for level in range(stage.levels):
+            check_probes(dev.probes(level), case.data[f"probes_p{p}_c{level}"], f"{name} pass {p} c{level}")
+            err = texel_rel_err(dev.atlas(level, 0), case.data[f"atlas_p{p}_c{level}"])
+            assert np.mean(err > TEXEL_RTOL) <= 1e-3 and err.max() <= 1e-2, (name, p, level, err.max())
+
+
+def test_scheduler_budget_edges(dev):
+    """budget <= 0 selects nothing; budget >= probes selects every probe once."""
+    case = load(SCHED_CASES[0])
+    stage = api.ProbeStage(dev, case.scene, cfg=case.cfg(), res=case.res, spacing=case.spacing)
+    cam = case.scene.camera
+    assert len(api.selectProbesForUpdate(dev, cam.position, cam.forward, 0, 0)) == 0
+    n = sum(dev.probe_count(level) for level in range(stage.levels))
+    refs = api.selectProbesForUpdate(dev, cam.position, cam.forward, n + 10, 0)
+    assert len(refs) == n and len({tuple(r) for r in refs}) == n
+
+
+def test_recenter_cascade_resets_only_that_cascade(dev):
+    """recenterCascade (probe_volume.hpp:80-86) + the atlas clear of pipeline.hpp:110-113."""
+    case = load("openfield")
+    stage = api.ProbeStage(dev, case.scene, cfg=case.cfg(), res=case.res, spacing=case.spacing)
+    for p in range(2):
+        stage.run_pass(p)
+    before = [(dev.probes(lv), dev.atlas(lv, 0)) for lv in range(stage.levels)]
+    res, sp, origin = dev.levels[0]
+    cam = np.asarray(case.scene.camera.position) + np.array([3.0 * sp, 0.0, 0.0])
+    assert not api.recenterCascade(dev, 0, *res, sp, origin, case.scene.camera.position)
+    assert api.recenterCascade(dev, 0, *res, sp, origin, cam)
+    p0, a0 = dev.probes(0), dev.atlas(0, 0)
+    assert np.array_equal(p0["pos"], p0["resting"]) and np.all(p0["reject_history"] == 1)
+    assert np.all(p0["last_update_frame"] == -1) and not np.any(a0)
+    assert np.allclose(p0["resting"][0], api.cascadeOriginFor(cam, *res, sp))
+    for lv in range(1, stage.levels):
+        assert np.array_equal(dev.probes(lv)["pos"], before[lv][0]["pos"])
+        assert np.array_equal(dev.atlas(lv, 0), before[lv][1])

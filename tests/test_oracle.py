@@ -11,7 +11,7 @@ import sys
 import numpy as np
 import pytest
 
-from golden_util import CASES, load
+from golden_util import CASES, SCHED_CASES, load
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -44,6 +44,28 @@ def test_oracle_is_bit_exact_with_reference(name):
             pr = st.probes(level)
             ref = case.data[f"probes_p{p}_c{level}"]
             for f in ("resting", "pos", "last_pos", "alive", "reject_history", "last_update_frame"):
+                assert np.array_equal(pr[f], ref[f]), (name, p, level, f)
+            assert np.array_equal(st.atlas(level), case.data[f"atlas_p{p}_c{level}"]), (name, p, level)
+    st.close()
+
+
+@pytest.mark.parametrize("name", SCHED_CASES)
+def test_oracle_scheduler_is_bit_exact_with_reference(name):
+    """Budgeted passes: selectProbesForUpdate's refs (order included), then the
+    update of exactly those probes, bit-identical to the reference."""
+    case = load(name)
+    st = oracle_py.Stage(case.scene, cfg=case.cfg(), res=case.res, spacing=case.spacing)
+    for p, want in enumerate(case.passes):
+        st.relocate_all()
+        refs = st.select(case.budget, p)
+        assert np.array_equal(refs, case.data[f"refs_p{p}"]), (name, p)
+        md, rays, upd, stats = st.update_refs(p, refs, threads=2)
+        assert rays == want["rays_traced"] and upd == want["probes_updated"], (name, p)
+        assert [int(x) for x in stats] == [want["update_stats"][k] for k in STAT_KEYS], (name, p)
+        for level in range(st.levels):
+            pr = st.probes(level)
+            ref = case.data[f"probes_p{p}_c{level}"]
+            for f in ("pos", "alive", "reject_history", "last_update_frame"):
                 assert np.array_equal(pr[f], ref[f]), (name, p, level, f)
             assert np.array_equal(st.atlas(level), case.data[f"atlas_p{p}_c{level}"]), (name, p, level)
     st.close()
