@@ -176,6 +176,51 @@ GATHER_CASES = {
 }
 
 
+# C5 dynamic sequences: sceneAtTime + cullAndLod per frame, the probe pass on
+# persistent cascades; every frame's active scene, probes/atlas every `every` frames.
+DYNAMIC_CASES = {
+    "dyn_sphere": dict(scene=os.path.join(SCENES, "dynamic-sphere.scene"), frames=60, every=12,
+                       extra=["--nrays", 32]),
+    "dyn_light": dict(scene=os.path.join(HERE, "scenes", "dynamic-light.scene"), frames=40, every=13,
+                      extra=["--nrays", 24]),
+}
+
+
+def build_dynamic_case(name, spec):
+    d = os.path.join(OUT, name)
+    os.makedirs(d, exist_ok=True)
+    with tempfile.TemporaryDirectory() as tmp:
+        args = ["dynamic", spec["scene"], tmp, "--passes", spec["frames"], "--threads", 2, "--dump-every",
+                spec["every"], *spec["extra"]]
+        summary = json.loads(run(*args))
+        data = {}
+        for fn in sorted(os.listdir(tmp)):
+            base, ext = os.path.splitext(fn)
+            path = os.path.join(tmp, fn)
+            if ext == ".sdfa":
+                data[base] = scene_io.read_sdfa(path)[2]
+            elif base.startswith("probes"):
+                data[base] = np.fromfile(path, scene_io.PROBE_DTYPE)
+            elif ext == ".sdfs":
+                sc = scene_io.read_sdfs(path)
+                f = base.split("_")[-1]
+                data[f"prims_{f}"] = sc.prims
+                data[f"lights_{f}"] = sc.lights
+                data[f"clusters_{f}"] = sc.clusters
+                data[f"mstart_{f}"] = sc.member_start
+                data[f"midx_{f}"] = sc.member_idx
+                data[f"sky_{f}"] = sc.sky
+    with open(spec["scene"]) as f:
+        scene_text = f.read()
+    summary.update(case=name, args=[str(a) for a in args[3:]], frames_total=spec["frames"], every=spec["every"],
+                   scene_text=scene_text,
+                   generator="oracle/gen_golden.py via oracle/_ref/ref_parity dynamic (-ffp-contract=off)")
+    with open(os.path.join(d, "summary.json"), "w") as f:
+        json.dump(summary, f, indent=1)
+    np.savez_compressed(os.path.join(d, "data.npz"), **data)
+    print(name, len(data), "arrays")
+
+
 def build_gather_case(name, spec):
     d = os.path.join(OUT, name)
     os.makedirs(d, exist_ok=True)
@@ -209,9 +254,11 @@ def build_gather_case(name, spec):
 def main():
     if not os.path.exists(REF):
         sys.exit("build oracle/_ref first: make -C oracle ref")
-    names = sys.argv[1:] or list(CASES) + list(GATHER_CASES)
+    names = sys.argv[1:] or list(CASES) + list(GATHER_CASES) + list(DYNAMIC_CASES)
     for n in names:
-        if n in GATHER_CASES:
+        if n in DYNAMIC_CASES:
+            build_dynamic_case(n, DYNAMIC_CASES[n])
+        elif n in GATHER_CASES:
             build_gather_case(n, GATHER_CASES[n])
         else:
             build_case(n, CASES[n])

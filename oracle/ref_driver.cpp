@@ -318,6 +318,7 @@ struct Opts {
     int width = 0, height = 0;  // gather
     int gatherFrames = 2;
     int budget = 0;  // probeBudget for selectProbesForUpdate (0 = every probe)
+    int dumpEvery = 1;  // dynamic: probes/atlas dump period
 };
 
 void applySet(RenderConfig& c, const std::string& kv) {
@@ -363,6 +364,7 @@ Opts parseOpts(int argc, char** argv, int first) {
             o.height = std::stoi(next());
         } else if (a == "--gather-frames") o.gatherFrames = std::stoi(next());
         else if (a == "--budget") o.budget = std::stoi(next());
+        else if (a == "--dump-every") o.dumpEvery = std::stoi(next());
         else throw std::runtime_error("unknown option " + a);
     }
     return o;
@@ -586,6 +588,57 @@ void dumpImage(const std::string& path, const ImageRgb& img) {
     writeVec(path, v);
 }
 
+// C5: a dynamic sequence. Per frame f: sceneAtTime(f / fps), cullAndLod with the
+// scene's clustering (pipeline.hpp:92-103), then the probe pass of renderFrame with
+// frame index f on the persistent cascades. Dumps every frame's active scene
+// (frame<f>.sdfs) and, every --dump-every frames and on the last, probes + atlas.
+int cmdDynamic(int argc, char** argv) {
+    if (argc < 4) throw std::runtime_error("usage: dynamic <file.scene> <outdir> [opts]");
+    SceneFile f = loadSceneFile(argv[2]);
+    std::string dir = argv[3];
+    Opts o = parseOpts(argc, argv, 4);
+    Camera cam = buildCamera(f.camera);
+    auto frameScene = [&](int frame) {
+        double t = static_cast<double>(frame) / static_cast<double>(f.config.fps);
+        SceneState state = sceneAtTime(f, t);
+        ActiveScene a = cullAndLod(state.primitives, cam.position, f.lodDistances,
+                                   {f.config.maxPerCluster, f.config.mergeRadius});
+        a.lights = state.lights;
+        a.sky = state.sky;
+        a.frameIndex = frame;
+        return a;
+    };
+    Loaded L;
+    L.scene = frameScene(0);
+    L.camera = cam;
+    L.cascade = f.cascade;
+    L.cfg = f.config;
+    ProbeStage st;
+    initStage(st, L, o);
+    std::ostringstream js;
+    js << "{\"frames\": [";
+    for (int fr = 0; fr < o.passes; ++fr) {
+        st.scene = frameScene(fr);
+        std::string sfx = "_f" + std::to_string(fr);
+        if (o.dump) writeSdfs(dir + "/frame" + sfx + ".sdfs", st.scene, cam, L.cascade, st.cfg);
+        PassResult r = runPass(st, fr, o, nullptr);
+        if (o.dump && (fr % std::max(1, o.dumpEvery) == 0 || fr + 1 == o.passes)) {
+            for (size_t ci = 0; ci < st.cascades.size(); ++ci) {
+                std::string c = "_c" + std::to_string(ci);
+                writeVec(dir + "/probes" + sfx + c + ".bin", probeDump(st.cascades[ci]));
+                st.atlas[st.readIdx][ci].dump(dir + "/atlas" + sfx + c + ".sdfa");
+            }
+        }
+        if (fr) js << ", ";
+        js << "{\"frame\": " << fr << ", \"relocated\": " << r.rep.relocated << ", \"rejected\": " << r.rep.rejected
+           << ", \"dead\": " << r.rep.dead << ", \"rays_traced\": " << r.rays << ", \"probes_updated\": " << r.updated
+           << ", \"max_texel_delta\": " << r.jitter << ", \"update_ms\": " << r.updateMs << "}";
+    }
+    js << "]}";
+    std::cout << js.str() << std::endl;
+    return 0;
+}
+
 // C3: probe passes, then renderGBuffer + the gather stages of renderFrame
 // (pipeline.hpp:155-207) for --gather-frames frames against the final atlas.
 int cmdGather(int argc, char** argv) {
@@ -709,6 +762,7 @@ int main(int argc, char** argv) {
         if (cmd == "passes") return cmdPasses(argc, argv);
         if (cmd == "recluster") return cmdRecluster(argc, argv);
         if (cmd == "gather") return cmdGather(argc, argv);
+        if (cmd == "dynamic") return cmdDynamic(argc, argv);
         std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
         return 2;
     } catch (const std::exception& e) {

@@ -114,6 +114,13 @@ class ProbeStage:
         for level in range(self.levels):
             makeCascade(self.dev, *self.res, self.spacing0, level, self.scene.camera.position, oct_res)
 
+    def set_scene(self, scene: sio.Scene):
+        """A new frame's ActiveScene (e.g. scene_file.activeScene at the frame's time,
+        pipeline.hpp:92-103) for the persistent cascades: probes and atlases keep
+        their state, as in a dynamic sequence."""
+        self.scene = scene
+        self.dev.upload_scene(scene)
+
     def spacing(self, level):
         return self.spacing0 * math.pow(2.0, level)
 

@@ -55,7 +55,30 @@ def load(name):
 
 GATHER_CASES = sorted(d for d in CASES if d.startswith("gather_"))
 SCHED_CASES = sorted(d for d in CASES if d.startswith("sched_"))  # budgeted selectProbesForUpdate
-CASES = [d for d in CASES if not d.startswith(("gather_", "sched_"))]
+DYNAMIC_CASES = sorted(d for d in CASES if d.startswith("dyn_"))  # C5 sequences
+CASES = [d for d in CASES if not d.startswith(("gather_", "sched_", "dyn_"))]
+
+
+class DynamicCase:
+    """A C5 fixture: the authored scene text, every frame's active scene as the
+    reference instantiated it, probes + atlas every `every` frames and on the last."""
+
+    def __init__(self, name):
+        d = os.path.join(GOLDEN, name)
+        with open(os.path.join(d, "summary.json")) as f:
+            self.summary = json.load(f)
+        with np.load(os.path.join(d, "data.npz")) as z:
+            self.data = {k: z[k] for k in z.files}
+        self.frames = self.summary["frames"]
+        self.scene_text = self.summary["scene_text"]
+        args = self.summary["args"]
+        self.n_rays = int(args[args.index("--nrays") + 1]) if "--nrays" in args else None
+        self.dumped = sorted(int(k.split("_f")[1].split("_")[0]) for k in self.data if k.startswith("atlas_f")
+                             and k.endswith("_c0"))
+
+
+def load_dynamic(name):
+    return DynamicCase(name)
 
 
 class GatherCase:
