@@ -186,6 +186,42 @@ DYNAMIC_CASES = {
 }
 
 
+# The reference's whole frame loop (Renderer::renderFrame): composed images + metrics.
+RENDER_CASES = {
+    "render_dynsphere": dict(scene=os.path.join(SCENES, "dynamic-sphere.scene"), frames=12, size=(80, 48),
+                             extra=["--nrays", 32]),
+    "render_light": dict(scene=os.path.join(HERE, "scenes", "dynamic-light.scene"), frames=8, size=(64, 40),
+                         extra=["--nrays", 24]),
+}
+
+
+def build_render_case(name, spec):
+    d = os.path.join(OUT, name)
+    os.makedirs(d, exist_ok=True)
+    with tempfile.TemporaryDirectory() as tmp:
+        args = ["render", spec["scene"], tmp, "--passes", spec["frames"], "--threads", 2, "--size", *spec["size"],
+                *spec["extra"]]
+        summary = json.loads(run(*args))
+        data = {}
+        for fn in sorted(os.listdir(tmp)):
+            base, ext = os.path.splitext(fn)
+            path = os.path.join(tmp, fn)
+            if ext == ".sdfi":
+                data[base] = scene_io.read_sdfi(path)[2]
+                if base == "image_f0":
+                    data["image_f0_bytes"] = np.fromfile(path, np.uint8)
+        with open(os.path.join(tmp, "metrics.csv")) as f:
+            summary["metrics_csv"] = f.read()
+    with open(spec["scene"]) as f:
+        summary["scene_text"] = f.read()
+    summary.update(case=name, args=[str(a) for a in args[3:]], size=list(spec["size"]),
+                   generator="oracle/gen_golden.py via oracle/_ref/ref_parity render (Renderer::renderFrame)")
+    with open(os.path.join(d, "summary.json"), "w") as f:
+        json.dump(summary, f, indent=1)
+    np.savez_compressed(os.path.join(d, "data.npz"), **data)
+    print(name, len(data), "arrays")
+
+
 def build_dynamic_case(name, spec):
     d = os.path.join(OUT, name)
     os.makedirs(d, exist_ok=True)
@@ -254,9 +290,11 @@ def build_gather_case(name, spec):
 def main():
     if not os.path.exists(REF):
         sys.exit("build oracle/_ref first: make -C oracle ref")
-    names = sys.argv[1:] or list(CASES) + list(GATHER_CASES) + list(DYNAMIC_CASES)
+    names = sys.argv[1:] or list(CASES) + list(GATHER_CASES) + list(DYNAMIC_CASES) + list(RENDER_CASES)
     for n in names:
-        if n in DYNAMIC_CASES:
+        if n in RENDER_CASES:
+            build_render_case(n, RENDER_CASES[n])
+        elif n in DYNAMIC_CASES:
             build_dynamic_case(n, DYNAMIC_CASES[n])
         elif n in GATHER_CASES:
             build_gather_case(n, GATHER_CASES[n])

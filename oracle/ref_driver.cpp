@@ -639,6 +639,42 @@ int cmdDynamic(int argc, char** argv) {
     return 0;
 }
 
+// The whole reference frame loop: Renderer::renderFrame (pipeline.hpp:84-230) for
+// --passes frames at --size W H; per frame the composed image (writeHdr, SDFI), and
+// every FrameMetrics row (csvRow) into metrics.csv. --nrays overrides n_rays.
+int cmdRender(int argc, char** argv) {
+    if (argc < 4) throw std::runtime_error("usage: render <file.scene> <outdir> [opts]");
+    SceneFile f = loadSceneFile(argv[2]);
+    std::string dir = argv[3];
+    Opts o = parseOpts(argc, argv, 4);
+    if (o.width <= 0) throw std::runtime_error("--size W H required");
+    if (o.nRays > 0) f.config.nRaysFull = o.nRays;
+    for (auto& kv : o.sets) applySet(f.config, kv);
+    Renderer r(f, o.width, o.height, std::max(1, o.threads));
+    std::ofstream csv(dir + "/metrics.csv");
+    csv << FrameMetrics::csvHeader() << "\n";
+    std::ostringstream js;
+    js << "{\"frames\": [";
+    for (int fr = 0; fr < o.passes; ++fr) {
+        FrameMetrics m = r.renderFrame();
+        csv << m.csvRow() << "\n";
+        if (o.dump) writeHdr(r.image(), dir + "/image_f" + std::to_string(fr) + ".sdfi");
+        if (fr) js << ", ";
+        js << "{\"frame\": " << m.frame << ", \"active_primitives\": " << m.activePrimitives
+           << ", \"clusters\": " << m.clusters << ", \"probes_total\": " << m.probesTotal
+           << ", \"probes_updated\": " << m.probesUpdated << ", \"relocated\": " << m.relocated
+           << ", \"rejected\": " << m.rejected << ", \"dead\": " << m.dead
+           << ", \"vis_traces_per_pixel\": " << m.visTracesPerPixel
+           << ", \"jitter_max_texel_delta\": " << m.jitterMaxTexelDelta
+           << ", \"ms\": " << (m.tCullMs + m.tProbePosMs + m.tProbeUpdateMs + m.tGBufferMs + m.tVisibilityMs +
+                                m.tGiResolveMs + m.tContactMs + m.tComposeMs)
+           << ", \"stats\": " << statsJson(m.stats) << "}";
+    }
+    js << "]}";
+    std::cout << js.str() << std::endl;
+    return 0;
+}
+
 // C3: probe passes, then renderGBuffer + the gather stages of renderFrame
 // (pipeline.hpp:155-207) for --gather-frames frames against the final atlas.
 int cmdGather(int argc, char** argv) {
@@ -763,6 +799,7 @@ int main(int argc, char** argv) {
         if (cmd == "recluster") return cmdRecluster(argc, argv);
         if (cmd == "gather") return cmdGather(argc, argv);
         if (cmd == "dynamic") return cmdDynamic(argc, argv);
+        if (cmd == "render") return cmdRender(argc, argv);
         std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
         return 2;
     } catch (const std::exception& e) {

@@ -269,3 +269,53 @@ def write_sdfa(path, atlas: np.ndarray) -> None:
     with open(path, "wb") as f:
         f.write(b"SDFA" + struct.pack("<3I", 1, t - 2, n))
         f.write(np.ascontiguousarray(atlas, "<f4").tobytes())
+
+
+# ------------------------------------------------------------- image.hpp:49-89
+def write_sdfi(path, rgb, width, height) -> None:
+    """writeHdr: "SDFI", u32 width, u32 height, u32 channels = 3, then row-major
+    float32 triplets (each channel rounded from double as static_cast<float>)."""
+    data = np.asarray(rgb, np.float64).reshape(-1)
+    assert data.size == 3 * width * height
+    with open(path, "wb") as f:
+        f.write(b"SDFI")
+        f.write(np.array([width, height, 3], "<u4").tobytes())
+        f.write(data.astype("<f4").tobytes())
+
+
+def read_sdfi(path):
+    """readHdr -> (width, height, float32[h, w, 3])."""
+    with open(path, "rb") as f:
+        raw = f.read()
+    if raw[:4] != b"SDFI":
+        raise ValueError(f"bad SDFI file {path}")
+    w, h, ch = np.frombuffer(raw[4:16], "<u4")
+    if ch != 3:
+        raise ValueError(f"SDFI channels {ch} != 3")
+    img = np.frombuffer(raw[16:16 + 12 * int(w) * int(h)], "<f4").reshape(int(h), int(w), 3)
+    return int(w), int(h), img.copy()
+
+
+# -------------------------------------------------------- pipeline.hpp:11-42
+METRICS_FIELDS = ["frame", "active_primitives", "clusters", "probes_total", "probes_updated", "relocated",
+                  "rejected", "dead", "t_cull_ms", "t_probe_pos_ms", "t_probe_update_ms", "t_gbuffer_ms",
+                  "t_visibility_ms", "t_gi_resolve_ms", "t_contact_ms", "t_compose_ms", "vis_traces_per_pixel",
+                  "jitter_max_texel_delta"]
+
+
+def metrics_csv_header() -> str:
+    """FrameMetrics::csvHeader."""
+    return ",".join(METRICS_FIELDS)
+
+
+def _fmt_g(v, prec):
+    """printf %.<prec>g (Python's 'g' matches C's for finite values)."""
+    return f"{v:.{prec}g}"
+
+
+def metrics_csv_row(m: dict) -> str:
+    """FrameMetrics::csvRow: %d x8, %.3f x8, %.6f, %.6g."""
+    ints = [str(int(m[k])) for k in METRICS_FIELDS[:8]]
+    times = [f"{float(m[k]):.3f}" for k in METRICS_FIELDS[8:16]]
+    return ",".join(ints + times + [f"{float(m['vis_traces_per_pixel']):.6f}",
+                                    _fmt_g(float(m["jitter_max_texel_delta"]), 6)])

@@ -56,7 +56,26 @@ def load(name):
 GATHER_CASES = sorted(d for d in CASES if d.startswith("gather_"))
 SCHED_CASES = sorted(d for d in CASES if d.startswith("sched_"))  # budgeted selectProbesForUpdate
 DYNAMIC_CASES = sorted(d for d in CASES if d.startswith("dyn_"))  # C5 sequences
-CASES = [d for d in CASES if not d.startswith(("gather_", "sched_", "dyn_"))]
+RENDER_CASES = sorted(d for d in CASES if d.startswith("render_"))  # Renderer::renderFrame loops
+CASES = [d for d in CASES if not d.startswith(("gather_", "sched_", "dyn_", "render_"))]
+
+
+class RenderCase:
+    def __init__(self, name):
+        d = os.path.join(GOLDEN, name)
+        with open(os.path.join(d, "summary.json")) as f:
+            self.summary = json.load(f)
+        with np.load(os.path.join(d, "data.npz")) as z:
+            self.data = {k: z[k] for k in z.files}
+        self.frames = self.summary["frames"]
+        self.w, self.h = self.summary["size"]
+        self.scene_text = self.summary["scene_text"]
+        args = self.summary["args"]
+        self.n_rays = int(args[args.index("--nrays") + 1]) if "--nrays" in args else None
+
+
+def load_render(name):
+    return RenderCase(name)
 
 
 class DynamicCase:
