@@ -212,6 +212,42 @@ __device__ __forceinline__ R evalPrim(const DPrim<R>& pr, V3<R> p) {
     }
 }
 
+// FP64 parity mode: the per-kind branches only set up sqrt((vx*vx + vy*vy) + vz*vz)
+// + post, and the one square root every kind ends in runs after the branches have
+// reconverged (lanes of a warp evaluate mixed kinds). Bit-identical to the switch
+// above: s + (-r) is s - r, and the cylinder's + 0*0 leaves its 2-D sum unchanged.
+template <>
+__device__ __forceinline__ double evalPrim<double>(const DPrim<double>& pr, V3<double> p) {
+    V3<double> q = p - mk(pr.trans[0], pr.trans[1], pr.trans[2]);
+    if (!pr.identity) {
+        const double* m = pr.rot;  // transposeMul, vec.hpp:113-117
+        q = mk(m[0] * q.x + m[3] * q.y + m[6] * q.z, m[1] * q.x + m[4] * q.y + m[7] * q.z,
+               m[2] * q.x + m[5] * q.y + m[8] * q.z);
+    }
+    const int kind = pr.kind;
+    if (kind == 2) return q.z;  // plane
+    double vx, vy, vz, post;
+    if (kind == 1) {  // box
+        const double ax = fabs(q.x) - pr.size[0], ay = fabs(q.y) - pr.size[1], az = fabs(q.z) - pr.size[2];
+        vx = smax(ax, 0.0);
+        vy = smax(ay, 0.0);
+        vz = smax(az, 0.0);
+        post = smin(smax(ax, smax(ay, az)), 0.0);
+    } else if (kind == 3) {  // cylinder
+        const double dx = sqrt(q.x * q.x + q.y * q.y) - pr.size[0], dy = fabs(q.z) - pr.size[1];
+        vx = smax(dx, 0.0);
+        vy = smax(dy, 0.0);
+        vz = 0.0;
+        post = smin(smax(dx, dy), 0.0);
+    } else {  // sphere (0) / capsule (4)
+        vx = q.x;
+        vy = q.y;
+        vz = kind == 0 ? q.z : q.z - sclamp(q.z, -pr.size[1], pr.size[1]);
+        post = -pr.size[0];
+    }
+    return sqrt(vx * vx + vy * vy + vz * vz) + post;
+}
+
 // FP32 perf mode: the five kinds as one branch-free formula so lanes evaluating
 // different kinds do not serialise. With q = R^T (p - t):
 //   u = (radial ? |q.xy| : |q.x|) - e0,  v = radial ? -inf : |q.y| - e1,  w = |q.z| - e2
