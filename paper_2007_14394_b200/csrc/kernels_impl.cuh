@@ -296,11 +296,30 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                 active = true;
                 fresh = true;
             }
-        } else if (fetchItem(P.ctr + 0, static_cast<unsigned long long>(total), active, exhausted, item)) {
+        } else {
+            const bool got = fetchItem(P.ctr + 0, static_cast<unsigned long long>(total), active, exhausted, item);
+            int s = 0;
+            if (MODE == 0) {
+                // the warp's new items are consecutive: one lane binary-searches the
+                // first one's probe, the others step forward from it
+                const unsigned gm = __ballot_sync(kFull, got);
+                if (gm) {
+                    const int leader = __ffs(gm) - 1;
+                    const unsigned long long first = __shfl_sync(kFull, item, leader);
+                    int s0 = 0;
+                    if (static_cast<int>(threadIdx.x & 31) == leader)
+                        s0 = findCandidate(P.rayStart, P.nCand, static_cast<long long>(first));
+                    s0 = __shfl_sync(kFull, s0, leader);
+                    if (got) {
+                        s = s0;
+                        while (P.rayStart[s + 1] <= static_cast<long long>(item)) ++s;
+                    }
+                }
+            }
+            if (got) {
             R startBound = R(INFINITY);
             bool ok = true;
             if (MODE == 0) {
-                const int s = findCandidate(P.rayStart, P.nCand, static_cast<long long>(item));
                 const int j = static_cast<int>(static_cast<long long>(item) - P.rayStart[s]);
                 const int n = static_cast<int>(P.rayStart[s + 1] - P.rayStart[s]);
                 // slot j traces sample i = perm[j]: consecutive lanes get neighbouring
@@ -345,6 +364,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                 h.status = 2 << 1;
                 P.hits[rid] = h;
                 active = false;
+            }
             }
         }
         if (!__any_sync(kFull, active)) {
@@ -442,13 +462,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                     h.p[1] = p.y;
                     h.p[2] = p.z;
                     h.t = t;
-                    h.owner = owner;
-                    if (owner >= 0) {
-                        V3<R> nn = evalGradient(P.scene.prims[owner], p);
-                        h.n[0] = nn.x;
-                        h.n[1] = nn.y;
-                        h.n[2] = nn.z;
-                    }
+                    h.owner = owner;  // normal: k_hit_normals (evalGradient of the owner)
                     h.status = 1 | ((step + 1) << 8);
                 } else {
                     h.p[0] = h.p[1] = h.p[2] = R(0);
@@ -472,6 +486,22 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
         }
     }
     if (ST) flushCounters(cnt, P.stats);
+}
+
+// The converged hits' normals (evalGradient of the owner, primitives.hpp:96-108)
+// over the compacted hit list — every lane has one, instead of the few lanes of a
+// K1 warp whose rays just converged.
+template <typename R>
+__global__ void __launch_bounds__(128) k_hit_normals(WaveParams<R> P) {
+    const unsigned long long n = P.ctr[1];
+    for (unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+        HitRec<R>& h = P.hits[P.hitList[i]];
+        const V3<R> nn = evalGradient(P.scene.prims[h.owner], mk(h.p[0], h.p[1], h.p[2]));
+        h.n[0] = nn.x;
+        h.n[1] = nn.y;
+        h.n[2] = nn.z;
+    }
 }
 
 // ----------------------------------------------------------- K2 shadow rays
@@ -843,6 +873,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
     static int b3 = persistentBlocks(k_shade_rays<R, ST>, 128, 0);
     k_trace_primary<R, ST, 0, 0><<<cap > 0 ? min(cap, b1) : b1, kWaveThreads, 0, st>>>(p);
     k_trace_primary<R, ST, 0, 1><<<cap > 0 ? min(cap, b1f) : b1f, kWaveThreads, 0, st>>>(p);
+    k_hit_normals<R><<<b3, 128, 0, st>>>(p);
     k_trace_shadow<R, ST, 0><<<cap > 0 ? min(cap, b2) : b2, kWaveThreads, 0, st>>>(p);
     k_trace_shadow<R, ST, 1><<<cap > 0 ? min(cap, b2f) : b2f, kWaveThreads, 0, st>>>(p);
     k_shade_rays<R, ST><<<b3, 128, 0, st>>>(p);
@@ -853,7 +884,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
         k3<<<p.nCand, kConvThreads, smem, st>>>(p);
     }
     if (e1) cudaEventRecord(e1, st);
-    if (launches) *launches += p.debug ? 7 : 8;
+    if (launches) *launches += p.debug ? 8 : 9;
 }
 
 // contactGI's per-pixel sum (shading.hpp:686-713): AO from the missed samples,
@@ -910,12 +941,13 @@ static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long*
     static int b3 = persistentBlocks(k_shade_rays<R, ST>, 128, 0);
     k_trace_primary<R, ST, 1, 0><<<b1, kWaveThreads, 0, st>>>(p);
     k_trace_primary<R, ST, 1, 1><<<b1f, kWaveThreads, 0, st>>>(p);
+    k_hit_normals<R><<<b3, 128, 0, st>>>(p);
     k_trace_shadow<R, ST, 0><<<b2, kWaveThreads, 0, st>>>(p);
     k_trace_shadow<R, ST, 1><<<b2f, kWaveThreads, 0, st>>>(p);
     k_shade_rays<R, ST><<<b3, 128, 0, st>>>(p);
     const long long np = static_cast<long long>(p.gw) * p.gh;
     k_contact_combine<R><<<static_cast<int>((np + 127) / 128), 128, 0, st>>>(p);
-    if (launches) *launches += 6;
+    if (launches) *launches += 7;
 }
 
 // composeFrame (shading.hpp:480-504) as a wavefront: every geometry pixel becomes a
