@@ -218,8 +218,8 @@ struct GridBuildParams {
     double* U;
     int* counts;
     const int* start;
-    int* list;
-    float* lkey;  // per entry: lower bound of the candidate's SDF over the cell
+    int* list;    // scratch: the cell's candidates while they are sorted
+    int2* entry;  // per entry: (float bits of the candidate's SDF lower bound over the cell, CSR position)
     int maxList;  // longer lists keep the nearest maxList + a sentinel (list = -1)
 };
 

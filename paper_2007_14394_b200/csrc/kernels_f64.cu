@@ -114,12 +114,9 @@ __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells
         }
         return lb;
     };
-    for (int a = 0; a < m; ++a) P.lkey[out + a] = bound(key(L[a]));
-    if (truncated) {
-        // sentinel: a query still open here walks the cluster hierarchy
-        L[m] = -1;
-        P.lkey[out + m] = bound(tail);
-    }
+    for (int a = 0; a < m; ++a) P.entry[out + a] = make_int2(__float_as_int(bound(key(L[a]))), L[a]);
+    if (truncated)  // sentinel: a query still open here walks the cluster hierarchy
+        P.entry[out + m] = make_int2(__float_as_int(bound(tail)), -1);
 }
 
 void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st) {

@@ -136,11 +136,11 @@ struct GridDev {
     int dim[3];
     int bvhRoot;    // code of the root (see BNode); meaningless when nBounded == 0
     const int* __restrict__ start;  // ncells + 1
-    const int* __restrict__ list;
-    // per list entry: a lower bound on that primitive's SDF anywhere in the cell
-    // (box distance to the cell centre - padded half diagonal, rounded down);
-    // entries are sorted by it, so a query stops at the first bound > its minimum
-    const float* __restrict__ lkey;
+    // per list entry, one 8-byte load: x = the bits of a float lower bound on that
+    // primitive's SDF anywhere in the cell (box distance to the cell centre - padded
+    // half diagonal, rounded down), y = its CSR position (-1: sentinel). Entries are
+    // sorted by the bound, so a query stops at the first bound > its minimum.
+    const int2* __restrict__ entry;
     const BNode* __restrict__ bvh;
     const int* __restrict__ unbounded;  // cluster ids of the unbounded clusters
     int nUnbounded;
@@ -331,7 +331,7 @@ __device__ __forceinline__ void visitMembers(const SceneView<R>& s, int k, V3<R>
 // An SDF query in flight: the point, the running minimum/owner, and (inside the
 // candidate grid) the cursor over the cell's candidate list. queryBegin either
 // sets the cursor or — off the grid, or with the grid disabled — completes the
-// whole query at once; queryStep evaluates one candidate. Splitting the query
+// whole query at once; query() then walks the cell list. Splitting the query
 // lets the persistent kernels interleave one evaluation per loop iteration with
 // per-lane ray state, so a lane whose query ends early moves on instead of
 // waiting for the slowest lane of its warp.
@@ -452,32 +452,10 @@ __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R ini
     q.walk = true;
 }
 
-// One candidate of the cell list (lowest-CSR-position tie-break: order-free). A
-// truncated list ends in a sentinel (-1) whose bound covers every omitted candidate;
-// a query still open there completes through the cluster hierarchy.
-template <typename R, bool ST>
-__device__ __forceinline__ void queryStep(const SceneView<R>& s, QueryState<R>& q, Counters* c) {
-    if (R(s.grid.lkey[q.cur]) > q.d) {  // this and every later candidate is farther
-        q.cur = q.end;
-        return;
-    }
-    const int j = s.grid.list[q.cur++];
-    if (j < 0) {
-        q.walk = true;
-        q.cur = q.end;
-        return;
-    }
-    if (ST) {
-        ++c->ek[s.kindId[j] & 0xff];
-        c->ek[5] += (s.kindId[j] >> 8) ? 0 : 1;
-    }
-    const R pd = evalPrim(s.prims[j], q.p);
-    if (pd < q.d || (pd == q.d && q.own >= 0 && j < q.own)) {
-        q.d = pd;
-        q.own = j;
-    }
-}
-
+// The cell list walk (lowest-CSR-position tie-break: order-free), with the next
+// entry loaded while the current candidate is evaluated. A truncated list ends in
+// a sentinel (-1) whose bound covers every omitted candidate; a query still open
+// there completes through the cluster hierarchy.
 template <typename R, bool ST>
 __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int* owner, Counters* c, int seed = -1) {
     QueryState<R> q;
@@ -496,7 +474,32 @@ __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int*
             q.own = seed;
         }
     }
-    while (q.cur < q.end) queryStep<R, ST>(s, q, c);
+    if (q.cur < q.end) {
+        int2 e = __ldg(&s.grid.entry[q.cur]);
+        while (true) {
+            if (R(__int_as_float(e.x)) > q.d) break;  // this and every later candidate is farther
+            ++q.cur;
+            const bool more = q.cur < q.end;
+            int2 en = make_int2(0, -1);
+            if (more) en = __ldg(&s.grid.entry[q.cur]);
+            const int j = e.y;
+            if (j < 0) {
+                q.walk = true;
+                break;
+            }
+            if (ST) {
+                ++c->ek[s.kindId[j] & 0xff];
+                c->ek[5] += (s.kindId[j] >> 8) ? 0 : 1;
+            }
+            const R pd = evalPrim(s.prims[j], q.p);
+            if (pd < q.d || (pd == q.d && q.own >= 0 && j < q.own)) {
+                q.d = pd;
+                q.own = j;
+            }
+            if (!more) break;
+            e = en;
+        }
+    }
     if (q.walk) hierarchyWalk<R, ST>(s, q, c);
     if (owner) *owner = q.own;
     return q.d;

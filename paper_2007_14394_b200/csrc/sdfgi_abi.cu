@@ -136,7 +136,7 @@ struct Ctx {
     GridDev grid{};
     long long gridEntries = 0;
     DBuf<int> gridStart, gridList, gridCounts;
-    DBuf<float> gridKey;
+    DBuf<int2> gridEntry;
     DBuf<double> gridU, primBox;
     DBuf<BNode> bvh;
     DBuf<int> unbList;
@@ -190,7 +190,7 @@ struct Ctx {
         if (stream) cudaStreamSynchronize(stream);
         prim64.free(); prim32.free(); cl64.free(); cl32.free(); cstart.free(); orig.free();
         albedo.free(); emission.free(); lights.free(); kindId.free();
-        gridStart.free(); gridList.free(); gridCounts.free(); gridU.free(); gridKey.free();
+        gridStart.free(); gridList.free(); gridCounts.free(); gridU.free(); gridEntry.free();
         bvh.free(); unbList.free(); primBox.free();
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
@@ -535,8 +535,8 @@ void buildGrid(Ctx* c) {
     start[ncells] = static_cast<int>(total);
     c->gridStart.upload(start.data(), start.size(), c->stream);
     c->gridList.alloc(std::max<long long>(total, 1));
-    c->gridKey.alloc(std::max<long long>(total, 1));
-    p.lkey = c->gridKey.p;
+    c->gridEntry.alloc(std::max<long long>(total, 1));
+    p.entry = c->gridEntry.p;
     p.start = c->gridStart.p;
     p.list = c->gridList.p;
     launch_grid_list(p, static_cast<int>(ncells), true, c->stream);
@@ -552,8 +552,7 @@ void buildGrid(Ctx* c) {
     for (int a = 0; a < 3; ++a) c->grid.flo[a] = static_cast<float>(lo[a]);
     c->grid.finvH = static_cast<float>(1.0 / h);
     c->grid.start = c->gridStart.p;
-    c->grid.list = c->gridList.p;
-    c->grid.lkey = c->gridKey.p;
+    c->grid.entry = c->gridEntry.p;
     c->gridEntries = total;
 
     // BVH over the bounded clusters for points off the grid: median split of the
