@@ -363,6 +363,9 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                 h.owner = -1;
                 h.status = 2 << 1;
                 P.hits[rid] = h;
+                P.rad[3 * rid] = R(P.scene.sky[0]);
+                P.rad[3 * rid + 1] = R(P.scene.sky[1]);
+                P.rad[3 * rid + 2] = R(P.scene.sky[2]);
                 active = false;
             }
             }
@@ -470,6 +473,11 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                     h.status = ((done == 2 ? 1 : 2) << 1) | ((done == 2 ? step + 1 : maxSteps) << 8);
                 }
                 P.hits[rid] = h;
+                if (!(done == 1 && owner >= 0)) {  // shadeHit's miss branch: K3a shades only the hit list
+                    P.rad[3 * rid] = R(P.scene.sky[0]);
+                    P.rad[3 * rid + 1] = R(P.scene.sky[1]);
+                    P.rad[3 * rid + 2] = R(P.scene.sky[2]);
+                }
                 active = false;
             }
             // compaction of converged hits with an owner (the only ones shadeHit lights)
@@ -714,9 +722,13 @@ __device__ __forceinline__ V3<double> shadeRay(const WaveParams<R>& P, const Hit
 // footprint does not cap the convolution's occupancy.
 template <typename R, bool ST>
 __global__ void __launch_bounds__(128, WaveOcc<R>::shade) k_shade_rays(WaveParams<R> P) {
-    const long long total = rayTotal(P);
+    // the compacted hit list (misses got the sky radiance in K1); every ray when
+    // per-ray debug records are written
+    const bool all = P.debug != 0;
+    const long long total = all ? rayTotal(P) : static_cast<long long>(P.ctr[1]);
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-    for (long long rid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; rid < total; rid += stride) {
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const long long rid = all ? i : static_cast<long long>(P.hitList[i]);
         const HitRec<R> h = P.hits[rid];
         const V3<double> L = shadeRay(P, h, static_cast<unsigned long long>(rid));
         P.rad[3 * rid] = R(L.x);
