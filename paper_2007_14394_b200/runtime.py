@@ -260,14 +260,14 @@ class Device:
         a = np.ascontiguousarray(rgb, np.float64).reshape(-1)
         _call("sdfgi_indirect_upload", self._ctx, _ptr(a), a.size)
 
-    def compose(self, cfg, stats=False):
+    def compose(self, cfg, stats=False, download=True):
         """composeFrame (shading.hpp:480-504) on the context's G-buffer and indirect
-        image; returns (image[w*h*3], device ms[, stats])."""
+        image; returns (image[w*h*3] or None, device ms[, stats])."""
         c = np.ascontiguousarray(cfg, sio.CFG_DTYPE)
         st = np.zeros(1, sio.STATS_DTYPE) if stats else None
         ms = np.zeros(1)
         _call("sdfgi_compose", self._ctx, _ptr(c), _ptr(st), _ptr(ms))
-        img = self.gather_buffer("composed")
+        img = self.gather_buffer("composed") if download else None
         return (img, float(ms[0]), st[0]) if stats else (img, float(ms[0]))
 
     def gather_buffer(self, name):
