@@ -77,6 +77,39 @@ def ncu_step_traffic(precision):
     return total, os.path.relpath(files[-1], ROOT)
 
 
+HBM_KERNELS = ("k_convolve", "k_downsample", "k_select", "k_resolve", "k_contact_combine", "k_compose")
+
+
+def ncu_hbm_kernels(precision, hbm_peak):
+    """Achieved DRAM GB/s of the memory-side kernels (atlas blend, gather stages)
+    from the committed ncu launch list: (read + write bytes) / duration per launch,
+    averaged over launches (cold-cache, serialised: a lower bound on the bench's)."""
+    import csv
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r01_step_launches_{precision}_v*.csv")))
+    if not files:
+        return None
+    rows = [r for r in csv.reader(open(files[-1])) if len(r) > 10]
+    h = rows[0]
+    ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
+    per = {}
+    for r in rows[1:]:
+        name = next((k for k in HBM_KERNELS if k in r[ki]), None)
+        if name is None:
+            continue
+        d = per.setdefault(name, {}).setdefault(r[ii], {})
+        d[r[mi]] = float(r[vi].replace(",", ""))
+    out = {}
+    for name, launches in per.items():
+        gbs = [(v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0)) / v["gpu__time_duration.sum"]
+               for v in launches.values() if v.get("gpu__time_duration.sum")]
+        if gbs:
+            a = sum(gbs) / len(gbs)
+            out[name] = {"achieved_gbs": a, "peak_gbs": hbm_peak, "frac": a / hbm_peak, "launches": len(gbs)}
+    return {"source": os.path.relpath(files[-1], ROOT), "kernels": out}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -295,6 +328,7 @@ def run_ours(args, rank, world, local_rank):
         "update_kernel_ms_per_step": kern_ms,
         "kernel_share_of_step": kern_ms / ms_step,
     }
+    hbm_peak = float(load_peaks().get("hbm_gbs", 7700.0))
     line = {
         "metric": METRIC,
         "value": value,
@@ -324,6 +358,7 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "roofline": roofline,
+        "roofline_hbm_kernels": ncu_hbm_kernels(args.precision, hbm_peak),
         "clocks": clk.summary(),
         "algorithmic_counters_step": work_all,
         "gather_c3": gather,
