@@ -698,7 +698,8 @@ __device__ __forceinline__ V3<double> directLight(const WaveParams<R>& P, const 
 }
 
 template <typename R>
-__device__ __forceinline__ V3<double> shadeRay(const WaveParams<R>& P, const HitRec<R>& h, unsigned long long rid) {
+__device__ __forceinline__ V3<double> shadeRay(const WaveParams<R>& P, const HitRec<R>& h, unsigned long long rid,
+                                               R* slab = nullptr) {
     const SceneView<R>& s = P.scene;
     if (!(h.status & 1) || h.owner < 0) return mk(s.sky[0], s.sky[1], s.sky[2]);
     const V3<double> total = directLight(P, h, rid);
@@ -710,7 +711,8 @@ __device__ __forceinline__ V3<double> shadeRay(const WaveParams<R>& P, const Hit
         V3<double> prev;
         V3<double> hp = mk<double>(h.p[0], h.p[1], h.p[2]);
         V3<double> hn = mk<double>(h.n[0], h.n[1], h.n[2]);
-        if (sampleBounceIrradiance<R>(P.pc.cas, P.pc.nCas, P.pc.probes, P.prevAtlas, P.oct, hp, hn, P.tc.mvcFrac, &prev))
+        if (sampleBounceIrradiance<R>(P.pc.cas, P.pc.nCas, P.pc.probes, P.prevAtlas, P.oct, hp, hn, P.tc.mvcFrac, &prev,
+                                      slab))
             radiance = radiance + brdf * (prev * P.tc.bounceCoeff);
     }
     return radiance;
@@ -724,13 +726,15 @@ template <typename R, bool ST>
 __global__ void __launch_bounds__(128, WaveOcc<R>::shade) k_shade_rays(WaveParams<R> P) {
     // the compacted hit list (misses got the sky radiance in K1); every ray when
     // per-ray debug records are written
+    extern __shared__ __align__(16) unsigned char k3aSmem[];
+    R* slab = reinterpret_cast<R*>(k3aSmem);  // kMvcSlab values per thread (MVC working set)
     const bool all = P.debug != 0;
     const long long total = all ? rayTotal(P) : static_cast<long long>(P.ctr[1]);
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
         const long long rid = all ? i : static_cast<long long>(P.hitList[i]);
         const HitRec<R> h = P.hits[rid];
-        const V3<double> L = shadeRay(P, h, static_cast<unsigned long long>(rid));
+        const V3<double> L = shadeRay(P, h, static_cast<unsigned long long>(rid), slab);
         P.rad[3 * rid] = R(L.x);
         P.rad[3 * rid + 1] = R(L.y);
         P.rad[3 * rid + 2] = R(L.z);
@@ -861,11 +865,11 @@ __global__ void __launch_bounds__(kConvThreads) k_convolve(WaveParams<R> P) {
 }
 
 template <typename K>
-static int persistentBlocks(K kernel, int threads, int cap) {
+static int persistentBlocks(K kernel, int threads, int cap, size_t smem = 0) {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
     int b = sms * (per > 0 ? per : 1);
     return cap > 0 ? min(b, cap) : b;
 }
@@ -882,13 +886,13 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
     static int b1f = persistentBlocks(k_trace_primary<R, ST, 0, 1>, kWaveThreads, 0);
     static int b2 = persistentBlocks(k_trace_shadow<R, ST, 0>, kWaveThreads, 0);
     static int b2f = persistentBlocks(k_trace_shadow<R, ST, 1>, kWaveThreads, 0);
-    static int b3 = persistentBlocks(k_shade_rays<R, ST>, 128, 0);
+    static int b3 = persistentBlocks(k_shade_rays<R, ST>, 128, 0, 128 * kMvcSlab * sizeof(R));
     k_trace_primary<R, ST, 0, 0><<<cap > 0 ? min(cap, b1) : b1, kWaveThreads, 0, st>>>(p);
     k_trace_primary<R, ST, 0, 1><<<cap > 0 ? min(cap, b1f) : b1f, kWaveThreads, 0, st>>>(p);
     k_hit_normals<R><<<b3, 128, 0, st>>>(p);
     k_trace_shadow<R, ST, 0><<<cap > 0 ? min(cap, b2) : b2, kWaveThreads, 0, st>>>(p);
     k_trace_shadow<R, ST, 1><<<cap > 0 ? min(cap, b2f) : b2f, kWaveThreads, 0, st>>>(p);
-    k_shade_rays<R, ST><<<b3, 128, 0, st>>>(p);
+    k_shade_rays<R, ST><<<b3, 128, 128 * kMvcSlab * sizeof(R), st>>>(p);
     if (!p.debug) {
         const size_t smem = static_cast<size_t>(2 * p.nRaysFull) * 6 * sizeof(R);
         auto k3 = k_convolve<R, ST>;
@@ -950,13 +954,13 @@ static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long*
     static int b1f = persistentBlocks(k_trace_primary<R, ST, 1, 1>, kWaveThreads, 0);
     static int b2 = persistentBlocks(k_trace_shadow<R, ST, 0>, kWaveThreads, 0);
     static int b2f = persistentBlocks(k_trace_shadow<R, ST, 1>, kWaveThreads, 0);
-    static int b3 = persistentBlocks(k_shade_rays<R, ST>, 128, 0);
+    static int b3 = persistentBlocks(k_shade_rays<R, ST>, 128, 0, 128 * kMvcSlab * sizeof(R));
     k_trace_primary<R, ST, 1, 0><<<b1, kWaveThreads, 0, st>>>(p);
     k_trace_primary<R, ST, 1, 1><<<b1f, kWaveThreads, 0, st>>>(p);
     k_hit_normals<R><<<b3, 128, 0, st>>>(p);
     k_trace_shadow<R, ST, 0><<<b2, kWaveThreads, 0, st>>>(p);
     k_trace_shadow<R, ST, 1><<<b2f, kWaveThreads, 0, st>>>(p);
-    k_shade_rays<R, ST><<<b3, 128, 0, st>>>(p);
+    k_shade_rays<R, ST><<<b3, 128, 128 * kMvcSlab * sizeof(R), st>>>(p);
     const long long np = static_cast<long long>(p.gw) * p.gh;
     k_contact_combine<R><<<static_cast<int>((np + 127) / 128), 128, 0, st>>>(p);
     if (launches) *launches += 7;

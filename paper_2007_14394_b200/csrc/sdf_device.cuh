@@ -683,26 +683,57 @@ template <> __device__ __forceinline__ float mvcAsin<float>(float v) { return as
 template <typename M> __device__ __forceinline__ M mvcDiv(M a, M b) { return a / b; }
 template <> __device__ __forceinline__ float mvcDiv<float>(float a, float b) { return __fdividef(a, b); }
 
+// The MVC working set (8 distances, unit vectors and weight sums, indexed by the
+// triangle corners) lives in per-thread local memory, or — for kernels that pass
+// a shared-memory slab (kMvcSlab values per thread, thread-interleaved) — in
+// shared memory, which keeps it out of the local-memory traffic of a
+// register-capped kernel.
+template <typename M, bool SH>
+struct MvcArrays;
 template <typename M>
-__device__ inline bool mvcWeightsHex(const V3<double>* corners, V3<double> xd, double* weights) {
+struct MvcArrays<M, false> {
+    M ld[8], lx[8], ly[8], lz[8], lw[8];
+    __device__ MvcArrays(M*) {}
+    __device__ M& dist(int i) { return ld[i]; }
+    __device__ M& ux(int i) { return lx[i]; }
+    __device__ M& uy(int i) { return ly[i]; }
+    __device__ M& uz(int i) { return lz[i]; }
+    __device__ M& wts(int i) { return lw[i]; }
+};
+template <typename M>
+struct MvcArrays<M, true> {
+    M* b;  // this thread's column of the slab
+    int s;
+    __device__ explicit MvcArrays(M* slab) : b(slab + threadIdx.x), s(blockDim.x) {}
+    __device__ M& dist(int i) { return b[i * s]; }
+    __device__ M& ux(int i) { return b[(8 + i) * s]; }
+    __device__ M& uy(int i) { return b[(16 + i) * s]; }
+    __device__ M& uz(int i) { return b[(24 + i) * s]; }
+    __device__ M& wts(int i) { return b[(32 + i) * s]; }
+};
+constexpr int kMvcSlab = 40;  // values per thread in a shared slab
+
+template <typename M, bool SH>
+__device__ inline bool mvcWeightsHexImpl(const V3<double>* corners, V3<double> xd, double* weights, M* slab) {
     const int faces[6][4] = {{0, 2, 3, 1}, {4, 5, 7, 6}, {0, 1, 5, 4}, {2, 6, 7, 3}, {0, 4, 6, 2}, {1, 3, 7, 5}};
     const M eps = M(1e-10);
     const M pi = M(kPi);
-    M wts[8];
-    for (int i = 0; i < 8; ++i) wts[i] = M(0);
+    MvcArrays<M, SH> a(slab);
+    for (int i = 0; i < 8; ++i) a.wts(i) = M(0);
     for (int i = 0; i < 8; ++i) weights[i] = 0.0;
-    M dist[8];
-    V3<M> unit[8];
     const V3<M> x = mk(M(xd.x), M(xd.y), M(xd.z));
     for (int i = 0; i < 8; ++i) {
         V3<M> v = mk(M(corners[i].x), M(corners[i].y), M(corners[i].z)) - x;
-        dist[i] = length(v);
-        if (dist[i] < eps) {
+        const M di = length(v);
+        a.dist(i) = di;
+        if (di < eps) {
             weights[i] = 1.0;
             return true;
         }
-        const M inv = mvcDiv(M(1), dist[i]);
-        unit[i] = mk(v.x * inv, v.y * inv, v.z * inv);
+        const M inv = mvcDiv(M(1), di);
+        a.ux(i) = v.x * inv;
+        a.uy(i) = v.y * inv;
+        a.uz(i) = v.z * inv;
     }
     bool any = false;
 #pragma unroll 1
@@ -714,8 +745,8 @@ __device__ inline bool mvcWeightsHex(const V3<double>* corners, V3<double> xd, d
             M d[3], sa[3], ca[3], theta[3], st[3];
             V3<M> u[3];
             for (int i = 0; i < 3; ++i) {
-                d[i] = dist[tri[i]];
-                u[i] = unit[tri[i]];
+                d[i] = a.dist(tri[i]);
+                u[i] = mk(a.ux(tri[i]), a.uy(tri[i]), a.uz(tri[i]));
             }
             for (int i = 0; i < 3; ++i) {
                 const M l = length(u[(i + 1) % 3] - u[(i + 2) % 3]);
@@ -765,17 +796,23 @@ __device__ inline bool mvcWeightsHex(const V3<double>* corners, V3<double> xd, d
             for (int i = 0; i < 3; ++i) {
                 const int j = (i + 1) % 3, k = (i + 2) % 3;
                 const M w = mvcDiv(theta[i] - c[j] * theta[k] - c[k] * theta[j], d[i] * st[j] * sv[k]);
-                wts[tri[i]] += w;
+                a.wts(tri[i]) += w;
                 any = true;
             }
         }
     }
     if (!any) return false;
     M total = 0;
-    for (int i = 0; i < 8; ++i) total += wts[i];
+    for (int i = 0; i < 8; ++i) total += a.wts(i);
     if (fabs(total) < eps || !isfinite(total)) return false;
-    for (int i = 0; i < 8; ++i) weights[i] = double(wts[i] / total);
+    for (int i = 0; i < 8; ++i) weights[i] = double(a.wts(i) / total);
     return true;
+}
+
+template <typename M>
+__device__ inline bool mvcWeightsHex(const V3<double>* corners, V3<double> xd, double* weights, M* slab = nullptr) {
+    return slab ? mvcWeightsHexImpl<M, true>(corners, xd, weights, slab)
+                : mvcWeightsHexImpl<M, false>(corners, xd, weights, slab);
 }
 
 struct Stencil {
@@ -791,7 +828,7 @@ struct Stencil {
 // double in both modes; MVC in precision M)
 template <typename M = double>
 __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, const ProbesView& pv, V3<double> point,
-                                        double mvcFrac) {
+                                        double mvcFrac, M* slab = nullptr) {
     Stencil st;
     st.count = 0;
     st.sky = 0;
@@ -842,7 +879,7 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
     bool wantMvc = maxDisp > mvcFrac * c.spacing || boundary;
     bool haveMvc = false;
     if (wantMvc) {
-        haveMvc = mvcWeightsHex<M>(corners, point, w);
+        haveMvc = mvcWeightsHex<M>(corners, point, w, slab);
         if (haveMvc) {
             for (int k = 0; k < 8; ++k) w[k] = smax(0.0, w[k]);
             st.usedMvc = 1;
@@ -878,9 +915,9 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
 template <typename M = double>
 __device__ inline bool sampleBounceIrradiance(const CascadeDev* cas, int nCas, const ProbesView& pv,
                                        const float* atlas, int oct, V3<double> pos, V3<double> normal,
-                                       double mvcFrac, V3<double>* out) {
+                                       double mvcFrac, V3<double>* out, M* slab = nullptr) {
     if (nCas <= 0) return false;
-    Stencil st = interpolationStencil<M>(cas, nCas, pv, pos, mvcFrac);
+    Stencil st = interpolationStencil<M>(cas, nCas, pv, pos, mvcFrac, slab);
     if (st.sky || st.count == 0) return false;
     const CascadeDev& c = cas[st.cascade];
     double wsum = 0;
