@@ -461,7 +461,7 @@ void buildGrid(Ctx* c) {
     // It also covers the probe volumes (the hint box grown by sdfgi_cascade_set):
     // probes above an open scene would otherwise query off the grid every step.
     const char* menv = std::getenv("SDFGI_GRID_MARGIN");
-    const double marginFrac = menv ? std::atof(menv) : 0.3;  // measured on C2: 0.02 -> 0.3 = -23% K1+K2
+    const double marginFrac = menv ? std::atof(menv) : 0.6;  // C2 sweep (profiles/README.md): 0.3 -> 0.6 with 8M cells = -9%
     for (int a = 0; a < 3; ++a) {
         double e = hi[a] - lo[a];
         double m = marginFrac * e + 1e-3;
@@ -475,9 +475,10 @@ void buildGrid(Ctx* c) {
         scale = std::max(scale, std::max(std::fabs(lo[a]), std::fabs(hi[a])));
     }
     const char* env = std::getenv("SDFGI_GRID_CELLS");
-    // finer cells -> smaller U -> shorter, more uniform candidate lists; measured on
-    // C2 (pass 0, FP32): 262k cells 75 ms, 2M cells 60 ms, 8M cells 67 ms
-    double target = env ? std::atof(env) : 2097152.0;
+    // finer cells -> smaller U -> shorter, more uniform candidate lists (and tighter
+    // per-entry bounds); measured on C2 with the current kernels (pass 0, FP64, warm):
+    // 2M cells 17.4 ms, 4M 16.6, 8M 15.9 (margin 0.6)
+    double target = env ? std::atof(env) : 8388608.0;
     if (target < 1) return;
     double h = std::cbrt(ext[0] * ext[1] * ext[2] / target);
     int dim[3];
