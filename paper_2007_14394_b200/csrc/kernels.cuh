@@ -254,8 +254,15 @@ constexpr int kWaveThreads = 128;   // K1/K2 persistent CTAs
 #ifndef SDFGI_SHADE_MINB
 #define SDFGI_SHADE_MINB 4
 #endif
+#ifndef SDFGI_SHADOW_MINB64
+#define SDFGI_SHADOW_MINB64 SDFGI_WAVE_MINB64
+#endif
+#ifndef SDFGI_SHADOW_MINB32
+#define SDFGI_SHADOW_MINB32 SDFGI_WAVE_MINB32
+#endif
 template <typename R> struct WaveOcc {
     static constexpr int trace = sizeof(R) == 8 ? SDFGI_WAVE_MINB64 : SDFGI_WAVE_MINB32;
+    static constexpr int shadow = sizeof(R) == 8 ? SDFGI_SHADOW_MINB64 : SDFGI_SHADOW_MINB32;
     static constexpr int shade = SDFGI_SHADE_MINB;
 };
 constexpr int kShadeThreads = 128;  // per-ray shading

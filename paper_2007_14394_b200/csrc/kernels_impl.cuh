@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(128) k_hit_normals(WaveParams<R> P) {
 // one query per iteration. vis = 1 when the segment is too short to trace.
 // PHASE 0 / 1 as in K1: off-grid shadow marches are parked and resumed together.
 template <typename R, bool ST, int PHASE>
-__global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_shadow(WaveParams<R> P) {
+__global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shadow(WaveParams<R> P) {
     const int L = P.scene.n_lights;
     const unsigned long long nHits = P.ctr[1];
     ParkShadow<R>* const park = reinterpret_cast<ParkShadow<R>*>(P.park);
