@@ -141,6 +141,8 @@ struct Ctx {
     DBuf<BNode> bvh;
     DBuf<int> unbList;
     double gridBox[6] = {0, 0, 0, 0, 0, 0};  // region the cells cover
+    uint64_t gridHash = 0;                     // geometry the grid/BVH were built for
+    int gridAccel = -1;
     bool hintValid = false;
     double hint[6] = {0, 0, 0, 0, 0, 0};     // probe volumes the grid must cover
     // host copy of the uploaded scene (the grid is rebuilt when the hint grows)
@@ -977,10 +979,31 @@ int sdfgi_scene_upload(void* ctx, const sdfgi_prim* prims, int n_prims, const sd
         c->nLights = n_lights;
         for (int k = 0; k < 3; ++k) c->sky[k] = sky[k];
         c->haveScene = true;
+        // the acceleration structures are a function of the geometry alone: an
+        // upload of the same primitives and clusters (a static scene, re-sent every
+        // frame) keeps the grid and BVH instead of rebuilding them
+        uint64_t hsh = 1469598103934665603ull;
+        auto mix = [&hsh](const void* p, size_t n) {
+            const unsigned char* b = static_cast<const unsigned char*>(p);
+            for (size_t i = 0; i < n; ++i) hsh = (hsh ^ b[i]) * 1099511628211ull;
+        };
+        mix(prims, sizeof(sdfgi_prim) * static_cast<size_t>(n_prims));
+        mix(clusters, sizeof(sdfgi_cluster) * static_cast<size_t>(n_clusters));
+        mix(member_start, sizeof(int32_t) * (static_cast<size_t>(n_clusters) + (n_clusters ? 1 : 0)));
+        mix(member_idx, sizeof(int32_t) * static_cast<size_t>(nMembers));
+        for (const char* k : {"SDFGI_GRID_MARGIN", "SDFGI_GRID_CELLS", "SDFGI_GRID_MAXLIST", "SDFGI_GRID_HINT"}) {
+            const char* v = std::getenv(k);  // the grid's build parameters
+            mix(v ? v : "-", v ? std::strlen(v) : 1);
+        }
+        const bool same = c->haveGrid && c->gridHash == hsh && c->gridAccel == c->accel;
         c->hPrims.assign(prims, prims + n_prims);
         c->hMember.assign(member_idx, member_idx + nMembers);
         c->hClusters.assign(clusters, clusters + n_clusters);
-        buildGrid(c);
+        if (!same) {
+            buildGrid(c);
+            c->gridHash = hsh;
+            c->gridAccel = c->accel;
+        }
     });
 }
 
