@@ -896,7 +896,11 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
     if (!p.debug) {
         const size_t smem = static_cast<size_t>(2 * p.nRaysFull) * 6 * sizeof(R);
         auto k3 = k_convolve<R, ST>;
-        if (smem > 48 * 1024) cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        // dynamic + static shared memory above the 48 KB default needs the opt-in
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, k3);
+        if (smem + fa.sharedSizeBytes > 48 * 1024)
+            cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         k3<<<p.nCand, kConvThreads, smem, st>>>(p);
     }
     if (e1) cudaEventRecord(e1, st);

@@ -714,14 +714,8 @@ def buildCamera(spec: CameraSpec) -> sio.Camera:
     return sio.Camera(np.array(pos), np.array(f), np.array(r), np.array(u), float(spec.fovY))
 
 
-def activeScene(s: SceneFile, time: float, cameraPos=None) -> sio.Scene:
-    """The frame's ActiveScene as an SDFS image: sceneAtTime + cullAndLod
-    (pipeline.hpp:95-103) with the scene's clustering parameters."""
-    cam = buildCamera(s.camera)
-    state = sceneAtTime(s, time)
-    cp = cam.position if cameraPos is None else cameraPos
-    prims, clusters = cullAndLod(state.primitives, cp, s.lodDistances, int(s.config["max_per_cluster"][0]),
-                                 float(s.config["merge_radius"][0]))
+def packScene(prims, clusters, lights, sky, camera, cascade, cfg) -> sio.Scene:
+    """An ActiveScene (primitives + buildClusters output) as an SDFS image."""
     pr = np.zeros(len(prims), sio.PRIM_DTYPE)
     for i, p in enumerate(prims):
         pr[i]["id"], pr[i]["kind"], pr[i]["lod_tier"] = p.id, p.kind, p.lodTier
@@ -734,5 +728,16 @@ def activeScene(s: SceneFile, time: float, cameraPos=None) -> sio.Scene:
         cl[k]["lo"], cl[k]["hi"], cl[k]["unbounded"] = lo, hi, 1 if unb else 0
         idx.extend(members)
         start.append(len(idx))
-    return sio.Scene(pr, state.lights, cl, np.array(start, np.int32), np.array(idx, np.int32),
-                     np.array(state.sky, np.float64), cam, s.cascade, s.config.copy())
+    return sio.Scene(pr, lights, cl, np.array(start, np.int32), np.array(idx, np.int32),
+                     np.array(sky, np.float64), camera, cascade, np.array(cfg, sio.CFG_DTYPE).reshape(1).copy())
+
+
+def activeScene(s: SceneFile, time: float, cameraPos=None) -> sio.Scene:
+    """The frame's ActiveScene as an SDFS image: sceneAtTime + cullAndLod
+    (pipeline.hpp:95-103) with the scene's clustering parameters."""
+    cam = buildCamera(s.camera)
+    state = sceneAtTime(s, time)
+    cp = cam.position if cameraPos is None else cameraPos
+    prims, clusters = cullAndLod(state.primitives, cp, s.lodDistances, int(s.config["max_per_cluster"][0]),
+                                 float(s.config["merge_radius"][0]))
+    return packScene(prims, clusters, state.lights, state.sky, cam, s.cascade, s.config)
