@@ -70,6 +70,11 @@ template <typename R> struct __align__(16) ParkRay {
     unsigned long long rid;
     int seed, pad;  // last known nearest primitive (query seed of the far phase)
 };
+// A Contact GI ray prepared by k_contact_setup (tMax < 0: sky pixel, no ray).
+template <typename R> struct __align__(16) ContactRay {
+    R o[3], dir[3];
+    R tMax, startBound;
+};
 // The same for a shadow march of K2.
 template <typename R> struct __align__(16) ParkShadow {
     R o[3], dir[3];
@@ -110,6 +115,7 @@ template <typename R> struct WaveParams {
     // (null: no parking). K1 and K2 reuse the buffer (K1's far phase ends first).
     void* park;
     unsigned long long parkBytes;
+    void* cray;  // contact batch: the prepared rays (ContactRay<R>), or null
     // results
     unsigned long long* stats;       // counters or null
     unsigned long long* maxDeltaBits;

@@ -246,6 +246,33 @@ __device__ __forceinline__ bool contactRay(const WaveParams<R>& P, long long ite
     return true;
 }
 
+// Every contact ray's setup (RNG draws, cosine-hemisphere direction, origin) at
+// full lane occupancy, ahead of K1: in K1 only the few refilling lanes of a warp
+// would run it.
+template <typename R>
+__global__ void __launch_bounds__(256) k_contact_setup(WaveParams<R> P) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= P.nRaysDirect) return;
+    ContactRay<R> r;
+    V3<R> o, dir;
+    R tMax = R(0), sb = R(0);
+    if (contactRay(P, i, o, dir, tMax, sb)) {
+        r.o[0] = o.x;
+        r.o[1] = o.y;
+        r.o[2] = o.z;
+        r.dir[0] = dir.x;
+        r.dir[1] = dir.y;
+        r.dir[2] = dir.z;
+        r.tMax = tMax;
+        r.startBound = sb;
+    } else {
+        r.o[0] = r.o[1] = r.o[2] = r.dir[0] = r.dir[1] = r.dir[2] = R(0);
+        r.tMax = R(-1);
+        r.startBound = R(0);
+    }
+    reinterpret_cast<ContactRay<R>*>(P.cray)[i] = r;
+}
+
 // Warp-aggregated slot in a parking buffer (all 32 lanes call; -1 = not parked).
 __device__ __forceinline__ long long parkSlot(unsigned long long* counter, bool park) {
     const unsigned m = __ballot_sync(kFull, park);
@@ -334,7 +361,16 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                 tMax = R(P.tc.rayTMax);
             } else {
                 rid = item;
-                ok = contactRay(P, static_cast<long long>(item), o, dir, tMax, startBound);
+                if (P.cray) {
+                    const ContactRay<R> r = reinterpret_cast<const ContactRay<R>*>(P.cray)[item];
+                    o = mk(r.o[0], r.o[1], r.o[2]);
+                    dir = mk(r.dir[0], r.dir[1], r.dir[2]);
+                    tMax = r.tMax;
+                    startBound = r.startBound;
+                    ok = r.tMax >= R(0);
+                } else {
+                    ok = contactRay(P, static_cast<long long>(item), o, dir, tMax, startBound);
+                }
             }
             t = R(0);
             lastD = startBound * R(0.5);
@@ -954,6 +990,7 @@ __global__ void __launch_bounds__(128) k_contact_combine(WaveParams<R> P) {
 template <typename R, bool ST>
 static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long* launches) {
     cudaMemsetAsync(p.ctr, 0, 8 * sizeof(unsigned long long), st);
+    if (p.cray) k_contact_setup<R><<<static_cast<int>((p.nRaysDirect + 255) / 256), 256, 0, st>>>(p);
     static int b1 = persistentBlocks(k_trace_primary<R, ST, 1, 0>, kWaveThreads, 0);
     static int b1f = persistentBlocks(k_trace_primary<R, ST, 1, 1>, kWaveThreads, 0);
     static int b2 = persistentBlocks(k_trace_shadow<R, ST, 0>, kWaveThreads, 0);
@@ -967,7 +1004,7 @@ static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long*
     k_shade_rays<R, ST><<<b3, 128, 128 * kMvcSlab * sizeof(R), st>>>(p);
     const long long np = static_cast<long long>(p.gw) * p.gh;
     k_contact_combine<R><<<static_cast<int>((np + 127) / 128), 128, 0, st>>>(p);
-    if (launches) *launches += 7;
+    if (launches) *launches += p.cray ? 8 : 7;
 }
 
 // composeFrame (shading.hpp:480-504) as a wavefront: every geometry pixel becomes a

@@ -171,7 +171,7 @@ struct Ctx {
     DBuf<double> wRot, fib;
     DBuf<int> perm;
     int fibN = -1;
-    DBuf<unsigned char> wHits, wVis, wRad, wPark;
+    DBuf<unsigned char> wHits, wVis, wRad, wPark, wCRay;
     DBuf<unsigned long long> wCtr;
     int persistCap = 0;  // 0 = occupancy-sized persistent grids
     // gather (e): G-buffer, stage buffers, history (pipeline.hpp:213-218)
@@ -198,7 +198,7 @@ struct Ctx {
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
         wRayCount.free(); wHitList.free(); wRayStart.free(); wRot.free(); fib.free(); wHits.free();
-        wVis.free(); wPark.free(); wCtr.free(); perm.free(); wRad.free();
+        wVis.free(); wPark.free(); wCRay.free(); wCtr.free(); perm.free(); wRad.free();
         gbuf.free(); halfDepth.free(); sparseIrr.free(); resolved.free(); indirect.free(); histIrr.free(); composed.free();
         histDepth.free(); halfSrc.free(); sel.free(); sparseValid.free(); sparseAnchor.free();
         for (auto& e : gev)
@@ -1560,6 +1560,7 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     reserve(c->wRad, cap * 3 * sizeof(R));
     reserve(c->wCtr, 8);
     reservePark<R>(c, cap, L);
+    reserve(c->wCRay, cap * sizeof(ContactRay<R>));
     WaveParams<R> p;
     std::memset(&p, 0, sizeof(p));
     p.scene = c->sceneView<R>();
@@ -1583,6 +1584,7 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     p.parkBytes = p.park ? c->wPark.n : 0;
     p.stats = c->scratch.p;
     p.nRaysDirect = nr;
+    p.cray = c->wCRay.p;
     p.gb = c->gbuf.p;
     p.gw = c->gw;
     p.gh = c->gh;
