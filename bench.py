@@ -254,7 +254,7 @@ def run_ours(args, rank, world, local_rank):
             if stats:
                 res, st = r
                 work = dev.last_work()
-                ops += workmodel.update_ops(st, work, int(res["rays_traced"]))
+                ops += workmodel.update_ops(st, work, int(res["rays_traced"]), shading=dev.last_shading_work())
                 work_all.append((dict(zip(st.dtype.names, map(int, st))), [int(w) for w in work]))
             else:
                 res = r

@@ -281,6 +281,10 @@ SDFGI_API int sdfgi_last_kernel_ms(void* ctx, double* update_ms, double* relocat
  * PrimitiveKind (sphere, box, plane, cylinder, capsule) and [5] how many of them
  * were rotated: with sdfgi_stats these define the algorithmic work. */
 SDFGI_API int sdfgi_last_work(void* ctx, uint64_t out[6]);
+/* Shading work of the last stats-enabled sdfgi_probes_update: {shadeHit calls
+ * (converged hits with an owner), mvcWeightsHex evaluations} — the W_stencil
+ * term of the algorithmic-work model. */
+SDFGI_API int sdfgi_last_shading_work(void* ctx, uint64_t out[2]);
 
 /* FP pipe throughput microbenchmark on the context's device: FP64 and FP32 fused
  * multiply-add instructions per second (the roofline denominators for the tracing

@@ -735,7 +735,7 @@ __device__ __forceinline__ V3<double> directLight(const WaveParams<R>& P, const 
 
 template <typename R>
 __device__ __forceinline__ V3<double> shadeRay(const WaveParams<R>& P, const HitRec<R>& h, unsigned long long rid,
-                                               R* slab = nullptr) {
+                                               R* slab = nullptr, int* usedMvc = nullptr) {
     const SceneView<R>& s = P.scene;
     if (!(h.status & 1) || h.owner < 0) return mk(s.sky[0], s.sky[1], s.sky[2]);
     const V3<double> total = directLight(P, h, rid);
@@ -748,7 +748,7 @@ __device__ __forceinline__ V3<double> shadeRay(const WaveParams<R>& P, const Hit
         V3<double> hp = mk<double>(h.p[0], h.p[1], h.p[2]);
         V3<double> hn = mk<double>(h.n[0], h.n[1], h.n[2]);
         if (sampleBounceIrradiance<R>(P.pc.cas, P.pc.nCas, P.pc.probes, P.prevAtlas, P.oct, hp, hn, P.tc.mvcFrac, &prev,
-                                      slab))
+                                      slab, usedMvc))
             radiance = radiance + brdf * (prev * P.tc.bounceCoeff);
     }
     return radiance;
@@ -767,10 +767,16 @@ __global__ void __launch_bounds__(128, WaveOcc<R>::shade) k_shade_rays(WaveParam
     const bool all = P.debug != 0;
     const long long total = all ? rayTotal(P) : static_cast<long long>(P.ctr[1]);
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    unsigned long long nShaded = 0, nMvc = 0;  // shading work (ST): shadeHit calls, MVC evaluations
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
         const long long rid = all ? i : static_cast<long long>(P.hitList[i]);
         const HitRec<R> h = P.hits[rid];
-        const V3<double> L = shadeRay(P, h, static_cast<unsigned long long>(rid), slab);
+        int mvc = 0;
+        const V3<double> L = shadeRay(P, h, static_cast<unsigned long long>(rid), slab, ST ? &mvc : nullptr);
+        if (ST && (h.status & 1) && h.owner >= 0) {
+            ++nShaded;
+            nMvc += mvc;
+        }
         P.rad[3 * rid] = R(L.x);
         P.rad[3 * rid + 1] = R(L.y);
         P.rad[3 * rid + 2] = R(L.z);
@@ -796,6 +802,16 @@ __global__ void __launch_bounds__(128, WaveOcc<R>::shade) k_shade_rays(WaveParam
             r.prim_index = h.owner >= 0 ? P.scene.orig[h.owner] : -1;
             r.steps = h.status >> 8;
             P.records[rid] = r;
+        }
+    }
+    if (ST) {  // every lane reaches here (the grid-stride loop has no early return)
+        for (int o = 16; o > 0; o >>= 1) {
+            nShaded += __shfl_xor_sync(kFull, nShaded, o);
+            nMvc += __shfl_xor_sync(kFull, nMvc, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (nShaded) atomicAdd(P.stats + 20, nShaded);
+            if (nMvc) atomicAdd(P.stats + 21, nMvc);
         }
     }
 }

@@ -915,9 +915,10 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
 template <typename M = double>
 __device__ inline bool sampleBounceIrradiance(const CascadeDev* cas, int nCas, const ProbesView& pv,
                                        const float* atlas, int oct, V3<double> pos, V3<double> normal,
-                                       double mvcFrac, V3<double>* out, M* slab = nullptr) {
+                                       double mvcFrac, V3<double>* out, M* slab = nullptr, int* usedMvc = nullptr) {
     if (nCas <= 0) return false;
     Stencil st = interpolationStencil<M>(cas, nCas, pv, pos, mvcFrac, slab);
+    if (usedMvc) *usedMvc = st.usedMvc;
     if (st.sky || st.count == 0) return false;
     const CascadeDev& c = cas[st.cascade];
     double wsum = 0;

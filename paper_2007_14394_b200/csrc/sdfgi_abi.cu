@@ -162,6 +162,7 @@ struct Ctx {
     // [17] rays, [18] probes updated
     DBuf<unsigned long long> scratch;
     unsigned long long lastWork[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long shadeWork[2] = {0, 0};
     DBuf<int> report;
     DBuf<int> refs;
     DBuf<RayRecord> records;
@@ -641,6 +642,8 @@ void readCounters(Ctx* c, sdfgi_stats* stats, unsigned long long* tail, int ntai
     CK(cudaStreamSynchronize(c->stream));
     if (stats) {
         for (int i = 0; i < 6; ++i) c->lastWork[i] = h[8 + i];
+        c->shadeWork[0] = h[20];  // shadeHit calls, MVC evaluations (K3a)
+        c->shadeWork[1] = h[21];
         stats->sdf_queries += h[0];
         stats->clusters_visited += h[1];
         stats->clusters_skipped += h[2];
@@ -1467,6 +1470,15 @@ int sdfgi_last_kernel_ms(void* ctx, double* update_ms, double* relocate_ms) {
         if (c->evReloc) CK(cudaEventElapsedTime(&b, c->ev[2], c->ev[3]));
         if (update_ms) *update_ms = a;
         if (relocate_ms) *relocate_ms = b;
+    });
+}
+
+int sdfgi_last_shading_work(void* ctx, uint64_t out[2]) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(out, SDFGI_ERR_INVALID, "null out");
+        out[0] = c->shadeWork[0];
+        out[1] = c->shadeWork[1];
     });
 }
 

@@ -54,6 +54,7 @@ _SIGS = {
     "sdfgi_query_points": [_P, _P, _P, _I, _P, _P],
     "sdfgi_last_kernel_ms": [_P, _P, _P],
     "sdfgi_last_work": [_P, _P],
+    "sdfgi_last_shading_work": [_P, _P],
     "sdfgi_measure_fp_peak": [_P, _P, _P],
     "sdfgi_set_accel": [_P, _I],
     "sdfgi_accel_info": [_P, _P],
@@ -200,6 +201,12 @@ class Device:
         a, b = ctypes.c_double(), ctypes.c_double()
         _call("sdfgi_last_kernel_ms", self._ctx, ctypes.byref(a), ctypes.byref(b))
         return a.value, b.value
+
+    def last_shading_work(self):
+        """(shadeHit calls, MVC evaluations) of the last stats-enabled update."""
+        out = np.zeros(2, np.uint64)
+        _call("sdfgi_last_shading_work", self._ctx, _ptr(out))
+        return int(out[0]), int(out[1])
 
     def last_work(self):
         """Evaluations by kind (sphere, box, plane, cylinder, capsule, rotated) of the last
