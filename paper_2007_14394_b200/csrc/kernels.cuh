@@ -227,7 +227,15 @@ struct GridBuildParams {
     int* list;    // scratch: the cell's candidates while they are sorted
     int2* entry;  // per entry: (float bits of the candidate's SDF lower bound over the cell, CSR position)
     int maxList;  // longer lists keep the nearest maxList + a sentinel (list = -1)
+    // bricks of kBrick^3 cells: the clusters any of the brick's cells can list
+    // (a superset of every cell's, ascending cluster order), so a cell scans its
+    // brick's clusters instead of all of them
+    int bdim[3];
+    int* bCounts;
+    const int* bStart;
+    int* bList;
 };
+constexpr int kBrick = 4;
 
 // Launch the whole wavefront for one batch (K0..K3) on `st`. `persistBlocks` sizes
 // the persistent K1/K2 grids; `ev` (optional, 2 events) brackets K1..K3.
@@ -247,6 +255,9 @@ void launch_relocate(const RelocParams& p, int nProbes, bool stats, cudaStream_t
 void launch_query_points(const QueryParams& p, cudaStream_t st);
 void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st);
 void launch_grid_list(const GridBuildParams& p, int ncells, bool fill, cudaStream_t st);
+void launch_brick_clusters(const GridBuildParams& p, int nbricks, bool fill, cudaStream_t st);
+// exclusive prefix sum of n ints on the device (CUB); temp == null: returns the bytes needed
+size_t scan_ints(const int* in, int* out, int n, void* temp, size_t tempBytes, cudaStream_t st);
 
 constexpr int kWaveThreads = 128;   // K1/K2 persistent CTAs
 // minimum resident K1/K2/K3a CTAs per SM (register cap = 64K / (128 * n)); the

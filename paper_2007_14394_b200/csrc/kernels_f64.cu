@@ -28,6 +28,47 @@ __global__ void __launch_bounds__(128) k_grid_bound(GridBuildParams P, int ncell
     P.U[cell] = f + half * (1.0 + 1e-12) + P.margin;
 }
 
+__global__ void __launch_bounds__(128) k_brick_clusters(GridBuildParams P, int nbricks, int fill) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nbricks) return;
+    const int bx = b % P.bdim[0], by = (b / P.bdim[0]) % P.bdim[1], bz = b / (P.bdim[0] * P.bdim[1]);
+    const int c0[3] = {bx * kBrick, by * kBrick, bz * kBrick};
+    int c1[3];
+    for (int a = 0; a < 3; ++a) c1[a] = min(c0[a] + kBrick, P.dim[a]);
+    // the largest cell reach in the brick, and the union of its padded cells
+    double rmax = 0.0;
+    for (int z = c0[2]; z < c1[2]; ++z)
+        for (int y = c0[1]; y < c1[1]; ++y)
+            for (int x = c0[0]; x < c1[0]; ++x)
+                rmax = fmax(rmax, fmax(P.U[x + P.dim[0] * (y + P.dim[1] * z)], 0.0));
+    const double r = rmax + P.margin;
+    const double r2 = isinf(r) ? INFINITY : r * r;
+    double lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = P.lo[a] + c0[a] * P.h - P.pad;
+        hi[a] = P.lo[a] + c1[a] * P.h + P.pad;
+    }
+    int n = 0;
+    const int out = fill ? P.bStart[b] : 0;
+    for (int k = 0; k < P.scene.n_clusters; ++k) {
+        const DCluster<double>& cl = P.scene.clusters[k];
+        bool keep = cl.unbounded != 0;
+        if (!keep) {
+            double g2 = 0;
+            for (int a = 0; a < 3; ++a) {
+                double g = fmax(fmax(cl.lo[a] - hi[a], lo[a] - cl.hi[a]), 0.0);
+                g2 += g * g;
+            }
+            keep = g2 <= r2;
+        }
+        if (keep) {
+            if (fill) P.bList[out + n] = k;
+            ++n;
+        }
+    }
+    if (!fill) P.bCounts[b] = n;
+}
+
 __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells, int fill) {
     const int cell = blockIdx.x * blockDim.x + threadIdx.x;
     if (cell >= ncells) return;
@@ -46,8 +87,10 @@ __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells
     };
     // candidate PRIMITIVES: every member of an unbounded cluster, and members of
     // nearby clusters whose own conservative box is within r of the cell
+    const int brick = ix / kBrick + P.bdim[0] * (iy / kBrick + P.bdim[1] * (iz / kBrick));
     auto forEach = [&](auto&& f) {
-        for (int k = 0; k < P.scene.n_clusters; ++k) {
+        for (int i = P.bStart[brick]; i < P.bStart[brick + 1]; ++i) {  // ascending cluster order
+            const int k = P.bList[i];
             const DCluster<double>& cl = P.scene.clusters[k];
             if (!cl.unbounded && gap2(cl.lo, cl.hi) > r2) continue;
             for (int j = P.scene.cstart[k]; j < P.scene.cstart[k + 1]; ++j) {
@@ -121,6 +164,9 @@ __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells
 
 void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st) {
     k_grid_bound<<<(ncells + 127) / 128, 128, 0, st>>>(p, ncells);
+}
+void launch_brick_clusters(const GridBuildParams& p, int nbricks, bool fill, cudaStream_t st) {
+    k_brick_clusters<<<(nbricks + 127) / 128, 128, 0, st>>>(p, nbricks, fill ? 1 : 0);
 }
 void launch_grid_list(const GridBuildParams& p, int ncells, bool fill, cudaStream_t st) {
     k_grid_list<<<(ncells + 127) / 128, 128, 0, st>>>(p, ncells, fill ? 1 : 0);

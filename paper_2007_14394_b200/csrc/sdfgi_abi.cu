@@ -137,6 +137,8 @@ struct Ctx {
     long long gridEntries = 0;
     DBuf<int> gridStart, gridList, gridCounts;
     DBuf<int2> gridEntry;
+    DBuf<int> brickCounts, brickStart, brickList;
+    DBuf<unsigned char> scanTemp;
     DBuf<double> gridU, primBox;
     DBuf<BNode> bvh;
     DBuf<int> unbList;
@@ -193,7 +195,7 @@ struct Ctx {
         if (stream) cudaStreamSynchronize(stream);
         prim64.free(); prim32.free(); cl64.free(); cl32.free(); cstart.free(); orig.free();
         albedo.free(); emission.free(); lights.free(); kindId.free();
-        gridStart.free(); gridList.free(); gridCounts.free(); gridU.free(); gridEntry.free();
+        gridStart.free(); gridList.free(); gridCounts.free(); gridU.free(); gridEntry.free(); brickCounts.free(); brickStart.free(); brickList.free(); scanTemp.free();
         bvh.free(); unbList.free(); primBox.free();
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
@@ -494,71 +496,6 @@ void buildGrid(Ctx* c) {
         ncells *= dim[a];
     }
     REQ(ncells < (1LL << 26), SDFGI_ERR_INVALID, "candidate grid too large");
-    GridBuildParams p;
-    std::memset(&p, 0, sizeof(p));
-    p.scene = c->sceneView<double>();
-    p.scene.useGrid = 0;  // the bound kernel uses the exact flat walk
-    for (int a = 0; a < 3; ++a) {
-        p.lo[a] = lo[a];
-        p.dim[a] = dim[a];
-    }
-    p.h = h;
-    // pad the cells for FP32 point->cell rounding; slack covers every rounding on the way
-    p.pad = 1e-4 * h + 4e-6 * scale;
-    p.margin = 1e-5 * (scale + 1.0);
-    // cells far from the geometry would list every primitive within their (large)
-    // bound; lists keep the maxList nearest plus a sentinel carrying the omitted
-    // candidates' lower bound (a query that cannot stop there walks the hierarchy)
-    const char* lenv = std::getenv("SDFGI_GRID_MAXLIST");
-    p.maxList = lenv ? std::max(8, std::atoi(lenv)) : 96;
-    c->gridU.alloc(ncells);
-    c->gridCounts.alloc(ncells);
-    c->gridStart.alloc(ncells + 1);
-    {
-        std::vector<double> boxes(6 * static_cast<size_t>(c->nPrims));
-        for (int j = 0; j < c->nPrims; ++j) primAabb(prims[member_idx[j]], &boxes[6 * static_cast<size_t>(j)]);
-        c->primBox.upload(boxes.data(), boxes.size(), c->stream);
-    }
-    p.primBox = c->primBox.p;
-    p.U = c->gridU.p;
-    p.counts = c->gridCounts.p;
-    launch_grid_bound(p, static_cast<int>(ncells), c->stream);
-    checkLaunch(c);
-    launch_grid_list(p, static_cast<int>(ncells), false, c->stream);
-    checkLaunch(c);
-    std::vector<int> counts(ncells);
-    CK(cudaMemcpyAsync(counts.data(), c->gridCounts.p, ncells * 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    std::vector<int> start(ncells + 1);
-    long long total = 0;
-    for (long long i = 0; i < ncells; ++i) {
-        start[i] = static_cast<int>(total);
-        total += counts[i];
-        REQ(total < (1LL << 30), SDFGI_ERR_INVALID, "candidate lists too large");
-    }
-    start[ncells] = static_cast<int>(total);
-    c->gridStart.upload(start.data(), start.size(), c->stream);
-    c->gridList.alloc(std::max<long long>(total, 1));
-    c->gridEntry.alloc(std::max<long long>(total, 1));
-    p.entry = c->gridEntry.p;
-    p.start = c->gridStart.p;
-    p.list = c->gridList.p;
-    launch_grid_list(p, static_cast<int>(ncells), true, c->stream);
-    checkLaunch(c);
-    CK(cudaStreamSynchronize(c->stream));
-    for (int a = 0; a < 3; ++a) {
-        c->grid.lo[a] = lo[a];
-        c->grid.dim[a] = dim[a];
-        c->gridBox[a] = lo[a];
-        c->gridBox[3 + a] = lo[a] + dim[a] * h;
-    }
-    c->grid.invH = 1.0 / h;
-    for (int a = 0; a < 3; ++a) c->grid.flo[a] = static_cast<float>(lo[a]);
-    c->grid.finvH = static_cast<float>(1.0 / h);
-    c->grid.start = c->gridStart.p;
-    c->grid.entry = c->gridEntry.p;
-    c->gridEntries = total;
-
     // BVH over the bounded clusters for points off the grid: median split of the
     // box centres along the widest axis (depth <= ceil(log2 n) < kBvhStack), one
     // cluster per leaf. Child boxes are padded like the FP32 cluster boxes and
@@ -633,6 +570,99 @@ void buildGrid(Ctx* c) {
     c->grid.nBounded = static_cast<int>(ids.size());
     c->grid.unbounded = c->unbList.p;
     c->grid.nUnbounded = static_cast<int>(unb.size());
+    GridBuildParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.scene = c->sceneView<double>();
+    // the bound kernel's exact queries walk the BVH: a grid of no cells puts every
+    // point "off the grid"
+    p.scene.useGrid = 1;
+    p.scene.grid = c->grid;
+    for (int a = 0; a < 3; ++a) p.scene.grid.dim[a] = 0;
+    p.scene.grid.invH = 0.0;
+    p.scene.grid.finvH = 0.f;
+    for (int a = 0; a < 3; ++a) {
+        p.lo[a] = lo[a];
+        p.dim[a] = dim[a];
+    }
+    p.h = h;
+    // pad the cells for FP32 point->cell rounding; slack covers every rounding on the way
+    p.pad = 1e-4 * h + 4e-6 * scale;
+    p.margin = 1e-5 * (scale + 1.0);
+    // cells far from the geometry would list every primitive within their (large)
+    // bound; lists keep the maxList nearest plus a sentinel carrying the omitted
+    // candidates' lower bound (a query that cannot stop there walks the hierarchy)
+    const char* lenv = std::getenv("SDFGI_GRID_MAXLIST");
+    p.maxList = lenv ? std::max(8, std::atoi(lenv)) : 96;
+    c->gridU.alloc(ncells);
+    c->gridCounts.alloc(ncells + 1);  // [ncells] = 0: the exclusive scan's last entry is the total
+    c->gridStart.alloc(ncells + 1);
+    CK(cudaMemsetAsync(c->gridCounts.p + ncells, 0, 4, c->stream));
+    {
+        std::vector<double> boxes(6 * static_cast<size_t>(c->nPrims));
+        for (int j = 0; j < c->nPrims; ++j) primAabb(prims[member_idx[j]], &boxes[6 * static_cast<size_t>(j)]);
+        c->primBox.upload(boxes.data(), boxes.size(), c->stream);
+    }
+    p.primBox = c->primBox.p;
+    p.U = c->gridU.p;
+    p.counts = c->gridCounts.p;
+    launch_grid_bound(p, static_cast<int>(ncells), c->stream);
+    checkLaunch(c);
+    // bricks of kBrick^3 cells and their candidate clusters
+    long long nbricks = 1;
+    for (int a = 0; a < 3; ++a) {
+        p.bdim[a] = (dim[a] + kBrick - 1) / kBrick;
+        nbricks *= p.bdim[a];
+    }
+    c->brickCounts.alloc(nbricks + 1);
+    c->brickStart.alloc(nbricks + 1);
+    CK(cudaMemsetAsync(c->brickCounts.p + nbricks, 0, 4, c->stream));
+    p.bCounts = c->brickCounts.p;
+    launch_brick_clusters(p, static_cast<int>(nbricks), false, c->stream);
+    checkLaunch(c);
+    // device prefix sums; only the totals come back to the host
+    auto deviceScan = [&](const int* in, int* out, long long n) {
+        const size_t need = scan_ints(in, out, static_cast<int>(n), nullptr, 0, c->stream);
+        if (c->scanTemp.n < std::max<size_t>(need, 1)) c->scanTemp.alloc(std::max<size_t>(need, 1));
+        scan_ints(in, out, static_cast<int>(n), c->scanTemp.p, c->scanTemp.n, c->stream);
+        int tot = 0;
+        CK(cudaMemcpyAsync(&tot, out + n - 1, 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return static_cast<long long>(tot);
+    };
+    {
+        const long long bt = deviceScan(c->brickCounts.p, c->brickStart.p, nbricks + 1);
+        REQ(bt >= 0 && bt < (1LL << 30), SDFGI_ERR_INVALID, "brick cluster lists too large");
+        c->brickList.alloc(std::max<long long>(bt, 1));
+    }
+    p.bStart = c->brickStart.p;
+    p.bList = c->brickList.p;
+    launch_brick_clusters(p, static_cast<int>(nbricks), true, c->stream);
+    checkLaunch(c);
+    launch_grid_list(p, static_cast<int>(ncells), false, c->stream);
+    checkLaunch(c);
+    const long long total = deviceScan(c->gridCounts.p, c->gridStart.p, ncells + 1);
+    REQ(total >= 0 && total < (1LL << 30), SDFGI_ERR_INVALID, "candidate lists too large");
+    c->gridList.alloc(std::max<long long>(total, 1));
+    c->gridEntry.alloc(std::max<long long>(total, 1));
+    p.entry = c->gridEntry.p;
+    p.start = c->gridStart.p;
+    p.list = c->gridList.p;
+    launch_grid_list(p, static_cast<int>(ncells), true, c->stream);
+    checkLaunch(c);
+    CK(cudaStreamSynchronize(c->stream));
+    for (int a = 0; a < 3; ++a) {
+        c->grid.lo[a] = lo[a];
+        c->grid.dim[a] = dim[a];
+        c->gridBox[a] = lo[a];
+        c->gridBox[3 + a] = lo[a] + dim[a] * h;
+    }
+    c->grid.invH = 1.0 / h;
+    for (int a = 0; a < 3; ++a) c->grid.flo[a] = static_cast<float>(lo[a]);
+    c->grid.finvH = static_cast<float>(1.0 / h);
+    c->grid.start = c->gridStart.p;
+    c->grid.entry = c->gridEntry.p;
+    c->gridEntries = total;
+
     c->haveGrid = true;
 }
 

@@ -10,6 +10,7 @@
 // as std::stable_sort does. Only the selected (cascade, index) pairs go back to
 // the host (budget x 8 bytes).
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
 #include "kernels.cuh"
@@ -109,6 +110,14 @@ int launch_select(const SelectParams& P, int budget, cudaStream_t st, long long*
     if (n > 0) k_select_emit<<<(n + 255) / 256, 256, 0, st>>>(P, P.idsF2, P.idsO2, P.counts, n);
     if (launches) *launches += 4 + (counts[0] > 0) + (counts[0] < n && counts[1] > 0) + (n > 0);
     return n;
+}
+
+size_t scan_ints(const int* in, int* out, int n, void* temp, size_t tempBytes, cudaStream_t st) {
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, in, out, n, st);
+    if (temp == nullptr) return need;
+    cub::DeviceScan::ExclusiveSum(temp, tempBytes, in, out, n, st);
+    return need;
 }
 
 }  // namespace sdfgi_dev
