@@ -482,8 +482,8 @@ void buildGrid(Ctx* c) {
     const char* env = std::getenv("SDFGI_GRID_CELLS");
     // finer cells -> smaller U -> shorter, more uniform candidate lists (and tighter
     // per-entry bounds); measured on C2 with the current kernels (pass 0, FP64, warm):
-    // 2M cells 17.4 ms, 4M 16.6, 8M 15.9 (margin 0.6)
-    double target = env ? std::atof(env) : 8388608.0;
+    // 2M cells 17.4 ms, 4M 16.6, 8M 15.9, 16M 15.5, 24M 15.3 (margin 0.6)
+    double target = env ? std::atof(env) : 16777216.0;
     if (target < 1) return;
     double h = std::cbrt(ext[0] * ext[1] * ext[2] / target);
     int dim[3];
