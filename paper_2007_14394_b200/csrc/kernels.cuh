@@ -100,6 +100,7 @@ template <typename R> struct WaveParams {
     int nCand;
     int* rayCount;            // per candidate (K0)
     long long* rayStart;      // nCand + 1 exclusive prefix (K0 scan)
+    int* chunkSlot;           // per 32-ray chunk c: the candidate holding ray 32c (K0)
     double* rot;              // 9 per candidate
     const double* fib;        // sphericalFibonacci table: n=N (N xyz) then n=2N (2N xyz)
     const int* perm;          // coherent trace order of the sample indices: n=N then n=2N

@@ -174,6 +174,17 @@ __global__ void __launch_bounds__(kScanThreads) k_ray_scan(WaveParams<R> P) {
     if (threadIdx.x == kScanThreads - 1) P.rayStart[n] = warpSums[31];
 }
 
+// The candidate of every 32-ray chunk's first ray, so K1's refill finds a ray's
+// probe with at most a step or two instead of a binary search on one lane: the
+// candidate whose range holds ray 32c writes chunk c.
+template <typename R>
+__global__ void __launch_bounds__(128) k_ray_chunks(WaveParams<R> P) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= P.nCand) return;
+    const long long b = P.rayStart[s], e = P.rayStart[s + 1];
+    for (long long c = (b + 31) >> 5; (c << 5) < e; ++c) P.chunkSlot[c] = s;
+}
+
 // sphericalFibonacci(i, n), sampling.hpp:11-17 — one table per ray count.
 static __global__ void k_fib_table(double* out, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -334,8 +345,10 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                     const int leader = __ffs(gm) - 1;
                     const unsigned long long first = __shfl_sync(kFull, item, leader);
                     int s0 = 0;
-                    if (static_cast<int>(threadIdx.x & 31) == leader)
-                        s0 = findCandidate(P.rayStart, P.nCand, static_cast<long long>(first));
+                    if (static_cast<int>(threadIdx.x & 31) == leader) {
+                        s0 = P.chunkSlot[first >> 5];
+                        while (P.rayStart[s0 + 1] <= static_cast<long long>(first)) ++s0;
+                    }
                     s0 = __shfl_sync(kFull, s0, leader);
                     if (got) {
                         s = s0;
@@ -932,6 +945,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
     if (p.nCand <= 0) return;
     k_ray_setup<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
     k_ray_scan<R><<<1, kScanThreads, 0, st>>>(p);
+    k_ray_chunks<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
     cudaMemsetAsync(p.ctr, 0, 8 * sizeof(unsigned long long), st);
     if (e0) cudaEventRecord(e0, st);
     static int b1 = persistentBlocks(k_trace_primary<R, ST, 0, 0>, kWaveThreads, 0);
@@ -956,7 +970,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
         k3<<<p.nCand, kConvThreads, smem, st>>>(p);
     }
     if (e1) cudaEventRecord(e1, st);
-    if (launches) *launches += p.debug ? 8 : 9;
+    if (launches) *launches += p.debug ? 9 : 10;
 }
 
 // contactGI's per-pixel sum (shading.hpp:686-713): AO from the missed samples,

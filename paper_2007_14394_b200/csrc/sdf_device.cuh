@@ -74,13 +74,15 @@ __device__ __forceinline__ uint64_t probeKey(int cascade, int index) {
 
 // --------------------------------------------------------------- scene data
 // One primitive in CSR (cluster) order. identity = the rotation's diagonal is all
-// 1.0 (primitives.hpp:76-77 fast path). 128 B for double.
+// 1.0 (primitives.hpp:76-77 fast path). 128 B for double, ordered for 16-byte
+// loads: translation, size, kind/identity and rot[0] in the first 64 B (four
+// loads cover an unrotated primitive), the rest of the rotation in the next 64 B.
 template <typename R> struct __align__(16) DPrim {
-    R rot[9];
     R trans[3];
     R size[3];
     int kind;
     int identity;
+    R rot[9];
 };
 // FP32 perf-mode record: every kind in one branch-free form (see evalPrim<float>):
 // e = half extents of a box, or (e0, -1, e2) for a radial shape (cylinder r/h,
@@ -216,25 +218,31 @@ __device__ __forceinline__ R evalPrim(const DPrim<R>& pr, V3<R> p) {
 // + post, and the one square root every kind ends in runs after the branches have
 // reconverged (lanes of a warp evaluate mixed kinds). Bit-identical to the switch
 // above: s + (-r) is s - r, and the cylinder's + 0*0 leaves its 2-D sum unchanged.
+// The record is read with 16-byte loads (four, plus four more for a rotation).
 template <>
 __device__ __forceinline__ double evalPrim<double>(const DPrim<double>& pr, V3<double> p) {
-    V3<double> q = p - mk(pr.trans[0], pr.trans[1], pr.trans[2]);
-    if (!pr.identity) {
-        const double* m = pr.rot;  // transposeMul, vec.hpp:113-117
-        q = mk(m[0] * q.x + m[3] * q.y + m[6] * q.z, m[1] * q.x + m[4] * q.y + m[7] * q.z,
-               m[2] * q.x + m[5] * q.y + m[8] * q.z);
+    const double2* v = reinterpret_cast<const double2*>(&pr);
+    const double2 a0 = __ldg(v), a1 = __ldg(v + 1), a2 = __ldg(v + 2);
+    const int4 a3 = __ldg(reinterpret_cast<const int4*>(v + 3));
+    const double size0 = a1.y, size1 = a2.x, size2 = a2.y;
+    V3<double> q = p - mk(a0.x, a0.y, a1.x);
+    if (!a3.y) {  // transposeMul, vec.hpp:113-117
+        const double m0 = __hiloint2double(a3.w, a3.z);
+        const double2 r12 = __ldg(v + 4), r34 = __ldg(v + 5), r56 = __ldg(v + 6), r78 = __ldg(v + 7);
+        q = mk(m0 * q.x + r34.x * q.y + r56.y * q.z, r12.x * q.x + r34.y * q.y + r78.x * q.z,
+               r12.y * q.x + r56.x * q.y + r78.y * q.z);
     }
-    const int kind = pr.kind;
+    const int kind = a3.x;
     if (kind == 2) return q.z;  // plane
     double vx, vy, vz, post;
     if (kind == 1) {  // box
-        const double ax = fabs(q.x) - pr.size[0], ay = fabs(q.y) - pr.size[1], az = fabs(q.z) - pr.size[2];
+        const double ax = fabs(q.x) - size0, ay = fabs(q.y) - size1, az = fabs(q.z) - size2;
         vx = smax(ax, 0.0);
         vy = smax(ay, 0.0);
         vz = smax(az, 0.0);
         post = smin(smax(ax, smax(ay, az)), 0.0);
     } else if (kind == 3) {  // cylinder
-        const double dx = sqrt(q.x * q.x + q.y * q.y) - pr.size[0], dy = fabs(q.z) - pr.size[1];
+        const double dx = sqrt(q.x * q.x + q.y * q.y) - size0, dy = fabs(q.z) - size1;
         vx = smax(dx, 0.0);
         vy = smax(dy, 0.0);
         vz = 0.0;
@@ -242,8 +250,8 @@ __device__ __forceinline__ double evalPrim<double>(const DPrim<double>& pr, V3<d
     } else {  // sphere (0) / capsule (4)
         vx = q.x;
         vy = q.y;
-        vz = kind == 0 ? q.z : q.z - sclamp(q.z, -pr.size[1], pr.size[1]);
-        post = -pr.size[0];
+        vz = kind == 0 ? q.z : q.z - sclamp(q.z, -size1, size1);
+        post = -size0;
     }
     return sqrt(vx * vx + vy * vy + vz * vz) + post;
 }

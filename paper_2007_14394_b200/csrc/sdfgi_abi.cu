@@ -35,6 +35,7 @@ double measure_fma_rate(bool f64, cudaStream_t st);
 
 static_assert(sizeof(sdfgi_prim) == 184, "prim ABI");
 static_assert(sizeof(sdfgi_light) == 80, "light ABI");
+static_assert(sizeof(DPrim<double>) == 128 && offsetof(DPrim<double>, rot) == 56, "FP64 primitive record layout (evalPrim<double> loads)");
 static_assert(sizeof(sdfgi_light) == sizeof(DLight), "light mirror");
 static_assert(sizeof(sdfgi_cluster) == 56, "cluster ABI");
 static_assert(sizeof(sdfgi_cfg) == 224, "cfg ABI");
@@ -169,7 +170,7 @@ struct Ctx {
     DBuf<int> refs;
     DBuf<RayRecord> records;
     // wavefront scratch (kernels.cuh)
-    DBuf<int> wRayCount, wHitList;
+    DBuf<int> wRayCount, wHitList, wChunk;
     DBuf<long long> wRayStart;
     DBuf<double> wRot, fib;
     DBuf<int> perm;
@@ -200,7 +201,7 @@ struct Ctx {
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
-        wRayCount.free(); wHitList.free(); wRayStart.free(); wRot.free(); fib.free(); wHits.free();
+        wRayCount.free(); wHitList.free(); wChunk.free(); wRayStart.free(); wRot.free(); fib.free(); wHits.free();
         wVis.free(); wPark.free(); wCRay.free(); wCtr.free(); perm.free(); wRad.free();
         gbuf.free(); halfDepth.free(); sparseIrr.free(); resolved.free(); indirect.free(); histIrr.free(); composed.free();
         histDepth.free(); halfSrc.free(); sel.free(); sparseValid.free(); sparseAnchor.free();
@@ -746,6 +747,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     const int L = std::max(c->nLights, 1);
     reserve(c->wRayCount, std::max(nCand, 1));
     reserve(c->wRayStart, static_cast<size_t>(nCand) + 1);
+    reserve(c->wChunk, maxRays / 32 + 2);
     reserve(c->wRot, 9 * static_cast<size_t>(std::max(nCand, 1)));
     reserve(c->wHits, std::max<size_t>(maxRays, 1) * sizeof(HitRec<R>));
     reserve(c->wHitList, std::max<size_t>(maxRays, 1));
@@ -773,6 +775,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.nCand = nCand;
     p.rayCount = c->wRayCount.p;
     p.rayStart = c->wRayStart.p;
+    p.chunkSlot = c->wChunk.p;
     p.rot = c->wRot.p;
     p.fib = c->fib.p;
     p.perm = c->perm.p;
