@@ -225,7 +225,6 @@ struct GridBuildParams {
     double* U;
     int* counts;
     const int* start;
-    int* list;    // scratch: the cell's candidates while they are sorted
     int2* entry;  // per entry: (float bits of the candidate's SDF lower bound over the cell, CSR position)
     int maxList;  // longer lists keep the nearest maxList + a sentinel (list = -1)
     // bricks of kBrick^3 cells: the clusters any of the brick's cells can list

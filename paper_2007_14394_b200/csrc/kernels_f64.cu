@@ -75,7 +75,8 @@ __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells
     const int ix = cell % P.dim[0], iy = (cell / P.dim[0]) % P.dim[1], iz = cell / (P.dim[0] * P.dim[1]);
     const double lo[3] = {P.lo[0] + ix * P.h - P.pad, P.lo[1] + iy * P.h - P.pad, P.lo[2] + iz * P.h - P.pad};
     const double hi[3] = {lo[0] + P.h + 2 * P.pad, lo[1] + P.h + 2 * P.pad, lo[2] + P.h + 2 * P.pad};
-    const double r = fmax(P.U[cell], 0.0) + P.margin;
+    const double U = P.U[cell];
+    const double r = fmax(U, 0.0) + P.margin;
     const double r2 = isinf(r) ? INFINITY : r * r;
     auto gap2 = [&](const double* blo, const double* bhi) {
         double g2 = 0;
@@ -85,8 +86,21 @@ __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells
         }
         return g2;
     };
-    // candidate PRIMITIVES: every member of an unbounded cluster, and members of
-    // nearby clusters whose own conservative box is within r of the cell
+    // Lower bound of candidate j's SDF anywhere in the (padded) cell: every
+    // primitive SDF is an exact signed distance (primitives.hpp:42-65), hence
+    // 1-Lipschitz, so SDF_j(p) >= SDF_j(centre) - (half padded diagonal); the
+    // build margin covers the evaluation's rounding (and the FP32 mode's). Much
+    // tighter than the distance to j's bounding box, so queries stop earlier.
+    const V3<double> centre = mk(0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2]));
+    const double half = 0.5 * sqrt(3.0) * (P.h + 2.0 * P.pad);
+    auto lowerBound = [&](int j) { return evalPrim<double>(P.scene.prims[j], centre) - half - P.margin; };
+    // candidate PRIMITIVES: members of nearby clusters (or of an unbounded one) whose
+    // bounding box is within r of the cell and whose lower bound does not exceed the
+    // cell's upper bound U on the scene SDF — only those can attain (or tie) the
+    // minimum at some point of the cell
+    // f(j, box bound) -> false: j is not needed exactly (its bound may stay the box
+    // bound: the lower bound of j's SDF from its bounding box, valid when the cell
+    // centre is outside the box). f returns true to stop the walk.
     const int brick = ix / kBrick + P.bdim[0] * (iy / kBrick + P.bdim[1] * (iz / kBrick));
     auto forEach = [&](auto&& f) {
         for (int i = P.bStart[brick]; i < P.bStart[brick + 1]; ++i) {  // ascending cluster order
@@ -95,71 +109,76 @@ __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells
             if (!cl.unbounded && gap2(cl.lo, cl.hi) > r2) continue;
             for (int j = P.scene.cstart[k]; j < P.scene.cstart[k + 1]; ++j) {
                 const double* b = P.primBox + 6 * static_cast<size_t>(j);
-                if (cl.unbounded || isinf(b[0]) || gap2(b, b + 3) <= r2) f(j);
+                if (!(cl.unbounded || isinf(b[0]) || gap2(b, b + 3) <= r2)) continue;
+                double boxLb = -INFINITY;
+                if (!isinf(b[0])) {
+                    const double gx = fmax(fmax(b[0] - centre.x, centre.x - b[3]), 0.0);
+                    const double gy = fmax(fmax(b[1] - centre.y, centre.y - b[4]), 0.0);
+                    const double gz = fmax(fmax(b[2] - centre.z, centre.z - b[5]), 0.0);
+                    const double g2 = gx * gx + gy * gy + gz * gz;
+                    if (g2 > 0) boxLb = sqrt(g2) - half - P.margin;
+                }
+                if (boxLb > U) continue;  // its SDF bound (>= the box bound) exceeds U too
+                if (f(j, boxLb)) return;
             }
         }
     };
     const int K = P.maxList;
-    if (!fill) {
+    if (!fill) {  // the list length, min(n, K + 1): the walk stops at K + 1
         int n = 0;
-        forEach([&](int) { ++n; });
-        P.counts[cell] = n > K ? K + 1 : n;
+        forEach([&](int j, double) {
+            if (lowerBound(j) <= U) ++n;
+            return n > K;
+        });
+        P.counts[cell] = n;
         return;
     }
-    // nearest first (box distance to the cell centre): order does not affect
-    // results (queries break ties towards the lowest CSR position)
-    const double cx = 0.5 * (lo[0] + hi[0]), cy = 0.5 * (lo[1] + hi[1]), cz = 0.5 * (lo[2] + hi[2]);
-    auto key = [&](int j) {
-        const double* b = P.primBox + 6 * static_cast<size_t>(j);
-        if (isinf(b[0])) return -1.0;
-        double gx = fmax(fmax(b[0] - cx, cx - b[3]), 0.0);
-        double gy = fmax(fmax(b[1] - cy, cy - b[4]), 0.0);
-        double gz = fmax(fmax(b[2] - cz, cz - b[5]), 0.0);
-        return gx * gx + gy * gy + gz * gz;
-    };
+    // entries sorted by their bound (rounded down into float, so `bound > d` proves
+    // the candidate cannot reach or tie d); order does not affect results (queries
+    // break ties towards the lowest CSR position). Insertion into the sorted prefix,
+    // keeping at most K; the smallest bound pushed out (or never admitted) bounds
+    // every omitted candidate and goes to the sentinel.
     const int out = P.start[cell];
     const int slots = P.start[cell + 1] - out;
     const bool truncated = slots == K + 1;
-    int* L = P.list + out;
-    // insertion into the sorted prefix, keeping at most K; the smallest key pushed
-    // out (or never admitted) bounds every omitted candidate
+    int2* E = P.entry + out;
     int m = 0;
-    double tail = INFINITY;
-    forEach([&](int v) {
-        const double kv = key(v);
+    float tail = INFINITY;
+    forEach([&](int v, double boxLb) {
         if (m == K) {
-            const double kl = key(L[K - 1]);
-            if (!(kv < kl)) {
-                tail = fmin(tail, kv);
-                return;
+            // a full list: a candidate whose box bound is already no better than the
+            // K-th entry's is pushed out without its (costlier) SDF bound; the box
+            // bound, below its SDF bound, still bounds it in the sentinel
+            const float kl = __int_as_float(E[K - 1].x);
+            const float kb = __double2float_rd(boxLb);
+            if (!(kb < kl)) {
+                tail = fminf(tail, kb);  // (conservative even if v fails the U test)
+                return false;
             }
-            tail = fmin(tail, kl);
+        }
+        const double lb = lowerBound(v);
+        if (!(lb <= U)) return false;
+        const float kv = __double2float_rd(lb);
+        if (m == K) {
+            const float kl = __int_as_float(E[K - 1].x);
+            if (!(kv < kl)) {
+                tail = fminf(tail, kv);
+                return false;
+            }
+            tail = fminf(tail, kl);
             --m;
         }
         int b = m - 1;
-        while (b >= 0 && key(L[b]) > kv) {
-            L[b + 1] = L[b];
+        while (b >= 0 && __int_as_float(E[b].x) > kv) {
+            E[b + 1] = E[b];
             --b;
         }
-        L[b + 1] = v;
+        E[b + 1] = make_int2(__float_as_int(kv), v);
         ++m;
+        return false;
     });
-    // lower bound of each candidate's SDF over the cell: its surface box is at
-    // least sqrt(key) - (half diagonal) from any point of the cell, and the SDF
-    // outside the box is at least the distance to it. Rounded down into float with
-    // the build margin, so `bound > d` proves the candidate cannot reach (or tie) d.
-    const double half = 0.5 * sqrt(3.0) * (P.h + 2.0 * P.pad);
-    auto bound = [&](double kv) {
-        float lb = -INFINITY;
-        if (kv >= 0) {
-            const double b = sqrt(kv) - half - P.margin;
-            lb = b > 0 ? __double2float_rd(b) : -INFINITY;  // no bound inside the reach of the cell
-        }
-        return lb;
-    };
-    for (int a = 0; a < m; ++a) P.entry[out + a] = make_int2(__float_as_int(bound(key(L[a]))), L[a]);
     if (truncated)  // sentinel: a query still open here walks the cluster hierarchy
-        P.entry[out + m] = make_int2(__float_as_int(bound(tail)), -1);
+        E[m] = make_int2(__float_as_int(tail), -1);
 }
 
 void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st) {

@@ -643,11 +643,9 @@ void buildGrid(Ctx* c) {
     checkLaunch(c);
     const long long total = deviceScan(c->gridCounts.p, c->gridStart.p, ncells + 1);
     REQ(total >= 0 && total < (1LL << 30), SDFGI_ERR_INVALID, "candidate lists too large");
-    c->gridList.alloc(std::max<long long>(total, 1));
     c->gridEntry.alloc(std::max<long long>(total, 1));
     p.entry = c->gridEntry.p;
     p.start = c->gridStart.p;
-    p.list = c->gridList.p;
     launch_grid_list(p, static_cast<int>(ncells), true, c->stream);
     checkLaunch(c);
     CK(cudaStreamSynchronize(c->stream));
