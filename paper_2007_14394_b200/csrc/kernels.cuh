@@ -83,6 +83,15 @@ template <typename R> struct __align__(16) ParkShadow {
     unsigned long long slot;
 };
 
+// A shadow march prepared by the hit setup (k_hit_normals / k_compose_setup): the
+// directIrradiance set-up of one (hit, light) pair whose segment is traced
+// (probe_update.hpp:100-128), compacted per light.
+template <typename R> struct __align__(16) ShadowRay {
+    R o[3], dir[3];
+    R t, tEnd;
+    int rid, li;
+};
+
 template <typename R> struct WaveParams {
     SceneView<R> scene;
     ProbeCommon pc;
@@ -108,8 +117,10 @@ template <typename R> struct WaveParams {
     int* hitList;             // compacted ray ids of converged hits with an owner
     R* vis;                   // per (ray, light)
     R* rad;                   // per ray: shaded radiance (3)
-    // [0] K1 ray cursor, [1] hit count, [2] K2 item cursor, [4] rays parked by K1,
-    // [5] K1 far-phase cursor, [6] shadow marches parked by K2, [7] K2 far cursor
+    // [kCtrRay] K1 ray cursor, [kCtrHits] hit count, [kCtrShadow] K2 item cursor,
+    // [kCtrParkRay] rays parked by K1, [kCtrFarRay] K1 far-phase cursor,
+    // [kCtrParkShadow] shadow marches parked by K2, [kCtrFarShadow] K2 far cursor,
+    // [kLightCtr + li] traced shadow marches toward light li
     unsigned long long* ctr;
     // off-grid marches are parked here and resumed together by a far phase, so
     // the hierarchy walks run side by side instead of stalling near-field warps
@@ -117,6 +128,9 @@ template <typename R> struct WaveParams {
     void* park;
     unsigned long long parkBytes;
     void* cray;  // contact batch: the prepared rays (ContactRay<R>), or null
+    // the traced shadow marches, light li's at [li * srayCap, + ctr[kLightCtr + li])
+    ShadowRay<R>* sray;
+    unsigned long long srayCap;
     // results
     unsigned long long* stats;       // counters or null
     unsigned long long* maxDeltaBits;
@@ -260,6 +274,13 @@ void launch_brick_clusters(const GridBuildParams& p, int nbricks, bool fill, cud
 size_t scan_ints(const int* in, int* out, int n, void* temp, size_t tempBytes, cudaStream_t st);
 
 constexpr int kWaveThreads = 128;   // K1/K2 persistent CTAs
+// WaveParams::ctr slots, each on its own 128-byte line: the work cursors and
+// compaction counters are hit by atomics from every SM, and counters sharing a
+// line would serialise there (and slow every read of the line); the per-light
+// shadow-march counts follow, read-only while K2 runs.
+constexpr int kCtrRay = 0, kCtrHits = 16, kCtrShadow = 32, kCtrParkRay = 48, kCtrFarRay = 64, kCtrParkShadow = 80,
+              kCtrFarShadow = 96;
+constexpr int kLightCtr = 112;
 // minimum resident K1/K2/K3a CTAs per SM (register cap = 64K / (128 * n)); the
 // tracing kernels are latency bound at low occupancy (measured, profiles/)
 #ifndef SDFGI_WAVE_MINB64

@@ -302,7 +302,7 @@ template <typename R, bool ST, int MODE, int PHASE>
 __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_primary(WaveParams<R> P) {
     ParkRay<R>* const park = reinterpret_cast<ParkRay<R>*>(P.park);
     const long long parkCap = static_cast<long long>(P.parkBytes / sizeof(ParkRay<R>));
-    const long long total = PHASE ? min(static_cast<long long>(P.ctr[4]), parkCap) : rayTotal(P);
+    const long long total = PHASE ? min(static_cast<long long>(P.ctr[kCtrParkRay]), parkCap) : rayTotal(P);
     const R eps = R(P.tc.eps);
     const int maxSteps = P.tc.maxSteps;
     Counters cnt;
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
         __syncwarp();
         unsigned long long item;
         if (PHASE == 1) {
-            if (fetchItem(P.ctr + 5, static_cast<unsigned long long>(total), active, exhausted, item)) {
+            if (fetchItem(P.ctr + kCtrFarRay, static_cast<unsigned long long>(total), active, exhausted, item)) {
                 const ParkRay<R>& r = park[item];
                 o = mk(r.o[0], r.o[1], r.o[2]);
                 dir = mk(r.dir[0], r.dir[1], r.dir[2]);
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                 fresh = true;
             }
         } else {
-            const bool got = fetchItem(P.ctr + 0, static_cast<unsigned long long>(total), active, exhausted, item);
+            const bool got = fetchItem(P.ctr + kCtrRay, static_cast<unsigned long long>(total), active, exhausted, item);
             int s = 0;
             if (MODE == 0) {
                 // the warp's new items are consecutive: one lane binary-searches the
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
             }
         }
         if (PHASE == 0) {
-            const long long ps = parkSlot(P.ctr + 4, parkIt);
+            const long long ps = parkSlot(P.ctr + kCtrParkRay, parkIt);
             if (ps >= parkCap) {  // buffer full: this march queries here after all
                 parkIt = false;
                 if (state == 0) {
@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                 const int leader = __ffs(m) - 1;
                 const unsigned lane = threadIdx.x & 31;
                 unsigned long long base = 0;
-                if (static_cast<int>(lane) == leader) base = atomicAdd(P.ctr + 1, static_cast<unsigned long long>(__popc(m)));
+                if (static_cast<int>(lane) == leader) base = atomicAdd(P.ctr + kCtrHits, static_cast<unsigned long long>(__popc(m)));
                 base = __shfl_sync(m, base, leader);
                 P.hitList[base + __popc(m & ((1u << lane) - 1u))] = static_cast<int>(rid);
             }
@@ -545,71 +545,24 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
     if (ST) flushCounters(cnt, P.stats);
 }
 
-// The converged hits' normals (evalGradient of the owner, primitives.hpp:96-108)
-// over the compacted hit list — every lane has one, instead of the few lanes of a
-// K1 warp whose rays just converged.
+// directIrradiance's per-light set-up (probe_update.hpp:100-128) for the hit `rid`
+// at pos with normal nrm: a light below the horizon (or on the point) gets vis -1
+// (no contribution), a segment too short to trace vis 1; every other pair becomes
+// a ShadowRay for K2, appended to its light's list. Called by the lanes `am` of a
+// warp together (uniform light loop), `valid` false for lanes without a hit.
 template <typename R>
-__global__ void __launch_bounds__(128) k_hit_normals(WaveParams<R> P) {
-    const unsigned long long n = P.ctr[1];
-    for (unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
-        HitRec<R>& h = P.hits[P.hitList[i]];
-        const V3<R> nn = evalGradient(P.scene.prims[h.owner], mk(h.p[0], h.p[1], h.p[2]));
-        h.n[0] = nn.x;
-        h.n[1] = nn.y;
-        h.n[2] = nn.z;
-    }
-}
-
-// ----------------------------------------------------------- K2 shadow rays
-// One (converged hit, light) item per lane: directIrradiance's setup
-// (probe_update.hpp:100-128) and the softShadowTrace march (scene.hpp:459-476),
-// one query per iteration. vis = 1 when the segment is too short to trace.
-// PHASE 0 / 1 as in K1: off-grid shadow marches are parked and resumed together.
-template <typename R, bool ST, int PHASE>
-__global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shadow(WaveParams<R> P) {
+__device__ __forceinline__ void shadowSetup(const WaveParams<R>& P, unsigned am, bool valid, int rid, V3<R> pos,
+                                            V3<R> nrm) {
     const int L = P.scene.n_lights;
-    const unsigned long long nHits = P.ctr[1];
-    ParkShadow<R>* const park = reinterpret_cast<ParkShadow<R>*>(P.park);
-    const unsigned long long parkCap = P.parkBytes / sizeof(ParkShadow<R>);
-    const unsigned long long total = PHASE ? min(P.ctr[6], parkCap) : nHits * static_cast<unsigned long long>(L);
-    const R minStep = R(5e-4), inf = R(INFINITY), k = R(P.tc.shadowK);
-    const int maxSteps = P.tc.shadowSteps;
-    Counters cnt;
-    cnt.zero();
-    bool active = false, exhausted = false;
-    unsigned long long slot = 0;
-    V3<R> o = mk(R(0), R(0), R(0)), dir = o;
-    R t = 0, tEnd = 0, v = 0, lastD = 0;
-    int step = 0, seed = -1;
-    while (true) {
-        __syncwarp();
-        unsigned long long item;
-        if (PHASE == 1) {
-            if (fetchItem(P.ctr + 7, total, active, exhausted, item)) {
-                const ParkShadow<R>& r = park[item];
-                o = mk(r.o[0], r.o[1], r.o[2]);
-                dir = mk(r.dir[0], r.dir[1], r.dir[2]);
-                t = r.t;
-                tEnd = r.tEnd;
-                v = r.v;
-                lastD = r.lastD;
-                step = r.step;
-                seed = r.seed;
-                slot = r.slot;
-                active = true;
-            }
-        } else if (fetchItem(P.ctr + 2, total, active, exhausted, item)) {
-            // light-major: consecutive lanes take consecutive hits toward the same light
-            const int rid = P.hitList[item % nHits];
-            const int li = static_cast<int>(item / nHits);
-            slot = static_cast<unsigned long long>(rid) * L + li;
-            const HitRec<R>& h = P.hits[rid];
-            const V3<R> pos = mk(h.p[0], h.p[1], h.p[2]);
-            const V3<R> nrm = mk(h.n[0], h.n[1], h.n[2]);
-            const DLight& Lt = P.scene.lights[li];
+    const unsigned lane = threadIdx.x & 31;
+    for (int li = 0; li < L; ++li) {
+        const DLight& Lt = P.scene.lights[li];
+        const unsigned long long slot = static_cast<unsigned long long>(rid) * L + li;
+        bool live = false;
+        V3<R> dir = mk(R(0), R(0), R(0));
+        R bias = R(0), tMax = R(0);
+        if (valid) {
             bool skip = false;
-            R tMax = R(0);
             if (Lt.kind == 0) {
                 V3<R> toLight = mk(R(Lt.position[0]), R(Lt.position[1]), R(Lt.position[2])) - pos;
                 R r2 = dot(toLight, toLight);
@@ -632,21 +585,113 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shad
                 P.vis[slot] = R(-1);
             } else {
                 const R cosT = dot(nrm, dir);
-                const R bias = R(2.0) * R(P.tc.eps) / smax(R(0.1), cosT);
-                if (tMax - bias > bias) {
-                    if (ST) ++cnt.shadow;
-                    o = pos + nrm * bias;
-                    t = bias;
-                    tEnd = tMax - bias;
-                    v = R(1);
-                    lastD = inf;
-                    step = 0;
-                    seed = -1;
-                    active = true;
-                } else {
-                    P.vis[slot] = R(1);
-                }
+                bias = R(2.0) * R(P.tc.eps) / smax(R(0.1), cosT);
+                live = tMax - bias > bias;
+                if (!live) P.vis[slot] = R(1);
             }
+        }
+        const unsigned m = __ballot_sync(am, live);
+        if (m == 0) continue;
+        const int leader = __ffs(m) - 1;
+        unsigned long long base = 0;
+        if (static_cast<int>(lane) == leader)
+            base = atomicAdd(P.ctr + kLightCtr + li, static_cast<unsigned long long>(__popc(m)));
+        base = __shfl_sync(am, base, leader);
+        if (live) {
+            ShadowRay<R> r;
+            const V3<R> o = pos + nrm * bias;
+            r.o[0] = o.x;
+            r.o[1] = o.y;
+            r.o[2] = o.z;
+            r.dir[0] = dir.x;
+            r.dir[1] = dir.y;
+            r.dir[2] = dir.z;
+            r.t = bias;
+            r.tEnd = tMax - bias;
+            r.rid = rid;
+            r.li = li;
+            P.sray[li * P.srayCap + base + __popc(m & ((1u << lane) - 1u))] = r;
+        }
+    }
+}
+
+// The converged hits' normals (evalGradient of the owner, primitives.hpp:96-108)
+// and their shadow-ray set-up over the compacted hit list — every lane has one,
+// instead of the few lanes of a K1 warp whose rays just converged.
+template <typename R>
+__global__ void __launch_bounds__(128) k_hit_normals(WaveParams<R> P) {
+    const unsigned long long n = P.ctr[kCtrHits];
+    for (unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+        const unsigned am = __activemask();
+        const int rid = P.hitList[i];
+        HitRec<R>& h = P.hits[rid];
+        const V3<R> pos = mk(h.p[0], h.p[1], h.p[2]);
+        const V3<R> nn = evalGradient(P.scene.prims[h.owner], pos);
+        h.n[0] = nn.x;
+        h.n[1] = nn.y;
+        h.n[2] = nn.z;
+        shadowSetup(P, am, true, rid, pos, nn);
+    }
+}
+
+// ----------------------------------------------------------- K2 shadow rays
+// One (converged hit, light) item per lane: directIrradiance's setup
+// (probe_update.hpp:100-128) and the softShadowTrace march (scene.hpp:459-476),
+// one query per iteration. vis = 1 when the segment is too short to trace.
+// PHASE 0 / 1 as in K1: off-grid shadow marches are parked and resumed together.
+template <typename R, bool ST, int PHASE>
+__global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shadow(WaveParams<R> P) {
+    const int L = P.scene.n_lights;
+    ParkShadow<R>* const park = reinterpret_cast<ParkShadow<R>*>(P.park);
+    const unsigned long long parkCap = P.parkBytes / sizeof(ParkShadow<R>);
+    unsigned long long traced = 0;
+    for (int li = 0; li < L; ++li) traced += P.ctr[kLightCtr + li];
+    const unsigned long long total = PHASE ? min(P.ctr[kCtrParkShadow], parkCap) : traced;
+    const R minStep = R(5e-4), inf = R(INFINITY), k = R(P.tc.shadowK);
+    const int maxSteps = P.tc.shadowSteps;
+    Counters cnt;
+    cnt.zero();
+    bool active = false, exhausted = false;
+    unsigned long long slot = 0;
+    V3<R> o = mk(R(0), R(0), R(0)), dir = o;
+    R t = 0, tEnd = 0, v = 0, lastD = 0;
+    int step = 0, seed = -1;
+    while (true) {
+        __syncwarp();
+        unsigned long long item;
+        if (PHASE == 1) {
+            if (fetchItem(P.ctr + kCtrFarShadow, total, active, exhausted, item)) {
+                const ParkShadow<R>& r = park[item];
+                o = mk(r.o[0], r.o[1], r.o[2]);
+                dir = mk(r.dir[0], r.dir[1], r.dir[2]);
+                t = r.t;
+                tEnd = r.tEnd;
+                v = r.v;
+                lastD = r.lastD;
+                step = r.step;
+                seed = r.seed;
+                slot = r.slot;
+                active = true;
+            }
+        } else if (fetchItem(P.ctr + kCtrShadow, total, active, exhausted, item)) {
+            // light-major: consecutive lanes take consecutive traced marches toward
+            // the same light (set up by the hit setup, shadowSetup)
+            int li = 0;
+            unsigned long long k = item;
+            while (li + 1 < L && k >= P.ctr[kLightCtr + li]) k -= P.ctr[kLightCtr + li++];
+            const ShadowRay<R> r = P.sray[li * P.srayCap + k];
+            o = mk(r.o[0], r.o[1], r.o[2]);
+            dir = mk(r.dir[0], r.dir[1], r.dir[2]);
+            t = r.t;
+            tEnd = r.tEnd;
+            slot = static_cast<unsigned long long>(r.rid) * L + r.li;
+            v = R(1);
+            lastD = inf;
+            step = 0;
+            seed = -1;
+            active = true;
+            if (ST) ++cnt.shadow;
         }
         if (!__any_sync(kFull, active)) {
             if (__all_sync(kFull, exhausted)) break;
@@ -657,7 +702,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shad
         if (want) p = o + dir * t;
         if (PHASE == 0) {
             bool parkIt = want && park && gridCell<R>(P.scene.grid, p) < 0;
-            const long long ps = parkSlot(P.ctr + 6, parkIt);
+            const long long ps = parkSlot(P.ctr + kCtrParkShadow, parkIt);
             if (ps >= static_cast<long long>(parkCap)) parkIt = false;  // buffer full
             if (parkIt) {
                 ParkShadow<R>& r = park[ps];
@@ -778,7 +823,7 @@ __global__ void __launch_bounds__(128, WaveOcc<R>::shade) k_shade_rays(WaveParam
     extern __shared__ __align__(16) unsigned char k3aSmem[];
     R* slab = reinterpret_cast<R*>(k3aSmem);  // kMvcSlab values per thread (MVC working set)
     const bool all = P.debug != 0;
-    const long long total = all ? rayTotal(P) : static_cast<long long>(P.ctr[1]);
+    const long long total = all ? rayTotal(P) : static_cast<long long>(P.ctr[kCtrHits]);
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
     unsigned long long nShaded = 0, nMvc = 0;  // shading work (ST): shadeHit calls, MVC evaluations
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
@@ -946,7 +991,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
     k_ray_setup<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
     k_ray_scan<R><<<1, kScanThreads, 0, st>>>(p);
     k_ray_chunks<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
-    cudaMemsetAsync(p.ctr, 0, 8 * sizeof(unsigned long long), st);
+    cudaMemsetAsync(p.ctr, 0, (kLightCtr + (p.scene.n_lights > 1 ? p.scene.n_lights : 1)) * sizeof(unsigned long long), st);
     if (e0) cudaEventRecord(e0, st);
     static int b1 = persistentBlocks(k_trace_primary<R, ST, 0, 0>, kWaveThreads, 0);
     static int b1f = persistentBlocks(k_trace_primary<R, ST, 0, 1>, kWaveThreads, 0);
@@ -1019,7 +1064,7 @@ __global__ void __launch_bounds__(128) k_contact_combine(WaveParams<R> P) {
 // then the per-pixel combine. Replaces the per-pixel k_contact loop.
 template <typename R, bool ST>
 static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long* launches) {
-    cudaMemsetAsync(p.ctr, 0, 8 * sizeof(unsigned long long), st);
+    cudaMemsetAsync(p.ctr, 0, (kLightCtr + (p.scene.n_lights > 1 ? p.scene.n_lights : 1)) * sizeof(unsigned long long), st);
     if (p.cray) k_contact_setup<R><<<static_cast<int>((p.nRaysDirect + 255) / 256), 256, 0, st>>>(p);
     static int b1 = persistentBlocks(k_trace_primary<R, ST, 1, 0>, kWaveThreads, 0);
     static int b1f = persistentBlocks(k_trace_primary<R, ST, 1, 1>, kWaveThreads, 0);
@@ -1060,8 +1105,15 @@ __global__ void __launch_bounds__(128) k_compose_setup(WaveParams<R> P) {
             P.hits[i] = h;
         }
     }
-    const long long slot = parkSlot(P.ctr + 1, geo);  // compacted pixel list for K2
+    const long long slot = parkSlot(P.ctr + kCtrHits, geo);  // compacted pixel list
     if (geo) P.hitList[slot] = static_cast<int>(i);
+    V3<R> pos = mk(R(0), R(0), R(0)), nrm = pos;
+    if (geo) {
+        const GPix& px = P.gb[i];
+        pos = mk(R(px.world_pos[0]), R(px.world_pos[1]), R(px.world_pos[2]));
+        nrm = mk(R(px.normal[0]), R(px.normal[1]), R(px.normal[2]));
+    }
+    shadowSetup(P, kFull, geo, static_cast<int>(i), pos, nrm);
 }
 
 template <typename R>
@@ -1088,7 +1140,7 @@ __global__ void __launch_bounds__(128) k_compose(WaveParams<R> P) {
 
 template <typename R, bool ST>
 static void composeWavefront(const WaveParams<R>& p, cudaStream_t st, long long* launches) {
-    cudaMemsetAsync(p.ctr, 0, 8 * sizeof(unsigned long long), st);
+    cudaMemsetAsync(p.ctr, 0, (kLightCtr + (p.scene.n_lights > 1 ? p.scene.n_lights : 1)) * sizeof(unsigned long long), st);
     const long long np = static_cast<long long>(p.gw) * p.gh;
     const int blocks = static_cast<int>((np + 127) / 128);
     static int b2 = persistentBlocks(k_trace_shadow<R, ST, 0>, kWaveThreads, 0);

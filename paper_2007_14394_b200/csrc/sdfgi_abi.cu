@@ -175,7 +175,7 @@ struct Ctx {
     DBuf<double> wRot, fib;
     DBuf<int> perm;
     int fibN = -1;
-    DBuf<unsigned char> wHits, wVis, wRad, wPark, wCRay;
+    DBuf<unsigned char> wHits, wVis, wRad, wPark, wCRay, wSRay;
     DBuf<unsigned long long> wCtr;
     int persistCap = 0;  // 0 = occupancy-sized persistent grids
     // gather (e): G-buffer, stage buffers, history (pipeline.hpp:213-218)
@@ -202,7 +202,7 @@ struct Ctx {
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
         wRayCount.free(); wHitList.free(); wChunk.free(); wRayStart.free(); wRot.free(); fib.free(); wHits.free();
-        wVis.free(); wPark.free(); wCRay.free(); wCtr.free(); perm.free(); wRad.free();
+        wVis.free(); wPark.free(); wCRay.free(); wSRay.free(); wCtr.free(); perm.free(); wRad.free();
         gbuf.free(); halfDepth.free(); sparseIrr.free(); resolved.free(); indirect.free(); histIrr.free(); composed.free();
         histDepth.free(); halfSrc.free(); sel.free(); sparseValid.free(); sparseAnchor.free();
         for (auto& e : gev)
@@ -751,8 +751,9 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     reserve(c->wHitList, std::max<size_t>(maxRays, 1));
     reserve(c->wVis, std::max<size_t>(maxRays, 1) * L * sizeof(R));
     reserve(c->wRad, std::max<size_t>(maxRays, 1) * 3 * sizeof(R));
-    reserve(c->wCtr, 8);
+    reserve(c->wCtr, kLightCtr + L);
     reservePark<R>(c, maxRays, L);
+    reserve(c->wSRay, std::max<size_t>(maxRays, 1) * L * sizeof(ShadowRay<R>));
     if (c->fibN != N) {
         reserve(c->fib, 9 * static_cast<size_t>(N));
         launch_fib_table(c->fib.p, N, c->stream);
@@ -783,6 +784,8 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.vis = reinterpret_cast<R*>(c->wVis.p);
     p.rad = reinterpret_cast<R*>(c->wRad.p);
     p.ctr = c->wCtr.p;
+    p.sray = reinterpret_cast<ShadowRay<R>*>(c->wSRay.p);
+    p.srayCap = std::max<size_t>(maxRays, 1);
     p.park = c->accel && c->haveGrid && c->wPark.n >= 4096 ? c->wPark.p : nullptr;  // SDFGI_PARK_MB=0: off
     p.parkBytes = p.park ? c->wPark.n : 0;
     p.prevAtlas = c->atlas[c->front].p;
@@ -1601,8 +1604,9 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     reserve(c->wHitList, cap);
     reserve(c->wVis, cap * L * sizeof(R));
     reserve(c->wRad, cap * 3 * sizeof(R));
-    reserve(c->wCtr, 8);
+    reserve(c->wCtr, kLightCtr + L);
     reservePark<R>(c, cap, L);
+    reserve(c->wSRay, cap * L * sizeof(ShadowRay<R>));
     reserve(c->wCRay, cap * sizeof(ContactRay<R>));
     WaveParams<R> p;
     std::memset(&p, 0, sizeof(p));
@@ -1623,6 +1627,8 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     p.vis = reinterpret_cast<R*>(c->wVis.p);
     p.rad = reinterpret_cast<R*>(c->wRad.p);
     p.ctr = c->wCtr.p;
+    p.sray = reinterpret_cast<ShadowRay<R>*>(c->wSRay.p);
+    p.srayCap = cap;
     p.park = c->accel && c->haveGrid && c->wPark.n >= 4096 ? c->wPark.p : nullptr;  // SDFGI_PARK_MB=0: off
     p.parkBytes = p.park ? c->wPark.n : 0;
     p.stats = c->scratch.p;
@@ -1649,8 +1655,9 @@ WaveParams<R> composeParams(Ctx* c, const sdfgi_cfg* cfg) {
     reserve(c->wHits, np * sizeof(HitRec<R>));
     reserve(c->wHitList, np);
     reserve(c->wVis, np * L * sizeof(R));
-    reserve(c->wCtr, 8);
+    reserve(c->wCtr, kLightCtr + L);
     reservePark<R>(c, np, L);
+    reserve(c->wSRay, std::max<size_t>(np, 1) * L * sizeof(ShadowRay<R>));
     WaveParams<R> p;
     std::memset(&p, 0, sizeof(p));
     p.scene = c->sceneView<R>();
@@ -1663,6 +1670,8 @@ WaveParams<R> composeParams(Ctx* c, const sdfgi_cfg* cfg) {
     p.hitList = c->wHitList.p;
     p.vis = reinterpret_cast<R*>(c->wVis.p);
     p.ctr = c->wCtr.p;
+    p.sray = reinterpret_cast<ShadowRay<R>*>(c->wSRay.p);
+    p.srayCap = std::max<size_t>(np, 1);
     p.park = c->accel && c->haveGrid && c->wPark.n >= 4096 ? c->wPark.p : nullptr;
     p.parkBytes = p.park ? c->wPark.n : 0;
     p.stats = c->scratch.p;
