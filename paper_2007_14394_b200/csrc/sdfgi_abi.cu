@@ -466,10 +466,19 @@ void buildGrid(Ctx* c) {
     // (cheap) candidate lists for their first steps; SDFGI_GRID_MARGIN overrides.
     // It also covers the probe volumes (the hint box grown by sdfgi_cascade_set):
     // probes above an open scene would otherwise query off the grid every step.
+    // The margin is a multiple of the geometry's SMALLEST extent on every axis: a
+    // flat open scene (C4: 240 x 20 x 240) keeps the rays that leave it upwards on
+    // the grid without spending cells on its far horizontal surroundings.
+    // Sweep (profiles/README.md, 50M cells): C2 pass 0 FP64 margin 0.6 per-axis
+    // 13.1 ms, 2.5 x min 12.0, 4 x min 12.3; C4 pass 1 0.235 -> 0.326 -> 0.374 Grays/s.
+    // SDFGI_GRID_MARGIN sets the multiple, SDFGI_GRID_MARGIN_MIN=0 the per-axis extent.
     const char* menv = std::getenv("SDFGI_GRID_MARGIN");
-    const double marginFrac = menv ? std::atof(menv) : 0.6;  // C2 sweep (profiles/README.md): 0.3 -> 0.6 with 8M cells = -9%
+    const double marginFrac = menv ? std::atof(menv) : 3.5;
+    const char* mmode = std::getenv("SDFGI_GRID_MARGIN_MIN");
+    const bool fromMin = !mmode || std::atoi(mmode) != 0;
+    const double minExt = std::min(hi[0] - lo[0], std::min(hi[1] - lo[1], hi[2] - lo[2]));
     for (int a = 0; a < 3; ++a) {
-        double e = hi[a] - lo[a];
+        double e = fromMin ? minExt : hi[a] - lo[a];
         double m = marginFrac * e + 1e-3;
         lo[a] -= m;
         hi[a] += m;
@@ -483,8 +492,10 @@ void buildGrid(Ctx* c) {
     const char* env = std::getenv("SDFGI_GRID_CELLS");
     // finer cells -> smaller U -> shorter, more uniform candidate lists (and tighter
     // per-entry bounds); measured on C2 with the current kernels (pass 0, FP64, warm):
-    // 2M cells 17.4 ms, 4M 16.6, 8M 15.9, 16M 15.5, 24M 15.3 (margin 0.6)
-    double target = env ? std::atof(env) : 16777216.0;
+    // 2M cells 17.4 ms, 4M 16.6, 8M 15.9, 16M 15.5, 24M 15.3 (margin 0.6, round-1
+    // kernels); with the SDF-bound lists and the min-extent margin 33M -> 50M -> 66M
+    // cells: C2 13.9 / 12.3 / 12.9 ms, C4 0.28 / 0.37 / 0.34 Grays/s
+    double target = env ? std::atof(env) : 50331648.0;
     if (target < 1) return;
     double h = std::cbrt(ext[0] * ext[1] * ext[2] / target);
     int dim[3];

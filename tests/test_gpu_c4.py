@@ -23,7 +23,11 @@ def c4():
     return scenegen.with_fast_clusters(scenegen.c4_scene(50000), 8)
 
 
-def test_c4_queries_bit_exact(c4):
+@pytest.mark.parametrize("margin", [None, ("0.6", "0")], ids=["default-grid", "tight-grid"])
+def test_c4_queries_bit_exact(c4, margin, monkeypatch):
+    if margin:  # a grid below the probe volume's top (the per-axis 0.6 margin)
+        monkeypatch.setenv("SDFGI_GRID_MARGIN", margin[0])
+        monkeypatch.setenv("SDFGI_GRID_MARGIN_MIN", margin[1])
     with Device(0, precision="f64") as dev:
         dev.upload_scene(c4)
         info = dev.accel_info()
@@ -42,7 +46,9 @@ def test_c4_queries_bit_exact(c4):
         cs = c4.cascade
         api.makeCascade(dev, *cs.res, cs.spacing, 0, c4.camera.position)
         info = dev.accel_info()
-        assert info["dim"] != dim0 and info["grid"]
+        assert info["grid"]
+        if margin:
+            assert info["dim"] != dim0
         d_g, o_g = dev.query_points(pts)
         assert np.array_equal(d_g, d_o)
         assert np.array_equal(o_g, o_o)
