@@ -686,7 +686,36 @@ __device__ __forceinline__ V3<double> sampleBilinear(const AtlasView& a, int pro
 // a_0 + a_1 + a_2 — 3 asin per triangle instead of 3 asin + 7 sin (the values
 // agree with the reference's to a few ulps of M). Same degenerate-case branches.
 template <typename M> __device__ __forceinline__ M mvcAsin(M v);
-template <> __device__ __forceinline__ double mvcAsin<double>(double v) { return asin(v); }
+// asin on [0, 1] without branches (lanes of a warp fall on both sides of 0.5, and
+// the library asin's two paths would run one after the other): z = x, or for
+// x > 0.5 z = sqrt((1 - x) / 2) with asin x = pi/2 - 2 asin z; asin z = z + z t P(t),
+// t = z^2 <= 1/4, P of degree 11 (Chebyshev fit on [0, 1/4], ~1e-16 relative; the
+// fit: scripts/fit_asin.py). Within ~1-2 ulp of the correctly rounded asin.
+__constant__ const double kAsinP[12] = {
+    0.16666666666666624,
+    0.07500000000029536,
+    0.04464285709453126,
+    0.030381947788153375,
+    0.022372036498208864,
+    0.017355440300771036,
+    0.01392777380792154,
+    0.011888341648348918,
+    0.007745641486205083,
+    0.016196107598564897,
+    -0.011005663933853308,
+    0.028347549339135487};
+__device__ __forceinline__ double asin01(double x) {
+    const bool big = x > 0.5;
+    const double s = sqrt(0.5 - 0.5 * x);  // exact argument for x >= 0.5
+    const double z = big ? s : x;
+    const double t = z * z;
+    double p = kAsinP[11];
+#pragma unroll
+    for (int k = 10; k >= 0; --k) p = fma(p, t, kAsinP[k]);
+    const double r = fma(z * t, p, z);
+    return big ? 1.5707963267948966 - fma(2.0, r, -6.123233995736766e-17) : r;
+}
+template <> __device__ __forceinline__ double mvcAsin<double>(double v) { return asin01(v); }
 template <> __device__ __forceinline__ float mvcAsin<float>(float v) { return asinf(v); }
 template <typename M> __device__ __forceinline__ M mvcDiv(M a, M b) { return a / b; }
 template <> __device__ __forceinline__ float mvcDiv<float>(float a, float b) { return __fdividef(a, b); }
