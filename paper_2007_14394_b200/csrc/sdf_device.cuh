@@ -750,21 +750,37 @@ struct MvcArrays<M, true> {
 };
 constexpr int kMvcSlab = 40;  // values per thread in a shared slab
 
+// The 8 corners of a cascade cell: probe positions read straight from the probe
+// array (corner k = cell + (k & 1, k >> 1 & 1, k >> 2 & 1)), no local copy.
+struct CellCorners {
+    const double* pos;  // probe positions, xyz per probe
+    int p0, dy, dz;     // global index of corner 0, strides in y and z
+    __device__ int index(int k) const { return p0 + (k & 1) + ((k >> 1) & 1) * dy + ((k >> 2) & 1) * dz; }
+    __device__ V3<double> corner(int k) const {
+        const double* P = pos + 3 * static_cast<size_t>(index(k));
+        return mk(P[0], P[1], P[2]);
+    }
+};
+
+// Triangulated hex faces (mean_value.hpp:18-20): warp-uniform loop index, so one
+// broadcast constant load per corner instead of a local-memory table.
+__constant__ const int kMvcFaces[6][4] = {{0, 2, 3, 1}, {4, 5, 7, 6}, {0, 1, 5, 4}, {2, 6, 7, 3}, {0, 4, 6, 2}, {1, 3, 7, 5}};
+
+// Result: the weights in a.wts(0..7) (precision M; the caller widens to double).
 template <typename M, bool SH>
-__device__ inline bool mvcWeightsHexImpl(const V3<double>* corners, V3<double> xd, double* weights, M* slab) {
-    const int faces[6][4] = {{0, 2, 3, 1}, {4, 5, 7, 6}, {0, 1, 5, 4}, {2, 6, 7, 3}, {0, 4, 6, 2}, {1, 3, 7, 5}};
+__device__ inline bool mvcWeightsHexImpl(const CellCorners& cc, V3<double> xd, MvcArrays<M, SH>& a) {
     const M eps = M(1e-10);
     const M pi = M(kPi);
-    MvcArrays<M, SH> a(slab);
     for (int i = 0; i < 8; ++i) a.wts(i) = M(0);
-    for (int i = 0; i < 8; ++i) weights[i] = 0.0;
     const V3<M> x = mk(M(xd.x), M(xd.y), M(xd.z));
     for (int i = 0; i < 8; ++i) {
-        V3<M> v = mk(M(corners[i].x), M(corners[i].y), M(corners[i].z)) - x;
+        const V3<double> ci = cc.corner(i);
+        V3<M> v = mk(M(ci.x), M(ci.y), M(ci.z)) - x;
         const M di = length(v);
         a.dist(i) = di;
         if (di < eps) {
-            weights[i] = 1.0;
+            for (int k = 0; k < 8; ++k) a.wts(k) = M(0);
+            a.wts(i) = M(1);
             return true;
         }
         const M inv = mvcDiv(M(1), di);
@@ -777,14 +793,16 @@ __device__ inline bool mvcWeightsHexImpl(const V3<double>* corners, V3<double> x
     for (int f = 0; f < 6; ++f) {
 #pragma unroll 1
         for (int tr = 0; tr < 2; ++tr) {
-            const int t0 = faces[f][0], t1 = faces[f][tr ? 2 : 1], t2 = faces[f][tr ? 3 : 2];
+            const int t0 = kMvcFaces[f][0], t1 = kMvcFaces[f][tr ? 2 : 1], t2 = kMvcFaces[f][tr ? 3 : 2];
             const int tri[3] = {t0, t1, t2};
             M d[3], sa[3], ca[3], theta[3], st[3];
             V3<M> u[3];
+#pragma unroll
             for (int i = 0; i < 3; ++i) {
                 d[i] = a.dist(tri[i]);
                 u[i] = mk(a.ux(tri[i]), a.uy(tri[i]), a.uz(tri[i]));
             }
+#pragma unroll
             for (int i = 0; i < 3; ++i) {
                 const M l = length(u[(i + 1) % 3] - u[(i + 2) % 3]);
                 sa[i] = sclamp(l * M(0.5), M(0), M(1));
@@ -796,13 +814,15 @@ __device__ inline bool mvcWeightsHexImpl(const V3<double>* corners, V3<double> x
             if (pi - h < M(1e-8)) {
                 M total = 0;
                 M w[3];
+#pragma unroll
                 for (int i = 0; i < 3; ++i) {
                     w[i] = st[i] * d[(i + 1) % 3] * d[(i + 2) % 3];
                     total += w[i];
                 }
                 if (total < eps) return false;
-                for (int i = 0; i < 8; ++i) weights[i] = 0.0;
-                for (int i = 0; i < 3; ++i) weights[tri[i]] = double(w[i] / total);
+                for (int k = 0; k < 8; ++k) a.wts(k) = M(0);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) a.wts(tri[i]) = w[i] / total;
                 return true;
             }
             V3<M> cr = mk(u[1].y * u[2].z - u[1].z * u[2].y, u[1].z * u[2].x - u[1].x * u[2].z,
@@ -812,24 +832,21 @@ __device__ inline bool mvcWeightsHexImpl(const V3<double>* corners, V3<double> x
             const M sh = sa[0] * ca[1] * ca[2] + ca[0] * sa[1] * ca[2] + ca[0] * ca[1] * sa[2] - sa[0] * sa[1] * sa[2];
             M c[3], sv[3];
             bool skip = false;
+#pragma unroll
             for (int i = 0; i < 3; ++i) {
                 const int j = (i + 1) % 3, k = (i + 2) % 3;
                 const M denom = st[j] * st[k];
-                if (fabs(denom) < eps) {
-                    skip = true;
-                    break;
-                }
                 // sin(h - theta_i) = sin(a_j + a_k - a_i)
                 const M sjk = sa[j] * ca[k] + ca[j] * sa[k], cjk = ca[j] * ca[k] - sa[j] * sa[k];
                 const M shi = sjk * ca[i] - cjk * sa[i];
                 c[i] = mvcDiv(M(2) * sh * shi, denom) - M(1);
                 sv[i] = sign * sqrt(smax(M(0), M(1) - c[i] * c[i]));
-                if (fabs(sv[i]) <= eps) {
-                    skip = true;
-                    break;
-                }
+                // the reference stops at the first degenerate i (mean_value.hpp:80-86);
+                // the values after it are unused either way
+                skip = skip || fabs(denom) < eps || fabs(sv[i]) <= eps;
             }
             if (skip) continue;
+#pragma unroll
             for (int i = 0; i < 3; ++i) {
                 const int j = (i + 1) % 3, k = (i + 2) % 3;
                 const M w = mvcDiv(theta[i] - c[j] * theta[k] - c[k] * theta[j], d[i] * st[j] * sv[k]);
@@ -842,14 +859,8 @@ __device__ inline bool mvcWeightsHexImpl(const V3<double>* corners, V3<double> x
     M total = 0;
     for (int i = 0; i < 8; ++i) total += a.wts(i);
     if (fabs(total) < eps || !isfinite(total)) return false;
-    for (int i = 0; i < 8; ++i) weights[i] = double(a.wts(i) / total);
+    for (int i = 0; i < 8; ++i) a.wts(i) = a.wts(i) / total;
     return true;
-}
-
-template <typename M>
-__device__ inline bool mvcWeightsHex(const V3<double>* corners, V3<double> xd, double* weights, M* slab = nullptr) {
-    return slab ? mvcWeightsHexImpl<M, true>(corners, xd, weights, slab)
-                : mvcWeightsHexImpl<M, false>(corners, xd, weights, slab);
 }
 
 struct Stencil {
@@ -898,17 +909,12 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
     const CascadeDev& c = cas[chosen];
     V3<double> f = (point - mk(c.origin[0], c.origin[1], c.origin[2])) / c.spacing;
     double tx = f.x - cell[0], ty = f.y - cell[1], tz = f.z - cell[2];
-    V3<double> corners[8];
-    int pidx[8];
+    const CellCorners cc{pv.pos, c.base + cell[0] + c.res[0] * (cell[1] + c.res[1] * cell[2]), c.res[0],
+                         c.res[0] * c.res[1]};
     double maxDisp = 0;
     for (int k = 0; k < 8; ++k) {
-        int ix = cell[0] + (k & 1), iy = cell[1] + ((k >> 1) & 1), iz = cell[2] + ((k >> 2) & 1);
-        int pi = ix + c.res[0] * (iy + c.res[1] * iz);
-        pidx[k] = pi;
-        const double* P = pv.pos + 3 * static_cast<size_t>(c.base + pi);
-        const double* Q = pv.rest + 3 * static_cast<size_t>(c.base + pi);
-        corners[k] = mk(P[0], P[1], P[2]);
-        maxDisp = smax(maxDisp, length(corners[k] - mk(Q[0], Q[1], Q[2])));
+        const double* Q = pv.rest + 3 * static_cast<size_t>(cc.index(k));
+        maxDisp = smax(maxDisp, length(cc.corner(k) - mk(Q[0], Q[1], Q[2])));
     }
     bool boundary = insideCoarser && (cell[0] == 0 || cell[0] + 2 == c.res[0] || cell[1] == 0 ||
                                       cell[1] + 2 == c.res[1] || cell[2] == 0 || cell[2] + 2 == c.res[2]);
@@ -916,7 +922,17 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
     bool wantMvc = maxDisp > mvcFrac * c.spacing || boundary;
     bool haveMvc = false;
     if (wantMvc) {
-        haveMvc = mvcWeightsHex<M>(corners, point, w, slab);
+        if (slab) {
+            MvcArrays<M, true> a(slab);
+            haveMvc = mvcWeightsHexImpl<M, true>(cc, point, a);
+            if (haveMvc)
+                for (int k = 0; k < 8; ++k) w[k] = double(a.wts(k));
+        } else {
+            MvcArrays<M, false> a(slab);
+            haveMvc = mvcWeightsHexImpl<M, false>(cc, point, a);
+            if (haveMvc)
+                for (int k = 0; k < 8; ++k) w[k] = double(a.wts(k));
+        }
         if (haveMvc) {
             for (int k = 0; k < 8; ++k) w[k] = smax(0.0, w[k]);
             st.usedMvc = 1;
@@ -932,7 +948,7 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
     }
     double sum = 0;
     for (int k = 0; k < 8; ++k) {
-        if (!pv.alive[c.base + pidx[k]]) w[k] = 0;
+        if (!pv.alive[cc.index(k)]) w[k] = 0;
         sum += w[k];
     }
     if (sum <= 1e-12) {
@@ -940,7 +956,7 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
         return st;
     }
     for (int k = 0; k < 8; ++k) {
-        st.probe[k] = pidx[k];
+        st.probe[k] = cc.index(k) - c.base;
         st.w[k] = w[k] / sum;
     }
     st.cascade = chosen;
