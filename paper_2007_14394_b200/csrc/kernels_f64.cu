@@ -86,14 +86,17 @@ __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells
         }
         return g2;
     };
-    // Lower bound of candidate j's SDF anywhere in the (padded) cell: every
-    // primitive SDF is an exact signed distance (primitives.hpp:42-65), hence
-    // 1-Lipschitz, so SDF_j(p) >= SDF_j(centre) - (half padded diagonal); the
-    // build margin covers the evaluation's rounding (and the FP32 mode's). Much
-    // tighter than the distance to j's bounding box, so queries stop earlier.
+    // Lower bounds of candidate j's SDF: every primitive SDF is an exact signed
+    // distance (primitives.hpp:42-65), hence 1-Lipschitz, so SDF_j(p) >=
+    // SDF_j(centre) - |p - centre| (the query's bound) >= SDF_j(centre) - (half
+    // padded diagonal) (the cell's); the build margin covers the evaluation's
+    // rounding (and the FP32 mode's). Much tighter than the distance to j's
+    // bounding box, so queries stop earlier.
     const V3<double> centre = mk(0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2]));
     const double half = 0.5 * sqrt(3.0) * (P.h + 2.0 * P.pad);
-    auto lowerBound = [&](int j) { return evalPrim<double>(P.scene.prims[j], centre) - half - P.margin; };
+    // centre value E_j = SDF_j(centre) - margin (what the entry stores: a query at p
+    // bounds j by E_j - |p - centre|); E_j - half bounds j over the whole cell
+    auto centreValue = [&](int j) { return evalPrim<double>(P.scene.prims[j], centre) - P.margin; };
     // candidate PRIMITIVES: members of nearby clusters (or of an unbounded one) whose
     // bounding box is within r of the cell and whose lower bound does not exceed the
     // cell's upper bound U on the scene SDF — only those can attain (or tie) the
@@ -110,16 +113,18 @@ __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells
             for (int j = P.scene.cstart[k]; j < P.scene.cstart[k + 1]; ++j) {
                 const double* b = P.primBox + 6 * static_cast<size_t>(j);
                 if (!(cl.unbounded || isinf(b[0]) || gap2(b, b + 3) <= r2)) continue;
-                double boxLb = -INFINITY;
+                // the box bound at the centre (<= SDF_j(centre) when the centre is
+                // outside j's box): box distance - margin
+                double boxE = -INFINITY;
                 if (!isinf(b[0])) {
                     const double gx = fmax(fmax(b[0] - centre.x, centre.x - b[3]), 0.0);
                     const double gy = fmax(fmax(b[1] - centre.y, centre.y - b[4]), 0.0);
                     const double gz = fmax(fmax(b[2] - centre.z, centre.z - b[5]), 0.0);
                     const double g2 = gx * gx + gy * gy + gz * gz;
-                    if (g2 > 0) boxLb = sqrt(g2) - half - P.margin;
+                    if (g2 > 0) boxE = sqrt(g2) - P.margin;
                 }
-                if (boxLb > U) continue;  // its SDF bound (>= the box bound) exceeds U too
-                if (f(j, boxLb)) return;
+                if (boxE - half > U) continue;  // its SDF bound (>= the box bound) exceeds U too
+                if (f(j, boxE)) return;
             }
         }
     };
@@ -127,7 +132,7 @@ __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells
     if (!fill) {  // the list length, min(n, K + 1): the walk stops at K + 1
         int n = 0;
         forEach([&](int j, double) {
-            if (lowerBound(j) <= U) ++n;
+            if (centreValue(j) - half <= U) ++n;
             return n > K;
         });
         P.counts[cell] = n;
@@ -144,21 +149,21 @@ __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells
     int2* E = P.entry + out;
     int m = 0;
     float tail = INFINITY;
-    forEach([&](int v, double boxLb) {
+    forEach([&](int v, double boxE) {
         if (m == K) {
             // a full list: a candidate whose box bound is already no better than the
-            // K-th entry's is pushed out without its (costlier) SDF bound; the box
-            // bound, below its SDF bound, still bounds it in the sentinel
+            // K-th entry's is pushed out without its (costlier) SDF value; the box
+            // bound, below its SDF value, still bounds it in the sentinel
             const float kl = __int_as_float(E[K - 1].x);
-            const float kb = __double2float_rd(boxLb);
+            const float kb = __double2float_rd(boxE);
             if (!(kb < kl)) {
                 tail = fminf(tail, kb);  // (conservative even if v fails the U test)
                 return false;
             }
         }
-        const double lb = lowerBound(v);
-        if (!(lb <= U)) return false;
-        const float kv = __double2float_rd(lb);
+        const double cv = centreValue(v);
+        if (!(cv - half <= U)) return false;
+        const float kv = __double2float_rd(cv);
         if (m == K) {
             const float kl = __int_as_float(E[K - 1].x);
             if (!(kv < kl)) {

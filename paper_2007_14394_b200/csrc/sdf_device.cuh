@@ -135,13 +135,15 @@ struct GridDev {
     double invH;
     float flo[3];   // the same in float for the FP32 path
     float finvH;
+    double h;       // cell size (cell centres: lo + (i + 1/2) h)
     int dim[3];
     int bvhRoot;    // code of the root (see BNode); meaningless when nBounded == 0
     const int* __restrict__ start;  // ncells + 1
-    // per list entry, one 8-byte load: x = the bits of a float lower bound on that
-    // primitive's SDF anywhere in the cell (box distance to the cell centre - padded
-    // half diagonal, rounded down), y = its CSR position (-1: sentinel). Entries are
-    // sorted by the bound, so a query stops at the first bound > its minimum.
+    // per list entry, one 8-byte load: x = the bits of a float lower bound E on that
+    // primitive's SDF at the cell centre c (minus the build margin, rounded down), y =
+    // its CSR position (-1: sentinel). Every primitive SDF is 1-Lipschitz, so at a
+    // query point p the primitive is at least E - |p - c| away; entries are sorted by
+    // E, so a query stops at the first E - |p - c| > its running minimum.
     const int2* __restrict__ entry;
     const BNode* __restrict__ bvh;
     const int* __restrict__ unbounded;  // cluster ids of the unbounded clusters
@@ -346,6 +348,7 @@ __device__ __forceinline__ void visitMembers(const SceneView<R>& s, int k, V3<R>
 template <typename R> struct QueryState {
     V3<R> p;
     R d;
+    R r;  // an upper bound on |p - centre of its cell| (candidate-grid walks)
     int own;
     int cur, end;
     bool walk;  // the query completes through hierarchyWalk
@@ -413,9 +416,11 @@ __device__ __forceinline__ void hierarchyWalk(const SceneView<R>& s, QueryState<
     }
 }
 
-// The candidate-grid cell holding p, or -1 off the grid.
+// The candidate-grid cell holding p, or -1 off the grid. With r: also an upper
+// bound on p's distance to the cell centre (float, rounded outwards: 1e-5 relative
+// covers every rounding of the float arithmetic and of the centre's position).
 template <typename R>
-__device__ __forceinline__ int gridCell(const GridDev& g, V3<R> p) {
+__device__ __forceinline__ int gridCell(const GridDev& g, V3<R> p, R* r = nullptr) {
     const bool f32 = sizeof(R) == 4;
     const R lx = f32 ? R(g.flo[0]) : R(g.lo[0]), ly = f32 ? R(g.flo[1]) : R(g.lo[1]);
     const R lz = f32 ? R(g.flo[2]) : R(g.lo[2]), ih = f32 ? R(g.finvH) : R(g.invH);
@@ -427,6 +432,12 @@ __device__ __forceinline__ int gridCell(const GridDev& g, V3<R> p) {
     int ix = min(static_cast<int>(fx), g.dim[0] - 1);
     int iy = min(static_cast<int>(fy), g.dim[1] - 1);
     int iz = min(static_cast<int>(fz), g.dim[2] - 1);
+    if (r) {  // (f - i - 1/2) h, in cell units first: no cancellation against the grid origin
+        const float dx = static_cast<float>(fx - R(ix)) - 0.5f, dy = static_cast<float>(fy - R(iy)) - 0.5f,
+                    dz = static_cast<float>(fz - R(iz)) - 0.5f;
+        const float h = static_cast<float>(g.h);
+        *r = R(sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))) * h * 1.00001f);
+    }
     return ix + g.dim[0] * (iy + g.dim[1] * iz);
 }
 
@@ -450,7 +461,7 @@ __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R ini
         return;
     }
     const GridDev& g = s.grid;
-    const int cell = gridCell<R>(g, p);
+    const int cell = gridCell<R>(g, p, &q.r);
     if (cell >= 0) {
         q.cur = g.start[cell];
         q.end = g.start[cell + 1];
@@ -485,7 +496,7 @@ __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int*
     if (q.cur < q.end) {
         int2 e = __ldg(&s.grid.entry[q.cur]);
         while (true) {
-            if (R(__int_as_float(e.x)) > q.d) break;  // this and every later candidate is farther
+            if (R(__int_as_float(e.x)) > q.d + q.r) break;  // this and every later candidate is farther
             ++q.cur;
             const bool more = q.cur < q.end;
             int2 en = make_int2(0, -1);

@@ -667,6 +667,7 @@ void buildGrid(Ctx* c) {
         c->gridBox[3 + a] = lo[a] + dim[a] * h;
     }
     c->grid.invH = 1.0 / h;
+    c->grid.h = h;
     for (int a = 0; a < 3; ++a) c->grid.flo[a] = static_cast<float>(lo[a]);
     c->grid.finvH = static_cast<float>(1.0 / h);
     c->grid.start = c->gridStart.p;
