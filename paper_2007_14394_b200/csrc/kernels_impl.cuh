@@ -426,11 +426,14 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
         V3<R> p = o;
         R initD = R(0);
         bool parkIt = false;
+        int cell = kCellUnknown;  // phase 0: p's cell (parking test), reused by the query
+        R cellR = R(0);
         if (active) {
             if (state == 2 && !fresh) t += d;
             fresh = false;
             p = o + dir * t;
-            parkIt = PHASE == 0 && park && gridCell<R>(P.scene.grid, p) < 0;
+            if (PHASE == 0 && P.scene.useGrid) cell = gridCell<R>(P.scene.grid, p, &cellR);
+            parkIt = PHASE == 0 && park && cell < 0;
             if (parkIt) {
             } else if (state == 0) {
                 if (ST) ++cnt.steps;
@@ -477,7 +480,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
         }
         int o2 = -1;
         R nd = R(0);
-        if (active) nd = query<R, ST>(P.scene, p, initD, &o2, &cnt, PHASE ? seed : -1);
+        if (active) nd = query<R, ST>(P.scene, p, initD, &o2, &cnt, PHASE ? seed : -1, cell, cellR);
         if (active) {
             if (o2 >= 0) seed = o2;
             int done = 0;  // 1 converged, 2 TMax, 3 StepLimit
@@ -700,8 +703,11 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shad
         bool want = active && step < maxSteps && t < tEnd;
         V3<R> p = o;
         if (want) p = o + dir * t;
+        int cell = kCellUnknown;  // phase 0: p's cell (parking test), reused by the query
+        R cellR = R(0);
+        if (PHASE == 0 && want && P.scene.useGrid) cell = gridCell<R>(P.scene.grid, p, &cellR);
         if (PHASE == 0) {
-            bool parkIt = want && park && gridCell<R>(P.scene.grid, p) < 0;
+            bool parkIt = want && park && cell < 0;
             const long long ps = parkSlot(P.ctr + kCtrParkShadow, parkIt);
             if (ps >= static_cast<long long>(parkCap)) parkIt = false;  // buffer full
             if (parkIt) {
@@ -726,7 +732,8 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shad
         if (ST && want) ++cnt.steps;
         R d = R(0);
         int o2 = -1;
-        if (want) d = query<R, ST>(P.scene, p, lastD == inf ? inf : R(2) * lastD, &o2, &cnt, PHASE ? seed : -1);
+        if (want)
+            d = query<R, ST>(P.scene, p, lastD == inf ? inf : R(2) * lastD, &o2, &cnt, PHASE ? seed : -1, cell, cellR);
         if (o2 >= 0) seed = o2;
         if (active) {
             bool done = false;

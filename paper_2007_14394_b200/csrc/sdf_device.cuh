@@ -441,8 +441,13 @@ __device__ __forceinline__ int gridCell(const GridDev& g, V3<R> p, R* r = nullpt
     return ix + g.dim[0] * (iy + g.dim[1] * iz);
 }
 
+constexpr int kCellUnknown = -2;  // queryBegin computes p's cell itself
+
+// cellHint / rHint: p's candidate-grid cell (-1 off the grid) and distance bound
+// when the caller has them already (the persistent kernels' parking test).
 template <typename R, bool ST>
-__device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R initD, QueryState<R>& q, Counters* c) {
+__device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R initD, QueryState<R>& q, Counters* c,
+                                           int cellHint = kCellUnknown, R rHint = R(0)) {
     q.p = p;
     q.d = initD;
     q.own = -1;
@@ -461,7 +466,8 @@ __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R ini
         return;
     }
     const GridDev& g = s.grid;
-    const int cell = gridCell<R>(g, p, &q.r);
+    q.r = rHint;
+    const int cell = cellHint == kCellUnknown ? gridCell<R>(g, p, &q.r) : cellHint;
     if (cell >= 0) {
         q.cur = g.start[cell];
         q.end = g.start[cell + 1];
@@ -476,9 +482,10 @@ __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R ini
 // a sentinel (-1) whose bound covers every omitted candidate; a query still open
 // there completes through the cluster hierarchy.
 template <typename R, bool ST>
-__device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int* owner, Counters* c, int seed = -1) {
+__device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int* owner, Counters* c, int seed = -1,
+                                   int cellHint = kCellUnknown, R rHint = R(0)) {
     QueryState<R> q;
-    queryBegin<R, ST>(s, p, initD, q, c);
+    queryBegin<R, ST>(s, p, initD, q, c, cellHint, rHint);
     // seed (candidate-grid walks only, which break ties by CSR position in any
     // visiting order): evaluate a likely owner first — e.g. the previous step's
     // — so the hierarchy prunes against a tight minimum from its first node
