@@ -68,7 +68,8 @@ template <typename R> struct __align__(16) ParkRay {
     R t, lastD, d, tMax;
     int step, state, pol, owner;
     unsigned long long rid;
-    int seed, pad;  // last known nearest primitive (query seed of the far phase)
+    int seed;  // last known nearest primitive (query seed of the far phase)
+    int item;  // the ray's position in the trace order (its hitAt slot)
 };
 // A Contact GI ray prepared by k_contact_setup (tMax < 0: sky pixel, no ray).
 template <typename R> struct __align__(16) ContactRay {
@@ -114,7 +115,11 @@ template <typename R> struct WaveParams {
     const double* fib;        // sphericalFibonacci table: n=N (N xyz) then n=2N (2N xyz)
     const int* perm;          // coherent trace order of the sample indices: n=N then n=2N
     HitRec<R>* hits;          // per ray
-    int* hitList;             // compacted ray ids of converged hits with an owner
+    int* hitList;             // compacted ray ids of converged hits with an owner, in trace order
+    int* hitAt;               // per trace-order item: its ray id if a lit hit, else -1 (compacted to hitList)
+    void* selTemp;            // CUB temporary storage of the compaction
+    size_t selTempBytes;
+    long long maxItems;       // hitAt slots (the batch's upper bound of rays)
     R* vis;                   // per (ray, light)
     R* rad;                   // per ray: shaded radiance (3)
     // [kCtrRay] K1 ray cursor, [kCtrHits] hit count, [kCtrShadow] K2 item cursor,
@@ -272,6 +277,9 @@ void launch_grid_list(const GridBuildParams& p, int ncells, bool fill, cudaStrea
 void launch_brick_clusters(const GridBuildParams& p, int nbricks, bool fill, cudaStream_t st);
 // exclusive prefix sum of n ints on the device (CUB); temp == null: returns the bytes needed
 size_t scan_ints(const int* in, int* out, int n, void* temp, size_t tempBytes, cudaStream_t st);
+// hitList = the ids >= 0 of hitAt in order, *count = their number (CUB select); temp == null: bytes needed
+size_t compact_hits(const int* hitAt, int* hitList, unsigned long long* count, int n, void* temp, size_t tempBytes,
+                    cudaStream_t st);
 
 constexpr int kWaveThreads = 128;   // K1/K2 persistent CTAs
 // WaveParams::ctr slots, each on its own 128-byte line: the work cursors and

@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
     V3<R> o = mk(R(0), R(0), R(0)), dir = o;
     R t = 0, lastD = 0, d = 0, tMax = 0;
     int step = 0, state = 0, pol = 0, owner = -1, seed = -1;
+    int titem = 0;       // the ray's trace-order position (its hitAt slot)
     bool fresh = false;  // resumed march: its pending t += d was applied before parking
     while (true) {
         __syncwarp();
@@ -354,6 +355,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                 pol = r.pol;
                 owner = r.owner;
                 seed = r.seed;
+                titem = r.item;
                 rid = r.rid;
                 active = true;
                 fresh = true;
@@ -368,6 +370,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                 while (P.rayStart[s + 1] <= static_cast<long long>(item)) ++s;
             }
             if (got) {
+            titem = static_cast<int>(item);
             R startBound = R(INFINITY);
             bool ok = true;
             if (MODE == 0) {
@@ -412,6 +415,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                 h.owner = -1;
                 h.status = 0;
                 P.hits[rid] = h;
+                P.hitAt[titem] = -1;
             }
             if (ST && ok) ++cnt.sphere;
             if (ok && maxSteps <= 0) {  // loop never runs: StepLimit
@@ -423,6 +427,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                 h.owner = -1;
                 h.status = 2 << 1;
                 P.hits[rid] = h;
+                P.hitAt[titem] = -1;
                 P.rad[3 * rid] = R(P.scene.sky[0]);
                 P.rad[3 * rid + 1] = R(P.scene.sky[1]);
                 P.rad[3 * rid + 2] = R(P.scene.sky[2]);
@@ -486,6 +491,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                 r.owner = owner;
                 r.rid = rid;
                 r.seed = seed;
+                r.item = titem;
                 active = false;
             }
         }
@@ -543,17 +549,9 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                 }
                 active = false;
             }
-            // compaction of converged hits with an owner (the only ones shadeHit lights)
-            const bool lit = done == 1 && owner >= 0;
-            const unsigned m = __ballot_sync(__activemask(), lit);
-            if (lit) {
-                const int leader = __ffs(m) - 1;
-                const unsigned lane = threadIdx.x & 31;
-                unsigned long long base = 0;
-                if (static_cast<int>(lane) == leader) base = atomicAdd(P.ctr + kCtrHits, static_cast<unsigned long long>(__popc(m)));
-                base = __shfl_sync(m, base, leader);
-                P.hitList[base + __popc(m & ((1u << lane) - 1u))] = static_cast<int>(rid);
-            }
+            // converged hits with an owner (the only ones shadeHit lights) are
+            // compacted after the kernel, in trace order (coherent K2/K3a warps)
+            if (done) P.hitAt[titem] = (done == 1 && owner >= 0) ? static_cast<int>(rid) : -1;
         }
     }
     if (ST) flushCounters(cnt, P.stats);
@@ -1017,8 +1015,11 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
     static int b2 = persistentBlocks(k_trace_shadow<R, ST, 0>, kWaveThreads, 0);
     static int b2f = persistentBlocks(k_trace_shadow<R, ST, 1>, kWaveThreads, 0);
     static int b3 = persistentBlocks(k_shade_rays<R, ST>, 128, 0, 128 * kMvcSlab * sizeof(R));
+    // hitAt covers the batch's upper bound of rays; slots past the traced ones stay -1
+    cudaMemsetAsync(p.hitAt, 0xff, static_cast<size_t>(p.maxItems) * sizeof(int), st);
     k_trace_primary<R, ST, 0, 0><<<cap > 0 ? min(cap, b1) : b1, kWaveThreads, 0, st>>>(p);
     k_trace_primary<R, ST, 0, 1><<<cap > 0 ? min(cap, b1f) : b1f, kWaveThreads, 0, st>>>(p);
+    compact_hits(p.hitAt, p.hitList, p.ctr + kCtrHits, static_cast<int>(p.maxItems), p.selTemp, p.selTempBytes, st);
     k_hit_normals<R><<<b3, 128, 0, st>>>(p);
     k_trace_shadow<R, ST, 0><<<cap > 0 ? min(cap, b2) : b2, kWaveThreads, 0, st>>>(p);
     k_trace_shadow<R, ST, 1><<<cap > 0 ? min(cap, b2f) : b2f, kWaveThreads, 0, st>>>(p);
@@ -1034,7 +1035,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
         k3<<<p.nCand, kConvThreads, smem, st>>>(p);
     }
     if (e1) cudaEventRecord(e1, st);
-    if (launches) *launches += p.debug ? 9 : 10;
+    if (launches) *launches += p.debug ? 10 : 11;
 }
 
 // contactGI's per-pixel sum (shading.hpp:686-713): AO from the missed samples,
@@ -1092,13 +1093,14 @@ static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long*
     static int b3 = persistentBlocks(k_shade_rays<R, ST>, 128, 0, 128 * kMvcSlab * sizeof(R));
     k_trace_primary<R, ST, 1, 0><<<b1, kWaveThreads, 0, st>>>(p);
     k_trace_primary<R, ST, 1, 1><<<b1f, kWaveThreads, 0, st>>>(p);
+    compact_hits(p.hitAt, p.hitList, p.ctr + kCtrHits, static_cast<int>(p.maxItems), p.selTemp, p.selTempBytes, st);
     k_hit_normals<R><<<b3, 128, 0, st>>>(p);
     k_trace_shadow<R, ST, 0><<<b2, kWaveThreads, 0, st>>>(p);
     k_trace_shadow<R, ST, 1><<<b2f, kWaveThreads, 0, st>>>(p);
     k_shade_rays<R, ST><<<b3, 128, 128 * kMvcSlab * sizeof(R), st>>>(p);
     const long long np = static_cast<long long>(p.gw) * p.gh;
     k_contact_combine<R><<<static_cast<int>((np + 127) / 128), 128, 0, st>>>(p);
-    if (launches) *launches += p.cray ? 8 : 7;
+    if (launches) *launches += p.cray ? 9 : 8;
 }
 
 // composeFrame (shading.hpp:480-504) as a wavefront: every geometry pixel becomes a

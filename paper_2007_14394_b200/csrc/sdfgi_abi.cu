@@ -170,12 +170,12 @@ struct Ctx {
     DBuf<int> refs;
     DBuf<RayRecord> records;
     // wavefront scratch (kernels.cuh)
-    DBuf<int> wRayCount, wHitList, wChunk;
+    DBuf<int> wRayCount, wHitList, wChunk, wHitAt;
     DBuf<long long> wRayStart;
     DBuf<double> wRot, fib;
     DBuf<int> perm;
     int fibN = -1;
-    DBuf<unsigned char> wHits, wVis, wRad, wPark, wCRay, wSRay;
+    DBuf<unsigned char> wHits, wVis, wRad, wPark, wCRay, wSRay, wSelTemp;
     DBuf<unsigned long long> wCtr;
     int persistCap = 0;  // 0 = occupancy-sized persistent grids
     // gather (e): G-buffer, stage buffers, history (pipeline.hpp:213-218)
@@ -201,7 +201,7 @@ struct Ctx {
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
-        wRayCount.free(); wHitList.free(); wChunk.free(); wRayStart.free(); wRot.free(); fib.free(); wHits.free();
+        wRayCount.free(); wHitList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); wHits.free();
         wVis.free(); wPark.free(); wCRay.free(); wSRay.free(); wCtr.free(); perm.free(); wRad.free();
         gbuf.free(); halfDepth.free(); sparseIrr.free(); resolved.free(); indirect.free(); histIrr.free(); composed.free();
         histDepth.free(); halfSrc.free(); sel.free(); sparseValid.free(); sparseAnchor.free();
@@ -750,6 +750,19 @@ void reservePark(Ctx* c, size_t rays, int lights) {
     reserve(c->wPark, std::max<size_t>(std::min(need, cap), 64));
 }
 
+// The trace-order hit slots and the compaction's temporary storage for n items.
+template <typename R>
+void reserveHitAt(Ctx* c, WaveParams<R>& p, size_t n) {
+    n = std::max<size_t>(n, 1);
+    reserve(c->wHitAt, n);
+    const size_t need = compact_hits(nullptr, nullptr, nullptr, static_cast<int>(n), nullptr, 0, c->stream);
+    reserve(c->wSelTemp, std::max<size_t>(need, 16));
+    p.hitAt = c->wHitAt.p;
+    p.selTemp = c->wSelTemp.p;
+    p.selTempBytes = c->wSelTemp.n;
+    p.maxItems = static_cast<long long>(n);
+}
+
 template <typename R>
 WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand) {
     const int N = static_cast<int>(cfg->n_rays_full);
@@ -797,6 +810,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.rad = reinterpret_cast<R*>(c->wRad.p);
     p.ctr = c->wCtr.p;
     p.sray = reinterpret_cast<ShadowRay<R>*>(c->wSRay.p);
+    reserveHitAt<R>(c, p, maxRays);
     p.srayCap = std::max<size_t>(maxRays, 1);
     p.park = c->accel && c->haveGrid && c->wPark.n >= 4096 ? c->wPark.p : nullptr;  // SDFGI_PARK_MB=0: off
     p.parkBytes = p.park ? c->wPark.n : 0;
@@ -1640,6 +1654,7 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     p.rad = reinterpret_cast<R*>(c->wRad.p);
     p.ctr = c->wCtr.p;
     p.sray = reinterpret_cast<ShadowRay<R>*>(c->wSRay.p);
+    reserveHitAt<R>(c, p, cap);
     p.srayCap = cap;
     p.park = c->accel && c->haveGrid && c->wPark.n >= 4096 ? c->wPark.p : nullptr;  // SDFGI_PARK_MB=0: off
     p.parkBytes = p.park ? c->wPark.n : 0;

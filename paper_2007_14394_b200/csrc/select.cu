@@ -112,6 +112,18 @@ int launch_select(const SelectParams& P, int budget, cudaStream_t st, long long*
     return n;
 }
 
+struct NonNegative {
+    __device__ __forceinline__ bool operator()(int x) const { return x >= 0; }
+};
+size_t compact_hits(const int* hitAt, int* hitList, unsigned long long* count, int n, void* temp, size_t tempBytes,
+                    cudaStream_t st) {
+    size_t need = 0;
+    cub::DeviceSelect::If(nullptr, need, hitAt, hitList, count, n, NonNegative(), st);
+    if (temp == nullptr) return need;
+    cub::DeviceSelect::If(temp, tempBytes, hitAt, hitList, count, n, NonNegative(), st);
+    return need;
+}
+
 size_t scan_ints(const int* in, int* out, int n, void* temp, size_t tempBytes, cudaStream_t st) {
     size_t need = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need, in, out, n, st);
