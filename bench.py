@@ -435,7 +435,7 @@ def e2e_run(args, dev, stage, scene, barrier, dist, torch):
             res = api.updateProbes(dev, stage.cfg, p)
             r += int(res["rays_traced"])
             dev.swap()
-        atlas_host[:] = dev.atlas(0, 0)
+        dev.atlas(0, 0, out=atlas_host)  # straight into the pinned buffer
         dt = time.perf_counter() - t0
         if i > 0:  # first iteration is a warm-up
             total += dt

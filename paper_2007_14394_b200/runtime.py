@@ -375,10 +375,15 @@ class Device:
     def swap(self):
         _call("sdfgi_atlas_swap", self._ctx)
 
-    def atlas(self, level, which=0) -> np.ndarray:
-        """which 0 = front (read) atlas, 1 = back (write). Shape [P, R+2, R+2, 3]."""
+    def atlas(self, level, which=0, out=None) -> np.ndarray:
+        """which 0 = front (read) atlas, 1 = back (write). Shape [P, R+2, R+2, 3].
+        out: a C-contiguous float32 array of that size (e.g. pinned) to download into."""
         t = self.oct_res + 2
-        out = np.zeros((self.probe_count(level), t, t, 3), np.float32)
+        shape = (self.probe_count(level), t, t, 3)
+        if out is None:
+            out = np.zeros(shape, np.float32)
+        elif out.dtype != np.float32 or not out.flags.c_contiguous or out.size != int(np.prod(shape)):
+            raise ValueError("atlas out: C-contiguous float32 array of %s expected" % (shape,))
         _call("sdfgi_atlas_download", self._ctx, level, which, _ptr(out), out.size)
         return out
 
