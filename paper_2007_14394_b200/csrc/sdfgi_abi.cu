@@ -495,7 +495,10 @@ void buildGrid(Ctx* c) {
     // 2M cells 17.4 ms, 4M 16.6, 8M 15.9, 16M 15.5, 24M 15.3 (margin 0.6, round-1
     // kernels); with the SDF-bound lists and the min-extent margin 33M -> 50M -> 66M
     // cells: C2 13.9 / 12.3 / 12.9 ms, C4 0.28 / 0.37 / 0.34 Grays/s
-    double target = env ? std::atof(env) : 50331648.0;
+    // Small scenes need far fewer cells (and an animated scene rebuilds its grid
+    // every frame): 25k cells per primitive, between 2M and 50M.
+    const double byPrims = std::min(50331648.0, std::max(2097152.0, 25000.0 * c->nPrims));
+    double target = env ? std::atof(env) : byPrims;
     if (target < 1) return;
     double h = std::cbrt(ext[0] * ext[1] * ext[2] / target);
     int dim[3];
