@@ -274,6 +274,7 @@ void launch_relocate(const RelocParams& p, int nProbes, bool stats, cudaStream_t
 void launch_query_points(const QueryParams& p, cudaStream_t st);
 void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st);
 void launch_grid_list(const GridBuildParams& p, int ncells, bool fill, cudaStream_t st);
+void launch_grid_cells(const int* start, const int2* entry, int4* cell, int ncells, cudaStream_t st);
 void launch_brick_clusters(const GridBuildParams& p, int nbricks, bool fill, cudaStream_t st);
 // exclusive prefix sum of n ints on the device (CUB); temp == null: returns the bytes needed
 size_t scan_ints(const int* in, int* out, int n, void* temp, size_t tempBytes, cudaStream_t st);

@@ -186,6 +186,18 @@ __global__ void __launch_bounds__(128) k_grid_list(GridBuildParams P, int ncells
         E[m] = make_int2(__float_as_int(tail), -1);
 }
 
+// The per-cell records (GridDev::cell): list range and first entry.
+__global__ void __launch_bounds__(256) k_grid_cells(const int* start, const int2* entry, int4* cell, int ncells) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncells) return;
+    const int b = start[c], e = start[c + 1];
+    const int2 f = b < e ? entry[b] : make_int2(__float_as_int(INFINITY), -1);
+    cell[c] = make_int4(b, e, f.x, f.y);
+}
+void launch_grid_cells(const int* start, const int2* entry, int4* cell, int ncells, cudaStream_t st) {
+    k_grid_cells<<<(ncells + 255) / 256, 256, 0, st>>>(start, entry, cell, ncells);
+}
+
 void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st) {
     k_grid_bound<<<(ncells + 127) / 128, 128, 0, st>>>(p, ncells);
 }

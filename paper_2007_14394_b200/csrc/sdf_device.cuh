@@ -139,6 +139,10 @@ struct GridDev {
     int dim[3];
     int bvhRoot;    // code of the root (see BNode); meaningless when nBounded == 0
     const int* __restrict__ start;  // ncells + 1
+    // per cell, one 16-byte load: x = start, y = end of its entries, (z, w) = its
+    // first entry (bound bits, CSR position; (+inf, -1) for an empty list) — the
+    // list range and the first candidate without a second dependent load
+    const int4* __restrict__ cell;
     // per list entry, one 8-byte load: x = the bits of a float lower bound E on that
     // primitive's SDF at the cell centre c (minus the build margin, rounded down), y =
     // its CSR position (-1: sentinel). Every primitive SDF is 1-Lipschitz, so at a
@@ -351,6 +355,7 @@ template <typename R> struct QueryState {
     R r;  // an upper bound on |p - centre of its cell| (candidate-grid walks)
     int own;
     int cur, end;
+    int2 first;  // the list's first entry (from the cell record)
     bool walk;  // the query completes through hierarchyWalk
 };
 
@@ -469,8 +474,10 @@ __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R ini
     q.r = rHint;
     const int cell = cellHint == kCellUnknown ? gridCell<R>(g, p, &q.r) : cellHint;
     if (cell >= 0) {
-        q.cur = g.start[cell];
-        q.end = g.start[cell + 1];
+        const int4 rec = __ldg(&g.cell[cell]);
+        q.cur = rec.x;
+        q.end = rec.y;
+        q.first = make_int2(rec.z, rec.w);
         if (ST) c->pe += q.end - q.cur;
         return;
     }
@@ -501,7 +508,7 @@ __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int*
         }
     }
     if (q.cur < q.end) {
-        int2 e = __ldg(&s.grid.entry[q.cur]);
+        int2 e = q.first;
         while (true) {
             if (R(__int_as_float(e.x)) > q.d + q.r) break;  // this and every later candidate is farther
             ++q.cur;

@@ -138,6 +138,7 @@ struct Ctx {
     long long gridEntries = 0;
     DBuf<int> gridStart, gridList, gridCounts;
     DBuf<int2> gridEntry;
+    DBuf<int4> gridCell;
     DBuf<int> brickCounts, brickStart, brickList;
     DBuf<unsigned char> scanTemp;
     DBuf<double> gridU, primBox;
@@ -196,7 +197,7 @@ struct Ctx {
         if (stream) cudaStreamSynchronize(stream);
         prim64.free(); prim32.free(); cl64.free(); cl32.free(); cstart.free(); orig.free();
         albedo.free(); emission.free(); lights.free(); kindId.free();
-        gridStart.free(); gridList.free(); gridCounts.free(); gridU.free(); gridEntry.free(); brickCounts.free(); brickStart.free(); brickList.free(); scanTemp.free();
+        gridStart.free(); gridList.free(); gridCounts.free(); gridU.free(); gridEntry.free(); gridCell.free(); brickCounts.free(); brickStart.free(); brickList.free(); scanTemp.free();
         bvh.free(); unbList.free(); primBox.free();
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
@@ -662,6 +663,9 @@ void buildGrid(Ctx* c) {
     p.start = c->gridStart.p;
     launch_grid_list(p, static_cast<int>(ncells), true, c->stream);
     checkLaunch(c);
+    c->gridCell.alloc(ncells);
+    launch_grid_cells(c->gridStart.p, c->gridEntry.p, c->gridCell.p, static_cast<int>(ncells), c->stream);
+    checkLaunch(c);
     CK(cudaStreamSynchronize(c->stream));
     for (int a = 0; a < 3; ++a) {
         c->grid.lo[a] = lo[a];
@@ -674,6 +678,7 @@ void buildGrid(Ctx* c) {
     for (int a = 0; a < 3; ++a) c->grid.flo[a] = static_cast<float>(lo[a]);
     c->grid.finvH = static_cast<float>(1.0 / h);
     c->grid.start = c->gridStart.p;
+    c->grid.cell = c->gridCell.p;
     c->grid.entry = c->gridEntry.p;
     c->gridEntries = total;
 
