@@ -857,6 +857,10 @@ __device__ inline bool mvcWeightsHexImpl(const CellCorners& cc, V3<double> xd, M
             const M sh = sa[0] * ca[1] * ca[2] + ca[0] * sa[1] * ca[2] + ca[0] * ca[1] * sa[2] - sa[0] * sa[1] * sa[2];
             M c[3], sv[3];
             bool skip = false;
+            // FP64: the three divisions by st_j st_k through one reciprocal of
+            // st_0 st_1 st_2 (1 / (st_j st_k) = st_i / P; a few ulps, far inside the
+            // range: a triangle with a product below eps is skipped)
+            const M invP = sizeof(M) == 8 ? M(1) / (st[0] * st[1] * st[2]) : M(0);
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 const int j = (i + 1) % 3, k = (i + 2) % 3;
@@ -864,17 +868,25 @@ __device__ inline bool mvcWeightsHexImpl(const CellCorners& cc, V3<double> xd, M
                 // sin(h - theta_i) = sin(a_j + a_k - a_i)
                 const M sjk = sa[j] * ca[k] + ca[j] * sa[k], cjk = ca[j] * ca[k] - sa[j] * sa[k];
                 const M shi = sjk * ca[i] - cjk * sa[i];
-                c[i] = mvcDiv(M(2) * sh * shi, denom) - M(1);
+                if (sizeof(M) == 8)
+                    c[i] = M(2) * sh * shi * (st[i] * invP) - M(1);
+                else
+                    c[i] = mvcDiv(M(2) * sh * shi, denom) - M(1);
                 sv[i] = sign * sqrt(smax(M(0), M(1) - c[i] * c[i]));
                 // the reference stops at the first degenerate i (mean_value.hpp:80-86);
                 // the values after it are unused either way
                 skip = skip || fabs(denom) < eps || fabs(sv[i]) <= eps;
             }
             if (skip) continue;
+            M D[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) D[i] = d[i] * st[(i + 1) % 3] * sv[(i + 2) % 3];
+            const M invQ = sizeof(M) == 8 ? M(1) / (D[0] * D[1] * D[2]) : M(0);  // FP64: one division
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 const int j = (i + 1) % 3, k = (i + 2) % 3;
-                const M w = mvcDiv(theta[i] - c[j] * theta[k] - c[k] * theta[j], d[i] * st[j] * sv[k]);
+                const M num = theta[i] - c[j] * theta[k] - c[k] * theta[j];
+                const M w = sizeof(M) == 8 ? num * (D[j] * D[k] * invQ) : mvcDiv(num, D[i]);
                 a.wts(tri[i]) += w;
                 any = true;
             }
