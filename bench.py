@@ -77,7 +77,38 @@ def ncu_step_traffic(precision):
     return total, os.path.relpath(files[-1], ROOT)
 
 
-HBM_KERNELS = ("k_convolve", "k_downsample", "k_select", "k_resolve", "k_contact_combine", "k_compose")
+# Memory-side kernels reported against the HBM roofline. k_convolve (the atlas
+# blend) is not among them: its 64-texel x n-ray cosine sums keep the FP64 pipe
+# ~77% busy (profiles/r01_ncu_step_f64_v6.json) while it moves 2 KB per probe.
+HBM_KERNELS = ("k_downsample", "k_select", "k_resolve", "k_contact_combine", "k_compose")
+
+
+def ncu_pipe_kernels(precision):
+    """Per-kernel pipe utilisation of the hot update kernels from the committed
+    `ncu --set full` capture summary (profiles/r01_ncu_step_<prec>_v*.json, newest):
+    the FP64 / FMA pipe cycles active, issue slots busy and active threads per
+    issued instruction (the divergence that bounds the tracing kernels)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r01_ncu_step_{precision}_v*.json")),
+                   key=lambda f: int(re.search(r"_v(\d+)\.json$", f).group(1)))
+    if not files:
+        return None
+    caps = json.load(open(files[-1])).get("full_captures", [])
+    out = {}
+    for c in caps:
+        name = re.sub(r"\(.*", "", c.get("Kernel Name", "")).replace("void ", "")
+        try:
+            out[name] = {
+                "ms": float(c["gpu__time_duration.sum"]),
+                "fp64_pipe_pct": float(c["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]),
+                "fma_pipe_pct": float(c["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"]),
+                "issue_active_pct": float(c["smsp__issue_active.avg.pct_of_peak_sustained_active"]),
+                "threads_per_inst": float(c["smsp__thread_inst_executed_per_inst_executed.ratio"]),
+            }
+        except (KeyError, ValueError):
+            continue
+    return {"source": os.path.relpath(files[-1], ROOT), "kernels": out}
 
 
 def ncu_hbm_kernels(precision, hbm_peak):
@@ -359,6 +390,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": launches,
         "roofline": roofline,
         "roofline_hbm_kernels": ncu_hbm_kernels(args.precision, hbm_peak),
+        "pipe_kernels_ncu": ncu_pipe_kernels(args.precision),
         "clocks": clk.summary(),
         "algorithmic_counters_step": work_all,
         "gather_c3": gather,
