@@ -250,6 +250,7 @@ struct GridBuildParams {
     // (a superset of every cell's, ascending cluster order), so a cell scans its
     // brick's clusters instead of all of them
     int bdim[3];
+    int* bSeed;   // per brick: the nearest primitive (CSR) at its centre, seeds the cells' bound queries
     int* bCounts;
     const int* bStart;
     int* bList;
@@ -273,6 +274,7 @@ void launch_gather(const GatherParams<R>& p, int stage, bool stats, cudaStream_t
 void launch_relocate(const RelocParams& p, int nProbes, bool stats, cudaStream_t st);
 void launch_query_points(const QueryParams& p, cudaStream_t st);
 void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st);
+void launch_grid_seed(const GridBuildParams& p, int nbricks, cudaStream_t st);
 void launch_grid_list(const GridBuildParams& p, int ncells, bool fill, cudaStream_t st);
 void launch_grid_cells(const int* start, const int2* entry, int4* cell, int ncells, cudaStream_t st);
 void launch_brick_clusters(const GridBuildParams& p, int nbricks, bool fill, cudaStream_t st);

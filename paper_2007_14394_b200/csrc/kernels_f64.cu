@@ -17,13 +17,28 @@ __global__ void __launch_bounds__(128) k_query_points(QueryParams P) {
     P.outOwner[i] = owner >= 0 ? P.scene.orig[owner] : -1;
 }
 
+// The nearest primitive at each brick centre (exact query; the seed of its cells').
+__global__ void __launch_bounds__(128) k_grid_seed(GridBuildParams P, int nbricks) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nbricks) return;
+    const int bx = b % P.bdim[0], by = (b / P.bdim[0]) % P.bdim[1], bz = b / (P.bdim[0] * P.bdim[1]);
+    const double hb = 0.5 * kBrick * P.h;
+    V3<double> c = mk(P.lo[0] + bx * kBrick * P.h + hb, P.lo[1] + by * kBrick * P.h + hb, P.lo[2] + bz * kBrick * P.h + hb);
+    Counters cnt;
+    int owner = -1;
+    query<double, false>(P.scene, c, INFINITY, &owner, &cnt);
+    P.bSeed[b] = owner;
+}
+
 __global__ void __launch_bounds__(128) k_grid_bound(GridBuildParams P, int ncells) {
     const int cell = blockIdx.x * blockDim.x + threadIdx.x;
     if (cell >= ncells) return;
     const int ix = cell % P.dim[0], iy = (cell / P.dim[0]) % P.dim[1], iz = cell / (P.dim[0] * P.dim[1]);
     V3<double> c = mk(P.lo[0] + (ix + 0.5) * P.h, P.lo[1] + (iy + 0.5) * P.h, P.lo[2] + (iz + 0.5) * P.h);
     Counters cnt;
-    double f = query<double, false>(P.scene, c, INFINITY, nullptr, &cnt);
+    // exact whatever the seed (the walk breaks ties by CSR position)
+    const int seed = P.bSeed[ix / kBrick + P.bdim[0] * (iy / kBrick + P.bdim[1] * (iz / kBrick))];
+    double f = query<double, false>(P.scene, c, INFINITY, nullptr, &cnt, seed);
     double half = 0.5 * sqrt(3.0) * (P.h + 2.0 * P.pad);
     P.U[cell] = f + half * (1.0 + 1e-12) + P.margin;
 }
@@ -196,6 +211,10 @@ __global__ void __launch_bounds__(256) k_grid_cells(const int* start, const int2
 }
 void launch_grid_cells(const int* start, const int2* entry, int4* cell, int ncells, cudaStream_t st) {
     k_grid_cells<<<(ncells + 255) / 256, 256, 0, st>>>(start, entry, cell, ncells);
+}
+
+void launch_grid_seed(const GridBuildParams& p, int nbricks, cudaStream_t st) {
+    k_grid_seed<<<(nbricks + 127) / 128, 128, 0, st>>>(p, nbricks);
 }
 
 void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st) {

@@ -139,7 +139,7 @@ struct Ctx {
     DBuf<int> gridStart, gridList, gridCounts;
     DBuf<int2> gridEntry;
     DBuf<int4> gridCell;
-    DBuf<int> brickCounts, brickStart, brickList;
+    DBuf<int> brickCounts, brickStart, brickList, brickSeed;
     DBuf<unsigned char> scanTemp;
     DBuf<double> gridU, primBox;
     DBuf<BNode> bvh;
@@ -197,7 +197,7 @@ struct Ctx {
         if (stream) cudaStreamSynchronize(stream);
         prim64.free(); prim32.free(); cl64.free(); cl32.free(); cstart.free(); orig.free();
         albedo.free(); emission.free(); lights.free(); kindId.free();
-        gridStart.free(); gridList.free(); gridCounts.free(); gridU.free(); gridEntry.free(); gridCell.free(); brickCounts.free(); brickStart.free(); brickList.free(); scanTemp.free();
+        gridStart.free(); gridList.free(); gridCounts.free(); gridU.free(); gridEntry.free(); gridCell.free(); brickCounts.free(); brickStart.free(); brickList.free(); brickSeed.free(); scanTemp.free();
         bvh.free(); unbList.free(); primBox.free();
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
@@ -621,14 +621,20 @@ void buildGrid(Ctx* c) {
     p.primBox = c->primBox.p;
     p.U = c->gridU.p;
     p.counts = c->gridCounts.p;
-    launch_grid_bound(p, static_cast<int>(ncells), c->stream);
-    checkLaunch(c);
-    // bricks of kBrick^3 cells and their candidate clusters
+    // bricks of kBrick^3 cells: the nearest primitive at each brick centre seeds the
+    // exact queries of its cells' bounds (the BVH walk then prunes against a tight
+    // minimum from its first node), and each brick lists its candidate clusters
     long long nbricks = 1;
     for (int a = 0; a < 3; ++a) {
         p.bdim[a] = (dim[a] + kBrick - 1) / kBrick;
         nbricks *= p.bdim[a];
     }
+    c->brickSeed.alloc(nbricks);
+    p.bSeed = c->brickSeed.p;
+    launch_grid_seed(p, static_cast<int>(nbricks), c->stream);
+    checkLaunch(c);
+    launch_grid_bound(p, static_cast<int>(ncells), c->stream);
+    checkLaunch(c);
     c->brickCounts.alloc(nbricks + 1);
     c->brickStart.alloc(nbricks + 1);
     CK(cudaMemsetAsync(c->brickCounts.p + nbricks, 0, 4, c->stream));
