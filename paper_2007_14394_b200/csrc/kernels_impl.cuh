@@ -7,6 +7,29 @@ namespace sdfgi_dev {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Streaming (evict-first) stores and loads of the per-ray wavefront records
+// (hit records, radiance, visibility, shadow rays: written once, read once), so
+// the hundreds of MB they stream through L2 per pass do not evict the candidate
+// grid and the primitive records the tracing kernels re-read.
+template <typename T>
+__device__ __forceinline__ void stStream(T* dst, const T& v) {
+    static_assert(sizeof(T) % 16 == 0 && alignof(T) >= 16, "16-byte records");
+    const int4* s = reinterpret_cast<const int4*>(&v);
+    int4* d = reinterpret_cast<int4*>(dst);
+#pragma unroll
+    for (int i = 0; i < static_cast<int>(sizeof(T) / 16); ++i) __stcs(d + i, s[i]);
+}
+template <typename T>
+__device__ __forceinline__ T ldStream(const T* src) {
+    static_assert(sizeof(T) % 16 == 0 && alignof(T) >= 16, "16-byte records");
+    T v;
+    const int4* s = reinterpret_cast<const int4*>(src);
+    int4* d = reinterpret_cast<int4*>(&v);
+#pragma unroll
+    for (int i = 0; i < static_cast<int>(sizeof(T) / 16); ++i) d[i] = __ldcs(s + i);
+    return v;
+}
+
 __device__ __forceinline__ int cascadeOf(const ProbeCommon& pc, int gp) {
     int ci = 0;
     for (int k = 1; k < pc.nCas; ++k)
@@ -541,11 +564,11 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                     h.t = R(0);
                     h.status = ((done == 2 ? 1 : 2) << 1) | ((done == 2 ? step + 1 : maxSteps) << 8);
                 }
-                P.hits[rid] = h;
+                stStream(&P.hits[rid], h);
                 if (!(done == 1 && owner >= 0)) {  // shadeHit's miss branch: K3a shades only the hit list
-                    P.rad[3 * rid] = R(P.scene.sky[0]);
-                    P.rad[3 * rid + 1] = R(P.scene.sky[1]);
-                    P.rad[3 * rid + 2] = R(P.scene.sky[2]);
+                    __stcs(&P.rad[3 * rid], R(P.scene.sky[0]));
+                    __stcs(&P.rad[3 * rid + 1], R(P.scene.sky[1]));
+                    __stcs(&P.rad[3 * rid + 2], R(P.scene.sky[2]));
                 }
                 active = false;
             }
@@ -622,7 +645,7 @@ __device__ __forceinline__ void shadowSetup(const WaveParams<R>& P, unsigned am,
             r.tEnd = tMax - bias;
             r.rid = rid;
             r.li = li;
-            P.sray[li * P.srayCap + base + __popc(m & ((1u << lane) - 1u))] = r;
+            stStream(&P.sray[li * P.srayCap + base + __popc(m & ((1u << lane) - 1u))], r);
         }
     }
 }
@@ -693,7 +716,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shad
             int li = 0;
             unsigned long long k = item;
             while (li + 1 < L && k >= P.ctr[kLightCtr + li]) k -= P.ctr[kLightCtr + li++];
-            const ShadowRay<R> r = P.sray[li * P.srayCap + k];
+            const ShadowRay<R> r = ldStream(&P.sray[li * P.srayCap + k]);
             o = mk(r.o[0], r.o[1], r.o[2]);
             dir = mk(r.dir[0], r.dir[1], r.dir[2]);
             t = r.t;
@@ -761,7 +784,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shad
                 }
             }
             if (done) {
-                P.vis[slot] = v;
+                __stcs(&P.vis[slot], v);
                 active = false;
             }
         }
@@ -845,16 +868,16 @@ __global__ void __launch_bounds__(128, WaveOcc<R>::shade) k_shade_rays(WaveParam
     unsigned long long nShaded = 0, nMvc = 0;  // shading work (ST): shadeHit calls, MVC evaluations
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
         const long long rid = all ? i : static_cast<long long>(P.hitList[i]);
-        const HitRec<R> h = P.hits[rid];
+        const HitRec<R> h = ldStream(&P.hits[rid]);
         int mvc = 0;
         const V3<double> L = shadeRay(P, h, static_cast<unsigned long long>(rid), slab, ST ? &mvc : nullptr);
         if (ST && (h.status & 1) && h.owner >= 0) {
             ++nShaded;
             nMvc += mvc;
         }
-        P.rad[3 * rid] = R(L.x);
-        P.rad[3 * rid + 1] = R(L.y);
-        P.rad[3 * rid + 2] = R(L.z);
+        __stcs(&P.rad[3 * rid], R(L.x));
+        __stcs(&P.rad[3 * rid + 1], R(L.y));
+        __stcs(&P.rad[3 * rid + 2], R(L.z));
         if (P.debug) {
             const int s = findCandidate(P.rayStart, P.nCand, rid);
             const int i = static_cast<int>(rid - P.rayStart[s]);
@@ -916,7 +939,7 @@ __global__ void __launch_bounds__(kConvThreads) k_convolve(WaveParams<R> P) {
         sdir[3 * i + 1] = R(dir.y);
         sdir[3 * i + 2] = R(dir.z);
     }
-    for (int k = threadIdx.x; k < 3 * n; k += blockDim.x) srad[k] = P.rad[3 * start + k];
+    for (int k = threadIdx.x; k < 3 * n; k += blockDim.x) srad[k] = __ldcs(&P.rad[3 * start + k]);
     __syncthreads();
 
     const int res = P.oct;
