@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(256) k_contact_setup(WaveParams<R> P) {
         r.tMax = R(-1);
         r.startBound = R(0);
     }
-    reinterpret_cast<ContactRay<R>*>(P.cray)[i] = r;
+    stStream(reinterpret_cast<ContactRay<R>*>(P.cray) + i, r);
 }
 
 // Warp-aggregated slot in a parking buffer (all 32 lanes call; -1 = not parked).
@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
         unsigned long long item;
         if (PHASE == 1) {
             if (fetchItem(P.ctr + kCtrFarRay, static_cast<unsigned long long>(total), active, exhausted, item, chunk)) {
-                const ParkRay<R>& r = park[item];
+                const ParkRay<R> r = ldStream(&park[item]);
                 o = mk(r.o[0], r.o[1], r.o[2]);
                 dir = mk(r.dir[0], r.dir[1], r.dir[2]);
                 t = r.t;
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
             } else {
                 rid = item;
                 if (P.cray) {
-                    const ContactRay<R> r = reinterpret_cast<const ContactRay<R>*>(P.cray)[item];
+                    const ContactRay<R> r = ldStream(reinterpret_cast<const ContactRay<R>*>(P.cray) + item);
                     o = mk(r.o[0], r.o[1], r.o[2]);
                     dir = mk(r.dir[0], r.dir[1], r.dir[2]);
                     tMax = r.tMax;
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                 }
             }
             if (parkIt) {
-                ParkRay<R>& r = park[ps];
+                ParkRay<R> r;
                 r.o[0] = o.x;
                 r.o[1] = o.y;
                 r.o[2] = o.z;
@@ -515,6 +515,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                 r.rid = rid;
                 r.seed = seed;
                 r.item = titem;
+                stStream(&park[ps], r);
                 active = false;
             }
         }
@@ -698,7 +699,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shad
         unsigned long long item;
         if (PHASE == 1) {
             if (fetchItem(P.ctr + kCtrFarShadow, total, active, exhausted, item, chunk)) {
-                const ParkShadow<R>& r = park[item];
+                const ParkShadow<R> r = ldStream(&park[item]);
                 o = mk(r.o[0], r.o[1], r.o[2]);
                 dir = mk(r.dir[0], r.dir[1], r.dir[2]);
                 t = r.t;
@@ -744,7 +745,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shad
             const long long ps = parkSlot(P.ctr + kCtrParkShadow, parkIt);
             if (ps >= static_cast<long long>(parkCap)) parkIt = false;  // buffer full
             if (parkIt) {
-                ParkShadow<R>& r = park[ps];
+                ParkShadow<R> r;
                 r.o[0] = o.x;
                 r.o[1] = o.y;
                 r.o[2] = o.z;
@@ -758,6 +759,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shad
                 r.step = step;
                 r.seed = seed;
                 r.slot = slot;
+                stStream(&park[ps], r);
                 active = false;
                 want = false;
             }
