@@ -315,7 +315,13 @@ template <typename R> struct WaveOcc {
     static constexpr int shade = SDFGI_SHADE_MINB;
 };
 constexpr int kShadeThreads = 128;  // per-ray shading
-constexpr int kConvThreads = 192;   // K3b CTA per probe: one thread per (texel, channel) at R = 8
+// K3b CTA per probe: one thread per texel summing its three channels over the
+// rays (one cosine per (texel, ray) instead of three), or per (texel, channel)
+#ifndef SDFGI_CONV_TEXEL
+#define SDFGI_CONV_TEXEL 1
+#endif
+constexpr bool kConvPerTexel = SDFGI_CONV_TEXEL != 0;
+constexpr int kConvThreads = kConvPerTexel ? 64 : 192;
 constexpr int kScanThreads = 1024;  // K0 prefix sum
 
 }  // namespace sdfgi_dev

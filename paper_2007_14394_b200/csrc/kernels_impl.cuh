@@ -950,6 +950,31 @@ __global__ void __launch_bounds__(kConvThreads) k_convolve(WaveParams<R> P) {
     const double scale = 4.0 * kPi / static_cast<double>(n);
     const float* oldTile = P.prevAtlas + static_cast<size_t>(g) * T * T * 3;
     double maxDelta = 0.0;
+    if (kConvPerTexel) {
+        for (int tx = threadIdx.x; tx < res * res; tx += blockDim.x) {
+            const int y = tx / res, x = tx % res;
+            const V3<double> dd = octDecode(V2<double>{(x + 0.5) / res, (y + 0.5) / res});
+            const R Dx = R(dd.x), Dy = R(dd.y), Dz = R(dd.z);
+            R a0 = 0, a1 = 0, a2 = 0;  // each channel summed in the rays' order
+            for (int i = 0; i < n; ++i) {
+                const R w = Dx * sdir[3 * i] + Dy * sdir[3 * i + 1] + Dz * sdir[3 * i + 2];
+                if (w > R(0)) {
+                    a0 = a0 + srad[3 * i] * w;
+                    a1 = a1 + srad[3 * i + 1] * w;
+                    a2 = a2 + srad[3 * i + 2] * w;
+                }
+            }
+            const R acc[3] = {a0, a1, a2};
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                const double fresh = double(acc[ch]) * scale;
+                const double old = oldTile[((y + 1) * T + (x + 1)) * 3 + ch];
+                const double bl = old + (fresh - old) * alpha;
+                maxDelta = smax(maxDelta, fabs(bl - old));
+                tile[((y + 1) * T + (x + 1)) * 3 + ch] = static_cast<float>(bl);
+            }
+        }
+    } else
     for (int item = threadIdx.x; item < 3 * res * res; item += blockDim.x) {
         const int tx = item / 3, ch = item % 3;
         const int y = tx / res, x = tx % res;
