@@ -153,6 +153,7 @@ struct GridDev {
     const int* __restrict__ unbounded;  // cluster ids of the unbounded clusters
     int nUnbounded;
     int nBounded;
+    float walkSlack;  // FP64 walks' float box tests: > the float rounding of |p - box| at this scale
 };
 
 template <typename R> struct SceneView {
@@ -376,12 +377,61 @@ __device__ __forceinline__ bool boxReaches(R boxSq, R d) {
     return d > R(0) ? boxSq <= d * d : boxSq <= R(0);
 }
 
+// The node box tests in float for both precisions (the boxes are float already):
+// with p rounded to float, the float box distance is within walkSlack of the exact
+// one, so a subtree is kept whenever dist - walkSlack <= d. That keeps every
+// subtree the exact test keeps (and a few more): the walk stays exact.
 template <typename R, bool ST>
 __device__ __forceinline__ void hierarchyWalk(const SceneView<R>& s, QueryState<R>& q, Counters* c) {
     const GridDev& g = s.grid;
     const V3<R> p = q.p;
     for (int i = 0; i < g.nUnbounded; ++i) visitMembers<R, ST, true>(s, g.unbounded[i], p, q.d, q.own, c);
     if (g.nBounded == 0) return;
+    if constexpr (sizeof(R) == 8) {
+        // FP64: float box tests with the slack (keep iff |p - box| <= max(d, 0) + slack)
+        const V3<float> pf = mk(float(p.x), float(p.y), float(p.z));
+        int stackN[kBvhStack];
+        float stackB[kBvhStack];
+        int sp = 0;
+        int next = g.bvhRoot;
+        auto reach = [&](float b) {
+            const float r = fmaxf(float(q.d), 0.f) * 1.000001f + g.walkSlack;
+            return b <= r * r;
+        };
+        while (true) {
+            if (next >= 0) {
+                const BNode& n = g.bvh[next];
+                const float b0 = boxDistSq<float>(n.lo[0], n.hi[0], pf), b1 = boxDistSq<float>(n.lo[1], n.hi[1], pf);
+                const bool k0 = reach(b0), k1 = reach(b1);
+                if (k0 && k1) {
+                    const int nr = b1 < b0 ? 1 : 0;
+                    stackN[sp] = n.child[1 - nr];
+                    stackB[sp] = nr ? b0 : b1;
+                    ++sp;
+                    next = n.child[nr];
+                    continue;
+                }
+                if (k0 || k1) {
+                    next = n.child[k0 ? 0 : 1];
+                    continue;
+                }
+                if (ST) c->cs += 2;
+            } else {
+                visitMembers<R, ST, true>(s, -next - 1, p, q.d, q.own, c);
+            }
+            bool more = false;
+            while (sp > 0) {
+                --sp;
+                if (reach(stackB[sp])) {
+                    next = stackN[sp];
+                    more = true;
+                    break;
+                }
+            }
+            if (!more) break;
+        }
+        return;
+    }
     int stackN[kBvhStack];
     R stackB[kBvhStack];
     int sp = 0;

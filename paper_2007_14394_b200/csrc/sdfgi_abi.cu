@@ -584,6 +584,9 @@ void buildGrid(Ctx* c) {
     c->grid.bvh = c->bvh.p;
     c->grid.bvhRoot = root;
     c->grid.nBounded = static_cast<int>(ids.size());
+    // FP64 walks test node boxes in float; the slack bounds the float rounding of
+    // a point-box distance at this coordinate scale (hierarchyWalk)
+    c->grid.walkSlack = static_cast<float>(4e-5 * (scale + 1.0));
     c->grid.unbounded = c->unbList.p;
     c->grid.nUnbounded = static_cast<int>(unb.size());
     GridBuildParams p;
@@ -681,6 +684,7 @@ void buildGrid(Ctx* c) {
     }
     c->grid.invH = 1.0 / h;
     c->grid.h = h;
+
     for (int a = 0; a < 3; ++a) c->grid.flo[a] = static_cast<float>(lo[a]);
     c->grid.finvH = static_cast<float>(1.0 / h);
     c->grid.start = c->gridStart.p;
