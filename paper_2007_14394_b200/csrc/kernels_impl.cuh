@@ -847,7 +847,7 @@ __device__ __forceinline__ V3<double> shadeRay(const WaveParams<R>& P, const Hit
         V3<double> prev;
         V3<double> hp = mk<double>(h.p[0], h.p[1], h.p[2]);
         V3<double> hn = mk<double>(h.n[0], h.n[1], h.n[2]);
-        if (sampleBounceIrradiance<R>(P.pc.cas, P.pc.nCas, P.pc.probes, P.prevAtlas, P.oct, hp, hn, P.tc.mvcFrac, &prev,
+        if (sampleBounceIrradiance<R, true>(P.pc.cas, P.pc.nCas, P.pc.probes, P.prevAtlas, P.oct, hp, hn, P.tc.mvcFrac, &prev,
                                       slab, usedMvc))
             radiance = radiance + brdf * (prev * P.tc.bounceCoeff);
     }

@@ -972,7 +972,9 @@ struct Stencil {
 
 // interpolationStencil, probe_volume.hpp:224-310 (cell and trilinear weights in
 // double in both modes; MVC in precision M)
-template <typename M = double>
+// SLAB_ONLY: the caller always passes a shared slab (K3a), so only that variant
+// of the MVC is compiled in (a second inlined copy cost instruction-cache misses).
+template <typename M = double, bool SLAB_ONLY = false>
 __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, const ProbesView& pv, V3<double> point,
                                         double mvcFrac, M* slab = nullptr) {
     Stencil st;
@@ -1020,12 +1022,12 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
     bool wantMvc = maxDisp > mvcFrac * c.spacing || boundary;
     bool haveMvc = false;
     if (wantMvc) {
-        if (slab) {
+        if (SLAB_ONLY || slab) {
             MvcArrays<M, true> a(slab);
             haveMvc = mvcWeightsHexImpl<M, true>(cc, point, a);
             if (haveMvc)
                 for (int k = 0; k < 8; ++k) w[k] = double(a.wts(k));
-        } else {
+        } else if (!SLAB_ONLY) {
             MvcArrays<M, false> a(slab);
             haveMvc = mvcWeightsHexImpl<M, false>(cc, point, a);
             if (haveMvc)
@@ -1063,12 +1065,12 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
 }
 
 // sampleBounceIrradiance, probe_update.hpp:63-92. Returns false when "empty".
-template <typename M = double>
+template <typename M = double, bool SLAB_ONLY = false>
 __device__ inline bool sampleBounceIrradiance(const CascadeDev* cas, int nCas, const ProbesView& pv,
                                        const float* atlas, int oct, V3<double> pos, V3<double> normal,
                                        double mvcFrac, V3<double>* out, M* slab = nullptr, int* usedMvc = nullptr) {
     if (nCas <= 0) return false;
-    Stencil st = interpolationStencil<M>(cas, nCas, pv, pos, mvcFrac, slab);
+    Stencil st = interpolationStencil<M, SLAB_ONLY>(cas, nCas, pv, pos, mvcFrac, slab);
     if (usedMvc) *usedMvc = st.usedMvc;
     if (st.sky || st.count == 0) return false;
     const CascadeDev& c = cas[st.cascade];
