@@ -355,6 +355,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
     cnt.zero();
     bool active = false, exhausted = false;
     WarpChunk chunk;
+    CellCache ccache;  // FP32 only (FP64 measured 1.5% slower at its 64-register cap)
     unsigned long long rid = 0;
     V3<R> o = mk(R(0), R(0), R(0)), dir = o;
     R t = 0, lastD = 0, d = 0, tMax = 0;
@@ -521,7 +522,9 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
         }
         int o2 = -1;
         R nd = R(0);
-        if (active) nd = query<R, ST>(P.scene, p, initD, &o2, &cnt, PHASE ? seed : -1, cell, cellR);
+        if (active)
+            nd = query<R, ST>(P.scene, p, initD, &o2, &cnt, PHASE ? seed : -1, cell, cellR,
+                              sizeof(R) == 4 ? &ccache : nullptr);
         if (active) {
             if (o2 >= 0) seed = o2;
             int done = 0;  // 1 converged, 2 TMax, 3 StepLimit
@@ -690,6 +693,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shad
     cnt.zero();
     bool active = false, exhausted = false;
     WarpChunk chunk;
+    CellCache ccache;  // FP32 only (FP64 measured 1.5% slower at its 64-register cap)
     unsigned long long slot = 0;
     V3<R> o = mk(R(0), R(0), R(0)), dir = o;
     R t = 0, tEnd = 0, v = 0, lastD = 0;
@@ -768,7 +772,8 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shad
         R d = R(0);
         int o2 = -1;
         if (want)
-            d = query<R, ST>(P.scene, p, lastD == inf ? inf : R(2) * lastD, &o2, &cnt, PHASE ? seed : -1, cell, cellR);
+            d = query<R, ST>(P.scene, p, lastD == inf ? inf : R(2) * lastD, &o2, &cnt, PHASE ? seed : -1, cell, cellR,
+                             sizeof(R) == 4 ? &ccache : nullptr);
         if (o2 >= 0) seed = o2;
         if (active) {
             bool done = false;

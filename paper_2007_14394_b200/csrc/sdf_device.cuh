@@ -498,11 +498,19 @@ __device__ __forceinline__ int gridCell(const GridDev& g, V3<R> p, R* r = nullpt
 
 constexpr int kCellUnknown = -2;  // queryBegin computes p's cell itself
 
+// A lane's last cell record: consecutive steps of a march near a surface (and the
+// owner / polish queries at a converged point) stay in one cell, and reuse its
+// record instead of another dependent load.
+struct CellCache {
+    int cell = -1;
+    int4 rec;
+};
+
 // cellHint / rHint: p's candidate-grid cell (-1 off the grid) and distance bound
 // when the caller has them already (the persistent kernels' parking test).
 template <typename R, bool ST>
 __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R initD, QueryState<R>& q, Counters* c,
-                                           int cellHint = kCellUnknown, R rHint = R(0)) {
+                                           int cellHint = kCellUnknown, R rHint = R(0), CellCache* cache = nullptr) {
     q.p = p;
     q.d = initD;
     q.own = -1;
@@ -524,7 +532,16 @@ __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R ini
     q.r = rHint;
     const int cell = cellHint == kCellUnknown ? gridCell<R>(g, p, &q.r) : cellHint;
     if (cell >= 0) {
-        const int4 rec = __ldg(&g.cell[cell]);
+        int4 rec;
+        if (cache && cache->cell == cell) {
+            rec = cache->rec;
+        } else {
+            rec = __ldg(&g.cell[cell]);
+            if (cache) {
+                cache->cell = cell;
+                cache->rec = rec;
+            }
+        }
         q.cur = rec.x;
         q.end = rec.y;
         q.first = make_int2(rec.z, rec.w);
@@ -540,9 +557,9 @@ __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R ini
 // there completes through the cluster hierarchy.
 template <typename R, bool ST>
 __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int* owner, Counters* c, int seed = -1,
-                                   int cellHint = kCellUnknown, R rHint = R(0)) {
+                                   int cellHint = kCellUnknown, R rHint = R(0), CellCache* cache = nullptr) {
     QueryState<R> q;
-    queryBegin<R, ST>(s, p, initD, q, c, cellHint, rHint);
+    queryBegin<R, ST>(s, p, initD, q, c, cellHint, rHint, cache);
     // seed (candidate-grid walks only, which break ties by CSR position in any
     // visiting order): evaluate a likely owner first — e.g. the previous step's
     // — so the hierarchy prunes against a tight minimum from its first node
