@@ -295,8 +295,8 @@ constexpr int kLightCtr = 112;
 // minimum resident K1/K2/K3a CTAs per SM (register cap = 64K / (128 * n)); the
 // tracing kernels are latency bound at low occupancy (measured, profiles/)
 #ifndef SDFGI_WAVE_MINB64
-#define SDFGI_WAVE_MINB64 8
-#endif
+#define SDFGI_WAVE_MINB64 7  // C2 pass 0 FP64 (K1 / K2 CTAs): 6/7 9.80, 7/6 9.75-9.83, 7/7 9.49-9.57,
+#endif                       // 7/8 9.51-9.55, 8/7 9.67-9.72, 8/8 9.68-9.73, 9/9 10.13-10.21 ms
 #ifndef SDFGI_WAVE_MINB32
 #define SDFGI_WAVE_MINB32 8  // C2 pass 0 FP32: 6 / 7 / 8 / 10 CTAs = 6.33 / 6.24 / 6.16 / 6.32 ms
 #endif
