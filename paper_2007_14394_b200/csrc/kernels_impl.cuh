@@ -60,6 +60,11 @@ __device__ __forceinline__ void flushCounters(const Counters& c, unsigned long l
 #define SDFGI_FETCH_CHUNK 32  // C2 pass 0: 32 -> 64 -> 128 = FP64 10.4 / 10.5 / 10.9 ms
 #endif
 constexpr unsigned long long kFetchChunk = SDFGI_FETCH_CHUNK;
+#ifndef SDFGI_CELL_CACHE64
+#define SDFGI_CELL_CACHE64 0
+#endif
+// K1/K2 per-lane cell-record cache (CellCache) in FP64 too
+template <typename R> __device__ __forceinline__ bool useCellCache() { return sizeof(R) == 4 || SDFGI_CELL_CACHE64 != 0; }
 static_assert(kFetchChunk >= 32, "one fresh chunk must cover a whole warp's request");
 struct WarpChunk {
     unsigned long long next = 0, end = 0;
@@ -355,7 +360,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
     cnt.zero();
     bool active = false, exhausted = false;
     WarpChunk chunk;
-    CellCache ccache;  // FP32 only (FP64 measured 1.5% slower at its 64-register cap)
+    CellCache ccache;  // FP32 only (FP64: 1.5% slower at 64 registers, 2% at 72; SDFGI_CELL_CACHE64)
     unsigned long long rid = 0;
     V3<R> o = mk(R(0), R(0), R(0)), dir = o;
     R t = 0, lastD = 0, d = 0, tMax = 0;
@@ -524,7 +529,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
         R nd = R(0);
         if (active)
             nd = query<R, ST>(P.scene, p, initD, &o2, &cnt, PHASE ? seed : -1, cell, cellR,
-                              sizeof(R) == 4 ? &ccache : nullptr);
+                              useCellCache<R>() ? &ccache : nullptr);
         if (active) {
             if (o2 >= 0) seed = o2;
             int done = 0;  // 1 converged, 2 TMax, 3 StepLimit
@@ -693,7 +698,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shad
     cnt.zero();
     bool active = false, exhausted = false;
     WarpChunk chunk;
-    CellCache ccache;  // FP32 only (FP64 measured 1.5% slower at its 64-register cap)
+    CellCache ccache;  // FP32 only (FP64: 1.5% slower at 64 registers, 2% at 72; SDFGI_CELL_CACHE64)
     unsigned long long slot = 0;
     V3<R> o = mk(R(0), R(0), R(0)), dir = o;
     R t = 0, tEnd = 0, v = 0, lastD = 0;
@@ -773,7 +778,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shad
         int o2 = -1;
         if (want)
             d = query<R, ST>(P.scene, p, lastD == inf ? inf : R(2) * lastD, &o2, &cnt, PHASE ? seed : -1, cell, cellR,
-                             sizeof(R) == 4 ? &ccache : nullptr);
+                             useCellCache<R>() ? &ccache : nullptr);
         if (o2 >= 0) seed = o2;
         if (active) {
             bool done = false;
