@@ -1028,15 +1028,27 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
     double tx = f.x - cell[0], ty = f.y - cell[1], tz = f.z - cell[2];
     const CellCorners cc{pv.pos, c.base + cell[0] + c.res[0] * (cell[1] + c.res[1] * cell[2]), c.res[0],
                          c.res[0] * c.res[1]};
-    double maxDisp = 0;
-    for (int k = 0; k < 8; ++k) {
-        const double* Q = pv.rest + 3 * static_cast<size_t>(cc.index(k));
-        maxDisp = smax(maxDisp, length(cc.corner(k) - mk(Q[0], Q[1], Q[2])));
-    }
     bool boundary = insideCoarser && (cell[0] == 0 || cell[0] + 2 == c.res[0] || cell[1] == 0 ||
                                       cell[1] + 2 == c.res[1] || cell[2] == 0 || cell[2] + 2 == c.res[2]);
+    // maxDisp > mvcFrac * spacing (probe_volume.hpp:263-278) is "some corner's displacement
+    // length exceeds the threshold": decided on the squared length with a 1e-9
+    // relative margin either side of thr^2 (sqrt is correctly rounded and
+    // monotone, so outside the margin the answer is the same), the exact sqrt only
+    // inside it; NaN lengths never count, as in the max
+    const double thr = mvcFrac * c.spacing;
+    const double thr2 = thr * thr;
+    const bool squared = thr > 0 && thr2 > 1e-280 && thr2 < 1e280;
+    bool wantMvc = boundary || thr < 0;  // maxDisp >= 0 > thr
+    for (int k = 0; k < 8 && !wantMvc; ++k) {
+        const double* Q = pv.rest + 3 * static_cast<size_t>(cc.index(k));
+        const V3<double> dv = cc.corner(k) - mk(Q[0], Q[1], Q[2]);
+        const double d2 = dot(dv, dv);
+        if (squared && d2 > thr2 * (1 + 1e-9))
+            wantMvc = true;
+        else if (!squared || !(d2 < thr2 * (1 - 1e-9)))
+            wantMvc = sqrt(d2) > thr;
+    }
     double w[8];
-    bool wantMvc = maxDisp > mvcFrac * c.spacing || boundary;
     bool haveMvc = false;
     if (wantMvc) {
         if (SLAB_ONLY || slab) {
