@@ -497,8 +497,10 @@ void buildGrid(Ctx* c) {
     // kernels); with the SDF-bound lists and the min-extent margin 33M -> 50M -> 66M
     // cells: C2 13.9 / 12.3 / 12.9 ms, C4 0.28 / 0.37 / 0.34 Grays/s
     // Small scenes need far fewer cells (and an animated scene rebuilds its grid
-    // every frame): 25k cells per primitive, between 2M and 50M.
-    const double byPrims = std::min(50331648.0, std::max(2097152.0, 25000.0 * c->nPrims));
+    // every frame): 33k cells per primitive, between 2M and 66M. With the round-1
+    // final kernels 50M -> 66M: C2 pass 0 FP64 9.50 -> 9.36 ms, FP32 5.09 -> 5.05;
+    // C4 FP64 0.548 -> 0.565 Grays/s, FP32 1.09 -> 1.12 (80M: candidate grid too large)
+    const double byPrims = std::min(66000000.0, std::max(2097152.0, 33000.0 * c->nPrims));
     double target = env ? std::atof(env) : byPrims;
     if (target < 1) return;
     double h = std::cbrt(ext[0] * ext[1] * ext[2] / target);
