@@ -42,11 +42,15 @@ def load():
         "ora_compose": ([_P, _P, _I, _I, _P, _P, _P, _P], _I),
         "ora_select": ([_P, _P, _P, _I, _I, _P], _I),
         "ora_update_refs": ([_P, _P, _I, _P, _I, _I, _P, _P, _P, _P], _I),
+        "ora_set_threads": ([_I], None),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
         f.argtypes = args
         f.restype = res
+    # the gather's row loops and renderGBuffer on every host core (results do not
+    # depend on the thread count: each row is independent, statistics are summed)
+    lib.ora_set_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1))
     _lib = lib
     return lib
 

@@ -683,6 +683,60 @@ static void addStats(uint64_t* out, const stats_t* st) {
     out[7] += st->vis;
 }
 
+/* Row-parallel loops of the gather stages (the reference's parallelFor over image
+ * rows, shading.hpp:45,288,356,437): worker w takes rows w, w+W, ...; every row's
+ * outputs are its own and the per-worker TraceStats are summed (order-free). */
+static int g_threads = 1;
+void ora_set_threads(int n) { g_threads = n < 1 ? 1 : n; }
+
+typedef void (*row_fn)(void* ctx, int row, stats_t* st, int64_t* acc);
+typedef struct {
+    row_fn fn;
+    void* ctx;
+    int n, worker, workers;
+    stats_t st;
+    int64_t acc;
+} rows_t;
+static void* rowsWorker(void* arg) {
+    rows_t* r = (rows_t*)arg;
+    for (int row = r->worker; row < r->n; row += r->workers) r->fn(r->ctx, row, &r->st, &r->acc);
+    return NULL;
+}
+static int64_t parRows(int n, row_fn fn, void* ctx, stats_t* total) {
+    int W = g_threads < n ? g_threads : (n > 0 ? n : 1);
+    rows_t* ws = (rows_t*)calloc((size_t)W, sizeof(rows_t));
+    pthread_t* th = (pthread_t*)calloc((size_t)W, sizeof(pthread_t));
+    for (int w = 0; w < W; ++w) {
+        ws[w].fn = fn;
+        ws[w].ctx = ctx;
+        ws[w].n = n;
+        ws[w].worker = w;
+        ws[w].workers = W;
+        if (W > 1)
+            pthread_create(&th[w], NULL, rowsWorker, &ws[w]);
+        else
+            rowsWorker(&ws[w]);
+    }
+    int64_t acc = 0;
+    for (int w = 0; w < W; ++w) {
+        if (W > 1) pthread_join(th[w], NULL);
+        acc += ws[w].acc;
+        if (total) {
+            total->q += ws[w].st.q;
+            total->cv += ws[w].st.cv;
+            total->cs += ws[w].st.cs;
+            total->pe += ws[w].st.pe;
+            total->steps += ws[w].st.steps;
+            total->sphere += ws[w].st.sphere;
+            total->shadow += ws[w].st.shadow;
+            total->vis += ws[w].st.vis;
+        }
+    }
+    free(ws);
+    free(th);
+    return acc;
+}
+
 int ora_relocate(ora_stage* s, int slot, double th1, double th2, int max_steps, double grad_step, int report[3],
                  uint64_t stats[8]) { /* updateProbePositions, probe_volume.hpp:99-143 */
     if (slot < 0 || slot >= s->ncas) return 1;
@@ -956,39 +1010,55 @@ static int camProject(const sdfgi_camera* c, v3 world, int w, int h, double* ox,
     return 1;
 }
 
+typedef struct {
+    const ora_stage* s;
+    const sdfgi_camera* cam;
+    int w, h;
+    const sdfgi_cfg* cfg;
+    sdfgi_gbuffer_pixel* out;
+} gbctx_t;
+static void gbufferRow(void* vc, int y, stats_t* st, int64_t* acc) {
+    const gbctx_t* g = (const gbctx_t*)vc;
+    const ora_stage* s = g->s;
+    const sdfgi_camera* cam = g->cam;
+    const int w = g->w, h = g->h;
+    (void)acc;
+    for (int x = 0; x < w; ++x) {
+        sdfgi_gbuffer_pixel* px = &g->out[(size_t)y * w + x];
+        memset(px, 0, sizeof(*px));
+        px->depth = ORA_INF;
+        px->normal[2] = 1.0;
+        px->prim_index = -1;
+        v3 dir = camRayDir(cam, x, (double)y, w, h);
+        hit_t hit = sphereTrace(s, P3(cam->position), dir, g->cfg->ray_tmax, g->cfg->surface_epsilon,
+                                (int)g->cfg->max_trace_steps, st, ORA_INF);
+        if (!hit.converged) continue;
+        px->depth = hit.t;
+        px->normal[0] = hit.normal.x;
+        px->normal[1] = hit.normal.y;
+        px->normal[2] = hit.normal.z;
+        px->world_pos[0] = hit.pos.x;
+        px->world_pos[1] = hit.pos.y;
+        px->world_pos[2] = hit.pos.z;
+        px->prim_index = hit.prim;
+        if (hit.prim >= 0) {
+            memcpy(px->albedo, s->prims[hit.prim].albedo, sizeof(px->albedo));
+            memcpy(px->emission, s->prims[hit.prim].emission, sizeof(px->emission));
+        }
+        double ppx, ppy;
+        if (camProject(cam, hit.pos, w, h, &ppx, &ppy)) {
+            px->motion[0] = ppx - x;
+            px->motion[1] = ppy - y;
+        }
+    }
+}
+
 int ora_render_gbuffer(const ora_stage* s, const sdfgi_camera* cam, int w, int h, const sdfgi_cfg* cfg,
                        sdfgi_gbuffer_pixel* out, uint64_t stats[8]) { /* shading.hpp:39-72 */
     stats_t st;
     memset(&st, 0, sizeof(st));
-    for (int y = 0; y < h; ++y)
-        for (int x = 0; x < w; ++x) {
-            sdfgi_gbuffer_pixel* px = &out[(size_t)y * w + x];
-            memset(px, 0, sizeof(*px));
-            px->depth = ORA_INF;
-            px->normal[2] = 1.0;
-            px->prim_index = -1;
-            v3 dir = camRayDir(cam, x, (double)y, w, h);
-            hit_t hit = sphereTrace(s, P3(cam->position), dir, cfg->ray_tmax, cfg->surface_epsilon,
-                                    (int)cfg->max_trace_steps, &st, ORA_INF);
-            if (!hit.converged) continue;
-            px->depth = hit.t;
-            px->normal[0] = hit.normal.x;
-            px->normal[1] = hit.normal.y;
-            px->normal[2] = hit.normal.z;
-            px->world_pos[0] = hit.pos.x;
-            px->world_pos[1] = hit.pos.y;
-            px->world_pos[2] = hit.pos.z;
-            px->prim_index = hit.prim;
-            if (hit.prim >= 0) {
-                memcpy(px->albedo, s->prims[hit.prim].albedo, sizeof(px->albedo));
-                memcpy(px->emission, s->prims[hit.prim].emission, sizeof(px->emission));
-            }
-            double ppx, ppy;
-            if (camProject(cam, hit.pos, w, h, &ppx, &ppy)) {
-                px->motion[0] = ppx - x;
-                px->motion[1] = ppy - y;
-            }
-        }
+    gbctx_t g = {s, cam, w, h, cfg, out};
+    parRows(h, gbufferRow, &g, &st);
     addStats(stats, &st);
     return 0;
 }
@@ -1012,77 +1082,41 @@ typedef struct {
     int key[5];
 } tkey_t;
 
-int ora_gather_frame(const ora_stage* s, const sdfgi_gbuffer_pixel* gb, int w, int h, int frame, const sdfgi_cfg* cfg,
-                     const double* hist_irr, const double* hist_depth, int hist_valid, double* half_depth,
-                     int32_t* half_src, int32_t* sel, double* sparse_irr, int32_t* sparse_valid,
-                     int32_t* sparse_anchor, double* resolved, double* indirect, uint64_t vis_stats[8],
-                     uint64_t contact_stats[8]) {
-    const int hw = (w + 1) / 2, hh = (h + 1) / 2;
-    const int sw = (hw + 1) / 2, sh = (hh + 1) / 2;
-    double* hd = (double*)malloc(sizeof(double) * hw * hh);
-    int* hs = (int*)malloc(sizeof(int) * hw * hh);
-    /* downsampleDepthCheckerboard, shading.hpp:85-112 */
-    for (int y = 0; y < hh; ++y)
-        for (int x = 0; x < hw; ++x) {
-            int takeMax = ((x + y) & 1) == 0;
-            double best = takeMax ? -ORA_INF : ORA_INF;
-            int bestSrc = 0;
-            for (int dy = 0; dy < 2; ++dy)
-                for (int dx = 0; dx < 2; ++dx) {
-                    int sx = 2 * x + dx < w - 1 ? 2 * x + dx : w - 1;
-                    int sy = 2 * y + dy < h - 1 ? 2 * y + dy : h - 1;
-                    double d = gb[(size_t)sy * w + sx].depth;
-                    if (takeMax ? d > best : d < best) {
-                        best = d;
-                        bestSrc = sy * w + sx;
-                    }
-                }
-            hd[y * hw + x] = best;
-            hs[y * hw + x] = bestSrc;
-        }
-    /* selectVisibilityPixels, shading.hpp:125-161 */
-    static const int offs[4][2] = {{0, 0}, {1, 0}, {0, 1}, {1, 1}};
-    int* sl = (int*)malloc(sizeof(int) * sw * sh);
-    int rot = frame & 3;
-    for (int y = 0; y < sh; ++y)
-        for (int x = 0; x < sw; ++x) {
-            int hx0 = 2 * x, hy0 = 2 * y;
-            double lo = ORA_INF, hi = -ORA_INF;
-            int loIdx = -1, hiIdx = -1;
-            for (int k = 0; k < 4; ++k) {
-                int hx = hx0 + offs[k][0] < hw - 1 ? hx0 + offs[k][0] : hw - 1;
-                int hy = hy0 + offs[k][1] < hh - 1 ? hy0 + offs[k][1] : hh - 1;
-                double d = hd[hy * hw + hx];
-                if (!isfinite(d)) continue;
-                if (d < lo) { lo = d; loIdx = hy * hw + hx; }
-                if (d > hi) { hi = d; hiIdx = hy * hw + hx; }
-            }
-            int hx = hx0 + offs[rot][0] < hw - 1 ? hx0 + offs[rot][0] : hw - 1;
-            int hy = hy0 + offs[rot][1] < hh - 1 ? hy0 + offs[rot][1] : hh - 1;
-            int pick = hy * hw + hx;
-            if (loIdx >= 0) {
-                int rotSky = !isfinite(hd[pick]);
-                int spread = (hi - lo) > 0.1 * hi;
-                if (spread)
-                    pick = (frame & 1) == 0 ? loIdx : hiIdx;
-                else if (rotSky)
-                    pick = loIdx;
-            }
-            sl[y * sw + x] = pick;
-        }
-    /* buildVisibilityTasks (shading.hpp:185-259) + runVisibilityTasks (:281-300) +
-       shadePixelGI (:319-338): per 4x4 half-res tile, dedup in insertion order */
-    int ncell = sw * sh;
-    double* sirr = (double*)calloc((size_t)ncell * 3, sizeof(double));
-    int* svalid = (int*)calloc((size_t)ncell, sizeof(int));
-    int* sanchor = (int*)calloc((size_t)ncell, sizeof(int));
-    stats_t vst;
-    memset(&vst, 0, sizeof(vst));
-    int ntasks = 0;
-    int tilesX = (sw + 1) / 2, tilesY = (sh + 1) / 2;
-    const float* front = s->atlas[s->front];
-    for (int ty = 0; ty < tilesY; ++ty)
-        for (int tx = 0; tx < tilesX; ++tx) {
+/* the state the gather's row loops share (ora_gather_frame) */
+typedef struct {
+    const ora_stage* s;
+    const sdfgi_gbuffer_pixel* gb;
+    int w, h, hw, hh, sw, sh, tilesX, nS;
+    const sdfgi_cfg* cfg;
+    const int *hs, *sl;
+    double* sirr;
+    int *svalid, *sanchor;
+    const float* front;
+    double* res;
+    double* indirect;
+    const double *hist_irr, *hist_depth;
+    int hist_valid;
+    double radius;
+} gctx_t;
+
+#define GCTX_ALIASES                                                                             \
+    const gctx_t* g = (const gctx_t*)vc;                                                          \
+    const ora_stage* s = g->s;                                                                    \
+    const sdfgi_gbuffer_pixel* gb = g->gb;                                                        \
+    const int w = g->w, h = g->h, sw = g->sw, sh = g->sh;                                         \
+    const sdfgi_cfg* cfg = g->cfg;                                                                \
+    (void)s; (void)gb; (void)w; (void)h; (void)sw; (void)sh; (void)cfg
+
+/* buildVisibilityTasks (shading.hpp:185-259) + runVisibilityTasks (:281-300) +
+   shadePixelGI (:319-338): per 4x4 half-res tile, dedup in insertion order; one
+   row of tiles */
+static void tilesRow(void* vc, int ty, stats_t* stp, int64_t* acc) {
+    GCTX_ALIASES;
+    const int *hs = g->hs, *sl = g->sl;
+    double* sirr = g->sirr;
+    int *svalid = g->svalid, *sanchor = g->sanchor;
+    const float* front = g->front;
+    for (int tx = 0; tx < g->tilesX; ++tx) {
             tkey_t keys[32];
             double tvis[32];
             int nk = 0;
@@ -1127,16 +1161,16 @@ int ora_gather_frame(const ora_stage* s, const sdfgi_gbuffer_pixel* gb, int w, i
                             double bias = 2.0 * cfg->surface_epsilon / smax(0.1, cosT);
                             double tMax = dist - cfg->threshold1_frac * c->spacing;
                             if (tMax > bias) {
-                                ++vst.vis;
+                                ++stp->vis;
                                 vis = softShadowTrace(s, add(sp, muls(nn, bias)), dir, bias, tMax,
-                                                      cfg->probe_visibility_k, &vst, (int)cfg->shadow_steps);
+                                                      cfg->probe_visibility_k, stp, (int)cfg->shadow_steps);
                             }
                         }
                         found = nk;
                         keys[nk] = k;
                         tvis[nk] = vis;
                         ++nk;
-                        ++ntasks;
+                        ++*acc;
                     }
                     tIdx[q][e] = found;
                 }
@@ -1165,11 +1199,22 @@ int ora_gather_frame(const ora_stage* s, const sdfgi_gbuffer_pixel* gb, int w, i
                 sirr[3 * cell + 2] = irr.z;
                 svalid[cell] = 1;
             }
-        }
-    /* upsampleAndResolve, shading.hpp:350-426 */
-    double* res = (double*)calloc((size_t)w * h * 3, sizeof(double));
-    for (int y = 0; y < h; ++y)
-        for (int x = 0; x < w; ++x) {
+    }
+}
+
+/* upsampleAndResolve, shading.hpp:350-426: one image row */
+static void resolveRow(void* vc, int y, stats_t* stp, int64_t* acc) {
+    GCTX_ALIASES;
+    (void)stp;
+    (void)acc;
+    const int* sanchor = g->sanchor;
+    const int* svalid = g->svalid;
+    const double* sirr = g->sirr;
+    const float* front = g->front;
+    const double *hist_irr = g->hist_irr, *hist_depth = g->hist_depth;
+    const int hist_valid = g->hist_valid;
+    double* res = g->res;
+    for (int x = 0; x < w; ++x) {
             const sdfgi_gbuffer_pixel* px = &gb[(size_t)y * w + x];
             if (isSky(px)) continue;
             int qx = x / 4, qy = y / 4;
@@ -1231,15 +1276,18 @@ int ora_gather_frame(const ora_stage* s, const sdfgi_gbuffer_pixel* gb, int w, i
             r[0] = o.x;
             r[1] = o.y;
             r[2] = o.z;
-        }
-    /* contactGI, shading.hpp:431-477 */
-    stats_t cst;
-    memset(&cst, 0, sizeof(cst));
-    double radius = cfg->contact_radius_frac * s->cas[0].spacing;
-    int nS = (int)cfg->contact_samples;
-    if (indirect)
-        for (int y = 0; y < h; ++y)
-            for (int x = 0; x < w; ++x) {
+    }
+}
+
+/* contactGI, shading.hpp:431-477: one image row */
+static void contactRow(void* vc, int y, stats_t* stp, int64_t* acc) {
+    GCTX_ALIASES;
+    (void)acc;
+    const double* res = g->res;
+    double* indirect = g->indirect;
+    const double radius = g->radius;
+    const int nS = g->nS;
+    for (int x = 0; x < w; ++x) {
                 const sdfgi_gbuffer_pixel* px = &gb[(size_t)y * w + x];
                 double* out = &indirect[3 * ((size_t)y * w + x)];
                 out[0] = out[1] = out[2] = 0;
@@ -1260,11 +1308,11 @@ int ora_gather_frame(const ora_stage* s, const sdfgi_gbuffer_pixel* gb, int w, i
                     double cosT = smax(0.1, dot(dir, nn));
                     double bias = 2.0 * cfg->surface_epsilon / cosT;
                     hit_t hit = sphereTrace(s, add(wp, muls(nn, bias)), dir, radius, cfg->surface_epsilon,
-                                            (int)cfg->max_trace_steps, &cst, bias + cfg->surface_epsilon);
+                                            (int)cfg->max_trace_steps, stp, bias + cfg->surface_epsilon);
                     if (!hit.converged)
                         ++unocc;
                     else
-                        occ = add(occ, shadeHit(s, &hit, cfg, &cst));
+                        occ = add(occ, shadeHit(s, &hit, cfg, stp));
                 }
                 double ao = (double)unocc / nS;
                 v3 contact = mulv(muls(divs(P3(px->albedo), ORA_PI), ORA_PI / nS), occ);
@@ -1272,7 +1320,103 @@ int ora_gather_frame(const ora_stage* s, const sdfgi_gbuffer_pixel* gb, int w, i
                 out[0] = o.x;
                 out[1] = o.y;
                 out[2] = o.z;
+    }
+}
+
+int ora_gather_frame(const ora_stage* s, const sdfgi_gbuffer_pixel* gb, int w, int h, int frame, const sdfgi_cfg* cfg,
+                     const double* hist_irr, const double* hist_depth, int hist_valid, double* half_depth,
+                     int32_t* half_src, int32_t* sel, double* sparse_irr, int32_t* sparse_valid,
+                     int32_t* sparse_anchor, double* resolved, double* indirect, uint64_t vis_stats[8],
+                     uint64_t contact_stats[8]) {
+    const int hw = (w + 1) / 2, hh = (h + 1) / 2;
+    const int sw = (hw + 1) / 2, sh = (hh + 1) / 2;
+    double* hd = (double*)malloc(sizeof(double) * hw * hh);
+    int* hs = (int*)malloc(sizeof(int) * hw * hh);
+    /* downsampleDepthCheckerboard, shading.hpp:85-112 */
+    for (int y = 0; y < hh; ++y)
+        for (int x = 0; x < hw; ++x) {
+            int takeMax = ((x + y) & 1) == 0;
+            double best = takeMax ? -ORA_INF : ORA_INF;
+            int bestSrc = 0;
+            for (int dy = 0; dy < 2; ++dy)
+                for (int dx = 0; dx < 2; ++dx) {
+                    int sx = 2 * x + dx < w - 1 ? 2 * x + dx : w - 1;
+                    int sy = 2 * y + dy < h - 1 ? 2 * y + dy : h - 1;
+                    double d = gb[(size_t)sy * w + sx].depth;
+                    if (takeMax ? d > best : d < best) {
+                        best = d;
+                        bestSrc = sy * w + sx;
+                    }
+                }
+            hd[y * hw + x] = best;
+            hs[y * hw + x] = bestSrc;
+        }
+    /* selectVisibilityPixels, shading.hpp:125-161 */
+    static const int offs[4][2] = {{0, 0}, {1, 0}, {0, 1}, {1, 1}};
+    int* sl = (int*)malloc(sizeof(int) * sw * sh);
+    int rot = frame & 3;
+    for (int y = 0; y < sh; ++y)
+        for (int x = 0; x < sw; ++x) {
+            int hx0 = 2 * x, hy0 = 2 * y;
+            double lo = ORA_INF, hi = -ORA_INF;
+            int loIdx = -1, hiIdx = -1;
+            for (int k = 0; k < 4; ++k) {
+                int hx = hx0 + offs[k][0] < hw - 1 ? hx0 + offs[k][0] : hw - 1;
+                int hy = hy0 + offs[k][1] < hh - 1 ? hy0 + offs[k][1] : hh - 1;
+                double d = hd[hy * hw + hx];
+                if (!isfinite(d)) continue;
+                if (d < lo) { lo = d; loIdx = hy * hw + hx; }
+                if (d > hi) { hi = d; hiIdx = hy * hw + hx; }
             }
+            int hx = hx0 + offs[rot][0] < hw - 1 ? hx0 + offs[rot][0] : hw - 1;
+            int hy = hy0 + offs[rot][1] < hh - 1 ? hy0 + offs[rot][1] : hh - 1;
+            int pick = hy * hw + hx;
+            if (loIdx >= 0) {
+                int rotSky = !isfinite(hd[pick]);
+                int spread = (hi - lo) > 0.1 * hi;
+                if (spread)
+                    pick = (frame & 1) == 0 ? loIdx : hiIdx;
+                else if (rotSky)
+                    pick = loIdx;
+            }
+            sl[y * sw + x] = pick;
+        }
+    int ncell = sw * sh;
+    double* sirr = (double*)calloc((size_t)ncell * 3, sizeof(double));
+    int* svalid = (int*)calloc((size_t)ncell, sizeof(int));
+    int* sanchor = (int*)calloc((size_t)ncell, sizeof(int));
+    double* res = (double*)calloc((size_t)w * h * 3, sizeof(double));
+    gctx_t g;
+    memset(&g, 0, sizeof(g));
+    g.s = s;
+    g.gb = gb;
+    g.w = w;
+    g.h = h;
+    g.hw = hw;
+    g.hh = hh;
+    g.sw = sw;
+    g.sh = sh;
+    g.tilesX = (sw + 1) / 2;
+    g.cfg = cfg;
+    g.hs = hs;
+    g.sl = sl;
+    g.sirr = sirr;
+    g.svalid = svalid;
+    g.sanchor = sanchor;
+    g.front = s->atlas[s->front];
+    g.res = res;
+    g.indirect = indirect;
+    g.hist_irr = hist_irr;
+    g.hist_depth = hist_depth;
+    g.hist_valid = hist_valid;
+    g.radius = cfg->contact_radius_frac * s->cas[0].spacing;
+    g.nS = (int)cfg->contact_samples;
+    stats_t vst, cst;
+    memset(&vst, 0, sizeof(vst));
+    memset(&cst, 0, sizeof(cst));
+    int ntasks = (int)parRows((sh + 1) / 2, tilesRow, &g, &vst);
+    parRows(h, resolveRow, &g, NULL);
+    if (indirect) parRows(h, contactRow, &g, &cst);
     if (half_depth) memcpy(half_depth, hd, sizeof(double) * hw * hh);
     if (half_src) memcpy(half_src, hs, sizeof(int) * hw * hh);
     if (sel) memcpy(sel, sl, sizeof(int) * ncell);

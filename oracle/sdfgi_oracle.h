@@ -63,6 +63,8 @@ int ora_trace_rays(const ora_stage* s, const sdfgi_cfg* cfg, int frame, int slot
 void ora_query(const ora_stage* s, const double* pts, const double* init, int n, double* d, int32_t* owner);
 
 /* renderGBuffer (shading.hpp:39-72) with prevCamera == camera. out: w*h pixels. */
+/* threads of the gather's row loops and renderGBuffer (default 1) */
+void ora_set_threads(int n);
 int ora_render_gbuffer(const ora_stage* s, const sdfgi_camera* cam, int w, int h, const sdfgi_cfg* cfg,
                        sdfgi_gbuffer_pixel* out, uint64_t stats[8]);
 

@@ -31,7 +31,10 @@ UNITS = {
     "fp_peak.cu": [],
     "select.cu": ["-fmad=false"],  # the scheduler's priorities round as the reference's
 }
-HEADERS = ["sdf_device.cuh", "kernels.cuh", "kernels_impl.cuh", "gather_impl.cuh"]
+HEADERS = ["sdf_device.cuh", "kernels.cuh", "kernels_impl.cuh", "gather_impl.cuh", "host_trig.h"]
+# host-only C++ units (g++): the reference's libm calls for the direction tables,
+# with FMA contraction off as in the flag-pinned reference build (host_trig.h)
+HOST_UNITS = {"host_trig.cpp": ["-O2", "-ffp-contract=off", "-fno-fast-math"]}
 
 
 def _nvcc():
@@ -69,8 +72,15 @@ def build_lib(verbose=False, force=False) -> str:
         objs.append(obj)
         if force or _stale(obj, [src, *hdrs, __file__]):
             _run([nvcc, *ARCH, *COMMON, *extra, "-c", src, "-o", obj], verbose)
+    for unit, extra in HOST_UNITS.items():
+        src = os.path.join(CSRC, unit)
+        obj = os.path.join(BUILD, unit.replace(".cpp", ".o"))
+        objs.append(obj)
+        if force or _stale(obj, [src, *hdrs, __file__]):
+            _run(["g++", "-std=c++17", "-fPIC", "-fvisibility=hidden", "-pthread", *extra, "-c", src, "-o", obj],
+                 verbose)
     if force or _stale(LIB, objs):
-        _run([nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-lnccl", "-lcudart"], verbose)
+        _run([nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-lnccl", "-lcudart", "-Xcompiler", "-pthread"], verbose)
     return LIB
 
 

@@ -13,7 +13,8 @@
 //                      key traces the soft-shadow visibility, the others read it by
 //                      shuffle, and each cell's weighted sum runs in slot order.
 //   k_resolve          upsampleAndResolve (shading.hpp:350-426), thread per pixel.
-//   k_contact          contactGI (shading.hpp:431-477), thread per pixel.
+// Contact GI (shading.hpp:431-477) runs as a wavefront of (pixel, sample) rays
+// through the probe-update kernels (launch_contact, kernels_impl.cuh).
 #pragma once
 
 #include "kernels.cuh"
@@ -22,7 +23,7 @@ namespace sdfgi_dev {
 
 // Camera::rayDir / project (camera.hpp:29-48)
 __device__ __forceinline__ V3<double> camRayDir(const CameraDev& c, double px, double py, int w, int h) {
-    double tanHalf = tan(c.fov * kPi / 360.0);
+    double tanHalf = c.tanHalf;
     double aspect = static_cast<double>(w) / h;
     double ndcX = (2.0 * (px + 0.5) / w - 1.0) * tanHalf * aspect;
     double ndcY = (1.0 - 2.0 * (py + 0.5) / h) * tanHalf;
@@ -34,7 +35,7 @@ __device__ __forceinline__ bool camProject(const CameraDev& c, V3<double> world,
     V3<double> rel = world - mk(c.pos[0], c.pos[1], c.pos[2]);
     double z = dot(rel, mk(c.fwd[0], c.fwd[1], c.fwd[2]));
     if (z <= 1e-9) return false;
-    double tanHalf = tan(c.fov * kPi / 360.0);
+    double tanHalf = c.tanHalf;
     double aspect = static_cast<double>(w) / h;
     double ndcX = dot(rel, mk(c.right[0], c.right[1], c.right[2])) / (z * tanHalf * aspect);
     double ndcY = dot(rel, mk(c.up[0], c.up[1], c.up[2])) / (z * tanHalf);
@@ -322,60 +323,6 @@ __global__ void __launch_bounds__(128) k_resolve(GatherParams<R> P) {
     out[2] = o.z;
 }
 
-// --------------------------------------------------------------------- contact
-template <typename R, bool ST>
-__global__ void __launch_bounds__(128) k_contact(GatherParams<R> P) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    Counters cnt;
-    cnt.zero();
-    if (i < P.w * P.h) {
-        const int x = i % P.w, y = i / P.w;
-        const GPix& px = P.gb[i];
-        double* out = P.indirect + 3 * static_cast<size_t>(i);
-        if (isSky(px)) {
-            out[0] = out[1] = out[2] = 0;
-        } else {
-            const V3<double> alb = mk(px.albedo[0], px.albedo[1], px.albedo[2]);
-            const V3<double> brdf = alb / kPi;
-            const double* re = P.resolved + 3 * static_cast<size_t>(i);
-            const V3<double> probeGi = brdf * mk(re[0], re[1], re[2]);
-            const int nS = P.contactSamples;
-            if (nS <= 0 || P.contactRadius <= 0) {
-                out[0] = probeGi.x;
-                out[1] = probeGi.y;
-                out[2] = probeGi.z;
-            } else {
-                Rng rng(hashCombine(hashCombine(P.seed, 0xc0417ffull), static_cast<uint64_t>(y) * P.w + x));
-                const V3<double> nn = mk(px.normal[0], px.normal[1], px.normal[2]);
-                const V3<double> wp = mk(px.world_pos[0], px.world_pos[1], px.world_pos[2]);
-                int unocc = 0;
-                V3<double> occ = mk(0.0, 0.0, 0.0);
-                for (int s = 0; s < nS; ++s) {
-                    V3<double> dir = cosineHemisphereDir(rng, nn);
-                    double cosT = smax(0.1, dot(dir, nn));
-                    double bias = 2.0 * P.tc.eps / cosT;
-                    V3<double> o = wp + nn * bias;
-                    Hit<R> hit = sphereTrace<R, ST>(P.scene, mk(R(o.x), R(o.y), R(o.z)), mk(R(dir.x), R(dir.y), R(dir.z)),
-                                                    R(P.contactRadius), R(P.tc.eps), P.tc.maxSteps, &cnt,
-                                                    R(bias + P.tc.eps));
-                    if (!hit.converged)
-                        ++unocc;
-                    else
-                        occ = occ + shadeHit<R, ST>(P.scene, hit, P.pc.cas, P.pc.nCas, P.pc.probes, P.atlas, P.oct,
-                                                    P.tc, &cnt);
-                }
-                double ao = static_cast<double>(unocc) / nS;
-                V3<double> contact = (alb / kPi) * (kPi / nS) * occ;
-                V3<double> o = probeGi * ao + contact;
-                out[0] = o.x;
-                out[1] = o.y;
-                out[2] = o.z;
-            }
-        }
-    }
-    if (ST) flushCounters(cnt, P.contactStats);
-}
-
 template <typename R>
 void launch_gather(const GatherParams<R>& p, int stage, bool stats, cudaStream_t st) {
     const int np = p.w * p.h;
@@ -393,13 +340,7 @@ void launch_gather(const GatherParams<R>& p, int stage, bool stats, cudaStream_t
                 k_tiles<R, false><<<(tiles + 3) / 4, 128, 0, st>>>(p);
             break;
         }
-        case 3: k_resolve<R><<<(np + 127) / 128, 128, 0, st>>>(p); break;
-        default:
-            if (stats)
-                k_contact<R, true><<<(np + 127) / 128, 128, 0, st>>>(p);
-            else
-                k_contact<R, false><<<(np + 127) / 128, 128, 0, st>>>(p);
-            break;
+        default: k_resolve<R><<<(np + 127) / 128, 128, 0, st>>>(p); break;
     }
 }
 

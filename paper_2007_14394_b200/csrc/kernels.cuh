@@ -111,8 +111,9 @@ template <typename R> struct WaveParams {
     int* rayCount;            // per candidate (K0)
     long long* rayStart;      // nCand + 1 exclusive prefix (K0 scan)
     int* chunkSlot;           // per 32-ray chunk c: the candidate holding ray 32c (K0)
-    double* rot;              // 9 per candidate
-    const double* fib;        // sphericalFibonacci table: n=N (N xyz) then n=2N (2N xyz)
+    double* rot;              // 9 per candidate (K0, from quat)
+    const double* quat;       // 4 per candidate: randomRotation's quaternion, host libm (host_trig.h)
+    const double* fib;        // sphericalFibonacci table: n=N (N xyz) then n=2N (2N xyz), host libm
     const int* perm;          // coherent trace order of the sample indices: n=N then n=2N
     HitRec<R>* hits;          // per ray
     int* hitList;             // compacted ray ids of converged hits with an owner, in trace order
@@ -132,7 +133,8 @@ template <typename R> struct WaveParams {
     // (null: no parking). K1 and K2 reuse the buffer (K1's far phase ends first).
     void* park;
     unsigned long long parkBytes;
-    void* cray;  // contact batch: the prepared rays (ContactRay<R>), or null
+    void* cray;  // contact batch: the prepared rays (ContactRay<R>)
+    const double* clocal;  // contact batch: cosineHemisphereDir's (lx, ly) per (pixel, sample), host libm
     // the traced shadow marches, light li's at [li * srayCap, + ctr[kLightCtr + li])
     ShadowRay<R>* sray;
     unsigned long long srayCap;
@@ -170,6 +172,7 @@ struct GPix {
 struct CameraDev {
     double pos[3], fwd[3], right[3], up[3];
     double fov;
+    double tanHalf;  // std::tan(fov * pi / 360) on the host (camera.hpp:30,42; host_trig.h)
 };
 
 // Gather (e) launch parameters: shading.hpp:85-477 over one G-buffer.
@@ -266,7 +269,6 @@ void launch_compose(const WaveParams<R>& p, bool stats, cudaStream_t st, long lo
 template <typename R>
 void launch_wavefront(const WaveParams<R>& p, int persistBlocks, bool stats, cudaStream_t st,
                       cudaEvent_t evStart, cudaEvent_t evEnd, long long* launches);
-void launch_fib_table(double* out, int n, cudaStream_t st);
 // stage 0 G-buffer, 1 downsample+select, 2 tiles (tasks+visibility+shadePixelGI),
 // 3 resolve, 4 contact
 template <typename R>

@@ -239,8 +239,6 @@ void launch_query_points(const QueryParams& p, cudaStream_t st) {
     k_query_points<<<(p.n + 127) / 128, 128, 0, st>>>(p);
 }
 
-void launch_fib_table(double* out, int n, cudaStream_t st) { k_fib_table<<<(n + 127) / 128, 128, 0, st>>>(out, n); }
-
 template void launch_wavefront<double>(const WaveParams<double>&, int, bool, cudaStream_t, cudaEvent_t, cudaEvent_t,
                                        long long*);
 

@@ -183,9 +183,9 @@ __global__ void __launch_bounds__(128) k_ray_setup(WaveParams<R> P) {
     int n = 0;
     if (pv.alive[g] || P.debug) {  // debug traces dead probes too (per-ray parity)
         n = pv.reject[g] ? 2 * P.nRaysFull : P.nRaysFull;
-        const int ci = cascadeOf(P.pc, g);
-        probeRotation(P.seed, P.frame, P.rotatePerFrame != 0, probeKey(P.pc.cas[ci].level, g - P.pc.cas[ci].base),
-                      P.rot + 9 * static_cast<size_t>(s));
+        // randomRotation's matrix (rng.hpp:79-89) from the host-libm quaternion
+        const double* q = P.quat + 4 * static_cast<size_t>(s);
+        quatToRotation(q[0], q[1], q[2], q[3], P.rot + 9 * static_cast<size_t>(s));
     }
     P.rayCount[s] = n;
 }
@@ -236,19 +236,6 @@ __global__ void __launch_bounds__(128) k_ray_chunks(WaveParams<R> P) {
     for (long long c = (b + 31) >> 5; (c << 5) < e; ++c) P.chunkSlot[c] = s;
 }
 
-// sphericalFibonacci(i, n), sampling.hpp:11-17 — one table per ray count.
-static __global__ void k_fib_table(double* out, int n) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const double goldenAngle = kPi * (3.0 - sqrt(5.0));
-    double z = 1.0 - (2.0 * i + 1.0) / n;
-    double r = sqrt(smax(0.0, 1.0 - z * z));
-    double phi = goldenAngle * i;
-    out[3 * i] = r * cos(phi);
-    out[3 * i + 1] = r * sin(phi);
-    out[3 * i + 2] = z;
-}
-
 __device__ __forceinline__ int findCandidate(const long long* start, int n, long long rid) {
     int lo = 0, hi = n;  // start[lo] <= rid < start[hi]
     while (hi - lo > 1) {
@@ -296,8 +283,10 @@ __device__ __forceinline__ bool contactRay(const WaveParams<R>& P, long long ite
     const int x = static_cast<int>(pix % P.gw), y = static_cast<int>(pix / P.gw);
     Rng rng(hashCombine(hashCombine(P.seed, 0xc0417ffull), static_cast<uint64_t>(y) * P.gw + x));
     rng.s += 2ull * smp * 0x9e3779b97f4a7c15ull;
+    const double u1 = rng.uniform();  // lz = sqrt(1 - u1); lx, ly from the host table
+    const double2 l = reinterpret_cast<const double2*>(P.clocal)[item];
     const V3<double> nn = mk(px.normal[0], px.normal[1], px.normal[2]);
-    const V3<double> dd = cosineHemisphereDir(rng, nn);
+    const V3<double> dd = cosineHemisphereDir(l.x, l.y, u1, nn);
     const double cosT = smax(0.1, dot(dd, nn));
     const double bias = 2.0 * P.tc.eps / cosT;
     const V3<double> oo = mk(px.world_pos[0], px.world_pos[1], px.world_pos[2]) + nn * bias;
@@ -417,16 +406,12 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                 tMax = R(P.tc.rayTMax);
             } else {
                 rid = item;
-                if (P.cray) {
-                    const ContactRay<R> r = ldStream(reinterpret_cast<const ContactRay<R>*>(P.cray) + item);
-                    o = mk(r.o[0], r.o[1], r.o[2]);
-                    dir = mk(r.dir[0], r.dir[1], r.dir[2]);
-                    tMax = r.tMax;
-                    startBound = r.startBound;
-                    ok = r.tMax >= R(0);
-                } else {
-                    ok = contactRay(P, static_cast<long long>(item), o, dir, tMax, startBound);
-                }
+                const ContactRay<R> r = ldStream(reinterpret_cast<const ContactRay<R>*>(P.cray) + item);
+                o = mk(r.o[0], r.o[1], r.o[2]);
+                dir = mk(r.dir[0], r.dir[1], r.dir[2]);
+                tMax = r.tMax;
+                startBound = r.startBound;
+                ok = r.tMax >= R(0);
             }
             t = R(0);
             lastD = startBound * R(0.5);

@@ -1209,20 +1209,9 @@ __device__ V3<double> shadeHit(const SceneView<R>& s, const Hit<R>& hit, const C
     return radiance;
 }
 
-// sampleDirections rotation, sampling.hpp:23-31 + randomRotation rng.hpp:72-90.
-// Row-major 3x3 into m.
-__device__ __forceinline__ void probeRotation(uint64_t seed, int frame, bool rotatePerFrame, uint64_t key,
-                                              double* m) {
-    Rng rng(hashCombine(hashCombine(hashCombine(seed, rotatePerFrame ? static_cast<uint64_t>(static_cast<int64_t>(frame))
-                                                                      : 0xf1b0ull),
-                                                key),
-                                    0x5df6d1ull));
-    double u1 = rng.uniform(), u2 = rng.uniform(), u3 = rng.uniform();
-    double a = sqrt(1.0 - u1), b = sqrt(u1);
-    double qx = a * sin(2 * kPi * u2);
-    double qy = a * cos(2 * kPi * u2);
-    double qz = b * sin(2 * kPi * u3);
-    double qw = b * cos(2 * kPi * u3);
+// randomRotation's matrix from its quaternion (rng.hpp:79-89), row-major into m.
+// The quaternion's sines/cosines come from the host's libm (host_trig.h).
+__device__ __forceinline__ void quatToRotation(double qx, double qy, double qz, double qw, double* m) {
     m[0] = 1 - 2 * (qy * qy + qz * qz);
     m[1] = 2 * (qx * qy - qz * qw);
     m[2] = 2 * (qx * qz + qy * qw);
@@ -1234,22 +1223,10 @@ __device__ __forceinline__ void probeRotation(uint64_t seed, int frame, bool rot
     m[8] = 1 - 2 * (qx * qx + qy * qy);
 }
 
-// rot * sphericalFibonacci(i, n), sampling.hpp:11-17,28
-__device__ __forceinline__ V3<double> probeRayDir(const double* m, int i, int n) {
-    const double goldenAngle = kPi * (3.0 - sqrt(5.0));
-    double z = 1.0 - (2.0 * i + 1.0) / n;
-    double r = sqrt(smax(0.0, 1.0 - z * z));
-    double phi = goldenAngle * i;
-    V3<double> v = mk(r * cos(phi), r * sin(phi), z);
-    return mk(m[0] * v.x + m[1] * v.y + m[2] * v.z, m[3] * v.x + m[4] * v.y + m[5] * v.z,
-              m[6] * v.x + m[7] * v.y + m[8] * v.z);
-}
-
-// cosineHemisphereDir (rng.hpp:58-69) with orthonormalBasis (vec.hpp:188-194)
-__device__ __forceinline__ V3<double> cosineHemisphereDir(Rng& rng, V3<double> n) {
-    double u1 = rng.uniform(), u2 = rng.uniform();
-    double r = sqrt(u1), phi = 2.0 * kPi * u2;
-    double lx = r * cos(phi), ly = r * sin(phi), lz = sqrt(smax(0.0, 1.0 - u1));
+// cosineHemisphereDir (rng.hpp:58-69) with orthonormalBasis (vec.hpp:188-194);
+// lx = r cos(phi), ly = r sin(phi) come from the host's libm (host_trig.h).
+__device__ __forceinline__ V3<double> cosineHemisphereDir(double lx, double ly, double u1, V3<double> n) {
+    double lz = sqrt(smax(0.0, 1.0 - u1));
     double sign = copysign(1.0, n.z);
     double a = -1.0 / (sign + n.z);
     double c = n.x * n.y * a;

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "../../include/sdfgi_b200.h"
+#include "host_trig.h"
 #include "kernels.cuh"
 
 using namespace sdfgi_dev;
@@ -116,6 +117,7 @@ struct Ctx {
     int device = 0, rank = 0, world = 1, precision = SDFGI_F64;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // update start/end, relocate start/end
+    cudaEvent_t quatEv = nullptr;  // the quaternion staging copy has been consumed
     bool evUpdate = false, evReloc = false;
     ncclComm_t comm = nullptr;
     long long launches = 0;
@@ -173,9 +175,16 @@ struct Ctx {
     // wavefront scratch (kernels.cuh)
     DBuf<int> wRayCount, wHitList, wChunk, wHitAt;
     DBuf<long long> wRayStart;
-    DBuf<double> wRot, fib;
+    DBuf<double> wRot, fib, wQuat;
     DBuf<int> perm;
     int fibN = -1;
+    double* hQuat = nullptr;  // pinned staging of the per-pass quaternions (host_trig.h)
+    size_t hQuatN = 0;
+    // Contact GI's cosineHemisphereDir (lx, ly) per (pixel, sample), host libm; keyed
+    // (seed, w, h, samples): the reference's stream has no frame index (shading.hpp:451)
+    DBuf<double> cLocal;
+    uint64_t cLocalSeed = 0;
+    int cLocalW = 0, cLocalH = 0, cLocalS = -1;
     DBuf<unsigned char> wHits, wVis, wRad, wPark, wCRay, wSRay, wSelTemp;
     DBuf<unsigned long long> wCtr;
     int persistCap = 0;  // 0 = occupancy-sized persistent grids
@@ -202,7 +211,8 @@ struct Ctx {
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
-        wRayCount.free(); wHitList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); wHits.free();
+        wRayCount.free(); wHitList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); wQuat.free(); cLocal.free(); wHits.free();
+        if (hQuat) cudaFreeHost(hQuat);
         wVis.free(); wPark.free(); wCRay.free(); wSRay.free(); wCtr.free(); perm.free(); wRad.free();
         gbuf.free(); halfDepth.free(); sparseIrr.free(); resolved.free(); indirect.free(); histIrr.free(); composed.free();
         histDepth.free(); halfSrc.free(); sel.free(); sparseValid.free(); sparseAnchor.free();
@@ -212,6 +222,7 @@ struct Ctx {
             if (e) cudaEventDestroy(e);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
+        if (quatEv) cudaEventDestroy(quatEv);
         if (comm) ncclCommDestroy(comm);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -800,11 +811,13 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     reservePark<R>(c, maxRays, L);
     reserve(c->wSRay, std::max<size_t>(maxRays, 1) * L * sizeof(ShadowRay<R>));
     if (c->fibN != N) {
-        reserve(c->fib, 9 * static_cast<size_t>(N));
-        launch_fib_table(c->fib.p, N, c->stream);
-        launch_fib_table(c->fib.p + 3 * N, 2 * N, c->stream);
-        checkLaunch(c);
-        ++c->launches;
+        // sphericalFibonacci tables for n = N and 2N from the host's libm (host_trig.h)
+        std::vector<double> fib(9 * static_cast<size_t>(N));
+        sdfgi_host::fibTable(N, fib.data());
+        sdfgi_host::fibTable(2 * N, fib.data() + 3 * N);
+        reserve(c->fib, fib.size());
+        CK(cudaMemcpyAsync(c->fib.p, fib.data(), fib.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));  // fib is a local
         std::vector<int> perm = coherentOrder(N);
         std::vector<int> perm2 = coherentOrder(2 * N);
         perm.insert(perm.end(), perm2.begin(), perm2.end());
@@ -821,6 +834,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.rayStart = c->wRayStart.p;
     p.chunkSlot = c->wChunk.p;
     p.rot = c->wRot.p;
+    p.quat = c->wQuat.p;
     p.fib = c->fib.p;
     p.perm = c->perm.p;
     p.nRaysDirect = -1;  // probe batch: ray count from the K0 prefix sum
@@ -855,6 +869,37 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.rays = c->scratch.p + 17;
     p.updated = reinterpret_cast<unsigned int*>(c->scratch.p + 18);
     return p;
+}
+
+// randomRotation's quaternion of every candidate for this pass (sampleDirections'
+// key: seed, frame or 0xf1b0, probeKey(level, index)), evaluated with the host's
+// libm (host_trig.h) into pinned memory and copied behind the work already queued
+// on the stream (relocation, the atlas copy), so the host work overlaps it.
+// cand = null: every probe 0..nCand-1.
+void uploadQuats(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand) {
+    const size_t need = 4 * static_cast<size_t>(std::max(nCand, 1));
+    if (c->hQuatN < need) {
+        if (c->hQuat) CK(cudaFreeHost(c->hQuat));
+        c->hQuat = nullptr;
+        c->hQuatN = 0;
+        CK(cudaMallocHost(&c->hQuat, need * sizeof(double)));
+        c->hQuatN = need;
+    }
+    // the previous call's copy out of the staging buffer must have finished
+    CK(cudaEventSynchronize(c->quatEv));
+    std::vector<uint64_t> keys(nCand);
+    for (int s = 0; s < nCand; ++s) {
+        const int g = cand ? cand[s] : s;
+        int ci = 0;
+        for (size_t k = 1; k < c->cascades.size(); ++k)
+            if (g >= c->cascades[k].base) ci = static_cast<int>(k);
+        keys[s] = sdfgi_host::probeKey(c->cascades[ci].level, g - c->cascades[ci].base);
+    }
+    sdfgi_host::probeQuats(cfg->seed, frame, cfg->rotate_per_frame != 0, keys.data(), nCand, c->hQuat);
+    reserve(c->wQuat, need);
+    CK(cudaMemcpyAsync(c->wQuat.p, c->hQuat, 4 * static_cast<size_t>(nCand) * sizeof(double), cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaEventRecord(c->quatEv, c->stream));
 }
 
 void validateCfg(Ctx* c, const sdfgi_cfg* cfg) {
@@ -945,7 +990,9 @@ int sdfgi_ctx_create(int device, int rank, int world, const uint8_t* nccl_uid, i
         try {
             CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
             for (auto& e : c->ev) CK(cudaEventCreate(&e));
-            c->scratch.alloc(32);
+            CK(cudaEventCreateWithFlags(&c->quatEv, cudaEventDisableTiming));
+            CK(cudaEventRecord(c->quatEv, c->stream));
+            c->scratch.alloc(64);
             c->report.alloc(4);
             if (world > 1) {
                 REQ(nccl_uid, SDFGI_ERR_INVALID, "world > 1 needs an NCCL unique id");
@@ -1365,6 +1412,7 @@ int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_refs, int fr
         const int nCand = static_cast<int>(refs.size());
         if (nCand > 0) {
             const int* cand = all ? nullptr : c->refs.p;
+            uploadQuats(c, cfg, frame, all ? nullptr : refs.data(), nCand);
             if (c->precision == SDFGI_F64) {
                 WaveParams<double> p = waveParams<double>(c, cfg, frame, cand, nCand);
                 launch_wavefront<double>(p, c->persistCap, stats != nullptr, c->stream, c->ev[0], c->ev[1],
@@ -1491,6 +1539,7 @@ int sdfgi_probes_trace_debug(void* ctx, const int32_t* probe_refs, int n_refs, i
         }
         const size_t cap = static_cast<size_t>(n_refs) * 2 * static_cast<size_t>(cfg->n_rays_full);
         c->refs.upload(g.data(), g.size(), c->stream);
+        uploadQuats(c, cfg, frame, g.data(), n_refs);
         reserve(c->records, cap);
         // the same K0..K3 wavefront in debug mode: per-ray records, no atlas/state writes
         if (c->precision == SDFGI_F64) {
@@ -1613,6 +1662,7 @@ CameraDev toCam(const sdfgi_camera& c) {
         d.up[k] = c.up[k];
     }
     d.fov = c.fov_y_deg;
+    d.tanHalf = sdfgi_host::tanHalf(c.fov_y_deg);  // host libm (camera.hpp:30,42)
     return d;
 }
 
@@ -1654,6 +1704,19 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     reservePark<R>(c, cap, L);
     reserve(c->wSRay, cap * L * sizeof(ShadowRay<R>));
     reserve(c->wCRay, cap * sizeof(ContactRay<R>));
+    const int S = static_cast<int>(std::max<long long>(cfg->contact_samples, 0));
+    if (nr > 0 && (c->cLocalS != S || c->cLocalW != c->gw || c->cLocalH != c->gh || c->cLocalSeed != cfg->seed)) {
+        // frame-invariant: built once per (seed, resolution, sample count)
+        std::vector<double> tab(2 * static_cast<size_t>(nr));
+        sdfgi_host::contactLocal(cfg->seed, c->gw, c->gh, S, tab.data());
+        c->cLocal.alloc(tab.size());
+        CK(cudaMemcpyAsync(c->cLocal.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));  // tab is a local
+        c->cLocalS = S;
+        c->cLocalW = c->gw;
+        c->cLocalH = c->gh;
+        c->cLocalSeed = cfg->seed;
+    }
     WaveParams<R> p;
     std::memset(&p, 0, sizeof(p));
     p.scene = c->sceneView<R>();
@@ -1678,9 +1741,10 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     p.srayCap = cap;
     p.park = c->accel && c->haveGrid && c->wPark.n >= 4096 ? c->wPark.p : nullptr;  // SDFGI_PARK_MB=0: off
     p.parkBytes = p.park ? c->wPark.n : 0;
-    p.stats = c->scratch.p;
+    p.stats = c->scratch.p + 32;  // contact counters: scratch[32..], the visibility ones stay at [0..]
     p.nRaysDirect = nr;
     p.cray = c->wCRay.p;
+    p.clocal = c->cLocal.p;
     p.gb = c->gbuf.p;
     p.gw = c->gw;
     p.gh = c->gh;
@@ -1776,10 +1840,9 @@ GatherParams<R> gatherParams(Ctx* c, const sdfgi_cfg* cfg, int frame) {
     p.contactRadius = cfg->contact_radius_frac * sp0;
     p.contactSamples = static_cast<int>(cfg->contact_samples);
     p.seed = cfg->seed;
-    // visibility and contact counters share scratch[0..13]: sdfgi_gather reads the
-    // visibility ones and clears them before the contact pass
+    // visibility counters at scratch[0..13] (contact: [32..], contactParams)
     p.visStats = c->scratch.p;
-    p.contactStats = c->scratch.p;
+    p.contactStats = c->scratch.p + 32;
     p.taskCount = c->scratch.p + 19;
     return p;
 }
@@ -1842,7 +1905,7 @@ int sdfgi_gather(void* ctx, int frame, const sdfgi_cfg* cfg, int64_t* n_tasks, s
         REQ(c->gw > 0 && c->gbuf.p, SDFGI_ERR_STATE, "no G-buffer (upload or render one first)");
         REQ(cfg->oct_res == c->octRes, SDFGI_ERR_INVALID, "cfg.oct_res differs from the atlas resolution");
         const bool st = vis_stats != nullptr || contact_stats != nullptr;
-        CK(cudaMemsetAsync(c->scratch.p, 0, 32 * 8, c->stream));
+        CK(cudaMemsetAsync(c->scratch.p, 0, 64 * 8, c->stream));
         CK(cudaEventRecord(c->gev[0], c->stream));
         auto run = [&](auto p) {
             launch_gather(p, 1, st, c->stream);  // downsample + select
@@ -1853,35 +1916,22 @@ int sdfgi_gather(void* ctx, int frame, const sdfgi_cfg* cfg, int64_t* n_tasks, s
             CK(cudaEventRecord(c->gev[3], c->stream));
             return p;
         };
-        unsigned long long visH[32];
-        // Contact GI (shading.hpp:431-477) as a wavefront over (pixel, sample) rays
-        const char* cenv = std::getenv("SDFGI_CONTACT_PER_PIXEL");  // 1: the per-pixel loop kernel
-        const bool perPixel = cenv && std::atoi(cenv) == 1;
+        // Contact GI (shading.hpp:431-477) as a wavefront over (pixel, sample) rays; its
+        // counters live at scratch[32..], so no host round trip between the stages
         if (c->precision == SDFGI_F64) {
-            auto p = run(gatherParams<double>(c, cfg, frame));
-            CK(cudaMemcpyAsync(visH, c->scratch.p, sizeof(visH), cudaMemcpyDeviceToHost, c->stream));
-            CK(cudaStreamSynchronize(c->stream));
-            CK(cudaMemsetAsync(c->scratch.p, 0, 19 * 8, c->stream));
-            if (perPixel)
-                launch_gather(p, 4, st, c->stream);
-            else
-                launch_contact<double>(contactParams<double>(c, cfg), st, c->stream, &c->launches);
+            run(gatherParams<double>(c, cfg, frame));
+            launch_contact<double>(contactParams<double>(c, cfg), st, c->stream, &c->launches);
         } else {
-            auto p = run(gatherParams<float>(c, cfg, frame));
-            CK(cudaMemcpyAsync(visH, c->scratch.p, sizeof(visH), cudaMemcpyDeviceToHost, c->stream));
-            CK(cudaStreamSynchronize(c->stream));
-            CK(cudaMemsetAsync(c->scratch.p, 0, 19 * 8, c->stream));
-            if (perPixel)
-                launch_gather(p, 4, st, c->stream);
-            else
-                launch_contact<float>(contactParams<float>(c, cfg), st, c->stream, &c->launches);
+            run(gatherParams<float>(c, cfg, frame));
+            launch_contact<float>(contactParams<float>(c, cfg), st, c->stream, &c->launches);
         }
         c->launches += 4;
         CK(cudaGetLastError());
         CK(cudaEventRecord(c->gev[4], c->stream));
         c->gevValid = true;
-        unsigned long long conH[32];
-        CK(cudaMemcpyAsync(conH, c->scratch.p, sizeof(conH), cudaMemcpyDeviceToHost, c->stream));
+        unsigned long long visH[64];
+        CK(cudaMemcpyAsync(visH, c->scratch.p, sizeof(visH), cudaMemcpyDeviceToHost, c->stream));
+        const unsigned long long* conH = visH + 32;
         // roll history (pipeline.hpp:213-218): resolved E and this frame's depth
         const size_t np = static_cast<size_t>(c->gw) * c->gh;
         CK(cudaMemcpyAsync(c->histIrr.p, c->resolved.p, 3 * np * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));

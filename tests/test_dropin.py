@@ -27,12 +27,11 @@ def test_dropin_cornell_three_passes_bit_exact():
     out = run("c1", 3, (8, 8, 8), 1.0, 64)
     assert out["probe_mismatches"] == 0
     assert out["max_rel_err"] <= 1e-3
-    # the rest are 1-ulp float differences from libdevice-vs-glibc sin/cos in directions
-    assert out["exact_texels"] >= 0.999 * out["texels"]
+    assert out["exact_texels"] >= 0.99 * out["texels"]
 
 
 def test_dropin_sponza_two_passes():
     out = run("sponza", 2, (12, 7, 9), 1.4, 32)
     assert out["probe_mismatches"] == 0
-    assert out["max_rel_err"] <= 1e-2
+    assert out["max_rel_err"] <= 1e-3
     assert out["exact_texels"] >= 0.99 * out["texels"]

@@ -44,6 +44,6 @@ def test_dynamic_sequence_matches_reference(name, precision):
                 err = texel_rel_err(dev.atlas(0, 0), case.data[f"atlas_f{fr}_c0"])
                 bad = float(np.mean(err > 1e-3))
                 if precision == "f64":
-                    assert bad <= 1e-3 and err.max() <= 1e-2, (name, fr, err.max())
+                    assert err.max() <= 1e-3, (name, fr, err.max())
                 else:
                     assert bad <= 1e-2, (name, fr, err.max(), bad)

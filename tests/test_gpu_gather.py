@@ -5,8 +5,9 @@ Inputs are made identical first (the golden atlas and probe state are uploaded),
 so each stage is compared on its own: integer stages (checkerboard downsample,
 pixel selection, anchors, task count) exactly; floating stages in FP64 within
 1e-9 relative where only the reference's arithmetic is involved, within 1e-6
-where libm exp/pow enter (bilateral weights), and within the north-star 1e-3 for
-Contact GI (its cosine directions carry sin/cos ulps into full traces).
+where libm exp/pow enter (bilateral weights), and within the north-star 1e-3 on
+every channel for Contact GI (its cosine directions are bit-identical: the
+sin/cos come from the host's libm, host_trig.h).
 """
 import os
 import sys
@@ -53,8 +54,8 @@ def test_gather_matches_reference(dev, name):
     sky = ~np.isfinite(want["depth"])
     assert np.array_equal(~np.isfinite(gb["depth"]), sky)
     geo = ~sky
-    assert np.mean(gb["prim_index"][geo] == want["prim_index"][geo]) > 0.999
-    assert np.allclose(gb["depth"][geo], want["depth"][geo], rtol=1e-9)
+    assert np.array_equal(gb["prim_index"], want["prim_index"])
+    assert np.array_equal(gb["depth"][geo], want["depth"][geo])
     # gather stages on the reference's own G-buffer
     dev.upload_gbuffer(g.w, g.h, want)
     dev.reset_history()
@@ -69,7 +70,7 @@ def test_gather_matches_reference(dev, name):
         e = rel(dev.gather_buffer("resolved"), g.data[f"resolved_f{f}"])
         assert e.max() <= 1e-6, (name, f, "resolved", e.max())
         e = rel(dev.gather_buffer("indirect"), g.data[f"indirect_f{f}"])
-        assert np.mean(e > 1e-3) <= 1e-3 and e.max() <= 5e-2, (name, f, "indirect", e.max())
+        assert e.max() <= 1e-3, (name, f, "indirect", e.max())
 
 
 @pytest.mark.parametrize("name", GATHER_CASES)
@@ -97,31 +98,43 @@ def test_compose_matches_reference(name, precision):
                 assert np.mean(e > 1e-3) <= 1e-3 and e.max() <= 5e-2, (name, f, e.max())
 
 
-def test_gather_1080p_properties(dev):
-    """C3 at full size on the C2 scene: the G-buffer rendered on the device agrees with
-    the oracle on a row sample; resolved irradiance is finite, >= 0, zero on sky."""
-    from paper_2007_14394_b200 import scene_io
-
-    scene = scene_io.read_sdfs(os.path.join(ROOT, "paper_2007_14394_b200", "data", "c2.sdfs"))
+def test_gather_1080p_matches_oracle(dev, oracle_c2):
+    """C3 (BASELINE configs[2]) at full size against the oracle: the 1920x1080 gather
+    on the C2 scene and volume after its 3 bounces (the oracle's probe state and
+    atlas uploaded, so the gather is compared on identical inputs). The device
+    G-buffer equals renderGBuffer's bit for bit; two frames (the second with
+    history): integer stages exact, sparse irradiance 1e-9, resolved 1e-6 (libm
+    exp/pow in the bilateral weights), indirect (Contact GI) within 1e-3 on every
+    channel."""
+    scene, ora = oracle_c2["scene"], oracle_c2["stage"]
+    last = oracle_c2["passes"][-1]
     stage = api.ProbeStage(dev, scene)
-    for p in range(3):
-        stage.run_pass(p)
-    # G-buffer parity with the oracle at a size the CPU finishes quickly
-    sw, sh = 160, 90
-    dev.render_gbuffer(scene.camera, sw, sh, stage.cfg)
-    small = dev.gbuffer()
-    ogb, _ = oracle_py.Stage(scene).render_gbuffer(sw, sh)
-    assert np.array_equal(np.isfinite(small["depth"]), np.isfinite(ogb["depth"]))
-    geo = np.isfinite(ogb["depth"])
-    assert np.mean(small["prim_index"][geo] == ogb["prim_index"][geo]) > 0.999
+    dev.upload_probes(0, last["probes"])
+    dev.upload_atlas(0, last["atlas"], which=0)
+    cfg = stage.cfg
     w, h = 1920, 1080
-    dev.render_gbuffer(scene.camera, w, h, stage.cfg)
+    ogb, _ = ora.render_gbuffer(w, h)
+    dev.render_gbuffer(scene.camera, w, h, cfg)
     gb = dev.gbuffer()
+    assert np.array_equal(gb["prim_index"], ogb["prim_index"])
+    geo = np.isfinite(ogb["depth"])
+    assert np.array_equal(np.isfinite(gb["depth"]), geo)
+    assert np.array_equal(gb["depth"][geo], ogb["depth"][geo])
+    assert np.array_equal(gb["normal"][geo], ogb["normal"][geo])
     dev.reset_history()
+    hist = None
     for f in range(2):
-        dev.gather(f, stage.cfg)
-        res = dev.gather_buffer("resolved").reshape(h * w, 3)
-        ind = dev.gather_buffer("indirect").reshape(h * w, 3)
-        assert np.all(np.isfinite(res)) and np.all(res >= 0) and np.all(np.isfinite(ind)) and np.all(ind >= 0)
-        sky = ~np.isfinite(gb["depth"])
-        assert np.all(res[sky] == 0) and np.all(ind[sky] == 0)
+        want = ora.gather_frame(ogb, w, h, f, hist)
+        n = dev.gather(f, cfg)
+        assert n == want["tasks"], f
+        for k in ("half_src", "sel", "sparse_anchor", "sparse_valid", "half_depth"):
+            assert np.array_equal(dev.gather_buffer(k), want[k]), (f, k)
+        e = rel(dev.gather_buffer("sparse_irr"), want["sparse_irr"])
+        assert e.max() <= 1e-9, (f, "sparse_irr", e.max())
+        e = rel(dev.gather_buffer("resolved"), want["resolved"])
+        assert e.max() <= 1e-6, (f, "resolved", e.max())
+        ind = dev.gather_buffer("indirect")
+        e = rel(ind, want["indirect"])
+        print(f"C3 frame {f}: indirect max rel err {e.max():.3e}, bit-identical {np.mean(ind == want['indirect']):.6f}")
+        assert e.max() <= 1e-3, (f, "indirect", e.max())
+        hist = (want["resolved"], ogb["depth"].copy())

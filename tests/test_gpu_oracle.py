@@ -79,27 +79,25 @@ def test_c2_relocation_bit_exact_full_volume(dev, scene):
         dev.swap()
 
 
-def test_c2_sampled_update_matches_oracle(dev, scene):
-    """Every 128th probe of the C2 volume through 2 bounces: identical probe states,
-    identical ray counts, texels within the 1e-3 bar (FP64; bit-identical except
-    where direction ulps flip a corner-tie owner)."""
-    stride = 128
+def test_c2_full_step_matches_oracle(dev, scene, oracle_c2):
+    """The bench workload itself, every probe of the 32x16x32 volume through all 3
+    bounces (15M rays) against the oracle: relocation reports and probe states
+    bit-exact; every texel channel within the north-star 1e-3 relative; nearly all
+    texels bit-identical (the MVC sines are evaluated algebraically, a few ulps)."""
     stage = api.ProbeStage(dev, scene)
-    ora = oracle_py.Stage(scene)
-    n = 32 * 16 * 32
-    refs = np.array([[0, i] for i in range(0, n, stride)], np.int32)
-    for p in range(2):
-        stage.relocate_all()
-        res = api.updateProbes(dev, stage.cfg, p, refs=refs)
+    for p, want in enumerate(oracle_c2["passes"]):
+        rep = stage.relocate_all()[0]
+        assert [int(rep["relocated"]), int(rep["rejected"]), int(rep["dead"])] == want["rep"], p
+        res = api.updateProbes(dev, stage.cfg, p)
         dev.swap()
-        _, _, (md, rays, upd, _) = ora.run_pass(p, stride=stride, threads=os.cpu_count() or 1)
-        assert int(res["rays_traced"]) == rays and int(res["probes_updated"]) == upd
-        g, o = dev.probes(0), ora.probes(0)
-        for f in ("pos", "alive", "reject_history", "last_update_frame"):
+        assert int(res["rays_traced"]) == want["rays"] and int(res["probes_updated"]) == want["upd"], p
+        g, o = dev.probes(0), want["probes"]
+        for f in ("pos", "last_pos", "alive", "reject_history", "last_update_frame"):
             assert np.array_equal(g[f], o[f]), (p, f)
-        ga, oa = dev.atlas(0), ora.atlas(0)
+        ga, oa = dev.atlas(0), want["atlas"]
         err = rel_err(ga, oa)
-        assert np.mean(err > 1e-3) <= 1e-3 and err.max() <= 1e-2, (p, err.max())
+        print(f"C2 pass {p}: max texel rel err {err.max():.3e}, bit-identical {np.mean(ga == oa):.6f}")
+        assert err.max() <= 1e-3, (p, err.max())
         assert np.mean(ga == oa) > 0.99, p
 
 
@@ -116,20 +114,16 @@ def test_c2_full_frame_deterministic_and_non_negative(dev, scene):
     assert np.all(out[0] >= 0) and np.all(np.isfinite(out[0]))
 
 
-def test_c2_f32_mode_error_report(scene):
-    """FP32 perf mode against the oracle on sampled probes: the north-star 1e-3 bar
-    holds for nearly every channel; the tail comes from hit/miss and owner flips."""
-    stride = 128
+def test_c2_f32_mode_error_report(scene, oracle_c2):
+    """FP32 perf mode against the oracle on the whole C2 step (every probe, 3
+    bounces): the error distribution is reported; the tail comes from hit/miss and
+    owner flips of float traces."""
     with Device(0, precision="f32") as d32:
         stage = api.ProbeStage(d32, scene)
-        ora = oracle_py.Stage(scene)
-        n = 32 * 16 * 32
-        refs = np.array([[0, i] for i in range(0, n, stride)], np.int32)
-        stage.relocate_all()
-        api.updateProbes(d32, stage.cfg, 0, refs=refs)
-        d32.swap()
-        ora.run_pass(0, stride=stride, threads=os.cpu_count() or 1)
-        err = rel_err(d32.atlas(0)[::stride], ora.atlas(0)[::stride])
-        frac = float(np.mean(err > 1e-3))
-        print(f"FP32 C2 texels: max rel err {err.max():.3e}, {frac:.2e} of channels over 1e-3")
-        assert frac < 2e-2
+        for p, want in enumerate(oracle_c2["passes"]):
+            stage.run_pass(p)
+            err = rel_err(d32.atlas(0), want["atlas"])
+            frac = float(np.mean(err > 1e-3))
+            print(f"FP32 C2 pass {p}: max rel err {err.max():.3e}, p99.9 {np.quantile(err, 0.999):.3e}, "
+                  f"{frac:.2e} of channels over 1e-3")
+            assert frac < 2e-2

@@ -1,8 +1,7 @@
 """The reference's whole frame loop, Renderer::renderFrame (pipeline.hpp:84-230),
 against the device Renderer (renderer.py): per frame the same metrics counts and
-composed images within the north-star 1e-3 on shaded pixels (the Contact GI
-cosine directions carry libdevice-vs-glibc ulps, so a small tail is allowed as in
-the gather tests)."""
+composed images within the north-star 1e-3 on every channel in FP64; the FP32
+perf mode's error tail (hit/owner flips of float traces) is bounded and reported."""
 import numpy as np
 import pytest
 
@@ -37,4 +36,7 @@ def test_renderer_matches_reference(name, precision):
             img = r.image().astype(np.float32).astype(np.float64)  # as writeHdr stores it
             e = rel(img, g.data[f"image_f{fr}"].astype(np.float64))
             bad = float(np.mean(e > 1e-3))
-            assert bad <= (2e-3 if precision == "f64" else 2e-2) and e.max() <= 0.2, (name, fr, bad, e.max())
+            if precision == "f64":
+                assert e.max() <= 1e-3, (name, fr, e.max())
+            else:
+                assert bad <= 2e-2 and e.max() <= 0.2, (name, fr, bad, e.max())
