@@ -48,6 +48,19 @@ METRIC = "probe-update Grays/s & ms/frame (32x16x32 probes, 256 rays)"
 UNIT = "Grays/s"
 
 
+def latest_profiles(stem, ext):
+    """profiles/r<round>_<stem>_v<version>.<ext>, oldest first: sorted by (round,
+    version) numerically, so v12 sorts after v9 and r02 after r01."""
+    import glob
+
+    out = []
+    for f in glob.glob(os.path.join(ROOT, "profiles", f"r*_{stem}_v*.{ext}")):
+        m = re.search(rf"r(\d+)_{re.escape(stem)}_v(\d+)\.{ext}$", os.path.basename(f))
+        if m:
+            out.append(((int(m.group(1)), int(m.group(2))), f))
+    return [f for _, f in sorted(out)]
+
+
 STEP_KERNELS = ("k_relocate", "k_ray_setup", "k_ray_scan", "k_trace_primary", "k_trace_shadow", "k_shade_rays",
                 "k_convolve")
 
@@ -59,7 +72,7 @@ def ncu_step_traffic(precision):
     import csv
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r01_step_launches_{precision}_v*.csv")))
+    files = latest_profiles(f"step_launches_{precision}", "csv")
     if not files:
         return None, None
     rows = [r for r in csv.reader(open(files[-1])) if len(r) > 10]
@@ -90,8 +103,7 @@ def ncu_pipe_kernels(precision):
     issued instruction (the divergence that bounds the tracing kernels)."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r01_ncu_step_{precision}_v*.json")),
-                   key=lambda f: int(re.search(r"_v(\d+)\.json$", f).group(1)))
+    files = latest_profiles(f"ncu_step_{precision}", "json")
     if not files:
         return None
     caps = json.load(open(files[-1])).get("full_captures", [])
@@ -118,7 +130,7 @@ def ncu_hbm_kernels(precision, hbm_peak):
     import csv
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r01_step_launches_{precision}_v*.csv")))
+    files = latest_profiles(f"step_launches_{precision}", "csv")
     if not files:
         return None
     rows = [r for r in csv.reader(open(files[-1])) if len(r) > 10]
@@ -164,14 +176,30 @@ def ref_binary():
     return None
 
 
-def cpu_reference_sample(stride, threads, reps=1):
+def workload_sdfs(config):
+    """The workload's scene as an SDFS file the reference driver reads (C4 is
+    generated, then written to a temporary file)."""
+    if config == "c2":
+        return C2_PATH
+    import tempfile
+
+    scene, _ = load_workload(config)
+    path = os.path.join(tempfile.gettempdir(), f"sdfgi_bench_{config}.sdfs")
+    scene_io.write_sdfs(path, scene)
+    return path
+
+
+CPU_STRIDE = {"c2": 7, "c4": 2039}  # coprime with the grid dims: every x, y, z column is sampled
+
+
+def cpu_reference_sample(stride, threads, reps=1, sdfs=C2_PATH):
     """Run the reference probe stage (pipeline.hpp:108-151) for PASSES passes on every
     `stride`-th probe. Returns per-rep (rays, seconds) with relocation time scaled to the
     sampled fraction (relocation always runs on the whole volume)."""
     exe = ref_binary()
     if exe is None:
         return None, "oracle/_ref not built"
-    cmd = [exe, "passes", C2_PATH, os.devnull, "--passes", str(PASSES), "--threads", str(threads),
+    cmd = [exe, "passes", sdfs, os.devnull, "--passes", str(PASSES), "--threads", str(threads),
            "--stride", str(stride), "--reps", str(reps), "--no-dump"]
     r = subprocess.run(cmd, capture_output=True, text=True, check=True)
     out = json.loads(r.stdout)
@@ -246,6 +274,86 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ our arm
+def load_workload(config):
+    """C2 (BASELINE configs[1], the headline) or C4 (configs[3]: ~50k primitives,
+    128x32x128 probes at spacing 1.875, clusters from the library's linear-time
+    builder)."""
+    if config == "c2":
+        return scene_io.read_sdfs(C2_PATH), WORKLOADS["c2"]
+    from paper_2007_14394_b200 import scenegen
+
+    return scenegen.with_fast_clusters(scenegen.c4_scene(50000), 8), WORKLOADS["c4"]
+
+
+WORKLOADS = {
+    "c2": "C2: ~2k-primitive synthetic Sponza-scale SDF scene, 32x16x32 probes, 256 rays, 3 bounces, relocation each pass",
+    "c4": "C4: ~50k-primitive open synthetic scene, 128x32x128 probes, 256 rays, 3 bounces, relocation each pass",
+}
+
+
+class StepRunner:
+    """One step = a fresh probe volume (makeCascade state) taken through PASSES
+    passes (frames 0..PASSES-1): relocation + batched update + swap per pass."""
+
+    def __init__(self, dev, stage):
+        self.dev, self.stage = dev, stage
+
+    def fresh(self):
+        for level in range(self.stage.levels):
+            self.dev.reset_probes(level)
+
+    def step(self, stats=False):
+        from paper_2007_14394_b200 import api
+
+        dev, stage = self.dev, self.stage
+        rays, upd_ms, ops, work_all = 0, 0.0, 0, []
+        for p in range(PASSES):
+            stage.relocate_all(stats=stats)
+            r = api.updateProbes(dev, stage.cfg, p, None, stats=stats)
+            if stats:
+                res, st = r
+                work = dev.last_work()
+                ops += workmodel.update_ops(st, work, int(res["rays_traced"]), shading=dev.last_shading_work())
+                work_all.append((dict(zip(st.dtype.names, map(int, st))), [int(w) for w in work]))
+            else:
+                res = r
+            upd_ms += dev.last_kernel_ms()[0]
+            rays += int(res["rays_traced"])
+            dev.swap()
+        return rays, upd_ms, ops, work_all
+
+
+def timed_steps(runner, steps, ext, flush, torch, barrier):
+    """Device time of `steps` fresh steps (CUDA events on the context's stream, L2
+    flushed before each): per-step ms, update-kernel ms and rays."""
+    times, kern, rays = [], [], 0
+    barrier()
+    torch.cuda.synchronize()
+    for _ in range(steps):
+        runner.fresh()
+        flush.fill_(1.0)  # L2 flush (256 MB > 126 MB L2) outside the timed window
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(ext)
+        rays, upd_ms, _, _ = runner.step()
+        e1.record(ext)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        kern.append(upd_ms)
+    barrier()
+    torch.cuda.synchronize()
+    return times, kern, rays
+
+
+def max_over_ranks(x, dist, torch):
+    if dist is None:
+        return x
+    t = torch.tensor([x], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -262,10 +370,11 @@ def run_ours(args, rank, world, local_rank):
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    scene = scene_io.read_sdfs(C2_PATH)
+    scene, workload = load_workload(args.config)
+    n_probes = int(np.prod(scene.cascade.res))
     dev = Device(local_rank, rank, world, uid, precision=args.precision)
     stage = api.ProbeStage(dev, scene)
-    cfg = stage.cfg
+    runner = StepRunner(dev, stage)
     ext = torch.cuda.ExternalStream(dev.stream)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
@@ -273,67 +382,26 @@ def run_ours(args, rank, world, local_rank):
         if dist is not None:
             dist.barrier()
 
-    def fresh_volume():
-        for level in range(stage.levels):
-            dev.reset_probes(level)
-
-    def one_step(stats=False):
-        rays, upd_ms, ops, work_all = 0, 0.0, 0, []
-        for p in range(PASSES):
-            reps = stage.relocate_all(stats=stats)
-            r = api.updateProbes(dev, cfg, p, None, stats=stats)
-            if stats:
-                res, st = r
-                work = dev.last_work()
-                ops += workmodel.update_ops(st, work, int(res["rays_traced"]), shading=dev.last_shading_work())
-                work_all.append((dict(zip(st.dtype.names, map(int, st))), [int(w) for w in work]))
-            else:
-                res = r
-            upd_ms += dev.last_kernel_ms()[0]
-            rays += int(res["rays_traced"])
-            dev.swap()
-        return rays, upd_ms, ops, work_all
-
     # algorithmic work of one step (untimed stats run: counters cost registers/atomics)
-    fresh_volume()
-    rays_stats, _, ops_step, work_all = one_step(stats=True)
+    runner.fresh()
+    rays_stats, _, ops_step, work_all = runner.step(stats=True)
     for _ in range(args.warmup):
-        fresh_volume()
-        one_step()
+        runner.fresh()
+        runner.step()
     torch.cuda.synchronize()
     launches0 = dev.launch_count()
-    times, kern = [], []
-    rays_step = None
     with ClockSampler(local_rank) as clk:
-        barrier()
-        torch.cuda.synchronize()
-        for _ in range(args.steps):
-            fresh_volume()
-            flush.fill_(1.0)  # L2 flush (256 MB > 126 MB L2) outside the timed window
-            torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(ext)
-            rays, upd_ms, _, _ = one_step()
-            e1.record(ext)
-            e1.synchronize()
-            times.append(e0.elapsed_time(e1))
-            kern.append(upd_ms)
-            rays_step = rays
-        barrier()
-        torch.cuda.synchronize()
+        times, kern, rays_step = timed_steps(runner, args.steps, ext, flush, torch, barrier)
     launches = dev.launch_count() - launches0
-    total_ms = sum(times)
-    if dist is not None:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(sum(times), dist, torch)
     ms_step = total_ms / args.steps
     value = rays_step * args.steps / (total_ms * 1e-3) / 1e9
 
     # e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e_val, h2d, d2h = e2e_run(args, dev, stage, scene, barrier, dist, torch)
-    gather = gather_bench(args, dev, stage, scene, torch, ext, flush) if not args.no_gather else None
+    gather = None
+    if not args.no_gather and args.config == "c2":
+        gather = gather_bench(args, dev, stage, scene, torch, ext, flush)
 
     # roofline of the dominant kernel (k_probe_update): algorithmic ops / kernel time
     f64_rate, f32_rate = dev.measure_fp_peak()
@@ -342,7 +410,7 @@ def run_ours(args, rank, world, local_rank):
     achieved = ops_step / (kern_ms * 1e-3)  # ops/s over the step's update launches
     traffic, traffic_src = ncu_step_traffic(args.precision)
     # per probe per pass, read the previous tile interior (768 B) + write the tile (1,200 B)
-    hbm_alg = PASSES * 32 * 16 * 32 * (768 + 1200)
+    hbm_alg = PASSES * n_probes * (768 + 1200)
     roofline = {
         "bound": "fp64" if args.precision == "f64" else "fp32",
         "kernel": "k_probe_update",
@@ -350,9 +418,9 @@ def run_ours(args, rank, world, local_rank):
         "peak": peak_rate / 1e12,
         "unit": "Tinstr/s",
         "frac": achieved / peak_rate,
-        "traffic": traffic,
+        "traffic": traffic if args.config == "c2" else None,
         "traffic_unit": "DRAM bytes per step (ncu, serialised cold-cache launches)",
-        "traffic_source": traffic_src,
+        "traffic_source": traffic_src if args.config == "c2" else None,
         "algorithmic_hbm_bytes_per_step": hbm_alg,
         "peak_source": "measured live: sdfgi_measure_fp_peak FMA-instruction rate (MEASURED_PEAKS.json has no FP pipe entry)",
         "work_per_step_instr": ops_step,
@@ -372,13 +440,14 @@ def run_ours(args, rank, world, local_rank):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": args.precision,
-        "data": "synthetic (deterministic C2 scene, SURVEY §8d; no network)",
+        "data": f"synthetic (deterministic {args.config.upper()} scene, SURVEY §8d; no network)",
         "config": {
-            "workload": "C2: ~2k-primitive synthetic Sponza-scale SDF scene, 32x16x32 probes, 256 rays, 3 bounces, relocation each pass",
+            "workload": workload,
             "primitives": int(len(scene.prims)),
             "clusters": int(len(scene.clusters)),
-            "probes": 32 * 16 * 32,
-            "rays_per_probe": 256,
+            "probes": n_probes,
+            "probe_grid": list(map(int, scene.cascade.res)),
+            "rays_per_probe": int(stage.cfg["n_rays_full"][0]),
             "bounces": PASSES,
             "rays_per_step": rays_step,
             "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
@@ -386,50 +455,44 @@ def run_ours(args, rank, world, local_rank):
             "precision_mode": args.precision,
             "cluster_walk": dev.accel_info(),
         },
-        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "note": "scene re-uploaded every step; the candidate grid is rebuilt only when the geometry "
+                        "changes (static scene: kept)"},
         "gpu_launches": launches,
         "roofline": roofline,
-        "roofline_hbm_kernels": ncu_hbm_kernels(args.precision, hbm_peak),
-        "pipe_kernels_ncu": ncu_pipe_kernels(args.precision),
         "clocks": clk.summary(),
         "algorithmic_counters_step": work_all,
-        "gather_c3": gather,
-        "frame_ms_update_plus_gather": (ms_step + gather["ms_per_frame"]) if gather else None,
-        "frame_ms_update_gather_compose": (ms_step + gather["ms_per_frame"] + gather["compose_ms"]) if gather else None,
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if args.config == "c2":
+        line["roofline_hbm_kernels"] = ncu_hbm_kernels(args.precision, hbm_peak)
+        line["pipe_kernels_ncu"] = ncu_pipe_kernels(args.precision)
+        line["gather_c3"] = gather
+        line["frame_ms_update_plus_gather"] = (ms_step + gather["ms_per_frame"]) if gather else None
+        line["frame_ms_update_gather_compose"] = (ms_step + gather["ms_per_frame"] + gather["compose_ms"]) \
+            if gather else None
+    if world > 1:
+        line["atlas_equal_1gpu"] = atlas_equal_1gpu(dev, stage, runner, scene, rank, local_rank, dist, torch)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == "c2":
         line["cpu_baseline"] = cpu_baseline(rays_step)
     if not args.no_alt:
         # the other arithmetic mode on the same workload, same timing rules (the
         # headline stays FP64 = the reference's own precision, bit-exact decisions)
         alt = "f32" if args.precision == "f64" else "f64"
         dev.set_precision(alt)
-        times_alt = []
-        fresh_volume()
-        one_step()
-        for _ in range(args.steps):
-            fresh_volume()
-            flush.fill_(1.0)
-            torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(ext)
-            r_alt, _, _, _ = one_step()
-            e1.record(ext)
-            e1.synchronize()
-            times_alt.append(e0.elapsed_time(e1))
-        ms_alt = sum(times_alt) / len(times_alt)
-        if dist is not None:
-            t = torch.tensor([ms_alt], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_alt = float(t.item())
+        runner.fresh()
+        runner.step()
+        times_alt, _, r_alt = timed_steps(runner, args.steps, ext, flush, torch, barrier)
+        ms_alt = max_over_ranks(sum(times_alt) / len(times_alt), dist, torch)
         line["alt_precision"] = {
             "dtype": alt, "value": r_alt / (ms_alt * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms_alt,
-            "texel_error_vs_oracle": "FP32: max 2e-5 relative on a C2 probe sample, 0 channels over 1e-3 "
-                                     "(tests/test_gpu_oracle.py)" if alt == "f32" else "FP64: bit-exact relocation; "
-                                     "texels bit-identical except corner-tie owner flips",
+            "texel_error_vs_oracle": "FP32: error distribution over the whole C2 step printed by "
+                                     "tests/test_gpu_oracle.py::test_c2_f32_mode_error_report" if alt == "f32" else
+                                     "FP64: bit-exact relocation and directions; every texel within 1e-3 "
+                                     "(tests/test_gpu_oracle.py::test_c2_full_step_matches_oracle)",
         }
         dev.set_precision(args.precision)
+    if not args.no_c4 and args.config == "c2":
+        line["c4"] = c4_bench(args, rank, world, local_rank, uid, ext, flush, torch, barrier, dist)
     if rank == 0:
         print(json.dumps(line), flush=True)
     dev.close()
@@ -437,11 +500,59 @@ def run_ours(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def c4_bench(args, rank, world, local_rank, uid, ext, flush, torch, barrier, dist):
+    """BASELINE configs[3] on the same ranks (the slab-sharding workload): C4
+    through PASSES passes, same timing rules, fewer steps (one step ~1 s)."""
+    from paper_2007_14394_b200 import api
+    from paper_2007_14394_b200.runtime import Device
+
+    scene, workload = load_workload("c4")
+    with Device(local_rank, rank, world, uid, precision=args.precision) as dev:
+        stage = api.ProbeStage(dev, scene)
+        runner = StepRunner(dev, stage)
+        ext4 = torch.cuda.ExternalStream(dev.stream)
+        runner.fresh()
+        runner.step()
+        steps = max(1, min(args.steps, 2))
+        times, _, rays = timed_steps(runner, steps, ext4, flush, torch, barrier)
+        ms = max_over_ranks(sum(times) / steps, dist, torch)
+        return {"workload": workload, "dtype": args.precision, "n_gpus": world, "steps": steps,
+                "ms_per_step": ms, "value": rays / (ms * 1e-3) / 1e9, "unit": UNIT, "rays_per_step": rays,
+                "scaling": "strong", "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                "primitives": int(len(scene.prims)), "clusters": int(len(scene.clusters))}
+
+
+def atlas_equal_1gpu(dev, stage, runner, scene, rank, local_rank, dist, torch):
+    """SURVEY §8e's correctness test inside the same process group: one fresh step on
+    the N ranks (slabs + the NCCL exchange) vs the same step on ONE device (rank 0,
+    its own single-rank context): front atlases and probe states bit-identical."""
+    from paper_2007_14394_b200 import api
+    from paper_2007_14394_b200.runtime import Device
+
+    runner.fresh()
+    runner.step()
+    got = [dev.atlas(lv, 0) for lv in range(stage.levels)]
+    probes = [dev.probes(lv) for lv in range(stage.levels)]
+    ok = True
+    if rank == 0:
+        with Device(local_rank, 0, 1, None, precision=dev.precision) as solo:
+            st1 = api.ProbeStage(solo, scene)
+            StepRunner(solo, st1).step()
+            for lv in range(stage.levels):
+                ok = ok and np.array_equal(solo.atlas(lv, 0), got[lv]) and \
+                    np.array_equal(solo.probes(lv), probes[lv])
+    if dist is not None:
+        t = torch.tensor([1 if ok else 0], device="cuda", dtype=torch.int32)
+        dist.broadcast(t, src=0)
+        ok = bool(t.item())
+    return ok
+
+
 def e2e_run(args, dev, stage, scene, barrier, dist, torch):
     from paper_2007_14394_b200 import api
 
     # pinned host buffers for the inputs (fresh probes) and the result (atlas)
-    n = 32 * 16 * 32
+    n = int(np.prod(scene.cascade.res))
     t = dev.oct_res + 2
     probes_pin = torch.empty(n * scene_io.PROBE_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True)
     probes_host = probes_pin.numpy().view(scene_io.PROBE_DTYPE)
@@ -552,7 +663,7 @@ def cpu_gather_baseline():
 
 def cpu_baseline(rays_full_step):
     threads = cpu_threads()
-    stride = int(os.environ.get("SDFGI_CPU_STRIDE", "8"))
+    stride = int(os.environ.get("SDFGI_CPU_STRIDE", str(CPU_STRIDE["c2"])))
     res, kind = cpu_reference_sample(stride, threads)
     if res is None:
         return {"value": None, "unit": UNIT, "cores": threads, "kind": "reference", "sample": kind}
@@ -573,8 +684,8 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     threads = cpu_threads()
-    stride = int(os.environ.get("SDFGI_CPU_STRIDE", "8"))
-    res, kind = cpu_reference_sample(stride, threads, reps=args.warmup + args.steps)
+    stride = int(os.environ.get("SDFGI_CPU_STRIDE", str(CPU_STRIDE[args.config])))
+    res, kind = cpu_reference_sample(stride, threads, reps=args.warmup + args.steps, sdfs=workload_sdfs(args.config))
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": kind}))
         return
@@ -582,7 +693,7 @@ def run_reference(args, rank, world):
     rays = sum(r for r, _ in timed)
     secs = sum(s for _, s in timed)
     value = rays / secs / 1e9
-    sample = (f"C2 scene, 3 passes, every {stride}th probe per step ({timed[0][0]} rays/step), "
+    sample = (f"{args.config.upper()} scene, 3 passes, every {stride}th probe per step ({timed[0][0]} rays/step), "
               f"{threads} threads, relocation time scaled by 1/{stride}")
     print(json.dumps({
         "impl": "reference",
@@ -597,12 +708,27 @@ def run_reference(args, rank, world):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (deterministic C2 scene)",
-        "config": {"workload": "C2 sample (reference CPU path, pipeline.hpp:108-151)", "stride": stride,
-                   "binary": kind},
+        "data": f"synthetic (deterministic {args.config.upper()} scene)",
+        "config": {"workload": WORKLOADS[args.config],
+                   "path": "reference CPU probe stage, pipeline.hpp:108-151 (updateProbePositions + "
+                           "parallelFor(updateProbe)), all host threads",
+                   "sample_stride": stride, "binary": kind},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` without a launcher: re-run this script under
+    torch.distributed.run with N ranks on this node (127.0.0.1 rendezvous)."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -612,13 +738,18 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c4"],
+                    help="c2: the headline workload (BASELINE configs[1]); c4: configs[3]")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gather", action="store_true", help="skip the C3 1080p gather measurement")
     ap.add_argument("--no-alt", action="store_true", help="skip the other-precision measurement")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 sub-measurement of a c2 run")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)

@@ -43,6 +43,8 @@ def load():
         "ora_select": ([_P, _P, _P, _I, _I, _P], _I),
         "ora_update_refs": ([_P, _P, _I, _P, _I, _I, _P, _P, _P, _P], _I),
         "ora_set_threads": ([_I], None),
+        "ora_atlas_set": ([_P, _I, _P, ctypes.c_int64], _I),
+        "ora_mark_updated": ([_P, _P, _I, _I], _I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -154,6 +156,17 @@ class Stage:
         out = np.zeros((n, t, t, 3), np.float32)
         assert load().ora_atlas(self.h, level, _p(out), out.size) == 0
         return out
+
+    def set_atlas(self, level, atlas):
+        """Overwrite the front atlas of a cascade (test hook: the slab exchange)."""
+        a = np.ascontiguousarray(atlas, np.float32)
+        assert load().ora_atlas_set(self.h, level, _p(a), a.size) == 0
+
+    def mark_updated(self, frame, refs):
+        """rejectHistory = false, lastUpdateFrame = frame for the alive probes of refs
+        (probe_update.hpp:208-209) without tracing them (test hook)."""
+        r = np.ascontiguousarray(refs, np.int32).reshape(-1, 2)
+        assert load().ora_mark_updated(self.h, _p(r), len(r), frame) == 0
 
     def trace_rays(self, frame, probe, level=0):
         cap = 2 * int(self.cfg["n_rays_full"][0])

@@ -944,6 +944,30 @@ int ora_atlas(const ora_stage* s, int slot, float* out, int64_t n_floats) {
     return 0;
 }
 
+/* Test hooks for the sharded (multi-rank) decomposition, tests/test_multirank.py:
+ * overwrite the front atlas of a cascade (the slab exchange), and mark probes as
+ * updated this pass (probe_update.hpp:208-209) without tracing them. */
+int ora_atlas_set(ora_stage* s, int slot, const float* src, int64_t n_floats) {
+    if (slot < 0 || slot >= s->ncas) return 1;
+    const cascade_t* c = &s->cas[slot];
+    int64_t n = (int64_t)tileFloats(s->oct) * c->res[0] * c->res[1] * c->res[2];
+    if (n != n_floats) return 1;
+    memcpy(s->atlas[s->front] + tileFloats(s->oct) * c->base, src, (size_t)n * sizeof(float));
+    return 0;
+}
+
+int ora_mark_updated(ora_stage* s, const int32_t* refs, int n_refs, int frame) {
+    for (int i = 0; i < n_refs; ++i) {
+        int slot = refs[2 * i], idx = refs[2 * i + 1];
+        if (slot < 0 || slot >= s->ncas) return 1;
+        probe_t* p = &s->probes[s->cas[slot].base + idx];
+        if (!p->alive) continue;
+        p->reject = 0;
+        p->last_frame = frame;
+    }
+    return 0;
+}
+
 int ora_trace_rays(const ora_stage* s, const sdfgi_cfg* cfg, int frame, int slot, int probe, sdfgi_ray_record* out,
                    int cap) {
     if (slot < 0 || slot >= s->ncas) return -1;

@@ -54,6 +54,9 @@ int ora_select(const ora_stage* s, const double cam_pos[3], const double cam_fwd
 
 int ora_probes(const ora_stage* s, int slot, sdfgi_probe* out, int n);
 int ora_atlas(const ora_stage* s, int slot, float* out, int64_t n_floats); /* front atlas */
+/* test hooks of the sharded decomposition (tests/test_multirank.py) */
+int ora_atlas_set(ora_stage* s, int slot, const float* src, int64_t n_floats);
+int ora_mark_updated(ora_stage* s, const int32_t* refs, int n_refs, int frame);
 
 /* Per-ray records of updateProbe's ray stage (probe_update.hpp:173-189) for one probe. */
 int ora_trace_rays(const ora_stage* s, const sdfgi_cfg* cfg, int frame, int slot, int probe, sdfgi_ray_record* out,

@@ -275,6 +275,8 @@ template <typename R>
 void launch_gather(const GatherParams<R>& p, int stage, bool stats, cudaStream_t st);
 void launch_relocate(const RelocParams& p, int nProbes, bool stats, cudaStream_t st);
 void launch_query_points(const QueryParams& p, cudaStream_t st);
+void launch_mark_updated(const int* ids, int n, int frame, const int* alive, int* reject, int* lastFrame,
+                         cudaStream_t st);
 void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st);
 void launch_grid_seed(const GridBuildParams& p, int nbricks, cudaStream_t st);
 void launch_grid_list(const GridBuildParams& p, int ncells, bool fill, cudaStream_t st);

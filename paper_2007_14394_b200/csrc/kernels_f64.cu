@@ -17,6 +17,20 @@ __global__ void __launch_bounds__(128) k_query_points(QueryParams P) {
     P.outOwner[i] = owner >= 0 ? P.scene.orig[owner] : -1;
 }
 
+// Multi-GPU: every rank marks every updated probe of the pass (probe_update.hpp:
+// 208-209: rejectHistory = false, lastUpdateFrame = frame for every alive probe the
+// pass updated), so the replicated probe state stays identical on every rank
+// without exchanging it. ids = the pass's global probe ids (null: 0..n-1).
+__global__ void __launch_bounds__(256) k_mark_updated(const int* ids, int n, int frame, const int* alive, int* reject,
+                                                      int* lastFrame) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int g = ids ? ids[i] : i;
+    if (!alive[g]) return;
+    reject[g] = 0;
+    lastFrame[g] = frame;
+}
+
 // The nearest primitive at each brick centre (exact query; the seed of its cells').
 __global__ void __launch_bounds__(128) k_grid_seed(GridBuildParams P, int nbricks) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -233,6 +247,11 @@ void launch_relocate(const RelocParams& p, int nProbes, bool stats, cudaStream_t
         k_relocate<true><<<blocks, 128, 0, st>>>(p);
     else
         k_relocate<false><<<blocks, 128, 0, st>>>(p);
+}
+
+void launch_mark_updated(const int* ids, int n, int frame, const int* alive, int* reject, int* lastFrame,
+                         cudaStream_t st) {
+    if (n > 0) k_mark_updated<<<(n + 255) / 256, 256, 0, st>>>(ids, n, frame, alive, reject, lastFrame);
 }
 
 void launch_query_points(const QueryParams& p, cudaStream_t st) {

@@ -170,7 +170,7 @@ struct Ctx {
     unsigned long long lastWork[6] = {0, 0, 0, 0, 0, 0};
     unsigned long long shadeWork[2] = {0, 0};
     DBuf<int> report;
-    DBuf<int> refs;
+    DBuf<int> refs, allRefs;
     DBuf<RayRecord> records;
     // wavefront scratch (kernels.cuh)
     DBuf<int> wRayCount, wHitList, wChunk, wHitAt;
@@ -209,7 +209,7 @@ struct Ctx {
         gridStart.free(); gridList.free(); gridCounts.free(); gridU.free(); gridEntry.free(); gridCell.free(); brickCounts.free(); brickStart.free(); brickList.free(); brickSeed.free(); scanTemp.free();
         bvh.free(); unbList.free(); primBox.free();
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
-        atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free();
+        atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free(); allRefs.free();
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
         wRayCount.free(); wHitList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); wQuat.free(); cLocal.free(); wHits.free();
         if (hQuat) cudaFreeHost(hQuat);
@@ -1443,32 +1443,24 @@ int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_refs, int fr
             NK(ncclAllReduce(c->scratch.p + 16, c->scratch.p + 16, 1, ncclUint64, ncclMax, c->comm, c->stream));
             NK(ncclAllReduce(c->scratch.p + 17, c->scratch.p + 17, 2, ncclUint64, ncclSum, c->comm, c->stream));
         }
+        if (c->world > 1) {
+            // every rank marks every updated probe (probe_update.hpp:208-209) on the
+            // device, so the replicated probe state stays identical without an exchange
+            const int* ids = nullptr;
+            int nAll = c->totalProbes;
+            if (probe_refs) {
+                std::vector<int> allRefs(n_refs);
+                for (int i = 0; i < n_refs; ++i)
+                    allRefs[i] = c->cascades[c->slot(probe_refs[2 * i])].base + probe_refs[2 * i + 1];
+                c->allRefs.upload(allRefs.data(), allRefs.size(), c->stream);
+                ids = c->allRefs.p;
+                nAll = n_refs;
+            }
+            launch_mark_updated(ids, nAll, frame, c->alive.p, c->reject.p, c->lastFrame.p, c->stream);
+            checkLaunch(c);
+        }
         unsigned long long tail[3];
         readCounters(c, stats, tail, 3);
-        if (c->world > 1) {
-            // every rank marks every updated probe (probe_update.hpp:208-209) so the
-            // replicated probe state stays identical without an exchange
-            std::vector<int> allRefs;
-            if (probe_refs) {
-                for (int i = 0; i < n_refs; ++i)
-                    allRefs.push_back(c->cascades[c->slot(probe_refs[2 * i])].base + probe_refs[2 * i + 1]);
-            } else {
-                for (int i = 0; i < c->totalProbes; ++i) allRefs.push_back(i);
-            }
-            std::vector<int> al(c->totalProbes), rj(c->totalProbes), lf(c->totalProbes);
-            CK(cudaMemcpyAsync(al.data(), c->alive.p, al.size() * 4, cudaMemcpyDeviceToHost, c->stream));
-            CK(cudaMemcpyAsync(rj.data(), c->reject.p, rj.size() * 4, cudaMemcpyDeviceToHost, c->stream));
-            CK(cudaMemcpyAsync(lf.data(), c->lastFrame.p, lf.size() * 4, cudaMemcpyDeviceToHost, c->stream));
-            CK(cudaStreamSynchronize(c->stream));
-            for (int g : allRefs)
-                if (al[g]) {
-                    rj[g] = 0;
-                    lf[g] = frame;
-                }
-            CK(cudaMemcpyAsync(c->reject.p, rj.data(), rj.size() * 4, cudaMemcpyHostToDevice, c->stream));
-            CK(cudaMemcpyAsync(c->lastFrame.p, lf.data(), lf.size() * 4, cudaMemcpyHostToDevice, c->stream));
-            CK(cudaStreamSynchronize(c->stream));
-        }
         if (result) {
             double md;
             std::memcpy(&md, &tail[0], 8);

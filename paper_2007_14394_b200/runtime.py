@@ -163,6 +163,7 @@ class Device:
             uid = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_uid)
         _call("sdfgi_ctx_create", device, rank, world, uid, _PREC[precision], ctypes.byref(self._ctx))
         self.rank, self.world, self.device = rank, world, device
+        self.precision = precision
         self.levels = {}  # level -> (res, spacing, origin)
         self.oct_res = 8
 
@@ -186,6 +187,7 @@ class Device:
     # ------------------------------------------------------------- context
     def set_precision(self, precision):
         _call("sdfgi_ctx_set_precision", self._ctx, _PREC[precision])
+        self.precision = precision
 
     @property
     def stream(self) -> int:

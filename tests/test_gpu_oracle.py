@@ -82,8 +82,9 @@ def test_c2_relocation_bit_exact_full_volume(dev, scene):
 def test_c2_full_step_matches_oracle(dev, scene, oracle_c2):
     """The bench workload itself, every probe of the 32x16x32 volume through all 3
     bounces (15M rays) against the oracle: relocation reports and probe states
-    bit-exact; every texel channel within the north-star 1e-3 relative; nearly all
-    texels bit-identical (the MVC sines are evaluated algebraically, a few ulps)."""
+    bit-exact; every texel channel within the north-star 1e-3 relative. Measured:
+    every texel of all three bounces bit-identical to the oracle (the MVC sines are
+    evaluated algebraically, a few FP64 ulps, which the float texels absorb)."""
     stage = api.ProbeStage(dev, scene)
     for p, want in enumerate(oracle_c2["passes"]):
         rep = stage.relocate_all()[0]
@@ -98,7 +99,7 @@ def test_c2_full_step_matches_oracle(dev, scene, oracle_c2):
         err = rel_err(ga, oa)
         print(f"C2 pass {p}: max texel rel err {err.max():.3e}, bit-identical {np.mean(ga == oa):.6f}")
         assert err.max() <= 1e-3, (p, err.max())
-        assert np.mean(ga == oa) > 0.99, p
+        assert np.mean(ga == oa) > 0.9999, p
 
 
 def test_c2_full_frame_deterministic_and_non_negative(dev, scene):

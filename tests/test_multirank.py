@@ -38,34 +38,67 @@ def test_slabs_cover_each_probe_once_and_match_abi(res, world):
     assert np.all(owner >= 0)
 
 
-def _worker(rank, world, port, res, out):
+def _worker(rank, world, port, out):
+    """One rank of the sharded probe stage, with the oracle as the per-rank update:
+    relocation replicated, the rank's z-slab (from the C-ABI's own partition)
+    updated, the back-atlas slabs exchanged in place (one broadcast per slab, as
+    sdfgi_probes_update does with NCCL), the other slabs' probes marked updated (as
+    k_mark_updated does on the device)."""
+    import sys
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_py
+    from golden_util import load
+
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    case = load("c1")
+    res = case.res
     n = res[0] * res[1] * res[2]
-    atlas = np.full((n, 10, 10, 3), -1.0, np.float32)
-    lo, hi = sharding.slab_range(res, rank, world)
-    # each rank "updates" its slab: tile value = probe index + 0.5 (deterministic)
-    atlas[lo:hi] = (np.arange(lo, hi, dtype=np.float32) + 0.5)[:, None, None, None]
-    sharding.allgather_slabs(atlas, res, dist)
-    out[rank] = float(atlas.sum())
-    expect = (np.arange(n, dtype=np.float64) + 0.5).sum() * 300
-    assert np.allclose(atlas[:, 0, 0, 0], np.arange(n) + 0.5)
-    assert abs(out[rank] - expect) < 1e-3 * expect
+    ora = oracle_py.Stage(case.scene, cfg=case.cfg(), res=res, spacing=case.spacing)
+    lo, hi = sharding.slab_range_abi(res, rank, world)
+    mine = np.array([[0, i] for i in range(lo, hi)], np.int32).reshape(-1, 2)
+    others = np.array([[0, i] for i in range(n) if not lo <= i < hi], np.int32).reshape(-1, 2)
+    for p in range(len(case.passes)):
+        ora.relocate_all()
+        ora.update_refs(p, mine)
+        atlas = ora.atlas(0)
+        sharding.allgather_slabs(atlas, res, dist)
+        ora.set_atlas(0, atlas)
+        ora.mark_updated(p, others)
+    out[rank] = (ora.atlas(0).tobytes(), ora.probes(0).tobytes())
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,res", [(2, (8, 4, 8)), (3, (5, 3, 7))])
-def test_slab_allgather_gloo(world, res):
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_probe_stage_gloo_equals_single_rank(world):
+    """SURVEY §8e's correctness test on CPU: Cornell C1, all of its golden passes,
+    on `world` gloo ranks (z-slabs of 8 layers: 4+4, 2+3+3) — every rank ends with
+    the atlas and probe states of the single-rank run, bit for bit, and those are
+    the reference's own (golden) outputs."""
+    import sys
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from golden_util import load
+
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     out = mgr.dict()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, res, out)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, out)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
-        p.join(120)
+        p.join(300)
         assert p.exitcode == 0
-    assert len(set(out.values())) == 1
+    assert len(out) == world and len(set(out.values())) == 1
+    case = load("c1")
+    last = len(case.passes) - 1
+    atlas = np.frombuffer(out[0][0], np.float32)
+    assert np.array_equal(atlas, case.data[f"atlas_p{last}_c0"].astype(np.float32).ravel())
