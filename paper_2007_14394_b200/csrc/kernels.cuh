@@ -99,6 +99,7 @@ template <typename R> struct WaveParams {
     TraceCfg tc;
     const float* prevAtlas;   // front (read) atlas, all cascades concatenated
     float* currAtlas;         // back (write) atlas
+    int prevZero;             // the whole front atlas is zero: every bounce lookup adds exactly 0 (skipped)
     int oct;
     int frame;
     double hysteresis, alphaMin;
@@ -118,6 +119,7 @@ template <typename R> struct WaveParams {
     HitRec<R>* hits;          // per ray
     int* hitList;             // compacted ray ids of converged hits with an owner, in trace order
     int* hitAt;               // per trace-order item: its ray id if a lit hit, else -1 (compacted to hitList)
+    int* mvcList;             // K3a -> K3c: ray ids of hits whose bounce lookup takes the MVC path
     void* selTemp;            // CUB temporary storage of the compaction
     size_t selTempBytes;
     long long maxItems;       // hitAt slots (the batch's upper bound of rays)
@@ -294,8 +296,8 @@ constexpr int kWaveThreads = 128;   // K1/K2 persistent CTAs
 // line would serialise there (and slow every read of the line); the per-light
 // shadow-march counts follow, read-only while K2 runs.
 constexpr int kCtrRay = 0, kCtrHits = 16, kCtrShadow = 32, kCtrParkRay = 48, kCtrFarRay = 64, kCtrParkShadow = 80,
-              kCtrFarShadow = 96;
-constexpr int kLightCtr = 112;
+              kCtrFarShadow = 96, kCtrMvc = 112;
+constexpr int kLightCtr = 128;
 // minimum resident K1/K2/K3a CTAs per SM (register cap = 64K / (128 * n)); the
 // tracing kernels are latency bound at low occupancy (measured, profiles/)
 #ifndef SDFGI_WAVE_MINB64
@@ -319,6 +321,10 @@ template <typename R> struct WaveOcc {
     static constexpr int shade = SDFGI_SHADE_MINB;
 };
 constexpr int kShadeThreads = 128;  // per-ray shading
+#ifndef SDFGI_MVC_MINB
+#define SDFGI_MVC_MINB 5
+#endif
+constexpr int kMvcMinBlocks = SDFGI_MVC_MINB;  // K3c resident CTAs per SM (128 threads, one MVC hit per thread)
 // K3b CTA per probe: one thread per texel summing its three channels over the
 // rays (one cosine per (texel, ray) instead of three), or per (texel, channel)
 #ifndef SDFGI_CONV_TEXEL

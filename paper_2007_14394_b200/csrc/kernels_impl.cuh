@@ -849,11 +849,47 @@ __device__ __forceinline__ V3<double> shadeRay(const WaveParams<R>& P, const Hit
     return radiance;
 }
 
+// shadeHit with the bounce lookup's MVC path deferred: the radiance so far (emission
+// + directIrradiance, and the trilinear bounce when the stencil takes it) in *out;
+// true when the stencil takes the MVC path (probe_volume.hpp:278), whose bounce
+// term K3c adds (radiance = radiance + brdf * (prev * bounceCoeff), the same
+// addition in the same order as probe_update.hpp:143-147).
+template <typename R>
+__device__ __forceinline__ bool shadeRayDeferred(const WaveParams<R>& P, const HitRec<R>& h, unsigned long long rid,
+                                                 V3<double>* out) {
+    const SceneView<R>& s = P.scene;
+    if (!(h.status & 1) || h.owner < 0) {
+        *out = mk(s.sky[0], s.sky[1], s.sky[2]);
+        return false;
+    }
+    const V3<double> total = directLight(P, h, rid);
+    const double* A = s.albedo + 3 * h.owner;
+    const double* E = s.emission + 3 * h.owner;
+    const V3<double> brdf = mk(A[0], A[1], A[2]) / kPi;
+    V3<double> radiance = mk(E[0], E[1], E[2]) + brdf * total;
+    *out = radiance;
+    if (!(P.tc.bounceCoeff > 0 && P.prevAtlas != nullptr && P.pc.nCas > 0) || P.prevZero) return false;
+    const V3<double> hp = mk<double>(h.p[0], h.p[1], h.p[2]);
+    const V3<double> hn = mk<double>(h.n[0], h.n[1], h.n[2]);
+    const StencilCell sc = stencilCell(P.pc.cas, P.pc.nCas, P.pc.probes, hp, P.tc.mvcFrac);
+    if (sc.chosen < 0) return false;  // sky fallback: no bounce
+    if (sc.wantMvc) return true;
+    double w[8];
+    for (int k = 0; k < 8; ++k) w[k] = trilinearWeight(sc, k);
+    const Stencil st = finishStencil(P.pc.cas, P.pc.probes, sc, w, 0);
+    V3<double> prev;
+    if (bounceFromStencil<R>(P.pc.cas, P.pc.probes, P.prevAtlas, P.oct, st, hp, hn, &prev))
+        *out = radiance + brdf * (prev * P.tc.bounceCoeff);
+    return false;
+}
+
 // K3a: shadeHit per ray (thread per ray, grid-stride): emission + directIrradiance
 // summed in light order with the K2 visibilities + the bounce lookup; radiance to
-// P.rad (3 per ray). Kept apart from the convolution so the stencil/MVC register
-// footprint does not cap the convolution's occupancy.
-template <typename R, bool ST>
+// P.rad (3 per ray). Kept apart from the convolution so the stencil register
+// footprint does not cap the convolution's occupancy. DEFER: hits whose stencil
+// takes the MVC path are appended to P.mvcList and finished by K3c (16 lanes per
+// hit); !DEFER (per-ray debug records) evaluates the MVC inline.
+template <typename R, bool ST, bool DEFER>
 __global__ void __launch_bounds__(128, WaveOcc<R>::shade) k_shade_rays(WaveParams<R> P) {
     // the compacted hit list (misses got the sky radiance in K1); every ray when
     // per-ray debug records are written
@@ -867,7 +903,22 @@ __global__ void __launch_bounds__(128, WaveOcc<R>::shade) k_shade_rays(WaveParam
         const long long rid = all ? i : static_cast<long long>(P.hitList[i]);
         const HitRec<R> h = ldStream(&P.hits[rid]);
         int mvc = 0;
-        const V3<double> L = shadeRay(P, h, static_cast<unsigned long long>(rid), slab, ST ? &mvc : nullptr);
+        V3<double> L;
+        if constexpr (DEFER) {
+            const bool defer = shadeRayDeferred(P, h, static_cast<unsigned long long>(rid), &L);
+            const unsigned am = __activemask();
+            const unsigned m = __ballot_sync(am, defer);
+            if (m) {
+                const int leader = __ffs(m) - 1;
+                unsigned long long base = 0;
+                if (static_cast<int>(threadIdx.x & 31) == leader)
+                    base = atomicAdd(P.ctr + kCtrMvc, static_cast<unsigned long long>(__popc(m)));
+                base = __shfl_sync(am, base, leader);
+                if (defer) P.mvcList[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = static_cast<int>(rid);
+            }
+        } else {
+            L = shadeRay(P, h, static_cast<unsigned long long>(rid), slab, ST ? &mvc : nullptr);
+        }
         if (ST && (h.status & 1) && h.owner >= 0) {
             ++nShaded;
             nMvc += mvc;
@@ -908,6 +959,43 @@ __global__ void __launch_bounds__(128, WaveOcc<R>::shade) k_shade_rays(WaveParam
             if (nShaded) atomicAdd(P.stats + 20, nShaded);
             if (nMvc) atomicAdd(P.stats + 21, nMvc);
         }
+    }
+}
+
+// K3c: the bounce lookup of the hits K3a deferred (interpolationStencil with
+// mvcWeightsHex, mean_value.hpp:16-107, then sampleBounceIrradiance's lookup,
+// probe_update.hpp:63-92), one thread per hit over the compacted list: every lane
+// of a warp runs the MVC (in K3a 18% of a warp's lanes took the trilinear path and
+// idled), and K3a no longer carries the MVC's registers. The MVC working set lives
+// in a per-thread shared-memory slab.
+template <typename R, bool ST>
+__global__ void __launch_bounds__(128, kMvcMinBlocks) k_shade_mvc(WaveParams<R> P) {
+    extern __shared__ __align__(16) unsigned char k3cSmem[];
+    R* slab = reinterpret_cast<R*>(k3cSmem);
+    const long long n = static_cast<long long>(P.ctr[kCtrMvc]);
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    unsigned long long nMvc = 0;
+    for (long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += stride) {
+        const int rid = P.mvcList[j];
+        const HitRec<R> h = P.hits[rid];
+        const V3<double> hp = mk<double>(h.p[0], h.p[1], h.p[2]);
+        const V3<double> hn = mk<double>(h.n[0], h.n[1], h.n[2]);
+        const Stencil st = interpolationStencil<R, true>(P.pc.cas, P.pc.nCas, P.pc.probes, hp, P.tc.mvcFrac, slab);
+        if (ST) nMvc += st.usedMvc;
+        V3<double> prev;
+        if (bounceFromStencil<R>(P.pc.cas, P.pc.probes, P.prevAtlas, P.oct, st, hp, hn, &prev)) {
+            const double* A = P.scene.albedo + 3 * h.owner;
+            const V3<double> brdf = mk(A[0], A[1], A[2]) / kPi;
+            const V3<double> base = mk(double(P.rad[3 * rid]), double(P.rad[3 * rid + 1]), double(P.rad[3 * rid + 2]));
+            const V3<double> L = base + brdf * (prev * P.tc.bounceCoeff);
+            P.rad[3 * rid] = R(L.x);
+            P.rad[3 * rid + 1] = R(L.y);
+            P.rad[3 * rid + 2] = R(L.z);
+        }
+    }
+    if (ST) {
+        for (int o = 16; o > 0; o >>= 1) nMvc += __shfl_xor_sync(kFull, nMvc, o);
+        if ((threadIdx.x & 31) == 0 && nMvc) atomicAdd(P.stats + 21, nMvc);
     }
 }
 
@@ -1059,7 +1147,9 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
     static int b1f = persistentBlocks(k_trace_primary<R, ST, 0, 1>, kWaveThreads, 0);
     static int b2 = persistentBlocks(k_trace_shadow<R, ST, 0>, kWaveThreads, 0);
     static int b2f = persistentBlocks(k_trace_shadow<R, ST, 1>, kWaveThreads, 0);
-    static int b3 = persistentBlocks(k_shade_rays<R, ST>, 128, 0, 128 * kMvcSlab * sizeof(R));
+    static int b3 = persistentBlocks(k_shade_rays<R, ST, true>, 128, 0);
+    static int b3d = persistentBlocks(k_shade_rays<R, ST, false>, 128, 0, 128 * kMvcSlab * sizeof(R));
+    static int b3c = persistentBlocks(k_shade_mvc<R, ST>, 128, 0, 128 * kMvcSlab * sizeof(R));
     // hitAt covers the batch's upper bound of rays; slots past the traced ones stay -1
     cudaMemsetAsync(p.hitAt, 0xff, static_cast<size_t>(p.maxItems) * sizeof(int), st);
     k_trace_primary<R, ST, 0, 0><<<cap > 0 ? min(cap, b1) : b1, kWaveThreads, 0, st>>>(p);
@@ -1068,7 +1158,12 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
     k_hit_normals<R><<<b3, 128, 0, st>>>(p);
     k_trace_shadow<R, ST, 0><<<cap > 0 ? min(cap, b2) : b2, kWaveThreads, 0, st>>>(p);
     k_trace_shadow<R, ST, 1><<<cap > 0 ? min(cap, b2f) : b2f, kWaveThreads, 0, st>>>(p);
-    k_shade_rays<R, ST><<<b3, 128, 128 * kMvcSlab * sizeof(R), st>>>(p);
+    if (p.debug) {
+        k_shade_rays<R, ST, false><<<b3d, 128, 128 * kMvcSlab * sizeof(R), st>>>(p);
+    } else {
+        k_shade_rays<R, ST, true><<<b3, 128, 0, st>>>(p);
+        k_shade_mvc<R, ST><<<b3c, 128, 128 * kMvcSlab * sizeof(R), st>>>(p);
+    }
     if (!p.debug) {
         const size_t smem = static_cast<size_t>(2 * p.nRaysFull) * 6 * sizeof(R);
         auto k3 = k_convolve<R, ST>;
@@ -1080,7 +1175,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
         k3<<<p.nCand, kConvThreads, smem, st>>>(p);
     }
     if (e1) cudaEventRecord(e1, st);
-    if (launches) *launches += p.debug ? 10 : 11;
+    if (launches) *launches += p.debug ? 10 : 12;
 }
 
 // contactGI's per-pixel sum (shading.hpp:686-713): AO from the missed samples,
@@ -1135,17 +1230,19 @@ static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long*
     static int b1f = persistentBlocks(k_trace_primary<R, ST, 1, 1>, kWaveThreads, 0);
     static int b2 = persistentBlocks(k_trace_shadow<R, ST, 0>, kWaveThreads, 0);
     static int b2f = persistentBlocks(k_trace_shadow<R, ST, 1>, kWaveThreads, 0);
-    static int b3 = persistentBlocks(k_shade_rays<R, ST>, 128, 0, 128 * kMvcSlab * sizeof(R));
+    static int b3 = persistentBlocks(k_shade_rays<R, ST, true>, 128, 0);
+    static int b3c = persistentBlocks(k_shade_mvc<R, ST>, 128, 0, 128 * kMvcSlab * sizeof(R));
     k_trace_primary<R, ST, 1, 0><<<b1, kWaveThreads, 0, st>>>(p);
     k_trace_primary<R, ST, 1, 1><<<b1f, kWaveThreads, 0, st>>>(p);
     compact_hits(p.hitAt, p.hitList, p.ctr + kCtrHits, static_cast<int>(p.maxItems), p.selTemp, p.selTempBytes, st);
     k_hit_normals<R><<<b3, 128, 0, st>>>(p);
     k_trace_shadow<R, ST, 0><<<b2, kWaveThreads, 0, st>>>(p);
     k_trace_shadow<R, ST, 1><<<b2f, kWaveThreads, 0, st>>>(p);
-    k_shade_rays<R, ST><<<b3, 128, 128 * kMvcSlab * sizeof(R), st>>>(p);
+    k_shade_rays<R, ST, true><<<b3, 128, 0, st>>>(p);
+    k_shade_mvc<R, ST><<<b3c, 128, 128 * kMvcSlab * sizeof(R), st>>>(p);
     const long long np = static_cast<long long>(p.gw) * p.gh;
     k_contact_combine<R><<<static_cast<int>((np + 127) / 128), 128, 0, st>>>(p);
-    if (launches) *launches += p.cray ? 9 : 8;
+    if (launches) *launches += p.cray ? 10 : 9;
 }
 
 // composeFrame (shading.hpp:480-504) as a wavefront: every geometry pixel becomes a

@@ -869,11 +869,83 @@ struct CellCorners {
 // broadcast constant load per corner instead of a local-memory table.
 __constant__ const int kMvcFaces[6][4] = {{0, 2, 3, 1}, {4, 5, 7, 6}, {0, 1, 5, 4}, {2, 6, 7, 3}, {0, 4, 6, 2}, {1, 3, 7, 5}};
 
+// One triangle of mvcWeightsHex's loop (mean_value.hpp:45-97) from its corners'
+// distances d and unit vectors u. Returns kTriSkip (degenerate, mean_value.hpp:
+// 80-89: no contribution), kTriAdd (w = the three weight contributions, :91-96),
+// kTriOn (x on the triangle: w = its normalised 2D barycentric weights, :57-71) or
+// kTriFail (on the triangle but degenerate: mvcWeightsHex returns false).
+constexpr int kTriSkip = 0, kTriAdd = 1, kTriOn = 2, kTriFail = 3;
+template <typename M>
+__device__ __forceinline__ int mvcTriangle(const M d[3], const V3<M> u[3], M w[3]) {
+    const M eps = M(1e-10);
+    const M pi = M(kPi);
+    M sa[3], ca[3], theta[3], st[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const M l = length(u[(i + 1) % 3] - u[(i + 2) % 3]);
+        sa[i] = sclamp(l * M(0.5), M(0), M(1));
+        ca[i] = sqrt(smax(M(0), M(1) - sa[i] * sa[i]));
+        theta[i] = M(2) * mvcAsin<M>(sa[i]);
+        st[i] = M(2) * sa[i] * ca[i];
+    }
+    const M h = (theta[0] + theta[1] + theta[2]) * M(0.5);
+    if (pi - h < M(1e-8)) {
+        M total = 0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            w[i] = st[i] * d[(i + 1) % 3] * d[(i + 2) % 3];
+            total += w[i];
+        }
+        if (total < eps) return kTriFail;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) w[i] = w[i] / total;
+        return kTriOn;
+    }
+    V3<M> cr = mk(u[1].y * u[2].z - u[1].z * u[2].y, u[1].z * u[2].x - u[1].x * u[2].z,
+                  u[1].x * u[2].y - u[1].y * u[2].x);
+    const M sign = dot(u[0], cr) >= M(0) ? M(1) : M(-1);
+    // sin h, h = a0 + a1 + a2
+    const M sh = sa[0] * ca[1] * ca[2] + ca[0] * sa[1] * ca[2] + ca[0] * ca[1] * sa[2] - sa[0] * sa[1] * sa[2];
+    M c[3], sv[3];
+    bool skip = false;
+    // FP64: the three divisions by st_j st_k through one reciprocal of
+    // st_0 st_1 st_2 (1 / (st_j st_k) = st_i / P; a few ulps, far inside the
+    // range: a triangle with a product below eps is skipped)
+    const M invP = sizeof(M) == 8 ? M(1) / (st[0] * st[1] * st[2]) : M(0);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const int j = (i + 1) % 3, k = (i + 2) % 3;
+        const M denom = st[j] * st[k];
+        // sin(h - theta_i) = sin(a_j + a_k - a_i)
+        const M sjk = sa[j] * ca[k] + ca[j] * sa[k], cjk = ca[j] * ca[k] - sa[j] * sa[k];
+        const M shi = sjk * ca[i] - cjk * sa[i];
+        if (sizeof(M) == 8)
+            c[i] = M(2) * sh * shi * (st[i] * invP) - M(1);
+        else
+            c[i] = mvcDiv(M(2) * sh * shi, denom) - M(1);
+        sv[i] = sign * sqrt(smax(M(0), M(1) - c[i] * c[i]));
+        // the reference stops at the first degenerate i (mean_value.hpp:80-86);
+        // the values after it are unused either way
+        skip = skip || fabs(denom) < eps || fabs(sv[i]) <= eps;
+    }
+    if (skip) return kTriSkip;
+    M D[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) D[i] = d[i] * st[(i + 1) % 3] * sv[(i + 2) % 3];
+    const M invQ = sizeof(M) == 8 ? M(1) / (D[0] * D[1] * D[2]) : M(0);  // FP64: one division
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const int j = (i + 1) % 3, k = (i + 2) % 3;
+        const M num = theta[i] - c[j] * theta[k] - c[k] * theta[j];
+        w[i] = sizeof(M) == 8 ? num * (D[j] * D[k] * invQ) : mvcDiv(num, D[i]);
+    }
+    return kTriAdd;
+}
+
 // Result: the weights in a.wts(0..7) (precision M; the caller widens to double).
 template <typename M, bool SH>
 __device__ inline bool mvcWeightsHexImpl(const CellCorners& cc, V3<double> xd, MvcArrays<M, SH>& a) {
     const M eps = M(1e-10);
-    const M pi = M(kPi);
     for (int i = 0; i < 8; ++i) a.wts(i) = M(0);
     const V3<M> x = mk(M(xd.x), M(xd.y), M(xd.z));
     for (int i = 0; i < 8; ++i) {
@@ -893,82 +965,28 @@ __device__ inline bool mvcWeightsHexImpl(const CellCorners& cc, V3<double> xd, M
     }
     bool any = false;
 #pragma unroll 1
-    for (int f = 0; f < 6; ++f) {
-#pragma unroll 1
-        for (int tr = 0; tr < 2; ++tr) {
-            const int t0 = kMvcFaces[f][0], t1 = kMvcFaces[f][tr ? 2 : 1], t2 = kMvcFaces[f][tr ? 3 : 2];
-            const int tri[3] = {t0, t1, t2};
-            M d[3], sa[3], ca[3], theta[3], st[3];
-            V3<M> u[3];
+    for (int t = 0; t < 12; ++t) {
+        const int f = t >> 1, tr = t & 1;
+        const int tri[3] = {kMvcFaces[f][0], kMvcFaces[f][tr ? 2 : 1], kMvcFaces[f][tr ? 3 : 2]};
+        M d[3], w[3];
+        V3<M> u[3];
 #pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                d[i] = a.dist(tri[i]);
-                u[i] = mk(a.ux(tri[i]), a.uy(tri[i]), a.uz(tri[i]));
-            }
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                const M l = length(u[(i + 1) % 3] - u[(i + 2) % 3]);
-                sa[i] = sclamp(l * M(0.5), M(0), M(1));
-                ca[i] = sqrt(smax(M(0), M(1) - sa[i] * sa[i]));
-                theta[i] = M(2) * mvcAsin<M>(sa[i]);
-                st[i] = M(2) * sa[i] * ca[i];
-            }
-            const M h = (theta[0] + theta[1] + theta[2]) * M(0.5);
-            if (pi - h < M(1e-8)) {
-                M total = 0;
-                M w[3];
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    w[i] = st[i] * d[(i + 1) % 3] * d[(i + 2) % 3];
-                    total += w[i];
-                }
-                if (total < eps) return false;
-                for (int k = 0; k < 8; ++k) a.wts(k) = M(0);
-#pragma unroll
-                for (int i = 0; i < 3; ++i) a.wts(tri[i]) = w[i] / total;
-                return true;
-            }
-            V3<M> cr = mk(u[1].y * u[2].z - u[1].z * u[2].y, u[1].z * u[2].x - u[1].x * u[2].z,
-                              u[1].x * u[2].y - u[1].y * u[2].x);
-            const M sign = dot(u[0], cr) >= M(0) ? M(1) : M(-1);
-            // sin h, h = a0 + a1 + a2
-            const M sh = sa[0] * ca[1] * ca[2] + ca[0] * sa[1] * ca[2] + ca[0] * ca[1] * sa[2] - sa[0] * sa[1] * sa[2];
-            M c[3], sv[3];
-            bool skip = false;
-            // FP64: the three divisions by st_j st_k through one reciprocal of
-            // st_0 st_1 st_2 (1 / (st_j st_k) = st_i / P; a few ulps, far inside the
-            // range: a triangle with a product below eps is skipped)
-            const M invP = sizeof(M) == 8 ? M(1) / (st[0] * st[1] * st[2]) : M(0);
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                const int j = (i + 1) % 3, k = (i + 2) % 3;
-                const M denom = st[j] * st[k];
-                // sin(h - theta_i) = sin(a_j + a_k - a_i)
-                const M sjk = sa[j] * ca[k] + ca[j] * sa[k], cjk = ca[j] * ca[k] - sa[j] * sa[k];
-                const M shi = sjk * ca[i] - cjk * sa[i];
-                if (sizeof(M) == 8)
-                    c[i] = M(2) * sh * shi * (st[i] * invP) - M(1);
-                else
-                    c[i] = mvcDiv(M(2) * sh * shi, denom) - M(1);
-                sv[i] = sign * sqrt(smax(M(0), M(1) - c[i] * c[i]));
-                // the reference stops at the first degenerate i (mean_value.hpp:80-86);
-                // the values after it are unused either way
-                skip = skip || fabs(denom) < eps || fabs(sv[i]) <= eps;
-            }
-            if (skip) continue;
-            M D[3];
-#pragma unroll
-            for (int i = 0; i < 3; ++i) D[i] = d[i] * st[(i + 1) % 3] * sv[(i + 2) % 3];
-            const M invQ = sizeof(M) == 8 ? M(1) / (D[0] * D[1] * D[2]) : M(0);  // FP64: one division
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                const int j = (i + 1) % 3, k = (i + 2) % 3;
-                const M num = theta[i] - c[j] * theta[k] - c[k] * theta[j];
-                const M w = sizeof(M) == 8 ? num * (D[j] * D[k] * invQ) : mvcDiv(num, D[i]);
-                a.wts(tri[i]) += w;
-                any = true;
-            }
+        for (int i = 0; i < 3; ++i) {
+            d[i] = a.dist(tri[i]);
+            u[i] = mk(a.ux(tri[i]), a.uy(tri[i]), a.uz(tri[i]));
         }
+        const int r = mvcTriangle<M>(d, u, w);
+        if (r == kTriFail) return false;
+        if (r == kTriOn) {
+            for (int k = 0; k < 8; ++k) a.wts(k) = M(0);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) a.wts(tri[i]) = w[i];
+            return true;
+        }
+        if (r == kTriSkip) continue;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) a.wts(tri[i]) += w[i];
+        any = true;
     }
     if (!any) return false;
     M total = 0;
@@ -987,18 +1005,21 @@ struct Stencil {
     int usedMvc;
 };
 
-// interpolationStencil, probe_volume.hpp:224-310 (cell and trilinear weights in
-// double in both modes; MVC in precision M)
-// SLAB_ONLY: the caller always passes a shared slab (K3a), so only that variant
-// of the MVC is compiled in (a second inlined copy cost instruction-cache misses).
-template <typename M = double, bool SLAB_ONLY = false>
-__device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, const ProbesView& pv, V3<double> point,
-                                        double mvcFrac, M* slab = nullptr) {
-    Stencil st;
-    st.count = 0;
-    st.sky = 0;
-    st.usedMvc = 0;
-    st.cascade = -1;
+// interpolationStencil's cell selection (probe_volume.hpp:224-278): the finest
+// containing cascade, the cell, its trilinear coordinates and whether the MVC path
+// is taken. chosen < 0: no cascade contains the point (sky fallback).
+struct StencilCell {
+    int chosen;
+    CellCorners cc;
+    double tx, ty, tz;
+    bool wantMvc;
+};
+__device__ inline StencilCell stencilCell(const CascadeDev* cas, int nCas, const ProbesView& pv, V3<double> point,
+                                          double mvcFrac) {
+    StencilCell sc;
+    sc.chosen = -1;
+    sc.wantMvc = false;
+    sc.tx = sc.ty = sc.tz = 0;
     int chosen = -1;
     int cell[3] = {0, 0, 0};
     int containing = 0;
@@ -1018,16 +1039,17 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
             cell[2] = iz;
         }
     }
+    if (chosen < 0) return sc;
     bool insideCoarser = containing > 1;
-    if (chosen < 0) {
-        st.sky = 1;
-        return st;
-    }
     const CascadeDev& c = cas[chosen];
     V3<double> f = (point - mk(c.origin[0], c.origin[1], c.origin[2])) / c.spacing;
-    double tx = f.x - cell[0], ty = f.y - cell[1], tz = f.z - cell[2];
-    const CellCorners cc{pv.pos, c.base + cell[0] + c.res[0] * (cell[1] + c.res[1] * cell[2]), c.res[0],
-                         c.res[0] * c.res[1]};
+    sc.chosen = chosen;
+    sc.tx = f.x - cell[0];
+    sc.ty = f.y - cell[1];
+    sc.tz = f.z - cell[2];
+    sc.cc = CellCorners{pv.pos, c.base + cell[0] + c.res[0] * (cell[1] + c.res[1] * cell[2]), c.res[0],
+                        c.res[0] * c.res[1]};
+    const CellCorners& cc = sc.cc;
     bool boundary = insideCoarser && (cell[0] == 0 || cell[0] + 2 == c.res[0] || cell[1] == 0 ||
                                       cell[1] + 2 == c.res[1] || cell[2] == 0 || cell[2] + 2 == c.res[2]);
     // maxDisp > mvcFrac * spacing (probe_volume.hpp:263-278) is "some corner's displacement
@@ -1048,9 +1070,69 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
         else if (!squared || !(d2 < thr2 * (1 - 1e-9)))
             wantMvc = sqrt(d2) > thr;
     }
+    sc.wantMvc = wantMvc;
+    return sc;
+}
+
+// trilinear weight of corner k (probe_volume.hpp:290-296)
+__device__ __forceinline__ double trilinearWeight(const StencilCell& sc, int k) {
+    double wx = (k & 1) ? sc.tx : 1 - sc.tx;
+    double wy = ((k >> 1) & 1) ? sc.ty : 1 - sc.ty;
+    double wz = ((k >> 2) & 1) ? sc.tz : 1 - sc.tz;
+    return wx * wy * wz;
+}
+
+// interpolationStencil's ending (probe_volume.hpp:297-309) from the cell's 8
+// weights: dead corners get 0, the sum must exceed 1e-12 (else sky fallback), the
+// weights are normalised.
+__device__ inline Stencil finishStencil(const CascadeDev* cas, const ProbesView& pv, const StencilCell& sc, double* w,
+                                        int usedMvc) {
+    Stencil st;
+    st.count = 0;
+    st.sky = 0;
+    st.usedMvc = usedMvc;
+    st.cascade = -1;
+    const CellCorners& cc = sc.cc;
+    double sum = 0;
+    for (int k = 0; k < 8; ++k) {
+        if (!pv.alive[cc.index(k)]) w[k] = 0;
+        sum += w[k];
+    }
+    if (sum <= 1e-12) {
+        st.sky = 1;
+        return st;
+    }
+    const int base = cas[sc.chosen].base;
+    for (int k = 0; k < 8; ++k) {
+        st.probe[k] = cc.index(k) - base;
+        st.w[k] = w[k] / sum;
+    }
+    st.cascade = sc.chosen;
+    st.count = 8;
+    return st;
+}
+
+// interpolationStencil, probe_volume.hpp:224-310 (cell and trilinear weights in
+// double in both modes; MVC in precision M)
+// SLAB_ONLY: the caller always passes a shared slab, so only that variant of the
+// MVC is compiled in (a second inlined copy cost instruction-cache misses).
+template <typename M = double, bool SLAB_ONLY = false>
+__device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, const ProbesView& pv, V3<double> point,
+                                        double mvcFrac, M* slab = nullptr) {
+    Stencil st;
+    st.count = 0;
+    st.sky = 0;
+    st.usedMvc = 0;
+    st.cascade = -1;
+    const StencilCell sc = stencilCell(cas, nCas, pv, point, mvcFrac);
+    if (sc.chosen < 0) {
+        st.sky = 1;
+        return st;
+    }
+    const CellCorners& cc = sc.cc;
     double w[8];
     bool haveMvc = false;
-    if (wantMvc) {
+    if (sc.wantMvc) {
         if (SLAB_ONLY || slab) {
             MvcArrays<M, true> a(slab);
             haveMvc = mvcWeightsHexImpl<M, true>(cc, point, a);
@@ -1067,46 +1149,26 @@ __device__ inline Stencil interpolationStencil(const CascadeDev* cas, int nCas, 
             st.usedMvc = 1;
         }
     }
-    if (!haveMvc) {
-        for (int k = 0; k < 8; ++k) {
-            double wx = (k & 1) ? tx : 1 - tx;
-            double wy = ((k >> 1) & 1) ? ty : 1 - ty;
-            double wz = ((k >> 2) & 1) ? tz : 1 - tz;
-            w[k] = wx * wy * wz;
-        }
-    }
-    double sum = 0;
-    for (int k = 0; k < 8; ++k) {
-        if (!pv.alive[cc.index(k)]) w[k] = 0;
-        sum += w[k];
-    }
-    if (sum <= 1e-12) {
-        st.sky = 1;
-        return st;
-    }
-    for (int k = 0; k < 8; ++k) {
-        st.probe[k] = cc.index(k) - c.base;
-        st.w[k] = w[k] / sum;
-    }
-    st.cascade = chosen;
-    st.count = 8;
-    return st;
+    if (!haveMvc)
+        for (int k = 0; k < 8; ++k) w[k] = trilinearWeight(sc, k);
+    return finishStencil(cas, pv, sc, w, st.usedMvc);
 }
 
-// sampleBounceIrradiance, probe_update.hpp:63-92. Returns false when "empty".
-template <typename M = double, bool SLAB_ONLY = false>
-__device__ inline bool sampleBounceIrradiance(const CascadeDev* cas, int nCas, const ProbesView& pv,
-                                       const float* atlas, int oct, V3<double> pos, V3<double> normal,
-                                       double mvcFrac, V3<double>* out, M* slab = nullptr, int* usedMvc = nullptr) {
-    if (nCas <= 0) return false;
-    Stencil st = interpolationStencil<M, SLAB_ONLY>(cas, nCas, pv, pos, mvcFrac, slab);
-    if (usedMvc) *usedMvc = st.usedMvc;
+// sampleBounceIrradiance's lookup (probe_update.hpp:70-91) from a finished stencil:
+// backface weight ((cos+1)/2)^2 per probe, renormalised, 8 bilinear lookups at
+// octEncode(normal). Returns false when "empty".
+template <typename M = double>
+__device__ inline bool bounceFromStencil(const CascadeDev* cas, const ProbesView& pv, const float* atlas, int oct,
+                                         const Stencil& st, V3<double> pos, V3<double> normal, V3<double>* out) {
     if (st.sky || st.count == 0) return false;
     const CascadeDev& c = cas[st.cascade];
     double wsum = 0;
     double w[8];
-    for (int i = 0; i < 8; ++i) w[i] = 0;
-    for (int i = 0; i < st.count; ++i) {
+    // a finished stencil has 8 entries (count is 0 or 8): fixed trip counts keep
+    // the arrays in registers
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        w[i] = 0;
         if (st.w[i] <= 0) continue;
         const double* P = pv.pos + 3 * static_cast<size_t>(c.base + st.probe[i]);
         V3<double> toProbe = mk(P[0], P[1], P[2]) - pos;
@@ -1128,12 +1190,24 @@ __device__ inline bool sampleBounceIrradiance(const CascadeDev* cas, int nCas, c
     V3<double> acc = mk(0.0, 0.0, 0.0);
     V2<double> uv = octEncode(normal);
     AtlasView av{atlas, oct, oct + 2};
-    for (int i = 0; i < st.count; ++i) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
         if (w[i] <= 0) continue;
         acc = acc + sampleBilinear(av, c.base + st.probe[i], uv) * (w[i] / wsum);
     }
     *out = acc;
     return true;
+}
+
+// sampleBounceIrradiance, probe_update.hpp:63-92. Returns false when "empty".
+template <typename M = double, bool SLAB_ONLY = false>
+__device__ inline bool sampleBounceIrradiance(const CascadeDev* cas, int nCas, const ProbesView& pv,
+                                       const float* atlas, int oct, V3<double> pos, V3<double> normal,
+                                       double mvcFrac, V3<double>* out, M* slab = nullptr, int* usedMvc = nullptr) {
+    if (nCas <= 0) return false;
+    Stencil st = interpolationStencil<M, SLAB_ONLY>(cas, nCas, pv, pos, mvcFrac, slab);
+    if (usedMvc) *usedMvc = st.usedMvc;
+    return bounceFromStencil<M>(cas, pv, atlas, oct, st, pos, normal, out);
 }
 
 // Everything updateProbe / contactGI needs from RenderConfig (config.hpp:9-50).

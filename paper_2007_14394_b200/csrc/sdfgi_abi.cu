@@ -163,6 +163,17 @@ struct Ctx {
     DBuf<int> alive, reject, lastFrame;
     DBuf<float> atlas[2];
     int front = 0;
+    // atlasZero[b][slot]: cascade `slot` of atlas buffer b is known to be all zeros
+    // (makeCascade / recenter state). While the whole front atlas is zero, every
+    // bounce lookup returns exactly 0 and adds nothing (probe_update.hpp:143-147),
+    // so the probe update skips it (SURVEY §7.7's exact saving: pass 0 of a fresh
+    // volume).
+    std::vector<char> atlasZero[2];
+    bool frontZero() const {
+        for (char z : atlasZero[front])
+            if (!z) return false;
+        return !atlasZero[front].empty();
+    }
     // scratch
     // [0..7] TraceStats, [8..13] evaluations by kind + rotated, [16] maxDelta bits,
     // [17] rays, [18] probes updated
@@ -173,7 +184,7 @@ struct Ctx {
     DBuf<int> refs, allRefs;
     DBuf<RayRecord> records;
     // wavefront scratch (kernels.cuh)
-    DBuf<int> wRayCount, wHitList, wChunk, wHitAt;
+    DBuf<int> wRayCount, wHitList, wChunk, wHitAt, wMvcList;
     DBuf<long long> wRayStart;
     DBuf<double> wRot, fib, wQuat;
     DBuf<int> perm;
@@ -211,7 +222,7 @@ struct Ctx {
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free(); allRefs.free();
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
-        wRayCount.free(); wHitList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); wQuat.free(); cLocal.free(); wHits.free();
+        wRayCount.free(); wHitList.free(); wMvcList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); wQuat.free(); cLocal.free(); wHits.free();
         if (hQuat) cudaFreeHost(hQuat);
         wVis.free(); wPark.free(); wCRay.free(); wSRay.free(); wCtr.free(); perm.free(); wRad.free();
         gbuf.free(); halfDepth.free(); sparseIrr.free(); resolved.free(); indirect.free(); histIrr.free(); composed.free();
@@ -351,8 +362,11 @@ void resetProbes(Ctx* c, int slot) {
     CK(cudaMemcpyAsync(c->alive.p + off, ones.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->reject.p + off, ones.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->lastFrame.p + off, minus.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
-    for (int b = 0; b < 2; ++b)
+    for (int b = 0; b < 2; ++b) {
         CK(cudaMemsetAsync(c->atlas[b].p + off * c->tileFloats(), 0, n * c->tileFloats() * 4, c->stream));
+        c->atlasZero[b].resize(c->cascades.size(), 0);
+        c->atlasZero[b][slot] = 1;
+    }
     CK(cudaStreamSynchronize(c->stream));
 }
 
@@ -373,6 +387,7 @@ void reallocProbes(Ctx* c) {
     c->lastFrame.alloc(total);
     c->atlas[0].alloc(c->atlasFloats());
     c->atlas[1].alloc(c->atlasFloats());
+    for (int b = 0; b < 2; ++b) c->atlasZero[b].assign(c->cascades.size(), 0);
     for (size_t i = 0; i < c->cascades.size(); ++i) resetProbes(c, static_cast<int>(i));
 }
 
@@ -805,6 +820,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     reserve(c->wRot, 9 * static_cast<size_t>(std::max(nCand, 1)));
     reserve(c->wHits, std::max<size_t>(maxRays, 1) * sizeof(HitRec<R>));
     reserve(c->wHitList, std::max<size_t>(maxRays, 1));
+    reserve(c->wMvcList, std::max<size_t>(maxRays, 1));
     reserve(c->wVis, std::max<size_t>(maxRays, 1) * L * sizeof(R));
     reserve(c->wRad, std::max<size_t>(maxRays, 1) * 3 * sizeof(R));
     reserve(c->wCtr, kLightCtr + L);
@@ -840,6 +856,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.nRaysDirect = -1;  // probe batch: ray count from the K0 prefix sum
     p.hits = reinterpret_cast<HitRec<R>*>(c->wHits.p);
     p.hitList = c->wHitList.p;
+    p.mvcList = c->wMvcList.p;
     p.vis = reinterpret_cast<R*>(c->wVis.p);
     p.rad = reinterpret_cast<R*>(c->wRad.p);
     p.ctr = c->wCtr.p;
@@ -850,6 +867,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.parkBytes = p.park ? c->wPark.n : 0;
     p.prevAtlas = c->atlas[c->front].p;
     p.currAtlas = c->atlas[1 - c->front].p;
+    p.prevZero = c->frontZero() ? 1 : 0;
     p.oct = c->octRes;
     p.frame = frame;
     p.tc.eps = cfg->surface_epsilon;
@@ -1408,6 +1426,11 @@ int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_refs, int fr
         CK(cudaMemcpyAsync(back, frontp, c->atlasFloats() * 4, cudaMemcpyDeviceToDevice, c->stream));
         CK(cudaMemsetAsync(c->scratch.p, 0, 32 * 8, c->stream));
         const bool all = (probe_refs == nullptr && c->world == 1);
+        // back <- front (copied above) + the updated tiles: still all-zero only if no
+        // probe anywhere is updated this pass
+        const bool anyUpdate = probe_refs == nullptr ? c->totalProbes > 0 : n_refs > 0;
+        c->atlasZero[1 - c->front] = c->atlasZero[c->front];
+        if (anyUpdate) std::fill(c->atlasZero[1 - c->front].begin(), c->atlasZero[1 - c->front].end(), 0);
         if (!all) c->refs.upload(refs.data(), refs.size(), c->stream);
         const int nCand = static_cast<int>(refs.size());
         if (nCand > 0) {
@@ -1499,6 +1522,7 @@ int sdfgi_atlas_upload(void* ctx, int level, int which, const float* src, size_t
         size_t n = c->tileFloats() * c->cascades[s].count();
         REQ(src && n_floats == n, SDFGI_ERR_INVALID, "atlas size mismatch");
         float* dst = c->atlas[which == 0 ? c->front : 1 - c->front].p + c->tileFloats() * c->cascades[s].base;
+        c->atlasZero[which == 0 ? c->front : 1 - c->front][s] = 0;
         CK(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyHostToDevice, c->stream));
         CK(cudaStreamSynchronize(c->stream));
     });
@@ -1511,6 +1535,7 @@ int sdfgi_atlas_device_ptr(void* ctx, int level, int which, void** out_ptr, size
         REQ(which == 0 || which == 1, SDFGI_ERR_INVALID, "which must be 0 or 1");
         REQ(out_ptr && out_bytes, SDFGI_ERR_INVALID, "null out");
         *out_ptr = c->atlas[which == 0 ? c->front : 1 - c->front].p + c->tileFloats() * c->cascades[s].base;
+        c->atlasZero[which == 0 ? c->front : 1 - c->front][s] = 0;  // the caller may write through it
         *out_bytes = c->tileFloats() * c->cascades[s].count() * 4;
     });
 }
@@ -1690,6 +1715,7 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     const int L = std::max(c->nLights, 1);
     reserve(c->wHits, cap * sizeof(HitRec<R>));
     reserve(c->wHitList, cap);
+    reserve(c->wMvcList, cap);
     reserve(c->wVis, cap * L * sizeof(R));
     reserve(c->wRad, cap * 3 * sizeof(R));
     reserve(c->wCtr, kLightCtr + L);
@@ -1725,6 +1751,7 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     p.seed = cfg->seed;
     p.hits = reinterpret_cast<HitRec<R>*>(c->wHits.p);
     p.hitList = c->wHitList.p;
+    p.mvcList = c->wMvcList.p;
     p.vis = reinterpret_cast<R*>(c->wVis.p);
     p.rad = reinterpret_cast<R*>(c->wRad.p);
     p.ctr = c->wCtr.p;
