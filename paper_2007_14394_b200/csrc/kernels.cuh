@@ -324,7 +324,12 @@ constexpr int kShadeThreads = 128;  // per-ray shading
 #ifndef SDFGI_MVC_MINB
 #define SDFGI_MVC_MINB 5
 #endif
-constexpr int kMvcMinBlocks = SDFGI_MVC_MINB;  // K3c resident CTAs per SM (128 threads, one MVC hit per thread)
+#ifndef SDFGI_MVC_THREADS
+#define SDFGI_MVC_THREADS 128
+#endif
+// K3c: one MVC hit per thread, kMvcThreads per CTA, kMvcMinBlocks resident per SM
+constexpr int kMvcThreads = SDFGI_MVC_THREADS;
+constexpr int kMvcMinBlocks = SDFGI_MVC_MINB;
 // K3b CTA per probe: one thread per texel summing its three channels over the
 // rays (one cosine per (texel, ray) instead of three), or per (texel, channel)
 #ifndef SDFGI_CONV_TEXEL

@@ -967,9 +967,11 @@ __global__ void __launch_bounds__(128, WaveOcc<R>::shade) k_shade_rays(WaveParam
 // probe_update.hpp:63-92), one thread per hit over the compacted list: every lane
 // of a warp runs the MVC (in K3a 18% of a warp's lanes took the trilinear path and
 // idled), and K3a no longer carries the MVC's registers. The MVC working set lives
-// in a per-thread shared-memory slab.
+// in a per-thread shared-memory slab. (Evaluating each of the cell's 18 distinct
+// edge angles once instead of per triangle was measured slower: the larger slab
+// halves the resident warps, profiles/README.md.)
 template <typename R, bool ST>
-__global__ void __launch_bounds__(128, kMvcMinBlocks) k_shade_mvc(WaveParams<R> P) {
+__global__ void __launch_bounds__(kMvcThreads, kMvcMinBlocks) k_shade_mvc(WaveParams<R> P) {
     extern __shared__ __align__(16) unsigned char k3cSmem[];
     R* slab = reinterpret_cast<R*>(k3cSmem);
     const long long n = static_cast<long long>(P.ctr[kCtrMvc]);
@@ -1149,7 +1151,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
     static int b2f = persistentBlocks(k_trace_shadow<R, ST, 1>, kWaveThreads, 0);
     static int b3 = persistentBlocks(k_shade_rays<R, ST, true>, 128, 0);
     static int b3d = persistentBlocks(k_shade_rays<R, ST, false>, 128, 0, 128 * kMvcSlab * sizeof(R));
-    static int b3c = persistentBlocks(k_shade_mvc<R, ST>, 128, 0, 128 * kMvcSlab * sizeof(R));
+    static int b3c = persistentBlocks(k_shade_mvc<R, ST>, kMvcThreads, 0, kMvcThreads * kMvcSlab * sizeof(R));
     // hitAt covers the batch's upper bound of rays; slots past the traced ones stay -1
     cudaMemsetAsync(p.hitAt, 0xff, static_cast<size_t>(p.maxItems) * sizeof(int), st);
     k_trace_primary<R, ST, 0, 0><<<cap > 0 ? min(cap, b1) : b1, kWaveThreads, 0, st>>>(p);
@@ -1162,7 +1164,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
         k_shade_rays<R, ST, false><<<b3d, 128, 128 * kMvcSlab * sizeof(R), st>>>(p);
     } else {
         k_shade_rays<R, ST, true><<<b3, 128, 0, st>>>(p);
-        k_shade_mvc<R, ST><<<b3c, 128, 128 * kMvcSlab * sizeof(R), st>>>(p);
+        k_shade_mvc<R, ST><<<b3c, kMvcThreads, kMvcThreads * kMvcSlab * sizeof(R), st>>>(p);
     }
     if (!p.debug) {
         const size_t smem = static_cast<size_t>(2 * p.nRaysFull) * 6 * sizeof(R);
@@ -1231,7 +1233,7 @@ static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long*
     static int b2 = persistentBlocks(k_trace_shadow<R, ST, 0>, kWaveThreads, 0);
     static int b2f = persistentBlocks(k_trace_shadow<R, ST, 1>, kWaveThreads, 0);
     static int b3 = persistentBlocks(k_shade_rays<R, ST, true>, 128, 0);
-    static int b3c = persistentBlocks(k_shade_mvc<R, ST>, 128, 0, 128 * kMvcSlab * sizeof(R));
+    static int b3c = persistentBlocks(k_shade_mvc<R, ST>, kMvcThreads, 0, kMvcThreads * kMvcSlab * sizeof(R));
     k_trace_primary<R, ST, 1, 0><<<b1, kWaveThreads, 0, st>>>(p);
     k_trace_primary<R, ST, 1, 1><<<b1f, kWaveThreads, 0, st>>>(p);
     compact_hits(p.hitAt, p.hitList, p.ctr + kCtrHits, static_cast<int>(p.maxItems), p.selTemp, p.selTempBytes, st);
@@ -1239,7 +1241,7 @@ static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long*
     k_trace_shadow<R, ST, 0><<<b2, kWaveThreads, 0, st>>>(p);
     k_trace_shadow<R, ST, 1><<<b2f, kWaveThreads, 0, st>>>(p);
     k_shade_rays<R, ST, true><<<b3, 128, 0, st>>>(p);
-    k_shade_mvc<R, ST><<<b3c, 128, 128 * kMvcSlab * sizeof(R), st>>>(p);
+    k_shade_mvc<R, ST><<<b3c, kMvcThreads, kMvcThreads * kMvcSlab * sizeof(R), st>>>(p);
     const long long np = static_cast<long long>(p.gw) * p.gh;
     k_contact_combine<R><<<static_cast<int>((np + 127) / 128), 128, 0, st>>>(p);
     if (launches) *launches += p.cray ? 10 : 9;

@@ -869,25 +869,39 @@ struct CellCorners {
 // broadcast constant load per corner instead of a local-memory table.
 __constant__ const int kMvcFaces[6][4] = {{0, 2, 3, 1}, {4, 5, 7, 6}, {0, 1, 5, 4}, {2, 6, 7, 3}, {0, 4, 6, 2}, {1, 3, 7, 5}};
 
+// The angle of one triangle edge (mean_value.hpp:53-55): theta = 2 asin(|u_a - u_b| / 2),
+// returned as sin and cos of the half angle a = theta / 2 and theta itself. The
+// value depends only on the unordered pair (u_a - u_b = -(u_b - u_a) exactly), so
+// the two triangles sharing an edge can share it.
+template <typename M>
+__device__ __forceinline__ void mvcEdgeAngles(V3<M> ua, V3<M> ub, M& sa, M& ca, M& th) {
+    const M l = length(ua - ub);
+    sa = sclamp(l * M(0.5), M(0), M(1));
+    ca = sqrt(smax(M(0), M(1) - sa * sa));
+    th = M(2) * mvcAsin<M>(sa);
+}
+// sign(det(u0, u1, u2)) (mean_value.hpp:73-74)
+template <typename M>
+__device__ __forceinline__ M mvcSign(V3<M> u0, V3<M> u1, V3<M> u2) {
+    V3<M> cr = mk(u1.y * u2.z - u1.z * u2.y, u1.z * u2.x - u1.x * u2.z, u1.x * u2.y - u1.y * u2.x);
+    return dot(u0, cr) >= M(0) ? M(1) : M(-1);
+}
+
 // One triangle of mvcWeightsHex's loop (mean_value.hpp:45-97) from its corners'
-// distances d and unit vectors u. Returns kTriSkip (degenerate, mean_value.hpp:
-// 80-89: no contribution), kTriAdd (w = the three weight contributions, :91-96),
-// kTriOn (x on the triangle: w = its normalised 2D barycentric weights, :57-71) or
-// kTriFail (on the triangle but degenerate: mvcWeightsHex returns false).
+// distances d, its edge angles (sa, ca, theta: the edge opposite corner i) and
+// the orientation sign. Returns kTriSkip (degenerate, mean_value.hpp:80-89: no
+// contribution), kTriAdd (w = the three weight contributions, :91-96), kTriOn (x
+// on the triangle: w = its normalised 2D barycentric weights, :57-71) or kTriFail
+// (on the triangle but degenerate: mvcWeightsHex returns false).
 constexpr int kTriSkip = 0, kTriAdd = 1, kTriOn = 2, kTriFail = 3;
 template <typename M>
-__device__ __forceinline__ int mvcTriangle(const M d[3], const V3<M> u[3], M w[3]) {
+__device__ __forceinline__ int mvcTriangleCore(const M d[3], const M sa[3], const M ca[3], const M theta[3], M sign,
+                                               M w[3]) {
     const M eps = M(1e-10);
     const M pi = M(kPi);
-    M sa[3], ca[3], theta[3], st[3];
+    M st[3];
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        const M l = length(u[(i + 1) % 3] - u[(i + 2) % 3]);
-        sa[i] = sclamp(l * M(0.5), M(0), M(1));
-        ca[i] = sqrt(smax(M(0), M(1) - sa[i] * sa[i]));
-        theta[i] = M(2) * mvcAsin<M>(sa[i]);
-        st[i] = M(2) * sa[i] * ca[i];
-    }
+    for (int i = 0; i < 3; ++i) st[i] = M(2) * sa[i] * ca[i];
     const M h = (theta[0] + theta[1] + theta[2]) * M(0.5);
     if (pi - h < M(1e-8)) {
         M total = 0;
@@ -901,9 +915,6 @@ __device__ __forceinline__ int mvcTriangle(const M d[3], const V3<M> u[3], M w[3
         for (int i = 0; i < 3; ++i) w[i] = w[i] / total;
         return kTriOn;
     }
-    V3<M> cr = mk(u[1].y * u[2].z - u[1].z * u[2].y, u[1].z * u[2].x - u[1].x * u[2].z,
-                  u[1].x * u[2].y - u[1].y * u[2].x);
-    const M sign = dot(u[0], cr) >= M(0) ? M(1) : M(-1);
     // sin h, h = a0 + a1 + a2
     const M sh = sa[0] * ca[1] * ca[2] + ca[0] * sa[1] * ca[2] + ca[0] * ca[1] * sa[2] - sa[0] * sa[1] * sa[2];
     M c[3], sv[3];
@@ -940,6 +951,13 @@ __device__ __forceinline__ int mvcTriangle(const M d[3], const V3<M> u[3], M w[3
         w[i] = sizeof(M) == 8 ? num * (D[j] * D[k] * invQ) : mvcDiv(num, D[i]);
     }
     return kTriAdd;
+}
+template <typename M>
+__device__ __forceinline__ int mvcTriangle(const M d[3], const V3<M> u[3], M w[3]) {
+    M sa[3], ca[3], theta[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) mvcEdgeAngles(u[(i + 1) % 3], u[(i + 2) % 3], sa[i], ca[i], theta[i]);
+    return mvcTriangleCore<M>(d, sa, ca, theta, mvcSign(u[0], u[1], u[2]), w);
 }
 
 // Result: the weights in a.wts(0..7) (precision M; the caller widens to double).

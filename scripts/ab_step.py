@@ -1,0 +1,42 @@
+"""A/B timing of the C2 step (3 passes, device events, L2 flushed) for library
+variants: python scripts/ab_step.py [prec] [reps] ; SDFGI_LIB selects the build."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import torch  # noqa: E402
+
+from paper_2007_14394_b200 import api, scene_io  # noqa: E402
+from paper_2007_14394_b200.runtime import Device  # noqa: E402
+
+prec = sys.argv[1] if len(sys.argv) > 1 else "f64"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+scene = scene_io.read_sdfs("paper_2007_14394_b200/data/c2.sdfs")
+flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+with Device(0, precision=prec) as dev:
+    stage = api.ProbeStage(dev, scene)
+    ext = torch.cuda.ExternalStream(dev.stream)
+    per_pass, steps = [], []
+    for r in range(reps + 2):
+        for lv in range(stage.levels):
+            dev.reset_probes(lv)
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ext)
+        pp = []
+        for p in range(3):
+            stage.relocate_all()
+            api.updateProbes(dev, stage.cfg, p)
+            pp.append(dev.last_kernel_ms()[0])
+            dev.swap()
+        e1.record(ext)
+        e1.synchronize()
+        if r >= 2:
+            steps.append(e0.elapsed_time(e1))
+            per_pass.append(pp)
+    pp = np.median(np.array(per_pass), axis=0)
+    lib = os.environ.get("SDFGI_LIB", "cur").split("/")[-2] if os.environ.get("SDFGI_LIB") else "cur"
+    print(f"{lib:12s} {prec} step {np.median(steps):7.2f} ms  passes " + " ".join(f"{x:6.2f}" for x in pp))

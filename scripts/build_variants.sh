@@ -16,7 +16,8 @@ while [ $# -gt 1 ]; do
   nvcc $COMMON $flags -c $P/csrc/sdfgi_abi.cu -o $OUT/$name/abi.o &
   nvcc $COMMON $flags -c $P/csrc/fp_peak.cu -o $OUT/$name/fp.o &
   nvcc $COMMON $flags -fmad=false -c $P/csrc/select.cu -o $OUT/$name/select.o &
+  g++ -std=c++17 -fPIC -fvisibility=hidden -pthread -O2 -ffp-contract=off -fno-fast-math -c $P/csrc/host_trig.cpp -o $OUT/$name/host_trig.o &
   wait
-  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/$name/libsdfgi_b200.so $OUT/$name/*.o -lnccl -lcudart
+  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/$name/libsdfgi_b200.so $OUT/$name/*.o -lnccl -lcudart -Xcompiler -pthread
   echo built $OUT/$name
 done
