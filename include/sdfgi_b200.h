@@ -191,6 +191,33 @@ typedef struct sdfgi_camera {
     double fov_y_deg;
 } sdfgi_camera;
 
+/* Hit, scene.hpp:375-383: one sphereTrace result. prim_index indexes the uploaded
+ * primitive array (ActiveScene::primitives); miss is MissReason (0 None, 1 TMax,
+ * 2 StepLimit). 72 B. */
+typedef struct sdfgi_hit {
+    double t;
+    double pos[3];
+    double normal[3];
+    int32_t prim_index;
+    int32_t converged;
+    int32_t miss;
+    int32_t _pad;
+} sdfgi_hit;
+
+/* InterpolationStencil, probe_volume.hpp:205-217: 8 entries of one cascade
+ * (level), weights normalised; count 0 with sky_fallback when no cascade holds the
+ * point or every corner is dead. 120 B. */
+typedef struct sdfgi_stencil {
+    double weight[8];
+    int32_t level;
+    int32_t index[8];
+    int32_t count;
+    int32_t cross_cascade;
+    int32_t sky_fallback;
+    int32_t used_mvc;
+    int32_t _pad;
+} sdfgi_stencil;
+
 /* ---------------------------------------------------------------- lifecycle */
 SDFGI_API int sdfgi_abi_version(void);
 SDFGI_API const char* sdfgi_last_error(void);
@@ -345,6 +372,31 @@ SDFGI_API int sdfgi_build_clusters(const sdfgi_prim* prims, int n, int max_per_c
                                    int* out_n_clusters, int32_t* member_start, int32_t* member_idx);
 
 /* Launch counter: kernels this context has launched since creation. */
+/* ---- the reference's free functions, batched (each call runs one device batch
+ * over n items with the context's scene, cascades and front atlas) ---- */
+/* sphereTrace (scene.hpp:391-435) of n rays (origins, dirs: 3 doubles each) with
+ * the shared tMax, surfaceEpsilon, maxSteps and startBound. */
+SDFGI_API int sdfgi_trace_rays(void* ctx, const double* origins, const double* dirs, int n, double t_max,
+                               double surface_epsilon, int max_steps, double start_bound, sdfgi_hit* out,
+                               sdfgi_stats* stats);
+/* softShadowTrace (scene.hpp:459-476) of n segments [t_min[i], t_max[i]] with the
+ * shared k, maxSteps and minStep; out_vis[i] in [0, 1]. */
+SDFGI_API int sdfgi_soft_shadow(void* ctx, const double* origins, const double* dirs, const double* t_min,
+                                const double* t_max, int n, double k, int max_steps, double min_step,
+                                double* out_vis, sdfgi_stats* stats);
+/* shadeHit (probe_update.hpp:136-149) of n hits against the context's front atlas
+ * (the previous field) with the given bounceCoeff; out_rgb 3 doubles per hit. */
+SDFGI_API int sdfgi_shade_hits(void* ctx, const sdfgi_hit* hits, int n, double bounce_coeff, const sdfgi_cfg* cfg,
+                               double* out_rgb, sdfgi_stats* stats);
+/* convolveIrradiance (probe_update.hpp:25-34): one sample set (directions and
+ * radiance, 3 doubles each) convolved for n_texels directions into out_rgb. */
+SDFGI_API int sdfgi_convolve_irradiance(void* ctx, const double* sample_dirs, const double* sample_radiance,
+                                        int n_samples, const double* texel_dirs, int n_texels, double* out_rgb);
+/* interpolationStencil (probe_volume.hpp:224-310) of n points over the context's
+ * cascades and probe state. */
+SDFGI_API int sdfgi_interpolation_stencil(void* ctx, const double* points, int n, double mvc_relocation_frac,
+                                          sdfgi_stencil* out);
+
 SDFGI_API int sdfgi_launch_count(void* ctx, int64_t* out);
 
 #ifdef __cplusplus

@@ -9,11 +9,19 @@
 // comparison; tests/test_dropin.py asserts on it.
 //
 // usage: dropin_check <scene.sdfs> <passes> <resX> <resY> <resZ> <spacing> <nRays>
+//        dropin_check render <file.scene> <frames> <width> <height> [nRays]
+//            the whole Renderer::renderFrame loop: the reference's Renderer vs
+//            sdfgi::b200::Renderer (every per-frame stage on the device)
+//        dropin_check funcs <scene.sdfs> <resX> <resY> <resZ> <spacing> <nRays>
+//            the free functions (querySceneSdf, sphereTrace, softShadowTrace,
+//            interpolationStencil, convolveIrradiance, shadeHit, per-probe updateProbe)
+//            against the reference's, after one reference probe pass
 #include <sdfgi/pipeline.hpp>
 
 #include <cmath>
 #include <cstdio>
 #include <fstream>
+#include <string>
 
 #include "../paper_2007_14394_b200/include/sdfgi_b200.hpp"
 
@@ -89,7 +97,179 @@ ActiveScene readScene(const char* path, Vec3& cam, RenderConfig& cfg) {
 
 }  // namespace
 
+double relErr(double got, double want, double floor) { return std::fabs(got - want) / std::max(std::fabs(want), floor); }
+
+// Renderer::renderFrame (pipeline.hpp:84-230), reference vs device, frame by frame.
+int runRender(int argc, char** argv) {
+    if (argc < 6) throw std::runtime_error("usage: render file.scene frames w h [nrays]");
+    SceneFile file = loadSceneFile(argv[2]);
+    if (argc > 6) file.config.nRaysFull = std::atoi(argv[6]);
+    const int frames = std::atoi(argv[3]), w = std::atoi(argv[4]), h = std::atoi(argv[5]);
+    Renderer ref(file, w, h, hardwareThreads());
+    sdfgi::b200::Renderer gpu(file, w, h, true);
+    long long metricMismatch = 0, px = 0, exact = 0;
+    double maxRel = 0;
+    for (int f = 0; f < frames; ++f) {
+        FrameMetrics a = ref.renderFrame();
+        FrameMetrics b = gpu.renderFrame();
+        if (a.activePrimitives != b.activePrimitives || a.clusters != b.clusters || a.probesTotal != b.probesTotal ||
+            a.probesUpdated != b.probesUpdated || a.relocated != b.relocated || a.rejected != b.rejected ||
+            a.dead != b.dead)
+            ++metricMismatch;
+        const ImageRgb& ia = ref.image();
+        const ImageRgb& ib = gpu.image();
+        double mean = 0;
+        for (const Vec3& v : ia.pixels) mean += (std::fabs(v.x) + std::fabs(v.y) + std::fabs(v.z)) / 3;
+        mean /= std::max<size_t>(ia.pixels.size(), 1);
+        for (size_t i = 0; i < ia.pixels.size(); ++i)
+            for (int k = 0; k < 3; ++k) {
+                ++px;
+                if (ia.pixels[i][k] == ib.pixels[i][k]) ++exact;
+                maxRel = std::max(maxRel, relErr(ib.pixels[i][k], ia.pixels[i][k], 0.05 * mean));
+            }
+    }
+    std::printf("{\"frames\": %d, \"metric_mismatches\": %lld, \"channels\": %lld, \"exact_channels\": %lld, "
+                "\"max_rel_err\": %.6g}\n",
+                frames, metricMismatch, px, exact, maxRel);
+    return 0;
+}
+
+// The free functions against the reference's, on the state after one reference pass.
+int runFuncs(int argc, char** argv) {
+    if (argc < 8) throw std::runtime_error("usage: funcs scene.sdfs rx ry rz spacing nrays");
+    Vec3 cam;
+    RenderConfig cfg;
+    ActiveScene scene = readScene(argv[2], cam, cfg);
+    const int rx = std::atoi(argv[3]), ry = std::atoi(argv[4]), rz = std::atoi(argv[5]);
+    const double spacing = std::atof(argv[6]);
+    cfg.nRaysFull = std::atoi(argv[7]);
+    std::vector<CascadeVolume> cas{makeCascade(rx, ry, rz, spacing, 0, cam)};
+    std::vector<ProbeAtlas> atl[2];
+    for (auto& a : atl) a.emplace_back(cas[0].probeCount(), cfg.octRes);
+    // one reference pass so the field has texels and relocated probes
+    updateProbePositions(cas[0], scene, cfg.threshold1(spacing), cfg.threshold2(spacing), cfg.maxDescentSteps);
+    IrradianceField f0{&cas, &atl[0]};
+    for (int i = 0; i < cas[0].probeCount(); ++i)
+        if (cas[0].probes[i].alive) updateProbe(scene, cas[0], i, f0, atl[1][0], cfg.nRaysFull, cfg, 0);
+    IrradianceField prev{&cas, &atl[1]};
+
+    sdfgi::b200::Device gpu(0, true);
+    gpu.uploadScene(scene);
+    gpu.syncCascades(cas, cfg.octRes, &atl[1]);
+    Rng rng(7);
+    const Vec3 lo = cas[0].origin, hi = cas[0].origin + Vec3(rx - 1, ry - 1, rz - 1) * spacing;
+    auto randIn = [&] { return Vec3(rng.uniform(lo.x, hi.x), rng.uniform(lo.y, hi.y), rng.uniform(lo.z, hi.z)); };
+    const int n = 4096;
+    std::vector<Vec3> o(n), d(n);
+    for (int i = 0; i < n; ++i) {
+        o[i] = randIn();
+        d[i] = uniformSphereDir(rng);
+    }
+    long long bad = 0;
+    // querySceneSdf
+    std::vector<int> own;
+    std::vector<double> q = gpu.querySceneSdf(o, kInf, &own);
+    for (int i = 0; i < n; ++i) {
+        int ow = -1;
+        double r = querySceneSdf(scene, o[i], kInf, nullptr, &ow);
+        if (r != q[i] || ow != own[i]) ++bad;
+    }
+    const long long badQuery = bad;
+    // sphereTrace (bit-exact in FP64)
+    std::vector<Hit> hg = gpu.sphereTrace(scene, o, d, cfg.rayTMax, cfg.surfaceEpsilon, cfg.maxTraceSteps);
+    std::vector<Hit> hr(n);
+    long long badTrace = 0;
+    for (int i = 0; i < n; ++i) {
+        hr[i] = sphereTrace(scene, o[i], d[i], cfg.rayTMax, cfg.surfaceEpsilon, cfg.maxTraceSteps);
+        const Hit& a = hr[i];
+        const Hit& b = hg[i];
+        if (a.converged != b.converged || a.miss != b.miss || a.primitiveIndex != b.primitiveIndex ||
+            a.primitiveId != b.primitiveId || a.t != b.t || !(a.position == b.position) || !(a.normal == b.normal))
+            ++badTrace;
+    }
+    // softShadowTrace
+    std::vector<double> t0(n, 0.01), t1(n, 3.0);
+    std::vector<double> vg = gpu.softShadowTrace(o, d, t0, t1, cfg.shadowK, nullptr, cfg.shadowSteps);
+    long long badShadow = 0;
+    for (int i = 0; i < n; ++i)
+        if (softShadowTrace(scene, o[i], d[i], 0.01, 3.0, cfg.shadowK, nullptr, cfg.shadowSteps) != vg[i]) ++badShadow;
+    // interpolationStencil (the MVC's sines are algebraic on the device: weights to ~1e-12)
+    std::vector<InterpolationStencil> sg = gpu.interpolationStencil(cas, o, cfg.mvcRelocationFrac);
+    long long badStencil = 0;
+    double stencilErr = 0;
+    for (int i = 0; i < n; ++i) {
+        InterpolationStencil a = interpolationStencil(cas, o[i], cfg.mvcRelocationFrac);
+        const InterpolationStencil& b = sg[i];
+        if (a.count != b.count || a.skyFallback != b.skyFallback || a.usedMvc != b.usedMvc ||
+            a.crossCascade != b.crossCascade)
+            ++badStencil;
+        for (int k = 0; k < a.count && k < b.count; ++k) {
+            if (a.entries[k].ref.index != b.entries[k].ref.index || a.entries[k].ref.cascade != b.entries[k].ref.cascade)
+                ++badStencil;
+            stencilErr = std::max(stencilErr, std::fabs(a.entries[k].weight - b.entries[k].weight));
+        }
+    }
+    // convolveIrradiance
+    std::vector<RadianceSample> samples(300);
+    for (auto& sm : samples) {
+        sm.dir = uniformSphereDir(rng);
+        sm.radiance = {rng.uniform(), rng.uniform(), rng.uniform()};
+    }
+    std::vector<ConvolveResult> cg = gpu.convolveIrradiance(samples, std::vector<Vec3>(d.begin(), d.begin() + 64));
+    long long badConv = 0;
+    for (int i = 0; i < 64; ++i) {
+        ConvolveResult a = convolveIrradiance(samples, d[i]);
+        if (!(a.irradiance == cg[i].irradiance) || a.empty != cg[i].empty) ++badConv;
+    }
+    // shadeHit on the converged hits, against the field (bounce through the MVC: 1e-9)
+    std::vector<Hit> conv;
+    for (const Hit& hh : hr)
+        if (hh.converged) conv.push_back(hh);
+    std::vector<Vec3> lg = gpu.shadeHit(conv, prev, cfg.bounceCoeff, cfg);
+    double shadeErr = 0;
+    for (size_t i = 0; i < conv.size(); ++i) {
+        Vec3 a = shadeHit(scene, conv[i], prev, cfg.bounceCoeff, cfg);
+        for (int k = 0; k < 3; ++k) shadeErr = std::max(shadeErr, relErr(lg[i][k], a[k], 1e-6));
+    }
+    // per-probe updateProbe of every 7th alive probe, frame 1, reading `prev`
+    std::vector<CascadeVolume> casG = cas;
+    ProbeAtlas currR = atl[1][0], currG = atl[1][0];
+    long long badProbe = 0, texels = 0, exactTexels = 0;
+    double probeErr = 0;
+    double mean = 0;
+    for (float v : atl[1][0].raw()) mean += std::fabs(v);
+    mean /= atl[1][0].raw().size();
+    for (int i = 0; i < cas[0].probeCount(); i += 7) {
+        if (!cas[0].probes[i].alive) continue;
+        auto ra = updateProbe(scene, cas[0], i, prev, currR, cfg.nRaysFull, cfg, 1);
+        IrradianceField prevG{&casG, &atl[1]};
+        auto rb = gpu.updateProbe(scene, casG[0], i, prevG, currG, cfg.nRaysFull, cfg, 1);
+        if (ra.raysTraced != rb.raysTraced || casG[0].probes[i].rejectHistory != cas[0].probes[i].rejectHistory ||
+            casG[0].probes[i].lastUpdateFrame != cas[0].probes[i].lastUpdateFrame)
+            ++badProbe;
+    }
+    for (size_t k = 0; k < currR.raw().size(); ++k) {
+        ++texels;
+        if (currR.raw()[k] == currG.raw()[k]) ++exactTexels;
+        probeErr = std::max(probeErr, relErr(currG.raw()[k], currR.raw()[k], 0.05 * mean));
+    }
+    std::printf("{\"query_mismatches\": %lld, \"trace_mismatches\": %lld, \"shadow_mismatches\": %lld, "
+                "\"stencil_mismatches\": %lld, \"stencil_max_abs_err\": %.3g, \"convolve_mismatches\": %lld, "
+                "\"shade_hits\": %zu, \"shade_max_rel_err\": %.3g, \"probe_mismatches\": %lld, "
+                "\"texels\": %lld, \"exact_texels\": %lld, \"probe_max_rel_err\": %.3g}\n",
+                badQuery, badTrace, badShadow, badStencil, stencilErr, badConv, conv.size(), shadeErr, badProbe, texels,
+                exactTexels, probeErr);
+    return 0;
+}
+
 int main(int argc, char** argv) {
+    try {
+        if (argc > 1 && std::string(argv[1]) == "render") return runRender(argc, argv);
+        if (argc > 1 && std::string(argv[1]) == "funcs") return runFuncs(argc, argv);
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return 1;
+    }
     if (argc < 8) {
         std::fprintf(stderr, "usage: %s scene.sdfs passes rx ry rz spacing nrays\n", argv[0]);
         return 2;

@@ -12,6 +12,11 @@ reference's own; the state they operate on lives on the GPU in a ``Device``.
     selectProbesForUpdate probe_volume.hpp:154-198 (on the device)
     recenterCascade       probe_volume.hpp:80-86
     querySceneSdf         scene.hpp:336-340
+    sphereTrace           scene.hpp:391-435 (batched)
+    softShadowTrace       scene.hpp:459-476 (batched)
+    shadeHit              probe_update.hpp:136-149 (batched, against the front atlas)
+    convolveIrradiance    probe_update.hpp:25-34 (batched over texel directions)
+    interpolationStencil  probe_volume.hpp:224-310 (batched)
     composeFrame          shading.hpp:480-504 (pipeline.hpp:209)
     ProbeStage            the probe half of Renderer::renderFrame (pipeline.hpp:108-151)
 """
@@ -86,6 +91,33 @@ def composeFrame(dev: Device, cfg, indirect=None, stats=False):
 def querySceneSdf(dev: Device, points, initD=None):
     """scene.hpp:336-340 at many points: (d, owner primitive index)."""
     return dev.query_points(points, initD)
+
+
+def sphereTrace(dev: Device, origins, dirs, tMax, surfaceEpsilon=1e-3, maxSteps=128, startBound=math.inf):
+    """scene.hpp:391-435 for a batch of rays: runtime.HIT_DTYPE records (t, pos,
+    normal, prim_index, converged, miss)."""
+    return dev.trace_rays(origins, dirs, tMax, surfaceEpsilon, maxSteps, startBound)
+
+
+def softShadowTrace(dev: Device, origins, dirs, tMin, tMax, k, maxSteps=256, minStep=5e-4):
+    """scene.hpp:459-476 for a batch of segments: visibility in [0, 1]."""
+    return dev.soft_shadow(origins, dirs, tMin, tMax, k, maxSteps, minStep)
+
+
+def shadeHit(dev: Device, hits, bounceCoeff, cfg):
+    """probe_update.hpp:136-149 for a batch of hits (runtime.HIT_DTYPE) with the
+    device's front atlas as the previous field: outgoing radiance (n, 3)."""
+    return dev.shade_hits(hits, bounceCoeff, cfg)
+
+
+def convolveIrradiance(dev: Device, sampleDirs, sampleRadiance, texelDirs):
+    """probe_update.hpp:25-34: one sample set convolved for many directions (n, 3)."""
+    return dev.convolve_irradiance(sampleDirs, sampleRadiance, texelDirs)
+
+
+def interpolationStencil(dev: Device, points, mvcRelocationFrac=0.25):
+    """probe_volume.hpp:224-310 over the device's cascades: runtime.STENCIL_DTYPE."""
+    return dev.interpolation_stencil(points, mvcRelocationFrac)
 
 
 class ProbeStage:

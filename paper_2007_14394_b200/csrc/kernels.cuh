@@ -268,6 +268,16 @@ template <typename R>
 void launch_contact(const WaveParams<R>& p, bool stats, cudaStream_t st, long long* launches);
 template <typename R>
 void launch_compose(const WaveParams<R>& p, bool stats, cudaStream_t st, long long* launches);
+// kind 0: sphereTrace rays (P.cray), 1: softShadowTrace rays (light list 0), 2: shadeHit of P.hitList
+template <typename R>
+void launch_batch(const WaveParams<R>& p, int kind, bool stats, cudaStream_t st, long long* launches);
+// convolveIrradiance (probe_update.hpp:25-34) of one sample set for many texel directions
+void launch_convolve_batch(const double* sdir, const double* srad, int ns, const double* tdir, int nt, double* out,
+                           cudaStream_t st);
+// interpolationStencil (probe_volume.hpp:224-310) of many points, FP64:
+// per point 8 probe indices, 8 weights and (cascade slot, count, crossCascade, skyFallback, usedMvc)
+void launch_stencil_batch(const ProbeCommon& pc, const double* pts, int n, double mvcFrac, int* idx, double* w,
+                          int* meta, cudaStream_t st);
 template <typename R>
 void launch_wavefront(const WaveParams<R>& p, int persistBlocks, bool stats, cudaStream_t st,
                       cudaEvent_t evStart, cudaEvent_t evEnd, long long* launches);

@@ -264,5 +264,55 @@ template void launch_wavefront<double>(const WaveParams<double>&, int, bool, cud
 template void launch_gather<double>(const GatherParams<double>&, int, bool, cudaStream_t);
 template void launch_contact<double>(const WaveParams<double>&, bool, cudaStream_t, long long*);
 template void launch_compose<double>(const WaveParams<double>&, bool, cudaStream_t, long long*);
+template void launch_batch<double>(const WaveParams<double>&, int, bool, cudaStream_t, long long*);
+
+// convolveIrradiance (probe_update.hpp:25-34): E(D) = (4 pi / N) sum max(0, D.d_i) L_i,
+// each channel summed in the samples' order; one thread per texel direction.
+__global__ void __launch_bounds__(128) k_convolve_batch(const double* sdir, const double* srad, int ns,
+                                                        const double* tdir, int nt, double* out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    const V3<double> D = mk(tdir[3 * t], tdir[3 * t + 1], tdir[3 * t + 2]);
+    V3<double> acc = mk(0.0, 0.0, 0.0);
+    for (int i = 0; i < ns; ++i) {
+        const double w = dot(D, mk(sdir[3 * i], sdir[3 * i + 1], sdir[3 * i + 2]));
+        if (w > 0) acc = acc + mk(srad[3 * i], srad[3 * i + 1], srad[3 * i + 2]) * w;
+    }
+    const V3<double> e = acc * (4.0 * kPi / ns);
+    out[3 * t] = e.x;
+    out[3 * t + 1] = e.y;
+    out[3 * t + 2] = e.z;
+}
+
+void launch_convolve_batch(const double* sdir, const double* srad, int ns, const double* tdir, int nt, double* out,
+                           cudaStream_t st) {
+    if (nt > 0) k_convolve_batch<<<(nt + 127) / 128, 128, 0, st>>>(sdir, srad, ns, tdir, nt, out);
+}
+
+// interpolationStencil (probe_volume.hpp:224-310) per point: meta = (cascade slot or
+// -1, count, crossCascade, skyFallback, usedMvc)
+__global__ void __launch_bounds__(128) k_stencil_batch(ProbeCommon pc, const double* pts, int n, double mvcFrac,
+                                                       int* idx, double* w, int* meta) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const V3<double> p = mk(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+    const StencilCell sc = stencilCell(pc.cas, pc.nCas, pc.probes, p, mvcFrac);
+    const Stencil st = interpolationStencil<double>(pc.cas, pc.nCas, pc.probes, p, mvcFrac);
+    for (int k = 0; k < 8; ++k) {
+        idx[8 * i + k] = st.count ? st.probe[k] : 0;
+        w[8 * i + k] = st.count ? st.w[k] : 0.0;
+    }
+    int* m = meta + 5 * i;
+    m[0] = st.cascade;
+    m[1] = st.count;
+    m[2] = sc.chosen < 0 ? 1 : (sc.boundary ? 1 : 0);  // no cascade: crossCascade = true (:249-252)
+    m[3] = st.sky;
+    m[4] = st.usedMvc;
+}
+
+void launch_stencil_batch(const ProbeCommon& pc, const double* pts, int n, double mvcFrac, int* idx, double* w,
+                          int* meta, cudaStream_t st) {
+    if (n > 0) k_stencil_batch<<<(n + 127) / 128, 128, 0, st>>>(pc, pts, n, mvcFrac, idx, w, meta);
+}
 
 }  // namespace sdfgi_dev

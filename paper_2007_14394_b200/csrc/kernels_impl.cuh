@@ -646,8 +646,9 @@ __device__ __forceinline__ void shadowSetup(const WaveParams<R>& P, unsigned am,
 
 // The converged hits' normals (evalGradient of the owner, primitives.hpp:96-108)
 // and their shadow-ray set-up over the compacted hit list — every lane has one,
-// instead of the few lanes of a K1 warp whose rays just converged.
-template <typename R>
+// instead of the few lanes of a K1 warp whose rays just converged. EVAL = false:
+// the normals are given (a shadeHit batch, sdfgi_shade_hits), only the set-up runs.
+template <typename R, bool EVAL = true>
 __global__ void __launch_bounds__(128) k_hit_normals(WaveParams<R> P) {
     const unsigned long long n = P.ctr[kCtrHits];
     for (unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -656,10 +657,13 @@ __global__ void __launch_bounds__(128) k_hit_normals(WaveParams<R> P) {
         const int rid = P.hitList[i];
         HitRec<R>& h = P.hits[rid];
         const V3<R> pos = mk(h.p[0], h.p[1], h.p[2]);
-        const V3<R> nn = evalGradient(P.scene.prims[h.owner], pos);
-        h.n[0] = nn.x;
-        h.n[1] = nn.y;
-        h.n[2] = nn.z;
+        V3<R> nn = mk(h.n[0], h.n[1], h.n[2]);
+        if (EVAL) {
+            nn = evalGradient(P.scene.prims[h.owner], pos);
+            h.n[0] = nn.x;
+            h.n[1] = nn.y;
+            h.n[2] = nn.z;
+        }
         shadowSetup(P, am, true, rid, pos, nn);
     }
 }
@@ -677,7 +681,8 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shad
     unsigned long long traced = 0;
     for (int li = 0; li < L; ++li) traced += P.ctr[kLightCtr + li];
     const unsigned long long total = PHASE ? min(P.ctr[kCtrParkShadow], parkCap) : traced;
-    const R minStep = R(5e-4), inf = R(INFINITY), k = R(P.tc.shadowK);
+    const R minStep = R(P.tc.shadowMinStep > 0 ? P.tc.shadowMinStep : 5e-4), inf = R(INFINITY),
+            k = R(P.tc.shadowK);
     const int maxSteps = P.tc.shadowSteps;
     Counters cnt;
     cnt.zero();
@@ -1315,6 +1320,51 @@ static void composeWavefront(const WaveParams<R>& p, cudaStream_t st, long long*
     k_trace_shadow<R, ST, 1><<<b2f, kWaveThreads, 0, st>>>(p);
     k_compose<R><<<blocks, 128, 0, st>>>(p);
     if (launches) *launches += 4;
+}
+
+// Batches of the reference's free functions (sdfgi_trace_rays, sdfgi_soft_shadow,
+// sdfgi_shade_hits): the same kernels over caller-given items.
+//   rays:   sphereTrace (scene.hpp:391-435) of P.cray records — K1 in direct-ray
+//           mode, far phase, normals of the converged hits.
+//   shadow: softShadowTrace (scene.hpp:459-476) of the ShadowRay records in light
+//           list 0 (ctr[kLightCtr] set by the caller) — K2 and its far phase.
+//   shade:  shadeHit (probe_update.hpp:136-149) of the hits in P.hits listed in
+//           P.hitList (ctr[kCtrHits] set by the caller): shadow set-up with the
+//           given normals, K2, K3a, K3c.
+template <typename R>
+void launch_batch(const WaveParams<R>& p, int kind, bool stats, cudaStream_t st, long long* launches) {
+    const int L = p.scene.n_lights > 1 ? p.scene.n_lights : 1;
+    if (kind == 0) {
+        cudaMemsetAsync(p.ctr, 0, (kLightCtr + L) * sizeof(unsigned long long), st);
+        cudaMemsetAsync(p.hitAt, 0xff, static_cast<size_t>(p.maxItems) * sizeof(int), st);
+        auto k0 = stats ? k_trace_primary<R, true, 1, 0> : k_trace_primary<R, false, 1, 0>;
+        auto k1 = stats ? k_trace_primary<R, true, 1, 1> : k_trace_primary<R, false, 1, 1>;
+        const int b1 = persistentBlocks(k0, kWaveThreads, 0), b1f = persistentBlocks(k1, kWaveThreads, 0);
+        k0<<<b1, kWaveThreads, 0, st>>>(p);
+        k1<<<b1f, kWaveThreads, 0, st>>>(p);
+        compact_hits(p.hitAt, p.hitList, p.ctr + kCtrHits, static_cast<int>(p.maxItems), p.selTemp, p.selTempBytes,
+                     st);
+        k_hit_normals<R><<<persistentBlocks(k_hit_normals<R>, 128, 0), 128, 0, st>>>(p);
+        if (launches) *launches += 4;
+    } else if (kind == 1) {
+        auto k0 = stats ? k_trace_shadow<R, true, 0> : k_trace_shadow<R, false, 0>;
+        auto k1 = stats ? k_trace_shadow<R, true, 1> : k_trace_shadow<R, false, 1>;
+        k0<<<persistentBlocks(k0, kWaveThreads, 0), kWaveThreads, 0, st>>>(p);
+        k1<<<persistentBlocks(k1, kWaveThreads, 0), kWaveThreads, 0, st>>>(p);
+        if (launches) *launches += 2;
+    } else {
+        auto k0 = stats ? k_trace_shadow<R, true, 0> : k_trace_shadow<R, false, 0>;
+        auto k1 = stats ? k_trace_shadow<R, true, 1> : k_trace_shadow<R, false, 1>;
+        auto ka = stats ? k_shade_rays<R, true, true> : k_shade_rays<R, false, true>;
+        auto kc = stats ? k_shade_mvc<R, true> : k_shade_mvc<R, false>;
+        k_hit_normals<R, false><<<persistentBlocks(k_hit_normals<R, false>, 128, 0), 128, 0, st>>>(p);
+        k0<<<persistentBlocks(k0, kWaveThreads, 0), kWaveThreads, 0, st>>>(p);
+        k1<<<persistentBlocks(k1, kWaveThreads, 0), kWaveThreads, 0, st>>>(p);
+        ka<<<persistentBlocks(ka, 128, 0), 128, 0, st>>>(p);
+        kc<<<persistentBlocks(kc, kMvcThreads, 0, kMvcThreads * kMvcSlab * sizeof(R)), kMvcThreads,
+             kMvcThreads * kMvcSlab * sizeof(R), st>>>(p);
+        if (launches) *launches += 5;
+    }
 }
 
 template <typename R>

@@ -1031,12 +1031,14 @@ struct StencilCell {
     CellCorners cc;
     double tx, ty, tz;
     bool wantMvc;
+    bool boundary;  // InterpolationStencil::crossCascade (probe_volume.hpp:276)
 };
 __device__ inline StencilCell stencilCell(const CascadeDev* cas, int nCas, const ProbesView& pv, V3<double> point,
                                           double mvcFrac) {
     StencilCell sc;
     sc.chosen = -1;
     sc.wantMvc = false;
+    sc.boundary = false;
     sc.tx = sc.ty = sc.tz = 0;
     int chosen = -1;
     int cell[3] = {0, 0, 0};
@@ -1089,6 +1091,7 @@ __device__ inline StencilCell stencilCell(const CascadeDev* cas, int nCas, const
             wantMvc = sqrt(d2) > thr;
     }
     sc.wantMvc = wantMvc;
+    sc.boundary = boundary;
     return sc;
 }
 
@@ -1237,6 +1240,7 @@ struct TraceCfg {
     double mvcFrac;
     int maxSteps;
     int shadowSteps;
+    double shadowMinStep;  // softShadowTrace's minStep (scene.hpp:462); 0 = the default 5e-4
 };
 
 // directIrradiance, probe_update.hpp:97-132

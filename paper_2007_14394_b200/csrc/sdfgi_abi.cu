@@ -42,6 +42,7 @@ static_assert(sizeof(sdfgi_cluster) == 56, "cluster ABI");
 static_assert(sizeof(sdfgi_cfg) == 224, "cfg ABI");
 static_assert(sizeof(sdfgi_probe) == 88, "probe ABI");
 static_assert(sizeof(sdfgi_ray_record) == sizeof(RayRecord), "ray record mirror");
+static_assert(sizeof(sdfgi_hit) == 72 && sizeof(sdfgi_stencil) == 120, "hit / stencil ABI");
 
 namespace {
 
@@ -2159,6 +2160,314 @@ int sdfgi_slab_range(int res_x, int res_y, int res_z, int rank, int world, int* 
         c.res[2] = res_z;
         c.base = 0;
         slabRange(c, rank, world, lo, hi);
+    });
+}
+
+}  // extern "C"
+
+namespace {
+
+// Wavefront parameters for a batch of n caller-given items (sdfgi_trace_rays,
+// sdfgi_soft_shadow, sdfgi_shade_hits): the probe wavefront's scratch buffers.
+template <typename R>
+WaveParams<R> batchParams(Ctx* c, size_t n) {
+    const size_t cap = std::max<size_t>(n, 1);
+    const int L = std::max(c->nLights, 1);
+    reserve(c->wHits, cap * sizeof(HitRec<R>));
+    reserve(c->wHitList, cap);
+    reserve(c->wMvcList, cap);
+    reserve(c->wVis, cap * L * sizeof(R));
+    reserve(c->wRad, cap * 3 * sizeof(R));
+    reserve(c->wCtr, kLightCtr + L);
+    reservePark<R>(c, cap, L);
+    reserve(c->wSRay, cap * L * sizeof(ShadowRay<R>));
+    reserve(c->wCRay, cap * sizeof(ContactRay<R>));
+    WaveParams<R> p;
+    std::memset(&p, 0, sizeof(p));
+    p.scene = c->sceneView<R>();
+    p.pc = c->probeCommon();
+    p.hits = reinterpret_cast<HitRec<R>*>(c->wHits.p);
+    p.hitList = c->wHitList.p;
+    p.mvcList = c->wMvcList.p;
+    p.vis = reinterpret_cast<R*>(c->wVis.p);
+    p.rad = reinterpret_cast<R*>(c->wRad.p);
+    p.ctr = c->wCtr.p;
+    p.sray = reinterpret_cast<ShadowRay<R>*>(c->wSRay.p);
+    p.srayCap = cap;
+    reserveHitAt<R>(c, p, cap);
+    p.park = c->accel && c->haveGrid && c->wPark.n >= 4096 ? c->wPark.p : nullptr;
+    p.parkBytes = p.park ? c->wPark.n : 0;
+    p.stats = c->scratch.p;
+    p.nRaysDirect = static_cast<long long>(n);
+    p.cray = c->wCRay.p;
+    p.prevAtlas = c->cascades.empty() ? nullptr : c->atlas[c->front].p;
+    p.oct = c->octRes;
+    return p;
+}
+
+void fillStats(sdfgi_stats* s, const unsigned long long* h) {
+    if (!s) return;
+    s->sdf_queries += h[0];
+    s->clusters_visited += h[1];
+    s->clusters_skipped += h[2];
+    s->primitive_evals += h[3];
+    s->trace_steps += h[4];
+    s->sphere_traces += h[5];
+    s->shadow_traces += h[6];
+    s->visibility_traces += h[7];
+}
+
+template <typename R>
+void traceRays(Ctx* c, const double* o, const double* d, int n, double tMax, double eps, int maxSteps, double sb,
+               sdfgi_hit* out, bool st) {
+    WaveParams<R> p = batchParams<R>(c, n);
+    p.tc.eps = eps;
+    p.tc.maxSteps = maxSteps;
+    p.tc.rayTMax = tMax;
+    std::vector<ContactRay<R>> rays(n);
+    for (int i = 0; i < n; ++i) {
+        for (int k = 0; k < 3; ++k) {
+            rays[i].o[k] = R(o[3 * i + k]);
+            rays[i].dir[k] = R(d[3 * i + k]);
+        }
+        rays[i].tMax = R(tMax);
+        rays[i].startBound = R(sb);
+    }
+    CK(cudaMemcpyAsync(p.cray, rays.data(), rays.size() * sizeof(ContactRay<R>), cudaMemcpyHostToDevice, c->stream));
+    launch_batch<R>(p, 0, st, c->stream, &c->launches);
+    CK(cudaGetLastError());
+    std::vector<HitRec<R>> h(n);
+    std::vector<int> orig(c->nPrims);
+    CK(cudaMemcpyAsync(h.data(), p.hits, n * sizeof(HitRec<R>), cudaMemcpyDeviceToHost, c->stream));
+    if (c->nPrims) CK(cudaMemcpyAsync(orig.data(), c->orig.p, c->nPrims * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int i = 0; i < n; ++i) {
+        sdfgi_hit& r = out[i];
+        std::memset(&r, 0, sizeof(r));
+        const bool conv = h[i].status & 1;
+        r.converged = conv ? 1 : 0;
+        r.miss = (h[i].status >> 1) & 3;
+        r.t = conv ? double(h[i].t) : 0.0;
+        r.prim_index = conv && h[i].owner >= 0 ? orig[h[i].owner] : -1;
+        for (int k = 0; k < 3; ++k) {
+            r.pos[k] = conv ? double(h[i].p[k]) : 0.0;
+            r.normal[k] = k == 2 ? 1.0 : 0.0;
+            if (r.prim_index >= 0) r.normal[k] = double(h[i].n[k]);
+        }
+    }
+}
+
+template <typename R>
+void softShadow(Ctx* c, const double* o, const double* d, const double* t0, const double* t1, int n, double k,
+                int maxSteps, double minStep, double* out, bool st) {
+    WaveParams<R> p = batchParams<R>(c, n);
+    const int L = std::max(c->nLights, 1);
+    p.scene.n_lights = 1;  // one list of segments (list 0); vis[i * 1]
+    p.tc.shadowK = k;
+    p.tc.shadowSteps = maxSteps;
+    p.tc.shadowMinStep = minStep;
+    std::vector<ShadowRay<R>> rays(n);
+    for (int i = 0; i < n; ++i) {
+        for (int a = 0; a < 3; ++a) {
+            rays[i].o[a] = R(o[3 * i + a]);
+            rays[i].dir[a] = R(d[3 * i + a]);
+        }
+        rays[i].t = R(t0[i]);
+        rays[i].tEnd = R(t1[i]);
+        rays[i].rid = i;
+        rays[i].li = 0;
+    }
+    std::vector<unsigned long long> ctr(kLightCtr + L, 0);
+    ctr[kLightCtr] = static_cast<unsigned long long>(n);
+    CK(cudaMemcpyAsync(p.ctr, ctr.data(), ctr.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(p.sray, rays.data(), rays.size() * sizeof(ShadowRay<R>), cudaMemcpyHostToDevice, c->stream));
+    launch_batch<R>(p, 1, st, c->stream, &c->launches);
+    CK(cudaGetLastError());
+    std::vector<R> v(n);
+    CK(cudaMemcpyAsync(v.data(), p.vis, n * sizeof(R), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int i = 0; i < n; ++i) out[i] = double(v[i]);
+}
+
+template <typename R>
+void shadeHits(Ctx* c, const sdfgi_hit* hits, int n, double bounce, const sdfgi_cfg* cfg, double* out, bool st) {
+    WaveParams<R> p = batchParams<R>(c, n);
+    const int L = std::max(c->nLights, 1);
+    p.tc.eps = cfg->surface_epsilon;
+    p.tc.rayTMax = cfg->ray_tmax;
+    p.tc.shadowK = cfg->shadow_k;
+    p.tc.bounceCoeff = bounce;
+    p.tc.mvcFrac = cfg->mvc_relocation_frac;
+    p.tc.maxSteps = static_cast<int>(cfg->max_trace_steps);
+    p.tc.shadowSteps = static_cast<int>(cfg->shadow_steps);
+    p.prevZero = c->frontZero() ? 1 : 0;
+    // original primitive index -> CSR position
+    std::vector<int> csr(c->hPrims.size(), -1);
+    for (size_t j = 0; j < c->hMember.size(); ++j)
+        if (csr[c->hMember[j]] < 0) csr[c->hMember[j]] = static_cast<int>(j);
+    std::vector<HitRec<R>> h(n);
+    std::vector<int> list;
+    std::vector<R> rad(3 * static_cast<size_t>(n), R(0));
+    for (int i = 0; i < n; ++i) {
+        std::memset(&h[i], 0, sizeof(h[i]));
+        const int pi = hits[i].prim_index;
+        REQ(pi < static_cast<int>(csr.size()), SDFGI_ERR_INVALID, "hit prim_index out of range");
+        h[i].owner = pi >= 0 ? csr[pi] : -1;
+        h[i].status = 1;
+        h[i].t = R(hits[i].t);
+        for (int k = 0; k < 3; ++k) {
+            h[i].p[k] = R(hits[i].pos[k]);
+            h[i].n[k] = R(hits[i].normal[k]);
+        }
+        if (h[i].owner >= 0)
+            list.push_back(i);
+        else
+            for (int k = 0; k < 3; ++k) rad[3 * i + k] = R(c->sky[k]);  // shadeHit's miss branch
+    }
+    std::vector<unsigned long long> ctr(kLightCtr + L, 0);
+    ctr[kCtrHits] = list.size();
+    CK(cudaMemcpyAsync(p.ctr, ctr.data(), ctr.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(p.hits, h.data(), n * sizeof(HitRec<R>), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(p.rad, rad.data(), rad.size() * sizeof(R), cudaMemcpyHostToDevice, c->stream));
+    if (!list.empty())
+        CK(cudaMemcpyAsync(p.hitList, list.data(), list.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    launch_batch<R>(p, 2, st, c->stream, &c->launches);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(rad.data(), p.rad, rad.size() * sizeof(R), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < rad.size(); ++i) out[i] = double(rad[i]);
+}
+
+template <typename F>
+void withStats(Ctx* c, sdfgi_stats* stats, F&& f) {
+    CK(cudaMemsetAsync(c->scratch.p, 0, 64 * 8, c->stream));
+    f();
+    unsigned long long h[32];
+    CK(cudaMemcpyAsync(h, c->scratch.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    fillStats(stats, h);
+}
+
+}  // namespace
+
+extern "C" {
+
+int sdfgi_trace_rays(void* ctx, const double* origins, const double* dirs, int n, double t_max,
+                     double surface_epsilon, int max_steps, double start_bound, sdfgi_hit* out, sdfgi_stats* stats) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(c->haveScene, SDFGI_ERR_STATE, "scene not uploaded");
+        REQ(n >= 0 && (n == 0 || (origins && dirs && out)), SDFGI_ERR_INVALID, "bad ray arguments");
+        if (n == 0) return;
+        withStats(c, stats, [&] {
+            if (c->precision == SDFGI_F64)
+                traceRays<double>(c, origins, dirs, n, t_max, surface_epsilon, max_steps, start_bound, out, stats);
+            else
+                traceRays<float>(c, origins, dirs, n, t_max, surface_epsilon, max_steps, start_bound, out, stats);
+        });
+    });
+}
+
+int sdfgi_soft_shadow(void* ctx, const double* origins, const double* dirs, const double* t_min,
+                      const double* t_max, int n, double k, int max_steps, double min_step, double* out_vis,
+                      sdfgi_stats* stats) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(c->haveScene, SDFGI_ERR_STATE, "scene not uploaded");
+        REQ(n >= 0 && (n == 0 || (origins && dirs && t_min && t_max && out_vis)), SDFGI_ERR_INVALID,
+            "bad shadow arguments");
+        REQ(min_step > 0, SDFGI_ERR_INVALID, "min_step must be > 0");
+        if (n == 0) return;
+        withStats(c, stats, [&] {
+            if (c->precision == SDFGI_F64)
+                softShadow<double>(c, origins, dirs, t_min, t_max, n, k, max_steps, min_step, out_vis, stats);
+            else
+                softShadow<float>(c, origins, dirs, t_min, t_max, n, k, max_steps, min_step, out_vis, stats);
+        });
+    });
+}
+
+int sdfgi_shade_hits(void* ctx, const sdfgi_hit* hits, int n, double bounce_coeff, const sdfgi_cfg* cfg,
+                     double* out_rgb, sdfgi_stats* stats) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(c->haveScene, SDFGI_ERR_STATE, "scene not uploaded");
+        REQ(cfg, SDFGI_ERR_INVALID, "null cfg");
+        REQ(n >= 0 && (n == 0 || (hits && out_rgb)), SDFGI_ERR_INVALID, "bad hit arguments");
+        if (n == 0) return;
+        withStats(c, stats, [&] {
+            if (c->precision == SDFGI_F64)
+                shadeHits<double>(c, hits, n, bounce_coeff, cfg, out_rgb, stats);
+            else
+                shadeHits<float>(c, hits, n, bounce_coeff, cfg, out_rgb, stats);
+        });
+    });
+}
+
+int sdfgi_convolve_irradiance(void* ctx, const double* sample_dirs, const double* sample_radiance, int n_samples,
+                              const double* texel_dirs, int n_texels, double* out_rgb) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(n_samples >= 0 && n_texels >= 0, SDFGI_ERR_INVALID, "negative count");
+        REQ(n_texels == 0 || (texel_dirs && out_rgb), SDFGI_ERR_INVALID, "null texel arguments");
+        REQ(n_samples == 0 || (sample_dirs && sample_radiance), SDFGI_ERR_INVALID, "null sample arguments");
+        if (n_texels == 0) return;
+        if (n_samples == 0) {  // ConvolveResult{0, empty}
+            std::fill(out_rgb, out_rgb + 3 * static_cast<size_t>(n_texels), 0.0);
+            return;
+        }
+        DBuf<double> buf;
+        const size_t ns = 3 * static_cast<size_t>(n_samples), nt = 3 * static_cast<size_t>(n_texels);
+        buf.alloc(2 * ns + 2 * nt);
+        CK(cudaMemcpyAsync(buf.p, sample_dirs, ns * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(buf.p + ns, sample_radiance, ns * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(buf.p + 2 * ns, texel_dirs, nt * 8, cudaMemcpyHostToDevice, c->stream));
+        launch_convolve_batch(buf.p, buf.p + ns, n_samples, buf.p + 2 * ns, n_texels, buf.p + 2 * ns + nt, c->stream);
+        checkLaunch(c);
+        CK(cudaMemcpyAsync(out_rgb, buf.p + 2 * ns + nt, nt * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        buf.free();
+    });
+}
+
+int sdfgi_interpolation_stencil(void* ctx, const double* points, int n, double mvc_relocation_frac,
+                                sdfgi_stencil* out) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(n >= 0 && (n == 0 || (points && out)), SDFGI_ERR_INVALID, "bad stencil arguments");
+        if (n == 0) return;
+        DBuf<double> pts, w;
+        DBuf<int> idx, meta;
+        pts.upload(points, 3 * static_cast<size_t>(n), c->stream);
+        w.alloc(8 * static_cast<size_t>(n));
+        idx.alloc(8 * static_cast<size_t>(n));
+        meta.alloc(5 * static_cast<size_t>(n));
+        launch_stencil_batch(c->probeCommon(), pts.p, n, mvc_relocation_frac, idx.p, w.p, meta.p, c->stream);
+        checkLaunch(c);
+        std::vector<double> hw(8 * static_cast<size_t>(n));
+        std::vector<int> hi(8 * static_cast<size_t>(n)), hm(5 * static_cast<size_t>(n));
+        CK(cudaMemcpyAsync(hw.data(), w.p, hw.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(hi.data(), idx.p, hi.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(hm.data(), meta.p, hm.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int i = 0; i < n; ++i) {
+            sdfgi_stencil& s = out[i];
+            std::memset(&s, 0, sizeof(s));
+            const int slot = hm[5 * i];
+            s.level = slot >= 0 ? c->cascades[slot].level : -1;
+            s.count = hm[5 * i + 1];
+            s.cross_cascade = hm[5 * i + 2];
+            s.sky_fallback = hm[5 * i + 3];
+            s.used_mvc = hm[5 * i + 4];
+            for (int k = 0; k < 8; ++k) {
+                s.index[k] = hi[8 * i + k];
+                s.weight[k] = hw[8 * i + k];
+            }
+        }
+        pts.free();
+        w.free();
+        idx.free();
+        meta.free();
     });
 }
 

@@ -71,7 +71,19 @@ _SIGS = {
     "sdfgi_compose": [_P, _P, _P, _P],
     "sdfgi_select_probes": [_P, _P, _P, _I, _I, _P, _P],
     "sdfgi_launch_count": [_P, _P],
+    "sdfgi_trace_rays": [_P, _P, _P, _I, _D, _D, _I, _D, _P, _P],
+    "sdfgi_soft_shadow": [_P, _P, _P, _P, _P, _I, _D, _I, _D, _P, _P],
+    "sdfgi_shade_hits": [_P, _P, _I, _D, _P, _P, _P],
+    "sdfgi_convolve_irradiance": [_P, _P, _P, _I, _P, _I, _P],
+    "sdfgi_interpolation_stencil": [_P, _P, _I, _D, _P],
 }
+
+# sdfgi_hit (Hit, scene.hpp:375-383) and sdfgi_stencil (InterpolationStencil,
+# probe_volume.hpp:205-217), include/sdfgi_b200.h
+HIT_DTYPE = np.dtype([("t", "<f8"), ("pos", "<f8", 3), ("normal", "<f8", 3), ("prim_index", "<i4"),
+                      ("converged", "<i4"), ("miss", "<i4"), ("_pad", "<i4")])
+STENCIL_DTYPE = np.dtype([("weight", "<f8", 8), ("level", "<i4"), ("index", "<i4", 8), ("count", "<i4"),
+                          ("cross_cascade", "<i4"), ("sky_fallback", "<i4"), ("used_mvc", "<i4"), ("_pad", "<i4")])
 
 RELOC_DTYPE = np.dtype([("relocated", "<i4"), ("rejected", "<i4"), ("dead", "<i4"), ("_pad", "<i4")])
 RESULT_DTYPE = np.dtype([("max_texel_delta", "<f8"), ("rays_traced", "<i8"), ("probes_updated", "<i8")])
@@ -408,6 +420,52 @@ class Device:
         _call("sdfgi_probes_trace_debug", self._ctx, _ptr(r), len(r), int(frame), _ptr(cfg), _ptr(out), cap,
               ctypes.byref(n))
         return out[: n.value]
+
+    def trace_rays(self, origins, dirs, t_max, eps=1e-3, max_steps=128, start_bound=np.inf, stats=False):
+        """sphereTrace (scene.hpp:391-435) of a batch of rays -> HIT_DTYPE array."""
+        o = np.ascontiguousarray(origins, np.float64).reshape(-1, 3)
+        d = np.ascontiguousarray(dirs, np.float64).reshape(-1, 3)
+        out = np.zeros(len(o), HIT_DTYPE)
+        st = np.zeros(1, sio.STATS_DTYPE) if stats else None
+        _call("sdfgi_trace_rays", self._ctx, _ptr(o), _ptr(d), len(o), float(t_max), float(eps), int(max_steps),
+              float(start_bound), _ptr(out), _ptr(st))
+        return (out, st[0]) if stats else out
+
+    def soft_shadow(self, origins, dirs, t_min, t_max, k, max_steps=256, min_step=5e-4, stats=False):
+        """softShadowTrace (scene.hpp:459-476) of a batch of segments -> visibility."""
+        o = np.ascontiguousarray(origins, np.float64).reshape(-1, 3)
+        d = np.ascontiguousarray(dirs, np.float64).reshape(-1, 3)
+        t0 = np.ascontiguousarray(np.broadcast_to(t_min, len(o)), np.float64)
+        t1 = np.ascontiguousarray(np.broadcast_to(t_max, len(o)), np.float64)
+        v = np.zeros(len(o))
+        st = np.zeros(1, sio.STATS_DTYPE) if stats else None
+        _call("sdfgi_soft_shadow", self._ctx, _ptr(o), _ptr(d), _ptr(t0), _ptr(t1), len(o), float(k), int(max_steps),
+              float(min_step), _ptr(v), _ptr(st))
+        return (v, st[0]) if stats else v
+
+    def shade_hits(self, hits, bounce_coeff, cfg):
+        """shadeHit (probe_update.hpp:136-149) of HIT_DTYPE hits against the front atlas."""
+        h = np.ascontiguousarray(hits, HIT_DTYPE)
+        c = np.ascontiguousarray(cfg, sio.CFG_DTYPE).reshape(1)
+        out = np.zeros((len(h), 3))
+        _call("sdfgi_shade_hits", self._ctx, _ptr(h), len(h), float(bounce_coeff), _ptr(c), _ptr(out), None)
+        return out
+
+    def convolve_irradiance(self, sample_dirs, sample_radiance, texel_dirs):
+        """convolveIrradiance (probe_update.hpp:25-34) for many texel directions."""
+        sd = np.ascontiguousarray(sample_dirs, np.float64).reshape(-1, 3)
+        sr = np.ascontiguousarray(sample_radiance, np.float64).reshape(-1, 3)
+        td = np.ascontiguousarray(texel_dirs, np.float64).reshape(-1, 3)
+        out = np.zeros((len(td), 3))
+        _call("sdfgi_convolve_irradiance", self._ctx, _ptr(sd), _ptr(sr), len(sd), _ptr(td), len(td), _ptr(out))
+        return out
+
+    def interpolation_stencil(self, points, mvc_frac=0.25):
+        """interpolationStencil (probe_volume.hpp:224-310) -> STENCIL_DTYPE array."""
+        p = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        out = np.zeros(len(p), STENCIL_DTYPE)
+        _call("sdfgi_interpolation_stencil", self._ctx, _ptr(p), len(p), float(mvc_frac), _ptr(out))
+        return out
 
     def query_points(self, pts, init=None):
         pts = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)
