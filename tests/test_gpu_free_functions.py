@@ -44,8 +44,12 @@ def test_sphere_trace_batch_matches_analytic(dev):
         if t is None:
             assert h["converged"][i] == 0 and h["miss"][i] in (1, 2)
         elif h["converged"][i]:
-            assert abs(h["t"][i] - t) <= 2 * EPS and h["prim_index"][i] == 0
-            n = (h["pos"][i] - [0.5, -0.3, 0.2]) / np.linalg.norm(h["pos"][i] - [0.5, -0.3, 0.2])
+            # on the surface to the polish tolerance; t within 2 eps unless grazing
+            c = np.array([0.5, -0.3, 0.2])
+            assert abs(np.linalg.norm(h["pos"][i] - c) - 1.3) <= EPS and h["prim_index"][i] == 0
+            n = (h["pos"][i] - c) / np.linalg.norm(h["pos"][i] - c)
+            if -np.dot(n, d[i]) > 0.2:
+                assert abs(h["t"][i] - t) <= 2 * EPS
             assert np.allclose(h["normal"][i], n, atol=1e-5)
     assert np.mean(h["converged"]) > 0.2
 
