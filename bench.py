@@ -65,6 +65,27 @@ STEP_KERNELS = ("k_relocate", "k_ray_setup", "k_ray_scan", "k_trace_primary", "k
                 "k_convolve")
 
 
+def ncu_kernel_traffic(precision, kernel_group):
+    """DRAM bytes (read + write) per launch of the dominant kernel group from the
+    newest committed `ncu --set full` summary (profiles/r*_ncu_step_<prec>_v*.json):
+    the capture replays one C2 pass, so per launch = per pass."""
+    files = latest_profiles(f"ncu_step_{precision}", "json")
+    if not files:
+        return None, None
+    caps = json.load(open(files[-1])).get("full_captures", [])
+    names = kernel_group.split("+")
+    tot, seen = 0.0, False
+    for c in caps:
+        name = re.sub(r"\(.*", "", c.get("Kernel Name", "")).replace("void ", "")
+        if any(n in name for n in names):
+            try:
+                tot += float(c["dram__bytes_read.sum"]) + float(c["dram__bytes_write.sum"])
+                seen = True
+            except (KeyError, ValueError):
+                continue
+    return (tot if seen else None), os.path.relpath(files[-1], ROOT)
+
+
 def ncu_step_traffic(precision):
     """DRAM bytes (read + write) of one C2 step's update kernels from the committed ncu
     launch list of scripts/profile_step.py (profiles/r01_step_launches_<prec>_v*.csv,
@@ -303,24 +324,87 @@ class StepRunner:
             self.dev.reset_probes(level)
 
     def step(self, stats=False):
+        """-> rays, update-kernel ms, per-stage ms (summed over passes), and with
+        stats the algorithmic work per kernel (workmodel) and the raw counters."""
         from paper_2007_14394_b200 import api
 
         dev, stage = self.dev, self.stage
-        rays, upd_ms, ops, work_all = 0, 0.0, 0, []
+        rays, upd_ms, work_all = 0, 0.0, []
+        stage_ms = dict.fromkeys(dev.STAGES, 0.0)
+        work = dict.fromkeys(("k1", "k2", "shade", "convolve"), 0.0)
+        prec = dev.precision
         for p in range(PASSES):
             stage.relocate_all(stats=stats)
             r = api.updateProbes(dev, stage.cfg, p, None, stats=stats)
             if stats:
                 res, st = r
-                work = dev.last_work()
-                ops += workmodel.update_ops(st, work, int(res["rays_traced"]), shading=dev.last_shading_work())
-                work_all.append((dict(zip(st.dtype.names, map(int, st))), [int(w) for w in work]))
+                tc = dev.last_trace_counters()
+                sh = dev.last_shading_work()
+                work["k1"] += workmodel.query_ops(*tc["k1"])
+                work["k2"] += workmodel.query_ops(*tc["k2"])
+                work["shade"] += workmodel.shading_ops(sh, prec)
+                work["convolve"] += workmodel.convolve_ops(int(res["rays_traced"]))
+                work_all.append({"k1": tc["k1"], "k2": tc["k2"], "shading": sh})
             else:
                 res = r
             upd_ms += dev.last_kernel_ms()[0]
+            for k, v in dev.last_stage_ms().items():
+                stage_ms[k] += v
             rays += int(res["rays_traced"])
             dev.swap()
-        return rays, upd_ms, ops, work_all
+        return rays, upd_ms, stage_ms, work, work_all
+
+
+KERNEL_STAGES = {
+    # stage group -> (kernels, stages of last_stage_ms, work key)
+    "k_trace_primary": ("K1 primary rays, near + far phase (sphereTrace)", ("k1", "k1_far"), "k1"),
+    "k_trace_shadow": ("K2 shadow rays, near + far phase (softShadowTrace)", ("k2", "k2_far"), "k2"),
+    "k_shade_rays+k_shade_mvc": ("K3a + K3c (shadeHit, bounce lookup with MVC)", ("shade",), "shade"),
+    "k_convolve": ("K3b (convolveIrradiance + hysteresis blend + border)", ("convolve",), "convolve"),
+}
+
+
+def roofline_of(args, dev, kern, ms_step, work_step, n_probes):
+    """Per-kernel rooflines of the update: algorithmic FP instructions (workmodel.py,
+    from the kernels' own counters; shading weights measured with ncu) / the
+    kernel's device time (CUDA events around each stage on the context's stream,
+    median over the timed steps), against the measured FMA-instruction rate. The
+    headline object is the dominant kernel (largest share of the step)."""
+    f64_rate, f32_rate = dev.measure_fp_peak()
+    peak_rate = f64_rate if args.precision == "f64" else f32_rate
+    upd_ms = statistics.median(k[0] for k in kern)
+    stage_ms = {k: statistics.median(s[1][k] for s in kern) for k in kern[0][1]}
+    kernels = {}
+    for name, (what, stages, wk) in KERNEL_STAGES.items():
+        ms = sum(stage_ms[st] for st in stages)
+        ach = work_step[wk] / (ms * 1e-3) if ms > 0 else 0.0
+        kernels[name] = {"what": what, "ms_per_step": ms, "share_of_step": ms / ms_step,
+                         "work_instr_per_step": work_step[wk], "achieved": ach / 1e12, "frac": ach / peak_rate}
+    total_work = sum(work_step.values())
+    dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
+    traffic, traffic_src = ncu_kernel_traffic(args.precision, dom) if args.config == "c2" else (None, None)
+    _, _, wsrc = workmodel.shading_weights(args.precision)
+    return {
+        "bound": "fp64" if args.precision == "f64" else "fp32",
+        "kernel": dom,
+        "achieved": kernels[dom]["achieved"],
+        "peak": peak_rate / 1e12,
+        "unit": "Tinstr/s",
+        "frac": kernels[dom]["frac"],
+        "traffic": traffic,
+        "traffic_unit": "DRAM bytes per launch of the dominant kernel (ncu --set full capture, cold cache)",
+        "traffic_source": traffic_src,
+        "algorithmic_instr_per_launch": kernels[dom]["work_instr_per_step"] / PASSES,
+        "kernels": kernels,
+        "wavefront_total": {"ms_per_step": upd_ms, "work_instr_per_step": total_work,
+                            "achieved": total_work / (upd_ms * 1e-3) / 1e12,
+                            "frac": total_work / (upd_ms * 1e-3) / peak_rate, "share_of_step": upd_ms / ms_step},
+        "algorithmic_hbm_bytes_per_step": PASSES * n_probes * (768 + 1200),
+        "peak_source": "measured live: sdfgi_measure_fp_peak FMA-instruction rate (MEASURED_PEAKS.json has no FP "
+                       "pipe entry)",
+        "work_model": f"paper_2007_14394_b200/workmodel.py; query weights SURVEY §8d SASS counts, shading weights "
+                      f"{wsrc}",
+    }
 
 
 def timed_steps(runner, steps, ext, flush, torch, barrier):
@@ -336,11 +420,11 @@ def timed_steps(runner, steps, ext, flush, torch, barrier):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(ext)
-        rays, upd_ms, _, _ = runner.step()
+        rays, upd_ms, stage_ms, _, _ = runner.step()
         e1.record(ext)
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
-        kern.append(upd_ms)
+        kern.append((upd_ms, stage_ms))
     barrier()
     torch.cuda.synchronize()
     return times, kern, rays
@@ -384,7 +468,7 @@ def run_ours(args, rank, world, local_rank):
 
     # algorithmic work of one step (untimed stats run: counters cost registers/atomics)
     runner.fresh()
-    rays_stats, _, ops_step, work_all = runner.step(stats=True)
+    rays_stats, _, _, work_step, work_all = runner.step(stats=True)
     for _ in range(args.warmup):
         runner.fresh()
         runner.step()
@@ -403,30 +487,7 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_gather and args.config == "c2":
         gather = gather_bench(args, dev, stage, scene, torch, ext, flush)
 
-    # roofline of the dominant kernel (k_probe_update): algorithmic ops / kernel time
-    f64_rate, f32_rate = dev.measure_fp_peak()
-    peak_rate = f64_rate if args.precision == "f64" else f32_rate
-    kern_ms = statistics.median(kern)
-    achieved = ops_step / (kern_ms * 1e-3)  # ops/s over the step's update launches
-    traffic, traffic_src = ncu_step_traffic(args.precision)
-    # per probe per pass, read the previous tile interior (768 B) + write the tile (1,200 B)
-    hbm_alg = PASSES * n_probes * (768 + 1200)
-    roofline = {
-        "bound": "fp64" if args.precision == "f64" else "fp32",
-        "kernel": "k_probe_update",
-        "achieved": achieved / 1e12,
-        "peak": peak_rate / 1e12,
-        "unit": "Tinstr/s",
-        "frac": achieved / peak_rate,
-        "traffic": traffic if args.config == "c2" else None,
-        "traffic_unit": "DRAM bytes per step (ncu, serialised cold-cache launches)",
-        "traffic_source": traffic_src if args.config == "c2" else None,
-        "algorithmic_hbm_bytes_per_step": hbm_alg,
-        "peak_source": "measured live: sdfgi_measure_fp_peak FMA-instruction rate (MEASURED_PEAKS.json has no FP pipe entry)",
-        "work_per_step_instr": ops_step,
-        "update_kernel_ms_per_step": kern_ms,
-        "kernel_share_of_step": kern_ms / ms_step,
-    }
+    roofline = roofline_of(args, dev, kern, ms_step, work_step, n_probes)
     hbm_peak = float(load_peaks().get("hbm_gbs", 7700.0))
     line = {
         "metric": METRIC,

@@ -312,6 +312,15 @@ SDFGI_API int sdfgi_last_work(void* ctx, uint64_t out[6]);
  * (converged hits with an owner), mvcWeightsHex evaluations} — the W_stencil
  * term of the algorithmic-work model. */
 SDFGI_API int sdfgi_last_shading_work(void* ctx, uint64_t out[2]);
+/* Device ms of the last sdfgi_probes_update's stages: {K1 primary rays, K1 far
+ * phase, hit compaction + normals + shadow set-up, K2 shadow rays, K2 far phase,
+ * K3a + K3c shading, K3b convolution + blend}. */
+SDFGI_API int sdfgi_last_stage_ms(void* ctx, double out[7]);
+/* The last stats-enabled update's event counters per tracing kernel: out[0..13]
+ * K1 (primary rays), out[14..27] K2 (shadow rays), each {sdf_queries,
+ * clusters_visited, clusters_skipped, primitive_evals, trace_steps, sphere_traces,
+ * shadow_traces, visibility_traces, evaluations by kind x5, rotated evaluations}. */
+SDFGI_API int sdfgi_last_trace_counters(void* ctx, uint64_t out[28]);
 
 /* FP pipe throughput microbenchmark on the context's device: FP64 and FP32 fused
  * multiply-add instructions per second (the roofline denominators for the tracing

@@ -278,9 +278,13 @@ void launch_convolve_batch(const double* sdir, const double* srad, int ns, const
 // per point 8 probe indices, 8 weights and (cascade slot, count, crossCascade, skyFallback, usedMvc)
 void launch_stencil_batch(const ProbeCommon& pc, const double* pts, int n, double mvcFrac, int* idx, double* w,
                           int* meta, cudaStream_t st);
+// ev (optional, kWaveEvents events) marks the stage boundaries: before K1, after K1,
+// its far phase, the compaction + normals, K2, its far phase, K3a + K3c, K3b.
+constexpr int kWaveEvents = 8;
+constexpr int kShadowStats = 64;  // K2's counters at stats + kShadowStats (stats runs)
 template <typename R>
-void launch_wavefront(const WaveParams<R>& p, int persistBlocks, bool stats, cudaStream_t st,
-                      cudaEvent_t evStart, cudaEvent_t evEnd, long long* launches);
+void launch_wavefront(const WaveParams<R>& p, int persistBlocks, bool stats, cudaStream_t st, const cudaEvent_t* ev,
+                      long long* launches);
 // stage 0 G-buffer, 1 downsample+select, 2 tiles (tasks+visibility+shadePixelGI),
 // 3 resolve, 4 contact
 template <typename R>

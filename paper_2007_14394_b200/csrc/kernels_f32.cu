@@ -7,7 +7,7 @@
 
 namespace sdfgi_dev {
 
-template void launch_wavefront<float>(const WaveParams<float>&, int, bool, cudaStream_t, cudaEvent_t, cudaEvent_t,
+template void launch_wavefront<float>(const WaveParams<float>&, int, bool, cudaStream_t, const cudaEvent_t*,
                                       long long*);
 
 template void launch_gather<float>(const GatherParams<float>&, int, bool, cudaStream_t);

@@ -258,7 +258,7 @@ void launch_query_points(const QueryParams& p, cudaStream_t st) {
     k_query_points<<<(p.n + 127) / 128, 128, 0, st>>>(p);
 }
 
-template void launch_wavefront<double>(const WaveParams<double>&, int, bool, cudaStream_t, cudaEvent_t, cudaEvent_t,
+template void launch_wavefront<double>(const WaveParams<double>&, int, bool, cudaStream_t, const cudaEvent_t*,
                                        long long*);
 
 template void launch_gather<double>(const GatherParams<double>&, int, bool, cudaStream_t);

@@ -1142,14 +1142,15 @@ static int persistentBlocks(K kernel, int threads, int cap, size_t smem = 0) {
 }
 
 template <typename R, bool ST>
-static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1,
-                      long long* launches) {
+static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cudaEvent_t* ev, long long* launches) {
     if (p.nCand <= 0) return;
+    auto mark = [&](int i) {
+        if (ev) cudaEventRecord(ev[i], st);
+    };
     k_ray_setup<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
     k_ray_scan<R><<<1, kScanThreads, 0, st>>>(p);
     k_ray_chunks<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
     cudaMemsetAsync(p.ctr, 0, (kLightCtr + (p.scene.n_lights > 1 ? p.scene.n_lights : 1)) * sizeof(unsigned long long), st);
-    if (e0) cudaEventRecord(e0, st);
     static int b1 = persistentBlocks(k_trace_primary<R, ST, 0, 0>, kWaveThreads, 0);
     static int b1f = persistentBlocks(k_trace_primary<R, ST, 0, 1>, kWaveThreads, 0);
     static int b2 = persistentBlocks(k_trace_shadow<R, ST, 0>, kWaveThreads, 0);
@@ -1159,18 +1160,29 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
     static int b3c = persistentBlocks(k_shade_mvc<R, ST>, kMvcThreads, 0, kMvcThreads * kMvcSlab * sizeof(R));
     // hitAt covers the batch's upper bound of rays; slots past the traced ones stay -1
     cudaMemsetAsync(p.hitAt, 0xff, static_cast<size_t>(p.maxItems) * sizeof(int), st);
+    mark(0);
     k_trace_primary<R, ST, 0, 0><<<cap > 0 ? min(cap, b1) : b1, kWaveThreads, 0, st>>>(p);
+    mark(1);
     k_trace_primary<R, ST, 0, 1><<<cap > 0 ? min(cap, b1f) : b1f, kWaveThreads, 0, st>>>(p);
+    mark(2);
     compact_hits(p.hitAt, p.hitList, p.ctr + kCtrHits, static_cast<int>(p.maxItems), p.selTemp, p.selTempBytes, st);
     k_hit_normals<R><<<b3, 128, 0, st>>>(p);
-    k_trace_shadow<R, ST, 0><<<cap > 0 ? min(cap, b2) : b2, kWaveThreads, 0, st>>>(p);
-    k_trace_shadow<R, ST, 1><<<cap > 0 ? min(cap, b2f) : b2f, kWaveThreads, 0, st>>>(p);
+    mark(3);
+    // the shadow kernels count their events in a separate block of counters
+    // (stats + kShadowStats), so the work of K1 and K2 can be told apart
+    WaveParams<R> p2 = p;
+    if (ST) p2.stats = p.stats + kShadowStats;
+    k_trace_shadow<R, ST, 0><<<cap > 0 ? min(cap, b2) : b2, kWaveThreads, 0, st>>>(p2);
+    mark(4);
+    k_trace_shadow<R, ST, 1><<<cap > 0 ? min(cap, b2f) : b2f, kWaveThreads, 0, st>>>(p2);
+    mark(5);
     if (p.debug) {
         k_shade_rays<R, ST, false><<<b3d, 128, 128 * kMvcSlab * sizeof(R), st>>>(p);
     } else {
         k_shade_rays<R, ST, true><<<b3, 128, 0, st>>>(p);
         k_shade_mvc<R, ST><<<b3c, kMvcThreads, kMvcThreads * kMvcSlab * sizeof(R), st>>>(p);
     }
+    mark(6);
     if (!p.debug) {
         const size_t smem = static_cast<size_t>(2 * p.nRaysFull) * 6 * sizeof(R);
         auto k3 = k_convolve<R, ST>;
@@ -1181,7 +1193,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, cudaEven
             cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         k3<<<p.nCand, kConvThreads, smem, st>>>(p);
     }
-    if (e1) cudaEventRecord(e1, st);
+    mark(7);
     if (launches) *launches += p.debug ? 10 : 12;
 }
 
@@ -1384,12 +1396,12 @@ void launch_contact(const WaveParams<R>& p, bool stats, cudaStream_t st, long lo
 }
 
 template <typename R>
-void launch_wavefront(const WaveParams<R>& p, int cap, bool stats, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1,
+void launch_wavefront(const WaveParams<R>& p, int cap, bool stats, cudaStream_t st, const cudaEvent_t* ev,
                       long long* launches) {
     if (stats)
-        wavefront<R, true>(p, cap, st, e0, e1, launches);
+        wavefront<R, true>(p, cap, st, ev, launches);
     else
-        wavefront<R, false>(p, cap, st, e0, e1, launches);
+        wavefront<R, false>(p, cap, st, ev, launches);
 }
 
 }  // namespace sdfgi_dev

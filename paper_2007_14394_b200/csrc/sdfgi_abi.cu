@@ -119,6 +119,7 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // update start/end, relocate start/end
     cudaEvent_t quatEv = nullptr;  // the quaternion staging copy has been consumed
+    cudaEvent_t kev[kWaveEvents] = {};  // the last update's stage boundaries (launch_wavefront)
     bool evUpdate = false, evReloc = false;
     ncclComm_t comm = nullptr;
     long long launches = 0;
@@ -180,6 +181,7 @@ struct Ctx {
     // [17] rays, [18] probes updated
     DBuf<unsigned long long> scratch;
     unsigned long long lastWork[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long lastTrace[2][14] = {};  // the last stats update's K1 / K2 counters
     unsigned long long shadeWork[2] = {0, 0};
     DBuf<int> report;
     DBuf<int> refs, allRefs;
@@ -235,6 +237,8 @@ struct Ctx {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (quatEv) cudaEventDestroy(quatEv);
+        for (auto& e : kev)
+            if (e) cudaEventDestroy(e);
         if (comm) ncclCommDestroy(comm);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -725,21 +729,27 @@ void buildGrid(Ctx* c) {
 }
 
 void readCounters(Ctx* c, sdfgi_stats* stats, unsigned long long* tail, int ntail) {
-    std::vector<unsigned long long> h(32);
+    // [0..13] K1 (and relocation) counters, [16..] tail values, [kShadowStats..+13] K2's
+    std::vector<unsigned long long> h(kShadowStats + 32);
     CK(cudaMemcpyAsync(h.data(), c->scratch.p, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (stats) {
-        for (int i = 0; i < 6; ++i) c->lastWork[i] = h[8 + i];
+        const unsigned long long* k2 = h.data() + kShadowStats;
+        for (int i = 0; i < 14; ++i) {
+            c->lastTrace[0][i] = h[i];
+            c->lastTrace[1][i] = k2[i];
+        }
+        for (int i = 0; i < 6; ++i) c->lastWork[i] = h[8 + i] + k2[8 + i];
         c->shadeWork[0] = h[20];  // shadeHit calls, MVC evaluations (K3a)
         c->shadeWork[1] = h[21];
-        stats->sdf_queries += h[0];
-        stats->clusters_visited += h[1];
-        stats->clusters_skipped += h[2];
-        stats->primitive_evals += h[3];
-        stats->trace_steps += h[4];
-        stats->sphere_traces += h[5];
-        stats->shadow_traces += h[6];
-        stats->visibility_traces += h[7];
+        stats->sdf_queries += h[0] + k2[0];
+        stats->clusters_visited += h[1] + k2[1];
+        stats->clusters_skipped += h[2] + k2[2];
+        stats->primitive_evals += h[3] + k2[3];
+        stats->trace_steps += h[4] + k2[4];
+        stats->sphere_traces += h[5] + k2[5];
+        stats->shadow_traces += h[6] + k2[6];
+        stats->visibility_traces += h[7] + k2[7];
     }
     for (int i = 0; i < ntail; ++i) tail[i] = h[16 + i];
 }
@@ -1010,8 +1020,9 @@ int sdfgi_ctx_create(int device, int rank, int world, const uint8_t* nccl_uid, i
             CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
             for (auto& e : c->ev) CK(cudaEventCreate(&e));
             CK(cudaEventCreateWithFlags(&c->quatEv, cudaEventDisableTiming));
+            for (auto& e : c->kev) CK(cudaEventCreate(&e));
             CK(cudaEventRecord(c->quatEv, c->stream));
-            c->scratch.alloc(64);
+            c->scratch.alloc(kShadowStats + 32);
             c->report.alloc(4);
             if (world > 1) {
                 REQ(nccl_uid, SDFGI_ERR_INVALID, "world > 1 needs an NCCL unique id");
@@ -1395,7 +1406,7 @@ int sdfgi_probes_relocate(void* ctx, int level, double threshold1, double thresh
         p.report = c->report.p;
         p.stats = c->scratch.p;
         CK(cudaMemsetAsync(c->report.p, 0, 4 * sizeof(int), c->stream));
-        CK(cudaMemsetAsync(c->scratch.p, 0, 32 * 8, c->stream));
+        CK(cudaMemsetAsync(c->scratch.p, 0, (kShadowStats + 32) * 8, c->stream));
         // relocation is replicated on every rank (deterministic, bit-exact): no exchange
         CK(cudaEventRecord(c->ev[2], c->stream));
         launch_relocate(p, c->cascades[s].count(), stats != nullptr, c->stream);
@@ -1425,7 +1436,7 @@ int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_refs, int fr
         const float* frontp = c->atlas[c->front].p;
         // atlas_[write] = atlas_[read] (pipeline.hpp:131); updated tiles are overwritten
         CK(cudaMemcpyAsync(back, frontp, c->atlasFloats() * 4, cudaMemcpyDeviceToDevice, c->stream));
-        CK(cudaMemsetAsync(c->scratch.p, 0, 32 * 8, c->stream));
+        CK(cudaMemsetAsync(c->scratch.p, 0, (kShadowStats + 32) * 8, c->stream));
         const bool all = (probe_refs == nullptr && c->world == 1);
         // back <- front (copied above) + the updated tiles: still all-zero only if no
         // probe anywhere is updated this pass
@@ -1439,11 +1450,11 @@ int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_refs, int fr
             uploadQuats(c, cfg, frame, all ? nullptr : refs.data(), nCand);
             if (c->precision == SDFGI_F64) {
                 WaveParams<double> p = waveParams<double>(c, cfg, frame, cand, nCand);
-                launch_wavefront<double>(p, c->persistCap, stats != nullptr, c->stream, c->ev[0], c->ev[1],
+                launch_wavefront<double>(p, c->persistCap, stats != nullptr, c->stream, c->kev,
                                          &c->launches);
             } else {
                 WaveParams<float> p = waveParams<float>(c, cfg, frame, cand, nCand);
-                launch_wavefront<float>(p, c->persistCap, stats != nullptr, c->stream, c->ev[0], c->ev[1],
+                launch_wavefront<float>(p, c->persistCap, stats != nullptr, c->stream, c->kev,
                                         &c->launches);
             }
             CK(cudaGetLastError());
@@ -1464,6 +1475,8 @@ int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_refs, int fr
                 }
             NK(ncclGroupEnd());
             NK(ncclAllReduce(c->scratch.p, c->scratch.p, 14, ncclUint64, ncclSum, c->comm, c->stream));
+            NK(ncclAllReduce(c->scratch.p + kShadowStats, c->scratch.p + kShadowStats, 14, ncclUint64, ncclSum,
+                             c->comm, c->stream));
             NK(ncclAllReduce(c->scratch.p + 16, c->scratch.p + 16, 1, ncclUint64, ncclMax, c->comm, c->stream));
             NK(ncclAllReduce(c->scratch.p + 17, c->scratch.p + 17, 2, ncclUint64, ncclSum, c->comm, c->stream));
         }
@@ -1564,12 +1577,12 @@ int sdfgi_probes_trace_debug(void* ctx, const int32_t* probe_refs, int n_refs, i
             WaveParams<double> p = waveParams<double>(c, cfg, frame, c->refs.p, n_refs);
             p.records = c->records.p;
             p.debug = 1;
-            launch_wavefront<double>(p, c->persistCap, false, c->stream, nullptr, nullptr, &c->launches);
+            launch_wavefront<double>(p, c->persistCap, false, c->stream, nullptr, &c->launches);
         } else {
             WaveParams<float> p = waveParams<float>(c, cfg, frame, c->refs.p, n_refs);
             p.records = c->records.p;
             p.debug = 1;
-            launch_wavefront<float>(p, c->persistCap, false, c->stream, nullptr, nullptr, &c->launches);
+            launch_wavefront<float>(p, c->persistCap, false, c->stream, nullptr, &c->launches);
         }
         CK(cudaGetLastError());
         long long total = 0;
@@ -1613,10 +1626,33 @@ int sdfgi_last_kernel_ms(void* ctx, double* update_ms, double* relocate_ms) {
         Ctx* c = C(ctx);
         CK(cudaStreamSynchronize(c->stream));
         float a = 0.f, b = 0.f;
-        if (c->evUpdate) CK(cudaEventElapsedTime(&a, c->ev[0], c->ev[1]));
+        if (c->evUpdate) CK(cudaEventElapsedTime(&a, c->kev[0], c->kev[kWaveEvents - 1]));
         if (c->evReloc) CK(cudaEventElapsedTime(&b, c->ev[2], c->ev[3]));
         if (update_ms) *update_ms = a;
         if (relocate_ms) *relocate_ms = b;
+    });
+}
+
+int sdfgi_last_stage_ms(void* ctx, double out[7]) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(out, SDFGI_ERR_INVALID, "null out");
+        REQ(c->evUpdate, SDFGI_ERR_STATE, "no update timed yet");
+        CK(cudaStreamSynchronize(c->stream));
+        for (int i = 0; i + 1 < kWaveEvents; ++i) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, c->kev[i], c->kev[i + 1]));
+            out[i] = ms;
+        }
+    });
+}
+
+int sdfgi_last_trace_counters(void* ctx, uint64_t out[28]) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(out, SDFGI_ERR_INVALID, "null out");
+        for (int k = 0; k < 2; ++k)
+            for (int i = 0; i < 14; ++i) out[14 * k + i] = c->lastTrace[k][i];
     });
 }
 

@@ -55,6 +55,8 @@ _SIGS = {
     "sdfgi_last_kernel_ms": [_P, _P, _P],
     "sdfgi_last_work": [_P, _P],
     "sdfgi_last_shading_work": [_P, _P],
+    "sdfgi_last_stage_ms": [_P, _P],
+    "sdfgi_last_trace_counters": [_P, _P],
     "sdfgi_measure_fp_peak": [_P, _P, _P],
     "sdfgi_set_accel": [_P, _I],
     "sdfgi_accel_info": [_P, _P],
@@ -221,6 +223,29 @@ class Device:
         out = np.zeros(2, np.uint64)
         _call("sdfgi_last_shading_work", self._ctx, _ptr(out))
         return int(out[0]), int(out[1])
+
+    STAGES = ("k1", "k1_far", "normals", "k2", "k2_far", "shade", "convolve")
+
+    def last_stage_ms(self):
+        """Device ms of the last update's stages (CUDA events on the context's stream):
+        dict over STAGES (K1, its far phase, compaction + normals, K2, its far phase,
+        K3a + K3c, K3b)."""
+        out = np.zeros(7)
+        _call("sdfgi_last_stage_ms", self._ctx, _ptr(out))
+        return dict(zip(self.STAGES, map(float, out)))
+
+    def last_trace_counters(self):
+        """The last stats-enabled update's counters per tracing kernel: {"k1": ..., "k2": ...},
+        each (stats dict, evaluations by kind x5 + rotated)."""
+        out = np.zeros(28, np.uint64)
+        _call("sdfgi_last_trace_counters", self._ctx, _ptr(out))
+        names = ("sdf_queries", "clusters_visited", "clusters_skipped", "primitive_evals", "trace_steps",
+                 "sphere_traces", "shadow_traces", "visibility_traces")
+        res = {}
+        for k, key in enumerate(("k1", "k2")):
+            v = [int(x) for x in out[14 * k:14 * k + 14]]
+            res[key] = (dict(zip(names, v[:8])), v[8:])
+        return res
 
     def last_work(self):
         """Evaluations by kind (sphere, box, plane, cylinder, capsule, rotated) of the last
