@@ -38,11 +38,20 @@ want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
         "launch__registers_per_thread", "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size", "launch__block_size"]
 idx = {w: h.index(w) for w in want if w in h}
+units = rr[1]
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3, "msecond": 1e6}
 summary["full_captures"] = []
 for r in rr[2:]:
     if len(r) != len(h):
         continue
-    summary["full_captures"].append({w: r[i] for w, i in idx.items()})
+    cap = {}
+    for w, i in idx.items():
+        u = units[i]
+        if u in SCALE:  # normalised: bytes and nanoseconds
+            cap[w] = repr(float(r[i].replace(",", "")) * SCALE[u])
+        else:
+            cap[w] = r[i]
+    summary["full_captures"].append(cap)
 json.dump(summary, open(out, "w"), indent=1)
 print(json.dumps(summary["launch_list"], indent=1)[:3000])
 for c in summary["full_captures"]:
