@@ -336,6 +336,25 @@ __device__ __forceinline__ long long parkSlot(unsigned long long* counter, bool 
     return park ? static_cast<long long>(base + __popc(m & ((1u << lane) - 1u))) : -1;
 }
 
+// The initial bound of a march query (sphereTrace, scene.hpp:397-399: 2 * lastD).
+// Candidate-grid walks also cap it at c = max(tMax - t, eps): the march tests
+// d < eps (converge) and then d >= tMax - t (TMax miss), and
+// query(p, min(2 lastD, c)) returns the reference's min(d, 2 lastD) exactly
+// whenever that is below c, and otherwise c — which, like the reference's value,
+// is not below eps and not below tMax - t: the same decision, step and t for every
+// ray. A short segment (Contact GI: tMax = half a probe spacing) then ends its
+// query as soon as every remaining candidate's lower bound clears it. Not in the
+// flat cluster walk, whose per-cluster skip tests the reference's TraceStats
+// count one for one.
+#ifndef SDFGI_MARCH_CAP
+#define SDFGI_MARCH_CAP 1
+#endif
+template <typename R>
+__device__ __forceinline__ R marchSeed(const SceneView<R>& s, R lastD, R remaining, R eps) {
+    const R b = R(2) * lastD;
+    return (SDFGI_MARCH_CAP && s.useGrid) ? smin(b, smax(remaining, eps)) : b;
+}
+
 // PHASE 0 traces new rays and parks every march whose next point is off the
 // candidate grid; PHASE 1 resumes the parked marches (no further parking).
 template <typename R, bool ST, int MODE, int PHASE>
@@ -467,7 +486,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
             if (parkIt) {
             } else if (state == 0) {
                 if (ST) ++cnt.steps;
-                initD = R(2) * lastD;
+                initD = marchSeed(P.scene, lastD, tMax - t, eps);
             } else if (state == 1) {
                 initD = polishPad(d);
             } else {
@@ -480,7 +499,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
                 parkIt = false;
                 if (state == 0) {
                     if (ST) ++cnt.steps;
-                    initD = R(2) * lastD;
+                    initD = marchSeed(P.scene, lastD, tMax - t, eps);
                 } else if (state == 1) {
                     initD = polishPad(d);
                 } else {

@@ -41,8 +41,11 @@ def test_sphere_trace_batch_matches_analytic(dev):
     h = api.sphereTrace(dev, o, d, 100.0, EPS, 128)
     for i in range(len(o)):
         t = ray_sphere(o[i], d[i], np.array([0.5, -0.3, 0.2]), 1.3)
-        if t is None:
-            assert h["converged"][i] == 0 and h["miss"][i] in (1, 2)
+        if t is None:  # a near miss may still converge within eps of the surface (d < eps)
+            if h["converged"][i]:
+                assert abs(np.linalg.norm(h["pos"][i] - [0.5, -0.3, 0.2]) - 1.3) <= EPS
+            else:
+                assert h["miss"][i] in (1, 2)
         elif h["converged"][i]:
             # on the surface to the polish tolerance; t within 2 eps unless grazing
             c = np.array([0.5, -0.3, 0.2])
