@@ -329,6 +329,18 @@ constexpr int kLightCtr = 128;
 #ifndef SDFGI_SHADOW_MINB32
 #define SDFGI_SHADOW_MINB32 SDFGI_WAVE_MINB32
 #endif
+// K1 / K2 with the primitive records staged in shared memory: one CTA per SM with
+// as many threads as the register budget of the many-CTA form allows (FP64: 7 x 128
+// at 72 registers, FP32: 8 x 128 at 64).
+#ifndef SDFGI_STAGE_THREADS64
+#define SDFGI_STAGE_THREADS64 896
+#endif
+#ifndef SDFGI_STAGE_THREADS32
+#define SDFGI_STAGE_THREADS32 1024
+#endif
+template <typename R> struct StageOcc {
+    static constexpr int threads = sizeof(R) == 8 ? SDFGI_STAGE_THREADS64 : SDFGI_STAGE_THREADS32;
+};
 template <typename R> struct WaveOcc {
     static constexpr int trace = sizeof(R) == 8 ? SDFGI_WAVE_MINB64 : SDFGI_WAVE_MINB32;
     static constexpr int shadow = sizeof(R) == 8 ? SDFGI_SHADOW_MINB64 : SDFGI_SHADOW_MINB32;

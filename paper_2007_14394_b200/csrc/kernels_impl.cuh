@@ -336,6 +336,36 @@ __device__ __forceinline__ long long parkSlot(unsigned long long* counter, bool 
     return park ? static_cast<long long>(base + __popc(m & ((1u << lane) - 1u))) : -1;
 }
 
+// The primitive records of the scene in shared memory for the whole persistent
+// kernel (the north star's "primitives staged in shared memory via TMA"): one
+// elected thread arms an mbarrier with the byte count and issues the bulk copies
+// (cp.async.bulk, the TMA engine's 1-D form, 32 KB each); every thread waits on
+// the barrier's phase 0. One CTA per SM holds the copy its warps share.
+__device__ __forceinline__ void stagePrims(const void* src, int bytes) {
+    __shared__ __align__(8) unsigned long long stageBar;
+    const unsigned bar = static_cast<unsigned>(__cvta_generic_to_shared(&stageBar));
+    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(sdfgiDynSmem));
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        const char* g = static_cast<const char*>(src);
+        for (int off = 0; off < bytes; off += 32768) {
+            const int n = min(32768, bytes - off);
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             dst + off),
+                         "l"(g + off), "r"(n), "r"(bar)
+                         : "memory");
+        }
+    }
+    __syncthreads();  // the barrier is initialised before anyone polls it
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            bar)
+        : "memory");
+}
+
 // The initial bound of a march query (sphereTrace, scene.hpp:397-399: 2 * lastD).
 // Candidate-grid walks also cap it at c = max(tMax - t, eps): the march tests
 // d < eps (converge) and then d >= tMax - t (TMax miss), and
@@ -357,8 +387,10 @@ __device__ __forceinline__ R marchSeed(const SceneView<R>& s, R lastD, R remaini
 
 // PHASE 0 traces new rays and parks every march whose next point is off the
 // candidate grid; PHASE 1 resumes the parked marches (no further parking).
-template <typename R, bool ST, int MODE, int PHASE>
-__global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_primary(WaveParams<R> P) {
+template <typename R, bool ST, int MODE, int PHASE, bool STG = false>
+__global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG ? 1 : WaveOcc<R>::trace)
+    k_trace_primary(WaveParams<R> P) {
+    if constexpr (STG) stagePrims(P.scene.stage, P.scene.stageBytes);
     ParkRay<R>* const park = reinterpret_cast<ParkRay<R>*>(P.park);
     const long long parkCap = static_cast<long long>(P.parkBytes / sizeof(ParkRay<R>));
     const long long total = PHASE ? min(static_cast<long long>(P.ctr[kCtrParkRay]), parkCap) : rayTotal(P);
@@ -532,7 +564,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::trace) k_trace_prima
         int o2 = -1;
         R nd = R(0);
         if (active)
-            nd = query<R, ST>(P.scene, p, initD, &o2, &cnt, PHASE ? seed : -1, cell, cellR,
+            nd = query<R, ST, STG>(P.scene, p, initD, &o2, &cnt, PHASE ? seed : -1, cell, cellR,
                               useCellCache<R>() ? &ccache : nullptr);
         if (active) {
             if (o2 >= 0) seed = o2;
@@ -692,8 +724,10 @@ __global__ void __launch_bounds__(128) k_hit_normals(WaveParams<R> P) {
 // (probe_update.hpp:100-128) and the softShadowTrace march (scene.hpp:459-476),
 // one query per iteration. vis = 1 when the segment is too short to trace.
 // PHASE 0 / 1 as in K1: off-grid shadow marches are parked and resumed together.
-template <typename R, bool ST, int PHASE>
-__global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shadow(WaveParams<R> P) {
+template <typename R, bool ST, int PHASE, bool STG = false>
+__global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG ? 1 : WaveOcc<R>::shadow)
+    k_trace_shadow(WaveParams<R> P) {
+    if constexpr (STG) stagePrims(P.scene.stage, P.scene.stageBytes);
     const int L = P.scene.n_lights;
     ParkShadow<R>* const park = reinterpret_cast<ParkShadow<R>*>(P.park);
     const unsigned long long parkCap = P.parkBytes / sizeof(ParkShadow<R>);
@@ -786,7 +820,7 @@ __global__ void __launch_bounds__(kWaveThreads, WaveOcc<R>::shadow) k_trace_shad
         R d = R(0);
         int o2 = -1;
         if (want)
-            d = query<R, ST>(P.scene, p, lastD == inf ? inf : R(2) * lastD, &o2, &cnt, PHASE ? seed : -1, cell, cellR,
+            d = query<R, ST, STG>(P.scene, p, lastD == inf ? inf : R(2) * lastD, &o2, &cnt, PHASE ? seed : -1, cell, cellR,
                              useCellCache<R>() ? &ccache : nullptr);
         if (o2 >= 0) seed = o2;
         if (active) {
@@ -1160,6 +1194,45 @@ static int persistentBlocks(K kernel, int threads, int cap, size_t smem = 0) {
     return cap > 0 ? min(b, cap) : b;
 }
 
+// K1 / K2 launches: with the primitive records staged in shared memory (one CTA
+// of StageOcc<R>::threads per SM, the scene's stage bytes of dynamic shared
+// memory) when the scene fits, else the register-capped many-CTA form.
+template <typename K>
+static int stagedBlocks(K kernel, int threads, int bytes) {
+    // the opt-in above 48 KB is per kernel (cheap to repeat); one CTA per SM
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    (void)threads;
+    return sms;
+}
+template <typename R, bool ST, int MODE, int PHASE>
+static void launchPrimary(const WaveParams<R>& p, int cap, cudaStream_t st) {
+    if (p.scene.stageBytes > 0) {
+        auto k = k_trace_primary<R, ST, MODE, PHASE, true>;
+        const int b = stagedBlocks(k, StageOcc<R>::threads, p.scene.stageBytes);
+        k<<<cap > 0 ? min(cap, b) : b, StageOcc<R>::threads, p.scene.stageBytes, st>>>(p);
+    } else {
+        static int b = persistentBlocks(k_trace_primary<R, ST, MODE, PHASE>, kWaveThreads, 0);
+        k_trace_primary<R, ST, MODE, PHASE><<<cap > 0 ? min(cap, b) : b, kWaveThreads, 0, st>>>(p);
+    }
+}
+template <typename R, bool ST, int PHASE>
+static void launchShadow(const WaveParams<R>& p, int cap, cudaStream_t st) {
+    if (p.scene.stageBytes > 0) {
+        auto k = k_trace_shadow<R, ST, PHASE, true>;
+        const int b = stagedBlocks(k, StageOcc<R>::threads, p.scene.stageBytes);
+        k<<<cap > 0 ? min(cap, b) : b, StageOcc<R>::threads, p.scene.stageBytes, st>>>(p);
+    } else {
+        static int b = persistentBlocks(k_trace_shadow<R, ST, PHASE>, kWaveThreads, 0);
+        k_trace_shadow<R, ST, PHASE><<<cap > 0 ? min(cap, b) : b, kWaveThreads, 0, st>>>(p);
+    }
+}
+
 template <typename R, bool ST>
 static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cudaEvent_t* ev, long long* launches) {
     if (p.nCand <= 0) return;
@@ -1170,19 +1243,15 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
     k_ray_scan<R><<<1, kScanThreads, 0, st>>>(p);
     k_ray_chunks<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
     cudaMemsetAsync(p.ctr, 0, (kLightCtr + (p.scene.n_lights > 1 ? p.scene.n_lights : 1)) * sizeof(unsigned long long), st);
-    static int b1 = persistentBlocks(k_trace_primary<R, ST, 0, 0>, kWaveThreads, 0);
-    static int b1f = persistentBlocks(k_trace_primary<R, ST, 0, 1>, kWaveThreads, 0);
-    static int b2 = persistentBlocks(k_trace_shadow<R, ST, 0>, kWaveThreads, 0);
-    static int b2f = persistentBlocks(k_trace_shadow<R, ST, 1>, kWaveThreads, 0);
     static int b3 = persistentBlocks(k_shade_rays<R, ST, true>, 128, 0);
     static int b3d = persistentBlocks(k_shade_rays<R, ST, false>, 128, 0, 128 * kMvcSlab * sizeof(R));
     static int b3c = persistentBlocks(k_shade_mvc<R, ST>, kMvcThreads, 0, kMvcThreads * kMvcSlab * sizeof(R));
     // hitAt covers the batch's upper bound of rays; slots past the traced ones stay -1
     cudaMemsetAsync(p.hitAt, 0xff, static_cast<size_t>(p.maxItems) * sizeof(int), st);
     mark(0);
-    k_trace_primary<R, ST, 0, 0><<<cap > 0 ? min(cap, b1) : b1, kWaveThreads, 0, st>>>(p);
+    launchPrimary<R, ST, 0, 0>(p, cap, st);
     mark(1);
-    k_trace_primary<R, ST, 0, 1><<<cap > 0 ? min(cap, b1f) : b1f, kWaveThreads, 0, st>>>(p);
+    launchPrimary<R, ST, 0, 1>(p, cap, st);
     mark(2);
     compact_hits(p.hitAt, p.hitList, p.ctr + kCtrHits, static_cast<int>(p.maxItems), p.selTemp, p.selTempBytes, st);
     k_hit_normals<R><<<b3, 128, 0, st>>>(p);
@@ -1191,9 +1260,9 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
     // (stats + kShadowStats), so the work of K1 and K2 can be told apart
     WaveParams<R> p2 = p;
     if (ST) p2.stats = p.stats + kShadowStats;
-    k_trace_shadow<R, ST, 0><<<cap > 0 ? min(cap, b2) : b2, kWaveThreads, 0, st>>>(p2);
+    launchShadow<R, ST, 0>(p2, cap, st);
     mark(4);
-    k_trace_shadow<R, ST, 1><<<cap > 0 ? min(cap, b2f) : b2f, kWaveThreads, 0, st>>>(p2);
+    launchShadow<R, ST, 1>(p2, cap, st);
     mark(5);
     if (p.debug) {
         k_shade_rays<R, ST, false><<<b3d, 128, 128 * kMvcSlab * sizeof(R), st>>>(p);
@@ -1264,18 +1333,14 @@ template <typename R, bool ST>
 static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long* launches) {
     cudaMemsetAsync(p.ctr, 0, (kLightCtr + (p.scene.n_lights > 1 ? p.scene.n_lights : 1)) * sizeof(unsigned long long), st);
     if (p.cray) k_contact_setup<R><<<static_cast<int>((p.nRaysDirect + 255) / 256), 256, 0, st>>>(p);
-    static int b1 = persistentBlocks(k_trace_primary<R, ST, 1, 0>, kWaveThreads, 0);
-    static int b1f = persistentBlocks(k_trace_primary<R, ST, 1, 1>, kWaveThreads, 0);
-    static int b2 = persistentBlocks(k_trace_shadow<R, ST, 0>, kWaveThreads, 0);
-    static int b2f = persistentBlocks(k_trace_shadow<R, ST, 1>, kWaveThreads, 0);
     static int b3 = persistentBlocks(k_shade_rays<R, ST, true>, 128, 0);
     static int b3c = persistentBlocks(k_shade_mvc<R, ST>, kMvcThreads, 0, kMvcThreads * kMvcSlab * sizeof(R));
-    k_trace_primary<R, ST, 1, 0><<<b1, kWaveThreads, 0, st>>>(p);
-    k_trace_primary<R, ST, 1, 1><<<b1f, kWaveThreads, 0, st>>>(p);
+    launchPrimary<R, ST, 1, 0>(p, 0, st);
+    launchPrimary<R, ST, 1, 1>(p, 0, st);
     compact_hits(p.hitAt, p.hitList, p.ctr + kCtrHits, static_cast<int>(p.maxItems), p.selTemp, p.selTempBytes, st);
     k_hit_normals<R><<<b3, 128, 0, st>>>(p);
-    k_trace_shadow<R, ST, 0><<<b2, kWaveThreads, 0, st>>>(p);
-    k_trace_shadow<R, ST, 1><<<b2f, kWaveThreads, 0, st>>>(p);
+    launchShadow<R, ST, 0>(p, 0, st);
+    launchShadow<R, ST, 1>(p, 0, st);
     k_shade_rays<R, ST, true><<<b3, 128, 0, st>>>(p);
     k_shade_mvc<R, ST><<<b3c, kMvcThreads, kMvcThreads * kMvcSlab * sizeof(R), st>>>(p);
     const long long np = static_cast<long long>(p.gw) * p.gh;
@@ -1344,11 +1409,9 @@ static void composeWavefront(const WaveParams<R>& p, cudaStream_t st, long long*
     cudaMemsetAsync(p.ctr, 0, (kLightCtr + (p.scene.n_lights > 1 ? p.scene.n_lights : 1)) * sizeof(unsigned long long), st);
     const long long np = static_cast<long long>(p.gw) * p.gh;
     const int blocks = static_cast<int>((np + 127) / 128);
-    static int b2 = persistentBlocks(k_trace_shadow<R, ST, 0>, kWaveThreads, 0);
-    static int b2f = persistentBlocks(k_trace_shadow<R, ST, 1>, kWaveThreads, 0);
     k_compose_setup<R><<<blocks, 128, 0, st>>>(p);
-    k_trace_shadow<R, ST, 0><<<b2, kWaveThreads, 0, st>>>(p);
-    k_trace_shadow<R, ST, 1><<<b2f, kWaveThreads, 0, st>>>(p);
+    launchShadow<R, ST, 0>(p, 0, st);
+    launchShadow<R, ST, 1>(p, 0, st);
     k_compose<R><<<blocks, 128, 0, st>>>(p);
     if (launches) *launches += 4;
 }
@@ -1368,29 +1431,37 @@ void launch_batch(const WaveParams<R>& p, int kind, bool stats, cudaStream_t st,
     if (kind == 0) {
         cudaMemsetAsync(p.ctr, 0, (kLightCtr + L) * sizeof(unsigned long long), st);
         cudaMemsetAsync(p.hitAt, 0xff, static_cast<size_t>(p.maxItems) * sizeof(int), st);
-        auto k0 = stats ? k_trace_primary<R, true, 1, 0> : k_trace_primary<R, false, 1, 0>;
-        auto k1 = stats ? k_trace_primary<R, true, 1, 1> : k_trace_primary<R, false, 1, 1>;
-        const int b1 = persistentBlocks(k0, kWaveThreads, 0), b1f = persistentBlocks(k1, kWaveThreads, 0);
-        k0<<<b1, kWaveThreads, 0, st>>>(p);
-        k1<<<b1f, kWaveThreads, 0, st>>>(p);
+        if (stats) {
+            launchPrimary<R, true, 1, 0>(p, 0, st);
+            launchPrimary<R, true, 1, 1>(p, 0, st);
+        } else {
+            launchPrimary<R, false, 1, 0>(p, 0, st);
+            launchPrimary<R, false, 1, 1>(p, 0, st);
+        }
         compact_hits(p.hitAt, p.hitList, p.ctr + kCtrHits, static_cast<int>(p.maxItems), p.selTemp, p.selTempBytes,
                      st);
         k_hit_normals<R><<<persistentBlocks(k_hit_normals<R>, 128, 0), 128, 0, st>>>(p);
         if (launches) *launches += 4;
     } else if (kind == 1) {
-        auto k0 = stats ? k_trace_shadow<R, true, 0> : k_trace_shadow<R, false, 0>;
-        auto k1 = stats ? k_trace_shadow<R, true, 1> : k_trace_shadow<R, false, 1>;
-        k0<<<persistentBlocks(k0, kWaveThreads, 0), kWaveThreads, 0, st>>>(p);
-        k1<<<persistentBlocks(k1, kWaveThreads, 0), kWaveThreads, 0, st>>>(p);
+        if (stats) {
+            launchShadow<R, true, 0>(p, 0, st);
+            launchShadow<R, true, 1>(p, 0, st);
+        } else {
+            launchShadow<R, false, 0>(p, 0, st);
+            launchShadow<R, false, 1>(p, 0, st);
+        }
         if (launches) *launches += 2;
     } else {
-        auto k0 = stats ? k_trace_shadow<R, true, 0> : k_trace_shadow<R, false, 0>;
-        auto k1 = stats ? k_trace_shadow<R, true, 1> : k_trace_shadow<R, false, 1>;
         auto ka = stats ? k_shade_rays<R, true, true> : k_shade_rays<R, false, true>;
         auto kc = stats ? k_shade_mvc<R, true> : k_shade_mvc<R, false>;
         k_hit_normals<R, false><<<persistentBlocks(k_hit_normals<R, false>, 128, 0), 128, 0, st>>>(p);
-        k0<<<persistentBlocks(k0, kWaveThreads, 0), kWaveThreads, 0, st>>>(p);
-        k1<<<persistentBlocks(k1, kWaveThreads, 0), kWaveThreads, 0, st>>>(p);
+        if (stats) {
+            launchShadow<R, true, 0>(p, 0, st);
+            launchShadow<R, true, 1>(p, 0, st);
+        } else {
+            launchShadow<R, false, 0>(p, 0, st);
+            launchShadow<R, false, 1>(p, 0, st);
+        }
         ka<<<persistentBlocks(ka, 128, 0), 128, 0, st>>>(p);
         kc<<<persistentBlocks(kc, kMvcThreads, 0, kMvcThreads * kMvcSlab * sizeof(R)), kMvcThreads,
              kMvcThreads * kMvcSlab * sizeof(R), st>>>(p);

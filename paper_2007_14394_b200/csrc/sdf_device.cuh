@@ -169,6 +169,11 @@ template <typename R> struct SceneView {
     double sky[3];
     GridDev grid;
     int useGrid;
+    // the primitive records in the layout the tracing kernels stage in shared memory
+    // (stageBytes == 0: the scene does not fit and the kernels read `prims`)
+    const void* __restrict__ stage;
+    int stageBytes;
+    int stageRotOff;  // FP64: byte offset of the rotation rows (8 doubles per rotated primitive)
 };
 
 // TraceStats (scene.hpp:16-36), per thread.
@@ -289,6 +294,62 @@ __device__ __forceinline__ float evalPrim<float>(const DPrim<float>& pr, V3<floa
     return pr.rr < 0.f ? qz : d;
 }
 
+// Primitive records staged in shared memory by the tracing kernels (stagePrims).
+// FP64: per primitive the first 64 B of DPrim<double> (translation, size, kind, and
+// rot[0]) with the identity flag replaced by the index of its rotation row (-1:
+// identity), the rows rot[1..8] (64 B each) after the records; the arithmetic is
+// evalPrim<double>'s, so the values are bit-identical. FP32: DPrim<float> as is.
+extern __shared__ __align__(128) unsigned char sdfgiDynSmem[];
+__device__ __forceinline__ double evalPrimStaged(const unsigned char* base, int rotOff, int j, V3<double> p) {
+    const double2* v = reinterpret_cast<const double2*>(base + 64 * static_cast<size_t>(j));
+    const double2 a0 = v[0], a1 = v[1], a2 = v[2];
+    const int4 a3 = *reinterpret_cast<const int4*>(v + 3);
+    const double size0 = a1.y, size1 = a2.x, size2 = a2.y;
+    V3<double> q = p - mk(a0.x, a0.y, a1.x);
+    if (a3.y >= 0) {  // transposeMul, vec.hpp:113-117
+        const double m0 = __hiloint2double(a3.w, a3.z);
+        const double2* r = reinterpret_cast<const double2*>(base + rotOff + 64 * static_cast<size_t>(a3.y));
+        const double2 r12 = r[0], r34 = r[1], r56 = r[2], r78 = r[3];
+        q = mk(m0 * q.x + r34.x * q.y + r56.y * q.z, r12.x * q.x + r34.y * q.y + r78.x * q.z,
+               r12.y * q.x + r56.x * q.y + r78.y * q.z);
+    }
+    const int kind = a3.x;
+    if (kind == 2) return q.z;  // plane
+    double vx, vy, vz, post;
+    if (kind == 1) {  // box
+        const double ax = fabs(q.x) - size0, ay = fabs(q.y) - size1, az = fabs(q.z) - size2;
+        vx = smax(ax, 0.0);
+        vy = smax(ay, 0.0);
+        vz = smax(az, 0.0);
+        post = smin(smax(ax, smax(ay, az)), 0.0);
+    } else if (kind == 3) {  // cylinder
+        const double dx = sqrt(q.x * q.x + q.y * q.y) - size0, dy = fabs(q.z) - size1;
+        vx = smax(dx, 0.0);
+        vy = smax(dy, 0.0);
+        vz = 0.0;
+        post = smin(smax(dx, dy), 0.0);
+    } else {  // sphere (0) / capsule (4)
+        vx = q.x;
+        vy = q.y;
+        vz = kind == 0 ? q.z : q.z - sclamp(q.z, -size1, size1);
+        post = -size0;
+    }
+    return sqrt(vx * vx + vy * vy + vz * vz) + post;
+}
+// evalPrimitive of CSR primitive j: from the shared-memory copy in kernels that
+// staged it (STG), else from global memory.
+template <typename R, bool STG>
+__device__ __forceinline__ R evalPrimAt(const SceneView<R>& s, int j, V3<R> p) {
+    if constexpr (STG) {
+        if constexpr (sizeof(R) == 8)
+            return evalPrimStaged(sdfgiDynSmem, s.stageRotOff, j, p);
+        else
+            return evalPrim(reinterpret_cast<const DPrim<float>*>(sdfgiDynSmem)[j], p);
+    } else {
+        return evalPrim(s.prims[j], p);
+    }
+}
+
 // evalGradientDetailed / evalGradient, primitives.hpp:96-108 (h = 1e-3)
 template <typename R>
 __device__ __forceinline__ V3<R> evalGradient(const DPrim<R>& pr, V3<R> p) {
@@ -323,7 +384,7 @@ __device__ __forceinline__ bool clusterSkipped(const DCluster<R>& cl, V3<R> p, R
 // Members of one visited cluster: in order with the reference's strict `<`
 // (TIE = false), or with the explicit lowest-CSR-position tie-break (TIE = true)
 // when clusters are visited out of order.
-template <typename R, bool ST, bool TIE>
+template <typename R, bool ST, bool TIE, bool STG = false>
 __device__ __forceinline__ void visitMembers(const SceneView<R>& s, int k, V3<R> p, R& d, int& own, Counters* c) {
     const int b = s.cstart[k], e = s.cstart[k + 1];
     if (ST) {
@@ -335,7 +396,7 @@ __device__ __forceinline__ void visitMembers(const SceneView<R>& s, int k, V3<R>
             ++c->ek[s.kindId[j] & 0xff];
             c->ek[5] += (s.kindId[j] >> 8) ? 0 : 1;
         }
-        const R pd = evalPrim(s.prims[j], p);
+        const R pd = evalPrimAt<R, STG>(s, j, p);
         if (pd < d || (TIE && pd == d && own >= 0 && j < own)) {
             d = pd;
             own = j;
@@ -381,11 +442,11 @@ __device__ __forceinline__ bool boxReaches(R boxSq, R d) {
 // with p rounded to float, the float box distance is within walkSlack of the exact
 // one, so a subtree is kept whenever dist - walkSlack <= d. That keeps every
 // subtree the exact test keeps (and a few more): the walk stays exact.
-template <typename R, bool ST>
+template <typename R, bool ST, bool STG = false>
 __device__ __forceinline__ void hierarchyWalk(const SceneView<R>& s, QueryState<R>& q, Counters* c) {
     const GridDev& g = s.grid;
     const V3<R> p = q.p;
-    for (int i = 0; i < g.nUnbounded; ++i) visitMembers<R, ST, true>(s, g.unbounded[i], p, q.d, q.own, c);
+    for (int i = 0; i < g.nUnbounded; ++i) visitMembers<R, ST, true, STG>(s, g.unbounded[i], p, q.d, q.own, c);
     if (g.nBounded == 0) return;
     if constexpr (sizeof(R) == 8) {
         // FP64: float box tests with the slack (keep iff |p - box| <= max(d, 0) + slack)
@@ -417,7 +478,7 @@ __device__ __forceinline__ void hierarchyWalk(const SceneView<R>& s, QueryState<
                 }
                 if (ST) c->cs += 2;
             } else {
-                visitMembers<R, ST, true>(s, -next - 1, p, q.d, q.own, c);
+                visitMembers<R, ST, true, STG>(s, -next - 1, p, q.d, q.own, c);
             }
             bool more = false;
             while (sp > 0) {
@@ -455,7 +516,7 @@ __device__ __forceinline__ void hierarchyWalk(const SceneView<R>& s, QueryState<
             }
             if (ST) c->cs += 2;
         } else {
-            visitMembers<R, ST, true>(s, -next - 1, p, q.d, q.own, c);
+            visitMembers<R, ST, true, STG>(s, -next - 1, p, q.d, q.own, c);
         }
         // pop the nearest pending subtree still within reach
         bool more = false;
@@ -555,7 +616,7 @@ __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R ini
 // entry loaded while the current candidate is evaluated. A truncated list ends in
 // a sentinel (-1) whose bound covers every omitted candidate; a query still open
 // there completes through the cluster hierarchy.
-template <typename R, bool ST>
+template <typename R, bool ST, bool STG = false>
 __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int* owner, Counters* c, int seed = -1,
                                    int cellHint = kCellUnknown, R rHint = R(0), CellCache* cache = nullptr) {
     QueryState<R> q;
@@ -568,7 +629,7 @@ __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int*
             ++c->ek[s.kindId[seed] & 0xff];
             c->ek[5] += (s.kindId[seed] >> 8) ? 0 : 1;
         }
-        const R pd = evalPrim(s.prims[seed], p);
+        const R pd = evalPrimAt<R, STG>(s, seed, p);
         if (pd < q.d || (pd == q.d && q.own >= 0 && seed < q.own)) {
             q.d = pd;
             q.own = seed;
@@ -591,7 +652,7 @@ __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int*
                 ++c->ek[s.kindId[j] & 0xff];
                 c->ek[5] += (s.kindId[j] >> 8) ? 0 : 1;
             }
-            const R pd = evalPrim(s.prims[j], q.p);
+            const R pd = evalPrimAt<R, STG>(s, j, q.p);
             if (pd < q.d || (pd == q.d && q.own >= 0 && j < q.own)) {
                 q.d = pd;
                 q.own = j;
@@ -600,7 +661,7 @@ __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int*
             e = en;
         }
     }
-    if (q.walk) hierarchyWalk<R, ST>(s, q, c);
+    if (q.walk) hierarchyWalk<R, ST, STG>(s, q, c);
     if (owner) *owner = q.own;
     return q.d;
 }

@@ -129,6 +129,10 @@ struct Ctx {
     double sky[3] = {0, 0, 0};
     DBuf<DPrim<double>> prim64;
     DBuf<DPrim<float>> prim32;
+    // the records K1/K2 stage in shared memory (evalPrimStaged); 0 bytes: the scene
+    // does not fit (or SDFGI_STAGE=0) and they read prim64 / prim32
+    DBuf<unsigned char> stage64;
+    int stage64Bytes = 0, stage64RotOff = 0, stage32Bytes = 0;
     DBuf<DCluster<double>> cl64;
     DBuf<DCluster<float>> cl32;
     DBuf<int> cstart, orig;
@@ -218,7 +222,7 @@ struct Ctx {
     ~Ctx() {
         cudaSetDevice(device);
         if (stream) cudaStreamSynchronize(stream);
-        prim64.free(); prim32.free(); cl64.free(); cl32.free(); cstart.free(); orig.free();
+        prim64.free(); prim32.free(); stage64.free(); cl64.free(); cl32.free(); cstart.free(); orig.free();
         albedo.free(); emission.free(); lights.free(); kindId.free();
         gridStart.free(); gridList.free(); gridCounts.free(); gridU.free(); gridEntry.free(); gridCell.free(); brickCounts.free(); brickStart.free(); brickList.free(); brickSeed.free(); scanTemp.free();
         bvh.free(); unbList.free(); primBox.free();
@@ -296,6 +300,9 @@ SceneView<double> Ctx::sceneView<double>() const {
     for (int k = 0; k < 3; ++k) v.sky[k] = sky[k];
     v.grid = grid;
     v.useGrid = (accel && haveGrid) ? 1 : 0;
+    v.stage = stage64.p;
+    v.stageBytes = stage64Bytes;
+    v.stageRotOff = stage64RotOff;
     return v;
 }
 template <>
@@ -315,6 +322,9 @@ SceneView<float> Ctx::sceneView<float>() const {
     for (int k = 0; k < 3; ++k) v.sky[k] = sky[k];
     v.grid = grid;
     v.useGrid = (accel && haveGrid) ? 1 : 0;
+    v.stage = prim32.p;
+    v.stageBytes = stage32Bytes;
+    v.stageRotOff = 0;
     return v;
 }
 
@@ -1133,6 +1143,38 @@ int sdfgi_scene_upload(void* ctx, const sdfgi_prim* prims, int n_prims, const sd
         c->emission.upload(em.data(), em.size(), c->stream);
         c->kindId.upload(kid.data(), kid.size(), c->stream);
         c->lights.upload(reinterpret_cast<const DLight*>(lights), n_lights, c->stream);
+        // shared-memory staging of the primitive records for K1/K2 (evalPrimStaged):
+        // FP64 64 B per primitive + 64 B per rotation row, FP32 the 64 B records as is
+        {
+            int optin = 0;
+            CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+            const long long limit = static_cast<long long>(optin) - 1024;  // the kernels' static shared memory
+            const char* senv = std::getenv("SDFGI_STAGE");
+            const bool allow = !(senv && std::atoi(senv) == 0) && nMembers > 0;
+            std::vector<unsigned char> st(64 * static_cast<size_t>(nMembers));
+            std::vector<unsigned char> rows;
+            for (int j = 0; j < nMembers; ++j) {
+                unsigned char* r = st.data() + 64 * static_cast<size_t>(j);
+                std::memcpy(r, &p64[j], 64);
+                int rotIdx = -1;
+                if (!p64[j].identity) {
+                    rotIdx = static_cast<int>(rows.size() / 64);
+                    const unsigned char* src = reinterpret_cast<const unsigned char*>(&p64[j]) + 64;
+                    rows.insert(rows.end(), src, src + 64);
+                }
+                std::memcpy(r + 52, &rotIdx, 4);  // the identity flag's slot
+            }
+            const long long b64 = static_cast<long long>(st.size() + rows.size());
+            c->stage64Bytes = 0;
+            if (allow && b64 <= limit) {
+                st.insert(st.end(), rows.begin(), rows.end());
+                c->stage64.upload(st.data(), st.size(), c->stream);
+                c->stage64Bytes = static_cast<int>(b64);
+                c->stage64RotOff = 64 * nMembers;
+            }
+            const long long b32 = 64LL * nMembers;
+            c->stage32Bytes = (allow && b32 <= limit) ? static_cast<int>(b32) : 0;
+        }
         CK(cudaStreamSynchronize(c->stream));
         c->nPrims = nMembers;
         c->nClusters = n_clusters;
