@@ -71,6 +71,13 @@ template <typename R> struct __align__(16) ParkRay {
     int seed;  // last known nearest primitive (query seed of the far phase)
     int item;  // the ray's position in the trace order (its hitAt slot)
 };
+// A probe ray prepared by k_probe_ray_setup: origin (the probe), direction and its
+// ray id, in trace order.
+template <typename R> struct __align__(16) ProbeRay {
+    R o[3], dir[3];
+    int rid;
+    int _pad;
+};
 // A Contact GI ray prepared by k_contact_setup (tMax < 0: sky pixel, no ray).
 template <typename R> struct __align__(16) ContactRay {
     R o[3], dir[3];
@@ -136,6 +143,7 @@ template <typename R> struct WaveParams {
     void* park;
     unsigned long long parkBytes;
     void* cray;  // contact batch: the prepared rays (ContactRay<R>)
+    void* pray;  // probe batch: the prepared rays (ProbeRay<R>) in trace order
     const double* clocal;  // contact batch: cosineHemisphereDir's (lx, ly) per (pixel, sample), host libm
     // the traced shadow marches, light li's at [li * srayCap, + ctr[kLightCtr + li])
     ShadowRay<R>* sray;

@@ -324,6 +324,35 @@ __global__ void __launch_bounds__(256) k_contact_setup(WaveParams<R> P) {
     stStream(reinterpret_cast<ContactRay<R>*>(P.cray) + i, r);
 }
 
+// Every probe ray's set-up at full lane occupancy, ahead of K1 (in K1 only the few
+// refilling lanes of a warp would run it): trace-order item -> its probe (the
+// candidate of its 32-ray chunk, then a step or two), its Fibonacci sample
+// (coherent order perm), ray id rayStart + sample, origin = the probe, direction =
+// rot * sphericalFibonacci (sampling.hpp:28).
+template <typename R>
+__global__ void __launch_bounds__(256) k_probe_ray_setup(WaveParams<R> P) {
+    const long long item = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (item >= P.rayStart[P.nCand]) return;
+    int s = P.chunkSlot[item >> 5];
+    while (P.rayStart[s + 1] <= item) ++s;
+    const int j = static_cast<int>(item - P.rayStart[s]);
+    const int n = static_cast<int>(P.rayStart[s + 1] - P.rayStart[s]);
+    const int i = P.perm[(n == P.nRaysFull ? 0 : P.nRaysFull) + j];
+    const int g = P.cand ? P.cand[s] : s;
+    const double* pp = P.pc.probes.pos + 3 * static_cast<size_t>(g);
+    const V3<double> dd = rayDirection(P, s, i, n);
+    ProbeRay<R> r;
+    r.o[0] = R(pp[0]);
+    r.o[1] = R(pp[1]);
+    r.o[2] = R(pp[2]);
+    r.dir[0] = R(dd.x);
+    r.dir[1] = R(dd.y);
+    r.dir[2] = R(dd.z);
+    r.rid = static_cast<int>(P.rayStart[s] + i);
+    r._pad = 0;
+    stStream(reinterpret_cast<ProbeRay<R>*>(P.pray) + item, r);
+}
+
 // Warp-aggregated slot in a parking buffer (all 32 lanes call; -1 = not parked).
 __device__ __forceinline__ long long parkSlot(unsigned long long* counter, bool park) {
     const unsigned m = __ballot_sync(kFull, park);
@@ -432,28 +461,17 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
         } else {
             const bool got =
                 fetchItem(P.ctr + kCtrRay, static_cast<unsigned long long>(total), active, exhausted, item, chunk);
-            int s = 0;
-            if (MODE == 0 && got) {
-                // the item's probe: the candidate of its 32-ray chunk, then a step or two
-                s = P.chunkSlot[item >> 5];
-                while (P.rayStart[s + 1] <= static_cast<long long>(item)) ++s;
-            }
             if (got) {
             titem = static_cast<int>(item);
             R startBound = R(INFINITY);
             bool ok = true;
             if (MODE == 0) {
-                const int j = static_cast<int>(static_cast<long long>(item) - P.rayStart[s]);
-                const int n = static_cast<int>(P.rayStart[s + 1] - P.rayStart[s]);
-                // slot j traces sample i = perm[j]: consecutive lanes get neighbouring
-                // directions (coherent warps); results are stored by sample index
-                const int i = P.perm[(n == P.nRaysFull ? 0 : P.nRaysFull) + j];
-                rid = static_cast<unsigned long long>(P.rayStart[s] + i);
-                const int g = P.cand ? P.cand[s] : s;
-                const double* pp = P.pc.probes.pos + 3 * static_cast<size_t>(g);
-                V3<double> dd = rayDirection(P, s, i, n);
-                o = mk(R(pp[0]), R(pp[1]), R(pp[2]));
-                dir = mk(R(dd.x), R(dd.y), R(dd.z));
+                // prepared by k_probe_ray_setup (trace order: consecutive lanes get
+                // neighbouring directions; results are stored by ray id)
+                const ProbeRay<R> r = ldStream(reinterpret_cast<const ProbeRay<R>*>(P.pray) + item);
+                rid = static_cast<unsigned long long>(r.rid);
+                o = mk(r.o[0], r.o[1], r.o[2]);
+                dir = mk(r.dir[0], r.dir[1], r.dir[2]);
                 tMax = R(P.tc.rayTMax);
             } else {
                 rid = item;
@@ -1242,6 +1260,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
     k_ray_setup<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
     k_ray_scan<R><<<1, kScanThreads, 0, st>>>(p);
     k_ray_chunks<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
+    k_probe_ray_setup<R><<<static_cast<int>((p.maxItems + 255) / 256), 256, 0, st>>>(p);
     cudaMemsetAsync(p.ctr, 0, (kLightCtr + (p.scene.n_lights > 1 ? p.scene.n_lights : 1)) * sizeof(unsigned long long), st);
     static int b3 = persistentBlocks(k_shade_rays<R, ST, true>, 128, 0);
     static int b3d = persistentBlocks(k_shade_rays<R, ST, false>, 128, 0, 128 * kMvcSlab * sizeof(R));
@@ -1282,7 +1301,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
         k3<<<p.nCand, kConvThreads, smem, st>>>(p);
     }
     mark(7);
-    if (launches) *launches += p.debug ? 10 : 12;
+    if (launches) *launches += p.debug ? 11 : 13;
 }
 
 // contactGI's per-pixel sum (shading.hpp:686-713): AO from the missed samples,

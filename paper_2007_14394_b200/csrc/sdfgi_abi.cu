@@ -203,7 +203,7 @@ struct Ctx {
     DBuf<double> cLocal;
     uint64_t cLocalSeed = 0;
     int cLocalW = 0, cLocalH = 0, cLocalS = -1;
-    DBuf<unsigned char> wHits, wVis, wRad, wPark, wCRay, wSRay, wSelTemp;
+    DBuf<unsigned char> wHits, wVis, wRad, wPark, wCRay, wPRay, wSRay, wSelTemp;
     DBuf<unsigned long long> wCtr;
     int persistCap = 0;  // 0 = occupancy-sized persistent grids
     // gather (e): G-buffer, stage buffers, history (pipeline.hpp:213-218)
@@ -231,7 +231,7 @@ struct Ctx {
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
         wRayCount.free(); wHitList.free(); wMvcList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); wQuat.free(); cLocal.free(); wHits.free();
         if (hQuat) cudaFreeHost(hQuat);
-        wVis.free(); wPark.free(); wCRay.free(); wSRay.free(); wCtr.free(); perm.free(); wRad.free();
+        wVis.free(); wPark.free(); wCRay.free(); wPRay.free(); wSRay.free(); wCtr.free(); perm.free(); wRad.free();
         gbuf.free(); halfDepth.free(); sparseIrr.free(); resolved.free(); indirect.free(); histIrr.free(); composed.free();
         histDepth.free(); halfSrc.free(); sel.free(); sparseValid.free(); sparseAnchor.free();
         for (auto& e : gev)
@@ -847,6 +847,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     reserve(c->wCtr, kLightCtr + L);
     reservePark<R>(c, maxRays, L);
     reserve(c->wSRay, std::max<size_t>(maxRays, 1) * L * sizeof(ShadowRay<R>));
+    reserve(c->wPRay, std::max<size_t>(maxRays, 1) * sizeof(ProbeRay<R>));
     if (c->fibN != N) {
         // sphericalFibonacci tables for n = N and 2N from the host's libm (host_trig.h)
         std::vector<double> fib(9 * static_cast<size_t>(N));
@@ -872,6 +873,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.chunkSlot = c->wChunk.p;
     p.rot = c->wRot.p;
     p.quat = c->wQuat.p;
+    p.pray = c->wPRay.p;
     p.fib = c->fib.p;
     p.perm = c->perm.p;
     p.nRaysDirect = -1;  // probe batch: ray count from the K0 prefix sum
