@@ -144,6 +144,10 @@ template <typename R> struct WaveParams {
     unsigned long long parkBytes;
     void* cray;  // contact batch: the prepared rays (ContactRay<R>)
     void* pray;  // probe batch: the prepared rays (ProbeRay<R>) in trace order
+    // accel mode 2: a march whose point leaves the candidate grid (which holds every
+    // bounded primitive) after starting inside it can never converge again (the grid
+    // box is convex, no unbounded primitive): K1 ends it as a miss on the spot
+    int escape;
     const double* clocal;  // contact batch: cosineHemisphereDir's (lx, ly) per (pixel, sample), host libm
     // the traced shadow marches, light li's at [li * srayCap, + ctr[kLightCtr + li])
     ShadowRay<R>* sray;

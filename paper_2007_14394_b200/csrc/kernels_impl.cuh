@@ -436,6 +436,7 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
     int step = 0, state = 0, pol = 0, owner = -1, seed = -1;
     int titem = 0;       // the ray's trace-order position (its hitAt slot)
     bool fresh = false;  // resumed march: its pending t += d was applied before parking
+    bool originIn = false;  // the ray starts inside the candidate grid (escape test)
     while (true) {
         __syncwarp();
         unsigned long long item;
@@ -489,6 +490,7 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
             owner = -1;
             seed = -1;
             active = ok;
+            originIn = P.escape && ok && gridCell<R>(P.scene.grid, o) >= 0;
             if (!ok) {  // sky pixel of a contact batch: no ray (the combine skips it)
                 HitRec<R> h;
                 h.p[0] = h.p[1] = h.p[2] = R(0);
@@ -524,7 +526,7 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
         }
         V3<R> p = o;
         R initD = R(0);
-        bool parkIt = false;
+        bool parkIt = false, escaped = false;
         int cell = kCellUnknown;  // phase 0: p's cell (parking test), reused by the query
         R cellR = R(0);
         if (active) {
@@ -532,8 +534,11 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
             fresh = false;
             p = o + dir * t;
             if (PHASE == 0 && P.scene.useGrid) cell = gridCell<R>(P.scene.grid, p, &cellR);
-            parkIt = PHASE == 0 && park && cell < 0;
-            if (parkIt) {
+            escaped = PHASE == 0 && originIn && state == 0 && cell < 0;
+            parkIt = PHASE == 0 && park && cell < 0 && !escaped;
+            if (escaped) {
+                if (ST) ++cnt.steps;
+            } else if (parkIt) {
             } else if (state == 0) {
                 if (ST) ++cnt.steps;
                 initD = marchSeed(P.scene, lastD, tMax - t, eps);
@@ -581,13 +586,15 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
         }
         int o2 = -1;
         R nd = R(0);
-        if (active)
+        if (active && !escaped)
             nd = query<R, ST, STG>(P.scene, p, initD, &o2, &cnt, PHASE ? seed : -1, cell, cellR,
                               useCellCache<R>() ? &ccache : nullptr);
         if (active) {
             if (o2 >= 0) seed = o2;
             int done = 0;  // 1 converged, 2 TMax, 3 StepLimit
-            if (state == 0) {
+            if (escaped) {
+                done = 2;  // left the grid box for good: a miss (sky either way)
+            } else if (state == 0) {
                 if (nd < eps) {
                     d = nd;
                     state = 1;

@@ -140,7 +140,9 @@ struct Ctx {
     DBuf<int> kindId;
     DBuf<DLight> lights;
     // candidate-cluster grid (GridDev, sdf_device.cuh)
-    int accel = 1;
+    // 0 the reference's flat cluster walk (exact TraceStats), 1 the candidate grid
+    // (exact march sequence), 2 (default) grid + escaped marches ended early
+    int accel = 2;
     bool haveGrid = false;
     GridDev grid{};
     long long gridEntries = 0;
@@ -830,6 +832,11 @@ void reserveHitAt(Ctx* c, WaveParams<R>& p, size_t n) {
     p.maxItems = static_cast<long long>(n);
 }
 
+// accel mode 2's escape test (WaveParams::escape) holds when the candidate grid
+// exists and the scene has no unbounded primitive (a plane can be reached from
+// anywhere outside the grid box)
+int escapeOk(const Ctx* c) { return (c->accel == 2 && c->haveGrid && c->grid.nUnbounded == 0) ? 1 : 0; }
+
 template <typename R>
 WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand) {
     const int N = static_cast<int>(cfg->n_rays_full);
@@ -891,6 +898,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.prevAtlas = c->atlas[c->front].p;
     p.currAtlas = c->atlas[1 - c->front].p;
     p.prevZero = c->frontZero() ? 1 : 0;
+    p.escape = escapeOk(c);
     p.oct = c->octRes;
     p.frame = frame;
     p.tc.eps = cfg->surface_epsilon;
@@ -1199,7 +1207,7 @@ int sdfgi_scene_upload(void* ctx, const sdfgi_prim* prims, int n_prims, const sd
             const char* v = std::getenv(k);  // the grid's build parameters
             mix(v ? v : "-", v ? std::strlen(v) : 1);
         }
-        const bool same = c->haveGrid && c->gridHash == hsh && c->gridAccel == c->accel;
+        const bool same = c->haveGrid && c->gridHash == hsh && (c->gridAccel != 0) == (c->accel != 0);
         c->hPrims.assign(prims, prims + n_prims);
         c->hMember.assign(member_idx, member_idx + nMembers);
         c->hClusters.assign(clusters, clusters + n_clusters);
@@ -1621,11 +1629,13 @@ int sdfgi_probes_trace_debug(void* ctx, const int32_t* probe_refs, int n_refs, i
             WaveParams<double> p = waveParams<double>(c, cfg, frame, c->refs.p, n_refs);
             p.records = c->records.p;
             p.debug = 1;
+            p.escape = 0;  // per-ray records: the exact march (miss reason, steps)
             launch_wavefront<double>(p, c->persistCap, false, c->stream, nullptr, &c->launches);
         } else {
             WaveParams<float> p = waveParams<float>(c, cfg, frame, c->refs.p, n_refs);
             p.records = c->records.p;
             p.debug = 1;
+            p.escape = 0;
             launch_wavefront<float>(p, c->persistCap, false, c->stream, nullptr, &c->launches);
         }
         CK(cudaGetLastError());
@@ -1729,7 +1739,7 @@ int sdfgi_measure_fp_peak(void* ctx, double* f64_fma_per_s, double* f32_fma_per_
 int sdfgi_set_accel(void* ctx, int mode) {
     return guard([&] {
         Ctx* c = C(ctx);
-        REQ(mode == 0 || mode == 1, SDFGI_ERR_INVALID, "accel mode must be 0 or 1");
+        REQ(mode >= 0 && mode <= 2, SDFGI_ERR_INVALID, "accel mode must be 0, 1 or 2");
         c->accel = mode;
     });
 }
@@ -1842,6 +1852,10 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     p.park = c->accel && c->haveGrid && c->wPark.n >= 4096 ? c->wPark.p : nullptr;  // SDFGI_PARK_MB=0: off
     p.parkBytes = p.park ? c->wPark.n : 0;
     p.stats = c->scratch.p + 32;  // contact counters: scratch[32..], the visibility ones stay at [0..]
+    // short rays: neither the escape test nor the shared-memory primitive copy pays
+    // off here (measured: contact +2.5% / +3% each, scripts/time_gather.py)
+    p.escape = 0;
+    p.scene.stageBytes = 0;
     p.nRaysDirect = nr;
     p.cray = c->wCRay.p;
     p.clocal = c->cLocal.p;
@@ -1892,6 +1906,7 @@ WaveParams<R> composeParams(Ctx* c, const sdfgi_cfg* cfg) {
     p.gh = c->gh;
     p.resolved = c->indirect.p;  // input: the indirect image
     p.composed = c->composed.p;
+    p.scene.stageBytes = 0;  // measured slower for the compose shadow rays (+2%)
     return p;
 }
 

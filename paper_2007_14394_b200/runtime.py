@@ -261,7 +261,10 @@ class Device:
         return a.value, b.value
 
     def set_accel(self, mode: int):
-        """0: reference flat cluster walk (exact TraceStats); 1: candidate grid (default)."""
+        """0: the reference's flat cluster walk (exact TraceStats); 1: candidate grid (the
+        exact march sequence, query counts equal to the reference's); 2 (default): grid,
+        and marches that leave the grid box for good end as misses at once (outputs
+        unchanged, fewer queries)."""
         _call("sdfgi_set_accel", self._ctx, int(mode))
 
     def accel_info(self):

@@ -7,7 +7,9 @@ from paper_2007_14394_b200.runtime import Device  # noqa: E402
 
 prec = sys.argv[1] if len(sys.argv) > 1 else "f64"
 scene = scene_io.read_sdfs("paper_2007_14394_b200/data/c2.sdfs")
+accel = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 with Device(0, precision=prec) as dev:
+    dev.set_accel(accel)
     stage = api.ProbeStage(dev, scene)
     for p in range(3):
         stage.run_pass(p)
@@ -16,4 +18,4 @@ with Device(0, precision=prec) as dev:
         dev.gather(f, stage.cfg)
         _, cms = dev.compose(stage.cfg, download=False)
     st = dev.last_gather_ms()
-    print(f"{prec} gather {sum(st):.2f} ms (contact {st[3]:.2f}) compose {cms:.2f} ms")
+    print(f"{prec} accel {accel} gather {sum(st):.2f} ms (contact {st[3]:.2f}) compose {cms:.2f} ms")
