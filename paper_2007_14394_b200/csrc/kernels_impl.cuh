@@ -817,6 +817,10 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
         int cell = kCellUnknown;  // phase 0: p's cell (parking test), reused by the query
         R cellR = R(0);
         if (PHASE == 0 && want && P.scene.useGrid) cell = gridCell<R>(P.scene.grid, p, &cellR);
+        // accel mode 2: off the grid, a march whose remaining terms cannot lower v
+        // ends here with v (shadowSettled)
+        if (P.escape && want && (PHASE == 1 || cell < 0) && shadowSettled(P.scene.grid, p, dir, t, tEnd, k, v))
+            want = false;
         if (PHASE == 0) {
             bool parkIt = want && park && cell < 0;
             const long long ps = parkSlot(P.ctr + kCtrParkShadow, parkIt);

@@ -154,7 +154,32 @@ struct GridDev {
     int nUnbounded;
     int nBounded;
     float walkSlack;  // FP64 walks' float box tests: > the float rounding of |p - box| at this scale
+    // the union of the bounded clusters' boxes: every bounded primitive's SDF is at
+    // least the distance to it from outside (the escape tests of accel mode 2)
+    double geoLo[3], geoHi[3];
 };
+
+// softShadowTrace (scene.hpp:459-476) from t on can no longer lower v: outside the
+// box holding every bounded primitive (no unbounded one in the scene) each
+// remaining query returns d >= L, the distance to the box, which is convex along
+// the ray: L(t') >= L(t) + L'(t) (t' - t). The lower bound (L + L' (t' - t)) / t' of
+// the remaining terms d / t' is monotone in t', so its minimum over [t, tEnd] sits
+// at an end; when k times it exceeds v (with a relative margin far above the FP64
+// rounding of the terms), min(v, clamp(k d / t')) stays v for every remaining step
+// and the march's result is v.
+template <typename R>
+__device__ __forceinline__ bool shadowSettled(const GridDev& g, V3<R> p, V3<R> dir, R t, R tEnd, R k, R v) {
+    const double px = p.x, py = p.y, pz = p.z;
+    const double dx = px - sclamp(px, g.geoLo[0], g.geoHi[0]);
+    const double dy = py - sclamp(py, g.geoLo[1], g.geoHi[1]);
+    const double dz = pz - sclamp(pz, g.geoLo[2], g.geoHi[2]);
+    const double L2 = dx * dx + dy * dy + dz * dz;
+    if (!(L2 > 0)) return false;
+    const double L = sqrt(L2);
+    const double dL = (double(dir.x) * dx + double(dir.y) * dy + double(dir.z) * dz) / L;
+    const double f0 = L / double(t), f1 = (L + dL * (double(tEnd) - double(t))) / double(tEnd);
+    return double(k) * fmin(f0, f1) * (1.0 - 1e-9) > double(v) * (1.0 + 1e-9);
+}
 
 template <typename R> struct SceneView {
     const DPrim<R>* __restrict__ prims;        // CSR order

@@ -634,6 +634,10 @@ void buildGrid(Ctx* c) {
     c->grid.walkSlack = static_cast<float>(4e-5 * (scale + 1.0));
     c->grid.unbounded = c->unbList.p;
     c->grid.nUnbounded = static_cast<int>(unb.size());
+    for (int a = 0; a < 3; ++a) {
+        c->grid.geoLo[a] = lo[a];
+        c->grid.geoHi[a] = hi[a];
+    }
     GridBuildParams p;
     std::memset(&p, 0, sizeof(p));
     p.scene = c->sceneView<double>();
