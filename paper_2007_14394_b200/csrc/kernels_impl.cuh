@@ -395,6 +395,9 @@ __device__ __forceinline__ void stagePrims(const void* src, int bytes) {
         : "memory");
 }
 
+#ifndef SDFGI_SHADOW_SETTLE_ON_GRID
+#define SDFGI_SHADOW_SETTLE_ON_GRID 0  // also test shadow marches still on the grid
+#endif
 // The initial bound of a march query (sphereTrace, scene.hpp:397-399: 2 * lastD).
 // Candidate-grid walks also cap it at c = max(tMax - t, eps): the march tests
 // d < eps (converge) and then d >= tMax - t (TMax miss), and
@@ -819,7 +822,8 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
         if (PHASE == 0 && want && P.scene.useGrid) cell = gridCell<R>(P.scene.grid, p, &cellR);
         // accel mode 2: off the grid, a march whose remaining terms cannot lower v
         // ends here with v (shadowSettled)
-        if (P.escape && want && (PHASE == 1 || cell < 0) && shadowSettled(P.scene.grid, p, dir, t, tEnd, k, v))
+        if (P.escape && want && (PHASE == 1 || cell < 0 || SDFGI_SHADOW_SETTLE_ON_GRID) &&
+            shadowSettled(P.scene.grid, p, dir, t, tEnd, k, v))
             want = false;
         if (PHASE == 0) {
             bool parkIt = want && park && cell < 0;

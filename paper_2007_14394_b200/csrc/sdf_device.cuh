@@ -170,6 +170,9 @@ struct GridDev {
 template <typename R>
 __device__ __forceinline__ bool shadowSettled(const GridDev& g, V3<R> p, V3<R> dir, R t, R tEnd, R k, R v) {
     const double px = p.x, py = p.y, pz = p.z;
+    if (px >= g.geoLo[0] && px <= g.geoHi[0] && py >= g.geoLo[1] && py <= g.geoHi[1] && pz >= g.geoLo[2] &&
+        pz <= g.geoHi[2])
+        return false;  // inside the geometry box: no bound
     const double dx = px - sclamp(px, g.geoLo[0], g.geoHi[0]);
     const double dy = py - sclamp(py, g.geoLo[1], g.geoHi[1]);
     const double dz = pz - sclamp(pz, g.geoLo[2], g.geoHi[2]);
