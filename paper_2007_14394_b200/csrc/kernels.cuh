@@ -273,6 +273,9 @@ struct GridBuildParams {
     int* bList;
 };
 constexpr int kBrick = 4;
+// at most this many moving primitives are kept out of the grid (evaluated by every
+// query) before the grid is rebuilt over all of them (SDFGI_DYNAMIC_MAX overrides)
+constexpr int kMaxDynamic = 32;
 
 // Launch the whole wavefront for one batch (K0..K3) on `st`. `persistBlocks` sizes
 // the persistent K1/K2 grids; `ev` (optional, 2 events) brackets K1..K3.
@@ -309,6 +312,8 @@ void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st);
 void launch_grid_seed(const GridBuildParams& p, int nbricks, cudaStream_t st);
 void launch_grid_list(const GridBuildParams& p, int ncells, bool fill, cudaStream_t st);
 void launch_grid_cells(const int* start, const int2* entry, int4* cell, int ncells, cudaStream_t st);
+// entry.y = map[entry.y] for every list entry (sentinels stay -1)
+void launch_grid_remap(int2* entry, long long n, const int* map, cudaStream_t st);
 void launch_brick_clusters(const GridBuildParams& p, int nbricks, bool fill, cudaStream_t st);
 // exclusive prefix sum of n ints on the device (CUB); temp == null: returns the bytes needed
 size_t scan_ints(const int* in, int* out, int n, void* temp, size_t tempBytes, cudaStream_t st);

@@ -223,6 +223,17 @@ __global__ void __launch_bounds__(256) k_grid_cells(const int* start, const int2
     const int2 f = b < e ? entry[b] : make_int2(__float_as_int(INFINITY), -1);
     cell[c] = make_int4(b, e, f.x, f.y);
 }
+__global__ void __launch_bounds__(256) k_grid_remap(int2* entry, long long n, const int* map) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int2 e = entry[i];
+    if (e.y >= 0) entry[i].y = map[e.y];
+}
+
+void launch_grid_remap(int2* entry, long long n, const int* map, cudaStream_t st) {
+    if (n > 0) k_grid_remap<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(entry, n, map);
+}
+
 void launch_grid_cells(const int* start, const int2* entry, int4* cell, int ncells, cudaStream_t st) {
     k_grid_cells<<<(ncells + 255) / 256, 256, 0, st>>>(start, entry, cell, ncells);
 }

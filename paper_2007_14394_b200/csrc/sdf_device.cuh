@@ -202,6 +202,10 @@ template <typename R> struct SceneView {
     const void* __restrict__ stage;
     int stageBytes;
     int stageRotOff;  // FP64: byte offset of the rotation rows (8 doubles per rotated primitive)
+    // dynamic primitives (moved since the candidate grid was built; not in its lists):
+    // CSR positions every on-grid query evaluates besides the cell's list
+    const int* __restrict__ dyn;
+    int nDyn;
 };
 
 // TraceStats (scene.hpp:16-36), per thread.
@@ -661,6 +665,21 @@ __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int*
         if (pd < q.d || (pd == q.d && q.own >= 0 && seed < q.own)) {
             q.d = pd;
             q.own = seed;
+        }
+    }
+    // the dynamic primitives (not in the cell lists), lowest-CSR-position tie-break
+    if (s.nDyn && !q.walk) {
+        for (int i = 0; i < s.nDyn; ++i) {
+            const int j = s.dyn[i];
+            if (ST) {
+                ++c->ek[s.kindId[j] & 0xff];
+                c->ek[5] += (s.kindId[j] >> 8) ? 0 : 1;
+            }
+            const R pd = evalPrimAt<R, STG>(s, j, p);
+            if (pd < q.d || (pd == q.d && q.own >= 0 && j < q.own)) {
+                q.d = pd;
+                q.own = j;
+            }
         }
     }
     if (q.cur < q.end) {

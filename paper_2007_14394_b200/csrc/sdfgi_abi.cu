@@ -155,14 +155,23 @@ struct Ctx {
     DBuf<BNode> bvh;
     DBuf<int> unbList;
     double gridBox[6] = {0, 0, 0, 0, 0, 0};  // region the cells cover
-    uint64_t gridHash = 0;                     // geometry the grid/BVH were built for
     int gridAccel = -1;
+    uint64_t gridParams = 0;  // hash of the grid's build parameters (environment knobs)
+    // dynamic primitives (original indices, sorted): left out of the grid lists (they
+    // moved since it was built) and evaluated by every on-grid query (dynCsr: their
+    // current CSR positions); gridCsrOrig: the CSR -> original map of the lists
+    std::vector<int> gridDyn, gridCsrOrig;
+    DBuf<int> dynCsr;
+    int nDyn = 0;
+    long long gridRefits = 0;
+    bool escapeValid = false;  // every bounded primitive inside the grid box (escape tests)
     bool hintValid = false;
     double hint[6] = {0, 0, 0, 0, 0, 0};     // probe volumes the grid must cover
     // host copy of the uploaded scene (the grid is rebuilt when the hint grows)
     std::vector<sdfgi_prim> hPrims;
-    std::vector<int32_t> hMember;
+    std::vector<int32_t> hMember, hStart;
     std::vector<sdfgi_cluster> hClusters;
+    std::vector<sdfgi_light> hLights;
     // probes
     std::vector<CascadeHost> cascades;
     int octRes = 8;
@@ -227,7 +236,7 @@ struct Ctx {
         prim64.free(); prim32.free(); stage64.free(); cl64.free(); cl32.free(); cstart.free(); orig.free();
         albedo.free(); emission.free(); lights.free(); kindId.free();
         gridStart.free(); gridList.free(); gridCounts.free(); gridU.free(); gridEntry.free(); gridCell.free(); brickCounts.free(); brickStart.free(); brickList.free(); brickSeed.free(); scanTemp.free();
-        bvh.free(); unbList.free(); primBox.free();
+        bvh.free(); unbList.free(); primBox.free(); dynCsr.free();
         pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free(); allRefs.free();
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
@@ -305,6 +314,8 @@ SceneView<double> Ctx::sceneView<double>() const {
     v.stage = stage64.p;
     v.stageBytes = stage64Bytes;
     v.stageRotOff = stage64RotOff;
+    v.dyn = dynCsr.p;
+    v.nDyn = haveGrid ? nDyn : 0;
     return v;
 }
 template <>
@@ -327,6 +338,8 @@ SceneView<float> Ctx::sceneView<float>() const {
     v.stage = prim32.p;
     v.stageBytes = stage32Bytes;
     v.stageRotOff = 0;
+    v.dyn = dynCsr.p;
+    v.nDyn = haveGrid ? nDyn : 0;
     return v;
 }
 
@@ -487,81 +500,27 @@ void primAabb(const sdfgi_prim& s, double* out) {
     }
 }
 
-void buildGrid(Ctx* c) {
-    const sdfgi_prim* prims = c->hPrims.data();
-    const int32_t* member_idx = c->hMember.data();
+// The cluster BVH for queries off the grid (and the grid build's exact queries),
+// the unbounded-cluster list and the box of the bounded geometry (the escape
+// tests of accel mode 2), for the context's current clusters. Median split of the
+// box centres along the widest axis (depth <= ceil(log2 n) < kBvhStack), one
+// cluster per leaf. Child boxes are padded like the FP32 cluster boxes and
+// rounded outward to float, so the subtree tests are conservative in both
+// precisions.
+void buildBvh(Ctx* c, double scaleHint) {
     const sdfgi_cluster* clusters = c->hClusters.data();
     const int n = static_cast<int>(c->hClusters.size());
-    c->haveGrid = false;
-    c->gridEntries = 0;
-    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    int bounded = 0;
+    double glo[3] = {INFINITY, INFINITY, INFINITY}, ghi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    double scale = 0;
     for (int k = 0; k < n; ++k) {
         if (clusters[k].unbounded) continue;
-        ++bounded;
         for (int a = 0; a < 3; ++a) {
-            lo[a] = std::min(lo[a], clusters[k].lo[a]);
-            hi[a] = std::max(hi[a], clusters[k].hi[a]);
+            glo[a] = std::min(glo[a], clusters[k].lo[a]);
+            ghi[a] = std::max(ghi[a], clusters[k].hi[a]);
+            scale = std::max(scale, std::max(std::fabs(clusters[k].lo[a]), std::fabs(clusters[k].hi[a])));
         }
     }
-    if (bounded == 0 || n < 2) return;
-    double ext[3], scale = 0;
-    // the grid extends past the geometry so rays leaving the scene stay on the
-    // (cheap) candidate lists for their first steps; SDFGI_GRID_MARGIN overrides.
-    // It also covers the probe volumes (the hint box grown by sdfgi_cascade_set):
-    // probes above an open scene would otherwise query off the grid every step.
-    // The margin is a multiple of the geometry's SMALLEST extent on every axis: a
-    // flat open scene (C4: 240 x 20 x 240) keeps the rays that leave it upwards on
-    // the grid without spending cells on its far horizontal surroundings.
-    // Sweep (profiles/README.md, 50M cells): C2 pass 0 FP64 margin 0.6 per-axis
-    // 13.1 ms, 2.5 x min 12.0, 4 x min 12.3; C4 pass 1 0.235 -> 0.326 -> 0.374 Grays/s.
-    // SDFGI_GRID_MARGIN sets the multiple, SDFGI_GRID_MARGIN_MIN=0 the per-axis extent.
-    const char* menv = std::getenv("SDFGI_GRID_MARGIN");
-    const double marginFrac = menv ? std::atof(menv) : 3.5;
-    const char* mmode = std::getenv("SDFGI_GRID_MARGIN_MIN");
-    const bool fromMin = !mmode || std::atoi(mmode) != 0;
-    const double minExt = std::min(hi[0] - lo[0], std::min(hi[1] - lo[1], hi[2] - lo[2]));
-    for (int a = 0; a < 3; ++a) {
-        double e = fromMin ? minExt : hi[a] - lo[a];
-        double m = marginFrac * e + 1e-3;
-        lo[a] -= m;
-        hi[a] += m;
-        if (c->hintValid) {
-            lo[a] = std::min(lo[a], c->hint[a]);
-            hi[a] = std::max(hi[a], c->hint[3 + a]);
-        }
-        ext[a] = hi[a] - lo[a];
-        scale = std::max(scale, std::max(std::fabs(lo[a]), std::fabs(hi[a])));
-    }
-    const char* env = std::getenv("SDFGI_GRID_CELLS");
-    // finer cells -> smaller U -> shorter, more uniform candidate lists (and tighter
-    // per-entry bounds); measured on C2 with the current kernels (pass 0, FP64, warm):
-    // 2M cells 17.4 ms, 4M 16.6, 8M 15.9, 16M 15.5, 24M 15.3 (margin 0.6, round-1
-    // kernels); with the SDF-bound lists and the min-extent margin 33M -> 50M -> 66M
-    // cells: C2 13.9 / 12.3 / 12.9 ms, C4 0.28 / 0.37 / 0.34 Grays/s
-    // Small scenes need far fewer cells (and an animated scene rebuilds its grid
-    // every frame): 33k cells per primitive, between 2M and 66M. With the round-1
-    // final kernels 50M -> 66M: C2 pass 0 FP64 9.50 -> 9.36 ms, FP32 5.09 -> 5.05;
-    // C4 FP64 0.548 -> 0.565 Grays/s, FP32 1.09 -> 1.12 (80M: candidate grid too large)
-    const double byPrims = std::min(66000000.0, std::max(2097152.0, 33000.0 * c->nPrims));
-    double target = env ? std::atof(env) : byPrims;
-    if (target < 1) return;
-    double h = std::cbrt(ext[0] * ext[1] * ext[2] / target);
-    int dim[3];
-    for (int a = 0; a < 3; ++a) {
-        h = std::max(h, ext[a] / 1024.0);
-    }
-    long long ncells = 1;
-    for (int a = 0; a < 3; ++a) {
-        dim[a] = std::max(1, static_cast<int>(std::ceil(ext[a] / h)));
-        ncells *= dim[a];
-    }
-    REQ(ncells < (1LL << 26), SDFGI_ERR_INVALID, "candidate grid too large");
-    // BVH over the bounded clusters for points off the grid: median split of the
-    // box centres along the widest axis (depth <= ceil(log2 n) < kBvhStack), one
-    // cluster per leaf. Child boxes are padded like the FP32 cluster boxes and
-    // rounded outward to float, so the subtree tests are conservative in both
-    // precisions.
+    scale = std::max(scale, scaleHint);  // the grid box's coordinate scale
     std::vector<int> unb, ids;
     for (int k = 0; k < n; ++k) (clusters[k].unbounded ? unb : ids).push_back(k);
     std::vector<BNode> nodes;
@@ -635,9 +594,89 @@ void buildGrid(Ctx* c) {
     c->grid.unbounded = c->unbList.p;
     c->grid.nUnbounded = static_cast<int>(unb.size());
     for (int a = 0; a < 3; ++a) {
-        c->grid.geoLo[a] = lo[a];
-        c->grid.geoHi[a] = hi[a];
+        c->grid.geoLo[a] = glo[a];
+        c->grid.geoHi[a] = ghi[a];
     }
+}
+
+void buildGrid(Ctx* c) {
+    const sdfgi_prim* prims = c->hPrims.data();
+    const int32_t* member_idx = c->hMember.data();
+    const sdfgi_cluster* clusters = c->hClusters.data();
+    const int n = static_cast<int>(c->hClusters.size());
+    c->haveGrid = false;
+    c->gridEntries = 0;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    int bounded = 0;
+    for (int k = 0; k < n; ++k) {
+        if (clusters[k].unbounded) continue;
+        ++bounded;
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], clusters[k].lo[a]);
+            hi[a] = std::max(hi[a], clusters[k].hi[a]);
+        }
+    }
+    if (bounded == 0 || n < 2) return;
+    double ext[3], scale = 0;
+    // the grid extends past the geometry so rays leaving the scene stay on the
+    // (cheap) candidate lists for their first steps; SDFGI_GRID_MARGIN overrides.
+    // It also covers the probe volumes (the hint box grown by sdfgi_cascade_set):
+    // probes above an open scene would otherwise query off the grid every step.
+    // The margin is a multiple of the geometry's SMALLEST extent on every axis: a
+    // flat open scene (C4: 240 x 20 x 240) keeps the rays that leave it upwards on
+    // the grid without spending cells on its far horizontal surroundings.
+    // Sweep (profiles/README.md, 50M cells): C2 pass 0 FP64 margin 0.6 per-axis
+    // 13.1 ms, 2.5 x min 12.0, 4 x min 12.3; C4 pass 1 0.235 -> 0.326 -> 0.374 Grays/s.
+    // SDFGI_GRID_MARGIN sets the multiple, SDFGI_GRID_MARGIN_MIN=0 the per-axis extent.
+    const char* menv = std::getenv("SDFGI_GRID_MARGIN");
+    const double marginFrac = menv ? std::atof(menv) : 3.5;
+    const char* mmode = std::getenv("SDFGI_GRID_MARGIN_MIN");
+    const bool fromMin = !mmode || std::atoi(mmode) != 0;
+    const double minExt = std::min(hi[0] - lo[0], std::min(hi[1] - lo[1], hi[2] - lo[2]));
+    for (int a = 0; a < 3; ++a) {
+        double e = fromMin ? minExt : hi[a] - lo[a];
+        double m = marginFrac * e + 1e-3;
+        lo[a] -= m;
+        hi[a] += m;
+        if (c->hintValid) {
+            lo[a] = std::min(lo[a], c->hint[a]);
+            hi[a] = std::max(hi[a], c->hint[3 + a]);
+        }
+        ext[a] = hi[a] - lo[a];
+        scale = std::max(scale, std::max(std::fabs(lo[a]), std::fabs(hi[a])));
+    }
+    const char* env = std::getenv("SDFGI_GRID_CELLS");
+    // finer cells -> smaller U -> shorter, more uniform candidate lists (and tighter
+    // per-entry bounds); measured on C2 with the current kernels (pass 0, FP64, warm):
+    // 2M cells 17.4 ms, 4M 16.6, 8M 15.9, 16M 15.5, 24M 15.3 (margin 0.6, round-1
+    // kernels); with the SDF-bound lists and the min-extent margin 33M -> 50M -> 66M
+    // cells: C2 13.9 / 12.3 / 12.9 ms, C4 0.28 / 0.37 / 0.34 Grays/s
+    // Small scenes need far fewer cells (and an animated scene rebuilds its grid
+    // every frame): 33k cells per primitive, between 2M and 66M. With the round-1
+    // final kernels 50M -> 66M: C2 pass 0 FP64 9.50 -> 9.36 ms, FP32 5.09 -> 5.05;
+    // C4 FP64 0.548 -> 0.565 Grays/s, FP32 1.09 -> 1.12 (80M: candidate grid too large)
+    const double byPrims = std::min(66000000.0, std::max(2097152.0, 33000.0 * c->nPrims));
+    double target = env ? std::atof(env) : byPrims;
+    if (target < 1) return;
+    double h = std::cbrt(ext[0] * ext[1] * ext[2] / target);
+    int dim[3];
+    for (int a = 0; a < 3; ++a) {
+        h = std::max(h, ext[a] / 1024.0);
+    }
+    // rounding every axis up can overshoot the target: grow h until the cell count
+    // is inside the 2^26 the cell indexing allows (never fail for a size we chose)
+    long long ncells = 1;
+    for (int tries = 0;; ++tries) {
+        ncells = 1;
+        for (int a = 0; a < 3; ++a) {
+            dim[a] = std::max(1, static_cast<int>(std::ceil(ext[a] / h)));
+            ncells *= dim[a];
+        }
+        if (ncells < (1LL << 26)) break;
+        REQ(tries < 64, SDFGI_ERR_INVALID, "candidate grid too large");
+        h *= std::cbrt(static_cast<double>(ncells) / static_cast<double>(1LL << 26)) * 1.001;
+    }
+    buildBvh(c, scale);
     GridBuildParams p;
     std::memset(&p, 0, sizeof(p));
     p.scene = c->sceneView<double>();
@@ -839,7 +878,9 @@ void reserveHitAt(Ctx* c, WaveParams<R>& p, size_t n) {
 // accel mode 2's escape test (WaveParams::escape) holds when the candidate grid
 // exists and the scene has no unbounded primitive (a plane can be reached from
 // anywhere outside the grid box)
-int escapeOk(const Ctx* c) { return (c->accel == 2 && c->haveGrid && c->grid.nUnbounded == 0) ? 1 : 0; }
+int escapeOk(const Ctx* c) {
+    return (c->accel == 2 && c->haveGrid && c->escapeValid && c->grid.nUnbounded == 0) ? 1 : 0;
+}
 
 template <typename R>
 WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand) {
@@ -1092,134 +1133,263 @@ int sdfgi_ctx_synchronize(void* ctx) {
     });
 }
 
+}  // extern "C"
+
+namespace {
+
+// The scene's device arrays (CSR order: device primitive j = prims[member_idx[j]])
+// and their host copies; no acceleration structure.
+void uploadSceneArrays(Ctx* c, const sdfgi_prim* prims, int n_prims, const sdfgi_cluster* clusters, int n_clusters,
+                       const int32_t* member_start, const int32_t* member_idx, const sdfgi_light* lights,
+                       int n_lights, const double sky[3]) {
+    REQ(n_prims >= 0 && n_clusters >= 0 && n_lights >= 0, SDFGI_ERR_INVALID, "negative count");
+    REQ(n_prims == 0 || prims, SDFGI_ERR_INVALID, "null prims");
+    REQ(n_clusters == 0 || (clusters && member_start && member_idx), SDFGI_ERR_INVALID, "null clusters");
+    REQ(n_lights == 0 || lights, SDFGI_ERR_INVALID, "null lights");
+    REQ(sky, SDFGI_ERR_INVALID, "null sky");
+    int nMembers = n_clusters ? member_start[n_clusters] : 0;
+    REQ(n_clusters == 0 || member_start[0] == 0, SDFGI_ERR_INVALID, "member_start[0] != 0");
+    for (int k = 0; k < n_clusters; ++k)
+        REQ(member_start[k + 1] >= member_start[k], SDFGI_ERR_INVALID, "member_start not monotone");
+    for (int m = 0; m < nMembers; ++m)
+        REQ(member_idx[m] >= 0 && member_idx[m] < n_prims, SDFGI_ERR_INVALID, "member index out of range");
+    for (int i = 0; i < n_prims; ++i)
+        REQ(prims[i].kind >= 0 && prims[i].kind <= 4, SDFGI_ERR_INVALID, "bad primitive kind");
+    // cluster (CSR) order: device primitive j = prims[member_idx[j]]
+    std::vector<DPrim<double>> p64(nMembers);
+    std::vector<DPrim<float>> p32(nMembers);
+    std::vector<int> orig(nMembers), kid(std::max(nMembers, 1));
+    std::vector<double> alb(3 * static_cast<size_t>(nMembers)), em(3 * static_cast<size_t>(nMembers));
+    for (int j = 0; j < nMembers; ++j) {
+        const sdfgi_prim& s = prims[member_idx[j]];
+        std::memset(&p64[j], 0, sizeof(p64[j]));
+        std::memset(&p32[j], 0, sizeof(p32[j]));
+        fillPrim(p64[j], s);
+        fillPrim(p32[j], s);
+        orig[j] = member_idx[j];
+        kid[j] = s.kind | (p64[j].identity << 8);
+        for (int k = 0; k < 3; ++k) {
+            alb[3 * j + k] = s.albedo[k];
+            em[3 * j + k] = s.emission[k];
+        }
+    }
+    std::vector<DCluster<double>> c64(n_clusters);
+    std::vector<DCluster<float>> c32(n_clusters);
+    for (int k = 0; k < n_clusters; ++k) {
+        std::memset(&c64[k], 0, sizeof(c64[k]));
+        std::memset(&c32[k], 0, sizeof(c32[k]));
+        for (int a = 0; a < 3; ++a) {
+            c64[k].lo[a] = clusters[k].lo[a];
+            c64[k].hi[a] = clusters[k].hi[a];
+            // FP32 cull boxes: widened so float rounding of the box distance can
+            // never skip a member the FP32 evaluation would have picked
+            double lo = clusters[k].lo[a], hi = clusters[k].hi[a];
+            double padLo = 1e-5 * (std::fabs(lo) + 1.0), padHi = 1e-5 * (std::fabs(hi) + 1.0);
+            c32[k].lo[a] = std::nextafter(static_cast<float>(lo - padLo), -INFINITY);
+            c32[k].hi[a] = std::nextafter(static_cast<float>(hi + padHi), INFINITY);
+        }
+        c64[k].unbounded = c32[k].unbounded = clusters[k].unbounded ? 1 : 0;
+    }
+    std::vector<int> starts(member_start, member_start + n_clusters + 1);
+    if (n_clusters == 0) starts.assign(1, 0);
+    c->prim64.upload(p64.data(), p64.size(), c->stream);
+    c->prim32.upload(p32.data(), p32.size(), c->stream);
+    c->cl64.upload(c64.data(), c64.size(), c->stream);
+    c->cl32.upload(c32.data(), c32.size(), c->stream);
+    c->cstart.upload(starts.data(), starts.size(), c->stream);
+    c->orig.upload(orig.data(), orig.size(), c->stream);
+    c->albedo.upload(alb.data(), alb.size(), c->stream);
+    c->emission.upload(em.data(), em.size(), c->stream);
+    c->kindId.upload(kid.data(), kid.size(), c->stream);
+    c->lights.upload(reinterpret_cast<const DLight*>(lights), n_lights, c->stream);
+    // shared-memory staging of the primitive records for K1/K2 (evalPrimStaged):
+    // FP64 64 B per primitive + 64 B per rotation row, FP32 the 64 B records as is
+    {
+        int optin = 0;
+        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+        const long long limit = static_cast<long long>(optin) - 1024;  // the kernels' static shared memory
+        const char* senv = std::getenv("SDFGI_STAGE");
+        const bool allow = !(senv && std::atoi(senv) == 0) && nMembers > 0;
+        std::vector<unsigned char> st(64 * static_cast<size_t>(nMembers));
+        std::vector<unsigned char> rows;
+        for (int j = 0; j < nMembers; ++j) {
+            unsigned char* r = st.data() + 64 * static_cast<size_t>(j);
+            std::memcpy(r, &p64[j], 64);
+            int rotIdx = -1;
+            if (!p64[j].identity) {
+                rotIdx = static_cast<int>(rows.size() / 64);
+                const unsigned char* src = reinterpret_cast<const unsigned char*>(&p64[j]) + 64;
+                rows.insert(rows.end(), src, src + 64);
+            }
+            std::memcpy(r + 52, &rotIdx, 4);  // the identity flag's slot
+        }
+        const long long b64 = static_cast<long long>(st.size() + rows.size());
+        c->stage64Bytes = 0;
+        if (allow && b64 <= limit) {
+            st.insert(st.end(), rows.begin(), rows.end());
+            c->stage64.upload(st.data(), st.size(), c->stream);
+            c->stage64Bytes = static_cast<int>(b64);
+            c->stage64RotOff = 64 * nMembers;
+        }
+        const long long b32 = 64LL * nMembers;
+        c->stage32Bytes = (allow && b32 <= limit) ? static_cast<int>(b32) : 0;
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    c->nPrims = nMembers;
+    c->nClusters = n_clusters;
+    c->nLights = n_lights;
+    for (int k = 0; k < 3; ++k) c->sky[k] = sky[k];
+    c->haveScene = true;
+    c->hPrims.assign(prims, prims + n_prims);
+    c->hMember.assign(member_idx, member_idx + (n_clusters ? member_start[n_clusters] : 0));
+    c->hClusters.assign(clusters, clusters + n_clusters);
+    c->hStart.assign(member_start, member_start + (n_clusters ? n_clusters + 1 : 0));
+    c->hLights.assign(lights, lights + n_lights);
+}
+
+// Geometry of primitive a and b equal (the fields the SDF reads)
+bool sameGeometry(const sdfgi_prim& a, const sdfgi_prim& b) {
+    return a.kind == b.kind && std::memcmp(a.rot, b.rot, sizeof(a.rot)) == 0 &&
+           std::memcmp(a.trans, b.trans, sizeof(a.trans)) == 0 && std::memcmp(a.size, b.size, sizeof(a.size)) == 0;
+}
+
+void checkEscape(Ctx* c);
+
+// The grid's CSR positions -> the current ones (the caller re-clustered: same
+// primitives, other cluster order), and the dynamic list's CSR positions.
+void remapGrid(Ctx* c) {
+    std::vector<int> csrOf(c->hPrims.size(), -1);
+    for (size_t j = 0; j < c->hMember.size(); ++j)
+        if (csrOf[c->hMember[j]] < 0) csrOf[c->hMember[j]] = static_cast<int>(j);
+    if (c->gridCsrOrig != c->hMember) {
+        std::vector<int> map(std::max<size_t>(c->gridCsrOrig.size(), 1));
+        for (size_t j = 0; j < c->gridCsrOrig.size(); ++j) map[j] = csrOf[c->gridCsrOrig[j]];
+        DBuf<int> dmap;
+        dmap.upload(map.data(), map.size(), c->stream);
+        launch_grid_remap(c->gridEntry.p, c->gridEntries, dmap.p, c->stream);
+        checkLaunch(c);
+        launch_grid_cells(c->gridStart.p, c->gridEntry.p, c->gridCell.p,
+                          c->grid.dim[0] * c->grid.dim[1] * c->grid.dim[2], c->stream);
+        checkLaunch(c);
+        CK(cudaStreamSynchronize(c->stream));
+        dmap.free();
+        c->gridCsrOrig = c->hMember;
+    }
+    std::vector<int> dyn;
+    for (int o : c->gridDyn)
+        if (csrOf[o] >= 0) dyn.push_back(csrOf[o]);
+    std::sort(dyn.begin(), dyn.end());
+    c->nDyn = static_cast<int>(dyn.size());
+    if (dyn.empty()) dyn.push_back(0);
+    c->dynCsr.upload(dyn.data(), dyn.size(), c->stream);
+    CK(cudaStreamSynchronize(c->stream));
+}
+
+// The candidate grid over every primitive not in gridDyn (the ones that moved since
+// it was built): with dynamic primitives the lists and bounds are built on a scene
+// of the static ones (clusters without their dynamic members), then mapped back to
+// the full scene's CSR order; queries evaluate the dynamic list besides the cell
+// list (query()). The cluster BVH is over the full scene.
+void rebuildGrid(Ctx* c) {
+    if (c->gridDyn.empty()) {
+        buildGrid(c);
+        c->gridCsrOrig = c->hMember;
+    } else {
+        const std::vector<sdfgi_prim> fp = c->hPrims;
+        const std::vector<int32_t> fm = c->hMember, fs = c->hStart;
+        const std::vector<sdfgi_cluster> fc = c->hClusters;
+        const std::vector<sdfgi_light> fl = c->hLights;
+        const double sky[3] = {c->sky[0], c->sky[1], c->sky[2]};
+        std::vector<char> isDyn(fp.size(), 0);
+        for (int o : c->gridDyn) isDyn[o] = 1;
+        std::vector<sdfgi_cluster> sc;
+        std::vector<int32_t> ss{0}, sm;
+        for (size_t k = 0; k + 1 < fs.size(); ++k) {
+            const size_t before = sm.size();
+            for (int m = fs[k]; m < fs[k + 1]; ++m)
+                if (!isDyn[fm[m]]) sm.push_back(fm[m]);
+            if (sm.size() == before) continue;
+            sc.push_back(fc[k]);
+            ss.push_back(static_cast<int32_t>(sm.size()));
+        }
+        uploadSceneArrays(c, fp.data(), static_cast<int>(fp.size()), sc.data(), static_cast<int>(sc.size()), ss.data(),
+                          sm.data(), fl.data(), static_cast<int>(fl.size()), sky);
+        buildGrid(c);
+        c->gridCsrOrig = sm;
+        uploadSceneArrays(c, fp.data(), static_cast<int>(fp.size()), fc.data(), static_cast<int>(fc.size()), fs.data(),
+                          fm.data(), fl.data(), static_cast<int>(fl.size()), sky);
+    }
+    double scale = 0;
+    for (int a = 0; a < 6; ++a) scale = std::max(scale, std::fabs(c->gridBox[a]));
+    buildBvh(c, scale);
+    if (c->haveGrid) remapGrid(c);
+    checkEscape(c);
+}
+
+// accel mode 2's escape tests need every bounded primitive inside the grid box
+void checkEscape(Ctx* c) {
+    bool inside = c->haveGrid;
+    for (int a = 0; a < 3 && inside; ++a)
+        inside = c->grid.geoLo[a] >= c->gridBox[a] && c->grid.geoHi[a] <= c->gridBox[3 + a];
+    c->escapeValid = inside;
+}
+
+}  // namespace
+
+extern "C" {
+
 int sdfgi_scene_upload(void* ctx, const sdfgi_prim* prims, int n_prims, const sdfgi_cluster* clusters,
                        int n_clusters, const int32_t* member_start, const int32_t* member_idx,
                        const sdfgi_light* lights, int n_lights, const double sky[3]) {
     return guard([&] {
         Ctx* c = C(ctx);
-        REQ(n_prims >= 0 && n_clusters >= 0 && n_lights >= 0, SDFGI_ERR_INVALID, "negative count");
-        REQ(n_prims == 0 || prims, SDFGI_ERR_INVALID, "null prims");
-        REQ(n_clusters == 0 || (clusters && member_start && member_idx), SDFGI_ERR_INVALID, "null clusters");
-        REQ(n_lights == 0 || lights, SDFGI_ERR_INVALID, "null lights");
-        REQ(sky, SDFGI_ERR_INVALID, "null sky");
-        int nMembers = n_clusters ? member_start[n_clusters] : 0;
-        REQ(n_clusters == 0 || member_start[0] == 0, SDFGI_ERR_INVALID, "member_start[0] != 0");
-        for (int k = 0; k < n_clusters; ++k)
-            REQ(member_start[k + 1] >= member_start[k], SDFGI_ERR_INVALID, "member_start not monotone");
-        for (int m = 0; m < nMembers; ++m)
-            REQ(member_idx[m] >= 0 && member_idx[m] < n_prims, SDFGI_ERR_INVALID, "member index out of range");
-        for (int i = 0; i < n_prims; ++i)
-            REQ(prims[i].kind >= 0 && prims[i].kind <= 4, SDFGI_ERR_INVALID, "bad primitive kind");
-        // cluster (CSR) order: device primitive j = prims[member_idx[j]]
-        std::vector<DPrim<double>> p64(nMembers);
-        std::vector<DPrim<float>> p32(nMembers);
-        std::vector<int> orig(nMembers), kid(std::max(nMembers, 1));
-        std::vector<double> alb(3 * static_cast<size_t>(nMembers)), em(3 * static_cast<size_t>(nMembers));
-        for (int j = 0; j < nMembers; ++j) {
-            const sdfgi_prim& s = prims[member_idx[j]];
-            std::memset(&p64[j], 0, sizeof(p64[j]));
-            std::memset(&p32[j], 0, sizeof(p32[j]));
-            fillPrim(p64[j], s);
-            fillPrim(p32[j], s);
-            orig[j] = member_idx[j];
-            kid[j] = s.kind | (p64[j].identity << 8);
-            for (int k = 0; k < 3; ++k) {
-                alb[3 * j + k] = s.albedo[k];
-                em[3 * j + k] = s.emission[k];
-            }
-        }
-        std::vector<DCluster<double>> c64(n_clusters);
-        std::vector<DCluster<float>> c32(n_clusters);
-        for (int k = 0; k < n_clusters; ++k) {
-            std::memset(&c64[k], 0, sizeof(c64[k]));
-            std::memset(&c32[k], 0, sizeof(c32[k]));
-            for (int a = 0; a < 3; ++a) {
-                c64[k].lo[a] = clusters[k].lo[a];
-                c64[k].hi[a] = clusters[k].hi[a];
-                // FP32 cull boxes: widened so float rounding of the box distance can
-                // never skip a member the FP32 evaluation would have picked
-                double lo = clusters[k].lo[a], hi = clusters[k].hi[a];
-                double padLo = 1e-5 * (std::fabs(lo) + 1.0), padHi = 1e-5 * (std::fabs(hi) + 1.0);
-                c32[k].lo[a] = std::nextafter(static_cast<float>(lo - padLo), -INFINITY);
-                c32[k].hi[a] = std::nextafter(static_cast<float>(hi + padHi), INFINITY);
-            }
-            c64[k].unbounded = c32[k].unbounded = clusters[k].unbounded ? 1 : 0;
-        }
-        std::vector<int> starts(member_start, member_start + n_clusters + 1);
-        if (n_clusters == 0) starts.assign(1, 0);
-        c->prim64.upload(p64.data(), p64.size(), c->stream);
-        c->prim32.upload(p32.data(), p32.size(), c->stream);
-        c->cl64.upload(c64.data(), c64.size(), c->stream);
-        c->cl32.upload(c32.data(), c32.size(), c->stream);
-        c->cstart.upload(starts.data(), starts.size(), c->stream);
-        c->orig.upload(orig.data(), orig.size(), c->stream);
-        c->albedo.upload(alb.data(), alb.size(), c->stream);
-        c->emission.upload(em.data(), em.size(), c->stream);
-        c->kindId.upload(kid.data(), kid.size(), c->stream);
-        c->lights.upload(reinterpret_cast<const DLight*>(lights), n_lights, c->stream);
-        // shared-memory staging of the primitive records for K1/K2 (evalPrimStaged):
-        // FP64 64 B per primitive + 64 B per rotation row, FP32 the 64 B records as is
-        {
-            int optin = 0;
-            CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
-            const long long limit = static_cast<long long>(optin) - 1024;  // the kernels' static shared memory
-            const char* senv = std::getenv("SDFGI_STAGE");
-            const bool allow = !(senv && std::atoi(senv) == 0) && nMembers > 0;
-            std::vector<unsigned char> st(64 * static_cast<size_t>(nMembers));
-            std::vector<unsigned char> rows;
-            for (int j = 0; j < nMembers; ++j) {
-                unsigned char* r = st.data() + 64 * static_cast<size_t>(j);
-                std::memcpy(r, &p64[j], 64);
-                int rotIdx = -1;
-                if (!p64[j].identity) {
-                    rotIdx = static_cast<int>(rows.size() / 64);
-                    const unsigned char* src = reinterpret_cast<const unsigned char*>(&p64[j]) + 64;
-                    rows.insert(rows.end(), src, src + 64);
-                }
-                std::memcpy(r + 52, &rotIdx, 4);  // the identity flag's slot
-            }
-            const long long b64 = static_cast<long long>(st.size() + rows.size());
-            c->stage64Bytes = 0;
-            if (allow && b64 <= limit) {
-                st.insert(st.end(), rows.begin(), rows.end());
-                c->stage64.upload(st.data(), st.size(), c->stream);
-                c->stage64Bytes = static_cast<int>(b64);
-                c->stage64RotOff = 64 * nMembers;
-            }
-            const long long b32 = 64LL * nMembers;
-            c->stage32Bytes = (allow && b32 <= limit) ? static_cast<int>(b32) : 0;
-        }
-        CK(cudaStreamSynchronize(c->stream));
-        c->nPrims = nMembers;
-        c->nClusters = n_clusters;
-        c->nLights = n_lights;
-        for (int k = 0; k < 3; ++k) c->sky[k] = sky[k];
-        c->haveScene = true;
-        // the acceleration structures are a function of the geometry alone: an
-        // upload of the same primitives and clusters (a static scene, re-sent every
-        // frame) keeps the grid and BVH instead of rebuilding them
-        uint64_t hsh = 1469598103934665603ull;
-        auto mix = [&hsh](const void* p, size_t n) {
-            const unsigned char* b = static_cast<const unsigned char*>(p);
-            for (size_t i = 0; i < n; ++i) hsh = (hsh ^ b[i]) * 1099511628211ull;
-        };
-        mix(prims, sizeof(sdfgi_prim) * static_cast<size_t>(n_prims));
-        mix(clusters, sizeof(sdfgi_cluster) * static_cast<size_t>(n_clusters));
-        mix(member_start, sizeof(int32_t) * (static_cast<size_t>(n_clusters) + (n_clusters ? 1 : 0)));
-        mix(member_idx, sizeof(int32_t) * static_cast<size_t>(nMembers));
-        for (const char* k : {"SDFGI_GRID_MARGIN", "SDFGI_GRID_CELLS", "SDFGI_GRID_MAXLIST", "SDFGI_GRID_HINT"}) {
+        const std::vector<sdfgi_prim> prev = c->hPrims;
+        uploadSceneArrays(c, prims, n_prims, clusters, n_clusters, member_start, member_idx, lights, n_lights, sky);
+        // The acceleration structures are a function of the geometry alone. A static
+        // scene re-sent every frame keeps its grid; when primitives move, the ones
+        // that moved become "dynamic" (left out of the grid lists, evaluated by every
+        // query) and only a primitive moving for the first time rebuilds the grid
+        // (without it); beyond kMaxDynamic moving primitives the grid is rebuilt over
+        // all of them. A re-clustering of the same geometry remaps the lists.
+        uint64_t ph = 1469598103934665603ull;
+        for (const char* k : {"SDFGI_GRID_MARGIN", "SDFGI_GRID_CELLS", "SDFGI_GRID_MAXLIST", "SDFGI_GRID_HINT",
+                              "SDFGI_DYNAMIC_MAX"}) {
             const char* v = std::getenv(k);  // the grid's build parameters
-            mix(v ? v : "-", v ? std::strlen(v) : 1);
+            const std::string t = v ? v : "-";
+            for (unsigned char ch : t) ph = (ph ^ ch) * 1099511628211ull;
         }
-        const bool same = c->haveGrid && c->gridHash == hsh && (c->gridAccel != 0) == (c->accel != 0);
-        c->hPrims.assign(prims, prims + n_prims);
-        c->hMember.assign(member_idx, member_idx + nMembers);
-        c->hClusters.assign(clusters, clusters + n_clusters);
-        if (!same) {
-            buildGrid(c);
-            c->gridHash = hsh;
+        bool sameSet = c->haveGrid && prev.size() == static_cast<size_t>(n_prims) && c->gridParams == ph &&
+                       (c->gridAccel != 0) == (c->accel != 0);
+        for (int i = 0; sameSet && i < n_prims; ++i) sameSet = prev[i].id == prims[i].id;
+        std::vector<int> moved;
+        if (sameSet)
+            for (int i = 0; i < n_prims; ++i)
+                if (!sameGeometry(prev[i], prims[i])) moved.push_back(i);
+        const char* denv = std::getenv("SDFGI_DYNAMIC_MAX");
+        const int maxDyn = denv ? std::atoi(denv) : kMaxDynamic;
+        if (!sameSet) {
+            c->gridDyn.clear();
+            c->gridParams = ph;
             c->gridAccel = c->accel;
+            rebuildGrid(c);
+            return;
         }
+        std::vector<int> grow;
+        std::set_difference(moved.begin(), moved.end(), c->gridDyn.begin(), c->gridDyn.end(), std::back_inserter(grow));
+        if (grow.empty()) {  // the grid's static geometry is unchanged: refit
+            double scale = 0;
+            for (int a = 0; a < 6; ++a) scale = std::max(scale, std::fabs(c->gridBox[a]));
+            buildBvh(c, scale);
+            remapGrid(c);
+            checkEscape(c);
+            ++c->gridRefits;
+            return;
+        }
+        std::vector<int> dyn;
+        std::set_union(c->gridDyn.begin(), c->gridDyn.end(), grow.begin(), grow.end(), std::back_inserter(dyn));
+        c->gridDyn = (static_cast<int>(dyn.size()) <= maxDyn && 4 * dyn.size() < static_cast<size_t>(n_prims))
+                         ? dyn : std::vector<int>();
+        rebuildGrid(c);
     });
 }
 
@@ -1296,7 +1466,7 @@ int sdfgi_cascade_set(void* ctx, int level, int res_x, int res_y, int res_z, dou
                 c->hint[3 + a] = c->hintValid ? std::max(c->hint[3 + a], bhi) : bhi;
             }
             c->hintValid = true;
-            if (c->haveScene) buildGrid(c);
+            if (c->haveScene) rebuildGrid(c);
         }
     });
 }
