@@ -324,6 +324,17 @@ __global__ void __launch_bounds__(256) k_contact_setup(WaveParams<R> P) {
     stStream(reinterpret_cast<ContactRay<R>*>(P.cray) + i, r);
 }
 
+// The radiance of every ray of a probe batch preset to the sky (shadeHit's miss
+// branch, probe_update.hpp:137); K3a overwrites the converged hits' entries.
+template <typename R>
+__global__ void __launch_bounds__(256) k_fill_sky(WaveParams<R> P) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= P.rayStart[P.nCand]) return;
+    __stcs(&P.rad[3 * i], R(P.scene.sky[0]));
+    __stcs(&P.rad[3 * i + 1], R(P.scene.sky[1]));
+    __stcs(&P.rad[3 * i + 2], R(P.scene.sky[2]));
+}
+
 // Every probe ray's set-up at full lane occupancy, ahead of K1 (in K1 only the few
 // refilling lanes of a warp would run it): trace-order item -> its probe (the
 // candidate of its 32-ray chunk, then a step or two), its Fibonacci sample
@@ -637,8 +648,13 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
                     h.t = R(0);
                     h.status = ((done == 2 ? 1 : 2) << 1) | ((done == 2 ? step + 1 : maxSteps) << 8);
                 }
-                stStream(&P.hits[rid], h);
-                if (!(done == 1 && owner >= 0)) {  // shadeHit's miss branch: K3a shades only the hit list
+                // a probe batch reads the record of converged rays only (K3a; the
+                // contact combine and per-ray records read every ray's), and its
+                // radiance buffer starts at the sky (k_fill_sky): shadeHit's miss
+                // branch needs no store
+                const bool lean = MODE == 0 && !P.debug;
+                if (!lean || done == 1) stStream(&P.hits[rid], h);
+                if (!lean && !(done == 1 && owner >= 0)) {  // shadeHit's miss branch: K3a shades only the hit list
                     __stcs(&P.rad[3 * rid], R(P.scene.sky[0]));
                     __stcs(&P.rad[3 * rid + 1], R(P.scene.sky[1]));
                     __stcs(&P.rad[3 * rid + 2], R(P.scene.sky[2]));
@@ -1276,6 +1292,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
     k_ray_scan<R><<<1, kScanThreads, 0, st>>>(p);
     k_ray_chunks<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
     k_probe_ray_setup<R><<<static_cast<int>((p.maxItems + 255) / 256), 256, 0, st>>>(p);
+    if (!p.debug) k_fill_sky<R><<<static_cast<int>((p.maxItems + 255) / 256), 256, 0, st>>>(p);
     cudaMemsetAsync(p.ctr, 0, (kLightCtr + (p.scene.n_lights > 1 ? p.scene.n_lights : 1)) * sizeof(unsigned long long), st);
     static int b3 = persistentBlocks(k_shade_rays<R, ST, true>, 128, 0);
     static int b3d = persistentBlocks(k_shade_rays<R, ST, false>, 128, 0, 128 * kMvcSlab * sizeof(R));
@@ -1316,7 +1333,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
         k3<<<p.nCand, kConvThreads, smem, st>>>(p);
     }
     mark(7);
-    if (launches) *launches += p.debug ? 11 : 13;
+    if (launches) *launches += p.debug ? 11 : 14;
 }
 
 // contactGI's per-pixel sum (shading.hpp:686-713): AO from the missed samples,

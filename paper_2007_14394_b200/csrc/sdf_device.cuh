@@ -258,6 +258,43 @@ __device__ __forceinline__ R evalPrim(const DPrim<R>& pr, V3<R> p) {
     }
 }
 
+// The per-kind tail of the FP64 evaluation (primitives.hpp:42-65) from the local
+// point q: the branches only set up sqrt((vx*vx + vy*vy) + vz*vz) + post, and the
+// one square root every kind ends in runs after they reconverge. SDFGI_EVAL_HOIST:
+// the cylinder's radial square root is taken by every lane before the branches
+// (same value; no divergent FP64 sqrt inside the cylinder branch) and max(x, 0)
+// is (x + |x|) / 2 (exact, and only ever squared).
+#ifndef SDFGI_EVAL_HOIST
+#define SDFGI_EVAL_HOIST 1  // C2 step FP64 30.68 -> 30.42 ms
+#endif
+__device__ __forceinline__ double pos0(double x) { return SDFGI_EVAL_HOIST ? (x + fabs(x)) * 0.5 : smax(x, 0.0); }
+__device__ __forceinline__ double evalKindTail(int kind, V3<double> q, double size0, double size1, double size2) {
+    if (kind == 2) return q.z;  // plane
+    double rho = 0.0;
+    if (SDFGI_EVAL_HOIST) rho = sqrt(q.x * q.x + q.y * q.y);
+    double vx, vy, vz, post;
+    if (kind == 1) {  // box
+        const double ax = fabs(q.x) - size0, ay = fabs(q.y) - size1, az = fabs(q.z) - size2;
+        vx = pos0(ax);
+        vy = pos0(ay);
+        vz = pos0(az);
+        post = smin(smax(ax, smax(ay, az)), 0.0);
+    } else if (kind == 3) {  // cylinder
+        if (!SDFGI_EVAL_HOIST) rho = sqrt(q.x * q.x + q.y * q.y);
+        const double dx = rho - size0, dy = fabs(q.z) - size1;
+        vx = pos0(dx);
+        vy = pos0(dy);
+        vz = 0.0;
+        post = smin(smax(dx, dy), 0.0);
+    } else {  // sphere (0) / capsule (4)
+        vx = q.x;
+        vy = q.y;
+        vz = kind == 0 ? q.z : q.z - sclamp(q.z, -size1, size1);
+        post = -size0;
+    }
+    return sqrt(vx * vx + vy * vy + vz * vz) + post;
+}
+
 // FP64 parity mode: the per-kind branches only set up sqrt((vx*vx + vy*vy) + vz*vz)
 // + post, and the one square root every kind ends in runs after the branches have
 // reconverged (lanes of a warp evaluate mixed kinds). Bit-identical to the switch
@@ -276,28 +313,7 @@ __device__ __forceinline__ double evalPrim<double>(const DPrim<double>& pr, V3<d
         q = mk(m0 * q.x + r34.x * q.y + r56.y * q.z, r12.x * q.x + r34.y * q.y + r78.x * q.z,
                r12.y * q.x + r56.x * q.y + r78.y * q.z);
     }
-    const int kind = a3.x;
-    if (kind == 2) return q.z;  // plane
-    double vx, vy, vz, post;
-    if (kind == 1) {  // box
-        const double ax = fabs(q.x) - size0, ay = fabs(q.y) - size1, az = fabs(q.z) - size2;
-        vx = smax(ax, 0.0);
-        vy = smax(ay, 0.0);
-        vz = smax(az, 0.0);
-        post = smin(smax(ax, smax(ay, az)), 0.0);
-    } else if (kind == 3) {  // cylinder
-        const double dx = sqrt(q.x * q.x + q.y * q.y) - size0, dy = fabs(q.z) - size1;
-        vx = smax(dx, 0.0);
-        vy = smax(dy, 0.0);
-        vz = 0.0;
-        post = smin(smax(dx, dy), 0.0);
-    } else {  // sphere (0) / capsule (4)
-        vx = q.x;
-        vy = q.y;
-        vz = kind == 0 ? q.z : q.z - sclamp(q.z, -size1, size1);
-        post = -size0;
-    }
-    return sqrt(vx * vx + vy * vy + vz * vz) + post;
+    return evalKindTail(a3.x, q, size0, size1, size2);
 }
 
 // FP32 perf mode: the five kinds as one branch-free formula so lanes evaluating
@@ -345,28 +361,7 @@ __device__ __forceinline__ double evalPrimStaged(const unsigned char* base, int 
         q = mk(m0 * q.x + r34.x * q.y + r56.y * q.z, r12.x * q.x + r34.y * q.y + r78.x * q.z,
                r12.y * q.x + r56.x * q.y + r78.y * q.z);
     }
-    const int kind = a3.x;
-    if (kind == 2) return q.z;  // plane
-    double vx, vy, vz, post;
-    if (kind == 1) {  // box
-        const double ax = fabs(q.x) - size0, ay = fabs(q.y) - size1, az = fabs(q.z) - size2;
-        vx = smax(ax, 0.0);
-        vy = smax(ay, 0.0);
-        vz = smax(az, 0.0);
-        post = smin(smax(ax, smax(ay, az)), 0.0);
-    } else if (kind == 3) {  // cylinder
-        const double dx = sqrt(q.x * q.x + q.y * q.y) - size0, dy = fabs(q.z) - size1;
-        vx = smax(dx, 0.0);
-        vy = smax(dy, 0.0);
-        vz = 0.0;
-        post = smin(smax(dx, dy), 0.0);
-    } else {  // sphere (0) / capsule (4)
-        vx = q.x;
-        vy = q.y;
-        vz = kind == 0 ? q.z : q.z - sclamp(q.z, -size1, size1);
-        post = -size0;
-    }
-    return sqrt(vx * vx + vy * vy + vz * vz) + post;
+    return evalKindTail(a3.x, q, size0, size1, size2);
 }
 // evalPrimitive of CSR primitive j: from the shared-memory copy in kernels that
 // staged it (STG), else from global memory.
