@@ -76,7 +76,7 @@ template <typename R> struct __align__(16) ParkRay {
 template <typename R> struct __align__(16) ProbeRay {
     R o[3], dir[3];
     int rid;
-    int _pad;
+    R clear;  // the probe's SDF (relocation's final query), < 0: not known
 };
 // A Contact GI ray prepared by k_contact_setup (tMax < 0: sky pixel, no ray).
 template <typename R> struct __align__(16) ContactRay {
@@ -144,6 +144,9 @@ template <typename R> struct WaveParams {
     unsigned long long parkBytes;
     void* cray;  // contact batch: the prepared rays (ContactRay<R>)
     void* pray;  // probe batch: the prepared rays (ProbeRay<R>) in trace order
+    // accel mode 2: every probe's SDF from the relocation that just ran (clear) is its
+    // rays' first query, the same query at the same point (k_probe_ray_setup)
+    int useClear;
     // accel mode 2: a march whose point leaves the candidate grid (which holds every
     // bounded primitive) after starting inside it can never converge again (the grid
     // box is convex, no unbounded primitive): K1 ends it as a miss on the spot

@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(128) k_relocate(RelocParams P) {
         pv.last[3 * gp] = prev.x;
         pv.last[3 * gp + 1] = prev.y;
         pv.last[3 * gp + 2] = prev.z;
+        pv.clear[gp] = d;  // query(pos, inf): the last query ran at the final position
         pv.pos[3 * gp] = pos.x;
         pv.pos[3 * gp + 1] = pos.y;
         pv.pos[3 * gp + 2] = pos.z;
@@ -360,7 +361,7 @@ __global__ void __launch_bounds__(256) k_probe_ray_setup(WaveParams<R> P) {
     r.dir[1] = R(dd.y);
     r.dir[2] = R(dd.z);
     r.rid = static_cast<int>(P.rayStart[s] + i);
-    r._pad = 0;
+    r.clear = P.useClear ? R(P.pc.probes.clear[g]) : R(-1);
     stStream(reinterpret_cast<ProbeRay<R>*>(P.pray) + item, r);
 }
 
@@ -451,6 +452,7 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
     int titem = 0;       // the ray's trace-order position (its hitAt slot)
     bool fresh = false;  // resumed march: its pending t += d was applied before parking
     bool originIn = false;  // the ray starts inside the candidate grid (escape test)
+    R pclear = R(-1);       // the probe's SDF for the march's first query (< 0: query it)
     while (true) {
         __syncwarp();
         unsigned long long item;
@@ -485,11 +487,13 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
                 // neighbouring directions; results are stored by ray id)
                 const ProbeRay<R> r = ldStream(reinterpret_cast<const ProbeRay<R>*>(P.pray) + item);
                 rid = static_cast<unsigned long long>(r.rid);
+                pclear = r.clear;
                 o = mk(r.o[0], r.o[1], r.o[2]);
                 dir = mk(r.dir[0], r.dir[1], r.dir[2]);
                 tMax = R(P.tc.rayTMax);
             } else {
                 rid = item;
+                pclear = R(-1);
                 const ContactRay<R> r = ldStream(reinterpret_cast<const ContactRay<R>*>(P.cray) + item);
                 o = mk(r.o[0], r.o[1], r.o[2]);
                 dir = mk(r.dir[0], r.dir[1], r.dir[2]);
@@ -540,7 +544,7 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
         }
         V3<R> p = o;
         R initD = R(0);
-        bool parkIt = false, escaped = false;
+        bool parkIt = false, escaped = false, known = false;
         int cell = kCellUnknown;  // phase 0: p's cell (parking test), reused by the query
         R cellR = R(0);
         if (active) {
@@ -548,8 +552,10 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
             fresh = false;
             p = o + dir * t;
             if (PHASE == 0 && P.scene.useGrid) cell = gridCell<R>(P.scene.grid, p, &cellR);
-            escaped = PHASE == 0 && originIn && state == 0 && cell < 0;
-            parkIt = PHASE == 0 && park && cell < 0 && !escaped;
+            // the first query of a probe ray is the probe's own SDF, known from the relocation
+            known = PHASE == 0 && state == 0 && step == 0 && pclear >= R(0);
+            escaped = PHASE == 0 && originIn && state == 0 && cell < 0 && !known;
+            parkIt = PHASE == 0 && park && cell < 0 && !escaped && !known;
             if (escaped) {
                 if (ST) ++cnt.steps;
             } else if (parkIt) {
@@ -600,7 +606,9 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
         }
         int o2 = -1;
         R nd = R(0);
-        if (active && !escaped)
+        if (active && known)
+            nd = smin(pclear, initD);  // exactly query(o, initD) = min(SDF(o), initD)
+        else if (active && !escaped)
             nd = query<R, ST, STG>(P.scene, p, initD, &o2, &cnt, PHASE ? seed : -1, cell, cellR,
                               useCellCache<R>() ? &ccache : nullptr);
         if (active) {

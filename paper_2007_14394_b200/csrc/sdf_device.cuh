@@ -844,6 +844,7 @@ struct ProbesView {
     int* alive;
     int* reject;
     int* lastFrame;
+    double* clear;     // the scene SDF at pos, from the last relocation (its final query)
 };
 
 // ProbeAtlas layout (atlas.hpp:119-124): tile (R+2)^2 texels of 3 floats, probe-major.

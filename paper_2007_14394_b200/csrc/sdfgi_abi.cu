@@ -176,7 +176,10 @@ struct Ctx {
     std::vector<CascadeHost> cascades;
     int octRes = 8;
     int totalProbes = 0;
-    DBuf<double> pos, rest, last;
+    DBuf<double> pos, rest, last, clear;
+    // clearValid[slot]: clear holds the SDF at every probe's position of that cascade
+    // (its relocation ran after the last scene, probe or cascade change)
+    std::vector<char> clearValid;
     DBuf<int> alive, reject, lastFrame;
     DBuf<float> atlas[2];
     int front = 0;
@@ -237,7 +240,7 @@ struct Ctx {
         albedo.free(); emission.free(); lights.free(); kindId.free();
         gridStart.free(); gridList.free(); gridCounts.free(); gridU.free(); gridEntry.free(); gridCell.free(); brickCounts.free(); brickStart.free(); brickList.free(); brickSeed.free(); scanTemp.free();
         bvh.free(); unbList.free(); primBox.free(); dynCsr.free();
-        pos.free(); rest.free(); last.free(); alive.free(); reject.free(); lastFrame.free();
+        pos.free(); rest.free(); last.free(); clear.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free(); allRefs.free();
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
         wRayCount.free(); wHitList.free(); wMvcList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); wQuat.free(); cLocal.free(); wHits.free();
@@ -281,6 +284,7 @@ struct Ctx {
         pc.probes.alive = alive.p;
         pc.probes.reject = reject.p;
         pc.probes.lastFrame = lastFrame.p;
+        pc.probes.clear = clear.p;
         return pc;
     }
 
@@ -372,6 +376,8 @@ void slabRange(const CascadeHost& c, int rank, int world, int* lo, int* hi) {
 }
 
 void resetProbes(Ctx* c, int slot) {
+    c->clearValid.resize(c->cascades.size(), 0);
+    c->clearValid[slot] = 0;
     const CascadeHost& cs = c->cascades[slot];
     const int n = cs.count();
     std::vector<double> r(3 * n);
@@ -410,6 +416,8 @@ void reallocProbes(Ctx* c) {
     // the concatenation may move, so reset all.
     c->totalProbes = total;
     c->pos.alloc(3 * static_cast<size_t>(total));
+    c->clear.alloc(std::max(total, 1));
+    c->clearValid.assign(c->cascades.size(), 0);
     c->rest.alloc(3 * static_cast<size_t>(total));
     c->last.alloc(3 * static_cast<size_t>(total));
     c->alive.alloc(total);
@@ -944,6 +952,8 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.currAtlas = c->atlas[1 - c->front].p;
     p.prevZero = c->frontZero() ? 1 : 0;
     p.escape = escapeOk(c);
+    p.useClear = c->accel == 2 && !c->clearValid.empty() &&
+                 std::all_of(c->clearValid.begin(), c->clearValid.end(), [](char v) { return v != 0; });
     p.oct = c->octRes;
     p.frame = frame;
     p.tc.eps = cfg->surface_epsilon;
@@ -1344,6 +1354,7 @@ int sdfgi_scene_upload(void* ctx, const sdfgi_prim* prims, int n_prims, const sd
     return guard([&] {
         Ctx* c = C(ctx);
         const std::vector<sdfgi_prim> prev = c->hPrims;
+        std::fill(c->clearValid.begin(), c->clearValid.end(), 0);  // the SDF may have changed
         uploadSceneArrays(c, prims, n_prims, clusters, n_clusters, member_start, member_idx, lights, n_lights, sky);
         // The acceleration structures are a function of the geometry alone. A static
         // scene re-sent every frame keeps its grid; when primitives move, the ones
@@ -1499,6 +1510,8 @@ int sdfgi_probes_upload(void* ctx, int level, const sdfgi_probe* probes, int n) 
     return guard([&] {
         Ctx* c = C(ctx);
         int s = c->slot(level);
+        c->clearValid.resize(c->cascades.size(), 0);
+        c->clearValid[s] = 0;
         const CascadeHost& cs = c->cascades[s];
         REQ(probes && n == cs.count(), SDFGI_ERR_INVALID, "probe count mismatch");
         std::vector<double> pos(3 * n), rest(3 * n), last(3 * n);
@@ -1637,6 +1650,8 @@ int sdfgi_probes_relocate(void* ctx, int level, double threshold1, double thresh
         CK(cudaEventRecord(c->ev[2], c->stream));
         launch_relocate(p, c->cascades[s].count(), stats != nullptr, c->stream);
         checkLaunch(c);
+        c->clearValid.resize(c->cascades.size(), 0);
+        c->clearValid[s] = 1;  // every probe's SDF at its new position (RelocParams: pv.clear)
         CK(cudaEventRecord(c->ev[3], c->stream));
         c->evReloc = true;
         int rep[4];
@@ -1804,6 +1819,7 @@ int sdfgi_probes_trace_debug(void* ctx, const int32_t* probe_refs, int n_refs, i
             p.records = c->records.p;
             p.debug = 1;
             p.escape = 0;  // per-ray records: the exact march (miss reason, steps)
+            p.useClear = 0;
             launch_wavefront<double>(p, c->persistCap, false, c->stream, nullptr, &c->launches);
         } else {
             WaveParams<float> p = waveParams<float>(c, cfg, frame, c->refs.p, n_refs);
