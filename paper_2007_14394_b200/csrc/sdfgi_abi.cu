@@ -212,6 +212,12 @@ struct Ctx {
     int fibN = -1;
     double* hQuat = nullptr;  // pinned staging of the per-pass quaternions (host_trig.h)
     size_t hQuatN = 0;
+    // the next frame's quaternions, computed on the host while the current pass runs
+    // on the device (a frame loop's next update finds them ready)
+    double* hQuatSpec = nullptr;
+    size_t hQuatSpecN = 0;
+    uint64_t specKey = 0;
+    bool specValid = false;
     // Contact GI's cosineHemisphereDir (lx, ly) per (pixel, sample), host libm; keyed
     // (seed, w, h, samples): the reference's stream has no frame index (shading.hpp:451)
     DBuf<double> cLocal;
@@ -245,6 +251,7 @@ struct Ctx {
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
         wRayCount.free(); wHitList.free(); wMvcList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); wQuat.free(); cLocal.free(); wHits.free();
         if (hQuat) cudaFreeHost(hQuat);
+        if (hQuatSpec) cudaFreeHost(hQuatSpec);
         wVis.free(); wPark.free(); wCRay.free(); wPRay.free(); wSRay.free(); wCtr.free(); perm.free(); wRad.free();
         gbuf.free(); halfDepth.free(); sparseIrr.free(); resolved.free(); indirect.free(); histIrr.free(); composed.free();
         histDepth.free(); halfSrc.free(); sel.free(); sparseValid.free(); sparseAnchor.free();
@@ -980,17 +987,36 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
 // libm (host_trig.h) into pinned memory and copied behind the work already queued
 // on the stream (relocation, the atlas copy), so the host work overlaps it.
 // cand = null: every probe 0..nCand-1.
-void uploadQuats(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand) {
-    const size_t need = 4 * static_cast<size_t>(std::max(nCand, 1));
-    if (c->hQuatN < need) {
-        if (c->hQuat) CK(cudaFreeHost(c->hQuat));
-        c->hQuat = nullptr;
-        c->hQuatN = 0;
-        CK(cudaMallocHost(&c->hQuat, need * sizeof(double)));
-        c->hQuatN = need;
+// Everything a pass's quaternions depend on: seed, frame (or none), the
+// candidates (null = every probe) and the cascades' levels and bases.
+uint64_t quatKey(const Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand) {
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&h](uint64_t v) {
+        for (int i = 0; i < 8; ++i, v >>= 8) h = (h ^ (v & 0xff)) * 1099511628211ull;
+    };
+    mix(cfg->seed);
+    mix(cfg->rotate_per_frame ? static_cast<uint64_t>(static_cast<int64_t>(frame)) : 0xf1b0ull);
+    mix(static_cast<uint64_t>(nCand));
+    mix(cand ? 1 : 0);
+    if (cand)
+        for (int s = 0; s < nCand; ++s) mix(static_cast<uint64_t>(cand[s]));
+    for (const auto& cs : c->cascades) {
+        mix(static_cast<uint64_t>(cs.level));
+        mix(static_cast<uint64_t>(cs.base));
     }
-    // the previous call's copy out of the staging buffer must have finished
-    CK(cudaEventSynchronize(c->quatEv));
+    return h;
+}
+
+void ensurePinned(double*& p, size_t& n, size_t need) {
+    if (n >= need) return;
+    if (p) CK(cudaFreeHost(p));
+    p = nullptr;
+    n = 0;
+    CK(cudaMallocHost(&p, need * sizeof(double)));
+    n = need;
+}
+
+void computeQuats(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand, double* out) {
     std::vector<uint64_t> keys(nCand);
     for (int s = 0; s < nCand; ++s) {
         const int g = cand ? cand[s] : s;
@@ -999,11 +1025,41 @@ void uploadQuats(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int n
             if (g >= c->cascades[k].base) ci = static_cast<int>(k);
         keys[s] = sdfgi_host::probeKey(c->cascades[ci].level, g - c->cascades[ci].base);
     }
-    sdfgi_host::probeQuats(cfg->seed, frame, cfg->rotate_per_frame != 0, keys.data(), nCand, c->hQuat);
+    sdfgi_host::probeQuats(cfg->seed, frame, cfg->rotate_per_frame != 0, keys.data(), nCand, out);
+}
+
+// randomRotation's quaternion of every candidate for this pass (sampleDirections'
+// key: seed, frame or 0xf1b0, probeKey(level, index)), evaluated with the host's
+// libm (host_trig.h) into pinned memory — or taken from the previous call's
+// speculation for this frame — and copied behind the work already queued on the
+// stream. cand = null: every probe 0..nCand-1.
+void uploadQuats(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand) {
+    const size_t need = 4 * static_cast<size_t>(std::max(nCand, 1));
+    // the previous call's copy out of the staging buffer must have finished
+    CK(cudaEventSynchronize(c->quatEv));
+    const uint64_t key = quatKey(c, cfg, frame, cand, nCand);
+    if (c->specValid && c->specKey == key && c->hQuatSpecN >= need) {
+        std::swap(c->hQuat, c->hQuatSpec);
+        std::swap(c->hQuatN, c->hQuatSpecN);
+    } else {
+        ensurePinned(c->hQuat, c->hQuatN, need);
+        computeQuats(c, cfg, frame, cand, nCand, c->hQuat);
+    }
+    c->specValid = false;
     reserve(c->wQuat, need);
     CK(cudaMemcpyAsync(c->wQuat.p, c->hQuat, 4 * static_cast<size_t>(nCand) * sizeof(double), cudaMemcpyHostToDevice,
                        c->stream));
     CK(cudaEventRecord(c->quatEv, c->stream));
+}
+
+// The next frame's quaternions for the same candidates, on the host while the
+// device runs this pass (the staging buffer not in flight).
+void speculateQuats(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand) {
+    if (!cfg->rotate_per_frame) return;  // frame-independent: recomputed (cheap) or identical anyway
+    ensurePinned(c->hQuatSpec, c->hQuatSpecN, 4 * static_cast<size_t>(std::max(nCand, 1)));
+    computeQuats(c, cfg, frame + 1, cand, nCand, c->hQuatSpec);
+    c->specKey = quatKey(c, cfg, frame + 1, cand, nCand);
+    c->specValid = true;
 }
 
 void validateCfg(Ctx* c, const sdfgi_cfg* cfg) {
@@ -1700,6 +1756,7 @@ int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_refs, int fr
             }
             CK(cudaGetLastError());
             c->evUpdate = true;
+            speculateQuats(c, cfg, frame, all ? nullptr : refs.data(), nCand);
         }
         if (c->world > 1) {
             // all-gather the back atlas slabs in place (one broadcast per rank-owned
