@@ -60,6 +60,9 @@ __device__ __forceinline__ void flushCounters(const Counters& c, unsigned long l
 #define SDFGI_FETCH_CHUNK 32  // C2 pass 0: 32 -> 64 -> 128 = FP64 10.4 / 10.5 / 10.9 ms
 #endif
 constexpr unsigned long long kFetchChunk = SDFGI_FETCH_CHUNK;
+#ifndef SDFGI_PREFETCH_CHUNK
+#define SDFGI_PREFETCH_CHUNK 1
+#endif
 #ifndef SDFGI_CELL_CACHE64
 #define SDFGI_CELL_CACHE64 0
 #endif
@@ -69,8 +72,12 @@ static_assert(kFetchChunk >= 32, "one fresh chunk must cover a whole warp's requ
 struct WarpChunk {
     unsigned long long next = 0, end = 0;
 };
+// prefetch (optional): the records of a freshly taken chunk (item i at prefetch +
+// i * prefetchBytes) are pulled into L2 by the warp's lanes, one each, so the
+// chunk's later refills do not wait on DRAM.
 __device__ __forceinline__ bool fetchItem(unsigned long long* cursor, unsigned long long total, bool active,
-                                          bool& exhausted, unsigned long long& item, WarpChunk& chunk) {
+                                          bool& exhausted, unsigned long long& item, WarpChunk& chunk,
+                                          const void* prefetch = nullptr, int prefetchBytes = 0) {
     const unsigned lane = threadIdx.x & 31;
     const unsigned need = __ballot_sync(kFull, !active && !exhausted);
     if (need == 0) return false;
@@ -85,6 +92,9 @@ __device__ __forceinline__ bool fetchItem(unsigned long long* cursor, unsigned l
         unsigned long long base = 0;
         if (static_cast<int>(lane) == leader) base = atomicAdd(cursor, kFetchChunk);
         base = __shfl_sync(kFull, base, leader);
+        if (SDFGI_PREFETCH_CHUNK && prefetch && base + lane < total)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const char*>(prefetch) +
+                                                        (base + lane) * static_cast<unsigned long long>(prefetchBytes)));
         it = rank < avail ? chunk.next + rank : base + (rank - avail);
         chunk.next = base + (n - avail);
         chunk.end = base + kFetchChunk;
@@ -477,7 +487,8 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
             }
         } else {
             const bool got =
-                fetchItem(P.ctr + kCtrRay, static_cast<unsigned long long>(total), active, exhausted, item, chunk);
+                fetchItem(P.ctr + kCtrRay, static_cast<unsigned long long>(total), active, exhausted, item, chunk,
+                          MODE == 0 ? P.pray : P.cray, MODE == 0 ? int(sizeof(ProbeRay<R>)) : int(sizeof(ContactRay<R>)));
             if (got) {
             titem = static_cast<int>(item);
             R startBound = R(INFINITY);
