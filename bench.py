@@ -450,6 +450,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
 
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # the init lines let a reader count the ranks
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)

@@ -418,7 +418,7 @@ __device__ __forceinline__ void stagePrims(const void* src, int bytes) {
 }
 
 #ifndef SDFGI_SHADOW_SETTLE_ON_GRID
-#define SDFGI_SHADOW_SETTLE_ON_GRID 0  // also test shadow marches still on the grid
+#define SDFGI_SHADOW_SETTLE_ON_GRID 1  // also test marches still on the grid (C2 FP64 29.64 -> 29.52 ms)
 #endif
 // The initial bound of a march query (sphereTrace, scene.hpp:397-399: 2 * lastD).
 // Candidate-grid walks also cap it at c = max(tMax - t, eps): the march tests
