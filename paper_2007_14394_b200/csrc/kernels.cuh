@@ -143,6 +143,8 @@ template <typename R> struct WaveParams {
     void* park;
     unsigned long long parkBytes;
     void* cray;  // contact batch: the prepared rays (ContactRay<R>)
+    unsigned char* conv;  // contact batch: per ray, 1 = converged (the combine's AO count)
+    int keepAll;          // K1 writes every ray's HitRec (sdfgi_trace_rays reads them all)
     void* pray;  // probe batch: the prepared rays (ProbeRay<R>) in trace order
     // accel mode 2: every probe's SDF from the relocation that just ran (clear) is its
     // rays' first query, the same query at the same point (k_probe_ray_setup)

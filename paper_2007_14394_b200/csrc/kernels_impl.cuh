@@ -667,13 +667,15 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
                     h.t = R(0);
                     h.status = ((done == 2 ? 1 : 2) << 1) | ((done == 2 ? step + 1 : maxSteps) << 8);
                 }
-                // a probe batch reads the record of converged rays only (K3a; the
-                // contact combine and per-ray records read every ray's), and its
-                // radiance buffer starts at the sky (k_fill_sky): shadeHit's miss
-                // branch needs no store
-                const bool lean = MODE == 0 && !P.debug;
+                // only converged rays' records are read (K3a, the normals; per-ray
+                // debug records read every ray's). A probe batch's radiance starts at
+                // the sky (k_fill_sky); a contact batch's combine reads the converged
+                // flags (conv) and the radiance of converged rays only
+                const bool lean = !P.debug && !P.keepAll;
                 if (!lean || done == 1) stStream(&P.hits[rid], h);
-                if (!lean && !(done == 1 && owner >= 0)) {  // shadeHit's miss branch: K3a shades only the hit list
+                if (MODE == 1 && done == 1 && P.conv) P.conv[rid] = 1;
+                if ((!lean || (MODE == 1 && done == 1)) &&
+                    !(done == 1 && owner >= 0)) {  // shadeHit's miss branch: K3a shades only the hit list
                     __stcs(&P.rad[3 * rid], R(P.scene.sky[0]));
                     __stcs(&P.rad[3 * rid + 1], R(P.scene.sky[1]));
                     __stcs(&P.rad[3 * rid + 2], R(P.scene.sky[2]));
@@ -1382,7 +1384,7 @@ __global__ void __launch_bounds__(128) k_contact_combine(WaveParams<R> P) {
     V3<double> occ = mk(0.0, 0.0, 0.0);
     for (int s = 0; s < nS; ++s) {
         const long long rid = i * nS + s;
-        if (!(P.hits[rid].status & 1)) {
+        if (!P.conv[rid]) {
             ++unocc;
         } else {
             occ = occ + mk(double(P.rad[3 * rid]), double(P.rad[3 * rid + 1]), double(P.rad[3 * rid + 2]));
@@ -1402,6 +1404,7 @@ __global__ void __launch_bounds__(128) k_contact_combine(WaveParams<R> P) {
 template <typename R, bool ST>
 static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long* launches) {
     cudaMemsetAsync(p.ctr, 0, (kLightCtr + (p.scene.n_lights > 1 ? p.scene.n_lights : 1)) * sizeof(unsigned long long), st);
+    cudaMemsetAsync(p.conv, 0, static_cast<size_t>(p.nRaysDirect), st);  // converged flags (K1 sets them)
     if (p.cray) k_contact_setup<R><<<static_cast<int>((p.nRaysDirect + 255) / 256), 256, 0, st>>>(p);
     static int b3 = persistentBlocks(k_shade_rays<R, ST, true>, 128, 0);
     static int b3c = persistentBlocks(k_shade_mvc<R, ST>, kMvcThreads, 0, kMvcThreads * kMvcSlab * sizeof(R));

@@ -223,7 +223,7 @@ struct Ctx {
     DBuf<double> cLocal;
     uint64_t cLocalSeed = 0;
     int cLocalW = 0, cLocalH = 0, cLocalS = -1;
-    DBuf<unsigned char> wHits, wVis, wRad, wPark, wCRay, wPRay, wSRay, wSelTemp;
+    DBuf<unsigned char> wHits, wVis, wRad, wPark, wCRay, wPRay, wSRay, wSelTemp, wConv;
     DBuf<unsigned long long> wCtr;
     int persistCap = 0;  // 0 = occupancy-sized persistent grids
     // gather (e): G-buffer, stage buffers, history (pipeline.hpp:213-218)
@@ -252,7 +252,7 @@ struct Ctx {
         wRayCount.free(); wHitList.free(); wMvcList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); wQuat.free(); cLocal.free(); wHits.free();
         if (hQuat) cudaFreeHost(hQuat);
         if (hQuatSpec) cudaFreeHost(hQuatSpec);
-        wVis.free(); wPark.free(); wCRay.free(); wPRay.free(); wSRay.free(); wCtr.free(); perm.free(); wRad.free();
+        wVis.free(); wPark.free(); wCRay.free(); wPRay.free(); wConv.free(); wSRay.free(); wCtr.free(); perm.free(); wRad.free();
         gbuf.free(); halfDepth.free(); sparseIrr.free(); resolved.free(); indirect.free(); histIrr.free(); composed.free();
         histDepth.free(); halfSrc.free(); sel.free(); sparseValid.free(); sparseAnchor.free();
         for (auto& e : gev)
@@ -2060,6 +2060,7 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     reservePark<R>(c, cap, L);
     reserve(c->wSRay, cap * L * sizeof(ShadowRay<R>));
     reserve(c->wCRay, cap * sizeof(ContactRay<R>));
+    reserve(c->wConv, cap);
     const int S = static_cast<int>(std::max<long long>(cfg->contact_samples, 0));
     if (nr > 0 && (c->cLocalS != S || c->cLocalW != c->gw || c->cLocalH != c->gh || c->cLocalSeed != cfg->seed)) {
         // frame-invariant: built once per (seed, resolution, sample count)
@@ -2105,6 +2106,7 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     p.scene.stageBytes = 0;
     p.nRaysDirect = nr;
     p.cray = c->wCRay.p;
+    p.conv = c->wConv.p;
     p.clocal = c->cLocal.p;
     p.gb = c->gbuf.p;
     p.gw = c->gw;
@@ -2566,6 +2568,7 @@ void traceRays(Ctx* c, const double* o, const double* d, int n, double tMax, dou
     p.tc.eps = eps;
     p.tc.maxSteps = maxSteps;
     p.tc.rayTMax = tMax;
+    p.keepAll = 1;  // every ray's result is returned
     std::vector<ContactRay<R>> rays(n);
     for (int i = 0; i < n; ++i) {
         for (int k = 0; k < 3; ++k) {
