@@ -334,8 +334,11 @@ class StepRunner:
         work = dict.fromkeys(("k1", "k2", "shade", "convolve"), 0.0)
         prec = dev.precision
         for p in range(PASSES):
-            stage.relocate_all(stats=stats)
-            r = api.updateProbes(dev, stage.cfg, p, None, stats=stats)
+            if stats:  # relocation and update counters apart: one call each
+                stage.relocate_all(stats=True)
+                r = api.updateProbes(dev, stage.cfg, p, None, stats=True)
+            else:  # the probe stage of pipeline.hpp:108-151 in one call, one host sync
+                r = dev.probe_stage(p, stage.cfg)[1]
             if stats:
                 res, st = r
                 tc = dev.last_trace_counters()
@@ -692,10 +695,8 @@ def e2e_run(args, dev, stage, scene, barrier, dist, torch):
         dev.upload_probes(0, probes_host)
         r = 0
         for p in range(PASSES):
-            stage.relocate_all()
-            res = api.updateProbes(dev, stage.cfg, p)
+            _, res = stage.run_pass(p)  # relocation + update (sdfgi_probe_stage) + swap
             r += int(res["rays_traced"])
-            dev.swap()
         dev.atlas(0, 0, out=atlas_host)  # straight into the pinned buffer
         dt = time.perf_counter() - t0
         if i > 0:  # first iteration is a warm-up

@@ -279,6 +279,20 @@ SDFGI_API int sdfgi_probes_relocate(void* ctx, int level, double threshold1, dou
  * world > 1 each rank updates its z-slab and the back atlas is all-gathered. */
 SDFGI_API int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_refs, int frame,
                         const sdfgi_cfg* cfg, sdfgi_update_result* result, sdfgi_stats* stats);
+/* The whole probe stage of renderFrame (pipeline.hpp:108-151; the recenter of
+ * :110-113 stays with the caller, sdfgi_cascade_set) in one call and one host
+ * synchronisation:
+ * updateProbePositions for every cascade with cfg's thresholds (threshold*_frac x
+ * the cascade's spacing, max_descent_steps, gradient_step), then — with
+ * cfg->probe_budget > 0 — selectProbesForUpdate from cam_pos/cam_fwd, and the
+ * updateProbe pass of sdfgi_probes_update (NULL refs = every probe when the budget
+ * is 0; cam_pos/cam_fwd may then be NULL). reports: one per cascade in the order
+ * sdfgi_cascade_set created them (n_reports >= cascade count) or NULL; stats sum relocation and update.
+ * Same results as the sequence of sdfgi_probes_relocate / sdfgi_select_probes /
+ * sdfgi_probes_update calls it replaces. */
+SDFGI_API int sdfgi_probe_stage(void* ctx, int frame, const sdfgi_cfg* cfg, const double cam_pos[3],
+                                const double cam_fwd[3], sdfgi_reloc_report* reports, int n_reports,
+                                sdfgi_update_result* result, sdfgi_stats* stats);
 /* readIdx swap at frame end (pipeline.hpp:220). */
 SDFGI_API int sdfgi_atlas_swap(void* ctx);
 /* which = 0: front (read) atlas, 1: back (write) atlas. Layout = ProbeAtlas::raw()

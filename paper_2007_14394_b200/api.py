@@ -168,14 +168,21 @@ class ProbeStage:
 
     def run_pass(self, frame, stats=False, camera=None):
         """One pass; cfg.probe_budget > 0 schedules selectProbesForUpdate's refs
-        (pipeline.hpp:133-135) from `camera` (position, forward; default: the scene's)."""
-        reps = self.relocate_all(stats)
+        (pipeline.hpp:133-135) from `camera` (position, forward; default: the scene's).
+        Without stats the pass is one sdfgi_probe_stage call (one host sync); with
+        stats it keeps the per-call sequence so relocation and update counters stay
+        apart."""
         budget = int(self.cfg["probe_budget"][0])
-        refs = None
+        pos = fwd = None
         if budget > 0:
             cam = self.scene.camera if camera is None else None
             pos, fwd = (cam.position, cam.forward) if cam is not None else camera
-            refs = selectProbesForUpdate(self.dev, pos, fwd, budget, frame)
+        if not stats:
+            reps, upd = self.dev.probe_stage(frame, self.cfg, pos, fwd)
+            self.dev.swap()
+            return list(reps[:self.levels]), upd
+        reps = self.relocate_all(stats)
+        refs = selectProbesForUpdate(self.dev, pos, fwd, budget, frame) if budget > 0 else None
         upd = updateProbes(self.dev, self.cfg, frame, refs, stats)
         self.dev.swap()
         return reps, upd

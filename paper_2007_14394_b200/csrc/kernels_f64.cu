@@ -253,7 +253,7 @@ void launch_grid_list(const GridBuildParams& p, int ncells, bool fill, cudaStrea
 }
 
 void launch_relocate(const RelocParams& p, int nProbes, bool stats, cudaStream_t st) {
-    const int blocks = (nProbes + 127) / 128;
+    const int blocks = (nProbes + kRelocLanes - 1) / kRelocLanes;
     if (stats)
         k_relocate<true><<<blocks, 128, 0, st>>>(p);
     else

@@ -109,44 +109,71 @@ __device__ __forceinline__ bool fetchItem(unsigned long long* cursor, unsigned l
 }
 
 // ------------------------------------------------------------ (d) relocation
-// updateProbePositions, probe_volume.hpp:99-143, one thread per probe of one cascade.
+// updateProbePositions, probe_volume.hpp:99-143, one 8-lane group per probe of one
+// cascade (kRelocLanes probes per 128-thread block): the six sceneGradient
+// queries of a descent step run on lanes 0-5 of the group at once, so a step
+// costs two query latencies instead of seven. Every lane of the group repeats the
+// step's arithmetic on the same values (identical results); lane 0 runs the
+// remaining queries and writes the probe.
+constexpr int kRelocGroup = 8;
+constexpr int kRelocLanes = 128 / kRelocGroup;
 template <bool ST>
 __global__ void __launch_bounds__(128) k_relocate(RelocParams P) {
     const CascadeDev& c = P.pc.cas[P.cascade];
     const int n = c.res[0] * c.res[1] * c.res[2];
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.x * kRelocLanes + threadIdx.x / kRelocGroup;
+    const int sub = threadIdx.x % kRelocGroup;
+    const bool valid = i < n;
     Counters cnt;
     cnt.zero();
     int relocated = 0, rejected = 0, dead = 0;
-    if (i < n) {
-        const int gp = c.base + i;
-        const ProbesView& pv = P.pc.probes;
-        const SceneView<double>& s = P.scene;
-        const double inf = INFINITY;
-        V3<double> prev = mk(pv.pos[3 * gp], pv.pos[3 * gp + 1], pv.pos[3 * gp + 2]);
-        V3<double> rest = mk(pv.rest[3 * gp], pv.rest[3 * gp + 1], pv.rest[3 * gp + 2]);
-        V3<double> pos = rest;
-        double budgetTotal = 0.5 * c.spacing;
-        double d = query<double, ST>(s, pos, inf, nullptr, &cnt);
+    const int gp = c.base + (valid ? i : 0);
+    const ProbesView& pv = P.pc.probes;
+    const SceneView<double>& s = P.scene;
+    const double inf = INFINITY;
+    V3<double> pos = mk(0.0, 0.0, 0.0), rest = pos, prev = pos;
+    if (valid) {
+        prev = mk(pv.pos[3 * gp], pv.pos[3 * gp + 1], pv.pos[3 * gp + 2]);
+        rest = mk(pv.rest[3 * gp], pv.rest[3 * gp + 1], pv.rest[3 * gp + 2]);
+        pos = rest;
+    }
+    double d = 0;
+    if (valid && sub == 0) d = query<double, ST>(s, pos, inf, nullptr, &cnt);
+    d = __shfl_sync(kFull, d, 0, kRelocGroup);
+    const bool descend = valid && d < P.th1;
+    double budget = 0.5 * c.spacing;
+    const double h = P.gradStep;
+    for (int step = 0; step < P.maxSteps; ++step) {
+        const bool go = descend && d < P.th1 && budget > 0;
+        if (!__any_sync(kFull, go)) break;
+        // sceneGradient, scene.hpp:360-371: lane k queries axis k / 2, +h for even k
+        double qv = 0;
+        if (go && sub < 6) {
+            const int ax = sub >> 1;
+            const double off = (sub & 1) ? -h : h;
+            const V3<double> q = mk(ax == 0 ? pos.x + off : pos.x, ax == 1 ? pos.y + off : pos.y,
+                                    ax == 2 ? pos.z + off : pos.z);  // (pos.x - h as pos.x + (-h): exact)
+            qv = query<double, ST>(s, q, inf, nullptr, &cnt);
+        }
+        double v[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) v[k] = __shfl_sync(kFull, qv, k, kRelocGroup);
+        double nd = 0;
+        if (go) {
+            const V3<double> g = mk(v[0] - v[1], v[2] - v[3], v[4] - v[5]);
+            const double gn = length(g);
+            const V3<double> dir = (gn < 1e-6 * 2 * h) ? mk(1.0, 0.0, 0.0) : g / gn;
+            const double want = smin((P.th1 - d) * 1.25, budget);
+            pos = pos + dir * want;
+            budget -= want;
+            if (sub == 0) nd = query<double, ST>(s, pos, inf, nullptr, &cnt);
+        }
+        nd = __shfl_sync(kFull, nd, 0, kRelocGroup);
+        if (go) d = nd;
+    }
+    if (valid && sub == 0) {
         bool alive = true;
-        if (d < P.th1) {
-            double budget = budgetTotal;
-            const double h = P.gradStep;
-            for (int step = 0; step < P.maxSteps && d < P.th1 && budget > 0; ++step) {
-                // sceneGradient, scene.hpp:360-371
-                V3<double> g = mk(query<double, ST>(s, mk(pos.x + h, pos.y, pos.z), inf, nullptr, &cnt) -
-                                      query<double, ST>(s, mk(pos.x - h, pos.y, pos.z), inf, nullptr, &cnt),
-                                  query<double, ST>(s, mk(pos.x, pos.y + h, pos.z), inf, nullptr, &cnt) -
-                                      query<double, ST>(s, mk(pos.x, pos.y - h, pos.z), inf, nullptr, &cnt),
-                                  query<double, ST>(s, mk(pos.x, pos.y, pos.z + h), inf, nullptr, &cnt) -
-                                      query<double, ST>(s, mk(pos.x, pos.y, pos.z - h), inf, nullptr, &cnt));
-                double gn = length(g);
-                V3<double> dir = (gn < 1e-6 * 2 * h) ? mk(1.0, 0.0, 0.0) : g / gn;
-                double want = smin((P.th1 - d) * 1.25, budget);
-                pos = pos + dir * want;
-                budget -= want;
-                d = query<double, ST>(s, pos, inf, nullptr, &cnt);
-            }
+        if (descend) {
             alive = d >= P.th1;
             if (alive && length(pos - rest) > 1e-12) ++relocated;
         }

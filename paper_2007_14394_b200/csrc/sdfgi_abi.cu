@@ -210,6 +210,7 @@ struct Ctx {
     DBuf<double> wRot, fib, wQuat;
     DBuf<int> perm;
     int fibN = -1;
+    int* hReport = nullptr;  // pinned: relocation reports of sdfgi_probe_stage (read after its one sync)
     double* hQuat = nullptr;  // pinned staging of the per-pass quaternions (host_trig.h)
     size_t hQuatN = 0;
     // the next frame's quaternions, computed on the host while the current pass runs
@@ -250,6 +251,7 @@ struct Ctx {
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free(); allRefs.free();
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
         wRayCount.free(); wHitList.free(); wMvcList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); wQuat.free(); cLocal.free(); wHits.free();
+        if (hReport) cudaFreeHost(hReport);
         if (hQuat) cudaFreeHost(hQuat);
         if (hQuatSpec) cudaFreeHost(hQuatSpec);
         wVis.free(); wPark.free(); wCRay.free(); wPRay.free(); wConv.free(); wSRay.free(); wCtr.free(); perm.free(); wRad.free();
@@ -1154,7 +1156,8 @@ int sdfgi_ctx_create(int device, int rank, int world, const uint8_t* nccl_uid, i
             for (auto& e : c->kev) CK(cudaEventCreate(&e));
             CK(cudaEventRecord(c->quatEv, c->stream));
             c->scratch.alloc(kShadowStats + 32);
-            c->report.alloc(4);
+            c->report.alloc(4 * kMaxCascades);
+            CK(cudaMallocHost(&c->hReport, 4 * kMaxCascades * sizeof(int)));
             if (world > 1) {
                 REQ(nccl_uid, SDFGI_ERR_INVALID, "world > 1 needs an NCCL unique id");
                 ncclUniqueId id;
@@ -1683,125 +1686,190 @@ int sdfgi_select_probes(void* ctx, const double cam_pos[3], const double cam_fwd
     });
 }
 
+// updateProbePositions for cascade slot s, enqueued on the context stream (no host
+// synchronisation): counts land in rep[0..2] on the device.
+void relocEnqueue(Ctx* c, int s, double threshold1, double threshold2, int max_descent_steps,
+                  double gradient_step, bool stats, int* rep, bool clearCounters = true) {
+    RelocParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.scene = c->sceneView<double>();
+    p.pc = c->probeCommon();
+    p.cascade = s;
+    p.th1 = threshold1;
+    p.th2 = threshold2;
+    p.maxSteps = max_descent_steps;
+    p.gradStep = gradient_step;
+    p.report = rep;
+    p.stats = c->scratch.p;
+    CK(cudaMemsetAsync(rep, 0, 4 * sizeof(int), c->stream));
+    if (clearCounters) CK(cudaMemsetAsync(c->scratch.p, 0, (kShadowStats + 32) * 8, c->stream));
+    // relocation is replicated on every rank (deterministic, bit-exact): no exchange
+    CK(cudaEventRecord(c->ev[2], c->stream));
+    launch_relocate(p, c->cascades[s].count(), stats, c->stream);
+    checkLaunch(c);
+    c->clearValid.resize(c->cascades.size(), 0);
+    c->clearValid[s] = 1;  // every probe's SDF at its new position (RelocParams: pv.clear)
+    CK(cudaEventRecord(c->ev[3], c->stream));
+    c->evReloc = true;
+}
+
+void fillReport(sdfgi_reloc_report* report, const int* rep) {
+    report->relocated = rep[0];
+    report->rejected = rep[1];
+    report->dead = rep[2];
+    report->_pad = 0;
+}
+
 int sdfgi_probes_relocate(void* ctx, int level, double threshold1, double threshold2, int max_descent_steps,
                           double gradient_step, sdfgi_reloc_report* report, sdfgi_stats* stats) {
     return guard([&] {
         Ctx* c = C(ctx);
         requireProbes(c);
         int s = c->slot(level);
-        RelocParams p;
-        std::memset(&p, 0, sizeof(p));
-        p.scene = c->sceneView<double>();
-        p.pc = c->probeCommon();
-        p.cascade = s;
-        p.th1 = threshold1;
-        p.th2 = threshold2;
-        p.maxSteps = max_descent_steps;
-        p.gradStep = gradient_step;
-        p.report = c->report.p;
-        p.stats = c->scratch.p;
-        CK(cudaMemsetAsync(c->report.p, 0, 4 * sizeof(int), c->stream));
-        CK(cudaMemsetAsync(c->scratch.p, 0, (kShadowStats + 32) * 8, c->stream));
-        // relocation is replicated on every rank (deterministic, bit-exact): no exchange
-        CK(cudaEventRecord(c->ev[2], c->stream));
-        launch_relocate(p, c->cascades[s].count(), stats != nullptr, c->stream);
-        checkLaunch(c);
-        c->clearValid.resize(c->cascades.size(), 0);
-        c->clearValid[s] = 1;  // every probe's SDF at its new position (RelocParams: pv.clear)
-        CK(cudaEventRecord(c->ev[3], c->stream));
-        c->evReloc = true;
+        relocEnqueue(c, s, threshold1, threshold2, max_descent_steps, gradient_step, stats != nullptr, c->report.p);
         int rep[4];
         CK(cudaMemcpyAsync(rep, c->report.p, sizeof(rep), cudaMemcpyDeviceToHost, c->stream));
         readCounters(c, stats, nullptr, 0);
-        if (report) {
-            report->relocated = rep[0];
-            report->rejected = rep[1];
-            report->dead = rep[2];
-            report->_pad = 0;
-        }
+        if (report) fillReport(report, rep);
     });
+}
+
+// The update half of the probe stage (pipeline.hpp:126-151); ends with the one
+// host synchronisation of the call (readCounters).
+void updateBody(Ctx* c, const int32_t* probe_refs, int n_refs, int frame, const sdfgi_cfg* cfg,
+                sdfgi_update_result* result, sdfgi_stats* stats) {
+    requireProbes(c);
+    validateCfg(c, cfg);
+    std::vector<int> refs = selectRefs(c, probe_refs, n_refs);
+    float* back = c->atlas[1 - c->front].p;
+    const float* frontp = c->atlas[c->front].p;
+    // atlas_[write] = atlas_[read] (pipeline.hpp:131); updated tiles are overwritten
+    CK(cudaMemcpyAsync(back, frontp, c->atlasFloats() * 4, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemsetAsync(c->scratch.p, 0, (kShadowStats + 32) * 8, c->stream));
+    const bool all = (probe_refs == nullptr && c->world == 1);
+    // back <- front (copied above) + the updated tiles: still all-zero only if no
+    // probe anywhere is updated this pass
+    const bool anyUpdate = probe_refs == nullptr ? c->totalProbes > 0 : n_refs > 0;
+    c->atlasZero[1 - c->front] = c->atlasZero[c->front];
+    if (anyUpdate) std::fill(c->atlasZero[1 - c->front].begin(), c->atlasZero[1 - c->front].end(), 0);
+    if (!all) c->refs.upload(refs.data(), refs.size(), c->stream);
+    const int nCand = static_cast<int>(refs.size());
+    if (nCand > 0) {
+        const int* cand = all ? nullptr : c->refs.p;
+        uploadQuats(c, cfg, frame, all ? nullptr : refs.data(), nCand);
+        if (c->precision == SDFGI_F64) {
+            WaveParams<double> p = waveParams<double>(c, cfg, frame, cand, nCand);
+            launch_wavefront<double>(p, c->persistCap, stats != nullptr, c->stream, c->kev,
+                                     &c->launches);
+        } else {
+            WaveParams<float> p = waveParams<float>(c, cfg, frame, cand, nCand);
+            launch_wavefront<float>(p, c->persistCap, stats != nullptr, c->stream, c->kev,
+                                    &c->launches);
+        }
+        CK(cudaGetLastError());
+        c->evUpdate = true;
+        speculateQuats(c, cfg, frame, all ? nullptr : refs.data(), nCand);
+    }
+    if (c->world > 1) {
+        // all-gather the back atlas slabs in place (one broadcast per rank-owned
+        // slab: slabs may be uneven), then sum counters / max the jitter metric.
+        NK(ncclGroupStart());
+        for (auto& cs : c->cascades)
+            for (int r = 0; r < c->world; ++r) {
+                int lo, hi;
+                slabRange(cs, r, c->world, &lo, &hi);
+                if (hi <= lo) continue;
+                float* ptr = back + static_cast<size_t>(lo) * c->tileFloats();
+                NK(ncclBroadcast(ptr, ptr, static_cast<size_t>(hi - lo) * c->tileFloats(), ncclFloat, r, c->comm,
+                                 c->stream));
+            }
+        NK(ncclGroupEnd());
+        NK(ncclAllReduce(c->scratch.p, c->scratch.p, 14, ncclUint64, ncclSum, c->comm, c->stream));
+        NK(ncclAllReduce(c->scratch.p + kShadowStats, c->scratch.p + kShadowStats, 14, ncclUint64, ncclSum,
+                         c->comm, c->stream));
+        NK(ncclAllReduce(c->scratch.p + 16, c->scratch.p + 16, 1, ncclUint64, ncclMax, c->comm, c->stream));
+        NK(ncclAllReduce(c->scratch.p + 17, c->scratch.p + 17, 2, ncclUint64, ncclSum, c->comm, c->stream));
+    }
+    if (c->world > 1) {
+        // every rank marks every updated probe (probe_update.hpp:208-209) on the
+        // device, so the replicated probe state stays identical without an exchange
+        const int* ids = nullptr;
+        int nAll = c->totalProbes;
+        if (probe_refs) {
+            std::vector<int> allRefs(n_refs);
+            for (int i = 0; i < n_refs; ++i)
+                allRefs[i] = c->cascades[c->slot(probe_refs[2 * i])].base + probe_refs[2 * i + 1];
+            c->allRefs.upload(allRefs.data(), allRefs.size(), c->stream);
+            ids = c->allRefs.p;
+            nAll = n_refs;
+        }
+        launch_mark_updated(ids, nAll, frame, c->alive.p, c->reject.p, c->lastFrame.p, c->stream);
+        checkLaunch(c);
+    }
+    unsigned long long tail[3];
+    readCounters(c, stats, tail, 3);
+    if (result) {
+        double md;
+        std::memcpy(&md, &tail[0], 8);
+        result->max_texel_delta = md;
+        result->rays_traced = static_cast<int64_t>(tail[1]);
+        result->probes_updated = static_cast<int64_t>(tail[2] & 0xffffffffull);
+    }
 }
 
 int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_refs, int frame, const sdfgi_cfg* cfg,
                         sdfgi_update_result* result, sdfgi_stats* stats) {
+    return guard([&] { updateBody(C(ctx), probe_refs, n_refs, frame, cfg, result, stats); });
+}
+
+int sdfgi_probe_stage(void* ctx, int frame, const sdfgi_cfg* cfg, const double cam_pos[3], const double cam_fwd[3],
+                      sdfgi_reloc_report* reports, int n_reports, sdfgi_update_result* result, sdfgi_stats* stats) {
     return guard([&] {
         Ctx* c = C(ctx);
         requireProbes(c);
         validateCfg(c, cfg);
-        std::vector<int> refs = selectRefs(c, probe_refs, n_refs);
-        float* back = c->atlas[1 - c->front].p;
-        const float* frontp = c->atlas[c->front].p;
-        // atlas_[write] = atlas_[read] (pipeline.hpp:131); updated tiles are overwritten
-        CK(cudaMemcpyAsync(back, frontp, c->atlasFloats() * 4, cudaMemcpyDeviceToDevice, c->stream));
+        const int nc = static_cast<int>(c->cascades.size());
+        REQ(reports == nullptr || n_reports >= nc, SDFGI_ERR_INVALID, "reports: one per cascade");
+        // probe placement for every cascade (pipeline.hpp:108-123), thresholds as
+        // cfg_.threshold1/2(spacing): fraction x spacing
         CK(cudaMemsetAsync(c->scratch.p, 0, (kShadowStats + 32) * 8, c->stream));
-        const bool all = (probe_refs == nullptr && c->world == 1);
-        // back <- front (copied above) + the updated tiles: still all-zero only if no
-        // probe anywhere is updated this pass
-        const bool anyUpdate = probe_refs == nullptr ? c->totalProbes > 0 : n_refs > 0;
-        c->atlasZero[1 - c->front] = c->atlasZero[c->front];
-        if (anyUpdate) std::fill(c->atlasZero[1 - c->front].begin(), c->atlasZero[1 - c->front].end(), 0);
-        if (!all) c->refs.upload(refs.data(), refs.size(), c->stream);
-        const int nCand = static_cast<int>(refs.size());
-        if (nCand > 0) {
-            const int* cand = all ? nullptr : c->refs.p;
-            uploadQuats(c, cfg, frame, all ? nullptr : refs.data(), nCand);
-            if (c->precision == SDFGI_F64) {
-                WaveParams<double> p = waveParams<double>(c, cfg, frame, cand, nCand);
-                launch_wavefront<double>(p, c->persistCap, stats != nullptr, c->stream, c->kev,
-                                         &c->launches);
-            } else {
-                WaveParams<float> p = waveParams<float>(c, cfg, frame, cand, nCand);
-                launch_wavefront<float>(p, c->persistCap, stats != nullptr, c->stream, c->kev,
-                                        &c->launches);
-            }
-            CK(cudaGetLastError());
-            c->evUpdate = true;
-            speculateQuats(c, cfg, frame, all ? nullptr : refs.data(), nCand);
+        for (int s = 0; s < nc; ++s) {
+            const double sp = c->cascades[s].spacing;
+            relocEnqueue(c, s, cfg->threshold1_frac * sp, cfg->threshold2_frac * sp,
+                         static_cast<int>(cfg->max_descent_steps), cfg->gradient_step, stats != nullptr,
+                         c->report.p + 4 * s, false);
         }
-        if (c->world > 1) {
-            // all-gather the back atlas slabs in place (one broadcast per rank-owned
-            // slab: slabs may be uneven), then sum counters / max the jitter metric.
-            NK(ncclGroupStart());
-            for (auto& cs : c->cascades)
-                for (int r = 0; r < c->world; ++r) {
-                    int lo, hi;
-                    slabRange(cs, r, c->world, &lo, &hi);
-                    if (hi <= lo) continue;
-                    float* ptr = back + static_cast<size_t>(lo) * c->tileFloats();
-                    NK(ncclBroadcast(ptr, ptr, static_cast<size_t>(hi - lo) * c->tileFloats(), ncclFloat, r, c->comm,
-                                     c->stream));
-                }
-            NK(ncclGroupEnd());
-            NK(ncclAllReduce(c->scratch.p, c->scratch.p, 14, ncclUint64, ncclSum, c->comm, c->stream));
-            NK(ncclAllReduce(c->scratch.p + kShadowStats, c->scratch.p + kShadowStats, 14, ncclUint64, ncclSum,
-                             c->comm, c->stream));
-            NK(ncclAllReduce(c->scratch.p + 16, c->scratch.p + 16, 1, ncclUint64, ncclMax, c->comm, c->stream));
-            NK(ncclAllReduce(c->scratch.p + 17, c->scratch.p + 17, 2, ncclUint64, ncclSum, c->comm, c->stream));
+        sdfgi_stats relocStats;
+        std::memset(&relocStats, 0, sizeof(relocStats));
+        if (stats) readCounters(c, &relocStats, nullptr, 0);  // the update clears the counters
+        std::vector<int32_t> refs;
+        const int32_t* pr = nullptr;
+        int nr = 0;
+        if (cfg->probe_budget > 0) {
+            // selectProbesForUpdate after placement (pipeline.hpp:132-135)
+            REQ(cam_pos && cam_fwd, SDFGI_ERR_INVALID, "a probe budget needs the camera");
+            refs.resize(2 * static_cast<size_t>(std::min<int64_t>(cfg->probe_budget, c->totalProbes)));
+            int rc = sdfgi_select_probes(ctx, cam_pos, cam_fwd, static_cast<int>(cfg->probe_budget), frame,
+                                         refs.data(), &nr);
+            REQ(rc == SDFGI_OK, rc, "probe selection failed");
+            pr = refs.data();
         }
-        if (c->world > 1) {
-            // every rank marks every updated probe (probe_update.hpp:208-209) on the
-            // device, so the replicated probe state stays identical without an exchange
-            const int* ids = nullptr;
-            int nAll = c->totalProbes;
-            if (probe_refs) {
-                std::vector<int> allRefs(n_refs);
-                for (int i = 0; i < n_refs; ++i)
-                    allRefs[i] = c->cascades[c->slot(probe_refs[2 * i])].base + probe_refs[2 * i + 1];
-                c->allRefs.upload(allRefs.data(), allRefs.size(), c->stream);
-                ids = c->allRefs.p;
-                nAll = n_refs;
-            }
-            launch_mark_updated(ids, nAll, frame, c->alive.p, c->reject.p, c->lastFrame.p, c->stream);
-            checkLaunch(c);
-        }
-        unsigned long long tail[3];
-        readCounters(c, stats, tail, 3);
-        if (result) {
-            double md;
-            std::memcpy(&md, &tail[0], 8);
-            result->max_texel_delta = md;
-            result->rays_traced = static_cast<int64_t>(tail[1]);
-            result->probes_updated = static_cast<int64_t>(tail[2] & 0xffffffffull);
+        // pinned destination: the copy stays asynchronous until the update's sync
+        CK(cudaMemcpyAsync(c->hReport, c->report.p, sizeof(int) * 4 * nc, cudaMemcpyDeviceToHost, c->stream));
+        static const int32_t kNoRefs[2] = {0, 0};
+        if (cfg->probe_budget > 0 && nr == 0) pr = kNoRefs;  // budget selected nothing: not "every probe"
+        updateBody(c, pr, nr, frame, cfg, result, stats);  // synchronises
+        if (reports)
+            for (int s = 0; s < nc; ++s) fillReport(&reports[s], c->hReport + 4 * s);
+        if (stats) {
+            stats->sdf_queries += relocStats.sdf_queries;
+            stats->clusters_visited += relocStats.clusters_visited;
+            stats->clusters_skipped += relocStats.clusters_skipped;
+            stats->primitive_evals += relocStats.primitive_evals;
+            stats->trace_steps += relocStats.trace_steps;
+            stats->sphere_traces += relocStats.sphere_traces;
+            stats->shadow_traces += relocStats.shadow_traces;
+            stats->visibility_traces += relocStats.visibility_traces;
         }
     });
 }

@@ -46,6 +46,7 @@ _SIGS = {
     "sdfgi_probes_download": [_P, _I, _P, _I],
     "sdfgi_probes_relocate": [_P, _I, _D, _D, _I, _D, _P, _P],
     "sdfgi_probes_update": [_P, _P, _I, _I, _P, _P, _P],
+    "sdfgi_probe_stage": [_P, _I, _P, _P, _P, _P, _I, _P, _P],
     "sdfgi_atlas_swap": [_P],
     "sdfgi_atlas_download": [_P, _I, _I, _P, _SZ],
     "sdfgi_atlas_upload": [_P, _I, _I, _P, _SZ],
@@ -403,6 +404,19 @@ class Device:
         _call("sdfgi_probes_update", self._ctx, _ptr(r), 0 if r is None else len(r), int(frame), _ptr(cfg),
               _ptr(res), _ptr(st))
         return (res[0], st[0]) if stats else res[0]
+
+    def probe_stage(self, frame, cfg, cam_pos=None, cam_fwd=None, stats=False):
+        """Relocation of every cascade + (budgeted) selection + update in one call
+        (sdfgi_probe_stage): -> (reports per cascade, result[, stats])."""
+        cfg = np.ascontiguousarray(cfg, sio.CFG_DTYPE)
+        reps = np.zeros(max(len(self.levels), 1), RELOC_DTYPE)  # cascade creation order
+        res = np.zeros(1, RESULT_DTYPE)
+        st = np.zeros(1, sio.STATS_DTYPE) if stats else None
+        cp = None if cam_pos is None else np.ascontiguousarray(cam_pos, np.float64)
+        cf = None if cam_fwd is None else np.ascontiguousarray(cam_fwd, np.float64)
+        _call("sdfgi_probe_stage", self._ctx, int(frame), _ptr(cfg), _ptr(cp), _ptr(cf), _ptr(reps), len(reps),
+              _ptr(res), _ptr(st))
+        return (reps, res[0], st[0]) if stats else (reps, res[0])
 
     def select(self, cam_pos, cam_fwd, budget, frame):
         """selectProbesForUpdate on the device -> (n, 2) int32 (level, index)."""

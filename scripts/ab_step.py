@@ -8,8 +8,15 @@ import numpy as np
 sys.path.insert(0, ".")
 import torch  # noqa: E402
 
-from paper_2007_14394_b200 import api, scene_io  # noqa: E402
+from paper_2007_14394_b200 import api, runtime, scene_io  # noqa: E402
 from paper_2007_14394_b200.runtime import Device  # noqa: E402
+
+if os.environ.get("SDFGI_LIB"):  # an older variant may lack newer entry points
+    import ctypes
+
+    _probe = ctypes.CDLL(os.environ["SDFGI_LIB"])
+    runtime._SIGS = {k: v for k, v in runtime._SIGS.items() if hasattr(_probe, k)}
+fused = os.environ.get("FUSED") == "1"  # one sdfgi_probe_stage call per pass
 
 prec = sys.argv[1] if len(sys.argv) > 1 else "f64"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
@@ -28,8 +35,11 @@ with Device(0, precision=prec) as dev:
         e0.record(ext)
         pp = []
         for p in range(3):
-            stage.relocate_all()
-            api.updateProbes(dev, stage.cfg, p)
+            if fused:
+                dev.probe_stage(p, stage.cfg)
+            else:
+                stage.relocate_all()
+                api.updateProbes(dev, stage.cfg, p)
             pp.append(dev.last_kernel_ms()[0])
             dev.swap()
         e1.record(ext)
@@ -39,4 +49,5 @@ with Device(0, precision=prec) as dev:
             per_pass.append(pp)
     pp = np.median(np.array(per_pass), axis=0)
     lib = os.environ.get("SDFGI_LIB", "cur").split("/")[-2] if os.environ.get("SDFGI_LIB") else "cur"
+    lib += "+fused" if fused else ""
     print(f"{lib:12s} {prec} step {np.median(steps):7.2f} ms  passes " + " ".join(f"{x:6.2f}" for x in pp))

@@ -184,3 +184,45 @@ def test_recenter_cascade_resets_only_that_cascade(dev):
     for lv in range(1, stage.levels):
         assert np.array_equal(dev.probes(lv)["pos"], before[lv][0]["pos"])
         assert np.array_equal(dev.atlas(lv, 0), before[lv][1])
+
+
+@pytest.mark.parametrize("name", [CASES[0], SCHED_CASES[0]])
+def test_probe_stage_call_matches_call_sequence(name):
+    """sdfgi_probe_stage (relocation of every cascade + selection + update, one
+    host sync) == the relocate / select / update sequence it replaces: same
+    reports, results, probe states and bit-identical atlases, stats summed."""
+    case = load(name)
+    outs = []
+    for fused in (False, True):
+        d = Device(0, precision="f64")
+        try:
+            stage = api.ProbeStage(d, case.scene, cfg=case.cfg(), res=case.res, spacing=case.spacing)
+            cam = case.scene.camera
+            got = []
+            for p in range(len(case.passes)):
+                if fused:
+                    reps, res, st = d.probe_stage(p, stage.cfg, cam.position, cam.forward, stats=True)
+                    reps = [tuple(int(r[k]) for k in ("relocated", "rejected", "dead")) for r in reps]
+                    d.swap()
+                else:
+                    rs = stage.relocate_all(stats=True)
+                    reps = [tuple(int(r[0][k]) for k in ("relocated", "rejected", "dead")) for r in rs]
+                    budget = int(stage.cfg["probe_budget"][0])
+                    refs = api.selectProbesForUpdate(d, cam.position, cam.forward, budget, p) if budget > 0 else None
+                    res, st = api.updateProbes(d, stage.cfg, p, refs, stats=True)
+                    st = dict(st=st, reloc=[r[1] for r in rs])
+                    d.swap()
+                got.append((reps, {k: res[k].item() for k in res.dtype.names}, st,
+                            [(d.probes(lv), d.atlas(lv, 0)) for lv in range(stage.levels)]))
+            outs.append(got)
+        finally:
+            d.close()
+    for p, (a, b) in enumerate(zip(*outs)):
+        assert a[0] == b[0], (name, p)
+        assert a[1] == b[1], (name, p)
+        for k in ("sdf_queries", "primitive_evals", "trace_steps", "shadow_traces"):
+            want = int(a[2]["st"][k]) + sum(int(r[k]) for r in a[2]["reloc"])
+            assert int(b[2][k]) == want, (name, p, k)
+        for (pa, aa), (pb, ab) in zip(a[3], b[3]):
+            check_probes(pb, pa, f"{name} pass {p}")
+            assert np.array_equal(aa, ab), (name, p)
