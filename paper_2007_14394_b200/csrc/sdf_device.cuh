@@ -887,6 +887,7 @@ template <typename M> __device__ __forceinline__ M mvcAsin(M v);
 // x > 0.5 z = sqrt((1 - x) / 2) with asin x = pi/2 - 2 asin z; asin z = z + z t P(t),
 // t = z^2 <= 1/4, P of degree 11 (Chebyshev fit on [0, 1/4], ~1e-16 relative; the
 // fit: scripts/fit_asin.py). Within ~1-2 ulp of the correctly rounded asin.
+__device__ __forceinline__ double asinSqrt(double x);  // mvcSqrt<double> (below)
 __constant__ const double kAsinP[12] = {
     0.16666666666666624,
     0.07500000000029536,
@@ -902,7 +903,7 @@ __constant__ const double kAsinP[12] = {
     0.028347549339135487};
 __device__ __forceinline__ double asin01(double x) {
     const bool big = x > 0.5;
-    const double s = sqrt(0.5 - 0.5 * x);  // exact argument for x >= 0.5
+    const double s = asinSqrt(0.5 - 0.5 * x);  // exact argument for x >= 0.5
     const double z = big ? s : x;
     const double t = z * z;
     double p = kAsinP[11];
@@ -926,6 +927,55 @@ __device__ __forceinline__ float asin01f(float x) {
 template <> __device__ __forceinline__ float mvcAsin<float>(float v) { return asin01f(v); }
 template <typename M> __device__ __forceinline__ M mvcDiv(M a, M b) { return a / b; }
 template <> __device__ __forceinline__ float mvcDiv<float>(float a, float b) { return __fdividef(a, b); }
+// MVC square roots and reciprocals in FP64: the MUFU seed (rsqrt/rcp.approx.ftz.f64)
+// refined by Newton steps in DFMA — within ~1 ulp, branch-free and a third of the
+// correctly rounded sequence (12 square roots per triangle). Arguments outside
+// [1e-300, 1e300] (zero, denormal, inf, NaN, negative) take the IEEE path.
+#ifndef SDFGI_MVC_FAST_SQRT
+#define SDFGI_MVC_FAST_SQRT 1
+#endif
+__device__ __forceinline__ double rsqrtSeed(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    return y;
+}
+__device__ __forceinline__ double rcpSeed(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    return y;
+}
+__device__ __forceinline__ bool mvcFastRange(double x) { return x > 1e-300 && x < 1e300; }
+// the IEEE operations out of line: one copy for every call site, run only by the
+// (degenerate) lanes outside the fast range
+static __device__ __noinline__ double mvcSqrtIeee(double x) { return sqrt(x); }
+static __device__ __noinline__ double mvcRcpIeee(double x) { return 1.0 / x; }
+// 1 / sqrt(x): the seed's relative error e0 (~2^-22) -> ~e0^3 after one
+// third-order step y (1 + e/2 + 3e^2/8), e = 1 - x y^2.
+__device__ __forceinline__ double rsqrtRefined(double x) {
+    const double y = rsqrtSeed(x);
+    const double e = fma(-x * y, y, 1.0);
+    return fma(y * e, fma(e, 0.375, 0.5), y);
+}
+template <typename M> __device__ __forceinline__ M mvcSqrt(M x) { return sqrt(x); }
+template <> __device__ __forceinline__ double mvcSqrt<double>(double x) {
+    if (!SDFGI_MVC_FAST_SQRT) return sqrt(x);
+    const double y = rsqrtRefined(x);
+    double r = x * y;
+    r = fma(fma(-r, r, x), 0.5 * y, r);  // one residual correction of x y
+    if (!mvcFastRange(x)) r = mvcSqrtIeee(x);
+    return r;
+}
+template <typename M> __device__ __forceinline__ M mvcRcp(M x) { return M(1) / x; }
+template <> __device__ __forceinline__ double mvcRcp<double>(double x) {
+    if (!SDFGI_MVC_FAST_SQRT) return 1.0 / x;
+    const double a = fabs(x);
+    double r = rcpSeed(x);
+    r = fma(r, fma(-x, r, 1.0), r);  // e0 -> e0^2
+    r = fma(r, fma(-x, r, 1.0), r);  // -> e0^4, below half an ulp
+    if (!mvcFastRange(a)) r = mvcRcpIeee(x);
+    return r;
+}
+__device__ __forceinline__ double asinSqrt(double x) { return mvcSqrt<double>(x); }
 
 // The MVC working set (8 distances, unit vectors and weight sums, indexed by the
 // triangle corners) lives in per-thread local memory, or — for kernels that pass
@@ -979,9 +1029,10 @@ __constant__ const int kMvcFaces[6][4] = {{0, 2, 3, 1}, {4, 5, 7, 6}, {0, 1, 5, 
 // the two triangles sharing an edge can share it.
 template <typename M>
 __device__ __forceinline__ void mvcEdgeAngles(V3<M> ua, V3<M> ub, M& sa, M& ca, M& th) {
-    const M l = length(ua - ub);
+    const V3<M> e = ua - ub;
+    const M l = mvcSqrt<M>(dot(e, e));
     sa = sclamp(l * M(0.5), M(0), M(1));
-    ca = sqrt(smax(M(0), M(1) - sa * sa));
+    ca = mvcSqrt<M>(smax(M(0), M(1) - sa * sa));
     th = M(2) * mvcAsin<M>(sa);
 }
 // sign(det(u0, u1, u2)) (mean_value.hpp:73-74)
@@ -1026,7 +1077,7 @@ __device__ __forceinline__ int mvcTriangleCore(const M d[3], const M sa[3], cons
     // FP64: the three divisions by st_j st_k through one reciprocal of
     // st_0 st_1 st_2 (1 / (st_j st_k) = st_i / P; a few ulps, far inside the
     // range: a triangle with a product below eps is skipped)
-    const M invP = sizeof(M) == 8 ? M(1) / (st[0] * st[1] * st[2]) : M(0);
+    const M invP = sizeof(M) == 8 ? mvcRcp<M>(st[0] * st[1] * st[2]) : M(0);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         const int j = (i + 1) % 3, k = (i + 2) % 3;
@@ -1038,7 +1089,7 @@ __device__ __forceinline__ int mvcTriangleCore(const M d[3], const M sa[3], cons
             c[i] = M(2) * sh * shi * (st[i] * invP) - M(1);
         else
             c[i] = mvcDiv(M(2) * sh * shi, denom) - M(1);
-        sv[i] = sign * sqrt(smax(M(0), M(1) - c[i] * c[i]));
+        sv[i] = sign * mvcSqrt<M>(smax(M(0), M(1) - c[i] * c[i]));
         // the reference stops at the first degenerate i (mean_value.hpp:80-86);
         // the values after it are unused either way
         skip = skip || fabs(denom) < eps || fabs(sv[i]) <= eps;
@@ -1047,7 +1098,7 @@ __device__ __forceinline__ int mvcTriangleCore(const M d[3], const M sa[3], cons
     M D[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) D[i] = d[i] * st[(i + 1) % 3] * sv[(i + 2) % 3];
-    const M invQ = sizeof(M) == 8 ? M(1) / (D[0] * D[1] * D[2]) : M(0);  // FP64: one division
+    const M invQ = sizeof(M) == 8 ? mvcRcp<M>(D[0] * D[1] * D[2]) : M(0);  // FP64: one reciprocal
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         const int j = (i + 1) % 3, k = (i + 2) % 3;
@@ -1073,14 +1124,14 @@ __device__ inline bool mvcWeightsHexImpl(const CellCorners& cc, V3<double> xd, M
     for (int i = 0; i < 8; ++i) {
         const V3<double> ci = cc.corner(i);
         V3<M> v = mk(M(ci.x), M(ci.y), M(ci.z)) - x;
-        const M di = length(v);
+        const M di = mvcSqrt<M>(dot(v, v));
         a.dist(i) = di;
         if (di < eps) {
             for (int k = 0; k < 8; ++k) a.wts(k) = M(0);
             a.wts(i) = M(1);
             return true;
         }
-        const M inv = mvcDiv(M(1), di);
+        const M inv = sizeof(M) == 8 ? mvcRcp<M>(di) : mvcDiv(M(1), di);
         a.ux(i) = v.x * inv;
         a.uy(i) = v.y * inv;
         a.uz(i) = v.z * inv;
