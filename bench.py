@@ -322,6 +322,7 @@ class StepRunner:
     def fresh(self):
         for level in range(self.stage.levels):
             self.dev.reset_probes(level)
+        self.dev.stage_ms_sum(reset=True)
 
     def step(self, stats=False):
         """-> rays, update-kernel ms, per-stage ms (summed over passes), and with
@@ -329,8 +330,7 @@ class StepRunner:
         from paper_2007_14394_b200 import api
 
         dev, stage = self.dev, self.stage
-        rays, upd_ms, work_all = 0, 0.0, []
-        stage_ms = dict.fromkeys(dev.STAGES, 0.0)
+        rays, work_all = 0, []
         work = dict.fromkeys(("k1", "k2", "shade", "convolve"), 0.0)
         prec = dev.precision
         for p in range(PASSES):
@@ -350,11 +350,10 @@ class StepRunner:
                 work_all.append({"k1": tc["k1"], "k2": tc["k2"], "shading": sh})
             else:
                 res = r
-            upd_ms += dev.last_kernel_ms()[0]
-            for k, v in dev.last_stage_ms().items():
-                stage_ms[k] += v
             rays += int(res["rays_traced"])
             dev.swap()
+        # every pass's stage events, summed on the device side (read once per step)
+        stage_ms, upd_ms = dev.stage_ms_sum(reset=True)
         return rays, upd_ms, stage_ms, work, work_all
 
 

@@ -330,6 +330,10 @@ SDFGI_API int sdfgi_last_shading_work(void* ctx, uint64_t out[2]);
  * phase, hit compaction + normals + shadow set-up, K2 shadow rays, K2 far phase,
  * K3a + K3c shading, K3b convolution + blend}. */
 SDFGI_API int sdfgi_last_stage_ms(void* ctx, double out[7]);
+/* The same stage times summed over every update since the last reset, out[7] = the
+ * updates' total (first to last stage event); reset != 0 zeroes the sums after
+ * reading. Lets a frame loop read its timings once instead of after every pass. */
+SDFGI_API int sdfgi_stage_ms_sum(void* ctx, double out[8], int reset);
 /* The last stats-enabled update's event counters per tracing kernel: out[0..13]
  * K1 (primary rays), out[14..27] K2 (shadow rays), each {sdf_queries,
  * clusters_visited, clusters_skipped, primitive_evals, trace_steps, sphere_traces,

@@ -118,9 +118,9 @@ struct Ctx {
     int device = 0, rank = 0, world = 1, precision = SDFGI_F64;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // update start/end, relocate start/end
-    cudaEvent_t quatEv = nullptr;  // the quaternion staging copy has been consumed
     cudaEvent_t kev[kWaveEvents] = {};  // the last update's stage boundaries (launch_wavefront)
     bool evUpdate = false, evReloc = false;
+    double stageSum[kWaveEvents] = {};  // sdfgi_stage_ms_sum: stages + update total since the last reset
     ncclComm_t comm = nullptr;
     long long launches = 0;
     // scene
@@ -207,18 +207,28 @@ struct Ctx {
     // wavefront scratch (kernels.cuh)
     DBuf<int> wRayCount, wHitList, wChunk, wHitAt, wMvcList;
     DBuf<long long> wRayStart;
-    DBuf<double> wRot, fib, wQuat;
+    DBuf<double> wRot, fib;
     DBuf<int> perm;
     int fibN = -1;
     int* hReport = nullptr;  // pinned: relocation reports of sdfgi_probe_stage (read after its one sync)
-    double* hQuat = nullptr;  // pinned staging of the per-pass quaternions (host_trig.h)
-    size_t hQuatN = 0;
-    // the next frame's quaternions, computed on the host while the current pass runs
-    // on the device (a frame loop's next update finds them ready)
-    double* hQuatSpec = nullptr;
-    size_t hQuatSpecN = 0;
-    uint64_t specKey = 0;
-    bool specValid = false;
+    // The per-pass quaternions (host_trig.h) in two slots: pinned host staging + a
+    // device copy made on copyStream. A pass reads one slot; the other takes the
+    // next frame's quaternions, computed on the host and copied while the current
+    // pass runs on the device (a frame loop's next update finds them on the device).
+    struct QuatSlot {
+        double* h = nullptr;
+        size_t hn = 0;
+        DBuf<double> d;
+        cudaEvent_t copied = nullptr;  // on copyStream: d holds h
+        cudaEvent_t used = nullptr;    // on stream: the last pass reading d is done
+        uint64_t key = 0;
+    };
+    QuatSlot qs[2];
+    int qLast = 0;    // slot of the latest pass
+    int qSpec = -1;   // slot holding the speculated next frame
+    int qReady = -1;  // slot prepared for the coming pass (sdfgi_probe_stage: before relocation)
+    const double* quatDev = nullptr;
+    cudaStream_t copyStream = nullptr;
     // Contact GI's cosineHemisphereDir (lx, ly) per (pixel, sample), host libm; keyed
     // (seed, w, h, samples): the reference's stream has no frame index (shading.hpp:451)
     DBuf<double> cLocal;
@@ -250,10 +260,15 @@ struct Ctx {
         pos.free(); rest.free(); last.free(); clear.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free(); allRefs.free();
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
-        wRayCount.free(); wHitList.free(); wMvcList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); wQuat.free(); cLocal.free(); wHits.free();
+        wRayCount.free(); wHitList.free(); wMvcList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); cLocal.free(); wHits.free();
         if (hReport) cudaFreeHost(hReport);
-        if (hQuat) cudaFreeHost(hQuat);
-        if (hQuatSpec) cudaFreeHost(hQuatSpec);
+        for (auto& q : qs) {
+            if (q.h) cudaFreeHost(q.h);
+            q.d.free();
+            if (q.copied) cudaEventDestroy(q.copied);
+            if (q.used) cudaEventDestroy(q.used);
+        }
+        if (copyStream) cudaStreamDestroy(copyStream);
         wVis.free(); wPark.free(); wCRay.free(); wPRay.free(); wConv.free(); wSRay.free(); wCtr.free(); perm.free(); wRad.free();
         gbuf.free(); halfDepth.free(); sparseIrr.free(); resolved.free(); indirect.free(); histIrr.free(); composed.free();
         histDepth.free(); halfSrc.free(); sel.free(); sparseValid.free(); sparseAnchor.free();
@@ -263,7 +278,6 @@ struct Ctx {
             if (e) cudaEventDestroy(e);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
-        if (quatEv) cudaEventDestroy(quatEv);
         for (auto& e : kev)
             if (e) cudaEventDestroy(e);
         if (comm) ncclCommDestroy(comm);
@@ -941,7 +955,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.rayStart = c->wRayStart.p;
     p.chunkSlot = c->wChunk.p;
     p.rot = c->wRot.p;
-    p.quat = c->wQuat.p;
+    p.quat = c->quatDev;
     p.pray = c->wPRay.p;
     p.fib = c->fib.p;
     p.perm = c->perm.p;
@@ -984,11 +998,6 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     return p;
 }
 
-// randomRotation's quaternion of every candidate for this pass (sampleDirections'
-// key: seed, frame or 0xf1b0, probeKey(level, index)), evaluated with the host's
-// libm (host_trig.h) into pinned memory and copied behind the work already queued
-// on the stream (relocation, the atlas copy), so the host work overlaps it.
-// cand = null: every probe 0..nCand-1.
 // Everything a pass's quaternions depend on: seed, frame (or none), the
 // candidates (null = every probe) and the cascades' levels and bases.
 uint64_t quatKey(const Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand) {
@@ -1030,38 +1039,62 @@ void computeQuats(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int 
     sdfgi_host::probeQuats(cfg->seed, frame, cfg->rotate_per_frame != 0, keys.data(), nCand, out);
 }
 
-// randomRotation's quaternion of every candidate for this pass (sampleDirections'
-// key: seed, frame or 0xf1b0, probeKey(level, index)), evaluated with the host's
-// libm (host_trig.h) into pinned memory — or taken from the previous call's
-// speculation for this frame — and copied behind the work already queued on the
-// stream. cand = null: every probe 0..nCand-1.
-void uploadQuats(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand) {
+// Slot u <- the quaternions of (frame, cand): host libm into its pinned buffer
+// (once the previous copy out of it is done), then copied on copyStream once no
+// queued pass reads the slot's device buffer.
+void fillQuatSlot(Ctx* c, int u, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand, uint64_t key) {
+    Ctx::QuatSlot& q = c->qs[u];
     const size_t need = 4 * static_cast<size_t>(std::max(nCand, 1));
-    // the previous call's copy out of the staging buffer must have finished
-    CK(cudaEventSynchronize(c->quatEv));
-    const uint64_t key = quatKey(c, cfg, frame, cand, nCand);
-    if (c->specValid && c->specKey == key && c->hQuatSpecN >= need) {
-        std::swap(c->hQuat, c->hQuatSpec);
-        std::swap(c->hQuatN, c->hQuatSpecN);
-    } else {
-        ensurePinned(c->hQuat, c->hQuatN, need);
-        computeQuats(c, cfg, frame, cand, nCand, c->hQuat);
-    }
-    c->specValid = false;
-    reserve(c->wQuat, need);
-    CK(cudaMemcpyAsync(c->wQuat.p, c->hQuat, 4 * static_cast<size_t>(nCand) * sizeof(double), cudaMemcpyHostToDevice,
-                       c->stream));
-    CK(cudaEventRecord(c->quatEv, c->stream));
+    CK(cudaEventSynchronize(q.copied));
+    ensurePinned(q.h, q.hn, need);
+    computeQuats(c, cfg, frame, cand, nCand, q.h);
+    reserve(q.d, need);
+    CK(cudaStreamWaitEvent(c->copyStream, q.used, 0));
+    CK(cudaMemcpyAsync(q.d.p, q.h, 4 * static_cast<size_t>(nCand) * sizeof(double), cudaMemcpyHostToDevice,
+                       c->copyStream));
+    CK(cudaEventRecord(q.copied, c->copyStream));
+    q.key = key;
 }
 
-// The next frame's quaternions for the same candidates, on the host while the
-// device runs this pass (the staging buffer not in flight).
+// randomRotation's quaternion of every candidate for this pass (sampleDirections'
+// key: seed, frame or 0xf1b0, probeKey(level, index)), evaluated with the host's
+// libm (host_trig.h) — or the previous pass's speculation when it was for this
+// frame — in a slot whose device copy runs beside the queued work. cand = null:
+// every probe 0..nCand-1. Returns the slot; nothing waits on it yet.
+int prepareQuats(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand) {
+    const uint64_t key = quatKey(c, cfg, frame, cand, nCand);
+    if (c->qReady >= 0 && c->qs[c->qReady].key == key) return c->qReady;
+    int u;
+    if (c->qSpec >= 0 && c->qs[c->qSpec].key == key) {
+        u = c->qSpec;
+    } else {
+        u = 1 - c->qLast;
+        fillQuatSlot(c, u, cfg, frame, cand, nCand, key);
+    }
+    c->qSpec = -1;
+    c->qReady = u;
+    return u;
+}
+
+// This pass's quaternions on the device: the stream waits for the slot's copy.
+void uploadQuats(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand) {
+    const int u = prepareQuats(c, cfg, frame, cand, nCand);
+    CK(cudaStreamWaitEvent(c->stream, c->qs[u].copied, 0));
+    c->quatDev = c->qs[u].d.p;
+    c->qLast = u;
+    c->qReady = -1;
+}
+
+// After the launches reading this pass's slot.
+void quatsConsumed(Ctx* c) { CK(cudaEventRecord(c->qs[c->qLast].used, c->stream)); }
+
+// The next frame's quaternions for the same candidates into the other slot, on the
+// host while the device runs this pass; copied on copyStream.
 void speculateQuats(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* cand, int nCand) {
-    if (!cfg->rotate_per_frame) return;  // frame-independent: recomputed (cheap) or identical anyway
-    ensurePinned(c->hQuatSpec, c->hQuatSpecN, 4 * static_cast<size_t>(std::max(nCand, 1)));
-    computeQuats(c, cfg, frame + 1, cand, nCand, c->hQuatSpec);
-    c->specKey = quatKey(c, cfg, frame + 1, cand, nCand);
-    c->specValid = true;
+    if (!cfg->rotate_per_frame) return;  // frame-independent: the key matches the current slot's next time
+    const int s = 1 - c->qLast;
+    fillQuatSlot(c, s, cfg, frame + 1, cand, nCand, quatKey(c, cfg, frame + 1, cand, nCand));
+    c->qSpec = s;
 }
 
 void validateCfg(Ctx* c, const sdfgi_cfg* cfg) {
@@ -1152,9 +1185,14 @@ int sdfgi_ctx_create(int device, int rank, int world, const uint8_t* nccl_uid, i
         try {
             CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
             for (auto& e : c->ev) CK(cudaEventCreate(&e));
-            CK(cudaEventCreateWithFlags(&c->quatEv, cudaEventDisableTiming));
+            CK(cudaStreamCreateWithFlags(&c->copyStream, cudaStreamNonBlocking));
+            for (auto& q : c->qs) {
+                CK(cudaEventCreateWithFlags(&q.copied, cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&q.used, cudaEventDisableTiming));
+                CK(cudaEventRecord(q.copied, c->copyStream));
+                CK(cudaEventRecord(q.used, c->stream));
+            }
             for (auto& e : c->kev) CK(cudaEventCreate(&e));
-            CK(cudaEventRecord(c->quatEv, c->stream));
             c->scratch.alloc(kShadowStats + 32);
             c->report.alloc(4 * kMaxCascades);
             CK(cudaMallocHost(&c->hReport, 4 * kMaxCascades * sizeof(int)));
@@ -1768,6 +1806,7 @@ void updateBody(Ctx* c, const int32_t* probe_refs, int n_refs, int frame, const 
         }
         CK(cudaGetLastError());
         c->evUpdate = true;
+        quatsConsumed(c);
         speculateQuats(c, cfg, frame, all ? nullptr : refs.data(), nCand);
     }
     if (c->world > 1) {
@@ -1808,6 +1847,16 @@ void updateBody(Ctx* c, const int32_t* probe_refs, int n_refs, int frame, const 
     }
     unsigned long long tail[3];
     readCounters(c, stats, tail, 3);
+    if (nCand > 0) {  // this update's stage events are complete (readCounters synchronised)
+        for (int i = 0; i + 1 < kWaveEvents; ++i) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, c->kev[i], c->kev[i + 1]));
+            c->stageSum[i] += ms;
+        }
+        float tot = 0.f;
+        CK(cudaEventElapsedTime(&tot, c->kev[0], c->kev[kWaveEvents - 1]));
+        c->stageSum[kWaveEvents - 1] += tot;
+    }
     if (result) {
         double md;
         std::memcpy(&md, &tail[0], 8);
@@ -1838,6 +1887,13 @@ int sdfgi_probe_stage(void* ctx, int frame, const sdfgi_cfg* cfg, const double c
             relocEnqueue(c, s, cfg->threshold1_frac * sp, cfg->threshold2_frac * sp,
                          static_cast<int>(cfg->max_descent_steps), cfg->gradient_step, stats != nullptr,
                          c->report.p + 4 * s, false);
+        }
+        if (cfg->probe_budget <= 0 && c->totalProbes > 0) {
+            // this pass's quaternions (unless speculated) on the host while the device
+            // relocates, copied beside it; the update's stream waits for them
+            const std::vector<int> cand = selectRefs(c, nullptr, 0);
+            if (!cand.empty())
+                prepareQuats(c, cfg, frame, c->world == 1 ? nullptr : cand.data(), static_cast<int>(cand.size()));
         }
         sdfgi_stats relocStats;
         std::memset(&relocStats, 0, sizeof(relocStats));
@@ -1954,6 +2010,7 @@ int sdfgi_probes_trace_debug(void* ctx, const int32_t* probe_refs, int n_refs, i
             launch_wavefront<float>(p, c->persistCap, false, c->stream, nullptr, &c->launches);
         }
         CK(cudaGetLastError());
+        quatsConsumed(c);
         long long total = 0;
         CK(cudaMemcpyAsync(&total, c->wRayStart.p + n_refs, sizeof(total), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
@@ -2013,6 +2070,16 @@ int sdfgi_last_stage_ms(void* ctx, double out[7]) {
             CK(cudaEventElapsedTime(&ms, c->kev[i], c->kev[i + 1]));
             out[i] = ms;
         }
+    });
+}
+
+int sdfgi_stage_ms_sum(void* ctx, double out[8], int reset) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(out, SDFGI_ERR_INVALID, "null out");
+        for (int i = 0; i < kWaveEvents; ++i) out[i] = c->stageSum[i];
+        if (reset)
+            for (double& v : c->stageSum) v = 0.0;
     });
 }
 

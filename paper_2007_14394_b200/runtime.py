@@ -47,6 +47,7 @@ _SIGS = {
     "sdfgi_probes_relocate": [_P, _I, _D, _D, _I, _D, _P, _P],
     "sdfgi_probes_update": [_P, _P, _I, _I, _P, _P, _P],
     "sdfgi_probe_stage": [_P, _I, _P, _P, _P, _P, _I, _P, _P],
+    "sdfgi_stage_ms_sum": [_P, _P, _I],
     "sdfgi_atlas_swap": [_P],
     "sdfgi_atlas_download": [_P, _I, _I, _P, _SZ],
     "sdfgi_atlas_upload": [_P, _I, _I, _P, _SZ],
@@ -234,6 +235,13 @@ class Device:
         out = np.zeros(7)
         _call("sdfgi_last_stage_ms", self._ctx, _ptr(out))
         return dict(zip(self.STAGES, map(float, out)))
+
+    def stage_ms_sum(self, reset=True):
+        """Stage ms summed over the updates since the last reset: (dict over STAGES,
+        the updates' total ms)."""
+        out = np.zeros(8)
+        _call("sdfgi_stage_ms_sum", self._ctx, _ptr(out), 1 if reset else 0)
+        return dict(zip(self.STAGES, map(float, out[:7]))), float(out[7])
 
     def last_trace_counters(self):
         """The last stats-enabled update's counters per tracing kernel: {"k1": ..., "k2": ...},

@@ -47,8 +47,12 @@ def main():
         last_end = max(last_end, e)
         prev = n
     gaps.sort(reverse=True)
+    per = {}
+    for st_, en, n in spans:
+        per[n] = per.get(n, 0.0) + (en - st_)
     out = {"precision": prec, "steps": steps, "span_us": t1 - t0, "busy_us": busy,
            "idle_us": (t1 - t0) - busy, "n_device_ops": len(spans),
+           "per_op_us": dict(sorted(((k[:90], v / steps) for k, v in per.items()), key=lambda kv: -kv[1])[:25]),
            "gaps_top": [{"us": g, "after": a[:80], "before": b[:80]} for g, a, b in gaps[:40]],
            "gap_hist": {k: sum(1 for g in gaps if lo <= g[0] < hi)
                         for k, lo, hi in (("<5us", 0, 5), ("5-20us", 5, 20), ("20-100us", 20, 100),
@@ -56,7 +60,9 @@ def main():
     os.makedirs("gpurun_out", exist_ok=True)
     with open(f"gpurun_out/timeline_{prec}.json", "w") as f:
         json.dump(out, f, indent=1)
-    print(json.dumps({k: v for k, v in out.items() if k != "gaps_top"}))
+    print(json.dumps({k: v for k, v in out.items() if k not in ("gaps_top", "per_op_us")}))
+    for k, v in out["per_op_us"].items():
+        print(f"{v:9.1f} us/step  {k}")
     for g in out["gaps_top"][:20]:
         print(f"{g['us']:8.1f} us  after {g['after']}  before {g['before']}")
 
