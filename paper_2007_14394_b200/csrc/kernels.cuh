@@ -311,6 +311,14 @@ template <typename R>
 void launch_gather(const GatherParams<R>& p, int stage, bool stats, cudaStream_t st);
 void launch_relocate(const RelocParams& p, int nProbes, bool stats, cudaStream_t st);
 void launch_query_points(const QueryParams& p, cudaStream_t st);
+// Probe state (ProbesView arrays at global index base..base+n): the makeCascade
+// state (restingAt, probe_volume.hpp:37-39: origin + i * spacing per axis; alive,
+// rejectHistory set, never updated), and the sdfgi_probe AoS <-> SoA conversions.
+void launch_probes_reset(ProbesView pv, int base, const int res[3], const double origin[3], double spacing,
+                         cudaStream_t st);
+// aos: 11 doubles per probe (sdfgi_probe: resting, pos, last_pos, then 4 int32)
+void launch_probes_unpack(ProbesView pv, int base, int n, const double* aos, cudaStream_t st);
+void launch_probes_pack(ProbesView pv, int base, int n, double* aos, cudaStream_t st);
 void launch_mark_updated(const int* ids, int n, int frame, const int* alive, int* reject, int* lastFrame,
                          cudaStream_t st);
 void launch_grid_bound(const GridBuildParams& p, int ncells, cudaStream_t st);

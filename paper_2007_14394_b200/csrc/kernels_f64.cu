@@ -260,6 +260,68 @@ void launch_relocate(const RelocParams& p, int nProbes, bool stats, cudaStream_t
         k_relocate<false><<<blocks, 128, 0, st>>>(p);
 }
 
+__global__ void __launch_bounds__(256) k_probes_reset(ProbesView pv, int base, int rx, int ry, int rz, double ox,
+                                                     double oy, double oz, double sp) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rx * ry * rz) return;
+    const int ix = i % rx, iy = (i / rx) % ry, iz = i / (rx * ry);
+    // restingAt (probe_volume.hpp:37-39), the host's operation order (-fmad=false)
+    const double r[3] = {ox + ix * sp, oy + iy * sp, oz + iz * sp};
+    const size_t g = static_cast<size_t>(base) + i;
+    for (int k = 0; k < 3; ++k) {
+        pv.rest[3 * g + k] = r[k];
+        pv.pos[3 * g + k] = r[k];
+        pv.last[3 * g + k] = r[k];
+    }
+    pv.alive[g] = 1;
+    pv.reject[g] = 1;
+    pv.lastFrame[g] = -1;
+}
+__global__ void __launch_bounds__(256) k_probes_unpack(ProbesView pv, int base, int n, const double* aos) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* a = aos + 11 * static_cast<size_t>(i);
+    const int* ai = reinterpret_cast<const int*>(a + 9);
+    const size_t g = static_cast<size_t>(base) + i;
+    for (int k = 0; k < 3; ++k) {
+        pv.rest[3 * g + k] = a[k];
+        pv.pos[3 * g + k] = a[3 + k];
+        pv.last[3 * g + k] = a[6 + k];
+    }
+    pv.reject[g] = ai[0];
+    pv.alive[g] = ai[1];
+    pv.lastFrame[g] = ai[2];
+}
+__global__ void __launch_bounds__(256) k_probes_pack(ProbesView pv, int base, int n, double* aos) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double* a = aos + 11 * static_cast<size_t>(i);
+    int* ai = reinterpret_cast<int*>(a + 9);
+    const size_t g = static_cast<size_t>(base) + i;
+    for (int k = 0; k < 3; ++k) {
+        a[k] = pv.rest[3 * g + k];
+        a[3 + k] = pv.pos[3 * g + k];
+        a[6 + k] = pv.last[3 * g + k];
+    }
+    ai[0] = pv.reject[g];
+    ai[1] = pv.alive[g];
+    ai[2] = pv.lastFrame[g];
+    ai[3] = 0;
+}
+void launch_probes_reset(ProbesView pv, int base, const int res[3], const double origin[3], double spacing,
+                         cudaStream_t st) {
+    const int n = res[0] * res[1] * res[2];
+    if (n > 0)
+        k_probes_reset<<<(n + 255) / 256, 256, 0, st>>>(pv, base, res[0], res[1], res[2], origin[0], origin[1],
+                                                         origin[2], spacing);
+}
+void launch_probes_unpack(ProbesView pv, int base, int n, const double* aos, cudaStream_t st) {
+    if (n > 0) k_probes_unpack<<<(n + 255) / 256, 256, 0, st>>>(pv, base, n, aos);
+}
+void launch_probes_pack(ProbesView pv, int base, int n, double* aos, cudaStream_t st) {
+    if (n > 0) k_probes_pack<<<(n + 255) / 256, 256, 0, st>>>(pv, base, n, aos);
+}
+
 void launch_mark_updated(const int* ids, int n, int frame, const int* alive, int* reject, int* lastFrame,
                          cudaStream_t st) {
     if (n > 0) k_mark_updated<<<(n + 255) / 256, 256, 0, st>>>(ids, n, frame, alive, reject, lastFrame);

@@ -15,6 +15,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <array>
 #include <cmath>
 #include <cstdlib>
@@ -169,6 +171,16 @@ struct Ctx {
     double hint[6] = {0, 0, 0, 0, 0, 0};     // probe volumes the grid must cover
     // host copy of the uploaded scene (the grid is rebuilt when the hint grows)
     std::vector<sdfgi_prim> hPrims;
+    // sdfgi_scene_upload's conversion buffers (reused across uploads)
+    std::vector<DPrim<double>> up64;
+    std::vector<DPrim<float>> up32;
+    std::vector<int> upOrig, upKid;
+    std::vector<double> upAlb, upEm;
+    std::vector<unsigned char> upStage, upRows;
+    // the cluster boxes and coordinate scale the BVH was built from (a re-sent scene
+    // with the same boxes keeps it)
+    std::vector<sdfgi_cluster> bvhClusters;
+    double bvhScale = -1;
     std::vector<int32_t> hMember, hStart;
     std::vector<sdfgi_cluster> hClusters;
     std::vector<sdfgi_light> hLights;
@@ -211,6 +223,13 @@ struct Ctx {
     DBuf<int> perm;
     int fibN = -1;
     int* hReport = nullptr;  // pinned: relocation reports of sdfgi_probe_stage (read after its one sync)
+    // pinned ring the host arrays of an upload are staged in, so their copies are
+    // asynchronous DMA (a pageable cudaMemcpyAsync costs ~50 us of staging each);
+    // arenaEv: the latest copy out of it
+    char* arena = nullptr;
+    size_t arenaCap = 0, arenaOff = 0;
+    cudaEvent_t arenaEv = nullptr;
+    DBuf<double> probeAos;  // sdfgi_probe records in transit (probes upload / download)
     // The per-pass quaternions (host_trig.h) in two slots: pinned host staging + a
     // device copy made on copyStream. A pass reads one slot; the other takes the
     // next frame's quaternions, computed on the host and copied while the current
@@ -262,6 +281,9 @@ struct Ctx {
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
         wRayCount.free(); wHitList.free(); wMvcList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); cLocal.free(); wHits.free();
         if (hReport) cudaFreeHost(hReport);
+        if (arena) cudaFreeHost(arena);
+        if (arenaEv) cudaEventDestroy(arenaEv);
+        probeAos.free();
         for (auto& q : qs) {
             if (q.h) cudaFreeHost(q.h);
             q.d.free();
@@ -320,6 +342,34 @@ struct Ctx {
         throw Error(SDFGI_ERR_INVALID, "no cascade with level " + std::to_string(level));
     }
 };
+
+// Host array -> device through the pinned ring (stream-ordered; the ring wraps
+// once every copy out of it has finished).
+void stageCopy(Ctx* c, void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return;
+    size_t off = (c->arenaOff + 255) & ~static_cast<size_t>(255);
+    if (off + bytes > c->arenaCap) {
+        CK(cudaEventSynchronize(c->arenaEv));
+        off = 0;
+        if (bytes > c->arenaCap) {
+            if (c->arena) CK(cudaFreeHost(c->arena));
+            c->arena = nullptr;
+            c->arenaCap = 0;
+            const size_t cap = std::max<size_t>(bytes, 8u << 20);
+            CK(cudaMallocHost(&c->arena, cap));
+            c->arenaCap = cap;
+        }
+    }
+    std::memcpy(c->arena + off, src, bytes);
+    CK(cudaMemcpyAsync(dst, c->arena + off, bytes, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaEventRecord(c->arenaEv, c->stream));
+    c->arenaOff = off + bytes;
+}
+template <class T>
+void upload(Ctx* c, DBuf<T>& b, const T* h, size_t n) {
+    b.alloc(n);
+    stageCopy(c, b.p, h, n * sizeof(T));
+}
 
 template <>
 SceneView<double> Ctx::sceneView<double>() const {
@@ -403,24 +453,10 @@ void resetProbes(Ctx* c, int slot) {
     c->clearValid[slot] = 0;
     const CascadeHost& cs = c->cascades[slot];
     const int n = cs.count();
-    std::vector<double> r(3 * n);
-    std::vector<int> ones(n, 1), minus(n, -1);
-    for (int iz = 0; iz < cs.res[2]; ++iz)
-        for (int iy = 0; iy < cs.res[1]; ++iy)
-            for (int ix = 0; ix < cs.res[0]; ++ix) {
-                // restingAt, probe_volume.hpp:37-39
-                int i = ix + cs.res[0] * (iy + cs.res[1] * iz);
-                r[3 * i] = cs.origin[0] + ix * cs.spacing;
-                r[3 * i + 1] = cs.origin[1] + iy * cs.spacing;
-                r[3 * i + 2] = cs.origin[2] + iz * cs.spacing;
-            }
-    size_t off = static_cast<size_t>(cs.base);
-    CK(cudaMemcpyAsync(c->rest.p + 3 * off, r.data(), r.size() * 8, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->pos.p + 3 * off, r.data(), r.size() * 8, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->last.p + 3 * off, r.data(), r.size() * 8, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->alive.p + off, ones.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->reject.p + off, ones.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->lastFrame.p + off, minus.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
+    const size_t off = static_cast<size_t>(cs.base);
+    // makeCascade's probes (restingAt, probe_volume.hpp:37-39) written on the device
+    launch_probes_reset(c->probeCommon().probes, cs.base, cs.res, cs.origin, cs.spacing, c->stream);
+    checkLaunch(c);
     for (int b = 0; b < 2; ++b) {
         CK(cudaMemsetAsync(c->atlas[b].p + off * c->tileFloats(), 0, n * c->tileFloats() * 4, c->stream));
         c->atlasZero[b].resize(c->cascades.size(), 0);
@@ -541,6 +577,11 @@ void primAabb(const sdfgi_prim& s, double* out) {
 void buildBvh(Ctx* c, double scaleHint) {
     const sdfgi_cluster* clusters = c->hClusters.data();
     const int n = static_cast<int>(c->hClusters.size());
+    if (c->bvhScale == scaleHint && c->bvhClusters.size() == c->hClusters.size() &&
+        std::memcmp(c->bvhClusters.data(), clusters, n * sizeof(sdfgi_cluster)) == 0)
+        return;  // same boxes: the same hierarchy (BNode refers to clusters by index)
+    c->bvhClusters = c->hClusters;
+    c->bvhScale = scaleHint;
     double glo[3] = {INFINITY, INFINITY, INFINITY}, ghi[3] = {-INFINITY, -INFINITY, -INFINITY};
     double scale = 0;
     for (int k = 0; k < n; ++k) {
@@ -613,8 +654,8 @@ void buildBvh(Ctx* c, double scaleHint) {
     std::vector<int> unbPad(unb);
     if (nodes.empty()) nodes.emplace_back();  // never read (nBounded < 2 uses the root code only)
     if (unbPad.empty()) unbPad.push_back(0);
-    c->bvh.upload(nodes.data(), nodes.size(), c->stream);
-    c->unbList.upload(unbPad.data(), unbPad.size(), c->stream);
+    upload(c, c->bvh, nodes.data(), nodes.size());
+    upload(c, c->unbList, unbPad.data(), unbPad.size());
     CK(cudaStreamSynchronize(c->stream));
     c->grid.bvh = c->bvh.p;
     c->grid.bvhRoot = root;
@@ -738,7 +779,7 @@ void buildGrid(Ctx* c) {
     {
         std::vector<double> boxes(6 * static_cast<size_t>(c->nPrims));
         for (int j = 0; j < c->nPrims; ++j) primAabb(prims[member_idx[j]], &boxes[6 * static_cast<size_t>(j)]);
-        c->primBox.upload(boxes.data(), boxes.size(), c->stream);
+        upload(c, c->primBox, boxes.data(), boxes.size());
     }
     p.primBox = c->primBox.p;
     p.U = c->gridU.p;
@@ -942,7 +983,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
         std::vector<int> perm = coherentOrder(N);
         std::vector<int> perm2 = coherentOrder(2 * N);
         perm.insert(perm.end(), perm2.begin(), perm2.end());
-        c->perm.upload(perm.data(), perm.size(), c->stream);
+        upload(c, c->perm, perm.data(), perm.size());
         c->fibN = N;
     }
     WaveParams<R> p;
@@ -1196,6 +1237,8 @@ int sdfgi_ctx_create(int device, int rank, int world, const uint8_t* nccl_uid, i
             c->scratch.alloc(kShadowStats + 32);
             c->report.alloc(4 * kMaxCascades);
             CK(cudaMallocHost(&c->hReport, 4 * kMaxCascades * sizeof(int)));
+            CK(cudaEventCreateWithFlags(&c->arenaEv, cudaEventDisableTiming));
+            CK(cudaEventRecord(c->arenaEv, c->stream));
             if (world > 1) {
                 REQ(nccl_uid, SDFGI_ERR_INVALID, "world > 1 needs an NCCL unique id");
                 ncclUniqueId id;
@@ -1263,10 +1306,19 @@ void uploadSceneArrays(Ctx* c, const sdfgi_prim* prims, int n_prims, const sdfgi
     for (int i = 0; i < n_prims; ++i)
         REQ(prims[i].kind >= 0 && prims[i].kind <= 4, SDFGI_ERR_INVALID, "bad primitive kind");
     // cluster (CSR) order: device primitive j = prims[member_idx[j]]
-    std::vector<DPrim<double>> p64(nMembers);
-    std::vector<DPrim<float>> p32(nMembers);
-    std::vector<int> orig(nMembers), kid(std::max(nMembers, 1));
-    std::vector<double> alb(3 * static_cast<size_t>(nMembers)), em(3 * static_cast<size_t>(nMembers));
+    // conversion buffers kept in the context (a re-sent scene touches no fresh pages)
+    auto& p64 = c->up64;
+    auto& p32 = c->up32;
+    auto& orig = c->upOrig;
+    auto& kid = c->upKid;
+    auto& alb = c->upAlb;
+    auto& em = c->upEm;
+    p64.resize(nMembers);
+    p32.resize(nMembers);
+    orig.resize(nMembers);
+    kid.resize(std::max(nMembers, 1));
+    alb.resize(3 * static_cast<size_t>(nMembers));
+    em.resize(3 * static_cast<size_t>(nMembers));
     for (int j = 0; j < nMembers; ++j) {
         const sdfgi_prim& s = prims[member_idx[j]];
         std::memset(&p64[j], 0, sizeof(p64[j]));
@@ -1299,16 +1351,16 @@ void uploadSceneArrays(Ctx* c, const sdfgi_prim* prims, int n_prims, const sdfgi
     }
     std::vector<int> starts(member_start, member_start + n_clusters + 1);
     if (n_clusters == 0) starts.assign(1, 0);
-    c->prim64.upload(p64.data(), p64.size(), c->stream);
-    c->prim32.upload(p32.data(), p32.size(), c->stream);
-    c->cl64.upload(c64.data(), c64.size(), c->stream);
-    c->cl32.upload(c32.data(), c32.size(), c->stream);
-    c->cstart.upload(starts.data(), starts.size(), c->stream);
-    c->orig.upload(orig.data(), orig.size(), c->stream);
-    c->albedo.upload(alb.data(), alb.size(), c->stream);
-    c->emission.upload(em.data(), em.size(), c->stream);
-    c->kindId.upload(kid.data(), kid.size(), c->stream);
-    c->lights.upload(reinterpret_cast<const DLight*>(lights), n_lights, c->stream);
+    upload(c, c->prim64, p64.data(), p64.size());
+    upload(c, c->prim32, p32.data(), p32.size());
+    upload(c, c->cl64, c64.data(), c64.size());
+    upload(c, c->cl32, c32.data(), c32.size());
+    upload(c, c->cstart, starts.data(), starts.size());
+    upload(c, c->orig, orig.data(), orig.size());
+    upload(c, c->albedo, alb.data(), alb.size());
+    upload(c, c->emission, em.data(), em.size());
+    upload(c, c->kindId, kid.data(), kid.size());
+    upload(c, c->lights, reinterpret_cast<const DLight*>(lights), n_lights);
     // shared-memory staging of the primitive records for K1/K2 (evalPrimStaged):
     // FP64 64 B per primitive + 64 B per rotation row, FP32 the 64 B records as is
     {
@@ -1317,8 +1369,10 @@ void uploadSceneArrays(Ctx* c, const sdfgi_prim* prims, int n_prims, const sdfgi
         const long long limit = static_cast<long long>(optin) - 1024;  // the kernels' static shared memory
         const char* senv = std::getenv("SDFGI_STAGE");
         const bool allow = !(senv && std::atoi(senv) == 0) && nMembers > 0;
-        std::vector<unsigned char> st(64 * static_cast<size_t>(nMembers));
-        std::vector<unsigned char> rows;
+        auto& st = c->upStage;
+        auto& rows = c->upRows;
+        st.resize(64 * static_cast<size_t>(nMembers));
+        rows.clear();
         for (int j = 0; j < nMembers; ++j) {
             unsigned char* r = st.data() + 64 * static_cast<size_t>(j);
             std::memcpy(r, &p64[j], 64);
@@ -1334,7 +1388,7 @@ void uploadSceneArrays(Ctx* c, const sdfgi_prim* prims, int n_prims, const sdfgi
         c->stage64Bytes = 0;
         if (allow && b64 <= limit) {
             st.insert(st.end(), rows.begin(), rows.end());
-            c->stage64.upload(st.data(), st.size(), c->stream);
+            upload(c, c->stage64, st.data(), st.size());
             c->stage64Bytes = static_cast<int>(b64);
             c->stage64RotOff = 64 * nMembers;
         }
@@ -1372,7 +1426,7 @@ void remapGrid(Ctx* c) {
         std::vector<int> map(std::max<size_t>(c->gridCsrOrig.size(), 1));
         for (size_t j = 0; j < c->gridCsrOrig.size(); ++j) map[j] = csrOf[c->gridCsrOrig[j]];
         DBuf<int> dmap;
-        dmap.upload(map.data(), map.size(), c->stream);
+        upload(c, dmap, map.data(), map.size());
         launch_grid_remap(c->gridEntry.p, c->gridEntries, dmap.p, c->stream);
         checkLaunch(c);
         launch_grid_cells(c->gridStart.p, c->gridEntry.p, c->gridCell.p,
@@ -1388,7 +1442,7 @@ void remapGrid(Ctx* c) {
     std::sort(dyn.begin(), dyn.end());
     c->nDyn = static_cast<int>(dyn.size());
     if (dyn.empty()) dyn.push_back(0);
-    c->dynCsr.upload(dyn.data(), dyn.size(), c->stream);
+    upload(c, c->dynCsr, dyn.data(), dyn.size());
     CK(cudaStreamSynchronize(c->stream));
 }
 
@@ -1450,9 +1504,12 @@ int sdfgi_scene_upload(void* ctx, const sdfgi_prim* prims, int n_prims, const sd
                        const sdfgi_light* lights, int n_lights, const double sky[3]) {
     return guard([&] {
         Ctx* c = C(ctx);
-        const std::vector<sdfgi_prim> prev = c->hPrims;
+        const auto T0 = std::chrono::steady_clock::now();
+        std::vector<sdfgi_prim> prev;
+        prev.swap(c->hPrims);  // uploadSceneArrays stores the new ones
         std::fill(c->clearValid.begin(), c->clearValid.end(), 0);  // the SDF may have changed
         uploadSceneArrays(c, prims, n_prims, clusters, n_clusters, member_start, member_idx, lights, n_lights, sky);
+        const auto T1 = std::chrono::steady_clock::now();
         // The acceleration structures are a function of the geometry alone. A static
         // scene re-sent every frame keeps its grid; when primitives move, the ones
         // that moved become "dynamic" (left out of the grid lists, evaluated by every
@@ -1487,9 +1544,16 @@ int sdfgi_scene_upload(void* ctx, const sdfgi_prim* prims, int n_prims, const sd
         if (grow.empty()) {  // the grid's static geometry is unchanged: refit
             double scale = 0;
             for (int a = 0; a < 6; ++a) scale = std::max(scale, std::fabs(c->gridBox[a]));
+            const auto T2 = std::chrono::steady_clock::now();
             buildBvh(c, scale);
+            const auto T3 = std::chrono::steady_clock::now();
             remapGrid(c);
             checkEscape(c);
+            if (std::getenv("SDFGI_TIMING")) {
+                auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+                std::fprintf(stderr, "scene_upload us: arrays %.1f compare %.1f bvh %.1f remap %.1f\n", us(T0, T1),
+                             us(T1, T2), us(T2, T3), us(T3, std::chrono::steady_clock::now()));
+            }
             ++c->gridRefits;
             return;
         }
@@ -1506,7 +1570,7 @@ int sdfgi_lights_upload(void* ctx, const sdfgi_light* lights, int n_lights, cons
         Ctx* c = C(ctx);
         REQ(c->haveScene, SDFGI_ERR_STATE, "scene not uploaded");
         REQ(n_lights >= 0 && (n_lights == 0 || lights) && sky, SDFGI_ERR_INVALID, "bad lights");
-        c->lights.upload(reinterpret_cast<const DLight*>(lights), n_lights, c->stream);
+        upload(c, c->lights, reinterpret_cast<const DLight*>(lights), n_lights);
         CK(cudaStreamSynchronize(c->stream));
         c->nLights = n_lights;
         for (int k = 0; k < 3; ++k) c->sky[k] = sky[k];
@@ -1603,6 +1667,8 @@ int sdfgi_probes_reset(void* ctx, int level) {
     });
 }
 
+static_assert(sizeof(sdfgi_probe) == 11 * sizeof(double), "sdfgi_probe is 11 doubles (k_probes_unpack)");
+
 int sdfgi_probes_upload(void* ctx, int level, const sdfgi_probe* probes, int n) {
     return guard([&] {
         Ctx* c = C(ctx);
@@ -1611,25 +1677,11 @@ int sdfgi_probes_upload(void* ctx, int level, const sdfgi_probe* probes, int n) 
         c->clearValid[s] = 0;
         const CascadeHost& cs = c->cascades[s];
         REQ(probes && n == cs.count(), SDFGI_ERR_INVALID, "probe count mismatch");
-        std::vector<double> pos(3 * n), rest(3 * n), last(3 * n);
-        std::vector<int> al(n), rj(n), lf(n);
-        for (int i = 0; i < n; ++i) {
-            for (int k = 0; k < 3; ++k) {
-                pos[3 * i + k] = probes[i].pos[k];
-                rest[3 * i + k] = probes[i].resting[k];
-                last[3 * i + k] = probes[i].last_pos[k];
-            }
-            al[i] = probes[i].alive;
-            rj[i] = probes[i].reject_history;
-            lf[i] = probes[i].last_update_frame;
-        }
-        size_t off = cs.base;
-        CK(cudaMemcpyAsync(c->pos.p + 3 * off, pos.data(), pos.size() * 8, cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->rest.p + 3 * off, rest.data(), rest.size() * 8, cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->last.p + 3 * off, last.data(), last.size() * 8, cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->alive.p + off, al.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->reject.p + off, rj.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->lastFrame.p + off, lf.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
+        // the records in one copy, split into the device arrays there
+        reserve(c->probeAos, 11 * static_cast<size_t>(n));
+        stageCopy(c, c->probeAos.p, probes, static_cast<size_t>(n) * sizeof(sdfgi_probe));
+        launch_probes_unpack(c->probeCommon().probes, cs.base, n, c->probeAos.p, c->stream);
+        checkLaunch(c);
         CK(cudaStreamSynchronize(c->stream));
     });
 }
@@ -1640,27 +1692,12 @@ int sdfgi_probes_download(void* ctx, int level, sdfgi_probe* probes, int n) {
         int s = c->slot(level);
         const CascadeHost& cs = c->cascades[s];
         REQ(probes && n == cs.count(), SDFGI_ERR_INVALID, "probe count mismatch");
-        std::vector<double> pos(3 * n), rest(3 * n), last(3 * n);
-        std::vector<int> al(n), rj(n), lf(n);
-        size_t off = cs.base;
-        CK(cudaMemcpyAsync(pos.data(), c->pos.p + 3 * off, pos.size() * 8, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(rest.data(), c->rest.p + 3 * off, rest.size() * 8, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(last.data(), c->last.p + 3 * off, last.size() * 8, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(al.data(), c->alive.p + off, n * 4, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(rj.data(), c->reject.p + off, n * 4, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(lf.data(), c->lastFrame.p + off, n * 4, cudaMemcpyDeviceToHost, c->stream));
+        reserve(c->probeAos, 11 * static_cast<size_t>(n));
+        launch_probes_pack(c->probeCommon().probes, cs.base, n, c->probeAos.p, c->stream);
+        checkLaunch(c);
+        CK(cudaMemcpyAsync(probes, c->probeAos.p, static_cast<size_t>(n) * sizeof(sdfgi_probe), cudaMemcpyDeviceToHost,
+                           c->stream));
         CK(cudaStreamSynchronize(c->stream));
-        for (int i = 0; i < n; ++i) {
-            std::memset(&probes[i], 0, sizeof(sdfgi_probe));
-            for (int k = 0; k < 3; ++k) {
-                probes[i].pos[k] = pos[3 * i + k];
-                probes[i].resting[k] = rest[3 * i + k];
-                probes[i].last_pos[k] = last[3 * i + k];
-            }
-            probes[i].alive = al[i];
-            probes[i].reject_history = rj[i];
-            probes[i].last_update_frame = lf[i];
-        }
     });
 }
 
@@ -1790,7 +1827,7 @@ void updateBody(Ctx* c, const int32_t* probe_refs, int n_refs, int frame, const 
     const bool anyUpdate = probe_refs == nullptr ? c->totalProbes > 0 : n_refs > 0;
     c->atlasZero[1 - c->front] = c->atlasZero[c->front];
     if (anyUpdate) std::fill(c->atlasZero[1 - c->front].begin(), c->atlasZero[1 - c->front].end(), 0);
-    if (!all) c->refs.upload(refs.data(), refs.size(), c->stream);
+    if (!all) upload(c, c->refs, refs.data(), refs.size());
     const int nCand = static_cast<int>(refs.size());
     if (nCand > 0) {
         const int* cand = all ? nullptr : c->refs.p;
@@ -1838,7 +1875,7 @@ void updateBody(Ctx* c, const int32_t* probe_refs, int n_refs, int frame, const 
             std::vector<int> allRefs(n_refs);
             for (int i = 0; i < n_refs; ++i)
                 allRefs[i] = c->cascades[c->slot(probe_refs[2 * i])].base + probe_refs[2 * i + 1];
-            c->allRefs.upload(allRefs.data(), allRefs.size(), c->stream);
+            upload(c, c->allRefs, allRefs.data(), allRefs.size());
             ids = c->allRefs.p;
             nAll = n_refs;
         }
@@ -1991,7 +2028,7 @@ int sdfgi_probes_trace_debug(void* ctx, const int32_t* probe_refs, int n_refs, i
             g.push_back(c->cascades[s].base + probe_refs[2 * i + 1]);
         }
         const size_t cap = static_cast<size_t>(n_refs) * 2 * static_cast<size_t>(cfg->n_rays_full);
-        c->refs.upload(g.data(), g.size(), c->stream);
+        upload(c, c->refs, g.data(), g.size());
         uploadQuats(c, cfg, frame, g.data(), n_refs);
         reserve(c->records, cap);
         // the same K0..K3 wavefront in debug mode: per-ray records, no atlas/state writes
@@ -2028,8 +2065,8 @@ int sdfgi_query_points(void* ctx, const double* points_xyz, const double* init_d
         REQ(c->haveScene, SDFGI_ERR_STATE, "scene not uploaded");
         REQ(n >= 0 && (n == 0 || (points_xyz && out_d && out_owner)), SDFGI_ERR_INVALID, "bad query arguments");
         if (n == 0) return;
-        c->qpts.upload(points_xyz, 3 * static_cast<size_t>(n), c->stream);
-        if (init_d) c->qinit.upload(init_d, n, c->stream);
+        upload(c, c->qpts, points_xyz, 3 * static_cast<size_t>(n));
+        if (init_d) upload(c, c->qinit, init_d, n);
         c->qd.alloc(n);
         c->qowner.alloc(n);
         QueryParams p;
@@ -2918,7 +2955,7 @@ int sdfgi_interpolation_stencil(void* ctx, const double* points, int n, double m
         if (n == 0) return;
         DBuf<double> pts, w;
         DBuf<int> idx, meta;
-        pts.upload(points, 3 * static_cast<size_t>(n), c->stream);
+        upload(c, pts, points, 3 * static_cast<size_t>(n));
         w.alloc(8 * static_cast<size_t>(n));
         idx.alloc(8 * static_cast<size_t>(n));
         meta.alloc(5 * static_cast<size_t>(n));
