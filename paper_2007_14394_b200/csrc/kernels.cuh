@@ -149,6 +149,10 @@ template <typename R> struct WaveParams {
     // accel mode 2: every probe's SDF from the relocation that just ran (clear) is its
     // rays' first query, the same query at the same point (k_probe_ray_setup)
     int useClear;
+    // a march query that lands within eps with an exact result (an owner found below
+    // its bound) already holds the owner query's answer at that point (same value,
+    // same lowest-CSR-position tie-break): the polish starts without re-querying
+    int ownerFromMarch;
     // accel mode 2: a march whose point leaves the candidate grid (which holds every
     // bounded primitive) after starting inside it can never converge again (the grid
     // box is convex, no unbounded primitive): K1 ends it as a miss on the spot

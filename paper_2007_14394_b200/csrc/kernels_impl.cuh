@@ -657,7 +657,14 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
             } else if (state == 0) {
                 if (nd < eps) {
                     d = nd;
-                    state = 1;
+                    if (P.ownerFromMarch && o2 >= 0) {  // the owner query's result, already known
+                        owner = o2;
+                        pol = 0;
+                        state = 2;
+                        if (!(fabs(d) > R(0.25) * eps)) done = 1;
+                    } else {
+                        state = 1;
+                    }
                 } else if (nd >= tMax - t) {
                     done = 2;
                 } else {

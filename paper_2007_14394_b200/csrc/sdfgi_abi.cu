@@ -1016,6 +1016,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.currAtlas = c->atlas[1 - c->front].p;
     p.prevZero = c->frontZero() ? 1 : 0;
     p.escape = escapeOk(c);
+    p.ownerFromMarch = c->accel == 2 && c->haveGrid ? 1 : 0;
     p.useClear = c->accel == 2 && !c->clearValid.empty() &&
                  std::all_of(c->clearValid.begin(), c->clearValid.end(), [](char v) { return v != 0; });
     p.oct = c->octRes;
