@@ -149,6 +149,9 @@ template <typename R> struct WaveParams {
     // accel mode 2: every probe's SDF from the relocation that just ran (clear) is its
     // rays' first query, the same query at the same point (k_probe_ray_setup)
     int useClear;
+    // K3a: hits whose bounce lookup takes the trilinear stencil, finished by K3c
+    // before its MVC list (null: K3a looks them up itself)
+    int* triList;
     // a march query that lands within eps with an exact result (an owner found below
     // its bound) already holds the owner query's answer at that point (same value,
     // same lowest-CSR-position tie-break): the polish starts without re-querying
@@ -344,8 +347,8 @@ constexpr int kWaveThreads = 128;   // K1/K2 persistent CTAs
 // line would serialise there (and slow every read of the line); the per-light
 // shadow-march counts follow, read-only while K2 runs.
 constexpr int kCtrRay = 0, kCtrHits = 16, kCtrShadow = 32, kCtrParkRay = 48, kCtrFarRay = 64, kCtrParkShadow = 80,
-              kCtrFarShadow = 96, kCtrMvc = 112;
-constexpr int kLightCtr = 128;
+              kCtrFarShadow = 96, kCtrMvc = 112, kCtrTri = 128;
+constexpr int kLightCtr = 144;
 // minimum resident K1/K2/K3a CTAs per SM (register cap = 64K / (128 * n)); the
 // tracing kernels are latency bound at low occupancy (measured, profiles/)
 #ifndef SDFGI_WAVE_MINB64

@@ -1016,13 +1016,15 @@ __device__ __forceinline__ V3<double> shadeRay(const WaveParams<R>& P, const Hit
 // true when the stencil takes the MVC path (probe_volume.hpp:278), whose bounce
 // term K3c adds (radiance = radiance + brdf * (prev * bounceCoeff), the same
 // addition in the same order as probe_update.hpp:143-147).
+// Returns 0 (done), 1 (MVC stencil: K3c) or 2 (trilinear stencil deferred to K3c's
+// list of those, when P.triList is set).
 template <typename R>
-__device__ __forceinline__ bool shadeRayDeferred(const WaveParams<R>& P, const HitRec<R>& h, unsigned long long rid,
-                                                 V3<double>* out) {
+__device__ __forceinline__ int shadeRayDeferred(const WaveParams<R>& P, const HitRec<R>& h, unsigned long long rid,
+                                                V3<double>* out) {
     const SceneView<R>& s = P.scene;
     if (!(h.status & 1) || h.owner < 0) {
         *out = mk(s.sky[0], s.sky[1], s.sky[2]);
-        return false;
+        return 0;
     }
     const V3<double> total = directLight(P, h, rid);
     const double* A = s.albedo + 3 * h.owner;
@@ -1030,19 +1032,33 @@ __device__ __forceinline__ bool shadeRayDeferred(const WaveParams<R>& P, const H
     const V3<double> brdf = mk(A[0], A[1], A[2]) / kPi;
     V3<double> radiance = mk(E[0], E[1], E[2]) + brdf * total;
     *out = radiance;
-    if (!(P.tc.bounceCoeff > 0 && P.prevAtlas != nullptr && P.pc.nCas > 0) || P.prevZero) return false;
+    if (!(P.tc.bounceCoeff > 0 && P.prevAtlas != nullptr && P.pc.nCas > 0) || P.prevZero) return 0;
     const V3<double> hp = mk<double>(h.p[0], h.p[1], h.p[2]);
     const V3<double> hn = mk<double>(h.n[0], h.n[1], h.n[2]);
     const StencilCell sc = stencilCell(P.pc.cas, P.pc.nCas, P.pc.probes, hp, P.tc.mvcFrac);
-    if (sc.chosen < 0) return false;  // sky fallback: no bounce
-    if (sc.wantMvc) return true;
+    if (sc.chosen < 0) return 0;  // sky fallback: no bounce
+    if (sc.wantMvc) return 1;
+    if (P.triList) return 2;
     double w[8];
     for (int k = 0; k < 8; ++k) w[k] = trilinearWeight(sc, k);
     const Stencil st = finishStencil(P.pc.cas, P.pc.probes, sc, w, 0);
     V3<double> prev;
     if (bounceFromStencil<R>(P.pc.cas, P.pc.probes, P.prevAtlas, P.oct, st, hp, hn, &prev))
         *out = radiance + brdf * (prev * P.tc.bounceCoeff);
-    return false;
+    return 0;
+}
+
+// Append rid to the list whose counter is ctr[slot] (lanes with want = true).
+__device__ __forceinline__ void appendList(unsigned long long* ctr, int slot, int* list, bool want, int rid) {
+    const unsigned am = __activemask();
+    const unsigned m = __ballot_sync(am, want);
+    if (!m) return;
+    const int leader = __ffs(m) - 1;
+    unsigned long long base = 0;
+    if (static_cast<int>(threadIdx.x & 31) == leader)
+        base = atomicAdd(ctr + slot, static_cast<unsigned long long>(__popc(m)));
+    base = __shfl_sync(am, base, leader);
+    if (want) list[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = rid;
 }
 
 // K3a: shadeHit per ray (thread per ray, grid-stride): emission + directIrradiance
@@ -1067,17 +1083,9 @@ __global__ void __launch_bounds__(128, WaveOcc<R>::shade) k_shade_rays(WaveParam
         int mvc = 0;
         V3<double> L;
         if constexpr (DEFER) {
-            const bool defer = shadeRayDeferred(P, h, static_cast<unsigned long long>(rid), &L);
-            const unsigned am = __activemask();
-            const unsigned m = __ballot_sync(am, defer);
-            if (m) {
-                const int leader = __ffs(m) - 1;
-                unsigned long long base = 0;
-                if (static_cast<int>(threadIdx.x & 31) == leader)
-                    base = atomicAdd(P.ctr + kCtrMvc, static_cast<unsigned long long>(__popc(m)));
-                base = __shfl_sync(am, base, leader);
-                if (defer) P.mvcList[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = static_cast<int>(rid);
-            }
+            const int defer = shadeRayDeferred(P, h, static_cast<unsigned long long>(rid), &L);
+            appendList(P.ctr, kCtrMvc, P.mvcList, defer == 1, static_cast<int>(rid));
+            if (P.triList) appendList(P.ctr, kCtrTri, P.triList, defer == 2, static_cast<int>(rid));
         } else {
             L = shadeRay(P, h, static_cast<unsigned long long>(rid), slab, ST ? &mvc : nullptr);
         }
@@ -1132,6 +1140,35 @@ __global__ void __launch_bounds__(128, WaveOcc<R>::shade) k_shade_rays(WaveParam
 // in a per-thread shared-memory slab. (Evaluating each of the cell's 18 distinct
 // edge angles once instead of per triangle was measured slower: the larger slab
 // halves the resident warps, profiles/README.md.)
+// K3a's deferred trilinear bounce lookups (P.triList): every lane takes the same
+// path at full occupancy; the same stencil and addition as in K3a
+// (shadeRayDeferred / probe_update.hpp:143-147).
+template <typename R>
+__global__ void __launch_bounds__(256) k_shade_tri(WaveParams<R> P) {
+    const long long n = static_cast<long long>(P.ctr[kCtrTri]);
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += stride) {
+        const int rid = P.triList[j];
+        const HitRec<R> h = P.hits[rid];
+        const V3<double> hp = mk<double>(h.p[0], h.p[1], h.p[2]);
+        const V3<double> hn = mk<double>(h.n[0], h.n[1], h.n[2]);
+        const StencilCell sc = stencilCell(P.pc.cas, P.pc.nCas, P.pc.probes, hp, P.tc.mvcFrac, false);
+        double w[8];
+        for (int k = 0; k < 8; ++k) w[k] = trilinearWeight(sc, k);
+        const Stencil st = finishStencil(P.pc.cas, P.pc.probes, sc, w, 0);
+        V3<double> prev;
+        if (bounceFromStencil<R>(P.pc.cas, P.pc.probes, P.prevAtlas, P.oct, st, hp, hn, &prev)) {
+            const double* A = P.scene.albedo + 3 * h.owner;
+            const V3<double> brdf = mk(A[0], A[1], A[2]) / kPi;
+            const V3<double> base = mk(double(P.rad[3 * rid]), double(P.rad[3 * rid + 1]), double(P.rad[3 * rid + 2]));
+            const V3<double> L = base + brdf * (prev * P.tc.bounceCoeff);
+            P.rad[3 * rid] = R(L.x);
+            P.rad[3 * rid + 1] = R(L.y);
+            P.rad[3 * rid + 2] = R(L.z);
+        }
+    }
+}
+
 template <typename R, bool ST>
 __global__ void __launch_bounds__(kMvcThreads, kMvcMinBlocks) k_shade_mvc(WaveParams<R> P) {
     extern __shared__ __align__(16) unsigned char k3cSmem[];
@@ -1352,6 +1389,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
     static int b3 = persistentBlocks(k_shade_rays<R, ST, true>, 128, 0);
     static int b3d = persistentBlocks(k_shade_rays<R, ST, false>, 128, 0, 128 * kMvcSlab * sizeof(R));
     static int b3c = persistentBlocks(k_shade_mvc<R, ST>, kMvcThreads, 0, kMvcThreads * kMvcSlab * sizeof(R));
+    static int b3t = persistentBlocks(k_shade_tri<R>, 256, 0);
     // hitAt covers the batch's upper bound of rays; slots past the traced ones stay -1
     cudaMemsetAsync(p.hitAt, 0xff, static_cast<size_t>(p.maxItems) * sizeof(int), st);
     mark(0);
@@ -1374,6 +1412,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
         k_shade_rays<R, ST, false><<<b3d, 128, 128 * kMvcSlab * sizeof(R), st>>>(p);
     } else {
         k_shade_rays<R, ST, true><<<b3, 128, 0, st>>>(p);
+        k_shade_tri<R><<<b3t, 256, 0, st>>>(p);
         k_shade_mvc<R, ST><<<b3c, kMvcThreads, kMvcThreads * kMvcSlab * sizeof(R), st>>>(p);
     }
     mark(6);
@@ -1388,7 +1427,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
         k3<<<p.nCand, kConvThreads, smem, st>>>(p);
     }
     mark(7);
-    if (launches) *launches += p.debug ? 11 : 14;
+    if (launches) *launches += p.debug ? 11 : 15;
 }
 
 // contactGI's per-pixel sum (shading.hpp:686-713): AO from the missed samples,
@@ -1442,6 +1481,7 @@ static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long*
     if (p.cray) k_contact_setup<R><<<static_cast<int>((p.nRaysDirect + 255) / 256), 256, 0, st>>>(p);
     static int b3 = persistentBlocks(k_shade_rays<R, ST, true>, 128, 0);
     static int b3c = persistentBlocks(k_shade_mvc<R, ST>, kMvcThreads, 0, kMvcThreads * kMvcSlab * sizeof(R));
+    static int b3t = persistentBlocks(k_shade_tri<R>, 256, 0);
     launchPrimary<R, ST, 1, 0>(p, 0, st);
     launchPrimary<R, ST, 1, 1>(p, 0, st);
     compact_hits(p.hitAt, p.hitList, p.ctr + kCtrHits, static_cast<int>(p.maxItems), p.selTemp, p.selTempBytes, st);
@@ -1449,10 +1489,11 @@ static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long*
     launchShadow<R, ST, 0>(p, 0, st);
     launchShadow<R, ST, 1>(p, 0, st);
     k_shade_rays<R, ST, true><<<b3, 128, 0, st>>>(p);
+    k_shade_tri<R><<<b3t, 256, 0, st>>>(p);
     k_shade_mvc<R, ST><<<b3c, kMvcThreads, kMvcThreads * kMvcSlab * sizeof(R), st>>>(p);
     const long long np = static_cast<long long>(p.gw) * p.gh;
     k_contact_combine<R><<<static_cast<int>((np + 127) / 128), 128, 0, st>>>(p);
-    if (launches) *launches += p.cray ? 10 : 9;
+    if (launches) *launches += p.cray ? 11 : 10;
 }
 
 // composeFrame (shading.hpp:480-504) as a wavefront: every geometry pixel becomes a
@@ -1570,9 +1611,10 @@ void launch_batch(const WaveParams<R>& p, int kind, bool stats, cudaStream_t st,
             launchShadow<R, false, 1>(p, 0, st);
         }
         ka<<<persistentBlocks(ka, 128, 0), 128, 0, st>>>(p);
+        k_shade_tri<R><<<persistentBlocks(k_shade_tri<R>, 256, 0), 256, 0, st>>>(p);
         kc<<<persistentBlocks(kc, kMvcThreads, 0, kMvcThreads * kMvcSlab * sizeof(R)), kMvcThreads,
              kMvcThreads * kMvcSlab * sizeof(R), st>>>(p);
-        if (launches) *launches += 5;
+        if (launches) *launches += 6;
     }
 }
 

@@ -1188,8 +1188,9 @@ struct StencilCell {
     bool wantMvc;
     bool boundary;  // InterpolationStencil::crossCascade (probe_volume.hpp:276)
 };
+// checkMvc = false: the caller knows the MVC test fails (wantMvc stays false).
 __device__ inline StencilCell stencilCell(const CascadeDev* cas, int nCas, const ProbesView& pv, V3<double> point,
-                                          double mvcFrac) {
+                                          double mvcFrac, bool checkMvc = true) {
     StencilCell sc;
     sc.chosen = -1;
     sc.wantMvc = false;
@@ -1235,8 +1236,8 @@ __device__ inline StencilCell stencilCell(const CascadeDev* cas, int nCas, const
     const double thr = mvcFrac * c.spacing;
     const double thr2 = thr * thr;
     const bool squared = thr > 0 && thr2 > 1e-280 && thr2 < 1e280;
-    bool wantMvc = boundary || thr < 0;  // maxDisp >= 0 > thr
-    for (int k = 0; k < 8 && !wantMvc; ++k) {
+    bool wantMvc = checkMvc && (boundary || thr < 0);  // maxDisp >= 0 > thr
+    for (int k = 0; k < 8 && checkMvc && !wantMvc; ++k) {
         const double* Q = pv.rest + 3 * static_cast<size_t>(cc.index(k));
         const V3<double> dv = cc.corner(k) - mk(Q[0], Q[1], Q[2]);
         const double d2 = dot(dv, dv);

@@ -217,7 +217,7 @@ struct Ctx {
     DBuf<int> refs, allRefs;
     DBuf<RayRecord> records;
     // wavefront scratch (kernels.cuh)
-    DBuf<int> wRayCount, wHitList, wChunk, wHitAt, wMvcList;
+    DBuf<int> wRayCount, wHitList, wChunk, wHitAt, wMvcList, wTriList;
     DBuf<long long> wRayStart;
     DBuf<double> wRot, fib;
     DBuf<int> perm;
@@ -279,7 +279,7 @@ struct Ctx {
         pos.free(); rest.free(); last.free(); clear.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free(); allRefs.free();
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
-        wRayCount.free(); wHitList.free(); wMvcList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); cLocal.free(); wHits.free();
+        wRayCount.free(); wHitList.free(); wMvcList.free(); wTriList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); cLocal.free(); wHits.free();
         if (hReport) cudaFreeHost(hReport);
         if (arena) cudaFreeHost(arena);
         if (arenaEv) cudaEventDestroy(arenaEv);
@@ -966,6 +966,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     reserve(c->wHits, std::max<size_t>(maxRays, 1) * sizeof(HitRec<R>));
     reserve(c->wHitList, std::max<size_t>(maxRays, 1));
     reserve(c->wMvcList, std::max<size_t>(maxRays, 1));
+    reserve(c->wTriList, std::max<size_t>(maxRays, 1));
     reserve(c->wVis, std::max<size_t>(maxRays, 1) * L * sizeof(R));
     reserve(c->wRad, std::max<size_t>(maxRays, 1) * 3 * sizeof(R));
     reserve(c->wCtr, kLightCtr + L);
@@ -1004,6 +1005,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.hits = reinterpret_cast<HitRec<R>*>(c->wHits.p);
     p.hitList = c->wHitList.p;
     p.mvcList = c->wMvcList.p;
+    p.triList = c->wTriList.p;
     p.vis = reinterpret_cast<R*>(c->wVis.p);
     p.rad = reinterpret_cast<R*>(c->wRad.p);
     p.ctr = c->wCtr.p;
@@ -2227,6 +2229,7 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     reserve(c->wHits, cap * sizeof(HitRec<R>));
     reserve(c->wHitList, cap);
     reserve(c->wMvcList, cap);
+    reserve(c->wTriList, cap);
     reserve(c->wVis, cap * L * sizeof(R));
     reserve(c->wRad, cap * 3 * sizeof(R));
     reserve(c->wCtr, kLightCtr + L);
@@ -2264,6 +2267,7 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     p.hits = reinterpret_cast<HitRec<R>*>(c->wHits.p);
     p.hitList = c->wHitList.p;
     p.mvcList = c->wMvcList.p;
+    p.triList = c->wTriList.p;
     p.vis = reinterpret_cast<R*>(c->wVis.p);
     p.rad = reinterpret_cast<R*>(c->wRad.p);
     p.ctr = c->wCtr.p;
@@ -2693,6 +2697,7 @@ WaveParams<R> batchParams(Ctx* c, size_t n) {
     reserve(c->wHits, cap * sizeof(HitRec<R>));
     reserve(c->wHitList, cap);
     reserve(c->wMvcList, cap);
+    reserve(c->wTriList, cap);
     reserve(c->wVis, cap * L * sizeof(R));
     reserve(c->wRad, cap * 3 * sizeof(R));
     reserve(c->wCtr, kLightCtr + L);
@@ -2706,6 +2711,7 @@ WaveParams<R> batchParams(Ctx* c, size_t n) {
     p.hits = reinterpret_cast<HitRec<R>*>(c->wHits.p);
     p.hitList = c->wHitList.p;
     p.mvcList = c->wMvcList.p;
+    p.triList = c->wTriList.p;
     p.vis = reinterpret_cast<R*>(c->wVis.p);
     p.rad = reinterpret_cast<R*>(c->wRad.p);
     p.ctr = c->wCtr.p;
