@@ -399,6 +399,12 @@ constexpr int kMvcMinBlocks = SDFGI_MVC_MINB;
 #define SDFGI_CONV_TEXEL 1
 #endif
 constexpr bool kConvPerTexel = SDFGI_CONV_TEXEL != 0;
+// K3b streams a probe's rays through shared memory in chunks of kConvChunk
+// (6 KB in FP64 instead of the whole 2N-ray set: 4x the resident CTAs)
+#ifndef SDFGI_CONV_CHUNK
+#define SDFGI_CONV_CHUNK 128
+#endif
+constexpr int kConvChunk = SDFGI_CONV_CHUNK;
 constexpr int kConvThreads = kConvPerTexel ? 64 : 192;
 constexpr int kScanThreads = 1024;  // K0 prefix sum
 

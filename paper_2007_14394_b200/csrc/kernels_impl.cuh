@@ -1217,8 +1217,81 @@ __global__ void __launch_bounds__(kConvThreads) k_convolve(WaveParams<R> P) {
     const ProbesView& pv = P.pc.probes;
     const int reject = n != P.nRaysFull;  // 2N rays <=> rejectHistory at setup
     const long long start = P.rayStart[s];
+    const int res = P.oct;
+    const int T = res + 2;
+    const double alpha = reject ? 1.0 : sclamp((1.0 - P.hysteresis) * n / P.nRaysFull, P.alphaMin, 1.0);
+    const double scale = 4.0 * kPi / static_cast<double>(n);
+    const float* oldTile = P.prevAtlas + static_cast<size_t>(g) * T * T * 3;
+    double maxDelta = 0.0;
+    if (kConvChunk > 0) {
+        // per ray (dir, radiance) as 6 values, read as three 16-byte words; each
+        // thread sums up to two texels, every channel in the rays' order
+        __shared__ __align__(16) R sray[(kConvChunk > 0 ? kConvChunk : 1) * 6];
+        const int nt = res * res;
+        const int txA = threadIdx.x, txB = threadIdx.x + blockDim.x;
+        R D[2][3];
+        for (int q = 0; q < 2; ++q) {
+            const int tx = q ? txB : txA;
+            const int y = tx / res, x = tx % res;
+            const V3<double> dd = octDecode(V2<double>{(x + 0.5) / res, (y + 0.5) / res});
+            D[q][0] = R(dd.x);
+            D[q][1] = R(dd.y);
+            D[q][2] = R(dd.z);
+        }
+        const bool hasA = txA < nt, hasB = txB < nt;
+        R a[2][3] = {{0, 0, 0}, {0, 0, 0}};
+        for (int c0 = 0; c0 < n; c0 += kConvChunk) {
+            const int m = min(kConvChunk, n - c0);
+            __syncthreads();  // the previous chunk is consumed
+            for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                const V3<double> dir = rayDirection(P, s, c0 + i, n);
+                sray[6 * i] = R(dir.x);
+                sray[6 * i + 1] = R(dir.y);
+                sray[6 * i + 2] = R(dir.z);
+            }
+            for (int k = threadIdx.x; k < 3 * m; k += blockDim.x)
+                sray[6 * (k / 3) + 3 + k % 3] = __ldcs(&P.rad[3 * (start + c0) + k]);
+            __syncthreads();
+            if (hasA) {
+                for (int i = 0; i < m; ++i) {
+                    R r[6];
+                    if constexpr (sizeof(R) == 8) {
+                        const double2* v = reinterpret_cast<const double2*>(sray + 6 * i);
+                        const double2 u0 = v[0], u1 = v[1], u2 = v[2];
+                        r[0] = u0.x; r[1] = u0.y; r[2] = u1.x; r[3] = u1.y; r[4] = u2.x; r[5] = u2.y;
+                    } else {
+                        for (int k = 0; k < 6; ++k) r[k] = sray[6 * i + k];
+                    }
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        if (q == 1 && !hasB) break;
+                        const R w = D[q][0] * r[0] + D[q][1] * r[1] + D[q][2] * r[2];
+                        if (w > R(0)) {
+                            a[q][0] = a[q][0] + r[3] * w;
+                            a[q][1] = a[q][1] + r[4] * w;
+                            a[q][2] = a[q][2] + r[5] * w;
+                        }
+                    }
+                }
+            }
+        }
+        for (int q = 0; q < 2; ++q) {
+            const int tx = q ? txB : txA;
+            if (tx >= nt) continue;
+            const int y = tx / res, x = tx % res;
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                const double fresh = double(a[q][ch]) * scale;
+                const double old = oldTile[((y + 1) * T + (x + 1)) * 3 + ch];
+                const double bl = old + (fresh - old) * alpha;
+                maxDelta = smax(maxDelta, fabs(bl - old));
+                tile[((y + 1) * T + (x + 1)) * 3 + ch] = static_cast<float>(bl);
+            }
+        }
+    }
     R* sdir = reinterpret_cast<R*>(smem_raw);  // 3n
     R* srad = sdir + 3 * n;                    // 3n
+    if (kConvChunk == 0) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const V3<double> dir = rayDirection(P, s, i, n);
         sdir[3 * i] = R(dir.x);
@@ -1227,14 +1300,9 @@ __global__ void __launch_bounds__(kConvThreads) k_convolve(WaveParams<R> P) {
     }
     for (int k = threadIdx.x; k < 3 * n; k += blockDim.x) srad[k] = __ldcs(&P.rad[3 * start + k]);
     __syncthreads();
-
-    const int res = P.oct;
-    const int T = res + 2;
-    const double alpha = reject ? 1.0 : sclamp((1.0 - P.hysteresis) * n / P.nRaysFull, P.alphaMin, 1.0);
-    const double scale = 4.0 * kPi / static_cast<double>(n);
-    const float* oldTile = P.prevAtlas + static_cast<size_t>(g) * T * T * 3;
-    double maxDelta = 0.0;
-    if (kConvPerTexel) {
+    }
+    if (kConvChunk > 0) {
+    } else if (kConvPerTexel) {
         for (int tx = threadIdx.x; tx < res * res; tx += blockDim.x) {
             const int y = tx / res, x = tx % res;
             const V3<double> dd = octDecode(V2<double>{(x + 0.5) / res, (y + 0.5) / res});
@@ -1417,7 +1485,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
     }
     mark(6);
     if (!p.debug) {
-        const size_t smem = static_cast<size_t>(2 * p.nRaysFull) * 6 * sizeof(R);
+        const size_t smem = kConvChunk > 0 ? 0 : static_cast<size_t>(2 * p.nRaysFull) * 6 * sizeof(R);
         auto k3 = k_convolve<R, ST>;
         // dynamic + static shared memory above the 48 KB default needs the opt-in
         cudaFuncAttributes fa;
