@@ -1458,6 +1458,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
     static int b3d = persistentBlocks(k_shade_rays<R, ST, false>, 128, 0, 128 * kMvcSlab * sizeof(R));
     static int b3c = persistentBlocks(k_shade_mvc<R, ST>, kMvcThreads, 0, kMvcThreads * kMvcSlab * sizeof(R));
     static int b3t = persistentBlocks(k_shade_tri<R>, 256, 0);
+    static int bn = persistentBlocks(k_hit_normals<R>, 128, 0);  // its own occupancy, not K3a's
     // hitAt covers the batch's upper bound of rays; slots past the traced ones stay -1
     cudaMemsetAsync(p.hitAt, 0xff, static_cast<size_t>(p.maxItems) * sizeof(int), st);
     mark(0);
@@ -1466,7 +1467,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
     launchPrimary<R, ST, 0, 1>(p, cap, st);
     mark(2);
     compact_hits(p.hitAt, p.hitList, p.ctr + kCtrHits, static_cast<int>(p.maxItems), p.selTemp, p.selTempBytes, st);
-    k_hit_normals<R><<<b3, 128, 0, st>>>(p);
+    k_hit_normals<R><<<bn, 128, 0, st>>>(p);
     mark(3);
     // the shadow kernels count their events in a separate block of counters
     // (stats + kShadowStats), so the work of K1 and K2 can be told apart
@@ -1550,10 +1551,11 @@ static void contactWavefront(const WaveParams<R>& p, cudaStream_t st, long long*
     static int b3 = persistentBlocks(k_shade_rays<R, ST, true>, 128, 0);
     static int b3c = persistentBlocks(k_shade_mvc<R, ST>, kMvcThreads, 0, kMvcThreads * kMvcSlab * sizeof(R));
     static int b3t = persistentBlocks(k_shade_tri<R>, 256, 0);
+    static int bn = persistentBlocks(k_hit_normals<R>, 128, 0);  // its own occupancy, not K3a's
     launchPrimary<R, ST, 1, 0>(p, 0, st);
     launchPrimary<R, ST, 1, 1>(p, 0, st);
     compact_hits(p.hitAt, p.hitList, p.ctr + kCtrHits, static_cast<int>(p.maxItems), p.selTemp, p.selTempBytes, st);
-    k_hit_normals<R><<<b3, 128, 0, st>>>(p);
+    k_hit_normals<R><<<bn, 128, 0, st>>>(p);
     launchShadow<R, ST, 0>(p, 0, st);
     launchShadow<R, ST, 1>(p, 0, st);
     k_shade_rays<R, ST, true><<<b3, 128, 0, st>>>(p);
