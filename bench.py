@@ -334,24 +334,25 @@ class StepRunner:
         work = dict.fromkeys(("k1", "k2", "shade", "convolve"), 0.0)
         prec = dev.precision
         for p in range(PASSES):
-            if stats:  # relocation and update counters apart: one call each
-                stage.relocate_all(stats=True)
-                r = api.updateProbes(dev, stage.cfg, p, None, stats=True)
-            else:  # the probe stage of pipeline.hpp:108-151 in one call, one host sync
-                r = dev.probe_stage(p, stage.cfg)[1]
-            if stats:
-                res, st = r
-                tc = dev.last_trace_counters()
-                sh = dev.last_shading_work()
-                work["k1"] += workmodel.query_ops(*tc["k1"])
-                work["k2"] += workmodel.query_ops(*tc["k2"])
-                work["shade"] += workmodel.shading_ops(sh, prec)
-                work["convolve"] += workmodel.convolve_ops(int(res["rays_traced"]))
-                work_all.append({"k1": tc["k1"], "k2": tc["k2"], "shading": sh})
-            else:
-                res = r
+            if not stats:  # the probe stage of pipeline.hpp:108-151 queued (one sync per step, below)
+                dev.probe_stage_async(p, stage.cfg)
+                dev.swap()
+                continue
+            # relocation and update counters apart: one call each
+            stage.relocate_all(stats=True)
+            res, st = api.updateProbes(dev, stage.cfg, p, None, stats=True)
+            tc = dev.last_trace_counters()
+            sh = dev.last_shading_work()
+            work["k1"] += workmodel.query_ops(*tc["k1"])
+            work["k2"] += workmodel.query_ops(*tc["k2"])
+            work["shade"] += workmodel.shading_ops(sh, prec)
+            work["convolve"] += workmodel.convolve_ops(int(res["rays_traced"]))
+            work_all.append({"k1": tc["k1"], "k2": tc["k2"], "shading": sh})
             rays += int(res["rays_traced"])
             dev.swap()
+        if not stats:  # the step's passes, their results read back
+            _, results = dev.probe_stage_collect()
+            rays = int(results["rays_traced"].sum())
         # every pass's stage events, summed on the device side (read once per step)
         stage_ms, upd_ms = dev.stage_ms_sum(reset=True)
         return rays, upd_ms, stage_ms, work, work_all
@@ -693,9 +694,10 @@ def e2e_run(args, dev, stage, scene, barrier, dist, torch):
         dev.reset_probes(0)  # fresh volume: zero atlases (makeCascade)
         dev.upload_probes(0, probes_host)
         r = 0
-        for p in range(PASSES):
-            _, res = stage.run_pass(p)  # relocation + update (sdfgi_probe_stage) + swap
-            r += int(res["rays_traced"])
+        for p in range(PASSES):  # relocation + update queued (sdfgi_probe_stage_async) + swap
+            dev.probe_stage_async(p, stage.cfg)
+            dev.swap()
+        r = int(dev.probe_stage_collect()[1]["rays_traced"].sum())
         dev.atlas(0, 0, out=atlas_host)  # straight into the pinned buffer
         dt = time.perf_counter() - t0
         if i > 0:  # first iteration is a warm-up

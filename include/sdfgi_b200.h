@@ -293,6 +293,18 @@ SDFGI_API int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_re
 SDFGI_API int sdfgi_probe_stage(void* ctx, int frame, const sdfgi_cfg* cfg, const double cam_pos[3],
                                 const double cam_fwd[3], sdfgi_reloc_report* reports, int n_reports,
                                 sdfgi_update_result* result, sdfgi_stats* stats);
+/* sdfgi_probe_stage without the host synchronisation: the pass is queued on the
+ * context's stream and the call returns; up to 8 passes (with sdfgi_atlas_swap
+ * between them) may be in flight, so the host prepares pass p+1 while the device
+ * runs pass p. Their reports and results come from sdfgi_probe_stage_collect, in
+ * pass order (reports: reports_per_pass per pass, cascade order; results: one per
+ * pass); it synchronises, adds the passes' stage times to sdfgi_stage_ms_sum and
+ * returns the pass count in *n_passes. No TraceStats in this form. A budgeted
+ * pass (cfg->probe_budget > 0) synchronises for its selection. */
+SDFGI_API int sdfgi_probe_stage_async(void* ctx, int frame, const sdfgi_cfg* cfg, const double cam_pos[3],
+                                      const double cam_fwd[3]);
+SDFGI_API int sdfgi_probe_stage_collect(void* ctx, sdfgi_reloc_report* reports, int reports_per_pass,
+                                        sdfgi_update_result* results, int max_passes, int* n_passes);
 /* readIdx swap at frame end (pipeline.hpp:220). */
 SDFGI_API int sdfgi_atlas_swap(void* ctx);
 /* which = 0: front (read) atlas, 1: back (write) atlas. Layout = ProbeAtlas::raw()

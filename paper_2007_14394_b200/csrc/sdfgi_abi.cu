@@ -123,6 +123,18 @@ struct Ctx {
     cudaEvent_t kev[kWaveEvents] = {};  // the last update's stage boundaries (launch_wavefront)
     bool evUpdate = false, evReloc = false;
     double stageSum[kWaveEvents] = {};  // sdfgi_stage_ms_sum: stages + update total since the last reset
+    // The probe stage's counters and stage events: the context's own (synchronous
+    // calls) or, for sdfgi_probe_stage_async, pass slot k's until it is collected.
+    unsigned long long* scr = nullptr;
+    cudaEvent_t* kevCur = nullptr;
+    static constexpr int kMaxPending = 8;
+    static constexpr int kSlotWords = kShadowStats + 32;
+    DBuf<unsigned long long> scratchAsync;           // kMaxPending x kSlotWords
+    cudaEvent_t kevAsync[kMaxPending][kWaveEvents] = {};
+    unsigned long long* hAsync = nullptr;            // pinned, per slot: 3 tail words + 2 * kMaxCascades report words
+    int nPending = 0;
+    bool pendingTimed[kMaxPending] = {};
+    int pendingCascades[kMaxPending] = {};
     ncclComm_t comm = nullptr;
     long long launches = 0;
     // scene
@@ -281,6 +293,11 @@ struct Ctx {
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
         wRayCount.free(); wHitList.free(); wMvcList.free(); wTriList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); cLocal.free(); wHits.free();
         if (hReport) cudaFreeHost(hReport);
+        if (hAsync) cudaFreeHost(hAsync);
+        scratchAsync.free();
+        for (auto& row : kevAsync)
+            for (auto& e : row)
+                if (e) cudaEventDestroy(e);
         if (arena) cudaFreeHost(arena);
         if (arenaEv) cudaEventDestroy(arenaEv);
         probeAos.free();
@@ -858,7 +875,7 @@ void buildGrid(Ctx* c) {
 void readCounters(Ctx* c, sdfgi_stats* stats, unsigned long long* tail, int ntail) {
     // [0..13] K1 (and relocation) counters, [16..] tail values, [kShadowStats..+13] K2's
     std::vector<unsigned long long> h(kShadowStats + 32);
-    CK(cudaMemcpyAsync(h.data(), c->scratch.p, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(h.data(), c->scr, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (stats) {
         const unsigned long long* k2 = h.data() + kShadowStats;
@@ -1035,10 +1052,10 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.nRaysFull = static_cast<int>(cfg->n_rays_full);
     p.seed = cfg->seed;
     p.rotatePerFrame = static_cast<int>(cfg->rotate_per_frame);
-    p.stats = c->scratch.p;
-    p.maxDeltaBits = c->scratch.p + 16;
-    p.rays = c->scratch.p + 17;
-    p.updated = reinterpret_cast<unsigned int*>(c->scratch.p + 18);
+    p.stats = c->scr;
+    p.maxDeltaBits = c->scr + 16;
+    p.rays = c->scr + 17;
+    p.updated = reinterpret_cast<unsigned int*>(c->scr + 18);
     return p;
 }
 
@@ -1238,7 +1255,9 @@ int sdfgi_ctx_create(int device, int rank, int world, const uint8_t* nccl_uid, i
             }
             for (auto& e : c->kev) CK(cudaEventCreate(&e));
             c->scratch.alloc(kShadowStats + 32);
-            c->report.alloc(4 * kMaxCascades);
+            c->report.alloc(4 * kMaxCascades * (Ctx::kMaxPending + 1));
+            c->scr = c->scratch.p;
+            c->kevCur = c->kev;
             CK(cudaMallocHost(&c->hReport, 4 * kMaxCascades * sizeof(int)));
             CK(cudaEventCreateWithFlags(&c->arenaEv, cudaEventDisableTiming));
             CK(cudaEventRecord(c->arenaEv, c->stream));
@@ -1778,9 +1797,9 @@ void relocEnqueue(Ctx* c, int s, double threshold1, double threshold2, int max_d
     p.maxSteps = max_descent_steps;
     p.gradStep = gradient_step;
     p.report = rep;
-    p.stats = c->scratch.p;
+    p.stats = c->scr;
     CK(cudaMemsetAsync(rep, 0, 4 * sizeof(int), c->stream));
-    if (clearCounters) CK(cudaMemsetAsync(c->scratch.p, 0, (kShadowStats + 32) * 8, c->stream));
+    if (clearCounters) CK(cudaMemsetAsync(c->scr, 0, (kShadowStats + 32) * 8, c->stream));
     // relocation is replicated on every rank (deterministic, bit-exact): no exchange
     CK(cudaEventRecord(c->ev[2], c->stream));
     launch_relocate(p, c->cascades[s].count(), stats, c->stream);
@@ -1814,8 +1833,10 @@ int sdfgi_probes_relocate(void* ctx, int level, double threshold1, double thresh
 
 // The update half of the probe stage (pipeline.hpp:126-151); ends with the one
 // host synchronisation of the call (readCounters).
-void updateBody(Ctx* c, const int32_t* probe_refs, int n_refs, int frame, const sdfgi_cfg* cfg,
-                sdfgi_update_result* result, sdfgi_stats* stats) {
+// noSync (sdfgi_probe_stage_async): the pass's tail counters are copied to the
+// slot's pinned words instead, read by sdfgi_probe_stage_collect.
+bool updateBody(Ctx* c, const int32_t* probe_refs, int n_refs, int frame, const sdfgi_cfg* cfg,
+                sdfgi_update_result* result, sdfgi_stats* stats, unsigned long long* noSync = nullptr) {
     requireProbes(c);
     validateCfg(c, cfg);
     std::vector<int> refs = selectRefs(c, probe_refs, n_refs);
@@ -1823,7 +1844,7 @@ void updateBody(Ctx* c, const int32_t* probe_refs, int n_refs, int frame, const 
     const float* frontp = c->atlas[c->front].p;
     // atlas_[write] = atlas_[read] (pipeline.hpp:131); updated tiles are overwritten
     CK(cudaMemcpyAsync(back, frontp, c->atlasFloats() * 4, cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaMemsetAsync(c->scratch.p, 0, (kShadowStats + 32) * 8, c->stream));
+    CK(cudaMemsetAsync(c->scr, 0, (kShadowStats + 32) * 8, c->stream));
     const bool all = (probe_refs == nullptr && c->world == 1);
     // back <- front (copied above) + the updated tiles: still all-zero only if no
     // probe anywhere is updated this pass
@@ -1837,11 +1858,11 @@ void updateBody(Ctx* c, const int32_t* probe_refs, int n_refs, int frame, const 
         uploadQuats(c, cfg, frame, all ? nullptr : refs.data(), nCand);
         if (c->precision == SDFGI_F64) {
             WaveParams<double> p = waveParams<double>(c, cfg, frame, cand, nCand);
-            launch_wavefront<double>(p, c->persistCap, stats != nullptr, c->stream, c->kev,
+            launch_wavefront<double>(p, c->persistCap, stats != nullptr, c->stream, c->kevCur,
                                      &c->launches);
         } else {
             WaveParams<float> p = waveParams<float>(c, cfg, frame, cand, nCand);
-            launch_wavefront<float>(p, c->persistCap, stats != nullptr, c->stream, c->kev,
+            launch_wavefront<float>(p, c->persistCap, stats != nullptr, c->stream, c->kevCur,
                                     &c->launches);
         }
         CK(cudaGetLastError());
@@ -1863,11 +1884,11 @@ void updateBody(Ctx* c, const int32_t* probe_refs, int n_refs, int frame, const 
                                  c->stream));
             }
         NK(ncclGroupEnd());
-        NK(ncclAllReduce(c->scratch.p, c->scratch.p, 14, ncclUint64, ncclSum, c->comm, c->stream));
-        NK(ncclAllReduce(c->scratch.p + kShadowStats, c->scratch.p + kShadowStats, 14, ncclUint64, ncclSum,
+        NK(ncclAllReduce(c->scr, c->scr, 14, ncclUint64, ncclSum, c->comm, c->stream));
+        NK(ncclAllReduce(c->scr + kShadowStats, c->scr + kShadowStats, 14, ncclUint64, ncclSum,
                          c->comm, c->stream));
-        NK(ncclAllReduce(c->scratch.p + 16, c->scratch.p + 16, 1, ncclUint64, ncclMax, c->comm, c->stream));
-        NK(ncclAllReduce(c->scratch.p + 17, c->scratch.p + 17, 2, ncclUint64, ncclSum, c->comm, c->stream));
+        NK(ncclAllReduce(c->scr + 16, c->scr + 16, 1, ncclUint64, ncclMax, c->comm, c->stream));
+        NK(ncclAllReduce(c->scr + 17, c->scr + 17, 2, ncclUint64, ncclSum, c->comm, c->stream));
     }
     if (c->world > 1) {
         // every rank marks every updated probe (probe_update.hpp:208-209) on the
@@ -1884,6 +1905,10 @@ void updateBody(Ctx* c, const int32_t* probe_refs, int n_refs, int frame, const 
         }
         launch_mark_updated(ids, nAll, frame, c->alive.p, c->reject.p, c->lastFrame.p, c->stream);
         checkLaunch(c);
+    }
+    if (noSync) {
+        CK(cudaMemcpyAsync(noSync, c->scr + 16, 3 * 8, cudaMemcpyDeviceToHost, c->stream));
+        return nCand > 0;
     }
     unsigned long long tail[3];
     readCounters(c, stats, tail, 3);
@@ -1904,6 +1929,7 @@ void updateBody(Ctx* c, const int32_t* probe_refs, int n_refs, int frame, const 
         result->rays_traced = static_cast<int64_t>(tail[1]);
         result->probes_updated = static_cast<int64_t>(tail[2] & 0xffffffffull);
     }
+    return nCand > 0;
 }
 
 int sdfgi_probes_update(void* ctx, const int32_t* probe_refs, int n_refs, int frame, const sdfgi_cfg* cfg,
@@ -1967,6 +1993,108 @@ int sdfgi_probe_stage(void* ctx, int frame, const sdfgi_cfg* cfg, const double c
             stats->shadow_traces += relocStats.shadow_traces;
             stats->visibility_traces += relocStats.visibility_traces;
         }
+    });
+}
+
+constexpr int kAsyncHostWords = 3 + 2 * kMaxCascades;  // tail counters + 4 int32 per cascade report
+
+int sdfgi_probe_stage_async(void* ctx, int frame, const sdfgi_cfg* cfg, const double cam_pos[3],
+                            const double cam_fwd[3]) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        requireProbes(c);
+        validateCfg(c, cfg);
+        REQ(c->nPending < Ctx::kMaxPending, SDFGI_ERR_STATE, "too many passes in flight: collect them first");
+        if (!c->hAsync) {
+            CK(cudaMallocHost(&c->hAsync, Ctx::kMaxPending * kAsyncHostWords * sizeof(unsigned long long)));
+            c->scratchAsync.alloc(static_cast<size_t>(Ctx::kMaxPending) * Ctx::kSlotWords);
+            for (auto& row : c->kevAsync)
+                for (auto& e : row) CK(cudaEventCreate(&e));
+        }
+        const int k = c->nPending;
+        const int nc = static_cast<int>(c->cascades.size());
+        // report region 0 belongs to the synchronous calls
+        int* rep = c->report.p + 4 * kMaxCascades * (k + 1);
+        unsigned long long* host = c->hAsync + k * kAsyncHostWords;
+        struct Restore {
+            Ctx* c;
+            ~Restore() {
+                c->scr = c->scratch.p;
+                c->kevCur = c->kev;
+            }
+        } restore{c};
+        c->scr = c->scratchAsync.p + static_cast<size_t>(k) * Ctx::kSlotWords;
+        c->kevCur = c->kevAsync[k];
+        CK(cudaMemsetAsync(c->scr, 0, Ctx::kSlotWords * 8, c->stream));
+        for (int s = 0; s < nc; ++s) {
+            const double sp = c->cascades[s].spacing;
+            relocEnqueue(c, s, cfg->threshold1_frac * sp, cfg->threshold2_frac * sp,
+                         static_cast<int>(cfg->max_descent_steps), cfg->gradient_step, false, rep + 4 * s, false);
+        }
+        std::vector<int32_t> refs;
+        const int32_t* pr = nullptr;
+        int nr = 0;
+        static const int32_t kNoRefs[2] = {0, 0};
+        if (cfg->probe_budget > 0) {  // the selection reads the relocated probes back: synchronous
+            REQ(cam_pos && cam_fwd, SDFGI_ERR_INVALID, "a probe budget needs the camera");
+            refs.resize(2 * static_cast<size_t>(std::min<int64_t>(cfg->probe_budget, c->totalProbes)));
+            int rc = sdfgi_select_probes(ctx, cam_pos, cam_fwd, static_cast<int>(cfg->probe_budget), frame,
+                                         refs.data(), &nr);
+            REQ(rc == SDFGI_OK, rc, "probe selection failed");
+            pr = nr > 0 ? refs.data() : kNoRefs;
+        } else if (c->totalProbes > 0) {
+            const std::vector<int> cand = selectRefs(c, nullptr, 0);
+            if (!cand.empty())
+                prepareQuats(c, cfg, frame, c->world == 1 ? nullptr : cand.data(), static_cast<int>(cand.size()));
+        }
+        CK(cudaMemcpyAsync(host + 3, rep, 4 * nc * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        c->pendingTimed[k] = updateBody(c, pr, nr, frame, cfg, nullptr, nullptr, host);
+        c->pendingCascades[k] = nc;
+        ++c->nPending;
+    });
+}
+
+int sdfgi_probe_stage_collect(void* ctx, sdfgi_reloc_report* reports, int reports_per_pass,
+                              sdfgi_update_result* results, int max_passes, int* n_passes) {
+    return guard([&] {
+        Ctx* c = C(ctx);
+        REQ(n_passes, SDFGI_ERR_INVALID, "null n_passes");
+        CK(cudaStreamSynchronize(c->stream));
+        const int np = c->nPending;
+        REQ(results == nullptr || max_passes >= np, SDFGI_ERR_INVALID, "results: one per pass in flight");
+        REQ(reports == nullptr || max_passes >= np, SDFGI_ERR_INVALID, "reports: one row per pass in flight");
+        for (int k = 0; k < np; ++k) {
+            const unsigned long long* host = c->hAsync + k * kAsyncHostWords;
+            if (results) {
+                double md;
+                std::memcpy(&md, &host[0], 8);
+                results[k].max_texel_delta = md;
+                results[k].rays_traced = static_cast<int64_t>(host[1]);
+                results[k].probes_updated = static_cast<int64_t>(host[2] & 0xffffffffull);
+            }
+            if (reports) {
+                const int* r = reinterpret_cast<const int*>(host + 3);
+                for (int s = 0; s < reports_per_pass; ++s) {
+                    if (s < c->pendingCascades[k])
+                        fillReport(&reports[static_cast<size_t>(k) * reports_per_pass + s], r + 4 * s);
+                    else
+                        std::memset(&reports[static_cast<size_t>(k) * reports_per_pass + s], 0, sizeof(sdfgi_reloc_report));
+                }
+            }
+            if (c->pendingTimed[k]) {
+                const cudaEvent_t* e = c->kevAsync[k];
+                for (int i = 0; i + 1 < kWaveEvents; ++i) {
+                    float ms = 0.f;
+                    CK(cudaEventElapsedTime(&ms, e[i], e[i + 1]));
+                    c->stageSum[i] += ms;
+                }
+                float tot = 0.f;
+                CK(cudaEventElapsedTime(&tot, e[0], e[kWaveEvents - 1]));
+                c->stageSum[kWaveEvents - 1] += tot;
+            }
+        }
+        c->nPending = 0;
+        *n_passes = np;
     });
 }
 

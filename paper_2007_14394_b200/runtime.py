@@ -48,6 +48,8 @@ _SIGS = {
     "sdfgi_probes_update": [_P, _P, _I, _I, _P, _P, _P],
     "sdfgi_probe_stage": [_P, _I, _P, _P, _P, _P, _I, _P, _P],
     "sdfgi_stage_ms_sum": [_P, _P, _I],
+    "sdfgi_probe_stage_async": [_P, _I, _P, _P, _P],
+    "sdfgi_probe_stage_collect": [_P, _P, _I, _P, _I, _P],
     "sdfgi_atlas_swap": [_P],
     "sdfgi_atlas_download": [_P, _I, _I, _P, _SZ],
     "sdfgi_atlas_upload": [_P, _I, _I, _P, _SZ],
@@ -425,6 +427,22 @@ class Device:
         _call("sdfgi_probe_stage", self._ctx, int(frame), _ptr(cfg), _ptr(cp), _ptr(cf), _ptr(reps), len(reps),
               _ptr(res), _ptr(st))
         return (reps, res[0], st[0]) if stats else (reps, res[0])
+
+    def probe_stage_async(self, frame, cfg, cam_pos=None, cam_fwd=None):
+        """Queue one probe stage pass (sdfgi_probe_stage_async) and return at once."""
+        cfg = np.ascontiguousarray(cfg, sio.CFG_DTYPE)
+        cp = None if cam_pos is None else np.ascontiguousarray(cam_pos, np.float64)
+        cf = None if cam_fwd is None else np.ascontiguousarray(cam_fwd, np.float64)
+        _call("sdfgi_probe_stage_async", self._ctx, int(frame), _ptr(cfg), _ptr(cp), _ptr(cf))
+
+    def probe_stage_collect(self, max_passes=8):
+        """Wait for the queued passes -> (reports [passes, cascades], results [passes])."""
+        nc = max(len(self.levels), 1)
+        reps = np.zeros((max_passes, nc), RELOC_DTYPE)
+        res = np.zeros(max_passes, RESULT_DTYPE)
+        n = ctypes.c_int()
+        _call("sdfgi_probe_stage_collect", self._ctx, _ptr(reps), nc, _ptr(res), max_passes, ctypes.byref(n))
+        return reps[:n.value], res[:n.value]
 
     def select(self, cam_pos, cam_fwd, budget, frame):
         """selectProbesForUpdate on the device -> (n, 2) int32 (level, index)."""

@@ -17,6 +17,7 @@ if os.environ.get("SDFGI_LIB"):  # an older variant may lack newer entry points
     _probe = ctypes.CDLL(os.environ["SDFGI_LIB"])
     runtime._SIGS = {k: v for k, v in runtime._SIGS.items() if hasattr(_probe, k)}
 fused = os.environ.get("FUSED") == "1"  # one sdfgi_probe_stage call per pass
+queued = os.environ.get("ASYNC") == "1"  # sdfgi_probe_stage_async per pass, one collect per step
 
 prec = sys.argv[1] if len(sys.argv) > 1 else "f64"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
@@ -35,13 +36,17 @@ with Device(0, precision=prec) as dev:
         e0.record(ext)
         pp = []
         for p in range(3):
-            if fused:
+            if queued:
+                dev.probe_stage_async(p, stage.cfg)
+            elif fused:
                 dev.probe_stage(p, stage.cfg)
             else:
                 stage.relocate_all()
                 api.updateProbes(dev, stage.cfg, p)
-            pp.append(dev.last_kernel_ms()[0])
+            pp.append(0.0 if queued else dev.last_kernel_ms()[0])
             dev.swap()
+        if queued:
+            dev.probe_stage_collect()
         e1.record(ext)
         e1.synchronize()
         if r >= 2:
@@ -49,5 +54,5 @@ with Device(0, precision=prec) as dev:
             per_pass.append(pp)
     pp = np.median(np.array(per_pass), axis=0)
     lib = os.environ.get("SDFGI_LIB", "cur").split("/")[-2] if os.environ.get("SDFGI_LIB") else "cur"
-    lib += "+fused" if fused else ""
+    lib += "+async" if queued else ("+fused" if fused else "")
     print(f"{lib:12s} {prec} step {np.median(steps):7.2f} ms  passes " + " ".join(f"{x:6.2f}" for x in pp))

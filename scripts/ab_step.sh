@@ -5,4 +5,5 @@ for v in ${VARIANTS:-} cur; do
   if [ $v = cur ]; then unset SDFGI_LIB; else export SDFGI_LIB=paper_2007_14394_b200/_variants/$v/libsdfgi_b200.so; fi
   python scripts/ab_step.py ${PREC:-f64} 5
   if [ $v = cur ] && [ -n "$FUSED_TOO" ]; then FUSED=1 python scripts/ab_step.py ${PREC:-f64} 5; fi
+  if [ $v = cur ] && [ -n "$ASYNC_TOO" ]; then ASYNC=1 python scripts/ab_step.py ${PREC:-f64} 5; fi
 done; done

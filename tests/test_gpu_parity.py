@@ -226,3 +226,40 @@ def test_probe_stage_call_matches_call_sequence(name):
         for (pa, aa), (pb, ab) in zip(a[3], b[3]):
             check_probes(pb, pa, f"{name} pass {p}")
             assert np.array_equal(aa, ab), (name, p)
+
+
+def test_probe_stage_async_matches_sync():
+    """Three passes queued with sdfgi_probe_stage_async (swap between them) and
+    collected once == the same passes with the synchronous call: identical
+    reports, results, probe states and bit-identical atlases; the collected stage
+    times are positive."""
+    case = load(CASES[0])
+    outs = []
+    for mode in ("sync", "async"):
+        d = Device(0, precision="f64")
+        try:
+            stage = api.ProbeStage(d, case.scene, cfg=case.cfg(), res=case.res, spacing=case.spacing)
+            d.stage_ms_sum(reset=True)
+            reps, results = [], []
+            for p in range(3):
+                if mode == "sync":
+                    r, res = d.probe_stage(p, stage.cfg)
+                    reps.append(r)
+                    results.append(res)
+                else:
+                    d.probe_stage_async(p, stage.cfg)
+                d.swap()
+            if mode == "async":
+                reps, results = d.probe_stage_collect()
+            stages, total = d.stage_ms_sum(reset=True)
+            assert total > 0 and all(v >= 0 for v in stages.values())
+            outs.append((np.asarray(reps), np.asarray(results),
+                         [(d.probes(lv), d.atlas(lv, 0)) for lv in range(stage.levels)]))
+        finally:
+            d.close()
+    (ra, sa, la), (rb, sb, lb) = outs
+    assert np.array_equal(ra.view(np.int32), rb.view(np.int32))
+    assert np.array_equal(sa, sb)
+    for (pa, aa), (pb, ab) in zip(la, lb):
+        check_probes(pb, pa, "async")
+        assert np.array_equal(aa, ab)
