@@ -1,8 +1,8 @@
 #!/bin/bash
 # One gpurun call: ncu launch lists of a full C2 step + G-buffer + gather
 # (scripts/profile_step.py) and a `--set full` capture of the update kernels of C2
-# pass 1 (N rays per probe, bounce lookups on: scripts/profile_pass.py, the 8
-# launches after pass 0's 8), summarised on the box into gpurun_out/ncu_step_<prec>.json
+# pass 1 (N rays per probe, bounce lookups on: scripts/profile_pass.py, the 9
+# launches after pass 0's 9), summarised on the box into gpurun_out/ncu_step_<prec>.json
 # (the .ncu-rep files are too big to bring back).
 # usage: bash scripts/gpu_profile_round.sh [f64 f32]
 mkdir -p gpurun_out
@@ -11,7 +11,7 @@ for prec in ${@:-f64 f32}; do
       --clock-control none --csv --log-file gpurun_out/step_launches_$prec.csv \
       python scripts/profile_step.py $prec > gpurun_out/ncu_launch_$prec.log 2>&1
   ncu --set full --clock-control none --import-source on -k regex:'k_trace|k_shade|k_convolve|k_hit' \
-      --launch-skip 8 --launch-count 8 -f -o /tmp/full_$prec python scripts/profile_pass.py $prec 2 \
+      --launch-skip 9 --launch-count 9 -f -o /tmp/full_$prec python scripts/profile_pass.py $prec 2 \
       > gpurun_out/ncu_full_$prec.log 2>&1
   python scripts/summarize_ncu.py gpurun_out/step_launches_$prec.csv /tmp/full_$prec.ncu-rep \
       gpurun_out/ncu_step_$prec.json > gpurun_out/summ_$prec.log 2>&1
