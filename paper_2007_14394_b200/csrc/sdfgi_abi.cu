@@ -2409,6 +2409,7 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     // off here (measured: contact +2.5% / +3% each, scripts/time_gather.py)
     p.escape = 0;
     p.scene.stageBytes = 0;
+    p.ownerFromMarch = c->accel == 2 && c->haveGrid ? 1 : 0;  // exact (see waveParams)
     p.nRaysDirect = nr;
     p.cray = c->wCRay.p;
     p.conv = c->wConv.p;
