@@ -688,7 +688,9 @@ void buildBvh(Ctx* c, double scaleHint) {
     }
 }
 
-void buildGrid(Ctx* c) {
+// One build attempt at cellScale x the default cell count; false when the lists
+// would overflow their 2^30-entry index (the caller retries coarser).
+bool buildGridAt(Ctx* c, double cellScale) {
     const sdfgi_prim* prims = c->hPrims.data();
     const int32_t* member_idx = c->hMember.data();
     const sdfgi_cluster* clusters = c->hClusters.data();
@@ -705,7 +707,7 @@ void buildGrid(Ctx* c) {
             hi[a] = std::max(hi[a], clusters[k].hi[a]);
         }
     }
-    if (bounded == 0 || n < 2) return;
+    if (bounded == 0 || n < 2) return true;
     double ext[3], scale = 0;
     // the grid extends past the geometry so rays leaving the scene stay on the
     // (cheap) candidate lists for their first steps; SDFGI_GRID_MARGIN overrides.
@@ -740,13 +742,16 @@ void buildGrid(Ctx* c) {
     // 2M cells 17.4 ms, 4M 16.6, 8M 15.9, 16M 15.5, 24M 15.3 (margin 0.6, round-1
     // kernels); with the SDF-bound lists and the min-extent margin 33M -> 50M -> 66M
     // cells: C2 13.9 / 12.3 / 12.9 ms, C4 0.28 / 0.37 / 0.34 Grays/s
-    // Small scenes need far fewer cells (and an animated scene rebuilds its grid
-    // every frame): 33k cells per primitive, between 2M and 66M. With the round-1
-    // final kernels 50M -> 66M: C2 pass 0 FP64 9.50 -> 9.36 ms, FP32 5.09 -> 5.05;
-    // C4 FP64 0.548 -> 0.565 Grays/s, FP32 1.09 -> 1.12 (80M: candidate grid too large)
-    const double byPrims = std::min(66000000.0, std::max(2097152.0, 33000.0 * c->nPrims));
-    double target = env ? std::atof(env) : byPrims;
-    if (target < 1) return;
+    // Small scenes need far fewer cells: 120k cells per primitive, between 2M and
+    // 240M (~12 GB of grid for C2, out of the 180 GB of HBM). With the round-1
+    // final kernels 50M -> 66M: C2 pass 0 FP64 9.50 -> 9.36 ms; with the round-2
+    // kernels (profiles/r02_sweep_grid_cells.log) C2 step 66M / 100M / 132M / 180M
+    // / 240M = 27.58 / 27.11 / 26.73 / 26.49 / 26.34 ms FP64, C4 pass 1 199.9 /
+    // 189.7 (132M) / 183.2 ms (240M). A grid build at 240M takes ~0.1 s (once per
+    // static scene; an animated scene refits, see sdfgi_scene_upload).
+    const double byPrims = std::min(240000000.0, std::max(2097152.0, 120000.0 * c->nPrims));
+    double target = (env ? std::atof(env) : byPrims) * cellScale;
+    if (target < 1) return true;
     double h = std::cbrt(ext[0] * ext[1] * ext[2] / target);
     int dim[3];
     for (int a = 0; a < 3; ++a) {
@@ -761,9 +766,9 @@ void buildGrid(Ctx* c) {
             dim[a] = std::max(1, static_cast<int>(std::ceil(ext[a] / h)));
             ncells *= dim[a];
         }
-        if (ncells < (1LL << 26)) break;
+        if (ncells < (1LL << 28)) break;
         REQ(tries < 64, SDFGI_ERR_INVALID, "candidate grid too large");
-        h *= std::cbrt(static_cast<double>(ncells) / static_cast<double>(1LL << 26)) * 1.001;
+        h *= std::cbrt(static_cast<double>(ncells) / static_cast<double>(1LL << 28)) * 1.001;
     }
     buildBvh(c, scale);
     GridBuildParams p;
@@ -833,7 +838,7 @@ void buildGrid(Ctx* c) {
     };
     {
         const long long bt = deviceScan(c->brickCounts.p, c->brickStart.p, nbricks + 1);
-        REQ(bt >= 0 && bt < (1LL << 30), SDFGI_ERR_INVALID, "brick cluster lists too large");
+        if (!(bt >= 0 && bt < (1LL << 30))) return false;  // brick cluster lists too large
         c->brickList.alloc(std::max<long long>(bt, 1));
     }
     p.bStart = c->brickStart.p;
@@ -843,7 +848,7 @@ void buildGrid(Ctx* c) {
     launch_grid_list(p, static_cast<int>(ncells), false, c->stream);
     checkLaunch(c);
     const long long total = deviceScan(c->gridCounts.p, c->gridStart.p, ncells + 1);
-    REQ(total >= 0 && total < (1LL << 30), SDFGI_ERR_INVALID, "candidate lists too large");
+    if (!(total >= 0 && total < (1LL << 30))) return false;  // candidate lists too large
     c->gridEntry.alloc(std::max<long long>(total, 1));
     p.entry = c->gridEntry.p;
     p.start = c->gridStart.p;
@@ -870,7 +875,17 @@ void buildGrid(Ctx* c) {
     c->gridEntries = total;
 
     c->haveGrid = true;
+    return true;
 }
+
+// The candidate grid at the default size, coarser while its lists overflow.
+void buildGrid(Ctx* c) {
+    for (double f = 1.0;; f *= 0.5) {
+        if (buildGridAt(c, f)) return;
+        REQ(f > 1.0 / 64, SDFGI_ERR_INVALID, "candidate lists too large");
+    }
+}
+
 
 void readCounters(Ctx* c, sdfgi_stats* stats, unsigned long long* tail, int ntail) {
     // [0..13] K1 (and relocation) counters, [16..] tail values, [kShadowStats..+13] K2's
