@@ -193,6 +193,7 @@ struct Ctx {
     // with the same boxes keeps it)
     std::vector<sdfgi_cluster> bvhClusters;
     double bvhScale = -1;
+    double gridMargin = -1;  // the margin multiple the grid was built with
     std::vector<int32_t> hMember, hStart;
     std::vector<sdfgi_cluster> hClusters;
     std::vector<sdfgi_light> hLights;
@@ -688,6 +689,14 @@ void buildBvh(Ctx* c, double scaleHint) {
     }
 }
 
+double gridMargin(const Ctx* c, int precision) {
+    const char* menv = std::getenv("SDFGI_GRID_MARGIN");
+    if (menv) return std::atof(menv);
+    bool unbounded = false;
+    for (const auto& k : c->hClusters) unbounded = unbounded || k.unbounded;
+    return !unbounded && precision == SDFGI_F64 ? 0.5 : 3.5;
+}
+
 // One build attempt at cellScale x the default cell count; false when the lists
 // would overflow their 2^30-entry index (the caller retries coarser).
 bool buildGridAt(Ctx* c, double cellScale) {
@@ -719,8 +728,15 @@ bool buildGridAt(Ctx* c, double cellScale) {
     // Sweep (profiles/README.md, 50M cells): C2 pass 0 FP64 margin 0.6 per-axis
     // 13.1 ms, 2.5 x min 12.0, 4 x min 12.3; C4 pass 1 0.235 -> 0.326 -> 0.374 Grays/s.
     // SDFGI_GRID_MARGIN sets the multiple, SDFGI_GRID_MARGIN_MIN=0 the per-axis extent.
-    const char* menv = std::getenv("SDFGI_GRID_MARGIN");
-    const double marginFrac = menv ? std::atof(menv) : 3.5;
+    // With escape (accel mode 2, every cluster bounded) a march ends as soon as it
+    // leaves the grid box, so cells beyond the geometry only delay that: FP64 takes
+    // a 0.5x margin (C2 step 26.3 -> 25.1 ms at 240M cells; the same cells then sit
+    // closer to the geometry). FP32 (per-lane cell cache) and scenes with unbounded
+    // primitives (C4's ground plane: no escape, its marches stay on the grid) keep
+    // 3.5x (FP32 C2 16.1 vs 16.8 ms; C4 pass 1 183 vs 217 ms at 2.5x).
+    // profiles/r02_sweep_grid_cells.log
+    const double marginFrac = gridMargin(c, c->precision);
+    c->gridMargin = marginFrac;
     const char* mmode = std::getenv("SDFGI_GRID_MARGIN_MIN");
     const bool fromMin = !mmode || std::atoi(mmode) != 0;
     const double minExt = std::min(hi[0] - lo[0], std::min(hi[1] - lo[1], hi[2] - lo[2]));
@@ -1213,6 +1229,8 @@ std::vector<int> selectRefs(Ctx* c, const int32_t* refs, int nRefs) {
     return out;
 }
 
+void rebuildGrid(Ctx* c);  // below (the grid's margin follows the precision)
+
 }  // namespace
 
 extern "C" {
@@ -1302,6 +1320,8 @@ int sdfgi_ctx_set_precision(void* ctx, int precision) {
         Ctx* c = C(ctx);
         REQ(precision == SDFGI_F64 || precision == SDFGI_F32, SDFGI_ERR_INVALID, "bad precision");
         c->precision = precision;
+        // the grid's margin depends on the precision (buildGridAt): rebuild when it changes
+        if (c->haveScene && c->haveGrid && gridMargin(c, precision) != c->gridMargin) rebuildGrid(c);
     });
 }
 
