@@ -263,3 +263,29 @@ def test_probe_stage_async_matches_sync():
     for (pa, aa), (pb, ab) in zip(la, lb):
         check_probes(pb, pa, "async")
         assert np.array_equal(aa, ab)
+
+
+@pytest.mark.parametrize("name", ["openfield", "kinds"])
+def test_accel2_with_planes_is_exact(name):
+    """Accel mode 2 (owner from the march, first query from the relocation, ...) on
+    scenes with an unbounded ground plane (no escape there): the probe states and
+    atlases equal accel mode 1's bit for bit, and the reference's texels within the
+    north-star bar."""
+    case = load(name)
+    outs = []
+    for accel in (1, 2):
+        d = Device(0, precision="f64")
+        try:
+            d.set_accel(accel)
+            stage = api.ProbeStage(d, case.scene, cfg=case.cfg(), res=case.res, spacing=case.spacing)
+            for p in range(len(case.passes)):
+                stage.run_pass(p)
+            outs.append([(d.probes(lv), d.atlas(lv, 0)) for lv in range(stage.levels)])
+        finally:
+            d.close()
+    for lv, ((pa, aa), (pb, ab)) in enumerate(zip(*outs)):
+        check_probes(pb, pa, f"{name} c{lv}")
+        assert np.array_equal(aa, ab), (name, lv)
+        p_last = len(case.passes) - 1
+        err = texel_rel_err(ab, case.data[f"atlas_p{p_last}_c{lv}"])
+        assert err.max() <= TEXEL_RTOL, (name, lv, err.max())
