@@ -482,14 +482,14 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
     bool active = false, exhausted = false;
     WarpChunk chunk;
     CellCache ccache;  // FP32 only (FP64: 1.5% slower at 64 registers, 2% at 72; SDFGI_CELL_CACHE64)
-    unsigned long long rid = 0;
+    int rid = 0;  // ray id (< 2^31)
     V3<R> o = mk(R(0), R(0), R(0)), dir = o;
-    R t = 0, lastD = 0, d = 0, tMax = 0;
+    R t = 0, lastD = 0, d = 0, tMax = 0;  // tMax: contact rays only (probe rays: P.tc.rayTMax)
+    auto tmax = [&]() { return MODE == 0 ? R(P.tc.rayTMax) : tMax; };
     int step = 0, state = 0, pol = 0, owner = -1, seed = -1;
     int titem = 0;       // the ray's trace-order position (its hitAt slot)
     bool fresh = false;  // resumed march: its pending t += d was applied before parking
     bool originIn = false;  // the ray starts inside the candidate grid (escape test)
-    R pclear = R(-1);       // the probe's SDF for the march's first query (< 0: query it)
     while (true) {
         __syncwarp();
         unsigned long long item;
@@ -501,14 +501,14 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
                 t = r.t;
                 lastD = r.lastD;
                 d = r.d;
-                tMax = r.tMax;
+                if (MODE == 1) tMax = r.tMax;  // probe rays: P.tc.rayTMax (tmax() below)
                 step = r.step;
                 state = r.state;
                 pol = r.pol;
                 owner = r.owner;
                 seed = r.seed;
                 titem = r.item;
-                rid = r.rid;
+                rid = static_cast<int>(r.rid);
                 active = true;
                 fresh = true;
             }
@@ -524,14 +524,15 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
                 // prepared by k_probe_ray_setup (trace order: consecutive lanes get
                 // neighbouring directions; results are stored by ray id)
                 const ProbeRay<R> r = ldStream(reinterpret_cast<const ProbeRay<R>*>(P.pray) + item);
-                rid = static_cast<unsigned long long>(r.rid);
-                pclear = r.clear;
+                rid = r.rid;
+                // the probe's SDF for the march's first query (< 0: query it), carried
+                // in d until state 1 sets it (one register fewer than a variable of its own)
+                d = r.clear;
                 o = mk(r.o[0], r.o[1], r.o[2]);
                 dir = mk(r.dir[0], r.dir[1], r.dir[2]);
-                tMax = R(P.tc.rayTMax);
             } else {
-                rid = item;
-                pclear = R(-1);
+                rid = static_cast<int>(item);
+                d = R(-1);
                 const ContactRay<R> r = ldStream(reinterpret_cast<const ContactRay<R>*>(P.cray) + item);
                 o = mk(r.o[0], r.o[1], r.o[2]);
                 dir = mk(r.dir[0], r.dir[1], r.dir[2]);
@@ -569,9 +570,9 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
                 h.status = 2 << 1;
                 P.hits[rid] = h;
                 P.hitAt[titem] = -1;
-                P.rad[3 * rid] = R(P.scene.sky[0]);
-                P.rad[3 * rid + 1] = R(P.scene.sky[1]);
-                P.rad[3 * rid + 2] = R(P.scene.sky[2]);
+                P.rad[3 * static_cast<size_t>(rid)] = R(P.scene.sky[0]);
+                P.rad[3 * static_cast<size_t>(rid) + 1] = R(P.scene.sky[1]);
+                P.rad[3 * static_cast<size_t>(rid) + 2] = R(P.scene.sky[2]);
                 active = false;
             }
             }
@@ -591,7 +592,7 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
             p = o + dir * t;
             if (PHASE == 0 && P.scene.useGrid) cell = gridCell<R>(P.scene.grid, p, &cellR);
             // the first query of a probe ray is the probe's own SDF, known from the relocation
-            known = PHASE == 0 && state == 0 && step == 0 && pclear >= R(0);
+            known = PHASE == 0 && state == 0 && step == 0 && d >= R(0);
             escaped = PHASE == 0 && originIn && state == 0 && cell < 0 && !known;
             parkIt = PHASE == 0 && park && cell < 0 && !escaped && !known;
             if (escaped) {
@@ -599,7 +600,7 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
             } else if (parkIt) {
             } else if (state == 0) {
                 if (ST) ++cnt.steps;
-                initD = marchSeed(P.scene, lastD, tMax - t, eps);
+                initD = marchSeed(P.scene, lastD, tmax() - t, eps);
             } else if (state == 1) {
                 initD = polishPad(d);
             } else {
@@ -612,7 +613,7 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
                 parkIt = false;
                 if (state == 0) {
                     if (ST) ++cnt.steps;
-                    initD = marchSeed(P.scene, lastD, tMax - t, eps);
+                    initD = marchSeed(P.scene, lastD, tmax() - t, eps);
                 } else if (state == 1) {
                     initD = polishPad(d);
                 } else {
@@ -630,7 +631,7 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
                 r.t = t;
                 r.lastD = lastD;
                 r.d = d;
-                r.tMax = tMax;
+                r.tMax = tmax();
                 r.step = step;
                 r.state = state;
                 r.pol = pol;
@@ -645,7 +646,7 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
         int o2 = -1;
         R nd = R(0);
         if (active && known)
-            nd = smin(pclear, initD);  // exactly query(o, initD) = min(SDF(o), initD)
+            nd = smin(d, initD);  // exactly query(o, initD) = min(SDF(o), initD)
         else if (active && !escaped)
             nd = query<R, ST, STG>(P.scene, p, initD, &o2, &cnt, PHASE ? seed : -1, cell, cellR,
                               useCellCache<R>() ? &ccache : nullptr);
@@ -665,7 +666,7 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
                     } else {
                         state = 1;
                     }
-                } else if (nd >= tMax - t) {
+                } else if (nd >= tmax() - t) {
                     done = 2;
                 } else {
                     t += nd;
@@ -710,15 +711,15 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
                 if (MODE == 1 && done == 1 && P.conv) P.conv[rid] = 1;
                 if ((!lean || (MODE == 1 && done == 1)) &&
                     !(done == 1 && owner >= 0)) {  // shadeHit's miss branch: K3a shades only the hit list
-                    __stcs(&P.rad[3 * rid], R(P.scene.sky[0]));
-                    __stcs(&P.rad[3 * rid + 1], R(P.scene.sky[1]));
-                    __stcs(&P.rad[3 * rid + 2], R(P.scene.sky[2]));
+                    __stcs(&P.rad[3 * static_cast<size_t>(rid)], R(P.scene.sky[0]));
+                    __stcs(&P.rad[3 * static_cast<size_t>(rid) + 1], R(P.scene.sky[1]));
+                    __stcs(&P.rad[3 * static_cast<size_t>(rid) + 2], R(P.scene.sky[2]));
                 }
                 active = false;
             }
             // converged hits with an owner (the only ones shadeHit lights) are
             // compacted after the kernel, in trace order (coherent K2/K3a warps)
-            if (done) P.hitAt[titem] = (done == 1 && owner >= 0) ? static_cast<int>(rid) : -1;
+            if (done) P.hitAt[titem] = (done == 1 && owner >= 0) ? rid : -1;
         }
     }
     if (ST) flushCounters(cnt, P.stats);
