@@ -289,3 +289,52 @@ def test_accel2_with_planes_is_exact(name):
         p_last = len(case.passes) - 1
         err = texel_rel_err(ab, case.data[f"atlas_p{p_last}_c{lv}"])
         assert err.max() <= TEXEL_RTOL, (name, lv, err.max())
+
+
+@pytest.mark.parametrize("name", SCHED_CASES[:1])
+def test_probe_stage_async_budgeted_matches_reference(name):
+    """Budgeted passes (cfg.probe_budget > 0) queued with sdfgi_probe_stage_async:
+    each selects from the camera after its relocation (the one synchronous step),
+    and the collected results, probe states and texels are the reference's."""
+    case = load(name)
+    d = Device(0, precision="f64")
+    try:
+        stage = api.ProbeStage(d, case.scene, cfg=case.cfg(), res=case.res, spacing=case.spacing)
+        stage.cfg["probe_budget"] = case.budget  # the reference run's selectProbesForUpdate budget
+        assert int(stage.cfg["probe_budget"][0]) > 0
+        cam = case.scene.camera
+        for p in range(len(case.passes)):
+            d.probe_stage_async(p, stage.cfg, cam.position, cam.forward)
+            d.swap()
+            # collected pass by pass: the probes of pass p are checked against the reference
+            reps, results = d.probe_stage_collect()
+            assert len(results) == 1
+            want = case.passes[p]
+            assert int(results[0]["rays_traced"]) == want["rays_traced"], (name, p)
+            assert int(results[0]["probes_updated"]) == want["probes_updated"], (name, p)
+            for lv in range(stage.levels):
+                check_probes(d.probes(lv), case.data[f"probes_p{p}_c{lv}"], f"{name} pass {p} c{lv}")
+                err = texel_rel_err(d.atlas(lv, 0), case.data[f"atlas_p{p}_c{lv}"])
+                assert err.max() <= TEXEL_RTOL, (name, p, lv, err.max())
+    finally:
+        d.close()
+
+
+def test_stage_ms_sum_adds_the_passes():
+    """sdfgi_stage_ms_sum accumulates every update's stage times until a reset."""
+    case = load(CASES[0])
+    d = Device(0, precision="f64")
+    try:
+        stage = api.ProbeStage(d, case.scene, cfg=case.cfg(), res=case.res, spacing=case.spacing)
+        d.stage_ms_sum(reset=True)
+        per_pass = []
+        for p in range(2):
+            stage.run_pass(p)
+            per_pass.append(d.last_stage_ms())
+        sums, total = d.stage_ms_sum(reset=True)
+        for k in sums:
+            assert abs(sums[k] - sum(pp[k] for pp in per_pass)) <= 1e-6 + 1e-6 * sums[k], k
+        assert total >= max(sums.values()) > 0
+        assert d.stage_ms_sum(reset=False)[1] == 0.0
+    finally:
+        d.close()
