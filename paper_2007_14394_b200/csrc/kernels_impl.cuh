@@ -385,32 +385,36 @@ __global__ void __launch_bounds__(256) k_fill_sky(WaveParams<R> P) {
 }
 
 // Every probe ray's set-up at full lane occupancy, ahead of K1 (in K1 only the few
-// refilling lanes of a warp would run it): trace-order item -> its probe (the
-// candidate of its 32-ray chunk, then a step or two), its Fibonacci sample
-// (coherent order perm), ray id rayStart + sample, origin = the probe, direction =
-// rot * sphericalFibonacci (sampling.hpp:28).
+// refilling lanes of a warp would run it), one CTA per probe: trace-order item
+// rayStart + j, its Fibonacci sample i = perm[j] (coherent order), ray id
+// rayStart + i, origin = the probe, direction = rot * sphericalFibonacci
+// (sampling.hpp:28).
 template <typename R>
 __global__ void __launch_bounds__(256) k_probe_ray_setup(WaveParams<R> P) {
-    const long long item = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (item >= P.rayStart[P.nCand]) return;
-    int s = P.chunkSlot[item >> 5];
-    while (P.rayStart[s + 1] <= item) ++s;
-    const int j = static_cast<int>(item - P.rayStart[s]);
-    const int n = static_cast<int>(P.rayStart[s + 1] - P.rayStart[s]);
-    const int i = P.perm[(n == P.nRaysFull ? 0 : P.nRaysFull) + j];
+    // one CTA per candidate probe: its rotation, position and SDF are loaded once
+    const int s = blockIdx.x;
+    const long long start = P.rayStart[s];
+    const int n = static_cast<int>(P.rayStart[s + 1] - start);
+    if (n == 0) return;
     const int g = P.cand ? P.cand[s] : s;
     const double* pp = P.pc.probes.pos + 3 * static_cast<size_t>(g);
-    const V3<double> dd = rayDirection(P, s, i, n);
-    ProbeRay<R> r;
-    r.o[0] = R(pp[0]);
-    r.o[1] = R(pp[1]);
-    r.o[2] = R(pp[2]);
-    r.dir[0] = R(dd.x);
-    r.dir[1] = R(dd.y);
-    r.dir[2] = R(dd.z);
-    r.rid = static_cast<int>(P.rayStart[s] + i);
-    r.clear = P.useClear ? R(P.pc.probes.clear[g]) : R(-1);
-    stStream(reinterpret_cast<ProbeRay<R>*>(P.pray) + item, r);
+    const R ox = R(pp[0]), oy = R(pp[1]), oz = R(pp[2]);
+    const R clear = P.useClear ? R(P.pc.probes.clear[g]) : R(-1);
+    const int* perm = P.perm + (n == P.nRaysFull ? 0 : P.nRaysFull);
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const int i = perm[j];
+        const V3<double> dd = rayDirection(P, s, i, n);
+        ProbeRay<R> r;
+        r.o[0] = ox;
+        r.o[1] = oy;
+        r.o[2] = oz;
+        r.dir[0] = R(dd.x);
+        r.dir[1] = R(dd.y);
+        r.dir[2] = R(dd.z);
+        r.rid = static_cast<int>(start + i);
+        r.clear = clear;
+        stStream(reinterpret_cast<ProbeRay<R>*>(P.pray) + start + j, r);
+    }
 }
 
 // Warp-aggregated slot in a parking buffer (all 32 lanes call; -1 = not parked).
@@ -1463,7 +1467,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
     k_ray_setup<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
     k_ray_scan<R><<<1, kScanThreads, 0, st>>>(p);
     k_ray_chunks<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
-    k_probe_ray_setup<R><<<static_cast<int>((p.maxItems + 255) / 256), 256, 0, st>>>(p);
+    k_probe_ray_setup<R><<<p.nCand, 256, 0, st>>>(p);
     if (!p.debug) k_fill_sky<R><<<static_cast<int>((p.maxItems + 255) / 256), 256, 0, st>>>(p);
     cudaMemsetAsync(p.ctr, 0, (kLightCtr + (p.scene.n_lights > 1 ? p.scene.n_lights : 1)) * sizeof(unsigned long long), st);
     static int b3 = persistentBlocks(k_shade_rays<R, ST, true>, 128, 0);
