@@ -373,17 +373,6 @@ __global__ void __launch_bounds__(256) k_contact_setup(WaveParams<R> P) {
     stStream(reinterpret_cast<ContactRay<R>*>(P.cray) + i, r);
 }
 
-// The radiance of every ray of a probe batch preset to the sky (shadeHit's miss
-// branch, probe_update.hpp:137); K3a overwrites the converged hits' entries.
-template <typename R>
-__global__ void __launch_bounds__(256) k_fill_sky(WaveParams<R> P) {
-    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= P.rayStart[P.nCand]) return;
-    __stcs(&P.rad[3 * i], R(P.scene.sky[0]));
-    __stcs(&P.rad[3 * i + 1], R(P.scene.sky[1]));
-    __stcs(&P.rad[3 * i + 2], R(P.scene.sky[2]));
-}
-
 // Every probe ray's set-up at full lane occupancy, ahead of K1 (in K1 only the few
 // refilling lanes of a warp would run it), one CTA per probe: trace-order item
 // rayStart + j, its Fibonacci sample i = perm[j] (coherent order), ray id
@@ -414,6 +403,12 @@ __global__ void __launch_bounds__(256) k_probe_ray_setup(WaveParams<R> P) {
         r.rid = static_cast<int>(start + i);
         r.clear = clear;
         stStream(reinterpret_cast<ProbeRay<R>*>(P.pray) + start + j, r);
+        if (!P.debug) {  // the sky radiance every ray starts with (K1 writes no miss records)
+            R* rad = P.rad + 3 * static_cast<size_t>(start + j);
+            __stcs(rad, R(P.scene.sky[0]));
+            __stcs(rad + 1, R(P.scene.sky[1]));
+            __stcs(rad + 2, R(P.scene.sky[2]));
+        }
     }
 }
 
@@ -719,7 +714,7 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
                 }
                 // only converged rays' records are read (K3a, the normals; per-ray
                 // debug records read every ray's). A probe batch's radiance starts at
-                // the sky (k_fill_sky); a contact batch's combine reads the converged
+                // the sky (k_probe_ray_setup); a contact batch's combine reads the converged
                 // flags (conv) and the radiance of converged rays only
                 const bool lean = !P.debug && !P.keepAll;
                 if (!lean || done == 1) stStream(&P.hits[rid], h);
@@ -1468,7 +1463,6 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
     k_ray_scan<R><<<1, kScanThreads, 0, st>>>(p);
     k_ray_chunks<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
     k_probe_ray_setup<R><<<p.nCand, 256, 0, st>>>(p);
-    if (!p.debug) k_fill_sky<R><<<static_cast<int>((p.maxItems + 255) / 256), 256, 0, st>>>(p);
     cudaMemsetAsync(p.ctr, 0, (kLightCtr + (p.scene.n_lights > 1 ? p.scene.n_lights : 1)) * sizeof(unsigned long long), st);
     static int b3 = persistentBlocks(k_shade_rays<R, ST, true>, 128, 0);
     static int b3d = persistentBlocks(k_shade_rays<R, ST, false>, 128, 0, 128 * kMvcSlab * sizeof(R));
@@ -1512,7 +1506,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
         k3<<<p.nCand, kConvThreads, smem, st>>>(p);
     }
     mark(7);
-    if (launches) *launches += p.debug ? 11 : 15;
+    if (launches) *launches += p.debug ? 11 : 14;
 }
 
 // contactGI's per-pixel sum (shading.hpp:686-713): AO from the missed samples,
