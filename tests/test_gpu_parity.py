@@ -186,7 +186,7 @@ def test_recenter_cascade_resets_only_that_cascade(dev):
         assert np.array_equal(dev.atlas(lv, 0), before[lv][1])
 
 
-@pytest.mark.parametrize("name", [CASES[0], SCHED_CASES[0]])
+@pytest.mark.parametrize("name", [CASES[0], "openfield", SCHED_CASES[0]])
 def test_probe_stage_call_matches_call_sequence(name):
     """sdfgi_probe_stage (relocation of every cascade + selection + update, one
     host sync) == the relocate / select / update sequence it replaces: same
