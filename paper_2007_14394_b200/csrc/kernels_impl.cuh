@@ -1075,9 +1075,10 @@ __device__ __forceinline__ void appendList(unsigned long long* ctr, int slot, in
 // K3a: shadeHit per ray (thread per ray, grid-stride): emission + directIrradiance
 // summed in light order with the K2 visibilities + the bounce lookup; radiance to
 // P.rad (3 per ray). Kept apart from the convolution so the stencil register
-// footprint does not cap the convolution's occupancy. DEFER: hits whose stencil
-// takes the MVC path are appended to P.mvcList and finished by K3c (16 lanes per
-// hit); !DEFER (per-ray debug records) evaluates the MVC inline.
+// footprint does not cap the convolution's occupancy. DEFER: the bounce lookup is
+// deferred — hits whose stencil takes the MVC path go to P.mvcList (K3c, one hit
+// per thread), the others to P.triList (K3d); !DEFER (per-ray debug records)
+// evaluates the whole lookup inline.
 template <typename R, bool ST, bool DEFER>
 __global__ void __launch_bounds__(128, WaveOcc<R>::shade) k_shade_rays(WaveParams<R> P) {
     // the compacted hit list (misses got the sky radiance in K1); every ray when

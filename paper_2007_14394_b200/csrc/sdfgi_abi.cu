@@ -774,7 +774,7 @@ bool buildGridAt(Ctx* c, double cellScale) {
         h = std::max(h, ext[a] / 1024.0);
     }
     // rounding every axis up can overshoot the target: grow h until the cell count
-    // is inside the 2^26 the cell indexing allows (never fail for a size we chose)
+    // is inside the 2^28 cells the grid allows (never fail for a size we chose)
     long long ncells = 1;
     for (int tries = 0;; ++tries) {
         ncells = 1;
