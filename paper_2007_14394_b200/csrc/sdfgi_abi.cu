@@ -86,20 +86,26 @@ int guard(F&& f) {
     }
 }
 
+// Device buffer: n = the size asked for, cap = what is allocated (grow-only: a grid
+// rebuild or a batch of another size reuses the memory instead of a cudaFree +
+// cudaMalloc pair, each of which synchronises the device).
 template <typename T>
 struct DBuf {
     T* p = nullptr;
-    size_t n = 0;
+    size_t n = 0, cap = 0;
     void alloc(size_t count) {
-        if (count == n && p) return;
+        if (count <= cap && p) {
+            n = count;
+            return;
+        }
         free();
         if (count) CK(cudaMalloc(&p, count * sizeof(T)));
-        n = count;
+        n = cap = count;
     }
     void free() {
         if (p) cudaFree(p);
         p = nullptr;
-        n = 0;
+        n = cap = 0;
     }
     void upload(const T* h, size_t count, cudaStream_t s) {
         alloc(count);
