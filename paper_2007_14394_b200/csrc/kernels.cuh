@@ -160,6 +160,9 @@ template <typename R> struct WaveParams {
     // bounded primitive) after starting inside it can never converge again (the grid
     // box is convex, no unbounded primitive): K1 ends it as a miss on the spot
     int escape;
+    // accel mode 2: K2's settled-shadow test (the same conditions as escape; the
+    // Contact GI and compose wavefronts keep it while K1's escape is off there)
+    int settle;
     const double* clocal;  // contact batch: cosineHemisphereDir's (lx, ly) per (pixel, sample), host libm
     // the traced shadow marches, light li's at [li * srayCap, + ctr[kLightCtr + li])
     ShadowRay<R>* sray;

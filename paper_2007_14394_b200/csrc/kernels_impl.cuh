@@ -904,7 +904,7 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
         if (PHASE == 0 && want && P.scene.useGrid) cell = gridCell<R>(P.scene.grid, p, &cellR);
         // accel mode 2: off the grid, a march whose remaining terms cannot lower v
         // ends here with v (shadowSettled)
-        if (P.escape && want && (PHASE == 1 || cell < 0 || SDFGI_SHADOW_SETTLE_ON_GRID) &&
+        if (P.settle && want && (PHASE == 1 || cell < 0 || SDFGI_SHADOW_SETTLE_ON_GRID) &&
             shadowSettled(P.scene.grid, p, dir, t, tEnd, k, v))
             want = false;
         if (PHASE == 0) {

@@ -1072,6 +1072,7 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.currAtlas = c->atlas[1 - c->front].p;
     p.prevZero = c->frontZero() ? 1 : 0;
     p.escape = escapeOk(c);
+    p.settle = p.escape;
     p.ownerFromMarch = c->accel == 2 && c->haveGrid ? 1 : 0;
     p.useClear = c->accel == 2 && !c->clearValid.empty() &&
                  std::all_of(c->clearValid.begin(), c->clearValid.end(), [](char v) { return v != 0; });
@@ -2209,6 +2210,7 @@ int sdfgi_probes_trace_debug(void* ctx, const int32_t* probe_refs, int n_refs, i
             p.records = c->records.p;
             p.debug = 1;
             p.escape = 0;  // per-ray records: the exact march (miss reason, steps)
+            p.settle = 0;
             p.useClear = 0;
             launch_wavefront<double>(p, c->persistCap, false, c->stream, nullptr, &c->launches);
         } else {
@@ -2216,6 +2218,7 @@ int sdfgi_probes_trace_debug(void* ctx, const int32_t* probe_refs, int n_refs, i
             p.records = c->records.p;
             p.debug = 1;
             p.escape = 0;
+            p.settle = 0;
             launch_wavefront<float>(p, c->persistCap, false, c->stream, nullptr, &c->launches);
         }
         CK(cudaGetLastError());
@@ -2449,6 +2452,10 @@ WaveParams<R> contactParams(Ctx* c, const sdfgi_cfg* cfg) {
     // short rays: neither the escape test nor the shared-memory primitive copy pays
     // off here (measured: contact +2.5% / +3% each, scripts/time_gather.py)
     p.escape = 0;
+    {
+        const char* e = std::getenv("SDFGI_CONTACT_SETTLE");
+        p.settle = (!e || std::atoi(e) != 0) ? escapeOk(c) : 0;
+    }
     p.scene.stageBytes = 0;
     p.ownerFromMarch = c->accel == 2 && c->haveGrid ? 1 : 0;  // exact (see waveParams)
     p.nRaysDirect = nr;
@@ -2720,10 +2727,19 @@ int sdfgi_compose(void* ctx, const sdfgi_cfg* cfg, sdfgi_stats* stats, double* m
         for (auto& e : c->cev)
             if (!e) CK(cudaEventCreate(&e));
         CK(cudaEventRecord(c->cev[0], c->stream));
-        if (c->precision == SDFGI_F64)
-            launch_compose<double>(composeParams<double>(c, cfg), st, c->stream, &c->launches);
-        else
-            launch_compose<float>(composeParams<float>(c, cfg), st, c->stream, &c->launches);
+        // settled shadows (exact) only without stats: the stats run keeps the
+        // reference's query sequence, whose counts the parity tests compare
+        const char* se = std::getenv("SDFGI_COMPOSE_SETTLE");
+        const int settle = (!st && (!se || std::atoi(se) != 0)) ? escapeOk(c) : 0;
+        if (c->precision == SDFGI_F64) {
+            WaveParams<double> p = composeParams<double>(c, cfg);
+            p.settle = settle;
+            launch_compose<double>(p, st, c->stream, &c->launches);
+        } else {
+            WaveParams<float> p = composeParams<float>(c, cfg);
+            p.settle = settle;
+            launch_compose<float>(p, st, c->stream, &c->launches);
+        }
         CK(cudaGetLastError());
         CK(cudaEventRecord(c->cev[1], c->stream));
         unsigned long long h[32];
