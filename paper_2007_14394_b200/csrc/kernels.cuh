@@ -118,7 +118,6 @@ template <typename R> struct WaveParams {
     int nCand;
     int* rayCount;            // per candidate (K0)
     long long* rayStart;      // nCand + 1 exclusive prefix (K0 scan)
-    int* chunkSlot;           // per 32-ray chunk c: the candidate holding ray 32c (K0)
     double* rot;              // 9 per candidate (K0, from quat)
     const double* quat;       // 4 per candidate: randomRotation's quaternion, host libm (host_trig.h)
     const double* fib;        // sphericalFibonacci table: n=N (N xyz) then n=2N (2N xyz), host libm

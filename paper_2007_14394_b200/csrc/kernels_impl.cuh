@@ -274,17 +274,6 @@ __global__ void __launch_bounds__(kScanThreads) k_ray_scan(WaveParams<R> P) {
     if (threadIdx.x == kScanThreads - 1) P.rayStart[n] = warpSums[31];
 }
 
-// The candidate of every 32-ray chunk's first ray, so K1's refill finds a ray's
-// probe with at most a step or two instead of a binary search on one lane: the
-// candidate whose range holds ray 32c writes chunk c.
-template <typename R>
-__global__ void __launch_bounds__(128) k_ray_chunks(WaveParams<R> P) {
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= P.nCand) return;
-    const long long b = P.rayStart[s], e = P.rayStart[s + 1];
-    for (long long c = (b + 31) >> 5; (c << 5) < e; ++c) P.chunkSlot[c] = s;
-}
-
 __device__ __forceinline__ int findCandidate(const long long* start, int n, long long rid) {
     int lo = 0, hi = n;  // start[lo] <= rid < start[hi]
     while (hi - lo > 1) {
@@ -1462,7 +1451,6 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
     };
     k_ray_setup<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
     k_ray_scan<R><<<1, kScanThreads, 0, st>>>(p);
-    k_ray_chunks<R><<<(p.nCand + 127) / 128, 128, 0, st>>>(p);
     k_probe_ray_setup<R><<<p.nCand, 256, 0, st>>>(p);
     cudaMemsetAsync(p.ctr, 0, (kLightCtr + (p.scene.n_lights > 1 ? p.scene.n_lights : 1)) * sizeof(unsigned long long), st);
     static int b3 = persistentBlocks(k_shade_rays<R, ST, true>, 128, 0);
@@ -1507,7 +1495,7 @@ static void wavefront(const WaveParams<R>& p, int cap, cudaStream_t st, const cu
         k3<<<p.nCand, kConvThreads, smem, st>>>(p);
     }
     mark(7);
-    if (launches) *launches += p.debug ? 11 : 14;
+    if (launches) *launches += p.debug ? 10 : 13;
 }
 
 // contactGI's per-pixel sum (shading.hpp:686-713): AO from the missed samples,

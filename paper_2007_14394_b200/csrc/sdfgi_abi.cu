@@ -236,7 +236,7 @@ struct Ctx {
     DBuf<int> refs, allRefs;
     DBuf<RayRecord> records;
     // wavefront scratch (kernels.cuh)
-    DBuf<int> wRayCount, wHitList, wChunk, wHitAt, wMvcList, wTriList;
+    DBuf<int> wRayCount, wHitList, wHitAt, wMvcList, wTriList;
     DBuf<long long> wRayStart;
     DBuf<double> wRot, fib;
     DBuf<int> perm;
@@ -298,7 +298,7 @@ struct Ctx {
         pos.free(); rest.free(); last.free(); clear.free(); alive.free(); reject.free(); lastFrame.free();
         atlas[0].free(); atlas[1].free(); scratch.free(); report.free(); refs.free(); allRefs.free();
         records.free(); selScratch.free(); qpts.free(); qinit.free(); qd.free(); qowner.free();
-        wRayCount.free(); wHitList.free(); wMvcList.free(); wTriList.free(); wChunk.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); cLocal.free(); wHits.free();
+        wRayCount.free(); wHitList.free(); wMvcList.free(); wTriList.free(); wHitAt.free(); wSelTemp.free(); wRayStart.free(); wRot.free(); fib.free(); cLocal.free(); wHits.free();
         if (hReport) cudaFreeHost(hReport);
         if (hAsync) cudaFreeHost(hAsync);
         scratchAsync.free();
@@ -1015,7 +1015,6 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     const int L = std::max(c->nLights, 1);
     reserve(c->wRayCount, std::max(nCand, 1));
     reserve(c->wRayStart, static_cast<size_t>(nCand) + 1);
-    reserve(c->wChunk, maxRays / 32 + 2);
     reserve(c->wRot, 9 * static_cast<size_t>(std::max(nCand, 1)));
     reserve(c->wHits, std::max<size_t>(maxRays, 1) * sizeof(HitRec<R>));
     reserve(c->wHitList, std::max<size_t>(maxRays, 1));
@@ -1049,7 +1048,6 @@ WaveParams<R> waveParams(Ctx* c, const sdfgi_cfg* cfg, int frame, const int* can
     p.nCand = nCand;
     p.rayCount = c->wRayCount.p;
     p.rayStart = c->wRayStart.p;
-    p.chunkSlot = c->wChunk.p;
     p.rot = c->wRot.p;
     p.quat = c->quatDev;
     p.pray = c->wPRay.p;
