@@ -360,7 +360,7 @@ constexpr int kLightCtr = 144;
 #define SDFGI_WAVE_MINB32 8  // C2 pass 0 FP32: 6 / 7 / 8 / 10 CTAs = 6.33 / 6.24 / 6.16 / 6.32 ms
 #endif
 #ifndef SDFGI_SHADE_MINB
-#define SDFGI_SHADE_MINB 5  // 96 registers; C2 pass 0 FP64 3 / 4 / 5 CTAs = 10.26 / 10.11 / 10.02 ms
+#define SDFGI_SHADE_MINB 6  // 80 registers since the bounce lookups left K3a: 5 / 6 / 8 CTAs = 0.69 / 0.63 / 0.65 ms per step (ncu); round 1: 3 / 4 / 5 = 10.26 / 10.11 / 10.02 ms
 #endif
 #ifndef SDFGI_SHADOW_MINB64
 #define SDFGI_SHADOW_MINB64 SDFGI_WAVE_MINB64
