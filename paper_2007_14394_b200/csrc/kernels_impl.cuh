@@ -61,6 +61,17 @@ __device__ __forceinline__ void flushCounters(const Counters& c, unsigned long l
 #define SDFGI_FETCH_CHUNK 32  // C2 pass 0: 32 -> 64 -> 128 = FP64 10.4 / 10.5 / 10.9 ms
 #endif
 constexpr unsigned long long kFetchChunk = SDFGI_FETCH_CHUNK;
+// The cell record of a march point is loaded as soon as its cell is known, so
+// its DRAM latency (the tracing kernels' top stall on the 240M-cell grid) runs
+// under the escape / parking / settle logic before the query needs it. K1 in
+// both precisions, K2 in FP64 (FP32's K2 keeps its per-lane cell cache):
+// C2 FP64 24.30 -> 23.86 ms, FP32 15.72 -> 15.63 ms.
+#ifndef SDFGI_HOIST_CELL_LOAD
+#define SDFGI_HOIST_CELL_LOAD 1
+#endif
+#ifndef SDFGI_HOIST_CELL_LOAD2
+#define SDFGI_HOIST_CELL_LOAD2 1
+#endif
 #ifndef SDFGI_PREFETCH_CHUNK
 #define SDFGI_PREFETCH_CHUNK 1
 #endif
@@ -585,11 +596,17 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
         bool parkIt = false, escaped = false, known = false;
         int cell = kCellUnknown;  // phase 0: p's cell (parking test), reused by the query
         R cellR = R(0);
+#if SDFGI_HOIST_CELL_LOAD
+        int4 preRec = make_int4(0, 0, 0, 0);
+#endif
         if (active) {
             if (state == 2 && !fresh) t += d;
             fresh = false;
             p = o + dir * t;
             if (PHASE == 0 && P.scene.useGrid) cell = gridCell<R>(P.scene.grid, p, &cellR);
+#if SDFGI_HOIST_CELL_LOAD
+            if (cell >= 0) preRec = __ldg(&P.scene.grid.cell[cell]);  // its latency under the logic below
+#endif
             // the first query of a probe ray is the probe's own SDF, known from the relocation
             known = PHASE == 0 && state == 0 && step == 0 && d >= R(0);
             escaped = PHASE == 0 && originIn && state == 0 && cell < 0 && !known;
@@ -648,7 +665,13 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
             nd = smin(d, initD);  // exactly query(o, initD) = min(SDF(o), initD)
         else if (active && !escaped)
             nd = query<R, ST, STG>(P.scene, p, initD, &o2, &cnt, PHASE ? seed : -1, cell, cellR,
-                              useCellCache<R>() ? &ccache : nullptr);
+                              useCellCache<R>() ? &ccache : nullptr,
+#if SDFGI_HOIST_CELL_LOAD
+                              cell >= 0 ? &preRec : nullptr
+#else
+                              nullptr
+#endif
+                              );
         if (active) {
             if (o2 >= 0) seed = o2;
             int done = 0;  // 1 converged, 2 TMax, 3 StepLimit
@@ -891,6 +914,11 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
         int cell = kCellUnknown;  // phase 0: p's cell (parking test), reused by the query
         R cellR = R(0);
         if (PHASE == 0 && want && P.scene.useGrid) cell = gridCell<R>(P.scene.grid, p, &cellR);
+#if SDFGI_HOIST_CELL_LOAD2
+        constexpr bool hoist2 = sizeof(R) == 8;
+        int4 preRec = make_int4(0, 0, 0, 0);
+        if (hoist2 && cell >= 0) preRec = __ldg(&P.scene.grid.cell[cell]);  // its latency under the settle test
+#endif
         // accel mode 2: off the grid, a march whose remaining terms cannot lower v
         // ends here with v (shadowSettled)
         if (P.settle && want && (PHASE == 1 || cell < 0 || SDFGI_SHADOW_SETTLE_ON_GRID) &&
@@ -925,7 +953,13 @@ __global__ void __launch_bounds__(STG ? StageOcc<R>::threads : kWaveThreads, STG
         int o2 = -1;
         if (want)
             d = query<R, ST, STG>(P.scene, p, lastD == inf ? inf : R(2) * lastD, &o2, &cnt, PHASE ? seed : -1, cell, cellR,
-                             useCellCache<R>() ? &ccache : nullptr);
+                             useCellCache<R>() ? &ccache : nullptr,
+#if SDFGI_HOIST_CELL_LOAD2
+                             hoist2 && cell >= 0 ? &preRec : nullptr
+#else
+                             nullptr
+#endif
+                             );
         if (o2 >= 0) seed = o2;
         if (active) {
             bool done = false;

@@ -598,7 +598,8 @@ struct CellCache {
 // when the caller has them already (the persistent kernels' parking test).
 template <typename R, bool ST>
 __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R initD, QueryState<R>& q, Counters* c,
-                                           int cellHint = kCellUnknown, R rHint = R(0), CellCache* cache = nullptr) {
+                                           int cellHint = kCellUnknown, R rHint = R(0), CellCache* cache = nullptr,
+                                           const int4* preRec = nullptr) {
     q.p = p;
     q.d = initD;
     q.own = -1;
@@ -621,7 +622,9 @@ __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R ini
     const int cell = cellHint == kCellUnknown ? gridCell<R>(g, p, &q.r) : cellHint;
     if (cell >= 0) {
         int4 rec;
-        if (cache && cache->cell == cell) {
+        if (preRec) {
+            rec = *preRec;  // loaded by the caller as soon as the cell was known
+        } else if (cache && cache->cell == cell) {
             rec = cache->rec;
         } else {
             rec = __ldg(&g.cell[cell]);
@@ -645,9 +648,10 @@ __device__ __forceinline__ void queryBegin(const SceneView<R>& s, V3<R> p, R ini
 // there completes through the cluster hierarchy.
 template <typename R, bool ST, bool STG = false>
 __device__ __forceinline__ R query(const SceneView<R>& s, V3<R> p, R initD, int* owner, Counters* c, int seed = -1,
-                                   int cellHint = kCellUnknown, R rHint = R(0), CellCache* cache = nullptr) {
+                                   int cellHint = kCellUnknown, R rHint = R(0), CellCache* cache = nullptr,
+                                   const int4* preRec = nullptr) {
     QueryState<R> q;
-    queryBegin<R, ST>(s, p, initD, q, c, cellHint, rHint, cache);
+    queryBegin<R, ST>(s, p, initD, q, c, cellHint, rHint, cache, preRec);
     // seed (candidate-grid walks only, which break ties by CSR position in any
     // visiting order): evaluate a likely owner first — e.g. the previous step's
     // — so the hierarchy prunes against a tight minimum from its first node
